@@ -1,0 +1,162 @@
+/*
+ * mpvmc_b200 — C ABI of the B200 (sm_100a) hot path for arXiv 2601.20782:
+ * batched Metropolis–Hastings sampling of an RBM neural quantum state in
+ * reduced precision, plus the local energies that consume the samples.
+ *
+ * Every entry point takes caller-owned DEVICE pointers and a cudaStream_t
+ * (passed as void*), launches asynchronously on that stream and returns an
+ * int status (MPV_OK ... MPV_ERR_NONFINITE).  The library never allocates
+ * device memory and keeps no state except a thread-local error string
+ * (mpv_last_error).  Citations "ref:" are into the reference package
+ * /root/reference/pkg/src/mpvmc/ (file:line) — the interface each function
+ * replaces; INTEGRATION.md shows the ctypes binding the reference would add.
+ */
+#ifndef MPVMC_B200_H
+#define MPVMC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define MPV_OK 0
+#define MPV_ERR_ARGS 1
+#define MPV_ERR_CUDA 2
+#define MPV_ERR_NONFINITE 3
+
+/* float formats (ref: precision.py:64-67) */
+#define MPV_FMT_F64 0
+#define MPV_FMT_F32 1
+#define MPV_FMT_F16 2
+#define MPV_FMT_BF16 3
+
+/* rounding modes (ref: precision.py:158-169, plus the device NATIVE mode) */
+#define MPV_MODE_NATIVE 0
+#define MPV_MODE_PER_OPERATION 1
+#define MPV_MODE_STORAGE_ONLY 2
+
+/* exact-theta accumulator variants of the fused sweep */
+#define MPV_ACC_X1 0  /* one f32 accumulator per component, exact by host planner check */
+#define MPV_ACC_X2 1  /* hi/lo f32 accumulators on a fixed split grid, exact */
+#define MPV_ACC_F64 2 /* f64 accumulators */
+
+/* proposals (ref: sampler.py:24-39) */
+#define MPV_PROPOSAL_FLIP 0
+#define MPV_PROPOSAL_EXCHANGE 1
+
+/* Hamiltonians (ref: hamiltonians.py:28-46) */
+#define MPV_HAM_TFIM 0
+#define MPV_HAM_HEISENBERG 1
+
+/*
+ * A prepared parameter snapshot in kernel layout (the device counterpart of
+ * ref: rbm.py:161-200 _PreparedRounded, built by the host from
+ * round_parameters(params, fmt), ref: rbm.py:91-101).  Column-major by site
+ * so one flip reads one contiguous column: entry (k, i) at table[k*hidden_pad+i].
+ *   entry type      table/bias element            vis element
+ *   X1, PER_OP      fmt pair (re,im): 4 B f16/bf16, 8 B f32      float (a_re)
+ *   X2              two fmt pairs (hi, lo)                       float2 (hi, lo)
+ *   F64             double2 (re, im)                             double
+ * `vis_im` (double[N], a_im) is only read by mpv_snapshot_forward (log psi).
+ */
+typedef struct {
+  int32_t n_visible, n_hidden, hidden_pad;
+  int32_t fmt, mode, variant;
+  int32_t lanes_per_chain, units_per_lane;
+  const void* table;
+  const void* bias;
+  const void* vis;
+  const double* vis_im;
+} mpv_snapshot;
+
+/* Chain state of one shard (device pointers; ref: sampler.py:55-65 state). */
+typedef struct {
+  int64_t n_chains;     /* chains in this shard */
+  int64_t chain_offset; /* global id of chain 0: draws depend on global ids only */
+  int32_t n_sites, words; /* words = ceil(n_sites / 32) */
+  uint32_t* bits;        /* [n_chains][words], bit k of a chain in word k>>5, bit k&31 */
+  double* log_probs;     /* [n_chains] */
+  int64_t* accepted;     /* [n_chains] accepted proposals since reset */
+  int64_t* status;       /* [2 + words]: {code, step*2^32 + chain, offending bits...} */
+} mpv_chains;
+
+/* ---- RNG (ref: rng.py:63-77 StreamSet.next_uniform, closed form) ---- */
+/* out[t][c] = draw t0+t of stream chain0+c of `key`. */
+int mpv_stream_uniforms(uint64_t key, int64_t n_chains, int64_t chain0, int64_t t0,
+                        int64_t n_draws, double* out, void* stream);
+
+/* ---- chain initialisation (ref: sampler.py:67-88 ChainEnsemble._initial_bits) ----
+ * flip: bit_k = u_k < 0.5 (N draws); exchange: Fisher–Yates of a weight-w
+ * template (N-1 draws).  Writes ch->bits; zeroes accepted/status. */
+int mpv_chains_init(const mpv_chains* ch, uint64_t key, int proposal, int sector_weight,
+                    void* stream);
+
+/* ---- fused MH sweep (ref: sampler.py:111-133 ChainEnsemble.step x n_steps,
+ *      sampler.py:142-167 collect) ----
+ * Runs n_steps proposals per chain.  step_index = proposals already made by
+ * this ensemble (the draw counter is init_draws + 2*step_index).  The cached
+ * log p is recomputed from the bits at launch start (set_evaluator
+ * semantics, ref: sampler.py:90-93) and written back at the end.
+ * If samples != NULL: after every `thin` steps round r = round_offset + j is
+ * recorded for chain c (global id) when r < count_c, into row offset_c + r
+ * relative to the shard's first row `row0` (count_c, offset_c from
+ * n_samples_total over n_chains_total, ref: sampler.py:152-166). */
+int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, int proposal,
+                 int64_t init_draws, int64_t step_index, int64_t n_steps, int64_t thin,
+                 uint32_t* samples, int64_t n_samples_total, int64_t n_chains_total,
+                 int64_t round_offset, int64_t row0, void* stream);
+
+/* ---- batched log-probability / log-psi in the snapshot's arithmetic ----
+ * bits: packed [B][words].  PER_OPERATION reproduces ref: _kernels.py:51-129
+ * (rounded_forward / rounded_log_prob) bit for bit; F64/STORAGE_ONLY follow
+ * ref: rbm.py:143-150 (_fast_forward); NATIVE is the fused sweep's arithmetic.
+ * out_re/out_im (log psi, may be NULL) are only produced by PER_OPERATION and F64. */
+int mpv_snapshot_forward(const mpv_snapshot* snap, const uint32_t* bits, int64_t B,
+                         double* out_lp, double* out_re, double* out_im, int64_t* status,
+                         void* stream);
+
+/* Drop-in for ref: _kernels.py:95-129 rounded_log_prob(bits, a_re, b_re, b_im,
+ * w_re, w_im, spl, mn, iq, qq, maxf): uint8 bits [B][N], f64 parameters already
+ * on fmt's grid in the reference layout (w row-major [M][N]); the quantizer
+ * constants are implied by fmt.  `scratch` >= mpv_rounded_scratch_bytes(B, N, M, fmt). */
+size_t mpv_rounded_scratch_bytes(int64_t B, int N, int M, int fmt);
+int mpv_rounded_log_prob(const uint8_t* bits, int64_t B, int N, int M, const double* a_re,
+                         const double* b_re, const double* b_im, const double* w_re,
+                         const double* w_im, int fmt, double* out_lp, void* scratch,
+                         void* stream);
+
+/* ---- local energies (ref: vmc.py:52-108 local_energies) ----
+ * eps(x) = J sum_bonds s_i s_j + sum_{x'} H(x,x') psi(x')/psi(x) in f64 with
+ * the master (unrounded) parameters.  params: a [N], b [M] double2 (re,im);
+ * w_t [N][M] double2 (column-major by site).  `tables` is a caller workspace
+ * of mpv_energy_tables_bytes(...) filled by mpv_energy_prepare. */
+size_t mpv_energy_tables_bytes(int N, int M, int ham, int n_bonds);
+int mpv_energy_prepare(int N, int M, const double* a, const double* b, const double* w_t,
+                       int ham, const int32_t* bonds, int n_bonds, void* tables, void* stream);
+int mpv_local_energies(int N, int M, const double* a, const double* b, const double* w_t,
+                       int ham, const int32_t* bonds, int n_bonds, double J, double h,
+                       const void* tables, const uint32_t* bits, int64_t B, double* out_eps,
+                       int64_t* status, void* stream);
+
+/* ---- helpers ---- */
+int mpv_unpack_bits(const uint32_t* words, int64_t B, int N, uint8_t* out, void* stream);
+int mpv_pack_bits(const uint8_t* bits, int64_t B, int N, uint32_t* out, void* stream);
+/* per-chain -> total accepted (int64 sum) */
+int mpv_sum_i64(const int64_t* x, int64_t n, int64_t* out, void* stream);
+
+/* Layout of the fused sweep for N sites, M hidden units: lanes per chain G
+ * (power of two, >= ceil(N/32)) and hidden units per lane U; hidden_pad = G*U.
+ * The f32 summation order of NATIVE log p depends on (G, U), so it is a fixed
+ * function of (N, M). */
+int mpv_plan_layout(int n_visible, int n_hidden, int32_t* lanes_per_chain, int32_t* units_per_lane);
+
+const char* mpv_last_error(void);
+const char* mpv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPVMC_B200_H */

@@ -1,0 +1,484 @@
+// C ABI of libmpvmc_b200 (include/mpvmc_b200.h): argument checks, launch
+// configuration and the small helper kernels.  No device allocation happens
+// here: every buffer is caller-owned.
+#include <mutex>
+#include <string>
+#include <unordered_set>
+
+#include "energy.cuh"
+#include "perop.cuh"
+#include "sweep.cuh"
+
+namespace mpv {
+void* sweep_kernel_ptr_f16(int variant, int U, int prop, int smem);
+void* sweep_kernel_ptr_bf16(int variant, int U, int prop, int smem);
+void* sweep_kernel_ptr_f32(int variant, int U, int prop, int smem);
+void* sweep_kernel_ptr_f64(int variant, int U, int prop, int smem);
+}  // namespace mpv
+
+using namespace mpv;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return MPV_OK;
+}
+
+int max_smem_optin() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  return v;
+}
+
+// cudaFuncSetAttribute once per (kernel, size class)
+int ensure_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_set<const void*> done;
+  if (bytes <= 48 * 1024) return MPV_OK;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(fn)) return MPV_OK;
+  const cudaError_t e =
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin());
+  if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  done.insert(fn);
+  return MPV_OK;
+}
+
+constexpr int kUnits[] = {4, 8, 10, 13, 16};
+constexpr int MAX_WORDS_INIT = 32;  // n_sites <= 1024
+
+size_t entry_bytes(int fmt, int variant) {
+  if (variant == MPV_ACC_F64 || fmt == MPV_FMT_F64) return 16;
+  const size_t pair = (fmt == MPV_FMT_F32) ? 8 : 4;
+  return variant == MPV_ACC_X2 ? 2 * pair : pair;
+}
+size_t vis_bytes(int fmt, int variant) {
+  if (variant == MPV_ACC_F64 || fmt == MPV_FMT_F64) return 8;
+  return variant == MPV_ACC_X2 ? 8 : 4;
+}
+
+// ---------------- helper kernels ----------------
+
+__global__ void stream_uniforms_kernel(uint64_t key, int64_t n_chains, int64_t chain0, int64_t t0,
+                                       int64_t n_draws, double* out) {
+  const int64_t n = n_chains * n_draws;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = idx / n_chains, c = idx % n_chains;
+    out[idx] = stream_draw(stream_state(key, (uint64_t)(chain0 + c)), (uint64_t)(t0 + t));
+  }
+}
+
+// ref: sampler.py:67-88
+__global__ void chains_init_kernel(mpv_chains ch, uint64_t key, int proposal, int weight) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ch.n_chains) return;
+  const uint64_t s0 = stream_state(key, (uint64_t)(ch.chain_offset + c));
+  uint32_t w[MAX_WORDS_INIT];
+  const int N = ch.n_sites;
+  for (int i = 0; i < ch.words; ++i) w[i] = 0u;
+  if (proposal == MPV_PROPOSAL_FLIP) {
+    for (int k = 0; k < N; ++k)
+      if (stream_draw(s0, (uint64_t)k) < 0.5) w[k >> 5] |= 1u << (k & 31);
+  } else {
+    for (int k = 0; k < weight; ++k) w[k >> 5] |= 1u << (k & 31);
+    uint64_t t = 0;
+    for (int i = N - 1; i > 0; --i) {
+      const int j = (int)floor_scaled(stream_draw(s0, t++), (double)(i + 1));
+      const uint32_t bi = (w[i >> 5] >> (i & 31)) & 1u, bj = (w[j >> 5] >> (j & 31)) & 1u;
+      if (bi != bj) {
+        w[i >> 5] ^= 1u << (i & 31);
+        w[j >> 5] ^= 1u << (j & 31);
+      }
+    }
+  }
+  for (int i = 0; i < ch.words; ++i) ch.bits[c * ch.words + i] = w[i];
+  if (ch.log_probs) ch.log_probs[c] = 0.0;
+  if (ch.accepted) ch.accepted[c] = 0;
+}
+
+__global__ void unpack_kernel(const uint32_t* words, int64_t B, int N, int nw, uint8_t* out) {
+  const int64_t n = B * N;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / N;
+    const int k = (int)(idx % N);
+    out[idx] = (uint8_t)((words[r * nw + (k >> 5)] >> (k & 31)) & 1u);
+  }
+}
+
+__global__ void pack_kernel(const uint8_t* bits, int64_t B, int N, int nw, uint32_t* out) {
+  const int64_t n = B * nw;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / nw;
+    const int w = (int)(idx % nw);
+    uint32_t v = 0;
+    for (int b = 0; b < 32 && w * 32 + b < N; ++b) v |= (uint32_t)(bits[r * N + w * 32 + b] & 1u) << b;
+    out[idx] = v;
+  }
+}
+
+__global__ void sum_i64_kernel(const int64_t* x, int64_t n, int64_t* out) {
+  __shared__ long long part[32];
+  long long acc = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = (threadIdx.x < (blockDim.x >> 5)) ? part[threadIdx.x] : 0;
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
+    if (threadIdx.x == 0) *out = acc;
+  }
+}
+
+// Table of a reference-layout parameter set for mpv_rounded_log_prob.
+template <int FMT>
+__global__ void perop_table_kernel(int N, int M, const double* a_re, const double* b_re,
+                                   const double* b_im, const double* w_re, const double* w_im,
+                                   void* table, void* bias, float* vis) {
+  using P = PerOp<FMT>;
+  using Entry = typename P::Entry;
+  Entry* T = reinterpret_cast<Entry*>(table);
+  Entry* Bv = reinterpret_cast<Entry*>(bias);
+  const int64_t n = (int64_t)N * M;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n + M + N;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    if (idx < n) {
+      const int k = (int)(idx / M), i = (int)(idx % M);
+      const double re = w_re[(size_t)i * N + k], im = w_im[(size_t)i * N + k];
+      if constexpr (FMT == MPV_FMT_F32) T[idx] = make_float2((float)re, (float)im);
+      else T[idx] = (uint32_t)P::q(re) | ((uint32_t)P::q(im) << 16);
+    } else if (idx < n + M) {
+      const int i = (int)(idx - n);
+      if constexpr (FMT == MPV_FMT_F32) Bv[i] = make_float2((float)b_re[i], (float)b_im[i]);
+      else Bv[i] = (uint32_t)P::q(b_re[i]) | ((uint32_t)P::q(b_im[i]) << 16);
+    } else {
+      const int k = (int)(idx - n - M);
+      vis[k] = (float)a_re[k];
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+#pragma GCC visibility push(default)
+
+int mpv_pack_bits(const uint8_t* bits, int64_t B, int N, uint32_t* out, void* stream);
+
+const char* mpv_last_error(void) { return g_error.c_str(); }
+const char* mpv_version(void) { return "mpvmc_b200 0.1.0 (sm_100a)"; }
+
+int mpv_plan_layout(int n_visible, int n_hidden, int32_t* lanes_per_chain, int32_t* units_per_lane) {
+  if (n_visible < 1 || n_visible > 1024 || n_hidden < 1 || !lanes_per_chain || !units_per_lane)
+    return fail(MPV_ERR_ARGS, "plan: bad args");
+  const int words = (n_visible + 31) / 32;
+  int G = 1;
+  while (G < 32 && ((n_hidden + G - 1) / G > 16 || G < words)) G *= 2;
+  const int need = (n_hidden + G - 1) / G;
+  for (int u : kUnits)
+    if (u >= need) {
+      *lanes_per_chain = G;
+      *units_per_lane = u;
+      return MPV_OK;
+    }
+  return fail(MPV_ERR_ARGS, "plan: n_hidden > 512 is not supported by the fused sweep");
+}
+
+int mpv_stream_uniforms(uint64_t key, int64_t n_chains, int64_t chain0, int64_t t0, int64_t n_draws,
+                        double* out, void* stream) {
+  if (n_chains < 0 || n_draws < 0 || (!out && n_chains * n_draws > 0)) return fail(MPV_ERR_ARGS, "stream_uniforms: bad args");
+  if (n_chains * n_draws == 0) return MPV_OK;
+  const int64_t n = n_chains * n_draws;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  stream_uniforms_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(key, n_chains, chain0, t0, n_draws, out);
+  return check_launch("stream_uniforms");
+}
+
+int mpv_chains_init(const mpv_chains* ch, uint64_t key, int proposal, int sector_weight, void* stream) {
+  if (!ch || ch->n_chains < 0 || ch->n_sites < 1 || ch->words != (ch->n_sites + 31) / 32 || !ch->bits)
+    return fail(MPV_ERR_ARGS, "chains_init: bad chain descriptor");
+  if (ch->words > MAX_WORDS_INIT) return fail(MPV_ERR_ARGS, "chains_init: n_sites too large");
+  if (proposal == MPV_PROPOSAL_EXCHANGE && (sector_weight < 0 || sector_weight > ch->n_sites))
+    return fail(MPV_ERR_ARGS, "sector weight out of range");
+  if (ch->status) {
+    const int64_t init[2] = {0, (int64_t)0x7FFFFFFFFFFFFFFFll};
+    cudaMemcpyAsync(ch->status, init, sizeof init, cudaMemcpyHostToDevice, (cudaStream_t)stream);
+  }
+  if (ch->n_chains == 0) return MPV_OK;
+  chains_init_kernel<<<(unsigned)((ch->n_chains + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      *ch, key, proposal, sector_weight);
+  return check_launch("chains_init");
+}
+
+int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, int proposal,
+                 int64_t init_draws, int64_t step_index, int64_t n_steps, int64_t thin,
+                 uint32_t* samples, int64_t n_samples_total, int64_t n_chains_total,
+                 int64_t round_offset, int64_t row0, void* stream) {
+  if (!snap || !ch || !snap->table || !snap->bias || !ch->bits || !ch->log_probs)
+    return fail(MPV_ERR_ARGS, "mh_sweep: null descriptor");
+  if (snap->n_visible != ch->n_sites || ch->words != (ch->n_sites + 31) / 32)
+    return fail(MPV_ERR_ARGS, "mh_sweep: snapshot/chain size mismatch");
+  if (n_steps < 0 || thin < 0 || (samples && thin < 1)) return fail(MPV_ERR_ARGS, "mh_sweep: bad schedule");
+  if (proposal != MPV_PROPOSAL_FLIP && proposal != MPV_PROPOSAL_EXCHANGE)
+    return fail(MPV_ERR_ARGS, "mh_sweep: unknown proposal");
+  if (proposal == MPV_PROPOSAL_EXCHANGE && ch->n_sites < 2)
+    return fail(MPV_ERR_ARGS, "mh_sweep: exchange needs >= 2 sites");
+  if (ch->n_sites >= 65536) return fail(MPV_ERR_ARGS, "mh_sweep: n_sites too large");
+  if (ch->n_chains == 0) return MPV_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t base = 0, extra = 0;
+  if (samples) {
+    if (n_chains_total < 1) return fail(MPV_ERR_ARGS, "mh_sweep: n_chains_total");
+    base = n_samples_total / n_chains_total;
+    extra = n_samples_total % n_chains_total;
+  }
+  const int fmt = snap->fmt, mode = snap->mode;
+
+  if (mode == MPV_MODE_PER_OPERATION && fmt != MPV_FMT_F64) {
+    PerOpSweepArgs a{};
+    a.f.N = snap->n_visible; a.f.M = snap->n_hidden; a.f.Mpad = snap->hidden_pad; a.f.words = ch->words;
+    a.f.table = snap->table; a.f.bias = snap->bias; a.f.vis = snap->vis; a.f.vis_im = snap->vis_im;
+    a.n_chains = ch->n_chains; a.chain_offset = ch->chain_offset; a.bits = ch->bits;
+    a.log_probs = ch->log_probs; a.accepted = ch->accepted; a.status = ch->status; a.key = key;
+    a.init_draws = init_draws; a.step_index = step_index; a.n_steps = n_steps; a.thin = thin;
+    a.samples = samples; a.sample_base = base; a.sample_extra = extra; a.round_offset = round_offset;
+    a.row0 = row0;
+    const int threads = 128, nw = threads / 32;
+    const size_t smem = nw * 64 * sizeof(uint32_t) + (size_t)nw * 2 * snap->n_hidden * sizeof(double);
+    const void* fn = nullptr;
+    const bool ex = proposal == MPV_PROPOSAL_EXCHANGE;
+    if (fmt == MPV_FMT_F16) fn = ex ? (const void*)&perop_sweep_kernel<MPV_FMT_F16, 1> : (const void*)&perop_sweep_kernel<MPV_FMT_F16, 0>;
+    else if (fmt == MPV_FMT_BF16) fn = ex ? (const void*)&perop_sweep_kernel<MPV_FMT_BF16, 1> : (const void*)&perop_sweep_kernel<MPV_FMT_BF16, 0>;
+    else fn = ex ? (const void*)&perop_sweep_kernel<MPV_FMT_F32, 1> : (const void*)&perop_sweep_kernel<MPV_FMT_F32, 0>;
+    if (int rc = ensure_smem(fn, smem)) return rc;
+    void* args[] = {&a};
+    const cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)((ch->n_chains + nw - 1) / nw)), dim3(threads), args, smem, st);
+    if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("perop sweep: ") + cudaGetErrorString(e));
+    return MPV_OK;
+  }
+
+  // fused sweep; f64 and storage-only run the f64 arithmetic
+  const bool f64arith = (fmt == MPV_FMT_F64) || (mode == MPV_MODE_STORAGE_ONLY);
+  const int kfmt = f64arith ? MPV_FMT_F64 : fmt;
+  const int variant = f64arith ? MPV_ACC_F64 : snap->variant;
+  const int G = snap->lanes_per_chain, U = snap->units_per_lane;
+  if (G < 1 || G > 32 || (G & (G - 1)) || G * U != snap->hidden_pad || snap->hidden_pad < snap->n_hidden)
+    return fail(MPV_ERR_ARGS, "mh_sweep: snapshot layout inconsistent");
+  if (G < ch->words) return fail(MPV_ERR_ARGS, "mh_sweep: lanes_per_chain < words");
+  const size_t tbytes = (size_t)snap->n_visible * snap->hidden_pad * entry_bytes(kfmt, variant) +
+                        (size_t)snap->n_visible * vis_bytes(kfmt, variant);
+  const size_t tbytes16 = (tbytes + 15) & ~(size_t)15;
+  const bool use_smem = tbytes16 + 1024 <= (size_t)max_smem_optin();
+  void* fn = nullptr;
+  const int sm = use_smem ? 1 : 0;
+  switch (kfmt) {
+    case MPV_FMT_F16: fn = sweep_kernel_ptr_f16(variant, U, proposal, sm); break;
+    case MPV_FMT_BF16: fn = sweep_kernel_ptr_bf16(variant, U, proposal, sm); break;
+    case MPV_FMT_F32: fn = sweep_kernel_ptr_f32(variant, U, proposal, sm); break;
+    default: fn = sweep_kernel_ptr_f64(variant, U, proposal, sm); break;
+  }
+  if (!fn) return fail(MPV_ERR_ARGS, "mh_sweep: no kernel for this (format, variant, units)");
+  SweepArgs a{};
+  a.N = snap->n_visible; a.M = snap->n_hidden; a.Mpad = snap->hidden_pad; a.G = G; a.words = ch->words;
+  a.table = snap->table; a.bias = snap->bias; a.vis = snap->vis; a.table_bytes = tbytes16;
+  a.table_in_smem = sm;
+  a.n_chains = ch->n_chains; a.chain_offset = ch->chain_offset; a.bits = ch->bits;
+  a.log_probs = ch->log_probs; a.accepted = ch->accepted; a.status = ch->status; a.key = key;
+  a.init_draws = init_draws; a.step_index = step_index; a.n_steps = n_steps; a.thin = thin;
+  a.samples = samples; a.sample_base = base; a.sample_extra = extra; a.round_offset = round_offset;
+  a.row0 = row0;
+  const int threads = 256;
+  const int64_t chains_per_block = (threads / 32) * (32 / G);
+  const size_t smem = use_smem ? tbytes16 : 0;
+  if (int rc = ensure_smem(fn, smem)) return rc;
+  void* args[] = {&a};
+  const cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)((ch->n_chains + chains_per_block - 1) / chains_per_block)),
+                                         dim3(threads), args, smem, st);
+  if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("mh_sweep: ") + cudaGetErrorString(e));
+  return MPV_OK;
+}
+
+int mpv_snapshot_forward(const mpv_snapshot* snap, const uint32_t* bits, int64_t B, double* out_lp,
+                         double* out_re, double* out_im, int64_t* status, void* stream) {
+  if (!snap || !bits || !out_lp || B < 0) return fail(MPV_ERR_ARGS, "snapshot_forward: bad args");
+  if (B == 0) return MPV_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int words = (snap->n_visible + 31) / 32;
+  const int fmt = snap->fmt, mode = snap->mode;
+  if (mode == MPV_MODE_NATIVE && fmt != MPV_FMT_F64) {
+    if (out_re || out_im) return fail(MPV_ERR_ARGS, "snapshot_forward: NATIVE mode has no log psi output");
+    // the fused sweep with zero steps: refresh theta from the bits and write log p
+    mpv_chains ch{};
+    ch.n_chains = B; ch.chain_offset = 0; ch.n_sites = snap->n_visible; ch.words = words;
+    ch.bits = const_cast<uint32_t*>(bits);  // read-only with n_steps == 0 (bits written back unchanged)
+    ch.log_probs = out_lp; ch.accepted = nullptr; ch.status = status;
+    return mpv_mh_sweep(snap, &ch, 0, MPV_PROPOSAL_FLIP, 0, 0, 0, 0, nullptr, 0, 1, 0, 0, stream);
+  }
+  FwdArgs a{};
+  a.N = snap->n_visible; a.M = snap->n_hidden; a.Mpad = snap->hidden_pad; a.words = words;
+  a.table = snap->table; a.bias = snap->bias; a.vis = snap->vis; a.vis_im = snap->vis_im;
+  a.bits = bits; a.B = B; a.out_lp = out_lp; a.out_re = out_re; a.out_im = out_im; a.status = status;
+  const bool want_im = out_re || out_im;
+  if (want_im && !snap->vis_im) return fail(MPV_ERR_ARGS, "snapshot_forward: log psi needs vis_im");
+  const int threads = 256, nw = threads / 32;
+  const size_t smem = nw * 32 * sizeof(uint32_t) + (size_t)nw * 2 * snap->n_hidden * sizeof(double);
+  const void* fn;
+  if (fmt == MPV_FMT_F64 || mode == MPV_MODE_STORAGE_ONLY) fn = (const void*)&forward_kernel<MPV_FMT_F64>;
+  else if (fmt == MPV_FMT_F16) fn = (const void*)&forward_kernel<MPV_FMT_F16>;
+  else if (fmt == MPV_FMT_BF16) fn = (const void*)&forward_kernel<MPV_FMT_BF16>;
+  else fn = (const void*)&forward_kernel<MPV_FMT_F32>;
+  if (int rc = ensure_smem(fn, smem)) return rc;
+  int wi = want_im ? 1 : 0;
+  void* args[] = {&a, &wi};
+  const unsigned grid = (unsigned)std::min<int64_t>((B + nw - 1) / nw, 148 * 32);
+  const cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, st);
+  if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("snapshot_forward: ") + cudaGetErrorString(e));
+  return MPV_OK;
+}
+
+static size_t rup(size_t x) { return (x + 255) / 256 * 256; }
+
+size_t mpv_rounded_scratch_bytes(int64_t B, int N, int M, int fmt) {
+  const size_t pair = fmt == MPV_FMT_F32 ? 8 : 4;
+  return rup((size_t)N * M * pair) + rup((size_t)M * pair) + rup((size_t)N * 4) +
+         rup((size_t)B * ((N + 31) / 32) * 4);
+}
+
+int mpv_rounded_log_prob(const uint8_t* bits, int64_t B, int N, int M, const double* a_re,
+                         const double* b_re, const double* b_im, const double* w_re,
+                         const double* w_im, int fmt, double* out_lp, void* scratch, void* stream) {
+  if (fmt != MPV_FMT_F32 && fmt != MPV_FMT_F16 && fmt != MPV_FMT_BF16)
+    return fail(MPV_ERR_ARGS, "rounded_log_prob: fmt must be f32, f16 or bf16");
+  if (!bits || !a_re || !b_re || !b_im || !w_re || !w_im || !out_lp || !scratch || N < 1 || M < 1 || B < 0)
+    return fail(MPV_ERR_ARGS, "rounded_log_prob: bad args");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t pair = fmt == MPV_FMT_F32 ? 8 : 4;
+  char* p = (char*)scratch;
+  void* table = p;
+  p += rup((size_t)N * M * pair);
+  void* bias = p;
+  p += rup((size_t)M * pair);
+  float* vis = (float*)p;
+  p += rup((size_t)N * 4);
+  uint32_t* packed = (uint32_t*)p;
+  const int64_t n = (int64_t)N * M + M + N;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  if (fmt == MPV_FMT_F16) perop_table_kernel<MPV_FMT_F16><<<grid, 256, 0, st>>>(N, M, a_re, b_re, b_im, w_re, w_im, table, bias, vis);
+  else if (fmt == MPV_FMT_BF16) perop_table_kernel<MPV_FMT_BF16><<<grid, 256, 0, st>>>(N, M, a_re, b_re, b_im, w_re, w_im, table, bias, vis);
+  else perop_table_kernel<MPV_FMT_F32><<<grid, 256, 0, st>>>(N, M, a_re, b_re, b_im, w_re, w_im, table, bias, vis);
+  if (int rc = check_launch("rounded_log_prob table")) return rc;
+  if (B == 0) return MPV_OK;
+  if (int rc = mpv_pack_bits(bits, B, N, packed, stream)) return rc;
+  mpv_snapshot snap{};
+  snap.n_visible = N; snap.n_hidden = M; snap.hidden_pad = M;
+  snap.fmt = fmt; snap.mode = MPV_MODE_PER_OPERATION; snap.variant = MPV_ACC_X1;
+  snap.lanes_per_chain = 1; snap.units_per_lane = M;
+  snap.table = table; snap.bias = bias; snap.vis = vis; snap.vis_im = nullptr;
+  return mpv_snapshot_forward(&snap, packed, B, out_lp, nullptr, nullptr, nullptr, stream);
+}
+
+size_t mpv_energy_tables_bytes(int N, int M, int ham, int n_bonds) {
+  const int T = ham == MPV_HAM_TFIM ? N : n_bonds;
+  return 2 * (size_t)M * T * sizeof(double2) + 2 * (size_t)T * sizeof(double2) + (size_t)T * sizeof(int32_t) + 64;
+}
+
+static void energy_layout(int N, int M, int ham, int n_bonds, void* tables, double2** C, double2** S,
+                          double2** ea, int32_t** slow) {
+  const int T = ham == MPV_HAM_TFIM ? N : n_bonds;
+  char* p = (char*)tables;
+  *C = (double2*)p;
+  p += (size_t)M * T * sizeof(double2);
+  *S = (double2*)p;
+  p += (size_t)M * T * sizeof(double2);
+  *ea = (double2*)p;
+  p += 2 * (size_t)T * sizeof(double2);
+  *slow = (int32_t*)p;
+}
+
+int mpv_energy_prepare(int N, int M, const double* a, const double* b, const double* w_t, int ham,
+                       const int32_t* bonds, int n_bonds, void* tables, void* stream) {
+  if (N < 1 || M < 1 || !a || !b || !w_t || !tables || (ham != MPV_HAM_TFIM && ham != MPV_HAM_HEISENBERG))
+    return fail(MPV_ERR_ARGS, "energy_prepare: bad args");
+  if (ham == MPV_HAM_HEISENBERG && (n_bonds < 1 || !bonds)) return fail(MPV_ERR_ARGS, "energy_prepare: bonds");
+  EnergyArgs e{};
+  e.N = N; e.M = M; e.ham = ham; e.n_bonds = n_bonds; e.n_terms = ham == MPV_HAM_TFIM ? N : n_bonds;
+  e.a = (const double2*)a; e.b = (const double2*)b; e.w_t = (const double2*)w_t; e.bonds = bonds;
+  double2 *C, *S, *ea;
+  int32_t* slow;
+  energy_layout(N, M, ham, n_bonds, tables, &C, &S, &ea, &slow);
+  const int64_t n = (int64_t)M * e.n_terms;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  energy_tables_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(e, C, S, ea, slow);
+  return check_launch("energy_prepare");
+}
+
+int mpv_local_energies(int N, int M, const double* a, const double* b, const double* w_t, int ham,
+                       const int32_t* bonds, int n_bonds, double J, double h, const void* tables,
+                       const uint32_t* bits, int64_t B, double* out_eps, int64_t* status, void* stream) {
+  if (N < 1 || M < 1 || !a || !b || !w_t || !tables || !bits || !out_eps || B < 0)
+    return fail(MPV_ERR_ARGS, "local_energies: bad args");
+  if (ham != MPV_HAM_TFIM && ham != MPV_HAM_HEISENBERG) return fail(MPV_ERR_ARGS, "local_energies: ham");
+  if (n_bonds > 0 && !bonds) return fail(MPV_ERR_ARGS, "local_energies: bonds");
+  if (B == 0) return MPV_OK;
+  EnergyArgs e{};
+  e.N = N; e.M = M; e.words = (N + 31) / 32; e.ham = ham; e.n_bonds = n_bonds;
+  e.n_terms = ham == MPV_HAM_TFIM ? N : n_bonds;
+  e.a = (const double2*)a; e.b = (const double2*)b; e.w_t = (const double2*)w_t; e.bonds = bonds;
+  e.J = J; e.h = h;
+  double2 *C, *S, *ea;
+  int32_t* slow;
+  energy_layout(N, M, ham, n_bonds, const_cast<void*>(tables), &C, &S, &ea, &slow);
+  e.C = C; e.S = S; e.ea = ea; e.slow = slow;
+  e.bits = bits; e.B = B; e.out = (double2*)out_eps; e.status = status;
+  const size_t smem = (size_t)kEnergyWarps * kSamplesPerWarp * 2 * M * sizeof(double2) +
+                      (size_t)kEnergyWarps * kSamplesPerWarp * 32 * sizeof(uint32_t);
+  if (smem > (size_t)max_smem_optin()) return fail(MPV_ERR_ARGS, "local_energies: n_hidden too large");
+  if (int rc = ensure_smem((const void*)&energy_kernel, smem)) return rc;
+  const int64_t per_block = (int64_t)kEnergyWarps * kSamplesPerWarp;
+  energy_kernel<<<(unsigned)((B + per_block - 1) / per_block), kEnergyWarps * 32, smem, (cudaStream_t)stream>>>(e);
+  return check_launch("local_energies");
+}
+
+int mpv_unpack_bits(const uint32_t* words, int64_t B, int N, uint8_t* out, void* stream) {
+  if (!words || !out || B < 0 || N < 1) return fail(MPV_ERR_ARGS, "unpack_bits: bad args");
+  if (B == 0) return MPV_OK;
+  const int64_t n = B * N;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  unpack_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(words, B, N, (N + 31) / 32, out);
+  return check_launch("unpack_bits");
+}
+
+int mpv_pack_bits(const uint8_t* bits, int64_t B, int N, uint32_t* out, void* stream) {
+  if (!bits || !out || B < 0 || N < 1) return fail(MPV_ERR_ARGS, "pack_bits: bad args");
+  if (B == 0) return MPV_OK;
+  const int nw = (N + 31) / 32;
+  const int64_t n = B * nw;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  pack_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(bits, B, N, nw, out);
+  return check_launch("pack_bits");
+}
+
+int mpv_sum_i64(const int64_t* x, int64_t n, int64_t* out, void* stream) {
+  if (!x || !out || n < 0) return fail(MPV_ERR_ARGS, "sum_i64: bad args");
+  sum_i64_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(x, n, out);
+  return check_launch("sum_i64");
+}
+
+#pragma GCC visibility pop
+}  // extern "C"

@@ -1,0 +1,522 @@
+// Fused Metropolis–Hastings sweep (ref: sampler.py:111-133 ChainEnsemble.step,
+// repeated n_steps times; sampler.py:142-167 collect) for the RBM log-probability
+// (ref: rbm.py:361-405 log_prob_evaluator) — one launch runs many proposals per
+// chain with the chain's state on chip.
+//
+// Layout: a chain is owned by a segment of G lanes of one warp (32/G chains
+// per warp).  Hidden unit i = u*G + gl lives in lane gl of the segment, slot u
+// (U slots per lane), so a flip of site k reads the contiguous column
+// table[k*Mpad + ...] with conflict-free shared-memory loads.  The packed
+// configuration is spread over the segment (word w in lane w).  theta = b + W x
+// is kept EXACT in registers (X1 / X2 / F64 accumulators), the
+// log p of a proposal is a fixed function of the proposed configuration, and
+// the accept test is the reference's f64 `log(u) < lp_new - lp_old`.
+#pragma once
+#include "common.cuh"
+
+namespace mpv {
+
+struct SweepArgs {
+  // snapshot
+  int N, M, Mpad, G, words;
+  const void* table;  // global copy of the table
+  const void* bias;
+  const void* vis;
+  size_t table_bytes;
+  int table_in_smem;
+  // chains
+  int64_t n_chains, chain_offset;
+  uint32_t* bits;
+  double* log_probs;
+  int64_t* accepted;
+  int64_t* status;
+  // schedule
+  uint64_t key;
+  int64_t init_draws, step_index, n_steps, thin;
+  uint32_t* samples;
+  int64_t sample_base, sample_extra, round_offset, row0;
+};
+
+// ------------------------------------------------------------------------
+// Unit evaluators: Re log cosh of one hidden unit in the snapshot's arithmetic.
+// ------------------------------------------------------------------------
+
+// f16 / bf16 NATIVE: theta' rounded once to the format, Re log cosh in f32 with
+// 3 MUFU ops  ½ log(1 + t² + 2 t cos 2y) + |x| - ln2,  t = e^{-2|x|}
+// (the same closed form as ref _logcosh_pair, rbm.py:130-140), result rounded
+// to the format by the caller (pairs of units share one F2FP).
+__device__ __forceinline__ float lc_fast(float x, float y) {
+  const float ax = fabsf(x);
+  const float t = ex2_approx(ax * -2.8853900817779268f);  // e^{-2|x|}
+  const float c = cos_approx(y + y);
+  const float s = fmaf(2.0f, c, t);
+  const float v = fmaf(t, s, 1.0f);
+  return fmaf(lg2_approx(v), 0.34657359027997264f, ax - 0.69314718055994531f);
+}
+
+// f32 NATIVE: accurate single-precision regime-split form:
+// |cosh z|² = 1 + sinh²x - sin²y = sinh²x + cos²y.
+__device__ __forceinline__ float lc_f32(float x, float y) {
+  const float ax = fabsf(x);
+  float s, c;
+  sincosf(y, &s, &c);
+  if (ax > 9.0f) {
+    const float t = expf(-2.0f * ax);
+    const float c2 = fmaf(2.0f * c, c, -1.0f);
+    return ax - 0.69314718055994531f + 0.5f * log1pf(t * (t + 2.0f * c2));
+  }
+  const float sh = sinhf(ax);
+  if (c * c >= 0.5f) return 0.5f * log1pf(fmaf(sh, sh, -s * s));
+  return 0.5f * logf(fmaf(sh, sh, c * c));
+}
+
+// f64: the reference formula op for op (rbm.py:130-140 / _kernels.py:101-106).
+__device__ __forceinline__ double lc_f64(double tr, double ti) {
+  const double u = fabs(tr);
+  const double v = tr >= 0.0 ? ti : -ti;
+  const double t = exp(-2.0 * u);
+  const double wr = __dmul_rn(__dadd_rn(1.0, t), cos(v));
+  const double wi = __dmul_rn(__dadd_rn(1.0, -t), sin(v));
+  const double q = __dadd_rn(__dmul_rn(wr, wr), __dmul_rn(wi, wi));
+  return __dadd_rn(__dadd_rn(u, -0.69314718055994530942), __dmul_rn(0.5, log(q)));
+}
+
+// ------------------------------------------------------------------------
+// Accumulator variants.  Each provides:
+//   Entry      table element type;  Vis  visible-bias element type
+//   init(b)    theta = bias;         add(e, d) theta += d*e (d in {-1,0,1})
+//   eval/lc    contribution of the unit for theta + d*e (proposal)
+// ------------------------------------------------------------------------
+
+template <int FMT, int VAR> struct Acc;
+
+// ---- X1, f16/bf16: theta in one f32 per component (exact by planner check) ----
+template <int FMT> struct Acc<FMT, MPV_ACC_X1> {
+  using H = Half<FMT>;
+  using Entry = uint32_t;
+  using Vis = float;
+  using Sign = uint16_t;
+  float re, im;
+  __device__ __forceinline__ static Sign sign(int d) {
+    return d > 0 ? H::kOne : (d < 0 ? H::kMinusOne : (uint16_t)0);
+  }
+  __device__ __forceinline__ void init(Entry b) { re = H::lo(b); im = H::hi(b); }
+  __device__ __forceinline__ void add(Entry e, Sign d) {
+    re = H::fma_lo(e, d, re);
+    im = H::fma_hi(e, d, im);
+  }
+  // theta' for a one-column move
+  __device__ __forceinline__ void prop1(Entry e, Sign d, float& xr, float& xi) const {
+    xr = H::fma_lo(e, d, re);
+    xi = H::fma_hi(e, d, im);
+  }
+  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float& xr,
+                                        float& xi) const {
+    xr = H::fma_lo(e1, d, H::fma_lo(e2, md, re));
+    xi = H::fma_hi(e1, d, H::fma_hi(e2, md, im));
+  }
+};
+
+// ---- X2, f16/bf16: hi/lo f32 accumulators on a fixed split grid ----
+template <int FMT> struct Acc<FMT, MPV_ACC_X2> {
+  using H = Half<FMT>;
+  using Entry = uint2;  // x: hi pair, y: lo pair
+  using Vis = float2;
+  using Sign = uint16_t;
+  float hr, hi_, lr, li;
+  __device__ __forceinline__ static Sign sign(int d) {
+    return d > 0 ? H::kOne : (d < 0 ? H::kMinusOne : (uint16_t)0);
+  }
+  __device__ __forceinline__ void init(Entry b) {
+    hr = H::lo(b.x); hi_ = H::hi(b.x); lr = H::lo(b.y); li = H::hi(b.y);
+  }
+  __device__ __forceinline__ void add(Entry e, Sign d) {
+    hr = H::fma_lo(e.x, d, hr); hi_ = H::fma_hi(e.x, d, hi_);
+    lr = H::fma_lo(e.y, d, lr); li = H::fma_hi(e.y, d, li);
+  }
+  __device__ __forceinline__ void prop1(Entry e, Sign d, float& xr, float& xi) const {
+    xr = H::fma_lo(e.x, d, hr) + H::fma_lo(e.y, d, lr);
+    xi = H::fma_hi(e.x, d, hi_) + H::fma_hi(e.y, d, li);
+  }
+  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float& xr,
+                                        float& xi) const {
+    xr = H::fma_lo(e1.x, d, H::fma_lo(e2.x, md, hr)) + H::fma_lo(e1.y, d, H::fma_lo(e2.y, md, lr));
+    xi = H::fma_hi(e1.x, d, H::fma_hi(e2.x, md, hi_)) + H::fma_hi(e1.y, d, H::fma_hi(e2.y, md, li));
+  }
+};
+
+// ---- X1, f32 format: float pairs ----
+template <> struct Acc<MPV_FMT_F32, MPV_ACC_X1> {
+  using Entry = float2;
+  using Vis = float;
+  using Sign = float;
+  float re, im;
+  __device__ __forceinline__ static Sign sign(int d) { return (float)d; }
+  __device__ __forceinline__ void init(Entry b) { re = b.x; im = b.y; }
+  __device__ __forceinline__ void add(Entry e, Sign d) { re = fmaf(e.x, d, re); im = fmaf(e.y, d, im); }
+  __device__ __forceinline__ void prop1(Entry e, Sign d, float& xr, float& xi) const {
+    xr = fmaf(e.x, d, re);
+    xi = fmaf(e.y, d, im);
+  }
+  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float& xr,
+                                        float& xi) const {
+    xr = fmaf(e1.x, d, fmaf(e2.x, md, re));
+    xi = fmaf(e1.y, d, fmaf(e2.y, md, im));
+  }
+};
+
+// ---- X2, f32 format ----
+template <> struct Acc<MPV_FMT_F32, MPV_ACC_X2> {
+  using Entry = float4;  // hi re, hi im, lo re, lo im
+  using Vis = float2;
+  using Sign = float;
+  float hr, hi_, lr, li;
+  __device__ __forceinline__ static Sign sign(int d) { return (float)d; }
+  __device__ __forceinline__ void init(Entry b) { hr = b.x; hi_ = b.y; lr = b.z; li = b.w; }
+  __device__ __forceinline__ void add(Entry e, Sign d) {
+    hr = fmaf(e.x, d, hr); hi_ = fmaf(e.y, d, hi_); lr = fmaf(e.z, d, lr); li = fmaf(e.w, d, li);
+  }
+  __device__ __forceinline__ void prop1(Entry e, Sign d, float& xr, float& xi) const {
+    xr = fmaf(e.x, d, hr) + fmaf(e.z, d, lr);
+    xi = fmaf(e.y, d, hi_) + fmaf(e.w, d, li);
+  }
+  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float& xr,
+                                        float& xi) const {
+    xr = fmaf(e1.x, d, fmaf(e2.x, md, hr)) + fmaf(e1.z, d, fmaf(e2.z, md, lr));
+    xi = fmaf(e1.y, d, fmaf(e2.y, md, hi_)) + fmaf(e1.w, d, fmaf(e2.w, md, li));
+  }
+};
+
+// ---- F64 accumulators (any format; f64/storage-only evaluate in f64) ----
+template <int FMT> struct Acc<FMT, MPV_ACC_F64> {
+  using Entry = double2;
+  using Vis = double;
+  using Sign = double;
+  double re, im;
+  __device__ __forceinline__ static Sign sign(int d) { return (double)d; }
+  __device__ __forceinline__ void init(Entry b) { re = b.x; im = b.y; }
+  __device__ __forceinline__ void add(Entry e, Sign d) { re = fma(e.x, d, re); im = fma(e.y, d, im); }
+  __device__ __forceinline__ void prop1(Entry e, Sign d, double& xr, double& xi) const {
+    xr = fma(e.x, d, re);
+    xi = fma(e.y, d, im);
+  }
+  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, double& xr,
+                                        double& xi) const {
+    xr = fma(e1.x, d, fma(e2.x, md, re));
+    xi = fma(e1.y, d, fma(e2.y, md, im));
+  }
+};
+
+// ------------------------------------------------------------------------
+// Per-unit contribution and the final log p for each (FMT, VAR) combination.
+// The f64 path (FMT == F64, or STORAGE_ONLY passed as FMT_F64) sums in f64;
+// the reduced formats sum in f32.
+// ------------------------------------------------------------------------
+template <int FMT, int VAR> struct Eval {
+  using A = Acc<FMT, VAR>;
+  static constexpr bool kF64 = (FMT == MPV_FMT_F64);
+  using Sum = typename std::conditional<kF64, double, float>::type;
+
+  // Contribution of two units (u0, u1) given proposed theta in f32 (or f64).
+  // Reduced formats: theta rounded to fmt, lc in f32, lc rounded to fmt, then
+  // accumulated in f32 (mask 0 for padded units).
+  template <typename T>
+  __device__ __forceinline__ static void pair(T xr0, T xi0, T xr1, T xi1, float m0, float m1,
+                                              Sum& acc) {
+    if constexpr (kF64) {
+      acc += (double)m0 * lc_f64(xr0, xi0);
+      acc += (double)m1 * lc_f64(xr1, xi1);
+    } else {
+      float a0 = (float)xr0, b0 = (float)xi0, a1 = (float)xr1, b1 = (float)xi1;
+      if constexpr (FMT == MPV_FMT_F32) {
+        acc = fmaf(m0, lc_f32(a0, b0), acc);
+        acc = fmaf(m1, lc_f32(a1, b1), acc);
+      } else {
+        using H = Half<FMT>;
+        const uint32_t p0 = H::pack(a0, b0), p1 = H::pack(a1, b1);
+        const float l0 = lc_fast(H::lo(p0), H::hi(p0));
+        const float l1 = lc_fast(H::lo(p1), H::hi(p1));
+        const uint32_t lp = H::pack(l0, l1);
+        acc = fmaf(m0, H::lo(lp), acc);
+        acc = fmaf(m1, H::hi(lp), acc);
+      }
+    }
+  }
+  template <typename T>
+  __device__ __forceinline__ static void single(T xr, T xi, float m, Sum& acc) {
+    if constexpr (kF64) {
+      acc += (double)m * lc_f64(xr, xi);
+    } else if constexpr (FMT == MPV_FMT_F32) {
+      acc = fmaf(m, lc_f32((float)xr, (float)xi), acc);
+    } else {
+      using H = Half<FMT>;
+      const uint32_t p = H::pack((float)xr, (float)xi);
+      const uint32_t lp = H::pack(lc_fast(H::lo(p), H::hi(p)), 0.0f);
+      acc = fmaf(m, H::lo(lp), acc);
+    }
+  }
+  // Visible term (exact) and hidden sum -> log p (double).
+  __device__ __forceinline__ static double finalize(typename A::Vis vis, Sum h) {
+    if constexpr (kF64) {
+      return 2.0 * (vis + h);
+    } else if constexpr (VAR == MPV_ACC_F64) {
+      return 2.0 * (double)__fadd_rn(__double2float_rn(vis), h);
+    } else if constexpr (VAR == MPV_ACC_X2) {
+      return 2.0 * (double)__fadd_rn(__fadd_rn(vis.x, vis.y), h);
+    } else {
+      return 2.0 * (double)__fadd_rn(vis, h);
+    }
+  }
+};
+
+template <typename V> __device__ __forceinline__ V vis_add(V v, V a, int d);
+template <> __device__ __forceinline__ float vis_add(float v, float a, int d) { return fmaf(a, (float)d, v); }
+template <> __device__ __forceinline__ float2 vis_add(float2 v, float2 a, int d) {
+  return make_float2(fmaf(a.x, (float)d, v.x), fmaf(a.y, (float)d, v.y));
+}
+template <> __device__ __forceinline__ double vis_add(double v, double a, int d) { return fma(a, (double)d, v); }
+template <typename V> __device__ __forceinline__ V vis_zero();
+template <> __device__ __forceinline__ float vis_zero<float>() { return 0.0f; }
+template <> __device__ __forceinline__ float2 vis_zero<float2>() { return make_float2(0.f, 0.f); }
+template <> __device__ __forceinline__ double vis_zero<double>() { return 0.0; }
+
+// Record the first (lowest step, then lowest chain) non-finite evaluation.
+__device__ __forceinline__ void report_nonfinite(int64_t* status, int64_t step, int64_t chain) {
+  if (!status) return;
+  atomicMin((unsigned long long*)&status[1], (unsigned long long)((step << 32) | chain));
+  atomicExch((unsigned long long*)&status[0], (unsigned long long)MPV_ERR_NONFINITE);
+}
+
+// ------------------------------------------------------------------------
+// The kernel.
+// ------------------------------------------------------------------------
+template <int FMT, int VAR, int U, int PROP, bool SMEM>
+__global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
+  using A = Acc<FMT, VAR>;
+  using E = Eval<FMT, VAR>;
+  using Entry = typename A::Entry;
+  using VisT = typename A::Vis;
+  using Sign = typename A::Sign;
+  using Sum = typename E::Sum;
+  using Theta = typename std::conditional<VAR == MPV_ACC_F64, double, float>::type;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Entry* tab;
+  const VisT* visv;
+  if constexpr (SMEM) {
+    // Stage the snapshot (column table, then visible biases) into shared memory
+    // with one bulk async copy (TMA engine, cp.async.bulk) on an mbarrier.
+    __shared__ __align__(8) uint64_t bar;
+    const uint32_t bytes = (uint32_t)a.table_bytes;
+    const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(&bar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(bytes)
+                   : "memory");
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem_raw);
+      uint32_t off = 0;
+      while (off < bytes) {
+        const uint32_t chunk = min(bytes - off, 65536u);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                dst + off),
+            "l"((const char*)a.table + off), "r"(chunk), "r"(sbar)
+            : "memory");
+        off += chunk;
+      }
+    }
+    asm volatile(
+        "{.reg .pred p;\nWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
+            sbar)
+        : "memory");
+    tab = reinterpret_cast<const Entry*>(smem_raw);
+    visv = reinterpret_cast<const VisT*>(smem_raw + (size_t)a.N * a.Mpad * sizeof(Entry));
+  } else {
+    tab = reinterpret_cast<const Entry*>(a.table);
+    visv = reinterpret_cast<const VisT*>((const char*)a.table + (size_t)a.N * a.Mpad * sizeof(Entry));
+  }
+
+  const int G = a.G;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int slot = lane / G;
+  const int cpw = 32 / G;
+  const int64_t chain = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * cpw + slot;
+  const bool live = chain < a.n_chains;
+  const int64_t cidx = live ? chain : 0;  // tail lanes mirror chain 0 and never write
+  const int64_t gchain = a.chain_offset + cidx;
+  const int N = a.N;
+  const int words = a.words;
+
+  uint32_t myword = (gl < words) ? a.bits[cidx * words + gl] : 0u;
+
+  // per-slot masks (padded hidden units contribute 0)
+  float mask[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) mask[u] = (u * G + gl < a.M) ? 1.0f : 0.0f;
+
+  // ---- refresh: theta = b + W x, vis = a.x, log p (set_evaluator semantics) ----
+  A acc[U];
+  const Entry* bias = reinterpret_cast<const Entry*>(a.bias);
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u].init(bias[u * G + gl]);
+  VisT vis = vis_zero<VisT>();
+  const Sign one = A::sign(1);
+  for (int w = 0; w < words; ++w) {
+    uint32_t word = __shfl_sync(kFull, myword, w, G);
+    while (word) {
+      const int b = __ffs(word) - 1;
+      word &= word - 1;
+      const int k = w * 32 + b;
+      const Entry* col = tab + (size_t)k * a.Mpad + gl;
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u].add(col[u * G], one);
+      vis = vis_add(vis, visv[k], 1);
+    }
+  }
+  Sum h0 = Sum(0);
+#pragma unroll
+  for (int u = 0; u + 1 < U; u += 2) {
+    Theta xr0, xi0, xr1, xi1;
+    acc[u].prop1(Entry{}, A::sign(0), xr0, xi0);
+    acc[u + 1].prop1(Entry{}, A::sign(0), xr1, xi1);
+    E::pair(xr0, xi0, xr1, xi1, mask[u], mask[u + 1], h0);
+  }
+  if constexpr (U & 1) {
+    Theta xr, xi;
+    acc[U - 1].prop1(Entry{}, A::sign(0), xr, xi);
+    E::single(xr, xi, mask[U - 1], h0);
+  }
+  h0 = segment_sum(h0, G);
+  double lp = E::finalize(vis, h0);
+  bool dead = false;
+  if (!isfinite(lp)) {
+    dead = true;
+    if (live && gl == 0) report_nonfinite(a.status, 0, cidx);
+  }
+
+  // ---- the MH loop ----
+  const uint64_t s0 = stream_state(a.key, (uint64_t)gchain);
+  const int64_t count_c =
+      a.sample_base + ((gchain < a.sample_extra) ? 1 : 0);
+  const int64_t offset_c =
+      gchain * a.sample_base + (gchain < a.sample_extra ? gchain : a.sample_extra) - a.row0;
+  int64_t n_acc = 0;
+  int sel_c = 0;        // cached selection (site, or pair i | j<<16)
+  double logu_c = 0.0;  // cached log(u_accept)
+  const double n_pairs = 0.5 * (double)N * (double)(N - 1);
+
+  int64_t next_record = (a.samples && a.thin > 0) ? a.thin : -1;
+  for (int64_t s = 0; s < a.n_steps; ++s) {
+    const int src = (int)(s & (G - 1));
+    if (src == 0) {
+      // lane gl draws the two uniforms of step s+gl (ref: sampler.py:113,127)
+      const uint64_t t = (uint64_t)(a.init_draws + 2 * (a.step_index + s + gl));
+      const double us = stream_draw(s0, t);
+      const double ua = stream_draw(s0, t + 1);
+      if (PROP == MPV_PROPOSAL_FLIP) {
+        sel_c = (int)floor_scaled(us, (double)N);
+      } else {
+        int i, j;
+        pair_of(floor_scaled(us, n_pairs), N, i, j);
+        sel_c = i | (j << 16);
+      }
+      logu_c = log(ua);
+    }
+    const int sel = __shfl_sync(kFull, sel_c, src, G);
+    const double logu = __shfl_sync(kFull, logu_c, src, G);
+
+    int dsign, k1, k2 = 0;
+    if (PROP == MPV_PROPOSAL_FLIP) {
+      k1 = sel;
+      const uint32_t wd = __shfl_sync(kFull, myword, k1 >> 5, G);
+      dsign = ((wd >> (k1 & 31)) & 1u) ? -1 : 1;
+    } else {
+      k1 = sel & 0xFFFF;
+      k2 = sel >> 16;
+      const uint32_t wi = __shfl_sync(kFull, myword, k1 >> 5, G);
+      const uint32_t wj = __shfl_sync(kFull, myword, k2 >> 5, G);
+      const int bi = (wi >> (k1 & 31)) & 1u, bj = (wj >> (k2 & 31)) & 1u;
+      dsign = bj - bi;  // x_i' = x_j: theta' = theta + d (W_:i - W_:j)
+    }
+    // Every segment evaluates (no divergence around the segment shuffles); an
+    // exchange of equal bits (dsign == 0) evaluates theta itself and is then
+    // accepted unconditionally: the reference evaluator returns the cached
+    // value, Δ = 0 and log u < 0 (sampler.py:119-131).
+    const Sign d = A::sign(dsign);
+    const Sign md = A::sign(-dsign);
+    Entry e1[U], e2[U];
+    const Entry* c1 = tab + (size_t)k1 * a.Mpad + gl;
+    const Entry* c2 = tab + (size_t)k2 * a.Mpad + gl;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      e1[u] = c1[u * G];
+      if (PROP == MPV_PROPOSAL_EXCHANGE) e2[u] = c2[u * G];
+    }
+    Sum h = Sum(0);
+#pragma unroll
+    for (int u = 0; u + 1 < U; u += 2) {
+      Theta xr0, xi0, xr1, xi1;
+      if (PROP == MPV_PROPOSAL_FLIP) {
+        acc[u].prop1(e1[u], d, xr0, xi0);
+        acc[u + 1].prop1(e1[u + 1], d, xr1, xi1);
+      } else {
+        acc[u].prop2(e1[u], e2[u], d, md, xr0, xi0);
+        acc[u + 1].prop2(e1[u + 1], e2[u + 1], d, md, xr1, xi1);
+      }
+      E::pair(xr0, xi0, xr1, xi1, mask[u], mask[u + 1], h);
+    }
+    if constexpr (U & 1) {
+      Theta xr, xi;
+      if (PROP == MPV_PROPOSAL_FLIP) acc[U - 1].prop1(e1[U - 1], d, xr, xi);
+      else acc[U - 1].prop2(e1[U - 1], e2[U - 1], d, md, xr, xi);
+      E::single(xr, xi, mask[U - 1], h);
+    }
+    h = segment_sum(h, G);
+    VisT vnew = vis_add(vis, visv[k1], dsign);
+    if (PROP == MPV_PROPOSAL_EXCHANGE) vnew = vis_add(vnew, visv[k2], -dsign);
+    const double lp_new = E::finalize(vnew, h);
+    // ref sampler.py:128-129: NaN compares false (reject); the reference raises
+    // EvaluationFailureError on any non-finite proposal (rbm.py:242-251): the
+    // chain freezes and the first failure is reported.
+    if (dsign != 0 && !isfinite(lp_new) && !dead) {
+      dead = true;
+      if (live && gl == 0) report_nonfinite(a.status, a.step_index + s + 1, cidx);
+    }
+    const bool accept = !dead && (dsign == 0 || logu < lp_new - lp);
+    const bool moved = accept && dsign != 0;
+    if (moved) {
+      vis = vnew;
+      lp = lp_new;
+      if (gl == (k1 >> 5)) myword ^= 1u << (k1 & 31);
+      if (PROP == MPV_PROPOSAL_EXCHANGE && gl == (k2 >> 5)) myword ^= 1u << (k2 & 31);
+    }
+    n_acc += accept ? 1 : 0;
+    const Sign dacc = moved ? d : A::sign(0);
+    const Sign mdacc = moved ? md : A::sign(0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (PROP == MPV_PROPOSAL_FLIP) acc[u].add(e1[u], dacc);
+      else { acc[u].add(e1[u], dacc); acc[u].add(e2[u], mdacc); }
+    }
+    if (s + 1 == next_record) {
+      next_record += a.thin;
+      const int64_t r = a.round_offset + (s + 1) / a.thin - 1;
+      if (live && r < count_c && gl < words) a.samples[(offset_c + r) * words + gl] = myword;
+    }
+  }
+
+  if (live) {
+    if (gl < words) a.bits[cidx * words + gl] = myword;
+    if (gl == 0) {
+      a.log_probs[cidx] = lp;
+      if (a.accepted) a.accepted[cidx] += n_acc;
+    }
+  }
+}
+
+}  // namespace mpv

@@ -1,0 +1,428 @@
+"""RBM neural quantum state on the B200: parameters (host, f64 master copy),
+the reduced-precision snapshot in kernel layout (device), and the evaluator
+objects the sampler and the local energies consume.
+
+Mirrors the reference rbm.py API: ``RbmParameters`` (rbm.py:27-75),
+``random_parameters`` (:78-88), ``round_parameters`` (:91-101),
+``save_parameters``/``load_parameters`` (:104-127), ``log_prob_evaluator``
+(:361-405), ``log_psi_evaluator`` (:419-425), ``log_prob_batch``/``log_psi_batch``
+(:254-296), ``grad_log_psi_batch`` (:307-325).  Evaluation always runs in the
+CUDA library; the evaluators are device objects that ``ChainEnsemble``
+recognises and fuses, and they stay callable on uint8 numpy rows (host round
+trip) so reference callers keep working.
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+
+from . import _native as nat
+from .errors import EvaluationFailureError
+from .lattice import pack_bits
+from .precision import F64, FloatFormat, RoundingMode, make_rounder
+from .rng import gaussian_field
+
+
+@dataclass(frozen=True)
+class RbmParameters:
+    """Complex visible biases a (N,), hidden biases b (M,), weights w (M, N)."""
+
+    a: np.ndarray
+    b: np.ndarray
+    w: np.ndarray
+
+    def __post_init__(self):
+        a = np.asarray(self.a, dtype=np.complex128)
+        b = np.asarray(self.b, dtype=np.complex128)
+        w = np.asarray(self.w, dtype=np.complex128)
+        if a.ndim != 1 or b.ndim != 1 or w.shape != (b.size, a.size):
+            raise ValueError(f"inconsistent dimensions: a{a.shape}, b{b.shape}, w{w.shape}")
+        for name, arr in (("a", a), ("b", b), ("w", w)):
+            if not np.all(np.isfinite(arr.view(np.float64))):
+                raise ValueError(f"non-finite entries in {name}")
+        object.__setattr__(self, "a", a)
+        object.__setattr__(self, "b", b)
+        object.__setattr__(self, "w", w)
+
+    @property
+    def n_visible(self) -> int:
+        return self.a.size
+
+    @property
+    def n_hidden(self) -> int:
+        return self.b.size
+
+    @property
+    def alpha_density(self) -> Fraction:
+        return Fraction(self.n_hidden, self.n_visible)
+
+    @property
+    def n_params(self) -> int:
+        return self.n_visible + self.n_hidden + self.n_visible * self.n_hidden
+
+    def flatten(self) -> np.ndarray:
+        return np.concatenate([self.a, self.b, self.w.reshape(-1)])
+
+    @classmethod
+    def from_flat(cls, theta, n_visible: int, n_hidden: int) -> "RbmParameters":
+        theta = np.asarray(theta, dtype=np.complex128)
+        return cls(theta[:n_visible], theta[n_visible:n_visible + n_hidden],
+                   theta[n_visible + n_hidden:].reshape(n_hidden, n_visible))
+
+
+def random_parameters(n_visible: int, alpha, key, scale: float = 0.01) -> RbmParameters:
+    """Re and Im i.i.d. N(0, scale^2) from the counter-based Gaussian field
+    (rbm.py:78-88); host-side, once per run."""
+    alpha = Fraction(alpha)
+    n_hidden = alpha * n_visible
+    if n_hidden.denominator != 1 or n_hidden <= 0:
+        raise ValueError(f"alpha*N must be a positive integer, got {n_hidden}")
+    n_hidden = int(n_hidden)
+    count = n_visible + n_hidden + n_hidden * n_visible
+    draws = scale * gaussian_field(key, np.arange(2 * count), 1.0)
+    return RbmParameters.from_flat(draws[:count] + 1j * draws[count:], n_visible, n_hidden)
+
+
+def round_parameters(params: RbmParameters, fmt: FloatFormat) -> RbmParameters:
+    """Two-copy downcast snapshot (rbm.py:91-101): Re and Im rounded RNE to fmt."""
+    if fmt.name == "f64":
+        return params
+    rnd = make_rounder(fmt)
+
+    def q(arr):
+        with np.errstate(over="ignore"):
+            return rnd(arr.real) + 1j * rnd(arr.imag)
+
+    return RbmParameters(q(params.a), q(params.b), q(params.w))
+
+
+def save_parameters(params: RbmParameters, path):
+    """rbm-params-v1 JSON (rbm.py:104-114)."""
+    payload = {
+        "format": "rbm-params-v1",
+        "n_visible": params.n_visible,
+        "n_hidden": params.n_hidden,
+        "a": [[float(v.real), float(v.imag)] for v in params.a],
+        "b": [[float(v.real), float(v.imag)] for v in params.b],
+        "w": [[[float(v.real), float(v.imag)] for v in row] for row in params.w],
+    }
+    with open(path, "w") as handle:
+        json.dump(payload, handle)
+
+
+def load_parameters(path) -> RbmParameters:
+    with open(path) as handle:
+        payload = json.load(handle)
+    if payload.get("format") != "rbm-params-v1":
+        raise ValueError(f"unrecognized parameter file {path}")
+
+    def decode(entries):
+        arr = np.asarray(entries, dtype=np.float64)
+        return arr[..., 0] + 1j * arr[..., 1]
+
+    return RbmParameters(decode(payload["a"]), decode(payload["b"]), decode(payload["w"]))
+
+
+# ---------------------------------------------------------------------------
+# Exact-theta planner
+# ---------------------------------------------------------------------------
+
+def finest_quantum(values: np.ndarray) -> float:
+    """Largest power of two dividing every nonzero finite value (1.0 if none)."""
+    v = np.abs(np.asarray(values, dtype=np.float64).ravel())
+    v = v[(v != 0) & np.isfinite(v)]
+    if v.size == 0:
+        return 1.0
+    m, e = np.frexp(v)
+    mi = (m * 2.0**53).astype(np.int64)
+    tz = np.log2((mi & -mi).astype(np.float64)).astype(np.int64)
+    return float(np.ldexp(1.0, int((e.astype(np.int64) - 53 + tz).min())))
+
+
+@dataclass(frozen=True)
+class ExactPlan:
+    """Which on-chip accumulator keeps theta = b + W x exact for a snapshot.
+
+    All partial sums of the snapshot's values are multiples of ``quantum`` and
+    bounded by ``bound``; f32 holds every multiple of q up to 2^24 q exactly.
+    X1: one f32 per component (bound <= 2^24 q).  X2: theta = hi + lo with
+    hi on the grid ``split`` (|hi| <= 2^24 split) and |lo| <= (N+1) split/2 <= 2^24 q.
+    F64: otherwise (f64 accumulators, converted per unit)."""
+
+    variant: int
+    quantum: float
+    bound: float
+    split: float
+
+
+def plan_exact(snap: RbmParameters) -> ExactPlan:
+    a, b, w = snap.a, snap.b, snap.w
+    vals = np.concatenate([a.real, b.real, b.imag, w.real.ravel(), w.imag.ravel()])
+    q = finest_quantum(vals)
+    bound = max(
+        float(np.max(np.abs(b.real) + np.abs(w.real).sum(axis=1))),
+        float(np.max(np.abs(b.imag) + np.abs(w.imag).sum(axis=1))),
+        float(np.abs(a.real).sum()),
+    )
+    if bound <= 2.0**24 * q:
+        return ExactPlan(nat.ACC_X1, q, bound, 0.0)
+    n_terms = snap.n_visible + 1
+    split = 2.0 ** math.floor(math.log2(2.0**25 * q / n_terms))
+    if split >= q and bound + n_terms * split / 2 <= 2.0**24 * split:
+        return ExactPlan(nat.ACC_X2, q, bound, split)
+    return ExactPlan(nat.ACC_F64, q, bound, 0.0)
+
+
+# ---------------------------------------------------------------------------
+# Device snapshot (kernel layout)
+# ---------------------------------------------------------------------------
+
+def _half_bits(x: np.ndarray, fmt: str) -> np.ndarray:
+    """uint16 bit patterns of values that are exactly representable in fmt."""
+    if fmt == "f16":
+        h = x.astype(np.float16)
+        return h.view(np.uint16)
+    f = x.astype(np.float32).view(np.uint32)
+    return (f >> np.uint32(16)).astype(np.uint16)
+
+
+def _pairs(re: np.ndarray, im: np.ndarray, fmt: str) -> np.ndarray:
+    """Entry array of (re, im) pairs in fmt: uint32 (f16/bf16) or float32x2."""
+    if fmt == "f32":
+        out = np.empty(re.shape + (2,), dtype=np.float32)
+        out[..., 0], out[..., 1] = re, im
+        return out
+    return _half_bits(re, fmt).astype(np.uint32) | (_half_bits(im, fmt).astype(np.uint32) << np.uint32(16))
+
+
+def _pad16(buf: bytes) -> bytes:
+    return buf + b"\0" * ((-len(buf)) % 16)
+
+
+class DeviceSnapshot:
+    """Parameters of one evaluator in kernel layout, resident on the device
+    (the device counterpart of rbm.py:161-200 _PreparedRounded)."""
+
+    def __init__(self, params: RbmParameters, fmt: FloatFormat, mode: RoundingMode, device=None):
+        import torch
+
+        nat.require_cuda()
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.fmt, self.mode = fmt, mode
+        f64arith = fmt.name == "f64" or mode is RoundingMode.STORAGE_ONLY
+        snap = round_parameters(params, fmt)
+        self.params = snap
+        N, M = snap.n_visible, snap.n_hidden
+        self.n_visible, self.n_hidden = N, M
+        wt = snap.w.T  # (N, M): column k of W is row k of the table
+        if mode is RoundingMode.PER_OPERATION and not f64arith:
+            G, U, Mpad = 1, M, M
+            variant = nat.ACC_X1
+            table = _pairs(wt.real, wt.imag, fmt.name)
+            bias = _pairs(snap.b.real, snap.b.imag, fmt.name)
+            vis = snap.a.real.astype(np.float32)
+        else:
+            G, U = nat.plan_layout(N, M)
+            Mpad = G * U
+            wpad = np.zeros((N, Mpad), dtype=np.complex128)
+            wpad[:, :M] = wt
+            bpad = np.zeros(Mpad, dtype=np.complex128)
+            bpad[:M] = snap.b
+            if f64arith:
+                variant = nat.ACC_F64
+            else:
+                self.plan = plan_exact(snap)
+                variant = self.plan.variant
+            if variant == nat.ACC_F64:
+                table = np.stack([wpad.real, wpad.imag], axis=-1)
+                bias = np.stack([bpad.real, bpad.imag], axis=-1)
+                vis = snap.a.real.astype(np.float64)
+            elif variant == nat.ACC_X1:
+                table = _pairs(wpad.real, wpad.imag, fmt.name)
+                bias = _pairs(bpad.real, bpad.imag, fmt.name)
+                vis = snap.a.real.astype(np.float32)
+            else:
+                g = self.plan.split
+
+                def split(x):
+                    hi = np.rint(x / g) * g
+                    return hi, x - hi
+
+                whr, wlr = split(wpad.real)
+                whi, wli = split(wpad.imag)
+                bhr, blr = split(bpad.real)
+                bhi, bli = split(bpad.imag)
+                ahi, alo = split(snap.a.real)
+                th, tl = _pairs(whr, whi, fmt.name), _pairs(wlr, wli, fmt.name)
+                bh, bl = _pairs(bhr, bhi, fmt.name), _pairs(blr, bli, fmt.name)
+                table = np.stack([th, tl], axis=-2 if fmt.name == "f32" else -1)
+                bias = np.stack([bh, bl], axis=-2 if fmt.name == "f32" else -1)
+                vis = np.stack([ahi, alo], axis=-1).astype(np.float32)
+        self.variant, self.lanes_per_chain, self.units_per_lane, self.hidden_pad = variant, G, U, Mpad
+        blob = _pad16(np.ascontiguousarray(table).tobytes()) + _pad16(np.ascontiguousarray(vis).tobytes())
+        self._table = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(self.device)
+        tbytes = len(_pad16(np.ascontiguousarray(table).tobytes()))
+        self._bias = torch.frombuffer(bytearray(_pad16(np.ascontiguousarray(bias).tobytes())),
+                                      dtype=torch.uint8).to(self.device)
+        self._vis_im = torch.from_numpy(np.ascontiguousarray(snap.a.imag, dtype=np.float64)).to(self.device)
+        base = self._table.data_ptr()
+        self.struct = nat.Snapshot(N, M, Mpad, fmt.code, mode.code, variant, G, U,
+                                   base, self._bias.data_ptr(), base + tbytes, self._vis_im.data_ptr())
+
+    @property
+    def label(self) -> str:
+        names = {nat.ACC_X1: "X1", nat.ACC_X2: "X2", nat.ACC_F64: "F64"}
+        return f"{self.fmt.name}/{self.mode.value}/{names[self.variant]}/G{self.lanes_per_chain}xU{self.units_per_lane}"
+
+
+# ---------------------------------------------------------------------------
+# Evaluators
+# ---------------------------------------------------------------------------
+
+def _status_tensor(device):
+    import torch
+
+    return torch.tensor([0, 2**63 - 1], dtype=torch.int64, device=device)
+
+
+class LogProbEvaluator:
+    """Batch log-probability evaluator ``uint8[B,N] -> float64[B]`` (the
+    reference evaluator protocol, sampler.py:49-53) backed by a device snapshot.
+    ChainEnsemble fuses it into the MH sweep instead of calling it."""
+
+    def __init__(self, params: RbmParameters, fmt: FloatFormat = F64,
+                 mode: RoundingMode = RoundingMode.PER_OPERATION, device=None):
+        if fmt.name == "f64":
+            mode = RoundingMode.PER_OPERATION  # f64 ignores the mode (rbm.py:364-372)
+        self.fmt, self.mode = fmt, mode
+        self.master = params
+        self.snapshot = DeviceSnapshot(params, fmt, mode, device)
+        self.device = self.snapshot.device
+
+    @property
+    def n_visible(self):
+        return self.snapshot.n_visible
+
+    def log_prob_packed(self, packed):
+        """Device path: packed uint32 [B, words] tensor -> float64 [B] tensor."""
+        import torch
+
+        B = packed.shape[0]
+        out = torch.empty(B, dtype=torch.float64, device=self.device)
+        status = _status_tensor(self.device)
+        nat.call("mpv_snapshot_forward", ctypes_byref(self.snapshot.struct), packed.data_ptr(), B,
+                 out.data_ptr(), None, None, status.data_ptr(), nat.stream_handle(self.device))
+        return out, status
+
+    def __call__(self, bits) -> np.ndarray:
+        import torch
+
+        bits = np.atleast_2d(np.asarray(bits, dtype=np.uint8))
+        if bits.shape[1] != self.n_visible:
+            raise ValueError(f"bit matrix has {bits.shape[1]} sites, ansatz has {self.n_visible}")
+        packed = torch.from_numpy(pack_bits(bits)).to(self.device)
+        out, status = self.log_prob_packed(packed)
+        out = out.cpu().numpy()
+        _raise_nonfinite(status, bits, "log probability")
+        return out
+
+
+class LogPsiEvaluator:
+    """f64 log-amplitude evaluator ``uint8[B,N] -> complex128[B]`` with the
+    master parameters (rbm.py:419-425); also carries the parameters the
+    device local-energy kernel needs."""
+
+    def __init__(self, params: RbmParameters, device=None):
+        self.params = params
+        self.snapshot = DeviceSnapshot(params, F64, RoundingMode.PER_OPERATION, device)
+        self.device = self.snapshot.device
+        self._energy_cache = {}
+
+    def log_psi_packed(self, packed):
+        import torch
+
+        B = packed.shape[0]
+        lp = torch.empty(B, dtype=torch.float64, device=self.device)
+        re = torch.empty_like(lp)
+        im = torch.empty_like(lp)
+        status = _status_tensor(self.device)
+        nat.call("mpv_snapshot_forward", ctypes_byref(self.snapshot.struct), packed.data_ptr(), B,
+                 lp.data_ptr(), re.data_ptr(), im.data_ptr(), status.data_ptr(), nat.stream_handle(self.device))
+        return re, im, status
+
+    def __call__(self, bits) -> np.ndarray:
+        import torch
+
+        bits = np.atleast_2d(np.asarray(bits, dtype=np.uint8))
+        if bits.shape[1] != self.snapshot.n_visible:
+            raise ValueError(f"bit matrix has {bits.shape[1]} sites, ansatz has {self.snapshot.n_visible}")
+        packed = torch.from_numpy(pack_bits(bits)).to(self.device)
+        re, im, status = self.log_psi_packed(packed)
+        out = re.cpu().numpy() + 1j * im.cpu().numpy()
+        _raise_nonfinite(status, bits, "log psi")
+        return out
+
+
+def ctypes_byref(struct):
+    import ctypes
+
+    return ctypes.byref(struct)
+
+
+def _raise_nonfinite(status, bits, what):
+    st = status.cpu().numpy()
+    if st[0] != 0:
+        bad = int(st[1])
+        raise EvaluationFailureError(f"non-finite {what} for configuration bits {bits[bad].tolist()}",
+                                     context={"bits": bits[bad].copy()})
+
+
+def log_prob_evaluator(params, fmt: FloatFormat = F64, mode: RoundingMode = RoundingMode.PER_OPERATION,
+                       device=None) -> LogProbEvaluator:
+    """Device log-probability evaluator (rbm.py:361-405); parameters are
+    downcast once at construction.  ``mode=RoundingMode.NATIVE`` selects the
+    B200 fused-sweep arithmetic."""
+    return LogProbEvaluator(params, fmt, mode, device)
+
+
+def log_psi_evaluator(params, device=None) -> LogPsiEvaluator:
+    return LogPsiEvaluator(params, device)
+
+
+def log_prob_batch(params, bits, fmt: FloatFormat = F64, mode: RoundingMode = RoundingMode.PER_OPERATION,
+                   device=None) -> np.ndarray:
+    """log p(x) for a (B, N) bit matrix (rbm.py:276-296)."""
+    bits = np.atleast_2d(np.asarray(bits))
+    if bits.shape[1] != params.n_visible:
+        raise ValueError(f"bit matrix has {bits.shape[1]} sites, ansatz has {params.n_visible}")
+    return LogProbEvaluator(params, fmt, mode, device)(bits)
+
+
+def log_psi_batch(params, bits, fmt: FloatFormat = F64, mode: RoundingMode = RoundingMode.PER_OPERATION,
+                  device=None) -> np.ndarray:
+    """log psi(x) (rbm.py:254-273): f64 / storage-only via the f64 kernel on
+    the (rounded) parameters, per-operation via the emulation kernel."""
+    import torch
+
+    bits = np.atleast_2d(np.asarray(bits, dtype=np.uint8))
+    if bits.shape[1] != params.n_visible:
+        raise ValueError(f"bit matrix has {bits.shape[1]} sites, ansatz has {params.n_visible}")
+    if fmt.name == "f64" or mode is RoundingMode.STORAGE_ONLY:
+        return LogPsiEvaluator(round_parameters(params, fmt), device)(bits)
+    if mode is RoundingMode.NATIVE:
+        raise ValueError("NATIVE mode computes log p only (use log_prob_batch)")
+    snap = DeviceSnapshot(params, fmt, mode, device)
+    packed = torch.from_numpy(pack_bits(bits)).to(snap.device)
+    B = bits.shape[0]
+    lp = torch.empty(B, dtype=torch.float64, device=snap.device)
+    re, im = torch.empty_like(lp), torch.empty_like(lp)
+    status = _status_tensor(snap.device)
+    nat.call("mpv_snapshot_forward", ctypes_byref(snap.struct), packed.data_ptr(), B, lp.data_ptr(),
+             re.data_ptr(), im.data_ptr(), status.data_ptr(), nat.stream_handle(snap.device))
+    out = re.cpu().numpy() + 1j * im.cpu().numpy()
+    _raise_nonfinite(status, bits, "log psi")
+    return out

@@ -1,0 +1,259 @@
+"""Metropolis–Hastings chain ensemble on the B200 (mirror of the reference
+sampler.py:24-251: ``Proposal``, ``pair_table``, ``ChainEnsemble``,
+``run_chains``, ``default_chain_count``).
+
+The ensemble state (packed configurations, cached log p, per-chain accepted
+counts) lives on the device.  ``step``/``run_steps``/``run_sweeps``/``collect``
+launch the fused sweep kernel (csrc/sweep.cuh) for any number of proposals,
+with draws from the reference's own counter-based splitmix64 streams, so a run
+reproduces the reference ChainEnsemble's decisions (bit for bit in
+PER_OPERATION mode; up to documented near-threshold ties in f32/f64).
+
+Sharding: ``chain_offset`` / ``n_chains_total`` place this ensemble's chains at
+global ids [offset, offset + n_chains); draws depend on global ids only, so the
+shards of a multi-GPU run reproduce the single-GPU run exactly.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .errors import EvaluationFailureError
+from .lattice import unpack_bits
+from .rng import derive_key, mix64, uniform_from_bits
+
+DEFAULT_SAMPLES_PER_CHAIN = 4
+MAX_STEPS_PER_LAUNCH = 1 << 16  # bounded kernel duration
+
+
+@dataclass(frozen=True)
+class Proposal:
+    """Single-flip or exchange proposal family (sampler.py:24-39)."""
+
+    kind: str
+    sector_weight: int | None = None
+
+    def __post_init__(self):
+        if self.kind not in ("flip", "exchange"):
+            raise ValueError(f"unknown proposal kind {self.kind!r}")
+
+    @property
+    def code(self) -> int:
+        return nat.PROPOSAL_FLIP if self.kind == "flip" else nat.PROPOSAL_EXCHANGE
+
+
+def pair_table(n: int) -> np.ndarray:
+    """All unordered site pairs (i < j) in lexicographic order (sampler.py:42-45)."""
+    i, j = np.triu_indices(n, k=1)
+    return np.stack([i, j], axis=1).astype(np.int64).reshape(-1, 2)
+
+
+def default_chain_count(n_samples: int) -> int:
+    return max(1, n_samples // DEFAULT_SAMPLES_PER_CHAIN)
+
+
+def _device_evaluator(evaluator):
+    from .rbm import LogProbEvaluator
+
+    if not isinstance(evaluator, LogProbEvaluator):
+        raise TypeError(
+            f"ChainEnsemble needs a device evaluator from rbm.log_prob_evaluator, got "
+            f"{type(evaluator).__name__} (the B200 path has no host-callable fallback)")
+    return evaluator
+
+
+class ChainEnsemble:
+    """A batch of independent MH chains sharing one device evaluator
+    (sampler.py:48-167).  Acceptance counters cover every proposal since the
+    last reset."""
+
+    def __init__(self, n_chains, n_sites, proposal: Proposal, evaluator, key, *, chain_offset: int = 0,
+                 n_chains_total: int | None = None):
+        import torch
+
+        nat.require_cuda()
+        self.n_chains = int(n_chains)
+        self.n_sites = int(n_sites)
+        if self.n_chains < 0 or self.n_sites < 1:
+            raise ValueError("need n_chains >= 0 and n_sites >= 1")
+        self.proposal = proposal
+        self.key = int(np.uint64(key))
+        self.chain_offset = int(chain_offset)
+        self.n_chains_total = int(n_chains_total) if n_chains_total is not None else self.n_chains + self.chain_offset
+        self._evaluator = _device_evaluator(evaluator)
+        if self._evaluator.n_visible != self.n_sites:
+            raise ValueError("evaluator and ensemble disagree on the number of sites")
+        self.device = self._evaluator.device
+        self.words = (self.n_sites + 31) // 32
+        dev = self.device
+        self._bits = torch.zeros((self.n_chains, self.words), dtype=torch.int32, device=dev)
+        self._logp = torch.zeros(self.n_chains, dtype=torch.float64, device=dev)
+        self._acc = torch.zeros(self.n_chains, dtype=torch.int64, device=dev)
+        self._status = torch.tensor([0, 2**63 - 1], dtype=torch.int64, device=dev)
+        self._acc_total = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.proposed = 0
+        self.steps_done = 0
+        if proposal.kind == "flip":
+            weight = 0
+            self.init_draws = self.n_sites
+        else:
+            weight = self.n_sites // 2 if proposal.sector_weight is None else int(proposal.sector_weight)
+            if not 0 <= weight <= self.n_sites:
+                raise ValueError(f"sector weight {weight} out of range")
+            self.init_draws = self.n_sites - 1
+        self._chains = nat.Chains(self.n_chains, self.chain_offset, self.n_sites, self.words,
+                                  self._bits.data_ptr(), self._logp.data_ptr(), self._acc.data_ptr(),
+                                  self._status.data_ptr())
+        nat.call("mpv_chains_init", ctypes.byref(self._chains), self.key, proposal.code, weight, self._stream())
+        self._launch(0)  # cached log p of the initial configurations (sampler.py:63)
+        self._check()
+
+    # -- internals ----------------------------------------------------------
+    def _stream(self):
+        return nat.stream_handle(self.device)
+
+    def _launch(self, n_steps, thin=0, samples=None, n_samples_total=0, round_offset=0, row0=0):
+        nat.call("mpv_mh_sweep", ctypes.byref(self._evaluator.snapshot.struct), ctypes.byref(self._chains),
+                 self.key, self.proposal.code, self.init_draws, self.steps_done, int(n_steps), int(thin),
+                 samples.data_ptr() if samples is not None else None, int(n_samples_total),
+                 self.n_chains_total, int(round_offset), int(row0), self._stream())
+        self.steps_done += int(n_steps)
+        self.proposed += self.n_chains * int(n_steps)
+
+    def _check(self):
+        st = self._status.cpu().numpy()
+        if st[0] != 0:
+            key = int(st[1])
+            step, chain = key >> 32, key & 0xFFFFFFFF
+            bits = self._proposal_bits(chain, step)
+            raise EvaluationFailureError(
+                f"non-finite log probability for configuration bits {bits.tolist()}",
+                context={"bits": bits, "chain": self.chain_offset + chain, "step": step})
+
+    def _proposal_bits(self, chain, step):
+        """Configuration whose evaluation failed: the chain is frozen at the
+        state before `step`; step 0 is the initial evaluation."""
+        x = unpack_bits(self._bits[chain:chain + 1].cpu().numpy().view(np.uint32), self.n_sites)[0].copy()
+        if step == 0:
+            return x
+        g = 0x9E3779B97F4A7C15
+        s0 = mix64(self.key ^ (((self.chain_offset + chain + 1) * g) & 0xFFFFFFFFFFFFFFFF))
+        t = self.init_draws + 2 * (step - 1)
+        u = float(uniform_from_bits(np.uint64(mix64((s0 + (t + 1) * g) & 0xFFFFFFFFFFFFFFFF))))
+        if self.proposal.kind == "flip":
+            x[int(u * self.n_sites)] ^= 1
+        else:
+            i, j = pair_table(self.n_sites)[int(u * (self.n_sites * (self.n_sites - 1) // 2))]
+            x[i], x[j] = x[j], x[i]
+        return x
+
+    # -- reference API ------------------------------------------------------
+    def set_evaluator(self, evaluator):
+        """Swap the target; refreshes every chain's cached log-probability (sampler.py:90-93)."""
+        ev = _device_evaluator(evaluator)
+        if ev.n_visible != self.n_sites:
+            raise ValueError("evaluator and ensemble disagree on the number of sites")
+        self._evaluator = ev
+        self._launch(0)
+        self._check()
+
+    def reset_counters(self):
+        self._acc.zero_()
+        self.proposed = 0
+
+    @property
+    def evaluator(self):
+        return self._evaluator
+
+    @property
+    def bits(self) -> np.ndarray:
+        return unpack_bits(self._bits.cpu().numpy().view(np.uint32), self.n_sites)
+
+    @property
+    def packed_bits(self):
+        """Device tensor of packed configurations (int32 view of uint32 words)."""
+        return self._bits
+
+    @property
+    def log_probs(self) -> np.ndarray:
+        return self._logp.cpu().numpy().copy()
+
+    @property
+    def accepted(self) -> int:
+        nat.call("mpv_sum_i64", self._acc.data_ptr(), self.n_chains, self._acc_total.data_ptr(), self._stream())
+        return int(self._acc_total.item())
+
+    @property
+    def accepted_per_chain(self):
+        return self._acc
+
+    @property
+    def acceptance_rate(self) -> float:
+        return self.accepted / self.proposed if self.proposed else float("nan")
+
+    def step(self):
+        """One MH proposal per chain (sampler.py:111-133)."""
+        self.run_steps(1)
+
+    def run_steps(self, n_steps: int, check: bool = True):
+        remaining = int(n_steps)
+        while remaining > 0:
+            chunk = min(remaining, MAX_STEPS_PER_LAUNCH)
+            self._launch(chunk)
+            remaining -= chunk
+        if check:
+            self._check()
+
+    def run_sweeps(self, n_sweeps: int, check: bool = True):
+        self.run_steps(int(n_sweeps) * self.n_sites, check)
+
+    def collect_packed(self, n_samples: int, thin_steps: int = 1, check: bool = True):
+        """collect() leaving the samples on the device as packed uint32 words
+        [rows of this shard, words] (int32 tensor)."""
+        import torch
+
+        n_samples, thin_steps = int(n_samples), int(thin_steps)
+        if thin_steps < 1:
+            raise ValueError("thin_steps must be >= 1")
+        base, extra = divmod(n_samples, self.n_chains_total)
+        rounds = base + (1 if extra else 0) if n_samples else 0
+        first = self.chain_offset
+        last = self.chain_offset + self.n_chains
+        row0 = first * base + min(first, extra)
+        row1 = last * base + min(last, extra)
+        samples = torch.zeros((row1 - row0, self.words), dtype=torch.int32, device=self.device)
+        r = 0
+        per_launch = max(1, MAX_STEPS_PER_LAUNCH // thin_steps)
+        while r < rounds:
+            k = min(per_launch, rounds - r)
+            self._launch(k * thin_steps, thin_steps, samples, n_samples, r, row0)
+            r += k
+        if check:
+            self._check()
+        return samples
+
+    def collect(self, n_samples: int, thin_steps: int = 1) -> np.ndarray:
+        """Record n_samples total, thinned by proposal steps, merged chain-major
+        (sampler.py:142-167); returns this shard's uint8 rows."""
+        import torch
+
+        packed = self.collect_packed(n_samples, thin_steps)
+        out = torch.empty((packed.shape[0], self.n_sites), dtype=torch.uint8, device=self.device)
+        if packed.shape[0]:
+            nat.call("mpv_unpack_bits", packed.data_ptr(), packed.shape[0], self.n_sites, out.data_ptr(),
+                     self._stream())
+        return out.cpu().numpy()
+
+
+def run_chains(n_chains, n_samples, burn_in_steps, thin_steps, seed, logprob, proposal: Proposal, n_sites):
+    """Run independent chains and pool samples (sampler.py:221-247)."""
+    if min(n_chains, n_samples) < 1 or thin_steps < 1 or burn_in_steps < 0:
+        raise ValueError("counts must be positive")
+    ensemble = ChainEnsemble(n_chains, n_sites, proposal, logprob, derive_key(seed, "chains"))
+    ensemble.run_steps(burn_in_steps)
+    ensemble.reset_counters()
+    samples = ensemble.collect(n_samples, thin_steps)
+    return samples, ensemble.acceptance_rate

@@ -1,0 +1,174 @@
+"""Generate golden vectors by running the REFERENCE implementation itself.
+
+Run in the build container (the reference lives at /root/reference, read-only):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONPATH=/root/reference/pkg/src \
+        python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz.  The GPU box never runs this (it has no
+/root/reference); tests load the committed .npz files.  Every array here is an
+output of the unmodified reference API (mpvmc), so the oracle and the CUDA path
+are pinned to the reference's own numbers.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+from mpvmc import rbm, sampler, vmc  # noqa: E402
+from mpvmc.bounds import pinsker_tv_bound, theorem3_gaussian_bound  # noqa: E402
+from mpvmc.hamiltonians import HeisenbergSpec, TfimSpec, exact_ground_state  # noqa: E402
+from mpvmc.lattice import LatticeSpec  # noqa: E402
+from mpvmc.precision import BF16, F16, F32, F64, RoundingMode  # noqa: E402
+from mpvmc.rng import StreamSet, derive_key, mix64  # noqa: E402
+from mpvmc.sampler import ChainEnsemble, Proposal, run_chains  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+FMTS = {"f64": F64, "f32": F32, "f16": F16, "bf16": BF16}
+PER_OP = RoundingMode.PER_OPERATION
+
+
+def save(name, **arrays):
+    path = os.path.join(OUT, name)
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+
+
+def gen_rng():
+    paths = [(0, ("chains",)), (0, ("init",)), (7, ("train",)), (7, ("chain", 0)), (7, ("chain", 1)),
+             (12345, ("params",)), (3, ("chains",)), (2**63 + 5, ("noise", 4))]
+    keys = np.array([derive_key(s, *p) for s, p in paths], dtype=np.uint64)
+    key = derive_key(0, "chains")
+    streams = StreamSet(key, 37)
+    draws = np.array([streams.next_uniform() for _ in range(50)])  # (50, 37)
+    mix_in = np.array([0, 1, 2, 0xDEADBEEF, 2**64 - 1], dtype=np.uint64)
+    save("rng.npz", path_seeds=np.array([s for s, _ in paths], dtype=np.uint64),
+         path_labels=np.array(["/".join(map(str, p)) for _, p in paths]), keys=keys,
+         stream_key=np.uint64(key), stream_draws=draws, mix_in=mix_in, mix_out=mix64(mix_in))
+
+
+def random_bits(rng, n_rows, n):
+    bits = rng.integers(0, 2, size=(n_rows, n), dtype=np.uint8)
+    bits[0] = 0
+    bits[1] = 1
+    return bits
+
+
+def gen_forward():
+    cases = [(10, 1, 5, 0.5), (16, 2, 6, 0.3), (12, 1, 7, 0.01), (20, 1, 8, 1.0)]
+    arrays = {}
+    rng = np.random.default_rng(2601)
+    for ci, (n, alpha, seed, scale) in enumerate(cases):
+        p = rbm.random_parameters(n, alpha, derive_key(seed, "params"), scale)
+        bits = random_bits(rng, 160, n)
+        arrays[f"c{ci}_meta"] = np.array([n, alpha, seed, scale])
+        arrays[f"c{ci}_a"], arrays[f"c{ci}_b"], arrays[f"c{ci}_w"] = p.a, p.b, p.w
+        arrays[f"c{ci}_bits"] = bits
+        for name, fmt in FMTS.items():
+            arrays[f"c{ci}_{name}_lp"] = rbm.log_prob_batch(p, bits, fmt, PER_OP)
+            arrays[f"c{ci}_{name}_psi"] = rbm.log_psi_batch(p, bits, fmt, PER_OP)
+            snap = rbm.round_parameters(p, fmt)
+            arrays[f"c{ci}_{name}_snap_a"] = snap.a
+            arrays[f"c{ci}_{name}_snap_b"] = snap.b
+            arrays[f"c{ci}_{name}_snap_w"] = snap.w
+            if name != "f64":
+                arrays[f"c{ci}_{name}_storage_lp"] = rbm.log_prob_batch(
+                    p, bits, fmt, RoundingMode.STORAGE_ONLY)
+    # SURVEY §8(c) value: p = random_parameters(4, 1, derive_key(0,"params"), 0.5), bits [1,0,1,1]
+    p = rbm.random_parameters(4, 1, derive_key(0, "params"), 0.5)
+    x = np.array([[1, 0, 1, 1]], dtype=np.uint8)
+    for name, fmt in FMTS.items():
+        arrays[f"kat_{name}_lp"] = rbm.log_prob_batch(p, x, fmt, PER_OP)
+    arrays["kat_a"], arrays["kat_b"], arrays["kat_w"] = p.a, p.b, p.w
+    # random_parameters for the host init (ndtri of counter uniforms)
+    q = rbm.random_parameters(6, 2, derive_key(11, "init"), 0.01)
+    arrays["init_a"], arrays["init_b"], arrays["init_w"] = q.a, q.b, q.w
+    save("forward.npz", n_cases=np.array(len(cases)), **arrays)
+
+
+def gen_chains():
+    arrays = {}
+    n, alpha = 12, 2
+    p = rbm.random_parameters(n, alpha, derive_key(0, "params"), 0.4)
+    arrays["a"], arrays["b"], arrays["w"] = p.a, p.b, p.w
+    key = derive_key(3, "chains")
+    arrays["key"] = np.uint64(key)
+    checkpoints = [0, 1, 50, 300]
+    for kind, weight in (("flip", None), ("exchange", 6)):
+        for name, fmt in FMTS.items():
+            ev = rbm.log_prob_evaluator(p, fmt, PER_OP)
+            ens = ChainEnsemble(64, n, Proposal(kind, weight), ev, key)
+            done = 0
+            for cp in checkpoints:
+                ens.run_steps(cp - done)
+                done = cp
+                arrays[f"{kind}_{name}_bits_{cp}"] = ens.bits
+                arrays[f"{kind}_{name}_logp_{cp}"] = ens.log_probs
+                arrays[f"{kind}_{name}_acc_{cp}"] = np.array(ens.accepted)
+    # run_chains layouts
+    for ri, (c, s, burn, thin) in enumerate([(64, 200, 37, 13), (50, 50, 0, 1), (40, 7, 5, 3)]):
+        for name in ("f64", "f32"):
+            ev = rbm.log_prob_evaluator(p, FMTS[name], PER_OP)
+            samples, rate = run_chains(c, s, burn, thin, 9, ev, Proposal("flip"), n)
+            arrays[f"run{ri}_{name}_samples"] = samples
+            arrays[f"run{ri}_{name}_rate"] = np.array(rate)
+            arrays[f"run{ri}_args"] = np.array([c, s, burn, thin, 9])
+    # run_chains(4, 8, 10, 5, seed 0, f32 per-op, flip, n=4)
+    p4 = rbm.random_parameters(4, 1, derive_key(0, "params"), 0.5)
+    samples, rate = run_chains(4, 8, 10, 5, 0, rbm.log_prob_evaluator(p4, F32, PER_OP), Proposal("flip"), 4)
+    arrays["kat4_samples"], arrays["kat4_rate"] = samples, np.array(rate)
+    save("chains.npz", **arrays)
+
+
+def gen_energy():
+    arrays = {}
+    rng = np.random.default_rng(77)
+    specs = [
+        ("tfim_chain10", TfimSpec(LatticeSpec.chain(10), 1.0, 0.7)),
+        ("tfim_sq4", TfimSpec(LatticeSpec.square(4), 1.0, 3.04)),
+        ("heis_chain8", HeisenbergSpec(LatticeSpec.chain(8, periodic=True), 1.0)),
+        ("heis_sq4", HeisenbergSpec(LatticeSpec.square(4), 1.0)),
+        ("tfim_chain20_open", TfimSpec(LatticeSpec.chain(20), 1.0, 1.0)),
+        ("tfim_sq10", TfimSpec(LatticeSpec.square(10), 1.0, 3.04)),
+    ]
+    for tag, spec in specs:
+        n = spec.lattice.n_sites
+        p = rbm.random_parameters(n, 2, derive_key(5, tag), 0.3)
+        if isinstance(spec, HeisenbergSpec):
+            bits = np.zeros((48, n), dtype=np.uint8)
+            for r in range(48):
+                bits[r, rng.permutation(n)[: n // 2]] = 1
+        else:
+            bits = rng.integers(0, 2, size=(48, n), dtype=np.uint8)
+        arrays[f"{tag}_bonds"] = spec.lattice.bond_array()
+        arrays[f"{tag}_a"], arrays[f"{tag}_b"], arrays[f"{tag}_w"] = p.a, p.b, p.w
+        arrays[f"{tag}_bits"] = bits
+        arrays[f"{tag}_eps"] = vmc.local_energies(spec, rbm.log_psi_evaluator(p), bits)
+        arrays[f"{tag}_coupling"] = np.array([spec.j, getattr(spec, "h", 0.0)])
+    for tag, spec in [("ed_tfim8", TfimSpec(LatticeSpec.chain(8), 1.0, 1.0)),
+                      ("ed_heis8", HeisenbergSpec(LatticeSpec.chain(8, periodic=True), 1.0)),
+                      ("ed_tfim3x3", TfimSpec(LatticeSpec.square(3), 1.0, 3.04))]:
+        e0, _ = exact_ground_state(spec)
+        arrays[tag] = np.array(e0)
+    # the survey's chain-4 KAT
+    p = rbm.random_parameters(4, 1, derive_key(0, "params"), 0.5)
+    x = np.array([[1, 0, 1, 1]], dtype=np.uint8)
+    arrays["kat_tfim4"] = vmc.local_energies(TfimSpec(LatticeSpec.chain(4), 1, 1), rbm.log_psi_evaluator(p), x)
+    arrays["kat_heis4"] = vmc.local_energies(HeisenbergSpec(LatticeSpec.chain(4), 1), rbm.log_psi_evaluator(p), x)
+    sig = np.array([0.0, 1e-4, 1e-2, 0.3, 1.0, 2.0])
+    arrays["bound_sigma"] = sig
+    arrays["bound_pinsker"] = np.array([pinsker_tv_bound(s) for s in sig])
+    arrays["bound_theorem3"] = np.array([theorem3_gaussian_bound(s, 0.0, 0.0) for s in sig])
+    save("energy.npz", **arrays)
+
+
+if __name__ == "__main__":
+    gen_rng()
+    gen_forward()
+    gen_chains()
+    gen_energy()
