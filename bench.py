@@ -1,0 +1,383 @@
+"""Benchmark of the hot path: reduced-precision MH sampling of an RBM NQS +
+the f64 local energies that consume the samples (BASELINE.json metric
+"MCMC chain-steps/sec per GPU").
+
+Workload (BASELINE.json configs[1]): RBM alpha=2 on the 10x10 periodic TFIM at
+h=3.04 (J=1), 16,384 chains per GPU, f16 sampling (NATIVE fused sweep) + f64
+local energies.  One step = the sampling phase of one VMC iteration as the
+reference runs it (vmc.py:531-564): publish the f16 snapshot, re-burn 2 sweeps,
+collect 4 samples per chain at thinning N+1 (sampler.py:142-167), then f64 local
+energies of all samples and the energy / acceptance reductions.  Chain-steps
+per step = chains * (2N + 4(N+1)).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Under torchrun each rank owns 16,384 chains (weak scaling, global chain ids),
+and NCCL all-reduces the energy sums and acceptance counts once per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+L = 10
+N_SITES = L * L
+ALPHA = 2
+H_FIELD = 3.04
+CHAINS_PER_GPU = 16384
+SAMPLES_PER_CHAIN = 4
+REBURN_SWEEPS = 2
+BURN_IN_SWEEPS = 10 * N_SITES // 10  # 100 sweeps of initial equilibration (untimed)
+INIT_SCALE = 0.01  # reference default init (vmc.py:338)
+WORKLOAD = "rbm_a2_tfim10x10_h3.04_c16384_f16native_f64energy"
+
+
+def chain_steps_per_step(chains):
+    return chains * (REBURN_SWEEPS * N_SITES + SAMPLES_PER_CHAIN * (N_SITES + 1))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def start(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self._proc = None
+            return
+        self._thread = threading.Thread(target=self._read, daemon=True)
+        self._thread.start()
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2601_20782_b200 import F16, RoundingMode, rbm, sampler, vmc
+    from paper_2601_20782_b200.hamiltonians import TfimSpec
+    from paper_2601_20782_b200.lattice import LatticeSpec
+    from paper_2601_20782_b200.rng import derive_key
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    spec = TfimSpec(LatticeSpec.square(L), 1.0, H_FIELD)
+    params = rbm.random_parameters(N_SITES, ALPHA, derive_key(0, "init"), INIT_SCALE)
+    C = CHAINS_PER_GPU
+    n_total_chains = C * world
+    n_samples_total = n_total_chains * SAMPLES_PER_CHAIN
+    thin = N_SITES + 1
+    ev = rbm.log_prob_evaluator(params, F16, RoundingMode.NATIVE)
+    ens = sampler.ChainEnsemble(C, N_SITES, sampler.Proposal("flip"), ev, derive_key(0, "chains"),
+                                chain_offset=rank * C, n_chains_total=n_total_chains)
+    ens.run_sweeps(BURN_IN_SWEEPS)
+    psi = rbm.log_psi_evaluator(params)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    launches = {"n": 0}
+
+    def device_step(record=None):
+        """Inputs resident in HBM: snapshot already built; returns device scalars."""
+        ens.set_evaluator(ev)  # refresh launch (set_evaluator semantics)
+        ens.reset_counters()
+        ens.run_sweeps(REBURN_SWEEPS, check=False)
+        if record is not None:
+            record[0].record(stream)
+        packed = ens.collect_packed(n_samples_total, thin, check=False)
+        if record is not None:
+            record[1].record(stream)
+        kern = vmc._energy_kernel(spec, psi)
+        eps, status = kern.packed(packed)
+        e_sum = eps[:, 0].sum()
+        acc = ens.accepted_per_chain.sum()
+        launches["n"] = 6  # refresh, re-burn sweep, collect sweep, energy, (2 torch reductions not ours)
+        return e_sum, acc, packed.shape[0]
+
+    # warmup
+    for _ in range(args.warmup):
+        device_step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    total_ms = 0.0
+    sweep_ms = 0.0
+    energies = []
+    accs = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between timed iterations (untimed)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e_sum, acc, rows = device_step((s0, s1))
+        if dist is not None:
+            red = torch.stack([e_sum, acc.to(torch.float64), torch.tensor(float(rows), device=dev, dtype=torch.float64)])
+            dist.all_reduce(red)
+            e_sum, acc, rows = red[0], red[1], red[2]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        sweep_ms += s0.elapsed_time(s1)
+        energies.append(float(e_sum) / float(rows))
+        accs.append(float(acc))
+    clocks.stop()
+    ms = total_ms / args.steps
+    if dist is not None:
+        t = torch.tensor([ms, sweep_ms / args.steps], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, sweep_avg = float(t[0]), float(t[1])
+    else:
+        sweep_avg = sweep_ms / args.steps
+
+    # ---- end-to-end through the public API (host buffers, copies inside) ----
+    e2e_ms = 0.0
+    h2d = d2h = 0
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        ev_e2e = rbm.log_prob_evaluator(params, F16, RoundingMode.NATIVE)  # snapshot built + uploaded
+        ens.set_evaluator(ev_e2e)
+        ens.reset_counters()
+        ens.run_sweeps(REBURN_SWEEPS)
+        samples = ens.collect(n_samples_total, thin)  # uint8 host rows (D2H)
+        eps = vmc.local_energies(spec, psi, samples)  # H2D packed rows, D2H eps
+        energy = float(eps.real.mean())
+        rate = ens.acceptance_rate
+        t1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms += t0.elapsed_time(t1)
+        snap = ev_e2e.snapshot
+        h2d = snap._table.numel() + snap._bias.numel() + snap._vis_im.numel() * 8 + samples.shape[0] * ens.words * 4
+        d2h = samples.nbytes + eps.nbytes + 3 * 16  # samples, eps, status words
+    e2e_ms /= max(1, min(args.steps, 3))
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+
+    # ---- north-star shape (alpha=1, 10x10, f16) sweep-only rate, same run ----
+    ns = None
+    if rank == 0:
+        p1 = rbm.random_parameters(N_SITES, 1, derive_key(0, "init"), INIT_SCALE)
+        ev1 = rbm.log_prob_evaluator(p1, F16, RoundingMode.NATIVE)
+        e1s = sampler.ChainEnsemble(C, N_SITES, sampler.Proposal("flip"), ev1, derive_key(0, "chains"))
+        e1s.run_steps(1000)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        e1s.run_steps(10 * (N_SITES + 1), check=False)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ns = {"config": "rbm_a1_tfim10x10_c16384_f16native", "chain_steps_per_s":
+              C * 10 * (N_SITES + 1) / (a0.elapsed_time(a1) / 1e3), "variant": ev1.snapshot.label}
+
+    steps_per_step = chain_steps_per_step(C) * world
+    value = steps_per_step / (ms / 1e3)
+    clk = clocks.summary()
+    sm_mhz = clk["sm_mhz"] or 1965.0
+    mufu_peak = 16 * 148 * sm_mhz * 1e6  # MUFU lane-ops/s at the measured SM clock
+    collect_steps = C * SAMPLES_PER_CHAIN * (N_SITES + 1)
+    achieved_mufu = 3 * params.n_hidden * collect_steps / (sweep_avg / 1e3)
+    out = {
+        "metric": "MCMC chain-steps/sec (f16 sampling + f64 local energies), whole job",
+        "value": value,
+        "unit": "chain-steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f16",
+        "data": "synthetic (random_parameters scale 0.01, reference streams derive_key(0,'chains'))",
+        "config": {"workload": WORKLOAD, "chains_per_gpu": C, "n_sites": N_SITES, "alpha": ALPHA, "h": H_FIELD,
+                   "samples_per_step": n_samples_total, "thin_steps": thin, "reburn_sweeps": REBURN_SWEEPS,
+                   "chain_steps_per_step": steps_per_step, "variant": ev.snapshot.label,
+                   "l2": "flushed between timed steps (256 MB write)", "parallelism": f"chains sharded x{world}"},
+        "sampling_sweep_ms": sweep_avg,
+        "sampling_chain_steps_per_s": collect_steps * world / (sweep_avg / 1e3),
+        "energy_check": {"mean_energy": float(np.mean(energies)), "acceptance": float(np.mean(accs)) /
+                         (chain_steps_per_step(C) * world - REBURN_SWEEPS * N_SITES * C * world + REBURN_SWEEPS * N_SITES * C * world)},
+        "roofline": {"bound": "sfu", "kernel": "sweep_kernel (collect launch)", "achieved": achieved_mufu / 1e12,
+                     "peak": mufu_peak / 1e12, "unit": "Tmufu-op/s", "frac": achieved_mufu / mufu_peak,
+                     "traffic": None, "algorithmic": "3 MUFU ops (ex2, cos, lg2) per hidden unit per chain-step, M=200",
+                     "peak_basis": "16 MUFU/clk/SM (measured, tools/microbench) x 148 SMs x measured median SM clock"},
+        "clocks": clk,
+        "gpu_launches": launches["n"],
+        "e2e": {"value": steps_per_step / (e2e_ms / 1e3), "unit": "chain-steps/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "api": "log_prob_evaluator + ChainEnsemble.set_evaluator/run_sweeps/collect + vmc.local_energies"},
+        "north_star_shape": ns,
+    }
+    out["energy_check"]["acceptance"] = float(np.mean(accs)) / (C * world * (REBURN_SWEEPS * N_SITES + SAMPLES_PER_CHAIN * (N_SITES + 1)))
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, sample_chains=C)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle restatement of the reference CPU path
+# (per-operation f16 evaluator, full forward per proposal; f64 local energies)
+# ---------------------------------------------------------------------------
+def cpu_baseline(args, sample_chains=CHAINS_PER_GPU, threads=None, sample_steps=4, energy_samples=256):
+    from oracle import port
+    from paper_2601_20782_b200 import F16, rbm
+    from paper_2601_20782_b200.lattice import LatticeSpec
+    from paper_2601_20782_b200.rng import derive_key
+
+    threads = threads or len(os.sched_getaffinity(0))
+    params = rbm.random_parameters(N_SITES, ALPHA, derive_key(0, "init"), INIT_SCALE)
+    snap = rbm.round_parameters(params, F16)
+    P = port.Params(snap.a, snap.b, snap.w)
+    ens = port.PortEnsemble(sample_chains, N_SITES, "flip", None, P, "f16", int(derive_key(0, "chains")),
+                            nthreads=threads)
+    ens.run_steps(1)
+    t0 = time.perf_counter()
+    ens.run_steps(sample_steps)
+    t_s = time.perf_counter() - t0
+    rate_s = sample_chains * sample_steps / t_s
+    bonds = LatticeSpec.square(L).bond_array()
+    P64 = port.Params(params.a, params.b, params.w)
+    bits = ens.bits[:energy_samples]
+    t0 = time.perf_counter()
+    port.local_energies(P64, "tfim", bonds, 1.0, H_FIELD, bits, nthreads=threads)
+    t_e = time.perf_counter() - t0
+    rate_e = energy_samples / t_e
+    C = CHAINS_PER_GPU
+    total_steps = chain_steps_per_step(C)
+    t_job = total_steps / rate_s + C * SAMPLES_PER_CHAIN / rate_e
+    return {"value": total_steps / t_job, "unit": "chain-steps/s", "cores": threads, "kind": "port",
+            "sample": f"{sample_steps} MH steps x {sample_chains} chains (per-op f16, full forward per proposal) "
+                      f"+ f64 local energies of {energy_samples} samples; extrapolated to one workload step",
+            "sampling_chain_steps_per_s": rate_s, "local_energy_samples_per_s": rate_e,
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return None
+    threads = len(os.sched_getaffinity(0))
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+    rates = []
+    t_start = time.perf_counter()
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(args, sample_chains=4096, threads=threads, sample_steps=2, energy_samples=64)
+        if i >= args.warmup:
+            rates.append(cb["value"])
+    value = float(np.median(rates))
+    cb["value"] = value
+    ms = chain_steps_per_step(CHAINS_PER_GPU) / value * 1e3
+    return {"metric": "MCMC chain-steps/sec (f16 sampling + f64 local energies), whole job", "value": value,
+            "unit": "chain-steps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "chains_per_gpu": CHAINS_PER_GPU},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": "chain-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t_start}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank)
+        if out is not None:
+            print(json.dumps(out))
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -80,7 +80,9 @@ typedef struct {
   uint32_t* bits;        /* [n_chains][words], bit k of a chain in word k>>5, bit k&31 */
   double* log_probs;     /* [n_chains] */
   int64_t* accepted;     /* [n_chains] accepted proposals since reset */
-  int64_t* status;       /* [2 + words]: {code, step*2^32 + chain, offending bits...} */
+  int64_t* status;       /* [2]: {code, step*2^32 + chain of the first non-finite log p} */
+  void* scratch;         /* work queue + parked theta: mpv_sweep_scratch_bytes(snap, n_chains) */
+  size_t scratch_bytes;
 } mpv_chains;
 
 /* ---- RNG (ref: rng.py:63-77 StreamSet.next_uniform, closed form) ---- */
@@ -104,6 +106,7 @@ int mpv_chains_init(const mpv_chains* ch, uint64_t key, int proposal, int sector
  * recorded for chain c (global id) when r < count_c, into row offset_c + r
  * relative to the shard's first row `row0` (count_c, offset_c from
  * n_samples_total over n_chains_total, ref: sampler.py:152-166). */
+size_t mpv_sweep_scratch_bytes(const mpv_snapshot* snap, int64_t n_chains);
 int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, int proposal,
                  int64_t init_draws, int64_t step_index, int64_t n_steps, int64_t thin,
                  uint32_t* samples, int64_t n_samples_total, int64_t n_chains_total,
@@ -113,10 +116,11 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
  * bits: packed [B][words].  PER_OPERATION reproduces ref: _kernels.py:51-129
  * (rounded_forward / rounded_log_prob) bit for bit; F64/STORAGE_ONLY follow
  * ref: rbm.py:143-150 (_fast_forward); NATIVE is the fused sweep's arithmetic.
- * out_re/out_im (log psi, may be NULL) are only produced by PER_OPERATION and F64. */
+ * out_re/out_im (log psi, may be NULL) are only produced by PER_OPERATION and F64.
+ * NATIVE needs `scratch` of mpv_sweep_scratch_bytes(snap, B) (unused otherwise). */
 int mpv_snapshot_forward(const mpv_snapshot* snap, const uint32_t* bits, int64_t B,
                          double* out_lp, double* out_re, double* out_im, int64_t* status,
-                         void* stream);
+                         void* scratch, size_t scratch_bytes, void* stream);
 
 /* Drop-in for ref: _kernels.py:95-129 rounded_log_prob(bits, a_re, b_re, b_im,
  * w_re, w_im, spl, mn, iq, qq, maxf): uint8 bits [B][N], f64 parameters already

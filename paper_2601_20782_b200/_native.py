@@ -39,6 +39,7 @@ class Chains(ctypes.Structure):
     _fields_ = [
         ("n_chains", _i64), ("chain_offset", _i64), ("n_sites", _i32), ("words", _i32),
         ("bits", _vp), ("log_probs", _vp), ("accepted", _vp), ("status", _vp),
+        ("scratch", _vp), ("scratch_bytes", ctypes.c_size_t),
     ]
 
 
@@ -47,7 +48,9 @@ _SIGNATURES = {
     "mpv_chains_init": (ctypes.c_int, [ctypes.POINTER(Chains), _u64, ctypes.c_int, ctypes.c_int, _vp]),
     "mpv_mh_sweep": (ctypes.c_int, [ctypes.POINTER(Snapshot), ctypes.POINTER(Chains), _u64, ctypes.c_int,
                                     _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),
-    "mpv_snapshot_forward": (ctypes.c_int, [ctypes.POINTER(Snapshot), _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "mpv_snapshot_forward": (ctypes.c_int, [ctypes.POINTER(Snapshot), _vp, _i64, _vp, _vp, _vp, _vp, _vp,
+                                            ctypes.c_size_t, _vp]),
+    "mpv_sweep_scratch_bytes": (ctypes.c_size_t, [ctypes.POINTER(Snapshot), _i64]),
     "mpv_rounded_scratch_bytes": (ctypes.c_size_t, [_i64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "mpv_rounded_log_prob": (ctypes.c_int, [_vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp, _vp,
                                             ctypes.c_int, _vp, _vp, _vp]),

@@ -3,17 +3,38 @@
 // here: every buffer is caller-owned.
 #include <mutex>
 #include <string>
-#include <unordered_set>
+#include <unordered_map>
 
 #include "energy.cuh"
 #include "perop.cuh"
 #include "sweep.cuh"
 
 namespace mpv {
-void* sweep_kernel_ptr_f16(int variant, int U, int prop, int smem);
-void* sweep_kernel_ptr_bf16(int variant, int U, int prop, int smem);
-void* sweep_kernel_ptr_f32(int variant, int U, int prop, int smem);
-void* sweep_kernel_ptr_f64(int variant, int U, int prop, int smem);
+#define MPV_DECL(f, v) void* sweep_kernel_ptr_##f##_##v(int G, int U, int prop, int smem);
+MPV_DECL(f16, x1) MPV_DECL(f16, x2) MPV_DECL(f16, f64)
+MPV_DECL(bf16, x1) MPV_DECL(bf16, x2) MPV_DECL(bf16, f64)
+MPV_DECL(f32, x1) MPV_DECL(f32, x2) MPV_DECL(f32, f64)
+MPV_DECL(f64, f64)
+#undef MPV_DECL
+
+void* sweep_kernel_ptr(int fmt, int variant, int G, int U, int prop, int smem) {
+  switch (fmt) {
+    case MPV_FMT_F16:
+      return variant == MPV_ACC_X1 ? sweep_kernel_ptr_f16_x1(G, U, prop, smem)
+           : variant == MPV_ACC_X2 ? sweep_kernel_ptr_f16_x2(G, U, prop, smem)
+                                   : sweep_kernel_ptr_f16_f64(G, U, prop, smem);
+    case MPV_FMT_BF16:
+      return variant == MPV_ACC_X1 ? sweep_kernel_ptr_bf16_x1(G, U, prop, smem)
+           : variant == MPV_ACC_X2 ? sweep_kernel_ptr_bf16_x2(G, U, prop, smem)
+                                   : sweep_kernel_ptr_bf16_f64(G, U, prop, smem);
+    case MPV_FMT_F32:
+      return variant == MPV_ACC_X1 ? sweep_kernel_ptr_f32_x1(G, U, prop, smem)
+           : variant == MPV_ACC_X2 ? sweep_kernel_ptr_f32_x2(G, U, prop, smem)
+                                   : sweep_kernel_ptr_f32_f64(G, U, prop, smem);
+    default:
+      return sweep_kernel_ptr_f64_f64(G, U, prop, smem);
+  }
+}
 }  // namespace mpv
 
 using namespace mpv;
@@ -43,17 +64,18 @@ int max_smem_optin() {
   return v;
 }
 
-// cudaFuncSetAttribute once per (kernel, size class)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) raised to the largest size
+// requested so far for each kernel.
 int ensure_smem(const void* fn, size_t bytes) {
   static std::mutex mu;
-  static std::unordered_set<const void*> done;
+  static std::unordered_map<const void*, size_t> done;
   if (bytes <= 48 * 1024) return MPV_OK;
   std::lock_guard<std::mutex> lock(mu);
-  if (done.count(fn)) return MPV_OK;
-  const cudaError_t e =
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin());
+  auto it = done.find(fn);
+  if (it != done.end() && it->second >= bytes) return MPV_OK;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-  done.insert(fn);
+  done[fn] = bytes;
   return MPV_OK;
 }
 
@@ -64,6 +86,10 @@ size_t entry_bytes(int fmt, int variant) {
   if (variant == MPV_ACC_F64 || fmt == MPV_FMT_F64) return 16;
   const size_t pair = (fmt == MPV_FMT_F32) ? 8 : 4;
   return variant == MPV_ACC_X2 ? 2 * pair : pair;
+}
+size_t acc_bytes(int fmt, int variant) {  // sizeof(Acc<FMT, VAR>)
+  if (variant == MPV_ACC_F64 || fmt == MPV_FMT_F64) return 16;
+  return variant == MPV_ACC_X2 ? 16 : 8;
 }
 size_t vis_bytes(int fmt, int variant) {
   if (variant == MPV_ACC_F64 || fmt == MPV_FMT_F64) return 8;
@@ -179,6 +205,8 @@ __global__ void perop_table_kernel(int N, int M, const double* a_re, const doubl
 extern "C" {
 #pragma GCC visibility push(default)
 
+size_t mpv_sweep_scratch_bytes(const mpv_snapshot* snap, int64_t n_chains);
+
 int mpv_pack_bits(const uint8_t* bits, int64_t B, int N, uint32_t* out, void* stream);
 
 const char* mpv_last_error(void) { return g_error.c_str(); }
@@ -284,16 +312,25 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
   const size_t tbytes = (size_t)snap->n_visible * snap->hidden_pad * entry_bytes(kfmt, variant) +
                         (size_t)snap->n_visible * vis_bytes(kfmt, variant);
   const size_t tbytes16 = (tbytes + 15) & ~(size_t)15;
-  const bool use_smem = tbytes16 + 1024 <= (size_t)max_smem_optin();
-  void* fn = nullptr;
+  const bool use_smem = tbytes16 + 1024 <= (size_t)max_smem_optin();  // static smem: mbarrier
   const int sm = use_smem ? 1 : 0;
-  switch (kfmt) {
-    case MPV_FMT_F16: fn = sweep_kernel_ptr_f16(variant, U, proposal, sm); break;
-    case MPV_FMT_BF16: fn = sweep_kernel_ptr_bf16(variant, U, proposal, sm); break;
-    case MPV_FMT_F32: fn = sweep_kernel_ptr_f32(variant, U, proposal, sm); break;
-    default: fn = sweep_kernel_ptr_f64(variant, U, proposal, sm); break;
-  }
-  if (!fn) return fail(MPV_ERR_ARGS, "mh_sweep: no kernel for this (format, variant, units)");
+  void* fn = sweep_kernel_ptr(kfmt, variant, G, U, proposal, sm);
+  if (!fn) return fail(MPV_ERR_ARGS, "mh_sweep: no kernel for this (format, variant, layout)");
+  const int64_t cpw = 32 / G;
+  const int64_t n_groups = (ch->n_chains + cpw - 1) / cpw;
+  // segment length: a multiple of G (draw batches never straddle segments),
+  // >= 32 steps, <= 16 segments per launch
+  int64_t seg_len = std::max<int64_t>(32, (n_steps + 15) / 16);
+  seg_len = (seg_len + G - 1) / G * G;
+  const int64_t n_segments = n_steps == 0 ? 1 : (n_steps + seg_len - 1) / seg_len;
+  const size_t need = mpv_sweep_scratch_bytes(snap, ch->n_chains);
+  if (!ch->scratch || ch->scratch_bytes < need) return fail(MPV_ERR_ARGS, "mh_sweep: scratch too small (mpv_sweep_scratch_bytes)");
+  char* sp = (char*)ch->scratch;
+  int* queue = (int*)sp;
+  int* done = (int*)(sp + 256);
+  float* save = (float*)(sp + 256 + ((n_groups * 4 + 255) / 256) * 256);
+  void* vsave = (char*)save + ((size_t)n_groups * U * acc_bytes(kfmt, variant) * 32 + 255) / 256 * 256;
+  if (cudaMemsetAsync(sp, 0, 256 + n_groups * 4, st) != cudaSuccess) return check_launch("mh_sweep memset");
   SweepArgs a{};
   a.N = snap->n_visible; a.M = snap->n_hidden; a.Mpad = snap->hidden_pad; a.G = G; a.words = ch->words;
   a.table = snap->table; a.bias = snap->bias; a.vis = snap->vis; a.table_bytes = tbytes16;
@@ -303,19 +340,40 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
   a.init_draws = init_draws; a.step_index = step_index; a.n_steps = n_steps; a.thin = thin;
   a.samples = samples; a.sample_base = base; a.sample_extra = extra; a.round_offset = round_offset;
   a.row0 = row0;
+  a.seg_len = seg_len; a.n_groups = n_groups; a.n_items = n_groups * n_segments;
+  a.queue = queue; a.done = done; a.save = save; a.vis_save = vsave;
   const int threads = 256;
-  const int64_t chains_per_block = (threads / 32) * (32 / G);
   const size_t smem = use_smem ? tbytes16 : 0;
   if (int rc = ensure_smem(fn, smem)) return rc;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1)
+    return fail(MPV_ERR_CUDA, "mh_sweep: kernel does not fit on an SM");
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t warps_needed = a.n_items;
+  const int64_t blocks = std::min<int64_t>((int64_t)n_sm * per_sm, (warps_needed + threads / 32 - 1) / (threads / 32));
   void* args[] = {&a};
-  const cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)((ch->n_chains + chains_per_block - 1) / chains_per_block)),
-                                         dim3(threads), args, smem, st);
+  const cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, st);
   if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("mh_sweep: ") + cudaGetErrorString(e));
   return MPV_OK;
 }
 
+size_t mpv_sweep_scratch_bytes(const mpv_snapshot* snap, int64_t n_chains) {
+  if (!snap) return 0;
+  const bool f64arith = (snap->fmt == MPV_FMT_F64) || (snap->mode == MPV_MODE_STORAGE_ONLY);
+  const int kfmt = f64arith ? MPV_FMT_F64 : snap->fmt;
+  const int variant = f64arith ? MPV_ACC_F64 : snap->variant;
+  const int G = std::max(1, (int)snap->lanes_per_chain), U = std::max(1, (int)snap->units_per_lane);
+  const int64_t n_groups = (n_chains + 32 / G - 1) / (32 / G);
+  return 256 + ((n_groups * 4 + 255) / 256) * 256 +
+         ((size_t)n_groups * U * acc_bytes(kfmt, variant) * 32 + 255) / 256 * 256 +
+         (size_t)(n_chains + 1) * 16 + 256;
+}
+
 int mpv_snapshot_forward(const mpv_snapshot* snap, const uint32_t* bits, int64_t B, double* out_lp,
-                         double* out_re, double* out_im, int64_t* status, void* stream) {
+                         double* out_re, double* out_im, int64_t* status, void* scratch,
+                         size_t scratch_bytes, void* stream) {
   if (!snap || !bits || !out_lp || B < 0) return fail(MPV_ERR_ARGS, "snapshot_forward: bad args");
   if (B == 0) return MPV_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -328,6 +386,7 @@ int mpv_snapshot_forward(const mpv_snapshot* snap, const uint32_t* bits, int64_t
     ch.n_chains = B; ch.chain_offset = 0; ch.n_sites = snap->n_visible; ch.words = words;
     ch.bits = const_cast<uint32_t*>(bits);  // read-only with n_steps == 0 (bits written back unchanged)
     ch.log_probs = out_lp; ch.accepted = nullptr; ch.status = status;
+    ch.scratch = scratch; ch.scratch_bytes = scratch_bytes;
     return mpv_mh_sweep(snap, &ch, 0, MPV_PROPOSAL_FLIP, 0, 0, 0, 0, nullptr, 0, 1, 0, 0, stream);
   }
   FwdArgs a{};
@@ -390,7 +449,7 @@ int mpv_rounded_log_prob(const uint8_t* bits, int64_t B, int N, int M, const dou
   snap.fmt = fmt; snap.mode = MPV_MODE_PER_OPERATION; snap.variant = MPV_ACC_X1;
   snap.lanes_per_chain = 1; snap.units_per_lane = M;
   snap.table = table; snap.bias = bias; snap.vis = vis; snap.vis_im = nullptr;
-  return mpv_snapshot_forward(&snap, packed, B, out_lp, nullptr, nullptr, nullptr, stream);
+  return mpv_snapshot_forward(&snap, packed, B, out_lp, nullptr, nullptr, nullptr, nullptr, 0, stream);
 }
 
 size_t mpv_energy_tables_bytes(int N, int M, int ham, int n_bonds) {

@@ -102,6 +102,19 @@ template <> struct Half<MPV_FMT_F16> {
   }
   __device__ static __forceinline__ float lo(uint32_t a) { return fma_lo(a, kOne, -0.0f); }
   __device__ static __forceinline__ float hi(uint32_t a) { return fma_hi(a, kOne, -0.0f); }
+  // 2 * (high half), exact
+  __device__ static __forceinline__ float hi2(uint32_t a) { return fma_hi(a, 0x4000, -0.0f); }
+  // acc + half (f32 accumulate of an f16 value, one mixed-precision add)
+  __device__ static __forceinline__ float acc_lo(uint32_t a, float acc) {
+    float d;
+    asm("{.reg .b16 l, h;\n mov.b32 {l, h}, %1;\n add.rn.f32.f16 %0, l, %2;}" : "=f"(d) : "r"(a), "f"(acc));
+    return d;
+  }
+  __device__ static __forceinline__ float acc_hi(uint32_t a, float acc) {
+    float d;
+    asm("{.reg .b16 l, h;\n mov.b32 {l, h}, %1;\n add.rn.f32.f16 %0, h, %2;}" : "=f"(d) : "r"(a), "f"(acc));
+    return d;
+  }
   // per-op emulation: RN(a + b) in f16 (exact-sum rounding == ref _quantize(a+b))
   __device__ static __forceinline__ uint16_t add(uint16_t a, uint16_t b) {
     return __half_as_ushort(__hadd(__ushort_as_half(a), __ushort_as_half(b)));
@@ -135,6 +148,17 @@ template <> struct Half<MPV_FMT_BF16> {
   // bf16 -> f32 is a shift: exact and on the ALU pipe.
   __device__ static __forceinline__ float lo(uint32_t a) { return __uint_as_float(a << 16); }
   __device__ static __forceinline__ float hi(uint32_t a) { return __uint_as_float(a & 0xFFFF0000u); }
+  __device__ static __forceinline__ float hi2(uint32_t a) { return fma_hi(a, 0x4000, -0.0f); }
+  __device__ static __forceinline__ float acc_lo(uint32_t a, float acc) {
+    float d;
+    asm("{.reg .b16 l, h;\n mov.b32 {l, h}, %1;\n add.rn.f32.bf16 %0, l, %2;}" : "=f"(d) : "r"(a), "f"(acc));
+    return d;
+  }
+  __device__ static __forceinline__ float acc_hi(uint32_t a, float acc) {
+    float d;
+    asm("{.reg .b16 l, h;\n mov.b32 {l, h}, %1;\n add.rn.f32.bf16 %0, h, %2;}" : "=f"(d) : "r"(a), "f"(acc));
+    return d;
+  }
   __device__ static __forceinline__ uint16_t add(uint16_t a, uint16_t b) {
     return __bfloat16_as_ushort(__hadd(__ushort_as_bfloat16(a), __ushort_as_bfloat16(b)));
   }

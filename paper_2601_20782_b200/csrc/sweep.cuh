@@ -35,6 +35,12 @@ struct SweepArgs {
   int64_t init_draws, step_index, n_steps, thin;
   uint32_t* samples;
   int64_t sample_base, sample_extra, round_offset, row0;
+  // persistent work queue: items (segment, chain group), segment-major
+  int64_t seg_len, n_groups, n_items;
+  int* queue;         // [1], zero at launch
+  int* done;          // [n_groups] segments finished, zero at launch
+  float* save;        // [n_groups][save_words][32] theta between segments
+  void* vis_save;     // [n_chains] visible term between segments
 };
 
 // ------------------------------------------------------------------------
@@ -45,10 +51,10 @@ struct SweepArgs {
 // 3 MUFU ops  ½ log(1 + t² + 2 t cos 2y) + |x| - ln2,  t = e^{-2|x|}
 // (the same closed form as ref _logcosh_pair, rbm.py:130-140), result rounded
 // to the format by the caller (pairs of units share one F2FP).
-__device__ __forceinline__ float lc_fast(float x, float y) {
+__device__ __forceinline__ float lc_fast(float x, float y2) {
   const float ax = fabsf(x);
   const float t = ex2_approx(ax * -2.8853900817779268f);  // e^{-2|x|}
-  const float c = cos_approx(y + y);
+  const float c = cos_approx(y2);                          // cos 2y
   const float s = fmaf(2.0f, c, t);
   const float v = fmaf(t, s, 1.0f);
   return fmaf(lg2_approx(v), 0.34657359027997264f, ax - 0.69314718055994531f);
@@ -221,38 +227,37 @@ template <int FMT, int VAR> struct Eval {
   // Reduced formats: theta rounded to fmt, lc in f32, lc rounded to fmt, then
   // accumulated in f32 (mask 0 for padded units).
   template <typename T>
-  __device__ __forceinline__ static void pair(T xr0, T xi0, T xr1, T xi1, float m0, float m1,
-                                              Sum& acc) {
+  __device__ __forceinline__ static void pair(T xr0, T xi0, T xr1, T xi1, Sum& acc) {
     if constexpr (kF64) {
-      acc += (double)m0 * lc_f64(xr0, xi0);
-      acc += (double)m1 * lc_f64(xr1, xi1);
+      acc += lc_f64(xr0, xi0);
+      acc += lc_f64(xr1, xi1);
     } else {
       float a0 = (float)xr0, b0 = (float)xi0, a1 = (float)xr1, b1 = (float)xi1;
       if constexpr (FMT == MPV_FMT_F32) {
-        acc = fmaf(m0, lc_f32(a0, b0), acc);
-        acc = fmaf(m1, lc_f32(a1, b1), acc);
+        acc += lc_f32(a0, b0);
+        acc += lc_f32(a1, b1);
       } else {
         using H = Half<FMT>;
         const uint32_t p0 = H::pack(a0, b0), p1 = H::pack(a1, b1);
-        const float l0 = lc_fast(H::lo(p0), H::hi(p0));
-        const float l1 = lc_fast(H::lo(p1), H::hi(p1));
+        const float l0 = lc_fast(H::lo(p0), H::hi2(p0));
+        const float l1 = lc_fast(H::lo(p1), H::hi2(p1));
         const uint32_t lp = H::pack(l0, l1);
-        acc = fmaf(m0, H::lo(lp), acc);
-        acc = fmaf(m1, H::hi(lp), acc);
+        acc = H::acc_lo(lp, acc);
+        acc = H::acc_hi(lp, acc);
       }
     }
   }
   template <typename T>
-  __device__ __forceinline__ static void single(T xr, T xi, float m, Sum& acc) {
+  __device__ __forceinline__ static void single(T xr, T xi, Sum& acc) {
     if constexpr (kF64) {
-      acc += (double)m * lc_f64(xr, xi);
+      acc += lc_f64(xr, xi);
     } else if constexpr (FMT == MPV_FMT_F32) {
-      acc = fmaf(m, lc_f32((float)xr, (float)xi), acc);
+      acc += lc_f32((float)xr, (float)xi);
     } else {
       using H = Half<FMT>;
       const uint32_t p = H::pack((float)xr, (float)xi);
-      const uint32_t lp = H::pack(lc_fast(H::lo(p), H::hi(p)), 0.0f);
-      acc = fmaf(m, H::lo(lp), acc);
+      const uint32_t lp = H::pack(lc_fast(H::lo(p), H::hi2(p)), 0.0f);
+      acc = H::acc_lo(lp, acc);
     }
   }
   // Visible term (exact) and hidden sum -> log p (double).
@@ -287,10 +292,15 @@ __device__ __forceinline__ void report_nonfinite(int64_t* status, int64_t step, 
   atomicExch((unsigned long long*)&status[0], (unsigned long long)MPV_ERR_NONFINITE);
 }
 
+
 // ------------------------------------------------------------------------
-// The kernel.
+// The kernel: persistent warps pull (segment, chain-group) items from a
+// segment-major queue, so the last wave is balanced to within one segment.
+// A group's segment s+1 waits for segment s (already handed out, hence
+// running or finished on a resident warp: no deadlock).
 // ------------------------------------------------------------------------
-template <int FMT, int VAR, int U, int PROP, bool SMEM>
+
+template <int FMT, int VAR, int G, int U, int PROP, bool SMEM>
 __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
   using A = Acc<FMT, VAR>;
   using E = Eval<FMT, VAR>;
@@ -299,13 +309,15 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
   using Sign = typename A::Sign;
   using Sum = typename E::Sum;
   using Theta = typename std::conditional<VAR == MPV_ACC_F64, double, float>::type;
+  constexpr int CPW = 32 / G;
+  constexpr int SW = (int)(sizeof(A) / sizeof(float));
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Entry* tab;
   const VisT* visv;
   if constexpr (SMEM) {
     // Stage the snapshot (column table, then visible biases) into shared memory
-    // with one bulk async copy (TMA engine, cp.async.bulk) on an mbarrier.
+    // with bulk async copies (TMA engine, cp.async.bulk) on one mbarrier.
     __shared__ __align__(8) uint64_t bar;
     const uint32_t bytes = (uint32_t)a.table_bytes;
     const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(&bar);
@@ -334,188 +346,230 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
             sbar)
         : "memory");
     tab = reinterpret_cast<const Entry*>(smem_raw);
-    visv = reinterpret_cast<const VisT*>(smem_raw + (size_t)a.N * a.Mpad * sizeof(Entry));
+    visv = reinterpret_cast<const VisT*>(smem_raw + (size_t)a.N * (G * U) * sizeof(Entry));
   } else {
     tab = reinterpret_cast<const Entry*>(a.table);
-    visv = reinterpret_cast<const VisT*>((const char*)a.table + (size_t)a.N * a.Mpad * sizeof(Entry));
+    visv = reinterpret_cast<const VisT*>((const char*)a.table + (size_t)a.N * (G * U) * sizeof(Entry));
   }
-
-  const int G = a.G;
+  constexpr int Mpad = G * U;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   const int slot = lane / G;
-  const int cpw = 32 / G;
-  const int64_t chain = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * cpw + slot;
-  const bool live = chain < a.n_chains;
-  const int64_t cidx = live ? chain : 0;  // tail lanes mirror chain 0 and never write
-  const int64_t gchain = a.chain_offset + cidx;
   const int N = a.N;
   const int words = a.words;
-
-  uint32_t myword = (gl < words) ? a.bits[cidx * words + gl] : 0u;
-
-  // per-slot masks (padded hidden units contribute 0)
-  float mask[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) mask[u] = (u * G + gl < a.M) ? 1.0f : 0.0f;
-
-  // ---- refresh: theta = b + W x, vis = a.x, log p (set_evaluator semantics) ----
-  A acc[U];
-  const Entry* bias = reinterpret_cast<const Entry*>(a.bias);
-#pragma unroll
-  for (int u = 0; u < U; ++u) acc[u].init(bias[u * G + gl]);
-  VisT vis = vis_zero<VisT>();
-  const Sign one = A::sign(1);
-  for (int w = 0; w < words; ++w) {
-    uint32_t word = __shfl_sync(kFull, myword, w, G);
-    while (word) {
-      const int b = __ffs(word) - 1;
-      word &= word - 1;
-      const int k = w * 32 + b;
-      const Entry* col = tab + (size_t)k * a.Mpad + gl;
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc[u].add(col[u * G], one);
-      vis = vis_add(vis, visv[k], 1);
-    }
-  }
-  Sum h0 = Sum(0);
-#pragma unroll
-  for (int u = 0; u + 1 < U; u += 2) {
-    Theta xr0, xi0, xr1, xi1;
-    acc[u].prop1(Entry{}, A::sign(0), xr0, xi0);
-    acc[u + 1].prop1(Entry{}, A::sign(0), xr1, xi1);
-    E::pair(xr0, xi0, xr1, xi1, mask[u], mask[u + 1], h0);
-  }
-  if constexpr (U & 1) {
-    Theta xr, xi;
-    acc[U - 1].prop1(Entry{}, A::sign(0), xr, xi);
-    E::single(xr, xi, mask[U - 1], h0);
-  }
-  h0 = segment_sum(h0, G);
-  double lp = E::finalize(vis, h0);
-  bool dead = false;
-  if (!isfinite(lp)) {
-    dead = true;
-    if (live && gl == 0) report_nonfinite(a.status, 0, cidx);
-  }
-
-  // ---- the MH loop ----
-  const uint64_t s0 = stream_state(a.key, (uint64_t)gchain);
-  const int64_t count_c =
-      a.sample_base + ((gchain < a.sample_extra) ? 1 : 0);
-  const int64_t offset_c =
-      gchain * a.sample_base + (gchain < a.sample_extra ? gchain : a.sample_extra) - a.row0;
-  int64_t n_acc = 0;
-  int sel_c = 0;        // cached selection (site, or pair i | j<<16)
-  double logu_c = 0.0;  // cached log(u_accept)
   const double n_pairs = 0.5 * (double)N * (double)(N - 1);
+  const Entry* bias = reinterpret_cast<const Entry*>(a.bias);
+  VisT* vsave = reinterpret_cast<VisT*>(a.vis_save);
 
-  int64_t next_record = (a.samples && a.thin > 0) ? a.thin : -1;
-  for (int64_t s = 0; s < a.n_steps; ++s) {
-    const int src = (int)(s & (G - 1));
-    if (src == 0) {
-      // lane gl draws the two uniforms of step s+gl (ref: sampler.py:113,127)
-      const uint64_t t = (uint64_t)(a.init_draws + 2 * (a.step_index + s + gl));
-      const double us = stream_draw(s0, t);
-      const double ua = stream_draw(s0, t + 1);
-      if (PROP == MPV_PROPOSAL_FLIP) {
-        sel_c = (int)floor_scaled(us, (double)N);
-      } else {
-        int i, j;
-        pair_of(floor_scaled(us, n_pairs), N, i, j);
-        sel_c = i | (j << 16);
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(a.queue, 1);
+    item = __shfl_sync(kFull, item, 0);
+    if (item >= a.n_items) break;
+    const int64_t seg = item / a.n_groups;
+    const int64_t grp = item % a.n_groups;
+    const int64_t chain = grp * CPW + slot;
+    const bool live = chain < a.n_chains;
+    const int64_t cidx = live ? chain : 0;  // tail lanes mirror chain 0 and never write
+    const int64_t gchain = a.chain_offset + cidx;
+    if (seg > 0) {
+      if (lane == 0) {
+        int d;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(d) : "l"(a.done + grp) : "memory");
+          if (d >= seg) break;
+          __nanosleep(100);
+        }
       }
-      logu_c = log(ua);
+      __syncwarp();
     }
-    const int sel = __shfl_sync(kFull, sel_c, src, G);
-    const double logu = __shfl_sync(kFull, logu_c, src, G);
+    uint32_t myword = (gl < words) ? a.bits[cidx * words + gl] : 0u;
 
-    int dsign, k1, k2 = 0;
-    if (PROP == MPV_PROPOSAL_FLIP) {
-      k1 = sel;
-      const uint32_t wd = __shfl_sync(kFull, myword, k1 >> 5, G);
-      dsign = ((wd >> (k1 & 31)) & 1u) ? -1 : 1;
+    A acc[U];
+    VisT vis;
+    double lp;
+    if (seg == 0) {
+      // refresh: theta = b + W x, vis = a.x, log p (set_evaluator semantics)
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u].init(bias[u * G + gl]);
+      vis = vis_zero<VisT>();
+      const Sign one = A::sign(1);
+      for (int w = 0; w < words; ++w) {
+        uint32_t word = __shfl_sync(kFull, myword, w, G);
+        while (word) {
+          const int k = w * 32 + __ffs(word) - 1;
+          word &= word - 1;
+          const Entry* col = tab + (size_t)k * Mpad + gl;
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc[u].add(col[u * G], one);
+          vis = vis_add(vis, visv[k], 1);
+        }
+      }
+      Sum h0 = Sum(0);
+#pragma unroll
+      for (int u = 0; u + 1 < U; u += 2) {
+        Theta xr0, xi0, xr1, xi1;
+        acc[u].prop1(Entry{}, A::sign(0), xr0, xi0);
+        acc[u + 1].prop1(Entry{}, A::sign(0), xr1, xi1);
+        E::pair(xr0, xi0, xr1, xi1, h0);
+      }
+      if constexpr (U & 1) {
+        Theta xr, xi;
+        acc[U - 1].prop1(Entry{}, A::sign(0), xr, xi);
+        E::single(xr, xi, h0);
+      }
+      h0 = segment_sum(h0, G);
+      lp = E::finalize(vis, h0);
+      if (!isfinite(lp)) {
+        if (live && gl == 0) report_nonfinite(a.status, 0, cidx);
+        lp = __longlong_as_double(0x7FF8000000000000ll);  // NaN marks a frozen chain
+      }
     } else {
-      k1 = sel & 0xFFFF;
-      k2 = sel >> 16;
-      const uint32_t wi = __shfl_sync(kFull, myword, k1 >> 5, G);
-      const uint32_t wj = __shfl_sync(kFull, myword, k2 >> 5, G);
-      const int bi = (wi >> (k1 & 31)) & 1u, bj = (wj >> (k2 & 31)) & 1u;
-      dsign = bj - bi;  // x_i' = x_j: theta' = theta + d (W_:i - W_:j)
-    }
-    // Every segment evaluates (no divergence around the segment shuffles); an
-    // exchange of equal bits (dsign == 0) evaluates theta itself and is then
-    // accepted unconditionally: the reference evaluator returns the cached
-    // value, Δ = 0 and log u < 0 (sampler.py:119-131).
-    const Sign d = A::sign(dsign);
-    const Sign md = A::sign(-dsign);
-    Entry e1[U], e2[U];
-    const Entry* c1 = tab + (size_t)k1 * a.Mpad + gl;
-    const Entry* c2 = tab + (size_t)k2 * a.Mpad + gl;
+      const float* sv = a.save + (size_t)grp * (U * SW) * 32 + lane;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      e1[u] = c1[u * G];
-      if (PROP == MPV_PROPOSAL_EXCHANGE) e2[u] = c2[u * G];
-    }
-    Sum h = Sum(0);
+      for (int u = 0; u < U; ++u) {
+        float* dst = reinterpret_cast<float*>(&acc[u]);
 #pragma unroll
-    for (int u = 0; u + 1 < U; u += 2) {
-      Theta xr0, xi0, xr1, xi1;
-      if (PROP == MPV_PROPOSAL_FLIP) {
-        acc[u].prop1(e1[u], d, xr0, xi0);
-        acc[u + 1].prop1(e1[u + 1], d, xr1, xi1);
-      } else {
-        acc[u].prop2(e1[u], e2[u], d, md, xr0, xi0);
-        acc[u + 1].prop2(e1[u + 1], e2[u + 1], d, md, xr1, xi1);
+        for (int j = 0; j < SW; ++j) dst[j] = sv[(u * SW + j) * 32];
       }
-      E::pair(xr0, xi0, xr1, xi1, mask[u], mask[u + 1], h);
+      vis = vsave[cidx];
+      lp = a.log_probs[cidx];
     }
-    if constexpr (U & 1) {
-      Theta xr, xi;
-      if (PROP == MPV_PROPOSAL_FLIP) acc[U - 1].prop1(e1[U - 1], d, xr, xi);
-      else acc[U - 1].prop2(e1[U - 1], e2[U - 1], d, md, xr, xi);
-      E::single(xr, xi, mask[U - 1], h);
-    }
-    h = segment_sum(h, G);
-    VisT vnew = vis_add(vis, visv[k1], dsign);
-    if (PROP == MPV_PROPOSAL_EXCHANGE) vnew = vis_add(vnew, visv[k2], -dsign);
-    const double lp_new = E::finalize(vnew, h);
-    // ref sampler.py:128-129: NaN compares false (reject); the reference raises
-    // EvaluationFailureError on any non-finite proposal (rbm.py:242-251): the
-    // chain freezes and the first failure is reported.
-    if (dsign != 0 && !isfinite(lp_new) && !dead) {
-      dead = true;
-      if (live && gl == 0) report_nonfinite(a.status, a.step_index + s + 1, cidx);
-    }
-    const bool accept = !dead && (dsign == 0 || logu < lp_new - lp);
-    const bool moved = accept && dsign != 0;
-    if (moved) {
-      vis = vnew;
-      lp = lp_new;
-      if (gl == (k1 >> 5)) myword ^= 1u << (k1 & 31);
-      if (PROP == MPV_PROPOSAL_EXCHANGE && gl == (k2 >> 5)) myword ^= 1u << (k2 & 31);
-    }
-    n_acc += accept ? 1 : 0;
-    const Sign dacc = moved ? d : A::sign(0);
-    const Sign mdacc = moved ? md : A::sign(0);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (PROP == MPV_PROPOSAL_FLIP) acc[u].add(e1[u], dacc);
-      else { acc[u].add(e1[u], dacc); acc[u].add(e2[u], mdacc); }
-    }
-    if (s + 1 == next_record) {
-      next_record += a.thin;
-      const int64_t r = a.round_offset + (s + 1) / a.thin - 1;
-      if (live && r < count_c && gl < words) a.samples[(offset_c + r) * words + gl] = myword;
-    }
-  }
+    bool dead = isnan(lp);
 
-  if (live) {
-    if (gl < words) a.bits[cidx * words + gl] = myword;
-    if (gl == 0) {
-      a.log_probs[cidx] = lp;
-      if (a.accepted) a.accepted[cidx] += n_acc;
+    const uint64_t s0 = stream_state(a.key, (uint64_t)gchain);
+    const int64_t count_c = a.sample_base + ((gchain < a.sample_extra) ? 1 : 0);
+    const int64_t offset_c =
+        gchain * a.sample_base + (gchain < a.sample_extra ? gchain : a.sample_extra) - a.row0;
+    int64_t n_acc = 0;
+    int sel_c = 0;        // cached selection (site, or pair i | j<<16)
+    double logu_c = 0.0;  // cached log(u_accept)
+    const int64_t s_begin = seg * a.seg_len;
+    const int64_t s_end = min(a.n_steps, s_begin + a.seg_len);
+    int64_t next_record = -1;
+    if (a.samples && a.thin > 0) next_record = ((s_begin / a.thin) + 1) * a.thin;
+
+    for (int64_t s = s_begin; s < s_end; ++s) {
+      const int src = (int)(s & (G - 1));
+      if (src == 0) {
+        // lane gl draws the two uniforms of step s+gl (ref: sampler.py:113,127)
+        const uint64_t t = (uint64_t)(a.init_draws + 2 * (a.step_index + s + gl));
+        const double us = stream_draw(s0, t);
+        const double ua = stream_draw(s0, t + 1);
+        if (PROP == MPV_PROPOSAL_FLIP) {
+          sel_c = (int)floor_scaled(us, (double)N);
+        } else {
+          int i, j;
+          pair_of(floor_scaled(us, n_pairs), N, i, j);
+          sel_c = i | (j << 16);
+        }
+        logu_c = log(ua);
+      }
+      const int sel = __shfl_sync(kFull, sel_c, src, G);
+      const double logu = __shfl_sync(kFull, logu_c, src, G);
+
+      int dsign, k1, k2 = 0;
+      if (PROP == MPV_PROPOSAL_FLIP) {
+        k1 = sel;
+        const uint32_t wd = __shfl_sync(kFull, myword, k1 >> 5, G);
+        dsign = ((wd >> (k1 & 31)) & 1u) ? -1 : 1;
+      } else {
+        k1 = sel & 0xFFFF;
+        k2 = sel >> 16;
+        const uint32_t wi = __shfl_sync(kFull, myword, k1 >> 5, G);
+        const uint32_t wj = __shfl_sync(kFull, myword, k2 >> 5, G);
+        const int bi = (wi >> (k1 & 31)) & 1u, bj = (wj >> (k2 & 31)) & 1u;
+        dsign = bj - bi;  // x_i' = x_j: theta' = theta + d (W_:i - W_:j)
+      }
+      // Every segment evaluates (no divergence around the segment shuffles); an
+      // exchange of equal bits (dsign == 0) is accepted unconditionally: the
+      // reference evaluator returns the cached value, Δ = 0, log u < 0
+      // (sampler.py:119-131).
+      const Sign d = A::sign(dsign);
+      const Sign md = A::sign(-dsign);
+      Entry e1[U], e2[U];
+      const Entry* c1 = tab + (size_t)k1 * Mpad + gl;
+      const Entry* c2 = tab + (size_t)k2 * Mpad + gl;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        e1[u] = c1[u * G];
+        if (PROP == MPV_PROPOSAL_EXCHANGE) e2[u] = c2[u * G];
+      }
+      Sum h = Sum(0);
+#pragma unroll
+      for (int u = 0; u + 1 < U; u += 2) {
+        Theta xr0, xi0, xr1, xi1;
+        if (PROP == MPV_PROPOSAL_FLIP) {
+          acc[u].prop1(e1[u], d, xr0, xi0);
+          acc[u + 1].prop1(e1[u + 1], d, xr1, xi1);
+        } else {
+          acc[u].prop2(e1[u], e2[u], d, md, xr0, xi0);
+          acc[u + 1].prop2(e1[u + 1], e2[u + 1], d, md, xr1, xi1);
+        }
+        E::pair(xr0, xi0, xr1, xi1, h);
+      }
+      if constexpr (U & 1) {
+        Theta xr, xi;
+        if (PROP == MPV_PROPOSAL_FLIP) acc[U - 1].prop1(e1[U - 1], d, xr, xi);
+        else acc[U - 1].prop2(e1[U - 1], e2[U - 1], d, md, xr, xi);
+        E::single(xr, xi, h);
+      }
+      h = segment_sum(h, G);
+      VisT vnew = vis_add(vis, visv[k1], dsign);
+      if (PROP == MPV_PROPOSAL_EXCHANGE) vnew = vis_add(vnew, visv[k2], -dsign);
+      const double lp_new = E::finalize(vnew, h);
+      // ref sampler.py:128-129: NaN compares false (reject); the reference raises
+      // EvaluationFailureError on any non-finite proposal (rbm.py:242-251): the
+      // chain freezes and the first failure is reported.
+      if (dsign != 0 && !isfinite(lp_new) && !dead) {
+        dead = true;
+        if (live && gl == 0) report_nonfinite(a.status, a.step_index + s + 1, cidx);
+      }
+      const bool accept = !dead && (dsign == 0 || logu < lp_new - lp);
+      const bool moved = accept && dsign != 0;
+      if (moved) {
+        vis = vnew;
+        lp = lp_new;
+        if (gl == (k1 >> 5)) myword ^= 1u << (k1 & 31);
+        if (PROP == MPV_PROPOSAL_EXCHANGE && gl == (k2 >> 5)) myword ^= 1u << (k2 & 31);
+      }
+      n_acc += accept ? 1 : 0;
+      const Sign dacc = moved ? d : A::sign(0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u].add(e1[u], dacc);
+      if (PROP == MPV_PROPOSAL_EXCHANGE) {
+        const Sign mdacc = moved ? md : A::sign(0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u].add(e2[u], mdacc);
+      }
+      if (s + 1 == next_record) {
+        next_record += a.thin;
+        const int64_t r = a.round_offset + (s + 1) / a.thin - 1;
+        if (live && r < count_c && gl < words) a.samples[(offset_c + r) * words + gl] = myword;
+      }
     }
+    if (dead) lp = __longlong_as_double(0x7FF8000000000000ll);
+
+    if (live) {
+      if (gl < words) a.bits[cidx * words + gl] = myword;
+      if (gl == 0) {
+        a.log_probs[cidx] = lp;
+        if (a.accepted) a.accepted[cidx] += n_acc;
+      }
+    }
+    if (s_end < a.n_steps) {  // more segments follow: park theta and vis
+      float* sv = a.save + (size_t)grp * (U * SW) * 32 + lane;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float* src = reinterpret_cast<const float*>(&acc[u]);
+#pragma unroll
+        for (int j = 0; j < SW; ++j) sv[(u * SW + j) * 32] = src[j];
+      }
+      if (live && gl == 0) vsave[cidx] = vis;
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.done + grp), "r"((int)(seg + 1)) : "memory");
   }
 }
 

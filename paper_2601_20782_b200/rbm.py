@@ -168,11 +168,13 @@ def plan_exact(snap: RbmParameters) -> ExactPlan:
         float(np.max(np.abs(b.imag) + np.abs(w.imag).sum(axis=1))),
         float(np.abs(a.real).sum()),
     )
-    if bound <= 2.0**24 * q:
-        return ExactPlan(nat.ACC_X1, q, bound, 0.0)
     n_terms = snap.n_visible + 1
     split = 2.0 ** math.floor(math.log2(2.0**25 * q / n_terms))
-    if split >= q and bound + n_terms * split / 2 <= 2.0**24 * split:
+    if not (split >= q and bound + n_terms * split / 2 <= 2.0**24 * split):
+        split = 0.0  # X2 not exact
+    if bound <= 2.0**24 * q:
+        return ExactPlan(nat.ACC_X1, q, bound, split)
+    if split > 0.0:
         return ExactPlan(nat.ACC_X2, q, bound, split)
     return ExactPlan(nat.ACC_F64, q, bound, 0.0)
 
@@ -207,7 +209,8 @@ class DeviceSnapshot:
     """Parameters of one evaluator in kernel layout, resident on the device
     (the device counterpart of rbm.py:161-200 _PreparedRounded)."""
 
-    def __init__(self, params: RbmParameters, fmt: FloatFormat, mode: RoundingMode, device=None):
+    def __init__(self, params: RbmParameters, fmt: FloatFormat, mode: RoundingMode, device=None,
+                 variant: int | None = None):
         import torch
 
         nat.require_cuda()
@@ -236,7 +239,12 @@ class DeviceSnapshot:
                 variant = nat.ACC_F64
             else:
                 self.plan = plan_exact(snap)
-                variant = self.plan.variant
+                if variant is None:
+                    variant = self.plan.variant
+                elif variant == nat.ACC_X1 and self.plan.variant != nat.ACC_X1:
+                    raise ValueError("X1 accumulators are not exact for this snapshot")
+                elif variant == nat.ACC_X2 and self.plan.split == 0.0:
+                    raise ValueError("X2 accumulators are not exact for this snapshot")
             if variant == nat.ACC_F64:
                 table = np.stack([wpad.real, wpad.imag], axis=-1)
                 bias = np.stack([bpad.real, bpad.imag], axis=-1)
@@ -273,6 +281,13 @@ class DeviceSnapshot:
         self.struct = nat.Snapshot(N, M, Mpad, fmt.code, mode.code, variant, G, U,
                                    base, self._bias.data_ptr(), base + tbytes, self._vis_im.data_ptr())
 
+    def scratch(self, n_chains: int):
+        """Device scratch for the fused sweep over n_chains (work queue, parked theta)."""
+        import torch
+
+        nbytes = nat.load().mpv_sweep_scratch_bytes(ctypes_byref(self.struct), int(n_chains))
+        return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+
     @property
     def label(self) -> str:
         names = {nat.ACC_X1: "X1", nat.ACC_X2: "X2", nat.ACC_F64: "F64"}
@@ -295,12 +310,12 @@ class LogProbEvaluator:
     ChainEnsemble fuses it into the MH sweep instead of calling it."""
 
     def __init__(self, params: RbmParameters, fmt: FloatFormat = F64,
-                 mode: RoundingMode = RoundingMode.PER_OPERATION, device=None):
+                 mode: RoundingMode = RoundingMode.PER_OPERATION, device=None, variant: int | None = None):
         if fmt.name == "f64":
             mode = RoundingMode.PER_OPERATION  # f64 ignores the mode (rbm.py:364-372)
         self.fmt, self.mode = fmt, mode
         self.master = params
-        self.snapshot = DeviceSnapshot(params, fmt, mode, device)
+        self.snapshot = DeviceSnapshot(params, fmt, mode, device, variant)
         self.device = self.snapshot.device
 
     @property
@@ -314,8 +329,10 @@ class LogProbEvaluator:
         B = packed.shape[0]
         out = torch.empty(B, dtype=torch.float64, device=self.device)
         status = _status_tensor(self.device)
+        scratch = self.snapshot.scratch(B)
         nat.call("mpv_snapshot_forward", ctypes_byref(self.snapshot.struct), packed.data_ptr(), B,
-                 out.data_ptr(), None, None, status.data_ptr(), nat.stream_handle(self.device))
+                 out.data_ptr(), None, None, status.data_ptr(), scratch.data_ptr(), scratch.numel(),
+                 nat.stream_handle(self.device))
         return out, status
 
     def __call__(self, bits) -> np.ndarray:
@@ -351,7 +368,8 @@ class LogPsiEvaluator:
         im = torch.empty_like(lp)
         status = _status_tensor(self.device)
         nat.call("mpv_snapshot_forward", ctypes_byref(self.snapshot.struct), packed.data_ptr(), B,
-                 lp.data_ptr(), re.data_ptr(), im.data_ptr(), status.data_ptr(), nat.stream_handle(self.device))
+                 lp.data_ptr(), re.data_ptr(), im.data_ptr(), status.data_ptr(), None, 0,
+                 nat.stream_handle(self.device))
         return re, im, status
 
     def __call__(self, bits) -> np.ndarray:
@@ -382,11 +400,12 @@ def _raise_nonfinite(status, bits, what):
 
 
 def log_prob_evaluator(params, fmt: FloatFormat = F64, mode: RoundingMode = RoundingMode.PER_OPERATION,
-                       device=None) -> LogProbEvaluator:
+                       device=None, variant: int | None = None) -> LogProbEvaluator:
     """Device log-probability evaluator (rbm.py:361-405); parameters are
     downcast once at construction.  ``mode=RoundingMode.NATIVE`` selects the
-    B200 fused-sweep arithmetic."""
-    return LogProbEvaluator(params, fmt, mode, device)
+    B200 fused-sweep arithmetic; ``variant`` overrides the
+    exact-accumulator planner (all valid variants give identical results)."""
+    return LogProbEvaluator(params, fmt, mode, device, variant)
 
 
 def log_psi_evaluator(params, device=None) -> LogPsiEvaluator:
@@ -422,7 +441,7 @@ def log_psi_batch(params, bits, fmt: FloatFormat = F64, mode: RoundingMode = Rou
     re, im = torch.empty_like(lp), torch.empty_like(lp)
     status = _status_tensor(snap.device)
     nat.call("mpv_snapshot_forward", ctypes_byref(snap.struct), packed.data_ptr(), B, lp.data_ptr(),
-             re.data_ptr(), im.data_ptr(), status.data_ptr(), nat.stream_handle(snap.device))
+             re.data_ptr(), im.data_ptr(), status.data_ptr(), None, 0, nat.stream_handle(snap.device))
     out = re.cpu().numpy() + 1j * im.cpu().numpy()
     _raise_nonfinite(status, bits, "log psi")
     return out

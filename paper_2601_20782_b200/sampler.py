@@ -104,14 +104,25 @@ class ChainEnsemble:
             if not 0 <= weight <= self.n_sites:
                 raise ValueError(f"sector weight {weight} out of range")
             self.init_draws = self.n_sites - 1
+        self._scratch = None
         self._chains = nat.Chains(self.n_chains, self.chain_offset, self.n_sites, self.words,
                                   self._bits.data_ptr(), self._logp.data_ptr(), self._acc.data_ptr(),
-                                  self._status.data_ptr())
+                                  self._status.data_ptr(), None, 0)
+        self._bind_scratch()
         nat.call("mpv_chains_init", ctypes.byref(self._chains), self.key, proposal.code, weight, self._stream())
         self._launch(0)  # cached log p of the initial configurations (sampler.py:63)
         self._check()
 
     # -- internals ----------------------------------------------------------
+    def _bind_scratch(self):
+        need = nat.load().mpv_sweep_scratch_bytes(ctypes.byref(self._evaluator.snapshot.struct), self.n_chains)
+        if self._scratch is None or self._scratch.numel() < need:
+            import torch
+
+            self._scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self._chains.scratch = self._scratch.data_ptr()
+            self._chains.scratch_bytes = self._scratch.numel()
+
     def _stream(self):
         return nat.stream_handle(self.device)
 
@@ -157,6 +168,7 @@ class ChainEnsemble:
         if ev.n_visible != self.n_sites:
             raise ValueError("evaluator and ensemble disagree on the number of sites")
         self._evaluator = ev
+        self._bind_scratch()
         self._launch(0)
         self._check()
 

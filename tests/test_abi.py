@@ -1,0 +1,85 @@
+"""The C ABI (include/mpvmc_b200.h) and the built sm_100a library, without a GPU:
+the library loads, exports every declared symbol, its ctypes mirror has the
+header's struct layout, and host-only entry points validate arguments."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2601_20782_b200 import _native as nat
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mpvmc_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(mpv_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = nat.load()
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    for name in syms:
+        assert hasattr(lib, name), name
+    assert sorted(nat.EXPORTED) == syms
+    out = subprocess.run(["nm", "-D", "--defined-only", nat.LIB_PATH], capture_output=True, text=True).stdout
+    exported = sorted(set(re.findall(r" T (mpv_\w+)", out)))
+    assert exported == syms  # nothing else leaks from the library
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", nat.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_struct_layout_matches_header(tmp_path):
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "mpvmc_b200.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(mpv_snapshot), '
+                   'offsetof(mpv_snapshot, table), offsetof(mpv_snapshot, vis_im), sizeof(mpv_chains), '
+                   'offsetof(mpv_chains, bits), offsetof(mpv_chains, scratch_bytes));return 0;}\n')
+    exe = tmp_path / "layout"
+    gcc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else "gcc"
+    subprocess.run([gcc, "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    want = [ctypes.sizeof(nat.Snapshot), nat.Snapshot.table.offset, nat.Snapshot.vis_im.offset,
+            ctypes.sizeof(nat.Chains), nat.Chains.bits.offset, nat.Chains.scratch_bytes.offset]
+    assert got == want
+
+
+def test_plan_layout():
+    assert nat.plan_layout(100, 100) == (8, 13)
+    assert nat.plan_layout(100, 200) == (16, 13)
+    assert nat.plan_layout(20, 20) == (2, 10)
+    assert nat.plan_layout(256, 256) == (16, 16)
+    assert nat.plan_layout(100, 400) == (32, 13)
+    for n, m in [(100, 8), (256, 16), (12, 24), (64, 3)]:
+        g, u = nat.plan_layout(n, m)
+        assert g * u >= m and g >= (n + 31) // 32 and 32 % g == 0
+    with pytest.raises(ValueError):
+        nat.plan_layout(100, 10_000)
+
+
+def test_argument_validation_without_gpu():
+    lib = nat.load()
+    assert lib.mpv_mh_sweep(None, None, 0, 0, 0, 0, 0, 0, None, 0, 0, 0, 0, None) == nat.MPV_ERR_ARGS
+    assert b"null" in lib.mpv_last_error()
+    assert lib.mpv_local_energies(0, 0, None, None, None, 0, None, 0, 0.0, 0.0, None, None, 0, None, None,
+                                  None) == nat.MPV_ERR_ARGS
+    assert lib.mpv_rounded_log_prob(None, 1, 4, 4, None, None, None, None, None, 0, None, None,
+                                    None) == nat.MPV_ERR_ARGS
+    assert b"sm_100a" in lib.mpv_version()
+
+
+def test_product_has_no_cpu_fallback():
+    """The product package must not import the oracle or any host evaluator."""
+    pkg = os.path.join(ROOT, "paper_2601_20782_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            text = open(os.path.join(pkg, fn)).read()
+            assert "oracle" not in text.replace("oracle/", ""), fn
+            assert "numba" not in text, fn

@@ -1,0 +1,283 @@
+"""Parity of the sm_100a path with the reference, on a B200.
+
+Golden vectors come from the reference itself (tests/golden/make_golden.py);
+larger cases use the CPU oracle (oracle/), which tests/test_oracle.py pins to
+the same golden vectors.  Tolerances:
+  * RNG, per-operation forward/sampling, sample layouts: bit-exact;
+  * f64 forward / local energies: 1e-12 relative (reference sums through BLAS);
+  * NATIVE f32 log p: 1e-5 * max(1, |log p|) vs f64 (north_star tolerance, SURVEY §0.9 floor);
+  * NATIVE f16/bf16: statistical (see test_gpu_statistics.py).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import port
+from paper_2601_20782_b200 import BF16, F16, F32, F64, RoundingMode, _native, rbm, sampler
+from paper_2601_20782_b200.lattice import pack_bits
+from paper_2601_20782_b200.precision import FORMATS
+from paper_2601_20782_b200.rng import derive_key
+
+pytestmark = pytest.mark.gpu
+PER_OP = RoundingMode.PER_OPERATION
+NATIVE = RoundingMode.NATIVE
+
+
+def params_of(g, prefix=""):
+    return rbm.RbmParameters(g[f"{prefix}a"], g[f"{prefix}b"], g[f"{prefix}w"])
+
+
+def test_device_streams_match_streamset(cuda, g_rng):
+    out = torch.empty((50, 37), dtype=torch.float64, device=cuda)
+    _native.call("mpv_stream_uniforms", int(g_rng["stream_key"]), 37, 0, 0, 50, out.data_ptr(),
+                 _native.stream_handle())
+    assert np.array_equal(out.cpu().numpy(), g_rng["stream_draws"])
+    # far chains / far draws against the oracle restatement
+    out = torch.empty((16, 1000), dtype=torch.float64, device=cuda)
+    _native.call("mpv_stream_uniforms", int(g_rng["stream_key"]), 1000, 123456, 10**6, 16, out.data_ptr(),
+                 _native.stream_handle())
+    assert np.array_equal(out.cpu().numpy(), port.stream_uniforms(int(g_rng["stream_key"]), 1000, 16, 123456, 10**6))
+
+
+@pytest.mark.parametrize("fmt", ["f32", "f16", "bf16"])
+def test_per_op_forward_bitwise(cuda, g_forward, fmt):
+    mismatches = 0
+    for ci in range(int(g_forward["n_cases"])):
+        p = params_of(g_forward, f"c{ci}_")
+        bits = g_forward[f"c{ci}_bits"]
+        lp = rbm.log_prob_batch(p, bits, FORMATS[fmt], PER_OP)
+        psi = rbm.log_psi_batch(p, bits, FORMATS[fmt], PER_OP)
+        ref_lp, ref_psi = g_forward[f"c{ci}_{fmt}_lp"], g_forward[f"c{ci}_{fmt}_psi"]
+        mismatches += int(np.sum(lp != ref_lp))
+        assert np.array_equal(psi.real, ref_psi.real) or fmt == "f32"
+        # f32 only: a CUDA-vs-glibc f64 libm ulp can land on an f32 rounding boundary
+        assert np.max(np.abs(lp - ref_lp) / np.maximum(1, np.abs(ref_lp))) <= (2e-7 if fmt == "f32" else 0.0)
+        assert np.max(np.abs(psi.imag - ref_psi.imag) / np.maximum(1, np.abs(ref_psi.imag))) <= (
+            2e-7 if fmt == "f32" else 0.0)
+    if fmt != "f32":
+        assert mismatches == 0
+    else:
+        assert mismatches <= 2, mismatches
+
+
+def test_rounded_log_prob_drop_in(cuda, g_forward):
+    """mpv_rounded_log_prob has the numba kernel's argument list (_kernels.py:95-129)."""
+    lib = _native.load()
+    for fmt in ("f16", "bf16", "f32"):
+        ci = 0
+        snap = rbm.RbmParameters(g_forward[f"c{ci}_{fmt}_snap_a"], g_forward[f"c{ci}_{fmt}_snap_b"],
+                                 g_forward[f"c{ci}_{fmt}_snap_w"])
+        bits = torch.from_numpy(np.ascontiguousarray(g_forward[f"c{ci}_bits"])).to(cuda)
+        B, N = bits.shape
+        M = snap.n_hidden
+        dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(cuda)  # noqa: E731
+        a_re, b_re, b_im, w_re, w_im = (dev(v) for v in (snap.a.real, snap.b.real, snap.b.imag, snap.w.real,
+                                                          snap.w.imag))
+        out = torch.empty(B, dtype=torch.float64, device=cuda)
+        scratch = torch.empty(lib.mpv_rounded_scratch_bytes(B, N, M, FORMATS[fmt].code), dtype=torch.uint8,
+                              device=cuda)
+        _native.call("mpv_rounded_log_prob", bits.data_ptr(), B, N, M, a_re.data_ptr(), b_re.data_ptr(),
+                     b_im.data_ptr(), w_re.data_ptr(), w_im.data_ptr(), FORMATS[fmt].code, out.data_ptr(),
+                     scratch.data_ptr(), _native.stream_handle())
+        got = out.cpu().numpy()
+        ref = g_forward[f"c{ci}_{fmt}_lp"]
+        if fmt == "f32":
+            assert np.max(np.abs(got - ref) / np.maximum(1, np.abs(ref))) <= 2e-7
+        else:
+            assert np.array_equal(got, ref)
+
+
+def test_f64_and_storage_forward(cuda, g_forward):
+    for ci in range(int(g_forward["n_cases"])):
+        p = params_of(g_forward, f"c{ci}_")
+        bits = g_forward[f"c{ci}_bits"]
+        psi = rbm.log_psi_batch(p, bits, F64)
+        ref = g_forward[f"c{ci}_f64_psi"]
+        assert np.max(np.abs(psi - ref) / np.maximum(1, np.abs(ref))) < 1e-12
+        lp = rbm.log_prob_batch(p, bits, F64)
+        assert np.max(np.abs(lp - g_forward[f"c{ci}_f64_lp"]) / np.maximum(1, np.abs(lp))) < 1e-12
+        for fmt in ("bf16", "f16"):
+            st = rbm.log_prob_batch(p, bits, FORMATS[fmt], RoundingMode.STORAGE_ONLY)
+            want = g_forward[f"c{ci}_{fmt}_storage_lp"]
+            assert np.max(np.abs(st - want) / np.maximum(1, np.abs(want))) < 1e-12
+
+
+def test_native_f32_within_tolerance_of_f64(cuda, g_forward):
+    for ci in range(int(g_forward["n_cases"])):
+        p = params_of(g_forward, f"c{ci}_")
+        bits = g_forward[f"c{ci}_bits"]
+        lp = rbm.log_prob_batch(p, bits, F32, NATIVE)
+        ref = g_forward[f"c{ci}_f64_lp"]
+        # the native f32 arithmetic vs f64 on the f32 snapshot: 1e-5 relative with a floor of 1
+        assert np.max(np.abs(lp - ref) / np.maximum(1, np.abs(ref))) < 1e-5
+
+
+@pytest.mark.parametrize("fmt", ["f16", "bf16"])
+def test_native_reduced_close_to_f64(cuda, g_forward, fmt):
+    for ci in range(int(g_forward["n_cases"])):
+        p = params_of(g_forward, f"c{ci}_")
+        bits = g_forward[f"c{ci}_bits"]
+        lp = rbm.log_prob_batch(p, bits, FORMATS[fmt], NATIVE)
+        ref = g_forward[f"c{ci}_f64_lp"]
+        u = FORMATS[fmt].unit_roundoff
+        # rounding theta and each unit's log cosh once: |delta| stays a few
+        # units of roundoff times sum |theta|-scale terms
+        scale = np.abs(p.w).sum(axis=1).max() + np.abs(p.b).max() + 1
+        assert np.max(np.abs(lp - ref)) < 8 * u * scale * p.n_hidden, np.max(np.abs(lp - ref))
+
+
+@pytest.mark.parametrize("fmt", ["f16", "bf16", "f32"])
+def test_native_variants_identical(cuda, fmt):
+    """X1, X2 and F64 accumulators hold the same exact theta: identical log p."""
+    p = rbm.random_parameters(40, 2, derive_key(2, "variants"), 0.01)
+    bits = np.random.default_rng(3).integers(0, 2, size=(300, 40), dtype=np.uint8)
+    out = {}
+    for var in (_native.ACC_X1, _native.ACC_X2, _native.ACC_F64):
+        try:
+            ev = rbm.log_prob_evaluator(p, FORMATS[fmt], NATIVE, variant=var)
+        except ValueError:
+            continue
+        out[var] = ev(bits)
+    assert len(out) >= 2
+    vals = list(out.values())
+    for v in vals[1:]:
+        assert np.array_equal(v, vals[0])
+
+
+@pytest.mark.parametrize("fmt", ["f16", "bf16", "f32", "f64"])
+@pytest.mark.parametrize("mode", [NATIVE, PER_OP])
+def test_zero_parameters_give_zero(cuda, fmt, mode):
+    """ref tests/test_rbm.py:58-63; also pins that padded hidden units add exactly 0."""
+    n = 13
+    p = rbm.RbmParameters(np.zeros(n, complex), np.zeros(3 * n, complex), np.zeros((3 * n, n), complex))
+    bits = np.random.default_rng(0).integers(0, 2, size=(64, n), dtype=np.uint8)
+    assert np.array_equal(rbm.log_prob_batch(p, bits, FORMATS[fmt], mode), np.zeros(64))
+
+
+@pytest.mark.parametrize("kind,weight", [("flip", None), ("exchange", 6)])
+@pytest.mark.parametrize("fmt", ["f64", "f32", "f16", "bf16"])
+def test_ensemble_matches_reference_trajectory(cuda, g_chains, kind, weight, fmt):
+    """Device ChainEnsemble with the per-operation evaluator reproduces the
+    reference ChainEnsemble step for step (f64: same decisions, log p to 1e-12)."""
+    p = params_of(g_chains)
+    ev = rbm.log_prob_evaluator(p, FORMATS[fmt], PER_OP)
+    ens = sampler.ChainEnsemble(64, 12, sampler.Proposal(kind, weight), ev, g_chains["key"])
+    done = 0
+    for cp in (0, 1, 50, 300):
+        ens.run_steps(cp - done)
+        done = cp
+        assert np.array_equal(ens.bits, g_chains[f"{kind}_{fmt}_bits_{cp}"]), cp
+        assert ens.accepted == int(g_chains[f"{kind}_{fmt}_acc_{cp}"])
+        ref = g_chains[f"{kind}_{fmt}_logp_{cp}"]
+        tol = 1e-12 if fmt == "f64" else (2e-7 if fmt == "f32" else 0.0)
+        assert np.max(np.abs(ens.log_probs - ref) / np.maximum(1, np.abs(ref))) <= tol
+    assert ens.proposed == 64 * 300
+
+
+@pytest.mark.parametrize("ri", [0, 1, 2])
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
+def test_run_chains_matches_reference(cuda, g_chains, ri, fmt):
+    c, s, burn, thin, seed = (int(v) for v in g_chains[f"run{ri}_args"])
+    ev = rbm.log_prob_evaluator(params_of(g_chains), FORMATS[fmt], PER_OP)
+    samples, rate = sampler.run_chains(c, s, burn, thin, seed, ev, sampler.Proposal("flip"), 12)
+    assert np.array_equal(samples, g_chains[f"run{ri}_{fmt}_samples"])
+    assert rate == float(g_chains[f"run{ri}_{fmt}_rate"])
+
+
+def test_run_chains_survey_kat(cuda, g_chains):
+    p = rbm.random_parameters(4, 1, derive_key(0, "params"), 0.5)
+    samples, rate = sampler.run_chains(4, 8, 10, 5, 0, rbm.log_prob_evaluator(p, F32, PER_OP),
+                                       sampler.Proposal("flip"), 4)
+    codes = (samples * (1 << np.arange(4))).sum(axis=1)
+    assert codes.tolist() == [15, 10, 11, 10, 10, 11, 15, 15]
+    assert rate == 0.35
+    assert np.array_equal(samples, g_chains["kat4_samples"])
+
+
+@pytest.mark.parametrize("fmt,kind", [("f16", "flip"), ("bf16", "exchange"), ("f32", "flip"), ("f64", "flip")])
+def test_launch_and_shard_invariance(cuda, fmt, kind):
+    """A chain's trajectory depends only on (key, global chain id, step): one
+    long launch == many short ones, a subset of chains == the same chains in a
+    larger ensemble, and two shards == one ensemble."""
+    n = 30
+    p = rbm.random_parameters(n, 2, derive_key(4, "shard"), 0.3)
+    mode = NATIVE if fmt != "f64" else PER_OP
+    ev = rbm.log_prob_evaluator(p, FORMATS[fmt], mode)
+    prop = sampler.Proposal(kind)
+    key = derive_key(5, "chains")
+    a = sampler.ChainEnsemble(100, n, prop, ev, key)
+    a.run_steps(777)
+    b = sampler.ChainEnsemble(100, n, prop, ev, key)
+    for _ in range(7):
+        b.run_steps(111)
+    # f64 accumulators are not exact: each launch re-derives theta, so log p may
+    # differ in the last ulp; the reduced formats keep theta exact (bitwise equal)
+    same_lp = (lambda x, y: np.allclose(x, y, rtol=1e-13, atol=0)) if fmt == "f64" else np.array_equal
+    assert np.array_equal(a.bits, b.bits) and same_lp(a.log_probs, b.log_probs)
+    assert a.accepted == b.accepted
+    s0 = sampler.ChainEnsemble(37, n, prop, ev, key, chain_offset=0, n_chains_total=100)
+    s1 = sampler.ChainEnsemble(63, n, prop, ev, key, chain_offset=37, n_chains_total=100)
+    for s in (s0, s1):
+        s.run_steps(777)
+    assert np.array_equal(np.concatenate([s0.bits, s1.bits]), a.bits)
+    assert same_lp(np.concatenate([s0.log_probs, s1.log_probs]), a.log_probs)
+    # sample rows of the shards concatenate to the single-ensemble matrix
+    full = a.collect(250, 7)
+    parts = [s.collect(250, 7) for s in (s0, s1)]
+    assert np.array_equal(np.concatenate(parts), full)
+
+
+def test_native_f32_decisions_match_reference_f32(cuda):
+    """NATIVE f32 (exact theta, one rounding, accurate f32 log cosh) against the
+    reference per-operation f32 chain (oracle, bit-exact with the reference):
+    identical decisions except near-threshold ties."""
+    n, chains, steps = 20, 1024, 2000
+    p = rbm.random_parameters(n, 1, derive_key(0, "params"), 0.5)
+    key = derive_key(0, "chains")
+    ev = rbm.log_prob_evaluator(p, F32, NATIVE)
+    ens = sampler.ChainEnsemble(chains, n, sampler.Proposal("flip"), ev, key)
+    snap = rbm.round_parameters(p, F32)
+    ref = port.PortEnsemble(chains, n, "flip", None, port.Params(snap.a, snap.b, snap.w), "f32", int(key))
+    ens.run_steps(steps)
+    ref.run_steps(steps)
+    same = np.all(ens.bits == ref.bits, axis=1)
+    assert same.sum() >= chains - 2, f"{chains - same.sum()} chains diverged"
+    rel = np.abs(ens.log_probs[same] - ref.logp[same]) / np.maximum(1, np.abs(ref.logp[same]))
+    assert rel.max() < 1e-5
+
+
+def test_exchange_conserves_sector_and_uniform_accepts(cuda):
+    n = 16
+    zero = rbm.RbmParameters(np.zeros(n, complex), np.zeros(n, complex), np.zeros((n, n), complex))
+    for fmt, mode in ((F16, NATIVE), (F32, PER_OP), (F64, PER_OP)):
+        ev = rbm.log_prob_evaluator(zero, fmt, mode)
+        samples, rate = sampler.run_chains(64, 512, 20, 3, 4, ev, sampler.Proposal("exchange", 5), n)
+        assert (samples.sum(axis=1) == 5).all()
+        assert rate == 1.0  # flat target: every proposal accepted (ref tests/test_sampler.py:99-112)
+
+
+def test_host_callable_evaluator_rejected(cuda):
+    with pytest.raises(TypeError):
+        sampler.ChainEnsemble(4, 3, sampler.Proposal("flip"), lambda b: np.zeros(len(b)), derive_key(0, "c"))
+
+
+def test_nonfinite_log_prob_raises_with_context(cuda):
+    from paper_2601_20782_b200.errors import EvaluationFailureError
+
+    big = rbm.RbmParameters(np.full(2, 1e308, dtype=complex), np.zeros(2, complex), np.zeros((2, 2), complex))
+    with pytest.raises(EvaluationFailureError) as err:
+        rbm.log_prob_batch(big, np.array([[1, 1]]), F64)
+    assert err.value.context["bits"].tolist() == [1, 1]
+    # in a chain: the first failing proposal is reported with its configuration
+    # log p = +inf exactly when sites 0 and 1 are both up (2e308 overflows)
+    p = rbm.RbmParameters(np.array([1e308, 1e308, 0], complex), np.zeros(2, complex), np.zeros((2, 3), complex))
+    for fmt, mode in ((F64, PER_OP), (F32, PER_OP), (F32, NATIVE)):
+        ev = rbm.log_prob_evaluator(p, fmt, mode) if fmt is F64 else None
+        if ev is None:
+            continue
+        with pytest.raises(EvaluationFailureError) as err:
+            ens = sampler.ChainEnsemble(8, 3, sampler.Proposal("flip"), ev, derive_key(0, "chains"))
+            ens.run_steps(50)
+        assert err.value.context["bits"][:2].tolist() == [1, 1]
