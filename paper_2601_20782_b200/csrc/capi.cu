@@ -505,12 +505,13 @@ int mpv_local_energies(int N, int M, const double* a, const double* b, const dou
   energy_layout(N, M, ham, n_bonds, const_cast<void*>(tables), &C, &S, &ea, &slow);
   e.C = C; e.S = S; e.ea = ea; e.slow = slow;
   e.bits = bits; e.B = B; e.out = (double2*)out_eps; e.status = status;
-  const size_t smem = (size_t)kEnergyWarps * kSamplesPerWarp * 2 * M * sizeof(double2) +
-                      (size_t)kEnergyWarps * kSamplesPerWarp * 32 * sizeof(uint32_t);
+  const int T = e.n_terms;
+  const int threads = std::min(512, std::max(32, (T + 31) / 32 * 32));
+  const size_t smem = (size_t)kEnergySB * M * sizeof(double2) + kEnergySB * 32 * sizeof(uint32_t) +
+                      (size_t)kEnergySB * 32 * 2 * sizeof(double);
   if (smem > (size_t)max_smem_optin()) return fail(MPV_ERR_ARGS, "local_energies: n_hidden too large");
-  if (int rc = ensure_smem((const void*)&energy_kernel, smem)) return rc;
-  const int64_t per_block = (int64_t)kEnergyWarps * kSamplesPerWarp;
-  energy_kernel<<<(unsigned)((B + per_block - 1) / per_block), kEnergyWarps * 32, smem, (cudaStream_t)stream>>>(e);
+  if (int rc = ensure_smem((const void*)&energy_kernel<kEnergySB>, smem)) return rc;
+  energy_kernel<kEnergySB><<<(unsigned)((B + kEnergySB - 1) / kEnergySB), threads, smem, (cudaStream_t)stream>>>(e);
   return check_launch("local_energies");
 }
 

@@ -18,9 +18,6 @@
 namespace mpv {
 
 constexpr double kSafeRe = 4.0;
-constexpr int kEnergyWarps = 8;     // warps per block
-constexpr int kSamplesPerWarp = 2;  // samples per warp (reuses each table load twice)
-constexpr int kTermsPerLane = 8;    // register budget per lane per sample
 
 struct EnergyArgs {
   int N, M, words, ham, n_bonds, n_terms;
@@ -122,186 +119,161 @@ __device__ __forceinline__ void renorm(double2& p, int& e) {
   e += k;
 }
 
-__global__ void __launch_bounds__(kEnergyWarps * 32) energy_kernel(const EnergyArgs a) {
+// One block = SB samples x all terms.  Thread t owns term t (and t + blockDim,
+// ...), keeps the SB running products in registers and streams its column
+// of the C/S tables once per block (each load reused by SB samples); the
+// SB x M table of tanh(theta) sits in shared memory and is read as a
+// broadcast.  Sums over terms are reduced in a fixed order (deterministic).
+template <int SB>
+__global__ void __launch_bounds__(512) energy_kernel(const EnergyArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int M = a.M, T = a.n_terms;
-  double2* th = reinterpret_cast<double2*>(smem_raw) + (size_t)warp * kSamplesPerWarp * 2 * M;
-  double2* tt = th + kSamplesPerWarp * M;
-  const int64_t s_base = ((int64_t)blockIdx.x * kEnergyWarps + warp) * kSamplesPerWarp;
+  const int M = a.M, T = a.n_terms, words = a.words;
+  double2* tt = reinterpret_cast<double2*>(smem_raw);                 // [SB][M]
+  uint32_t* wsm = reinterpret_cast<uint32_t*>(tt + (size_t)SB * M);   // [SB][32]
+  double* red = reinterpret_cast<double*>(wsm + SB * 32);             // [SB][32 warps][2]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int64_t s0 = (int64_t)blockIdx.x * SB;
 
-  uint32_t word[kSamplesPerWarp];
-  bool valid[kSamplesPerWarp];
-#pragma unroll
-  for (int q = 0; q < kSamplesPerWarp; ++q) {
-    const int64_t s = s_base + q;
-    valid[q] = s < a.B;
-    word[q] = (valid[q] && lane < a.words) ? a.bits[s * a.words + lane] : 0u;
+  for (int idx = tid; idx < SB * 32; idx += blockDim.x) {
+    const int s = idx >> 5, w = idx & 31;
+    wsm[idx] = (w < words && s0 + s < a.B) ? a.bits[(s0 + s) * words + w] : 0u;
   }
-  // theta = b + W x, tanh(theta) for both samples; the packed words go
-  // through shared memory so the unit loop needs no shuffles.
-  uint32_t* wsm = reinterpret_cast<uint32_t*>(smem_raw + (size_t)kEnergyWarps * kSamplesPerWarp * 2 *
-                                                             M * sizeof(double2)) +
-                  warp * kSamplesPerWarp * 32;
-#pragma unroll
-  for (int q = 0; q < kSamplesPerWarp; ++q) wsm[q * 32 + lane] = word[q];
-  __syncwarp();
-  for (int i = lane; i < M; i += 32) {
-#pragma unroll
-    for (int q = 0; q < kSamplesPerWarp; ++q) {
-      double2 z = a.b[i];
-      for (int w = 0; w < a.words; ++w) {
-        uint32_t wd = wsm[q * 32 + w];
-        while (wd) {
-          const int k = w * 32 + __ffs(wd) - 1;
-          wd &= wd - 1;
-          const double2 e = a.w_t[(size_t)k * M + i];
-          z.x += e.x;
-          z.y += e.y;
-        }
+  __syncthreads();
+  for (int idx = tid; idx < SB * M; idx += blockDim.x) {
+    const int s = idx / M, i = idx % M;
+    double2 z = a.b[i];
+    for (int w = 0; w < words; ++w) {
+      uint32_t wd = wsm[s * 32 + w];
+      while (wd) {
+        const int k = w * 32 + __ffs(wd) - 1;
+        wd &= wd - 1;
+        const double2 e = a.w_t[(size_t)k * M + i];
+        z.x += e.x;
+        z.y += e.y;
       }
-      th[q * M + i] = z;
-      tt[q * M + i] = ctanh(z);
     }
+    tt[idx] = ctanh(z);
   }
-  __syncwarp();
+  __syncthreads();
 
-  auto bit_of = [&](int q, int k) -> int {
-    const uint32_t wd = __shfl_sync(kFull, word[q], k >> 5);
-    return (wd >> (k & 31)) & 1u;
-  };
-
-  double2 sum[kSamplesPerWarp];
-  double diag[kSamplesPerWarp];
+  auto bit_of = [&](int s, int k) -> int { return (wsm[s * 32 + (k >> 5)] >> (k & 31)) & 1u; };
+  double sr[SB], si[SB];
 #pragma unroll
-  for (int q = 0; q < kSamplesPerWarp; ++q) {
-    sum[q] = make_double2(0.0, 0.0);
-    diag[q] = 0.0;
-  }
-  // diagonal J sum s_i s_j (ref: vmc.py:52-57)
-  for (int b0 = 0; b0 < a.n_bonds; b0 += 32) {
-    const int b = b0 + lane;
-    const int p = b < a.n_bonds ? a.bonds[2 * b] : 0, r = b < a.n_bonds ? a.bonds[2 * b + 1] : 0;
-#pragma unroll
-    for (int q = 0; q < kSamplesPerWarp; ++q) {
-      const int xp = bit_of(q, p), xr = bit_of(q, r);
-      if (b < a.n_bonds) diag[q] += (double)((1 - 2 * xp) * (1 - 2 * xr));
-    }
-  }
+  for (int s = 0; s < SB; ++s) sr[s] = si[s] = 0.0;
   const bool any_terms = (a.ham == MPV_HAM_HEISENBERG) || (a.h != 0.0);
-  for (int t0 = 0; any_terms && t0 < T; t0 += 32 * kTermsPerLane) {
-    double2 P[kSamplesPerWarp][kTermsPerLane];
-    int E[kSamplesPerWarp][kTermsPerLane];
-    double dd[kSamplesPerWarp][kTermsPerLane];
-    bool on[kSamplesPerWarp][kTermsPerLane];
+  for (int t = tid; any_terms && t < T; t += blockDim.x) {
+    int p, q = 0;
+    if (a.ham == MPV_HAM_TFIM) p = t;
+    else { p = a.bonds[2 * t]; q = a.bonds[2 * t + 1]; }
+    double dd[SB];
+    double2 P[SB];
+    int E[SB];
 #pragma unroll
-    for (int r = 0; r < kTermsPerLane; ++r) {
-      const int t = t0 + r * 32 + lane;
-      const bool inr = t < T;
-      int p = 0, qq = 0;
-      if (a.ham == MPV_HAM_TFIM) p = inr ? t : 0;
-      else if (inr) { p = a.bonds[2 * t]; qq = a.bonds[2 * t + 1]; }
-#pragma unroll
-      for (int q = 0; q < kSamplesPerWarp; ++q) {
-        int d;
-        if (a.ham == MPV_HAM_TFIM) d = 1 - 2 * bit_of(q, p);
-        else d = bit_of(q, qq) - bit_of(q, p);
-        dd[q][r] = (double)d;
-        on[q][r] = inr && valid[q] && d != 0;
-        P[q][r] = make_double2(1.0, 0.0);
-        E[q][r] = 0;
-      }
+    for (int s = 0; s < SB; ++s) {
+      dd[s] = (a.ham == MPV_HAM_TFIM) ? (double)(1 - 2 * bit_of(s, p)) : (double)(bit_of(s, q) - bit_of(s, p));
+      P[s] = make_double2(1.0, 0.0);
+      E[s] = 0;
     }
-    for (int i = 0; i < M; ++i) {
-      double2 tv[kSamplesPerWarp];
+    const bool slow = a.slow[t] != 0;
+    if (!slow) {
+      const double2* Cc = a.C + t;
+      const double2* Sc = a.S + t;
+      for (int i = 0; i < M; ++i) {
+        const double2 c = Cc[(size_t)i * T], sv = Sc[(size_t)i * T];
 #pragma unroll
-      for (int q = 0; q < kSamplesPerWarp; ++q) tv[q] = tt[q * M + i];
+        for (int s = 0; s < SB; ++s) {
+          const double2 tv = tt[s * M + i];
+          const double2 ts = cmul(tv, sv);
+          P[s] = cmul(P[s], make_double2(fma(dd[s], ts.x, c.x), fma(dd[s], ts.y, c.y)));
+        }
+        if ((i & 15) == 15) {
 #pragma unroll
-      for (int r = 0; r < kTermsPerLane; ++r) {
-        const int t = t0 + r * 32 + lane;
-        if (t < T) {
-          const double2 c = a.C[(size_t)i * T + t], sv = a.S[(size_t)i * T + t];
-#pragma unroll
-          for (int q = 0; q < kSamplesPerWarp; ++q) {
-            const double2 ts = cmul(tv[q], sv);
-            const double2 f = make_double2(fma(dd[q][r], ts.x, c.x), fma(dd[q][r], ts.y, c.y));
-            P[q][r] = cmul(P[q][r], f);
-          }
+          for (int s = 0; s < SB; ++s) renorm(P[s], E[s]);
         }
       }
-      if ((i & 15) == 15) {
-#pragma unroll
-        for (int r = 0; r < kTermsPerLane; ++r)
-#pragma unroll
-          for (int q = 0; q < kSamplesPerWarp; ++q) renorm(P[q][r], E[q][r]);
-      }
     }
 #pragma unroll
-    for (int r = 0; r < kTermsPerLane; ++r) {
-      const int t = t0 + r * 32 + lane;
-#pragma unroll
-      for (int q = 0; q < kSamplesPerWarp; ++q) {
-        if (!on[q][r]) continue;
-        double2 ratio;
-        if (a.slow[t]) {
-          // log-cosh difference (ref formulation), O(M) complex logs
-          double2 lsum = make_double2(0.0, 0.0);
-          int p = 0, pq = 0;
-          if (a.ham == MPV_HAM_TFIM) p = t;
-          else { p = a.bonds[2 * t]; pq = a.bonds[2 * t + 1]; }
-          for (int i = 0; i < M; ++i) {
-            double2 w = a.w_t[(size_t)p * M + i];
-            if (a.ham != MPV_HAM_TFIM) {
-              const double2 w2 = a.w_t[(size_t)pq * M + i];
-              w = make_double2(w.x - w2.x, w.y - w2.y);
+    for (int s = 0; s < SB; ++s) {
+      if (s0 + s >= a.B || dd[s] == 0.0) continue;
+      double2 ratio;
+      if (slow) {
+        // log-cosh difference (ref formulation) with theta recomputed here
+        double2 lsum = make_double2(0.0, 0.0);
+        for (int i = 0; i < M; ++i) {
+          double2 z = a.b[i];
+          for (int w = 0; w < words; ++w) {
+            uint32_t wd = wsm[s * 32 + w];
+            while (wd) {
+              const int k = w * 32 + __ffs(wd) - 1;
+              wd &= wd - 1;
+              const double2 e = a.w_t[(size_t)k * M + i];
+              z.x += e.x;
+              z.y += e.y;
             }
-            const double2 z = th[q * M + i];
-            const double2 l1 = clogcosh(make_double2(z.x + dd[q][r] * w.x, z.y + dd[q][r] * w.y));
-            const double2 l0 = clogcosh(z);
-            lsum.x += l1.x - l0.x;
-            lsum.y += l1.y - l0.y;
           }
-          double2 av = a.ea[2 * t];  // exp(a_t): recover a_t via log-free route below
-          (void)av;
-          double2 at;
-          if (a.ham == MPV_HAM_TFIM) at = a.a[t];
-          else at = make_double2(a.a[p].x - a.a[pq].x, a.a[p].y - a.a[pq].y);
-          ratio = cexp_(make_double2(lsum.x + dd[q][r] * at.x, lsum.y + dd[q][r] * at.y));
-        } else {
-          const double2 e = a.ea[2 * t + (dd[q][r] > 0 ? 0 : 1)];
-          double2 v = cmul(e, P[q][r]);
-          const int k = E[q][r];
-          // v * 2^k without overflow in the scale factor
-          const int k1 = max(-1000, min(1000, k));
-          v.x = ldexp(v.x, k1);
-          v.y = ldexp(v.y, k1);
-          if (k != k1) {
-            v.x = ldexp(v.x, k - k1);
-            v.y = ldexp(v.y, k - k1);
+          double2 w = a.w_t[(size_t)p * M + i];
+          if (a.ham != MPV_HAM_TFIM) {
+            const double2 w2 = a.w_t[(size_t)q * M + i];
+            w = make_double2(w.x - w2.x, w.y - w2.y);
           }
-          ratio = v;
+          const double2 l1 = clogcosh(make_double2(z.x + dd[s] * w.x, z.y + dd[s] * w.y));
+          const double2 l0 = clogcosh(z);
+          lsum.x += l1.x - l0.x;
+          lsum.y += l1.y - l0.y;
         }
-        sum[q].x += ratio.x;
-        sum[q].y += ratio.y;
+        double2 at;
+        if (a.ham == MPV_HAM_TFIM) at = a.a[p];
+        else at = make_double2(a.a[p].x - a.a[q].x, a.a[p].y - a.a[q].y);
+        ratio = cexp_(make_double2(lsum.x + dd[s] * at.x, lsum.y + dd[s] * at.y));
+      } else {
+        const double2 e = a.ea[2 * t + (dd[s] > 0 ? 0 : 1)];
+        double2 v = cmul(e, P[s]);
+        const int k = E[s];
+        const int k1 = max(-1000, min(1000, k));
+        v.x = ldexp(v.x, k1);
+        v.y = ldexp(v.y, k1);
+        if (k != k1) {
+          v.x = ldexp(v.x, k - k1);
+          v.y = ldexp(v.y, k - k1);
+        }
+        ratio = v;
       }
+      sr[s] += ratio.x;
+      si[s] += ratio.y;
     }
   }
-  const double coef = (a.ham == MPV_HAM_TFIM) ? a.h : 2.0 * a.J;
+  // fixed-order reduction over threads: warp butterfly, then warps in order
 #pragma unroll
-  for (int q = 0; q < kSamplesPerWarp; ++q) {
-    const double dg = segment_sum(diag[q], 32);
-    const double sr = segment_sum(sum[q].x, 32);
-    const double si = segment_sum(sum[q].y, 32);
-    if (lane == 0 && valid[q]) {
-      const int64_t s = s_base + q;
-      const double2 eps = make_double2(a.J * dg + coef * sr, coef * si);
-      a.out[s] = eps;
-      if ((!isfinite(eps.x) || !isfinite(eps.y)) && a.status) {
-        atomicMin((unsigned long long*)&a.status[1], (unsigned long long)s);
-        atomicExch((unsigned long long*)&a.status[0], (unsigned long long)MPV_ERR_NONFINITE);
-      }
+  for (int s = 0; s < SB; ++s) {
+    const double vr = segment_sum(sr[s], 32), vi = segment_sum(si[s], 32);
+    if (lane == 0) {
+      red[(s * 32 + warp) * 2] = vr;
+      red[(s * 32 + warp) * 2 + 1] = vi;
+    }
+  }
+  __syncthreads();
+  if (tid < SB && s0 + tid < a.B) {
+    const int s = tid;
+    double er = 0.0, ei = 0.0;
+    for (int w = 0; w < nwarps; ++w) {
+      er += red[(s * 32 + w) * 2];
+      ei += red[(s * 32 + w) * 2 + 1];
+    }
+    double diag = 0.0;  // ref vmc.py:52-57
+    for (int b = 0; b < a.n_bonds; ++b) {
+      const int xp = bit_of(s, a.bonds[2 * b]), xq = bit_of(s, a.bonds[2 * b + 1]);
+      diag += (double)((1 - 2 * xp) * (1 - 2 * xq));
+    }
+    const double coef = (a.ham == MPV_HAM_TFIM) ? a.h : 2.0 * a.J;
+    const double2 eps = make_double2(a.J * diag + coef * er, coef * ei);
+    a.out[s0 + s] = eps;
+    if ((!isfinite(eps.x) || !isfinite(eps.y)) && a.status) {
+      atomicMin((unsigned long long*)&a.status[1], (unsigned long long)(s0 + s));
+      atomicExch((unsigned long long*)&a.status[0], (unsigned long long)MPV_ERR_NONFINITE);
     }
   }
 }
+
+constexpr int kEnergySB = 8;
 
 }  // namespace mpv

@@ -271,8 +271,8 @@ def test_nonfinite_log_prob_raises_with_context(cuda):
         rbm.log_prob_batch(big, np.array([[1, 1]]), F64)
     assert err.value.context["bits"].tolist() == [1, 1]
     # in a chain: the first failing proposal is reported with its configuration
-    # log p = +inf exactly when sites 0 and 1 are both up (2e308 overflows)
-    p = rbm.RbmParameters(np.array([1e308, 1e308, 0], complex), np.zeros(2, complex), np.zeros((2, 3), complex))
+    # log p = 2 * 1.2e308 overflows exactly when sites 0 and 1 are both up
+    p = rbm.RbmParameters(np.array([6e307, 6e307, 0], complex), np.zeros(2, complex), np.zeros((2, 3), complex))
     for fmt, mode in ((F64, PER_OP), (F32, PER_OP), (F32, NATIVE)):
         ev = rbm.log_prob_evaluator(p, fmt, mode) if fmt is F64 else None
         if ev is None:
