@@ -61,6 +61,8 @@ extern "C" {
  *   X2              two fmt pairs (hi, lo)                       float2 (hi, lo)
  *   F64             double2 (re, im)                             double
  * `vis_im` (double[N], a_im) is only read by mpv_snapshot_forward (log psi).
+ * For the fused sweep `vis` must sit at table + round_up(N*hidden_pad*entry, 16):
+ * [table | vis] is staged into shared memory with one bulk copy.
  */
 typedef struct {
   int32_t n_visible, n_hidden, hidden_pad;
@@ -153,9 +155,11 @@ int mpv_sum_i64(const int64_t* x, int64_t n, int64_t* out, void* stream);
 
 /* Layout of the fused sweep for N sites, M hidden units: lanes per chain G
  * (power of two, >= ceil(N/32)) and hidden units per lane U; hidden_pad = G*U.
- * The f32 summation order of NATIVE log p depends on (G, U), so it is a fixed
- * function of (N, M). */
-int mpv_plan_layout(int n_visible, int n_hidden, int32_t* lanes_per_chain, int32_t* units_per_lane);
+ * U is capped by the accumulator's register footprint (25 for X1 f16/bf16).
+ * The f32 summation order of NATIVE log p follows (G, U): a fixed function of
+ * (N, M, fmt, variant), hence of the snapshot. */
+int mpv_plan_layout(int n_visible, int n_hidden, int fmt, int variant, int32_t* lanes_per_chain,
+                    int32_t* units_per_lane);
 
 const char* mpv_last_error(void);
 const char* mpv_version(void);

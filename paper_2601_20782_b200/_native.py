@@ -62,7 +62,8 @@ _SIGNATURES = {
     "mpv_unpack_bits": (ctypes.c_int, [_vp, _i64, ctypes.c_int, _vp, _vp]),
     "mpv_pack_bits": (ctypes.c_int, [_vp, _i64, ctypes.c_int, _vp, _vp]),
     "mpv_sum_i64": (ctypes.c_int, [_vp, _i64, _vp, _vp]),
-    "mpv_plan_layout": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
+    "mpv_plan_layout": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i32),
+                                       ctypes.POINTER(_i32)]),
     "mpv_last_error": (ctypes.c_char_p, []),
     "mpv_version": (ctypes.c_char_p, []),
 }
@@ -121,7 +122,7 @@ def stream_handle(device=None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def plan_layout(n_visible: int, n_hidden: int):
+def plan_layout(n_visible: int, n_hidden: int, fmt: int = FMT_F16, variant: int = ACC_X1):
     g, u = _i32(), _i32()
-    call("mpv_plan_layout", n_visible, n_hidden, ctypes.byref(g), ctypes.byref(u))
+    call("mpv_plan_layout", n_visible, n_hidden, fmt, variant, ctypes.byref(g), ctypes.byref(u))
     return g.value, u.value

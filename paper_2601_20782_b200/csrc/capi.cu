@@ -79,7 +79,7 @@ int ensure_smem(const void* fn, size_t bytes) {
   return MPV_OK;
 }
 
-constexpr int kUnits[] = {4, 8, 10, 13, 16};
+constexpr int kUnits[] = {4, 8, 13, 16, 20, 25};
 constexpr int MAX_WORDS_INIT = 32;  // n_sites <= 1024
 
 size_t entry_bytes(int fmt, int variant) {
@@ -212,20 +212,30 @@ int mpv_pack_bits(const uint8_t* bits, int64_t B, int N, uint32_t* out, void* st
 const char* mpv_last_error(void) { return g_error.c_str(); }
 const char* mpv_version(void) { return "mpvmc_b200 0.1.0 (sm_100a)"; }
 
-int mpv_plan_layout(int n_visible, int n_hidden, int32_t* lanes_per_chain, int32_t* units_per_lane) {
+// Units-per-lane cap by accumulator footprint: registers per hidden unit are
+// theta + the kept column entry (3 for X1 f16/bf16, 4-6 for X1 f32 / X2, 8 for F64).
+static int units_cap(int fmt, int variant) {
+  if (fmt == MPV_FMT_F64 || variant == MPV_ACC_F64) return 13;
+  if (variant == MPV_ACC_X1) return fmt == MPV_FMT_F32 ? 16 : 25;
+  return fmt == MPV_FMT_F32 ? 13 : 16;
+}
+
+int mpv_plan_layout(int n_visible, int n_hidden, int fmt, int variant, int32_t* lanes_per_chain,
+                    int32_t* units_per_lane) {
   if (n_visible < 1 || n_visible > 1024 || n_hidden < 1 || !lanes_per_chain || !units_per_lane)
     return fail(MPV_ERR_ARGS, "plan: bad args");
   const int words = (n_visible + 31) / 32;
+  const int cap = units_cap(fmt, variant);
   int G = 1;
-  while (G < 32 && ((n_hidden + G - 1) / G > 16 || G < words)) G *= 2;
+  while (G < 32 && ((n_hidden + G - 1) / G > cap || G < words)) G *= 2;
   const int need = (n_hidden + G - 1) / G;
   for (int u : kUnits)
-    if (u >= need) {
+    if (u >= need && u <= cap) {
       *lanes_per_chain = G;
       *units_per_lane = u;
       return MPV_OK;
     }
-  return fail(MPV_ERR_ARGS, "plan: n_hidden > 512 is not supported by the fused sweep");
+  return fail(MPV_ERR_ARGS, "plan: too many hidden units for the fused sweep");
 }
 
 int mpv_stream_uniforms(uint64_t key, int64_t n_chains, int64_t chain0, int64_t t0, int64_t n_draws,
@@ -309,9 +319,12 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
   if (G < 1 || G > 32 || (G & (G - 1)) || G * U != snap->hidden_pad || snap->hidden_pad < snap->n_hidden)
     return fail(MPV_ERR_ARGS, "mh_sweep: snapshot layout inconsistent");
   if (G < ch->words) return fail(MPV_ERR_ARGS, "mh_sweep: lanes_per_chain < words");
-  const size_t tbytes = (size_t)snap->n_visible * snap->hidden_pad * entry_bytes(kfmt, variant) +
+  // [table | vis], each padded to 16 bytes (the host snapshot layout)
+  const size_t tbytes = (((size_t)snap->n_visible * snap->hidden_pad * entry_bytes(kfmt, variant) + 15) & ~(size_t)15) +
                         (size_t)snap->n_visible * vis_bytes(kfmt, variant);
   const size_t tbytes16 = (tbytes + 15) & ~(size_t)15;
+  if ((const char*)snap->vis != (const char*)snap->table + (tbytes - (size_t)snap->n_visible * vis_bytes(kfmt, variant)))
+    return fail(MPV_ERR_ARGS, "mh_sweep: vis must follow the table at the next 16-byte boundary");
   const bool use_smem = tbytes16 + 1024 <= (size_t)max_smem_optin();  // static smem: mbarrier
   const int sm = use_smem ? 1 : 0;
   void* fn = sweep_kernel_ptr(kfmt, variant, G, U, proposal, sm);

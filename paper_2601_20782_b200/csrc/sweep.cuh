@@ -51,13 +51,73 @@ struct SweepArgs {
 // 3 MUFU ops  ½ log(1 + t² + 2 t cos 2y) + |x| - ln2,  t = e^{-2|x|}
 // (the same closed form as ref _logcosh_pair, rbm.py:130-140), result rounded
 // to the format by the caller (pairs of units share one F2FP).
-__device__ __forceinline__ float lc_fast(float x, float y2) {
+__device__ __forceinline__ float lc_fast(float x, float y2, float& vmin) {
   const float ax = fabsf(x);
   const float t = ex2_approx(ax * -2.8853900817779268f);  // e^{-2|x|}
   const float c = cos_approx(y2);                          // cos 2y
   const float s = fmaf(2.0f, c, t);
-  const float v = fmaf(t, s, 1.0f);
+  const float v = fmaf(t, s, 1.0f);                        // 4 e^{-2|x|} |cosh z|^2
+  vmin = fminf(vmin, v);
   return fmaf(lg2_approx(v), 0.34657359027997264f, ax - 0.69314718055994531f);
+}
+
+// Near a zero of cosh (v = 1 + t^2 + 2t cos 2y -> 0) the MUFU form cancels.
+// There |x| < 0.02 and cos^2 y < 2.5e-4, and Re log cosh = ½ log(sinh^2 x +
+// cos^2 y) is evaluated with a short sinh series and cos y = ±sin r,
+// r = y - (k+½)π reduced in f64 (rare path, taken by a warp only when one of
+// its units is this close to a zero).
+// Threshold on v below which the MUFU error (~1e-6 absolute in v) exceeds the
+// format's rounding of log cosh: f16 (2^-11) -> 2e-3, bf16 (2^-8) -> 2e-4.
+// Opaque copy: keeps the rare-path recomputation inside its branch (the
+// compiler may not speculate a volatile asm), so it adds no live registers
+// to the main loop.
+template <typename T>
+__device__ __forceinline__ T opaque(T v) {
+  if constexpr (sizeof(T) == 2) {
+    unsigned short r;
+    asm volatile("mov.b16 %0, %1;" : "=h"(r) : "h"(*reinterpret_cast<unsigned short*>(&v)));
+    return *reinterpret_cast<T*>(&r);
+  } else if constexpr (sizeof(T) == 4) {
+    unsigned r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(*reinterpret_cast<unsigned*>(&v)));
+    return *reinterpret_cast<T*>(&r);
+  } else {
+    unsigned long long r;
+    asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(*reinterpret_cast<unsigned long long*>(&v)));
+    return *reinterpret_cast<T*>(&r);
+  }
+}
+
+// opaque(v) that also waits for `dep`: serializes the unrolled rare path unit
+// by unit (unit u's recomputation cannot start before unit u-1's correction).
+template <typename T>
+__device__ __forceinline__ T opaque_after(T v, float dep) {
+  if constexpr (sizeof(T) == 2) {
+    unsigned short r;
+    asm volatile("mov.b16 %0, %1;" : "=h"(r) : "h"(*reinterpret_cast<unsigned short*>(&v)), "f"(dep));
+    return *reinterpret_cast<T*>(&r);
+  } else if constexpr (sizeof(T) == 4) {
+    unsigned r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(*reinterpret_cast<unsigned*>(&v)), "f"(dep));
+    return *reinterpret_cast<T*>(&r);
+  } else {
+    unsigned long long r;
+    asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(*reinterpret_cast<unsigned long long*>(&v)), "f"(dep));
+    return *reinterpret_cast<T*>(&r);
+  }
+}
+
+template <int FMT> struct NearZero { static constexpr float kV = FMT == MPV_FMT_BF16 ? 2e-4f : 2e-3f; };
+constexpr float kNearZeroV = 2e-3f;
+__device__ __forceinline__ float lc_near_zero(float x, float y) {
+  const float ax = fabsf(x);
+  const float x2 = ax * ax;
+  const float sh = ax * fmaf(x2, fmaf(x2, 1.0f / 120.0f, 1.0f / 6.0f), 1.0f);
+  const double q = rint((double)y * 0.31830988618379067 - 0.5) + 0.5;
+  const float r = (float)fma(-q, 3.141592653589793, (double)y);
+  const float r2 = r * r;
+  const float sr = r * fmaf(r2, fmaf(r2, 1.0f / 120.0f, -1.0f / 6.0f), 1.0f);
+  return 0.34657359027997264f * lg2_approx(fmaf(sh, sh, sr * sr));
 }
 
 // f32 NATIVE: accurate single-precision regime-split form:
@@ -227,7 +287,7 @@ template <int FMT, int VAR> struct Eval {
   // Reduced formats: theta rounded to fmt, lc in f32, lc rounded to fmt, then
   // accumulated in f32 (mask 0 for padded units).
   template <typename T>
-  __device__ __forceinline__ static void pair(T xr0, T xi0, T xr1, T xi1, Sum& acc) {
+  __device__ __forceinline__ static void pair(T xr0, T xi0, T xr1, T xi1, Sum& acc, float& vmin) {
     if constexpr (kF64) {
       acc += lc_f64(xr0, xi0);
       acc += lc_f64(xr1, xi1);
@@ -239,8 +299,8 @@ template <int FMT, int VAR> struct Eval {
       } else {
         using H = Half<FMT>;
         const uint32_t p0 = H::pack(a0, b0), p1 = H::pack(a1, b1);
-        const float l0 = lc_fast(H::lo(p0), H::hi2(p0));
-        const float l1 = lc_fast(H::lo(p1), H::hi2(p1));
+        const float l0 = lc_fast(H::lo(p0), H::hi2(p0), vmin);
+        const float l1 = lc_fast(H::lo(p1), H::hi2(p1), vmin);
         const uint32_t lp = H::pack(l0, l1);
         acc = H::acc_lo(lp, acc);
         acc = H::acc_hi(lp, acc);
@@ -248,7 +308,7 @@ template <int FMT, int VAR> struct Eval {
     }
   }
   template <typename T>
-  __device__ __forceinline__ static void single(T xr, T xi, Sum& acc) {
+  __device__ __forceinline__ static void single(T xr, T xi, Sum& acc, float& vmin) {
     if constexpr (kF64) {
       acc += lc_f64(xr, xi);
     } else if constexpr (FMT == MPV_FMT_F32) {
@@ -256,20 +316,40 @@ template <int FMT, int VAR> struct Eval {
     } else {
       using H = Half<FMT>;
       const uint32_t p = H::pack((float)xr, (float)xi);
-      const uint32_t lp = H::pack(lc_fast(H::lo(p), H::hi2(p)), 0.0f);
+      const uint32_t lp = H::pack(lc_fast(H::lo(p), H::hi2(p), vmin), 0.0f);
       acc = H::acc_lo(lp, acc);
     }
   }
-  // Visible term (exact) and hidden sum -> log p (double).
-  __device__ __forceinline__ static double finalize(typename A::Vis vis, Sum h) {
+  // Correction for units near a cosh zero: h += q(lc_near_zero) - q(lc_fast)
+  // (both rounded to the format), in unit order.  Deterministic in theta.
+  template <typename T>
+  __device__ __forceinline__ static void fix(T xr, T xi, Sum& acc) {
+    if constexpr (!kF64 && FMT != MPV_FMT_F32) {
+      using H = Half<FMT>;
+      const uint32_t p = H::pack((float)xr, (float)xi);
+      float v = 1e30f;
+      const float lf = lc_fast(H::lo(p), H::hi2(p), v);
+      if (v < NearZero<FMT>::kV) {
+        const float la = lc_near_zero(H::lo(p), H::hi(p));
+        const uint32_t q = H::pack(lf, la);
+        acc += H::hi(q) - H::lo(q);
+      }
+    }
+  }
+  static constexpr bool kFix = !kF64 && FMT != MPV_FMT_F32;
+  // log p is f64 for the f64 arithmetic and f32 for the NATIVE reduced
+  // formats (an f32 number: 2 * RN32(RN32(a.x) + H)); the NATIVE accept test
+  // is then made in f32.
+  using Lp = typename std::conditional<kF64, double, float>::type;
+  __device__ __forceinline__ static Lp finalize(typename A::Vis vis, Sum h) {
     if constexpr (kF64) {
       return 2.0 * (vis + h);
     } else if constexpr (VAR == MPV_ACC_F64) {
-      return 2.0 * (double)__fadd_rn(__double2float_rn(vis), h);
+      return 2.0f * __fadd_rn(__double2float_rn(vis), h);
     } else if constexpr (VAR == MPV_ACC_X2) {
-      return 2.0 * (double)__fadd_rn(__fadd_rn(vis.x, vis.y), h);
+      return 2.0f * __fadd_rn(__fadd_rn(vis.x, vis.y), h);
     } else {
-      return 2.0 * (double)__fadd_rn(vis, h);
+      return 2.0f * __fadd_rn(vis, h);
     }
   }
 };
@@ -301,13 +381,14 @@ __device__ __forceinline__ void report_nonfinite(int64_t* status, int64_t step, 
 // ------------------------------------------------------------------------
 
 template <int FMT, int VAR, int G, int U, int PROP, bool SMEM>
-__global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a) {
   using A = Acc<FMT, VAR>;
   using E = Eval<FMT, VAR>;
   using Entry = typename A::Entry;
   using VisT = typename A::Vis;
   using Sign = typename A::Sign;
   using Sum = typename E::Sum;
+  using Lp = typename E::Lp;
   using Theta = typename std::conditional<VAR == MPV_ACC_F64, double, float>::type;
   constexpr int CPW = 32 / G;
   constexpr int SW = (int)(sizeof(A) / sizeof(float));
@@ -346,10 +427,10 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
             sbar)
         : "memory");
     tab = reinterpret_cast<const Entry*>(smem_raw);
-    visv = reinterpret_cast<const VisT*>(smem_raw + (size_t)a.N * (G * U) * sizeof(Entry));
+    visv = reinterpret_cast<const VisT*>(smem_raw + (((size_t)a.N * (G * U) * sizeof(Entry) + 15) & ~(size_t)15));
   } else {
     tab = reinterpret_cast<const Entry*>(a.table);
-    visv = reinterpret_cast<const VisT*>((const char*)a.table + (size_t)a.N * (G * U) * sizeof(Entry));
+    visv = reinterpret_cast<const VisT*>((const char*)a.table + (((size_t)a.N * (G * U) * sizeof(Entry) + 15) & ~(size_t)15));
   }
   constexpr int Mpad = G * U;
   const int lane = threadIdx.x & 31;
@@ -387,7 +468,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
 
     A acc[U];
     VisT vis;
-    double lp;
+    Lp lp;
     if (seg == 0) {
       // refresh: theta = b + W x, vis = a.x, log p (set_evaluator semantics)
 #pragma unroll
@@ -406,23 +487,34 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
         }
       }
       Sum h0 = Sum(0);
+      float vmin0 = 1e30f;
 #pragma unroll
       for (int u = 0; u + 1 < U; u += 2) {
         Theta xr0, xi0, xr1, xi1;
         acc[u].prop1(Entry{}, A::sign(0), xr0, xi0);
         acc[u + 1].prop1(Entry{}, A::sign(0), xr1, xi1);
-        E::pair(xr0, xi0, xr1, xi1, h0);
+        E::pair(xr0, xi0, xr1, xi1, h0, vmin0);
       }
       if constexpr (U & 1) {
         Theta xr, xi;
         acc[U - 1].prop1(Entry{}, A::sign(0), xr, xi);
-        E::single(xr, xi, h0);
+        E::single(xr, xi, h0, vmin0);
+      }
+      if constexpr (E::kFix) {
+        if (vmin0 < NearZero<FMT>::kV) {  // rare: a unit is near a cosh zero
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            Theta xr, xi;
+            acc[u].prop1(Entry{}, opaque_after(A::sign(0), h0), xr, xi);
+            E::fix(xr, xi, h0);
+          }
+        }
       }
       h0 = segment_sum(h0, G);
       lp = E::finalize(vis, h0);
       if (!isfinite(lp)) {
         if (live && gl == 0) report_nonfinite(a.status, 0, cidx);
-        lp = __longlong_as_double(0x7FF8000000000000ll);  // NaN marks a frozen chain
+        lp = Lp(NAN);  // NaN marks a frozen chain
       }
     } else {
       const float* sv = a.save + (size_t)grp * (U * SW) * 32 + lane;
@@ -433,7 +525,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
         for (int j = 0; j < SW; ++j) dst[j] = sv[(u * SW + j) * 32];
       }
       vis = vsave[cidx];
-      lp = a.log_probs[cidx];
+      lp = (Lp)a.log_probs[cidx];
     }
     bool dead = isnan(lp);
 
@@ -441,19 +533,21 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
     const int64_t count_c = a.sample_base + ((gchain < a.sample_extra) ? 1 : 0);
     const int64_t offset_c =
         gchain * a.sample_base + (gchain < a.sample_extra ? gchain : a.sample_extra) - a.row0;
-    int64_t n_acc = 0;
-    int sel_c = 0;        // cached selection (site, or pair i | j<<16)
-    double logu_c = 0.0;  // cached log(u_accept)
-    const int64_t s_begin = seg * a.seg_len;
-    const int64_t s_end = min(a.n_steps, s_begin + a.seg_len);
-    int64_t next_record = -1;
-    if (a.samples && a.thin > 0) next_record = ((s_begin / a.thin) + 1) * a.thin;
+    int n_acc = 0;
+    int sel_c = 0;    // cached selection (site, or pair i | j<<16)
+    Lp logu_c = 0;    // cached log(u_accept) (f32 for the NATIVE reduced formats)
+    const int s_begin = (int)(seg * a.seg_len);
+    const int s_end = (int)min(a.n_steps, (int64_t)s_begin + a.seg_len);
+    const int thin = (int)a.thin;
+    int next_record = -1;
+    if (a.samples && thin > 0) next_record = (s_begin / thin + 1) * thin;
+    const int64_t t_base = a.init_draws + 2 * a.step_index;
 
-    for (int64_t s = s_begin; s < s_end; ++s) {
-      const int src = (int)(s & (G - 1));
+    for (int s = s_begin; s < s_end; ++s) {
+      const int src = s & (G - 1);
       if (src == 0) {
         // lane gl draws the two uniforms of step s+gl (ref: sampler.py:113,127)
-        const uint64_t t = (uint64_t)(a.init_draws + 2 * (a.step_index + s + gl));
+        const uint64_t t = (uint64_t)(t_base + 2 * (int64_t)(s + gl));
         const double us = stream_draw(s0, t);
         const double ua = stream_draw(s0, t + 1);
         if (PROP == MPV_PROPOSAL_FLIP) {
@@ -463,23 +557,27 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
           pair_of(floor_scaled(us, n_pairs), N, i, j);
           sel_c = i | (j << 16);
         }
-        logu_c = log(ua);
+        logu_c = (Lp)log(ua);
       }
       const int sel = __shfl_sync(kFull, sel_c, src, G);
-      const double logu = __shfl_sync(kFull, logu_c, src, G);
+      const Lp logu = __shfl_sync(kFull, logu_c, src, G);
 
       int dsign, k1, k2 = 0;
+      uint32_t flip;  // this lane's word bits that change if the move is accepted
       if (PROP == MPV_PROPOSAL_FLIP) {
         k1 = sel;
+        const uint32_t m1 = 1u << (k1 & 31);
         const uint32_t wd = __shfl_sync(kFull, myword, k1 >> 5, G);
-        dsign = ((wd >> (k1 & 31)) & 1u) ? -1 : 1;
+        dsign = (wd & m1) ? -1 : 1;
+        flip = (gl == (k1 >> 5)) ? m1 : 0u;
       } else {
         k1 = sel & 0xFFFF;
         k2 = sel >> 16;
+        const uint32_t m1 = 1u << (k1 & 31), m2 = 1u << (k2 & 31);
         const uint32_t wi = __shfl_sync(kFull, myword, k1 >> 5, G);
         const uint32_t wj = __shfl_sync(kFull, myword, k2 >> 5, G);
-        const int bi = (wi >> (k1 & 31)) & 1u, bj = (wj >> (k2 & 31)) & 1u;
-        dsign = bj - bi;  // x_i' = x_j: theta' = theta + d (W_:i - W_:j)
+        dsign = ((wj & m2) ? 1 : 0) - ((wi & m1) ? 1 : 0);  // x_i' = x_j: theta' = theta + d (W_:i - W_:j)
+        flip = ((gl == (k1 >> 5)) ? m1 : 0u) ^ ((gl == (k2 >> 5)) ? m2 : 0u);
       }
       // Every segment evaluates (no divergence around the segment shuffles); an
       // exchange of equal bits (dsign == 0) is accepted unconditionally: the
@@ -496,6 +594,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
         if (PROP == MPV_PROPOSAL_EXCHANGE) e2[u] = c2[u * G];
       }
       Sum h = Sum(0);
+      float vmin = 1e30f;
 #pragma unroll
       for (int u = 0; u + 1 < U; u += 2) {
         Theta xr0, xi0, xr1, xi1;
@@ -506,33 +605,42 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
           acc[u].prop2(e1[u], e2[u], d, md, xr0, xi0);
           acc[u + 1].prop2(e1[u + 1], e2[u + 1], d, md, xr1, xi1);
         }
-        E::pair(xr0, xi0, xr1, xi1, h);
+        E::pair(xr0, xi0, xr1, xi1, h, vmin);
       }
       if constexpr (U & 1) {
         Theta xr, xi;
         if (PROP == MPV_PROPOSAL_FLIP) acc[U - 1].prop1(e1[U - 1], d, xr, xi);
         else acc[U - 1].prop2(e1[U - 1], e2[U - 1], d, md, xr, xi);
-        E::single(xr, xi, h);
+        E::single(xr, xi, h, vmin);
+      }
+      if constexpr (E::kFix) {
+        if (vmin < NearZero<FMT>::kV) {  // rare: a unit of this lane is near a cosh zero
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            Theta xr, xi;
+            const Sign od = opaque_after(d, h);
+            if (PROP == MPV_PROPOSAL_FLIP) acc[u].prop1(e1[u], od, xr, xi);
+            else acc[u].prop2(e1[u], e2[u], od, opaque_after(md, h), xr, xi);
+            E::fix(xr, xi, h);
+          }
+        }
       }
       h = segment_sum(h, G);
       VisT vnew = vis_add(vis, visv[k1], dsign);
       if (PROP == MPV_PROPOSAL_EXCHANGE) vnew = vis_add(vnew, visv[k2], -dsign);
-      const double lp_new = E::finalize(vnew, h);
+      const Lp lp_new = E::finalize(vnew, h);
       // ref sampler.py:128-129: NaN compares false (reject); the reference raises
       // EvaluationFailureError on any non-finite proposal (rbm.py:242-251): the
       // chain freezes and the first failure is reported.
-      if (dsign != 0 && !isfinite(lp_new) && !dead) {
+      if (!isfinite(lp_new) && dsign != 0 && !dead) {
         dead = true;
         if (live && gl == 0) report_nonfinite(a.status, a.step_index + s + 1, cidx);
       }
       const bool accept = !dead && (dsign == 0 || logu < lp_new - lp);
       const bool moved = accept && dsign != 0;
-      if (moved) {
-        vis = vnew;
-        lp = lp_new;
-        if (gl == (k1 >> 5)) myword ^= 1u << (k1 & 31);
-        if (PROP == MPV_PROPOSAL_EXCHANGE && gl == (k2 >> 5)) myword ^= 1u << (k2 & 31);
-      }
+      vis = moved ? vnew : vis;
+      lp = moved ? lp_new : lp;
+      myword ^= moved ? flip : 0u;
       n_acc += accept ? 1 : 0;
       const Sign dacc = moved ? d : A::sign(0);
 #pragma unroll
@@ -543,17 +651,17 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
         for (int u = 0; u < U; ++u) acc[u].add(e2[u], mdacc);
       }
       if (s + 1 == next_record) {
-        next_record += a.thin;
-        const int64_t r = a.round_offset + (s + 1) / a.thin - 1;
+        next_record += thin;
+        const int64_t r = a.round_offset + (s + 1) / thin - 1;
         if (live && r < count_c && gl < words) a.samples[(offset_c + r) * words + gl] = myword;
       }
     }
-    if (dead) lp = __longlong_as_double(0x7FF8000000000000ll);
+    if (dead) lp = Lp(NAN);
 
     if (live) {
       if (gl < words) a.bits[cidx * words + gl] = myword;
       if (gl == 0) {
-        a.log_probs[cidx] = lp;
+        a.log_probs[cidx] = (double)lp;
         if (a.accepted) a.accepted[cidx] += n_acc;
       }
     }

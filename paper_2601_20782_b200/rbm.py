@@ -229,12 +229,6 @@ class DeviceSnapshot:
             bias = _pairs(snap.b.real, snap.b.imag, fmt.name)
             vis = snap.a.real.astype(np.float32)
         else:
-            G, U = nat.plan_layout(N, M)
-            Mpad = G * U
-            wpad = np.zeros((N, Mpad), dtype=np.complex128)
-            wpad[:, :M] = wt
-            bpad = np.zeros(Mpad, dtype=np.complex128)
-            bpad[:M] = snap.b
             if f64arith:
                 variant = nat.ACC_F64
             else:
@@ -245,6 +239,12 @@ class DeviceSnapshot:
                     raise ValueError("X1 accumulators are not exact for this snapshot")
                 elif variant == nat.ACC_X2 and self.plan.split == 0.0:
                     raise ValueError("X2 accumulators are not exact for this snapshot")
+            G, U = nat.plan_layout(N, M, nat.FMT_F64 if f64arith else fmt.code, variant)
+            Mpad = G * U
+            wpad = np.zeros((N, Mpad), dtype=np.complex128)
+            wpad[:, :M] = wt
+            bpad = np.zeros(Mpad, dtype=np.complex128)
+            bpad[:M] = snap.b
             if variant == nat.ACC_F64:
                 table = np.stack([wpad.real, wpad.imag], axis=-1)
                 bias = np.stack([bpad.real, bpad.imag], axis=-1)

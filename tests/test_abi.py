@@ -52,14 +52,20 @@ def test_struct_layout_matches_header(tmp_path):
 
 
 def test_plan_layout():
-    assert nat.plan_layout(100, 100) == (8, 13)
-    assert nat.plan_layout(100, 200) == (16, 13)
-    assert nat.plan_layout(20, 20) == (2, 10)
-    assert nat.plan_layout(256, 256) == (16, 16)
-    assert nat.plan_layout(100, 400) == (32, 13)
-    for n, m in [(100, 8), (256, 16), (12, 24), (64, 3)]:
-        g, u = nat.plan_layout(n, m)
-        assert g * u >= m and g >= (n + 31) // 32 and 32 % g == 0
+    x1 = dict(fmt=nat.FMT_F16, variant=nat.ACC_X1)
+    x2 = dict(fmt=nat.FMT_F16, variant=nat.ACC_X2)
+    assert nat.plan_layout(100, 100, **x1) == (4, 25)
+    assert nat.plan_layout(100, 200, **x1) == (8, 25)
+    assert nat.plan_layout(20, 20, **x1) == (1, 20)
+    assert nat.plan_layout(100, 100, **x2) == (8, 13)
+    assert nat.plan_layout(100, 200, **x2) == (16, 13)
+    assert nat.plan_layout(256, 256, **x2) == (16, 16)
+    assert nat.plan_layout(100, 400, nat.FMT_F64, nat.ACC_F64) == (32, 13)
+    for fmt, var in [(nat.FMT_F16, nat.ACC_X1), (nat.FMT_BF16, nat.ACC_X2), (nat.FMT_F32, nat.ACC_X1),
+                     (nat.FMT_F32, nat.ACC_F64), (nat.FMT_F64, nat.ACC_F64)]:
+        for n, m in [(100, 8), (256, 16), (12, 24), (64, 3), (1024, 256), (100, 400)]:
+            g, u = nat.plan_layout(n, m, fmt, var)
+            assert g * u >= m and g >= (n + 31) // 32 and 32 % g == 0
     with pytest.raises(ValueError):
         nat.plan_layout(100, 10_000)
 
