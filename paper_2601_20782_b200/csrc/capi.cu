@@ -1,6 +1,7 @@
 // C ABI of libmpvmc_b200 (include/mpvmc_b200.h): argument checks, launch
 // configuration and the small helper kernels.  No device allocation happens
 // here: every buffer is caller-owned.
+#include <algorithm>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -519,12 +520,24 @@ int mpv_local_energies(int N, int M, const double* a, const double* b, const dou
   e.C = C; e.S = S; e.ea = ea; e.slow = slow;
   e.bits = bits; e.B = B; e.out = (double2*)out_eps; e.status = status;
   const int T = e.n_terms;
-  const int threads = std::min(512, std::max(32, (T + 31) / 32 * 32));
-  const size_t smem = (size_t)kEnergySB * M * sizeof(double2) + kEnergySB * 32 * sizeof(uint32_t) +
-                      (size_t)kEnergySB * 32 * 2 * sizeof(double);
+  const int TT = (T + 31) / 32 * 32;
+  if (TT > 512 || M > 512) return fail(MPV_ERR_ARGS, "local_energies: more than 512 terms or hidden units");
+  // staging buffer: a chunk of kRows C and S rows, or >= 8 W_t rows
+  const int stage = (int)std::max<size_t>((size_t)2 * kRows * T * sizeof(double2), (size_t)8 * M * sizeof(double2));
+  auto smem_for = [&](int ng) {
+    return (size_t)kEnergyST * ng * M * sizeof(double2) + (size_t)kEnergyST * ng * 32 * sizeof(uint32_t) +
+           (size_t)((N + 3) / 4) * 4 * sizeof(uint32_t) + (size_t)kMaxSB * 16 * 2 * sizeof(double) +
+           2 * (size_t)stage + 2 * sizeof(uint64_t);
+  };
+  int NG = (2 * TT <= 512 && 2 * kEnergyST <= kMaxSB) ? 2 : 1;  // sample groups per block (table reuse)
+  if (smem_for(NG) > (size_t)max_smem_optin()) NG = 1;
+  const size_t smem = smem_for(NG);
   if (smem > (size_t)max_smem_optin()) return fail(MPV_ERR_ARGS, "local_energies: n_hidden too large");
-  if (int rc = ensure_smem((const void*)&energy_kernel<kEnergySB>, smem)) return rc;
-  energy_kernel<kEnergySB><<<(unsigned)((B + kEnergySB - 1) / kEnergySB), threads, smem, (cudaStream_t)stream>>>(e);
+  const int SB = kEnergyST * NG;
+  const int threads = std::max(std::max(32, NG * TT), (M + 31) / 32 * 32);
+  if (threads > 512) return fail(MPV_ERR_ARGS, "local_energies: block too large");
+  if (int rc = ensure_smem((const void*)&energy_kernel<kEnergyST>, smem)) return rc;
+  energy_kernel<kEnergyST><<<(unsigned)((B + SB - 1) / SB), threads, smem, (cudaStream_t)stream>>>(e, NG, stage);
   return check_launch("local_energies");
 }
 
