@@ -68,45 +68,6 @@ __device__ __forceinline__ float lc_fast(float x, float y2, float& vmin) {
 // its units is this close to a zero).
 // Threshold on v below which the MUFU error (~1e-6 absolute in v) exceeds the
 // format's rounding of log cosh: f16 (2^-11) -> 2e-3, bf16 (2^-8) -> 2e-4.
-// Opaque copy: keeps the rare-path recomputation inside its branch (the
-// compiler may not speculate a volatile asm), so it adds no live registers
-// to the main loop.
-template <typename T>
-__device__ __forceinline__ T opaque(T v) {
-  if constexpr (sizeof(T) == 2) {
-    unsigned short r;
-    asm volatile("mov.b16 %0, %1;" : "=h"(r) : "h"(*reinterpret_cast<unsigned short*>(&v)));
-    return *reinterpret_cast<T*>(&r);
-  } else if constexpr (sizeof(T) == 4) {
-    unsigned r;
-    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(*reinterpret_cast<unsigned*>(&v)));
-    return *reinterpret_cast<T*>(&r);
-  } else {
-    unsigned long long r;
-    asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(*reinterpret_cast<unsigned long long*>(&v)));
-    return *reinterpret_cast<T*>(&r);
-  }
-}
-
-// opaque(v) that also waits for `dep`: serializes the unrolled rare path unit
-// by unit (unit u's recomputation cannot start before unit u-1's correction).
-template <typename T>
-__device__ __forceinline__ T opaque_after(T v, float dep) {
-  if constexpr (sizeof(T) == 2) {
-    unsigned short r;
-    asm volatile("mov.b16 %0, %1;" : "=h"(r) : "h"(*reinterpret_cast<unsigned short*>(&v)), "f"(dep));
-    return *reinterpret_cast<T*>(&r);
-  } else if constexpr (sizeof(T) == 4) {
-    unsigned r;
-    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(*reinterpret_cast<unsigned*>(&v)), "f"(dep));
-    return *reinterpret_cast<T*>(&r);
-  } else {
-    unsigned long long r;
-    asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(*reinterpret_cast<unsigned long long*>(&v)), "f"(dep));
-    return *reinterpret_cast<T*>(&r);
-  }
-}
-
 template <int FMT> struct NearZero { static constexpr float kV = FMT == MPV_FMT_BF16 ? 2e-4f : 2e-3f; };
 constexpr float kNearZeroV = 2e-3f;
 __device__ __forceinline__ float lc_near_zero(float x, float y) {
@@ -381,7 +342,7 @@ __device__ __forceinline__ void report_nonfinite(int64_t* status, int64_t step, 
 // ------------------------------------------------------------------------
 
 template <int FMT, int VAR, int G, int U, int PROP, bool SMEM>
-__global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
   using A = Acc<FMT, VAR>;
   using E = Eval<FMT, VAR>;
   using Entry = typename A::Entry;
@@ -502,10 +463,20 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a) {
       }
       if constexpr (E::kFix) {
         if (vmin0 < NearZero<FMT>::kV) {  // rare: a unit is near a cosh zero
+          // the accumulators go through this lane's parking slot so the
+          // correction loop is a compact rolled loop (no register pressure)
+          float* sv = a.save + (size_t)grp * (U * SW) * 32 + lane;
 #pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < SW; ++j) sv[(u * SW + j) * 32] = reinterpret_cast<const float*>(&acc[u])[j];
+#pragma unroll 1
           for (int u = 0; u < U; ++u) {
+            A au;
+#pragma unroll
+            for (int j = 0; j < SW; ++j) reinterpret_cast<float*>(&au)[j] = sv[(u * SW + j) * 32];
             Theta xr, xi;
-            acc[u].prop1(Entry{}, opaque_after(A::sign(0), h0), xr, xi);
+            au.prop1(Entry{}, A::sign(0), xr, xi);
             E::fix(xr, xi, h0);
           }
         }
@@ -585,42 +556,43 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a) {
       // (sampler.py:119-131).
       const Sign d = A::sign(dsign);
       const Sign md = A::sign(-dsign);
-      Entry e1[U], e2[U];
       const Entry* c1 = tab + (size_t)k1 * Mpad + gl;
       const Entry* c2 = tab + (size_t)k2 * Mpad + gl;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        e1[u] = c1[u * G];
-        if (PROP == MPV_PROPOSAL_EXCHANGE) e2[u] = c2[u * G];
-      }
       Sum h = Sum(0);
       float vmin = 1e30f;
 #pragma unroll
       for (int u = 0; u + 1 < U; u += 2) {
         Theta xr0, xi0, xr1, xi1;
         if (PROP == MPV_PROPOSAL_FLIP) {
-          acc[u].prop1(e1[u], d, xr0, xi0);
-          acc[u + 1].prop1(e1[u + 1], d, xr1, xi1);
+          acc[u].prop1(c1[u * G], d, xr0, xi0);
+          acc[u + 1].prop1(c1[(u + 1) * G], d, xr1, xi1);
         } else {
-          acc[u].prop2(e1[u], e2[u], d, md, xr0, xi0);
-          acc[u + 1].prop2(e1[u + 1], e2[u + 1], d, md, xr1, xi1);
+          acc[u].prop2(c1[u * G], c2[u * G], d, md, xr0, xi0);
+          acc[u + 1].prop2(c1[(u + 1) * G], c2[(u + 1) * G], d, md, xr1, xi1);
         }
         E::pair(xr0, xi0, xr1, xi1, h, vmin);
       }
       if constexpr (U & 1) {
         Theta xr, xi;
-        if (PROP == MPV_PROPOSAL_FLIP) acc[U - 1].prop1(e1[U - 1], d, xr, xi);
-        else acc[U - 1].prop2(e1[U - 1], e2[U - 1], d, md, xr, xi);
+        if (PROP == MPV_PROPOSAL_FLIP) acc[U - 1].prop1(c1[(U - 1) * G], d, xr, xi);
+        else acc[U - 1].prop2(c1[(U - 1) * G], c2[(U - 1) * G], d, md, xr, xi);
         E::single(xr, xi, h, vmin);
       }
       if constexpr (E::kFix) {
         if (vmin < NearZero<FMT>::kV) {  // rare: a unit of this lane is near a cosh zero
+          float* sv = a.save + (size_t)grp * (U * SW) * 32 + lane;
 #pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < SW; ++j) sv[(u * SW + j) * 32] = reinterpret_cast<const float*>(&acc[u])[j];
+#pragma unroll 1
           for (int u = 0; u < U; ++u) {
+            A au;
+#pragma unroll
+            for (int j = 0; j < SW; ++j) reinterpret_cast<float*>(&au)[j] = sv[(u * SW + j) * 32];
             Theta xr, xi;
-            const Sign od = opaque_after(d, h);
-            if (PROP == MPV_PROPOSAL_FLIP) acc[u].prop1(e1[u], od, xr, xi);
-            else acc[u].prop2(e1[u], e2[u], od, opaque_after(md, h), xr, xi);
+            if (PROP == MPV_PROPOSAL_FLIP) au.prop1(c1[u * G], d, xr, xi);
+            else au.prop2(c1[u * G], c2[u * G], d, md, xr, xi);
             E::fix(xr, xi, h);
           }
         }
@@ -642,13 +614,15 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a) {
       lp = moved ? lp_new : lp;
       myword ^= moved ? flip : 0u;
       n_acc += accept ? 1 : 0;
+      // commit: the column entries are re-read from shared memory (cheaper than
+      // keeping U entries live in registers across the evaluation)
       const Sign dacc = moved ? d : A::sign(0);
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc[u].add(e1[u], dacc);
+      for (int u = 0; u < U; ++u) acc[u].add(c1[u * G], dacc);
       if (PROP == MPV_PROPOSAL_EXCHANGE) {
         const Sign mdacc = moved ? md : A::sign(0);
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc[u].add(e2[u], mdacc);
+        for (int u = 0; u < U; ++u) acc[u].add(c2[u * G], mdacc);
       }
       if (s + 1 == next_record) {
         next_record += thin;

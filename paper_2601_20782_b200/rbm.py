@@ -304,6 +304,20 @@ def _status_tensor(device):
     return torch.tensor([0, 2**63 - 1], dtype=torch.int64, device=device)
 
 
+def device_pack(bits, device):
+    """uint8 (B, N) host rows -> packed uint32 words on the device (int32 tensor):
+    one H2D copy of the rows and the mpv_pack_bits kernel."""
+    import torch
+
+    bits = np.ascontiguousarray(np.atleast_2d(bits), dtype=np.uint8)
+    B, N = bits.shape
+    rows = torch.from_numpy(bits).to(device, non_blocking=False)
+    packed = torch.empty((B, (N + 31) // 32), dtype=torch.int32, device=device)
+    if B:
+        nat.call("mpv_pack_bits", rows.data_ptr(), B, N, packed.data_ptr(), nat.stream_handle(device))
+    return packed
+
+
 class LogProbEvaluator:
     """Batch log-probability evaluator ``uint8[B,N] -> float64[B]`` (the
     reference evaluator protocol, sampler.py:49-53) backed by a device snapshot.
@@ -341,7 +355,7 @@ class LogProbEvaluator:
         bits = np.atleast_2d(np.asarray(bits, dtype=np.uint8))
         if bits.shape[1] != self.n_visible:
             raise ValueError(f"bit matrix has {bits.shape[1]} sites, ansatz has {self.n_visible}")
-        packed = torch.from_numpy(pack_bits(bits)).to(self.device)
+        packed = device_pack(bits, self.device)
         out, status = self.log_prob_packed(packed)
         out = out.cpu().numpy()
         _raise_nonfinite(status, bits, "log probability")
@@ -378,7 +392,7 @@ class LogPsiEvaluator:
         bits = np.atleast_2d(np.asarray(bits, dtype=np.uint8))
         if bits.shape[1] != self.snapshot.n_visible:
             raise ValueError(f"bit matrix has {bits.shape[1]} sites, ansatz has {self.snapshot.n_visible}")
-        packed = torch.from_numpy(pack_bits(bits)).to(self.device)
+        packed = device_pack(bits, self.device)
         re, im, status = self.log_psi_packed(packed)
         out = re.cpu().numpy() + 1j * im.cpu().numpy()
         _raise_nonfinite(status, bits, "log psi")
@@ -435,7 +449,7 @@ def log_psi_batch(params, bits, fmt: FloatFormat = F64, mode: RoundingMode = Rou
     if mode is RoundingMode.NATIVE:
         raise ValueError("NATIVE mode computes log p only (use log_prob_batch)")
     snap = DeviceSnapshot(params, fmt, mode, device)
-    packed = torch.from_numpy(pack_bits(bits)).to(snap.device)
+    packed = device_pack(bits, snap.device)
     B = bits.shape[0]
     lp = torch.empty(B, dtype=torch.float64, device=snap.device)
     re, im = torch.empty_like(lp), torch.empty_like(lp)

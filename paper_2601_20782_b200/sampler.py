@@ -257,7 +257,10 @@ class ChainEnsemble:
         if packed.shape[0]:
             nat.call("mpv_unpack_bits", packed.data_ptr(), packed.shape[0], self.n_sites, out.data_ptr(),
                      self._stream())
-        return out.cpu().numpy()
+        host = torch.empty(out.shape, dtype=torch.uint8, pin_memory=True)
+        host.copy_(out, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return host.numpy()
 
 
 def run_chains(n_chains, n_samples, burn_in_steps, thin_steps, seed, logprob, proposal: Proposal, n_sites):

@@ -86,7 +86,9 @@ def local_energies(spec, log_amplitude, bits) -> np.ndarray:
     bits = np.atleast_2d(np.asarray(bits, dtype=np.uint8))
     if bits.shape[1] != kern.N:
         raise ValueError(f"bit matrix has {bits.shape[1]} sites, lattice has {kern.N}")
-    packed = torch.from_numpy(pack_bits(bits)).to(kern.device)
+    from .rbm import device_pack
+
+    packed = device_pack(bits, kern.device)
     out, status = kern.packed(packed)
     eps = out.cpu().numpy()
     st = status.cpu().numpy()
