@@ -523,14 +523,14 @@ int mpv_local_energies(int N, int M, const double* a, const double* b, const dou
   const int TT = (T + 31) / 32 * 32;
   if (TT > 512 || M > 512) return fail(MPV_ERR_ARGS, "local_energies: more than 512 terms or hidden units");
   // staging buffer: a chunk of kRows C and S rows, or >= 8 W_t rows
-  const int stage = (int)std::max<size_t>((size_t)2 * kRows * T * sizeof(double2), (size_t)8 * M * sizeof(double2));
+  const int stage = (int)std::max<size_t>((size_t)2 * kRows * T * sizeof(double2), (size_t)kRows * M * sizeof(double2));
   auto smem_for = [&](int ng) {
     return (size_t)kEnergyST * ng * M * sizeof(double2) + (size_t)kEnergyST * ng * 32 * sizeof(uint32_t) +
            (size_t)((N + 3) / 4) * 4 * sizeof(uint32_t) + (size_t)kMaxSB * 16 * 2 * sizeof(double) +
-           2 * (size_t)stage + 2 * sizeof(uint64_t);
+           2 * (size_t)stage + 16 + (size_t)N * kMaxSB * sizeof(double);
   };
-  int NG = (2 * TT <= 512 && 2 * kEnergyST <= kMaxSB) ? 2 : 1;  // sample groups per block (table reuse)
-  if (smem_for(NG) > (size_t)max_smem_optin()) NG = 1;
+  int NG = std::max(1, std::min(kMaxSB / kEnergyST, 512 / TT));  // sample groups per block (table reuse)
+  while (NG > 1 && smem_for(NG) > (size_t)max_smem_optin()) --NG;
   const size_t smem = smem_for(NG);
   if (smem > (size_t)max_smem_optin()) return fail(MPV_ERR_ARGS, "local_energies: n_hidden too large");
   const int SB = kEnergyST * NG;

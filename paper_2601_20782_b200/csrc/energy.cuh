@@ -129,7 +129,7 @@ __device__ __forceinline__ void renorm(double2& p, int& e) {
 // shared by all SB samples (per-site sample masks), then tanh(theta) sits in
 // shared memory, read as a broadcast.  Sums over terms are reduced in a fixed
 // order (deterministic).
-constexpr int kRows = 8;   // C/S rows per staged chunk
+constexpr int kRows = 6;   // C/S rows per staged chunk
 constexpr int kMaxSB = 16;  // samples per block (NG * ST)
 
 // Bulk-async (TMA engine) staging of contiguous global chunks into a double
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(512) energy_kernel(const EnergyArgs a, int NG,
   const int M = a.M, T = a.n_terms, words = a.words, N = a.N;
   const int SB = ST * NG;
   const int TT = (T + 31) / 32 * 32;  // threads per group
-  double2* tt = reinterpret_cast<double2*>(smem_raw);                  // [SB][M]
+  double2* tt = reinterpret_cast<double2*>(smem_raw);                  // [M][SB]
   uint32_t* wsm = reinterpret_cast<uint32_t*>(tt + (size_t)SB * M);    // [SB][32]
   uint32_t* smask = wsm + SB * 32;                                     // [N], padded to 16 B
   double* red = reinterpret_cast<double*>(smask + ((N + 3) / 4) * 4);  // [SB][16 warps][2]
@@ -205,6 +205,12 @@ __global__ void __launch_bounds__(512) energy_kernel(const EnergyArgs a, int NG,
     uint32_t m = 0;
     for (int s = 0; s < SB; ++s) m |= ((wsm[s * 32 + (k >> 5)] >> (k & 31)) & 1u) << s;
     smask[k] = m;
+  }
+  // 0/1 multipliers x[k][s] as doubles (theta phase uses DFMA, no selects)
+  double* xk = reinterpret_cast<double*>(stage_base + 2 * (size_t)stage_bytes + 16);  // [N][kMaxSB]
+  for (int idx = tid; idx < N * kMaxSB; idx += blockDim.x) {
+    const int k = idx / kMaxSB, s2 = idx % kMaxSB;
+    xk[idx] = (s2 < SB) ? (double)((wsm[s2 * 32 + (k >> 5)] >> (k & 31)) & 1u) : 0.0;
   }
   // ---- phase 1: theta ----
   {
@@ -234,13 +240,13 @@ __global__ void __launch_bounds__(512) energy_kernel(const EnergyArgs a, int NG,
         const int k0 = c * rW, nr = min(rW, N - k0);
         for (int r = 0; r < nr; ++r) {
           const double2 w = wr[r * M];
-          const uint32_t m = smask[k0 + r];
+          const double* xr = xk + (k0 + r) * kMaxSB;
 #pragma unroll
-          for (int s = 0; s < kMaxSB; ++s)
-            if (m & (1u << s)) {
-              zr[s] += w.x;
-              zi[s] += w.y;
-            }
+          for (int s = 0; s < kMaxSB; ++s) {
+            const double x = xr[s];
+            zr[s] = fma(x, w.x, zr[s]);
+            zi[s] = fma(x, w.y, zi[s]);
+          }
         }
       }
       __syncthreads();
@@ -249,7 +255,7 @@ __global__ void __launch_bounds__(512) energy_kernel(const EnergyArgs a, int NG,
     if (i < M) {
 #pragma unroll
       for (int s = 0; s < kMaxSB; ++s)
-        if (s < SB) tt[s * M + i] = ctanh(make_double2(zr[s], zi[s]));
+        if (s < SB) tt[i * SB + s] = ctanh(make_double2(zr[s], zi[s]));
     }
   }
   __syncthreads();
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(512) energy_kernel(const EnergyArgs a, int NG,
       dd[j] = (a.ham == MPV_HAM_TFIM) ? (double)(1 - 2 * bit_of(s, p)) : (double)(bit_of(s, q) - bit_of(s, p));
     }
     slow = a.slow[t] != 0;
-    tg = tt + (size_t)g * ST * M;
+    tg = tt + g * ST;
   }
   // ---- phase 2: products over hidden units ----
   if (any_terms) {
@@ -302,14 +308,27 @@ __global__ void __launch_bounds__(512) energy_kernel(const EnergyArgs a, int NG,
         const double2* Cs = reinterpret_cast<const double2*>(st.buf[b]) + t;
         const double2* Ss = Cs + kRows * T;
         const int r0 = c * kRows, nr = min(kRows, M - r0);
-        for (int r = 0; r < nr; ++r) {
-          const double2 cv = Cs[r * T], sv = Ss[r * T];
-          const int i = r0 + r;
+        const double2* trow = tg + (size_t)r0 * SB;
+        if (nr == kRows) {
+          // full chunk: fully unrolled so the factor of row r+1 overlaps the
+          // product chain of row r
 #pragma unroll
-          for (int j = 0; j < ST; ++j) {
-            const double2 tv = tg[j * M + i];
-            const double2 ts = cmul(tv, sv);
-            P[j] = cmul(P[j], make_double2(fma(dd[j], ts.x, cv.x), fma(dd[j], ts.y, cv.y)));
+          for (int r = 0; r < kRows; ++r) {
+            const double2 cv = Cs[r * T], sv = Ss[r * T];
+#pragma unroll
+            for (int j = 0; j < ST; ++j) {
+              const double2 ts = cmul(trow[r * SB + j], sv);
+              P[j] = cmul(P[j], make_double2(fma(dd[j], ts.x, cv.x), fma(dd[j], ts.y, cv.y)));
+            }
+          }
+        } else {
+          for (int r = 0; r < nr; ++r, trow += SB) {
+            const double2 cv = Cs[r * T], sv = Ss[r * T];
+#pragma unroll
+            for (int j = 0; j < ST; ++j) {
+              const double2 ts = cmul(trow[j], sv);
+              P[j] = cmul(P[j], make_double2(fma(dd[j], ts.x, cv.x), fma(dd[j], ts.y, cv.y)));
+            }
           }
         }
         if ((c & 3) == 3) {
