@@ -257,8 +257,7 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "flushed between timed steps (256 MB write)", "parallelism": f"chains sharded x{world}"},
         "sampling_sweep_ms": sweep_avg,
         "sampling_chain_steps_per_s": collect_steps * world / (sweep_avg / 1e3),
-        "energy_check": {"mean_energy": float(np.mean(energies)), "acceptance": float(np.mean(accs)) /
-                         (chain_steps_per_step(C) * world - REBURN_SWEEPS * N_SITES * C * world + REBURN_SWEEPS * N_SITES * C * world)},
+        "energy_check": {"mean_energy": float(np.mean(energies)), "acceptance": None},
         "roofline": {"bound": "sfu", "kernel": "sweep_kernel (collect launch)", "achieved": achieved_mufu / 1e12,
                      "peak": mufu_peak / 1e12, "unit": "Tmufu-op/s", "frac": achieved_mufu / mufu_peak,
                      "traffic": None, "algorithmic": "3 MUFU ops (ex2, cos, lg2) per hidden unit per chain-step, M=200",
@@ -271,6 +270,11 @@ def run_ours(args, rank, world, local_rank):
         "north_star_shape": ns,
     }
     out["energy_check"]["acceptance"] = float(np.mean(accs)) / (C * world * (REBURN_SWEEPS * N_SITES + SAMPLES_PER_CHAIN * (N_SITES + 1)))
+    tr = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+    if os.path.exists(tr):
+        with open(tr) as f:
+            out["roofline"]["traffic"] = json.load(f)["sweep_kernel"]["dram_bytes_per_launch"]
+            out["roofline"]["traffic_unit"] = "bytes/launch (ncu --set full, profiles/r01)"
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, sample_chains=C)
     return out
