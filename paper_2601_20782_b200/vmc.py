@@ -109,3 +109,255 @@ def mc_error(values) -> float:
     if values.size < 2:
         raise DegenerateInputError("need >= 2 values")
     return float(np.sqrt(values.var(ddof=1) / values.size))
+
+
+# ---------------------------------------------------------------------------
+# Training loop: two-copy mixed-precision SR (mirror of the reference
+# vmc.py:145-229, 320-639).  Sampling and local energies run in the CUDA
+# library; the f64 statistics O, F, S and the SR solve stay in f64 on the
+# device (torch / cuBLAS / cuSOLVER library calls: plain GEMM/Cholesky).
+# ---------------------------------------------------------------------------
+import time  # noqa: E402
+from dataclasses import dataclass, field  # noqa: E402
+from fractions import Fraction  # noqa: E402
+
+from .errors import SolverError  # noqa: E402
+from .precision import F64, FloatFormat, RoundingMode  # noqa: E402
+
+
+def _t(x, device):
+    import torch
+
+    return torch.as_tensor(np.asarray(x), device=device)
+
+
+def grad_log_psi_device(params, bits_u8, device=None):
+    """O(x) = d log psi / d theta (rbm.py:307-325) for a (U, N) uint8 device
+    tensor: columns a, b, W row-major; complex128 [U, P] on the device."""
+    import torch
+
+    dev = bits_u8.device
+    x = bits_u8.to(torch.float64).to(torch.complex128)
+    w = _t(params.w, dev)
+    b = _t(params.b, dev)
+    th = x @ w.T + b[None, :]
+    t = torch.tanh(th)
+    U, N = x.shape
+    M = b.numel()
+    out = torch.empty((U, N + M + M * N), dtype=torch.complex128, device=dev)
+    out[:, :N] = x
+    out[:, N:N + M] = t
+    out[:, N + M:] = (t[:, :, None] * x[:, None, :]).reshape(U, M * N)
+    return out
+
+
+def forces(*, o, eps, weights=None):
+    """F_k = E[conj(O_k) eps] - E[conj(O_k)] E[eps] (vmc.py:145-165), device tensors."""
+    if o.shape[0] != eps.numel() or eps.numel() == 0:
+        raise DegenerateInputError("need at least one (O, eps) pair")
+    oc = o.conj()
+    if weights is None:
+        if eps.numel() < 2:
+            raise DegenerateInputError("need >= 2 samples")
+        return oc.T @ eps / eps.numel() - oc.mean(dim=0) * eps.mean()
+    w = weights.to(oc.dtype)
+    return (oc * w[:, None]).T @ eps - (w @ oc) * (w @ eps)
+
+
+def s_matrix(*, o, weights=None):
+    """S = E[conj(O) O^T] - E[conj O] E[O^T], Hermitised (vmc.py:168-188)."""
+    if o.shape[0] == 0:
+        raise DegenerateInputError("empty sample set")
+    if weights is None:
+        c = o - o.mean(dim=0, keepdim=True)
+        s = c.conj().T @ c / o.shape[0]
+    else:
+        w = weights.to(o.dtype)
+        mean = w @ o
+        c = o - mean[None, :]
+        s = c.conj().T @ (c * w[:, None])
+    return 0.5 * (s + s.conj().T)
+
+
+@dataclass(frozen=True)
+class SrUpdate:
+    g: object
+    kappa: float
+    residual: float
+    lambda_shift: float
+    eta: float
+
+
+def sr_step(f, s, lambda_shift: float, eta: float, compute_kappa: bool = True) -> SrUpdate:
+    """(S + lambda I) g = F by Cholesky + one refinement pass (vmc.py:202-229)."""
+    import torch
+
+    if lambda_shift < 0:
+        raise ValueError("lambda must be >= 0")
+    if eta <= 0:
+        raise ValueError("eta must be > 0")
+    shifted = s + lambda_shift * torch.eye(s.shape[0], dtype=s.dtype, device=s.device)
+    L, info = torch.linalg.cholesky_ex(shifted)
+    if int(info) != 0:
+        smallest = float(torch.linalg.eigvalsh(shifted)[0])
+        raise SolverError(f"shifted S is not positive definite (smallest eigenvalue {smallest:.3e})")
+    g = torch.cholesky_solve(f[:, None], L)[:, 0]
+    g = g + torch.cholesky_solve((f - shifted @ g)[:, None], L)[:, 0]
+    kappa = float("nan")
+    if compute_kappa:
+        ev = torch.linalg.eigvalsh(shifted)
+        kappa = float(ev[-1] / ev[0]) if float(ev[0]) > 0 else float("inf")
+    fn = float(torch.linalg.norm(f))
+    residual = float(torch.linalg.norm(shifted @ g - f)) / fn if fn > 0 else 0.0
+    if fn > 0 and residual > 1e-10:
+        raise SolverError(f"SR solve residual {residual:.3e} exceeds 1e-10")
+    return SrUpdate(g, kappa, residual, lambda_shift, eta)
+
+
+@dataclass
+class TrainConfig:
+    """Reference TrainConfig (vmc.py:320-351) plus compute_kappa (the eigvalsh of
+    S + lambda I is O(P^3); large-P runs may switch it off)."""
+
+    hamiltonian: object
+    alpha: object = 1
+    n_steps: int = 500
+    n_samples: int = 4096
+    eta: float = 0.01
+    lambda_shift: float = 1e-3
+    seed: int = 0
+    sampling_format: FloatFormat = F64
+    rounding_mode: RoundingMode = RoundingMode.PER_OPERATION
+    sampling_mode: str = "mcmc"
+    proposal: object = None
+    n_chains: int | None = None
+    burn_in_sweeps: int | None = None
+    reburn_sweeps: int = 2
+    thin_sweeps: int = 1
+    log_every: int = 1
+    init_scale: float = 0.01
+    track_forces: bool = False
+    track_timings: bool = False
+    reference_energy: float | None = None
+    compute_kappa: bool = True
+
+    def __post_init__(self):
+        if self.n_steps < 1 or self.n_samples < 2:
+            raise ValueError("n_steps and n_samples must be positive")
+        if self.sampling_mode not in ("mcmc", "exact"):
+            raise ValueError(f"unknown sampling mode {self.sampling_mode!r}")
+        if self.proposal is None:
+            from .sampler import Proposal
+
+            self.proposal = Proposal("flip")
+
+
+@dataclass
+class TrainResult:
+    records: list
+    params: object
+    force_history: list = field(default_factory=list)
+
+
+def train(config: TrainConfig, device=None) -> TrainResult:
+    """Two-copy mixed-precision SR training (vmc.py:472-639) on the device."""
+    import torch
+
+    from . import rbm
+    from .bounds import pinsker_tv_bound, theorem3_gaussian_bound
+    from .lattice import enumerate_bits, unpack_bits
+    from .rng import derive_key
+    from .sampler import ChainEnsemble, default_chain_count
+
+    nat.require_cuda()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    spec = config.hamiltonian
+    n = spec.lattice.n_sites
+    params = rbm.random_parameters(n, Fraction(config.alpha), derive_key(config.seed, "init"), config.init_scale)
+    n_chains = config.n_chains or default_chain_count(config.n_samples)
+    burn_in = config.burn_in_sweeps if config.burn_in_sweeps is not None else 10 * n
+    exact_mode = config.sampling_mode == "exact"
+    words = (n + 31) // 32
+    if exact_mode:
+        from .lattice import pack_bits
+
+        all_u8 = enumerate_bits(n)
+        all_packed = torch.from_numpy(pack_bits(all_u8)).to(dev)
+    else:
+        base, extra = divmod(config.n_samples, n_chains)
+        counts = np.array([base + (1 if c < extra else 0) for c in range(n_chains)])
+        chain_ids = torch.as_tensor(np.repeat(np.arange(n_chains), counts), device=dev)
+        per_chain = torch.as_tensor(counts, device=dev, dtype=torch.float64)
+    ensemble = None
+    records, force_history = [], []
+    for step in range(config.n_steps):
+        torch.cuda.synchronize(dev)
+        t_sample = time.perf_counter()
+        if exact_mode:
+            lp = rbm.LogProbEvaluator(params, F64, RoundingMode.PER_OPERATION, dev).log_prob_packed(all_packed)[0]
+            weights = torch.softmax(lp, dim=0)
+            uniq = all_packed
+            est_w = weights
+            acceptance = float("nan")
+            ev = None
+        else:
+            ev = rbm.log_prob_evaluator(params, config.sampling_format, config.rounding_mode, dev)
+            if ensemble is None:
+                ensemble = ChainEnsemble(n_chains, n, config.proposal, ev, derive_key(config.seed, "chains"))
+                ensemble.run_sweeps(burn_in)
+            else:
+                ensemble.set_evaluator(ev)
+                ensemble.run_sweeps(config.reburn_sweeps)
+            ensemble.reset_counters()
+            packed = ensemble.collect_packed(config.n_samples, config.thin_sweeps * n + 1)
+            acceptance = ensemble.acceptance_rate
+            # np.unique(..., axis=0) over the sample stream (vmc.py:560-563)
+            uniq, inverse, cnt = torch.unique(packed, dim=0, return_inverse=True, return_counts=True)
+            est_w = cnt.to(torch.float64) / config.n_samples
+        torch.cuda.synchronize(dev)
+        t_update = time.perf_counter()
+        psi = rbm.log_psi_evaluator(params, dev)
+        eps_ri, status = _energy_kernel(spec, psi).packed(uniq)
+        if int(status[0]) != 0:
+            raise EvaluationFailureError("non-finite local energy", context={"step": step})
+        eps = torch.complex(eps_ri[:, 0], eps_ri[:, 1])
+        u8 = torch.empty((uniq.shape[0], n), dtype=torch.uint8, device=dev)
+        nat.call("mpv_unpack_bits", uniq.data_ptr(), uniq.shape[0], n, u8.data_ptr(), nat.stream_handle(dev))
+        o = grad_log_psi_device(params, u8)
+        f = forces(o=o, eps=eps, weights=est_w)
+        s = s_matrix(o=o, weights=est_w)
+        update = sr_step(f, s, config.lambda_shift, config.eta, config.compute_kappa)
+        theta = params.flatten() - config.eta * update.g.cpu().numpy()
+        new_params = rbm.RbmParameters.from_flat(theta, params.n_visible, params.n_hidden)
+        energy = float((est_w.to(eps.dtype) @ eps).real)
+        if exact_mode:
+            err = 0.0
+        else:
+            stream = eps.real[inverse]
+            if n_chains > 1:
+                sums = torch.zeros(n_chains, dtype=torch.float64, device=dev).index_add_(0, chain_ids, stream)
+                err = mc_error((sums / per_chain).cpu().numpy())
+            else:
+                err = mc_error(stream.cpu().numpy())
+        if config.track_forces:
+            force_history.append(f.cpu().numpy())
+        if step % config.log_every == 0 or step == config.n_steps - 1:
+            if exact_mode or config.sampling_format.name == "f64":
+                sigma_hat = 0.0
+            else:
+                lp_fmt, _ = ev.log_prob_packed(uniq)
+                lp64 = rbm.LogProbEvaluator(params, F64, RoundingMode.PER_OPERATION, dev).log_prob_packed(uniq)[0]
+                delta = lp_fmt - lp64
+                sigma_hat = float(delta.std()) if delta.numel() > 1 else 0.0
+            record = {"step": step, "energy": energy, "mc_error": err, "acceptance": acceptance,
+                      "sigma_hat": sigma_hat, "bound_pinsker": pinsker_tv_bound(sigma_hat),
+                      "bound_theorem3": theorem3_gaussian_bound(sigma_hat, 0.0, 0.0), "kappa": update.kappa}
+            if config.track_timings:
+                torch.cuda.synchronize(dev)
+                record["sampling_seconds"] = t_update - t_sample
+                record["update_seconds"] = time.perf_counter() - t_update
+            if config.reference_energy is not None:
+                record["rel_error"] = abs(energy - config.reference_energy) / abs(config.reference_energy)
+            records.append(record)
+        params = new_params
+    return TrainResult(records, params, force_history)

@@ -167,7 +167,34 @@ def gen_energy():
     save("energy.npz", **arrays)
 
 
+def gen_train():
+    """Reference training runs (vmc.py:472-639) for tests/test_gpu_train.py."""
+    from mpvmc.precision import F32
+    from mpvmc.sampler import Proposal
+
+    arrays = {}
+    runs = {
+        "exact6": dict(hamiltonian=TfimSpec(LatticeSpec.chain(6), 1.0, 1.0), n_steps=30, sampling_mode="exact",
+                       eta=0.05, lambda_shift=1e-3, seed=2),
+        "mcmc8_f32": dict(hamiltonian=TfimSpec(LatticeSpec.chain(8), 1.0, 1.0), n_steps=6, n_samples=256,
+                          n_chains=64, eta=0.02, seed=3, sampling_format=F32),
+        "mcmc8_f64": dict(hamiltonian=TfimSpec(LatticeSpec.chain(8), 1.0, 1.0), n_steps=6, n_samples=256,
+                          n_chains=64, eta=0.02, seed=3),
+        "heis6_f16": dict(hamiltonian=HeisenbergSpec(LatticeSpec.chain(6, periodic=True), 1.0), n_steps=4,
+                          n_samples=128, n_chains=32, eta=0.02, seed=4, sampling_format=F16,
+                          proposal=Proposal("exchange", 3)),
+    }
+    keys = ("energy", "mc_error", "acceptance", "sigma_hat", "bound_pinsker", "bound_theorem3", "kappa")
+    for tag, cfg in runs.items():
+        res = vmc.train(vmc.TrainConfig(**cfg))
+        for k in keys:
+            arrays[f"{tag}_{k}"] = np.array([r[k] for r in res.records], dtype=np.float64)
+        arrays[f"{tag}_w"] = res.params.w
+    save("train.npz", **arrays)
+
+
 if __name__ == "__main__":
+    gen_train()
     gen_rng()
     gen_forward()
     gen_chains()
