@@ -188,7 +188,8 @@ def run_ours(args, rank, world, local_rank):
     # ---- end-to-end through the public API (host buffers, copies inside) ----
     e2e_ms = 0.0
     h2d = d2h = 0
-    for _ in range(max(1, min(args.steps, 3))):
+    n_e2e = max(1, min(args.steps, 3))
+    for it in range(n_e2e + 1):  # first iteration is an untimed warm-up
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
@@ -205,11 +206,12 @@ def run_ours(args, rank, world, local_rank):
         rate = ens.acceptance_rate
         t1.record(stream)
         torch.cuda.synchronize()
-        e2e_ms += t0.elapsed_time(t1)
+        if it > 0:
+            e2e_ms += t0.elapsed_time(t1)
         snap = ev_e2e.snapshot
         h2d = snap._table.numel() + snap._bias.numel() + snap._vis_im.numel() * 8 + samples.shape[0] * ens.words * 4
         d2h = samples.nbytes + eps.nbytes + 3 * 16  # samples, eps, status words
-    e2e_ms /= max(1, min(args.steps, 3))
+    e2e_ms /= n_e2e
     if dist is not None:
         t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -230,6 +232,21 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         ns = {"config": "rbm_a1_tfim10x10_c16384_f16native", "chain_steps_per_s":
               C * 10 * (N_SITES + 1) / (a0.elapsed_time(a1) / 1e3), "variant": ev1.snapshot.label}
+
+    # ---- VMC iteration time at BASELINE configs[0] (N=20 open TFIM chain, alpha=1,
+    # 4,096 samples, 1,024 chains, f16 sampling), reference: vmc.py:472-639 ----
+    vmc_iter = None
+    if rank == 0 and not args.no_vmc:
+        from paper_2601_20782_b200.lattice import LatticeSpec as _LS
+
+        cfg = vmc.TrainConfig(TfimSpec(_LS.chain(20), 1.0, 1.0), alpha=1, n_steps=10, n_samples=4096, n_chains=1024,
+                              sampling_format=F16, rounding_mode=RoundingMode.NATIVE, track_timings=True)
+        recs = vmc.train(cfg).records[2:]
+        vmc_iter = {"config": "tfim_chain20_open_h1_a1_s4096_c1024_f16native",
+                    "sampling_ms": 1e3 * float(np.median([r["sampling_seconds"] for r in recs])),
+                    "update_ms": 1e3 * float(np.median([r["update_seconds"] for r in recs])),
+                    "energy_last": recs[-1]["energy"]}
+        vmc_iter["iteration_ms"] = vmc_iter["sampling_ms"] + vmc_iter["update_ms"]
 
     steps_per_step = chain_steps_per_step(C) * world
     value = steps_per_step / (ms / 1e3)
@@ -268,6 +285,7 @@ def run_ours(args, rank, world, local_rank):
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "api": "log_prob_evaluator + ChainEnsemble.set_evaluator/run_sweeps/collect + vmc.local_energies"},
         "north_star_shape": ns,
+        "vmc_iteration": vmc_iter,
     }
     out["energy_check"]["acceptance"] = float(np.mean(accs)) / (C * world * (REBURN_SWEEPS * N_SITES + SAMPLES_PER_CHAIN * (N_SITES + 1)))
     tr = os.path.join(ROOT, "profiles", "r01", "traffic.json")
@@ -359,6 +377,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-vmc", action="store_true", help="skip the VMC iteration-time measurement")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

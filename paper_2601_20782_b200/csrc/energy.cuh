@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(512) energy_kernel(const EnergyArgs a, int NG,
       const int b = c & 1;
       st.wait(b);
       if (i < M) {
-        const double2* wr = reinterpret_cast<const double2*>(st.buf[b]) + i;
+        const double2* wr = reinterpret_cast<const double2*>(stage_base + (size_t)b * stage_bytes) + i;
         const int k0 = c * rW, nr = min(rW, N - k0);
         for (int r = 0; r < nr; ++r) {
           const double2 w = wr[r * M];
@@ -305,31 +305,24 @@ __global__ void __launch_bounds__(512) energy_kernel(const EnergyArgs a, int NG,
       const int b = c & 1;
       st.wait(b);
       if (active && !slow) {
-        const double2* Cs = reinterpret_cast<const double2*>(st.buf[b]) + t;
+        // shared-space pointers derived from the dynamic smem array (LDS, not generic LD)
+        const double2* Cs = reinterpret_cast<const double2*>(stage_base + (size_t)b * stage_bytes) + t;
         const double2* Ss = Cs + kRows * T;
         const int r0 = c * kRows, nr = min(kRows, M - r0);
         const double2* trow = tg + (size_t)r0 * SB;
-        if (nr == kRows) {
-          // full chunk: fully unrolled so the factor of row r+1 overlaps the
-          // product chain of row r
+        for (int r = 0; r < nr; ++r, trow += SB) {
+          const double2 cv = Cs[r * T], sv = Ss[r * T];
+          // three independent phases over the ST samples: ts = tanh*S, f = C + d ts, P *= f
+          double2 f[ST];
 #pragma unroll
-          for (int r = 0; r < kRows; ++r) {
-            const double2 cv = Cs[r * T], sv = Ss[r * T];
-#pragma unroll
-            for (int j = 0; j < ST; ++j) {
-              const double2 ts = cmul(trow[r * SB + j], sv);
-              P[j] = cmul(P[j], make_double2(fma(dd[j], ts.x, cv.x), fma(dd[j], ts.y, cv.y)));
-            }
+          for (int j = 0; j < ST; ++j) {
+            const double2 tv = trow[j];
+            f[j] = make_double2(fma(tv.x, sv.x, -tv.y * sv.y), fma(tv.x, sv.y, tv.y * sv.x));
           }
-        } else {
-          for (int r = 0; r < nr; ++r, trow += SB) {
-            const double2 cv = Cs[r * T], sv = Ss[r * T];
 #pragma unroll
-            for (int j = 0; j < ST; ++j) {
-              const double2 ts = cmul(trow[j], sv);
-              P[j] = cmul(P[j], make_double2(fma(dd[j], ts.x, cv.x), fma(dd[j], ts.y, cv.y)));
-            }
-          }
+          for (int j = 0; j < ST; ++j) f[j] = make_double2(fma(dd[j], f[j].x, cv.x), fma(dd[j], f[j].y, cv.y));
+#pragma unroll
+          for (int j = 0; j < ST; ++j) P[j] = cmul(P[j], f[j]);
         }
         if ((c & 3) == 3) {
 #pragma unroll
