@@ -233,6 +233,41 @@ def run_ours(args, rank, world, local_rank):
         ns = {"config": "rbm_a1_tfim10x10_c16384_f16native", "chain_steps_per_s":
               C * 10 * (N_SITES + 1) / (a0.elapsed_time(a1) / 1e3), "variant": ev1.snapshot.label}
 
+    # ---- sampling-only rates: precision sweep at the config-2 shape, BASELINE
+    # configs[2] (Heisenberg 10x10, alpha=4, exchange Sz=0, bf16) and configs[4]
+    # (16x16 TFIM, alpha=1) ----
+    extra = None
+    if rank == 0 and not args.no_extras:
+        from paper_2601_20782_b200 import BF16, F32, F64
+
+        def rate(n, alpha, fmt, mode, prop, chains=C, steps=None, scale=INIT_SCALE):
+            p = rbm.random_parameters(n, alpha, derive_key(0, "init"), scale)
+            e = rbm.log_prob_evaluator(p, fmt, mode)
+            en = sampler.ChainEnsemble(chains, n, prop, e, derive_key(0, "chains"))
+            en.run_steps(4 * n)
+            torch.cuda.synchronize()
+            k = steps or 4 * (n + 1)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            en.run_steps(k, check=False)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            return {"chain_steps_per_s": chains * k / (a0.elapsed_time(a1) / 1e3), "variant": e.snapshot.label}
+
+        flip = sampler.Proposal("flip")
+        extra = {"precision_sweep_a2_10x10": {
+            "f16": rate(N_SITES, ALPHA, F16, RoundingMode.NATIVE, flip),
+            "bf16": rate(N_SITES, ALPHA, BF16, RoundingMode.NATIVE, flip),
+            "f32": rate(N_SITES, ALPHA, F32, RoundingMode.NATIVE, flip),
+            "f64": rate(N_SITES, ALPHA, F64, RoundingMode.PER_OPERATION, flip),
+            "f16_per_operation_reference_arithmetic": rate(N_SITES, ALPHA, F16, RoundingMode.PER_OPERATION, flip,
+                                                           steps=40)},
+            "peaked_state_scale0.5_f16": rate(N_SITES, ALPHA, F16, RoundingMode.NATIVE, flip, scale=0.5),
+            "config3_heis10x10_a4_exchange_bf16": rate(N_SITES, 4, BF16, RoundingMode.NATIVE,
+                                                        sampler.Proposal("exchange", N_SITES // 2)),
+            "config5_tfim16x16_a1_f16": rate(256, 1, F16, RoundingMode.NATIVE, flip, chains=4096 * 4),
+        }
+
     # ---- VMC iteration time at BASELINE configs[0] (N=20 open TFIM chain, alpha=1,
     # 4,096 samples, 1,024 chains, f16 sampling), reference: vmc.py:472-639 ----
     vmc_iter = None
@@ -286,6 +321,7 @@ def run_ours(args, rank, world, local_rank):
                 "api": "log_prob_evaluator + ChainEnsemble.set_evaluator/run_sweeps/collect + vmc.local_energies"},
         "north_star_shape": ns,
         "vmc_iteration": vmc_iter,
+        "sampling_rates": extra,
     }
     out["energy_check"]["acceptance"] = float(np.mean(accs)) / (C * world * (REBURN_SWEEPS * N_SITES + SAMPLES_PER_CHAIN * (N_SITES + 1)))
     tr = os.path.join(ROOT, "profiles", "r01", "traffic.json")
@@ -378,6 +414,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-vmc", action="store_true", help="skip the VMC iteration-time measurement")
+    ap.add_argument("--no-extras", action="store_true", help="skip the per-format / per-config sampling rates")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

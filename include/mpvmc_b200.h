@@ -42,6 +42,7 @@ extern "C" {
 #define MPV_ACC_X1 0  /* one f32 accumulator per component, exact by host planner check */
 #define MPV_ACC_X2 1  /* hi/lo f32 accumulators on a fixed split grid, exact */
 #define MPV_ACC_F64 2 /* f64 accumulators */
+#define MPV_ACC_XI 3  /* int32 accumulators in units of the snapshot quantum (exact) */
 
 /* proposals (ref: sampler.py:24-39) */
 #define MPV_PROPOSAL_FLIP 0
@@ -60,6 +61,7 @@ extern "C" {
  *   X1, PER_OP      fmt pair (re,im): 4 B f16/bf16, 8 B f32      float (a_re)
  *   X2              two fmt pairs (hi, lo)                       float2 (hi, lo)
  *   F64             double2 (re, im)                             double
+ *   XI              int2 (re, im) = value / quantum              int
  * `vis_im` (double[N], a_im) is only read by mpv_snapshot_forward (log psi).
  * For the fused sweep `vis` must sit at table + round_up(N*hidden_pad*entry, 16):
  * [table | vis] is staged into shared memory with one bulk copy.
@@ -72,6 +74,7 @@ typedef struct {
   const void* bias;
   const void* vis;
   const double* vis_im;
+  double quantum; /* XI: table integers are multiples of this power of two */
 } mpv_snapshot;
 
 /* Chain state of one shard (device pointers; ref: sampler.py:55-65 state). */

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libm
 MPV_OK, MPV_ERR_ARGS, MPV_ERR_CUDA, MPV_ERR_NONFINITE = 0, 1, 2, 3
 FMT_F64, FMT_F32, FMT_F16, FMT_BF16 = 0, 1, 2, 3
 MODE_NATIVE, MODE_PER_OPERATION, MODE_STORAGE_ONLY = 0, 1, 2
-ACC_X1, ACC_X2, ACC_F64 = 0, 1, 2
+ACC_X1, ACC_X2, ACC_F64, ACC_XI = 0, 1, 2, 3
 PROPOSAL_FLIP, PROPOSAL_EXCHANGE = 0, 1
 HAM_TFIM, HAM_HEISENBERG = 0, 1
 
@@ -31,7 +31,7 @@ class Snapshot(ctypes.Structure):
         ("n_visible", _i32), ("n_hidden", _i32), ("hidden_pad", _i32),
         ("fmt", _i32), ("mode", _i32), ("variant", _i32),
         ("lanes_per_chain", _i32), ("units_per_lane", _i32),
-        ("table", _vp), ("bias", _vp), ("vis", _vp), ("vis_im", _vp),
+        ("table", _vp), ("bias", _vp), ("vis", _vp), ("vis_im", _vp), ("quantum", _f64),
     ]
 
 

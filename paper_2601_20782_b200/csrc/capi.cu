@@ -12,8 +12,8 @@
 
 namespace mpv {
 #define MPV_DECL(f, v) void* sweep_kernel_ptr_##f##_##v(int G, int U, int prop, int smem);
-MPV_DECL(f16, x1) MPV_DECL(f16, x2) MPV_DECL(f16, f64)
-MPV_DECL(bf16, x1) MPV_DECL(bf16, x2) MPV_DECL(bf16, f64)
+MPV_DECL(f16, x1) MPV_DECL(f16, x2) MPV_DECL(f16, f64) MPV_DECL(f16, xi)
+MPV_DECL(bf16, x1) MPV_DECL(bf16, x2) MPV_DECL(bf16, f64) MPV_DECL(bf16, xi)
 MPV_DECL(f32, x1) MPV_DECL(f32, x2) MPV_DECL(f32, f64)
 MPV_DECL(f64, f64)
 #undef MPV_DECL
@@ -23,10 +23,12 @@ void* sweep_kernel_ptr(int fmt, int variant, int G, int U, int prop, int smem) {
     case MPV_FMT_F16:
       return variant == MPV_ACC_X1 ? sweep_kernel_ptr_f16_x1(G, U, prop, smem)
            : variant == MPV_ACC_X2 ? sweep_kernel_ptr_f16_x2(G, U, prop, smem)
+           : variant == MPV_ACC_XI ? sweep_kernel_ptr_f16_xi(G, U, prop, smem)
                                    : sweep_kernel_ptr_f16_f64(G, U, prop, smem);
     case MPV_FMT_BF16:
       return variant == MPV_ACC_X1 ? sweep_kernel_ptr_bf16_x1(G, U, prop, smem)
            : variant == MPV_ACC_X2 ? sweep_kernel_ptr_bf16_x2(G, U, prop, smem)
+           : variant == MPV_ACC_XI ? sweep_kernel_ptr_bf16_xi(G, U, prop, smem)
                                    : sweep_kernel_ptr_bf16_f64(G, U, prop, smem);
     case MPV_FMT_F32:
       return variant == MPV_ACC_X1 ? sweep_kernel_ptr_f32_x1(G, U, prop, smem)
@@ -85,15 +87,18 @@ constexpr int MAX_WORDS_INIT = 32;  // n_sites <= 1024
 
 size_t entry_bytes(int fmt, int variant) {
   if (variant == MPV_ACC_F64 || fmt == MPV_FMT_F64) return 16;
+  if (variant == MPV_ACC_XI) return 8;
   const size_t pair = (fmt == MPV_FMT_F32) ? 8 : 4;
   return variant == MPV_ACC_X2 ? 2 * pair : pair;
 }
 size_t acc_bytes(int fmt, int variant) {  // sizeof(Acc<FMT, VAR>)
   if (variant == MPV_ACC_F64 || fmt == MPV_FMT_F64) return 16;
+  if (variant == MPV_ACC_XI) return 8;
   return variant == MPV_ACC_X2 ? 16 : 8;
 }
 size_t vis_bytes(int fmt, int variant) {
   if (variant == MPV_ACC_F64 || fmt == MPV_FMT_F64) return 8;
+  if (variant == MPV_ACC_XI) return 4;
   return variant == MPV_ACC_X2 ? 8 : 4;
 }
 
@@ -217,6 +222,7 @@ const char* mpv_version(void) { return "mpvmc_b200 0.1.0 (sm_100a)"; }
 // theta + the kept column entry (3 for X1 f16/bf16, 4-6 for X1 f32 / X2, 8 for F64).
 static int units_cap(int fmt, int variant) {
   if (fmt == MPV_FMT_F64 || variant == MPV_ACC_F64) return 13;
+  if (variant == MPV_ACC_XI) return 25;
   if (variant == MPV_ACC_X1) return fmt == MPV_FMT_F32 ? 16 : 25;
   return fmt == MPV_FMT_F32 ? 13 : 16;
 }
@@ -356,7 +362,11 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
   a.row0 = row0;
   a.seg_len = seg_len; a.n_groups = n_groups; a.n_items = n_groups * n_segments;
   a.queue = queue; a.done = done; a.save = save; a.vis_save = vsave;
-  const int threads = 256;
+  a.xi_scale = (float)snap->quantum;
+  if (variant == MPV_ACC_XI && !(snap->quantum > 0.0)) return fail(MPV_ERR_ARGS, "mh_sweep: XI needs quantum > 0");
+  // flip kernels: 512-thread blocks (one staged table per 16 warps, <= 128 regs);
+  // exchange kernels need more registers: 256-thread blocks
+  const int threads = (proposal == MPV_PROPOSAL_FLIP) ? 512 : 256;
   const size_t smem = use_smem ? tbytes16 : 0;
   if (int rc = ensure_smem(fn, smem)) return rc;
   int per_sm = 0;

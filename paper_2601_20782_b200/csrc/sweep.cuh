@@ -37,6 +37,7 @@ struct SweepArgs {
   int64_t sample_base, sample_extra, round_offset, row0;
   // persistent work queue: items (segment, chain group), segment-major
   int64_t seg_len, n_groups, n_items;
+  float xi_scale;     // quantum q of the XI variant (theta = integer * q)
   int* queue;         // [1], zero at launch
   int* done;          // [n_groups] segments finished, zero at launch
   float* save;        // [n_groups][save_words][32] theta between segments
@@ -133,11 +134,11 @@ template <int FMT> struct Acc<FMT, MPV_ACC_X1> {
     im = H::fma_hi(e, d, im);
   }
   // theta' for a one-column move
-  __device__ __forceinline__ void prop1(Entry e, Sign d, float& xr, float& xi) const {
+  __device__ __forceinline__ void prop1(Entry e, Sign d, float sc, float& xr, float& xi) const {
     xr = H::fma_lo(e, d, re);
     xi = H::fma_hi(e, d, im);
   }
-  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float& xr,
+  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float sc, float& xr,
                                         float& xi) const {
     xr = H::fma_lo(e1, d, H::fma_lo(e2, md, re));
     xi = H::fma_hi(e1, d, H::fma_hi(e2, md, im));
@@ -161,14 +162,36 @@ template <int FMT> struct Acc<FMT, MPV_ACC_X2> {
     hr = H::fma_lo(e.x, d, hr); hi_ = H::fma_hi(e.x, d, hi_);
     lr = H::fma_lo(e.y, d, lr); li = H::fma_hi(e.y, d, li);
   }
-  __device__ __forceinline__ void prop1(Entry e, Sign d, float& xr, float& xi) const {
+  __device__ __forceinline__ void prop1(Entry e, Sign d, float sc, float& xr, float& xi) const {
     xr = H::fma_lo(e.x, d, hr) + H::fma_lo(e.y, d, lr);
     xi = H::fma_hi(e.x, d, hi_) + H::fma_hi(e.y, d, li);
   }
-  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float& xr,
+  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float sc, float& xr,
                                         float& xi) const {
     xr = H::fma_lo(e1.x, d, H::fma_lo(e2.x, md, hr)) + H::fma_lo(e1.y, d, H::fma_lo(e2.y, md, lr));
     xi = H::fma_hi(e1.x, d, H::fma_hi(e2.x, md, hi_)) + H::fma_hi(e1.y, d, H::fma_hi(e2.y, md, li));
+  }
+};
+
+// ---- XI, f16/bf16: theta as an exact int32 multiple of the snapshot quantum q
+// (host planner: B/q < 2^31); one IMAD per component, the f32 value is the
+// correctly rounded I2F of the integer times q (a power of two: exact).
+template <int FMT> struct Acc<FMT, MPV_ACC_XI> {
+  using Entry = int2;
+  using Vis = int;
+  using Sign = int;
+  int re, im;
+  __device__ __forceinline__ static Sign sign(int d) { return d; }
+  __device__ __forceinline__ void init(Entry b) { re = b.x; im = b.y; }
+  __device__ __forceinline__ void add(Entry e, Sign d) { re += d * e.x; im += d * e.y; }
+  __device__ __forceinline__ void prop1(Entry e, Sign d, float sc, float& xr, float& xi) const {
+    xr = __int2float_rn(re + d * e.x) * sc;
+    xi = __int2float_rn(im + d * e.y) * sc;
+  }
+  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float sc, float& xr,
+                                        float& xi) const {
+    xr = __int2float_rn(re + d * e1.x + md * e2.x) * sc;
+    xi = __int2float_rn(im + d * e1.y + md * e2.y) * sc;
   }
 };
 
@@ -181,11 +204,11 @@ template <> struct Acc<MPV_FMT_F32, MPV_ACC_X1> {
   __device__ __forceinline__ static Sign sign(int d) { return (float)d; }
   __device__ __forceinline__ void init(Entry b) { re = b.x; im = b.y; }
   __device__ __forceinline__ void add(Entry e, Sign d) { re = fmaf(e.x, d, re); im = fmaf(e.y, d, im); }
-  __device__ __forceinline__ void prop1(Entry e, Sign d, float& xr, float& xi) const {
+  __device__ __forceinline__ void prop1(Entry e, Sign d, float sc, float& xr, float& xi) const {
     xr = fmaf(e.x, d, re);
     xi = fmaf(e.y, d, im);
   }
-  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float& xr,
+  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float sc, float& xr,
                                         float& xi) const {
     xr = fmaf(e1.x, d, fmaf(e2.x, md, re));
     xi = fmaf(e1.y, d, fmaf(e2.y, md, im));
@@ -203,11 +226,11 @@ template <> struct Acc<MPV_FMT_F32, MPV_ACC_X2> {
   __device__ __forceinline__ void add(Entry e, Sign d) {
     hr = fmaf(e.x, d, hr); hi_ = fmaf(e.y, d, hi_); lr = fmaf(e.z, d, lr); li = fmaf(e.w, d, li);
   }
-  __device__ __forceinline__ void prop1(Entry e, Sign d, float& xr, float& xi) const {
+  __device__ __forceinline__ void prop1(Entry e, Sign d, float sc, float& xr, float& xi) const {
     xr = fmaf(e.x, d, hr) + fmaf(e.z, d, lr);
     xi = fmaf(e.y, d, hi_) + fmaf(e.w, d, li);
   }
-  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float& xr,
+  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float sc, float& xr,
                                         float& xi) const {
     xr = fmaf(e1.x, d, fmaf(e2.x, md, hr)) + fmaf(e1.z, d, fmaf(e2.z, md, lr));
     xi = fmaf(e1.y, d, fmaf(e2.y, md, hi_)) + fmaf(e1.w, d, fmaf(e2.w, md, li));
@@ -223,11 +246,11 @@ template <int FMT> struct Acc<FMT, MPV_ACC_F64> {
   __device__ __forceinline__ static Sign sign(int d) { return (double)d; }
   __device__ __forceinline__ void init(Entry b) { re = b.x; im = b.y; }
   __device__ __forceinline__ void add(Entry e, Sign d) { re = fma(e.x, d, re); im = fma(e.y, d, im); }
-  __device__ __forceinline__ void prop1(Entry e, Sign d, double& xr, double& xi) const {
+  __device__ __forceinline__ void prop1(Entry e, Sign d, float sc, double& xr, double& xi) const {
     xr = fma(e.x, d, re);
     xi = fma(e.y, d, im);
   }
-  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, double& xr,
+  __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float sc, double& xr,
                                         double& xi) const {
     xr = fma(e1.x, d, fma(e2.x, md, re));
     xi = fma(e1.y, d, fma(e2.y, md, im));
@@ -302,13 +325,15 @@ template <int FMT, int VAR> struct Eval {
   // formats (an f32 number: 2 * RN32(RN32(a.x) + H)); the NATIVE accept test
   // is then made in f32.
   using Lp = typename std::conditional<kF64, double, float>::type;
-  __device__ __forceinline__ static Lp finalize(typename A::Vis vis, Sum h) {
+  __device__ __forceinline__ static Lp finalize(typename A::Vis vis, Sum h, float xi_scale_) {
     if constexpr (kF64) {
       return 2.0 * (vis + h);
     } else if constexpr (VAR == MPV_ACC_F64) {
       return 2.0f * __fadd_rn(__double2float_rn(vis), h);
     } else if constexpr (VAR == MPV_ACC_X2) {
       return 2.0f * __fadd_rn(__fadd_rn(vis.x, vis.y), h);
+    } else if constexpr (VAR == MPV_ACC_XI) {
+      return 2.0f * __fadd_rn(__int2float_rn(vis) * xi_scale_, h);
     } else {
       return 2.0f * __fadd_rn(vis, h);
     }
@@ -321,10 +346,12 @@ template <> __device__ __forceinline__ float2 vis_add(float2 v, float2 a, int d)
   return make_float2(fmaf(a.x, (float)d, v.x), fmaf(a.y, (float)d, v.y));
 }
 template <> __device__ __forceinline__ double vis_add(double v, double a, int d) { return fma(a, (double)d, v); }
+template <> __device__ __forceinline__ int vis_add(int v, int a, int d) { return v + d * a; }
 template <typename V> __device__ __forceinline__ V vis_zero();
 template <> __device__ __forceinline__ float vis_zero<float>() { return 0.0f; }
 template <> __device__ __forceinline__ float2 vis_zero<float2>() { return make_float2(0.f, 0.f); }
 template <> __device__ __forceinline__ double vis_zero<double>() { return 0.0; }
+template <> __device__ __forceinline__ int vis_zero<int>() { return 0; }
 
 // Record the first (lowest step, then lowest chain) non-finite evaluation.
 __device__ __forceinline__ void report_nonfinite(int64_t* status, int64_t step, int64_t chain) {
@@ -342,7 +369,7 @@ __device__ __forceinline__ void report_nonfinite(int64_t* status, int64_t step, 
 // ------------------------------------------------------------------------
 
 template <int FMT, int VAR, int G, int U, int PROP, bool SMEM>
-__global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, 1) sweep_kernel(const SweepArgs a) {
   using A = Acc<FMT, VAR>;
   using E = Eval<FMT, VAR>;
   using Entry = typename A::Entry;
@@ -394,6 +421,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
     visv = reinterpret_cast<const VisT*>((const char*)a.table + (((size_t)a.N * (G * U) * sizeof(Entry) + 15) & ~(size_t)15));
   }
   constexpr int Mpad = G * U;
+  const float sc = a.xi_scale;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   const int slot = lane / G;
@@ -452,13 +480,13 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
 #pragma unroll
       for (int u = 0; u + 1 < U; u += 2) {
         Theta xr0, xi0, xr1, xi1;
-        acc[u].prop1(Entry{}, A::sign(0), xr0, xi0);
-        acc[u + 1].prop1(Entry{}, A::sign(0), xr1, xi1);
+        acc[u].prop1(Entry{}, A::sign(0), sc, xr0, xi0);
+        acc[u + 1].prop1(Entry{}, A::sign(0), sc, xr1, xi1);
         E::pair(xr0, xi0, xr1, xi1, h0, vmin0);
       }
       if constexpr (U & 1) {
         Theta xr, xi;
-        acc[U - 1].prop1(Entry{}, A::sign(0), xr, xi);
+        acc[U - 1].prop1(Entry{}, A::sign(0), sc, xr, xi);
         E::single(xr, xi, h0, vmin0);
       }
       if constexpr (E::kFix) {
@@ -476,13 +504,13 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
 #pragma unroll
             for (int j = 0; j < SW; ++j) reinterpret_cast<float*>(&au)[j] = sv[(u * SW + j) * 32];
             Theta xr, xi;
-            au.prop1(Entry{}, A::sign(0), xr, xi);
+            au.prop1(Entry{}, A::sign(0), sc, xr, xi);
             E::fix(xr, xi, h0);
           }
         }
       }
       h0 = segment_sum(h0, G);
-      lp = E::finalize(vis, h0);
+      lp = E::finalize(vis, h0, sc);
       if (!isfinite(lp)) {
         if (live && gl == 0) report_nonfinite(a.status, 0, cidx);
         lp = Lp(NAN);  // NaN marks a frozen chain
@@ -564,18 +592,18 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
       for (int u = 0; u + 1 < U; u += 2) {
         Theta xr0, xi0, xr1, xi1;
         if (PROP == MPV_PROPOSAL_FLIP) {
-          acc[u].prop1(c1[u * G], d, xr0, xi0);
-          acc[u + 1].prop1(c1[(u + 1) * G], d, xr1, xi1);
+          acc[u].prop1(c1[u * G], d, sc, xr0, xi0);
+          acc[u + 1].prop1(c1[(u + 1) * G], d, sc, xr1, xi1);
         } else {
-          acc[u].prop2(c1[u * G], c2[u * G], d, md, xr0, xi0);
-          acc[u + 1].prop2(c1[(u + 1) * G], c2[(u + 1) * G], d, md, xr1, xi1);
+          acc[u].prop2(c1[u * G], c2[u * G], d, md, sc, xr0, xi0);
+          acc[u + 1].prop2(c1[(u + 1) * G], c2[(u + 1) * G], d, md, sc, xr1, xi1);
         }
         E::pair(xr0, xi0, xr1, xi1, h, vmin);
       }
       if constexpr (U & 1) {
         Theta xr, xi;
-        if (PROP == MPV_PROPOSAL_FLIP) acc[U - 1].prop1(c1[(U - 1) * G], d, xr, xi);
-        else acc[U - 1].prop2(c1[(U - 1) * G], c2[(U - 1) * G], d, md, xr, xi);
+        if (PROP == MPV_PROPOSAL_FLIP) acc[U - 1].prop1(c1[(U - 1) * G], d, sc, xr, xi);
+        else acc[U - 1].prop2(c1[(U - 1) * G], c2[(U - 1) * G], d, md, sc, xr, xi);
         E::single(xr, xi, h, vmin);
       }
       if constexpr (E::kFix) {
@@ -591,8 +619,8 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
 #pragma unroll
             for (int j = 0; j < SW; ++j) reinterpret_cast<float*>(&au)[j] = sv[(u * SW + j) * 32];
             Theta xr, xi;
-            if (PROP == MPV_PROPOSAL_FLIP) au.prop1(c1[u * G], d, xr, xi);
-            else au.prop2(c1[u * G], c2[u * G], d, md, xr, xi);
+            if (PROP == MPV_PROPOSAL_FLIP) au.prop1(c1[u * G], d, sc, xr, xi);
+            else au.prop2(c1[u * G], c2[u * G], d, md, sc, xr, xi);
             E::fix(xr, xi, h);
           }
         }
@@ -600,7 +628,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
       h = segment_sum(h, G);
       VisT vnew = vis_add(vis, visv[k1], dsign);
       if (PROP == MPV_PROPOSAL_EXCHANGE) vnew = vis_add(vnew, visv[k2], -dsign);
-      const Lp lp_new = E::finalize(vnew, h);
+      const Lp lp_new = E::finalize(vnew, h, sc);
       // ref sampler.py:128-129: NaN compares false (reject); the reference raises
       // EvaluationFailureError on any non-finite proposal (rbm.py:242-251): the
       // chain freezes and the first failure is reported.

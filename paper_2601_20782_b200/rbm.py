@@ -149,8 +149,9 @@ class ExactPlan:
 
     All partial sums of the snapshot's values are multiples of ``quantum`` and
     bounded by ``bound``; f32 holds every multiple of q up to 2^24 q exactly.
-    X1: one f32 per component (bound <= 2^24 q).  X2: theta = hi + lo with
-    hi on the grid ``split`` (|hi| <= 2^24 split) and |lo| <= (N+1) split/2 <= 2^24 q.
+    X1: one f32 per component (bound <= 2^24 q).  XI: one int32 per component
+    counting multiples of q (bound < 2^30 q).  X2: theta = hi + lo with hi on the
+    grid ``split`` (|hi| <= 2^24 split) and |lo| <= (N+1) split/2 <= 2^24 q.
     F64: otherwise (f64 accumulators, converted per unit)."""
 
     variant: int
@@ -174,6 +175,8 @@ def plan_exact(snap: RbmParameters) -> ExactPlan:
         split = 0.0  # X2 not exact
     if bound <= 2.0**24 * q:
         return ExactPlan(nat.ACC_X1, q, bound, split)
+    if bound < 2.0**30 * q:
+        return ExactPlan(nat.ACC_XI, q, bound, split)
     if split > 0.0:
         return ExactPlan(nat.ACC_X2, q, bound, split)
     return ExactPlan(nat.ACC_F64, q, bound, 0.0)
@@ -239,6 +242,8 @@ class DeviceSnapshot:
                     raise ValueError("X1 accumulators are not exact for this snapshot")
                 elif variant == nat.ACC_X2 and self.plan.split == 0.0:
                     raise ValueError("X2 accumulators are not exact for this snapshot")
+                elif variant == nat.ACC_XI and not self.plan.bound < 2.0**30 * self.plan.quantum:
+                    raise ValueError("XI accumulators are not exact for this snapshot")
             G, U = nat.plan_layout(N, M, nat.FMT_F64 if f64arith else fmt.code, variant)
             Mpad = G * U
             wpad = np.zeros((N, Mpad), dtype=np.complex128)
@@ -253,6 +258,17 @@ class DeviceSnapshot:
                 table = _pairs(wpad.real, wpad.imag, fmt.name)
                 bias = _pairs(bpad.real, bpad.imag, fmt.name)
                 vis = snap.a.real.astype(np.float32)
+            elif variant == nat.ACC_XI:
+                q = self.plan.quantum
+
+                def ints(x):
+                    v = np.rint(x / q)
+                    assert np.array_equal(v * q, x), "XI: value not on the quantum grid"
+                    return v.astype(np.int32)
+
+                table = np.stack([ints(wpad.real), ints(wpad.imag)], axis=-1)
+                bias = np.stack([ints(bpad.real), ints(bpad.imag)], axis=-1)
+                vis = ints(snap.a.real)
             else:
                 g = self.plan.split
 
@@ -278,8 +294,9 @@ class DeviceSnapshot:
                                       dtype=torch.uint8).to(self.device)
         self._vis_im = torch.from_numpy(np.ascontiguousarray(snap.a.imag, dtype=np.float64)).to(self.device)
         base = self._table.data_ptr()
+        quantum = self.plan.quantum if (variant == nat.ACC_XI) else 0.0
         self.struct = nat.Snapshot(N, M, Mpad, fmt.code, mode.code, variant, G, U,
-                                   base, self._bias.data_ptr(), base + tbytes, self._vis_im.data_ptr())
+                                   base, self._bias.data_ptr(), base + tbytes, self._vis_im.data_ptr(), quantum)
 
     def scratch(self, n_chains: int):
         """Device scratch for the fused sweep over n_chains (work queue, parked theta)."""
@@ -290,7 +307,7 @@ class DeviceSnapshot:
 
     @property
     def label(self) -> str:
-        names = {nat.ACC_X1: "X1", nat.ACC_X2: "X2", nat.ACC_F64: "F64"}
+        names = {nat.ACC_X1: "X1", nat.ACC_X2: "X2", nat.ACC_F64: "F64", nat.ACC_XI: "XI"}
         return f"{self.fmt.name}/{self.mode.value}/{names[self.variant]}/G{self.lanes_per_chain}xU{self.units_per_lane}"
 
 

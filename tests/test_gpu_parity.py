@@ -138,7 +138,7 @@ def test_native_variants_identical(cuda, fmt):
     p = rbm.random_parameters(40, 2, derive_key(2, "variants"), 0.01)
     bits = np.random.default_rng(3).integers(0, 2, size=(300, 40), dtype=np.uint8)
     by_layout = {}
-    for var in (_native.ACC_X1, _native.ACC_X2, _native.ACC_F64):
+    for var in (_native.ACC_X1, _native.ACC_XI, _native.ACC_X2, _native.ACC_F64):
         try:
             ev = rbm.log_prob_evaluator(p, FORMATS[fmt], NATIVE, variant=var)
         except ValueError:

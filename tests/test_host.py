@@ -97,7 +97,7 @@ def _exact_sums_fit_f32(values_fn, n_trials, rng, plan, snap):
                     assert Fraction(float(np.float32(float(total)))) == total
 
 
-@pytest.mark.parametrize("scale,fmt,variant", [(0.01, "f16", 0), (0.5, "f16", 1), (0.3, "bf16", None)])
+@pytest.mark.parametrize("scale,fmt,variant", [(0.01, "f16", 0), (0.5, "f16", 3), (0.3, "bf16", None)])
 def test_exact_planner(scale, fmt, variant):
     p = rbm.random_parameters(100, 1, derive_key(0, "init"), scale)
     snap = rbm.round_parameters(p, precision.FORMATS[fmt])
