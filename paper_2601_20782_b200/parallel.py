@@ -84,3 +84,34 @@ def sharded_ensemble(n_chains_total, n_sites, proposal, evaluator, key, rank, wo
     offset, count = shard(n_chains_total, rank, world)
     return ChainEnsemble(count, n_sites, proposal, evaluator, key, chain_offset=offset,
                          n_chains_total=n_chains_total)
+
+
+def sharded_statistics(o, eps, weights, group=None):
+    """Forces and S-matrix of the reference estimators (vmc.py:145-188) from
+    per-rank shards of the sample set, with NCCL/gloo all-reduces only:
+
+      F = sum_w conj(O) eps - (sum_w conj O)(sum_w eps)
+      S = sum_w (O - Obar)^H (O - Obar),  Obar = sum_w O     (two passes)
+
+    `weights` are this rank's sample weights normalised over the GLOBAL sample
+    count, so the all-reduced sums are the single-process weighted sums.
+    Returns (f, s, energy) identical on every rank (then every rank solves the
+    same SR system and keeps identical parameters)."""
+    import torch
+
+    w = weights.to(o.dtype)
+    oc = o.conj()
+    s_oe = (oc * w[:, None]).T @ eps
+    s_o = w @ oc
+    s_e = (w @ eps).reshape(1)
+    s_wo = w @ o
+    first = torch.cat([s_oe, s_o, s_e, s_wo])
+    all_reduce_sum(first, group)
+    P = o.shape[1]
+    s_oe, s_o, s_e, mean = first[:P], first[P:2 * P], first[2 * P], first[2 * P + 1:]
+    f = s_oe - s_o * s_e
+    c = o - mean[None, :]
+    s = c.conj().T @ (c * w[:, None])
+    all_reduce_sum(s, group)
+    s = 0.5 * (s + s.conj().T)
+    return f, s, s_e.real

@@ -259,9 +259,19 @@ class TrainResult:
     force_history: list = field(default_factory=list)
 
 
-def train(config: TrainConfig, device=None) -> TrainResult:
-    """Two-copy mixed-precision SR training (vmc.py:472-639) on the device."""
+def train(config: TrainConfig, device=None, group=None) -> TrainResult:
+    """Two-copy mixed-precision SR training (vmc.py:472-639) on the device.
+
+    Under torch.distributed (world > 1) each rank samples its contiguous slice
+    of the global chains (draws depend on global chain ids only), evaluates
+    local energies and O on its own samples, and the forces, S-matrix, energy,
+    split-chain error and acceptance come from all-reduces
+    (parallel.sharded_statistics / energy_statistics); every rank then solves
+    the same SR system.  sigma-hat pools per-rank deduplicated batches."""
     import torch
+    import torch.distributed as tdist
+
+    from . import parallel
 
     from . import rbm
     from .bounds import pinsker_tv_bound, theorem3_gaussian_bound
@@ -271,6 +281,8 @@ def train(config: TrainConfig, device=None) -> TrainResult:
 
     nat.require_cuda()
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    world = tdist.get_world_size(group) if (tdist.is_available() and tdist.is_initialized()) else 1
+    rank = tdist.get_rank(group) if world > 1 else 0
     spec = config.hamiltonian
     n = spec.lattice.n_sites
     params = rbm.random_parameters(n, Fraction(config.alpha), derive_key(config.seed, "init"), config.init_scale)
@@ -284,9 +296,9 @@ def train(config: TrainConfig, device=None) -> TrainResult:
         all_u8 = enumerate_bits(n)
         all_packed = torch.from_numpy(pack_bits(all_u8)).to(dev)
     else:
-        base, extra = divmod(config.n_samples, n_chains)
-        counts = np.array([base + (1 if c < extra else 0) for c in range(n_chains)])
-        chain_ids = torch.as_tensor(np.repeat(np.arange(n_chains), counts), device=dev)
+        c_off, c_cnt = parallel.shard(n_chains, rank, world)
+        counts = parallel.chain_counts(config.n_samples, n_chains, c_off, c_cnt)
+        chain_ids = torch.as_tensor(np.repeat(np.arange(c_cnt), counts), device=dev)
         per_chain = torch.as_tensor(counts, device=dev, dtype=torch.float64)
     ensemble = None
     records, force_history = [], []
@@ -303,7 +315,8 @@ def train(config: TrainConfig, device=None) -> TrainResult:
         else:
             ev = rbm.log_prob_evaluator(params, config.sampling_format, config.rounding_mode, dev)
             if ensemble is None:
-                ensemble = ChainEnsemble(n_chains, n, config.proposal, ev, derive_key(config.seed, "chains"))
+                ensemble = ChainEnsemble(c_cnt, n, config.proposal, ev, derive_key(config.seed, "chains"),
+                                         chain_offset=c_off, n_chains_total=n_chains)
                 ensemble.run_sweeps(burn_in)
             else:
                 ensemble.set_evaluator(ev)
@@ -311,6 +324,11 @@ def train(config: TrainConfig, device=None) -> TrainResult:
             ensemble.reset_counters()
             packed = ensemble.collect_packed(config.n_samples, config.thin_sweeps * n + 1)
             acceptance = ensemble.acceptance_rate
+            if world > 1:
+                ap = torch.tensor([float(ensemble.accepted), float(ensemble.proposed)], dtype=torch.float64,
+                                  device=dev)
+                parallel.all_reduce_sum(ap, group)
+                acceptance = float(ap[0] / ap[1])
             # np.unique(..., axis=0) over the sample stream (vmc.py:560-563)
             uniq, inverse, cnt = torch.unique(packed, dim=0, return_inverse=True, return_counts=True)
             est_w = cnt.to(torch.float64) / config.n_samples
@@ -324,14 +342,20 @@ def train(config: TrainConfig, device=None) -> TrainResult:
         u8 = torch.empty((uniq.shape[0], n), dtype=torch.uint8, device=dev)
         nat.call("mpv_unpack_bits", uniq.data_ptr(), uniq.shape[0], n, u8.data_ptr(), nat.stream_handle(dev))
         o = grad_log_psi_device(params, u8)
-        f = forces(o=o, eps=eps, weights=est_w)
-        s = s_matrix(o=o, weights=est_w)
+        if world > 1:
+            f, s, e_glob = parallel.sharded_statistics(o, eps, est_w, group)
+            energy = float(e_glob)
+        else:
+            f = forces(o=o, eps=eps, weights=est_w)
+            s = s_matrix(o=o, weights=est_w)
+            energy = float((est_w.to(eps.dtype) @ eps).real)
         update = sr_step(f, s, config.lambda_shift, config.eta, config.compute_kappa)
         theta = params.flatten() - config.eta * update.g.cpu().numpy()
         new_params = rbm.RbmParameters.from_flat(theta, params.n_visible, params.n_hidden)
-        energy = float((est_w.to(eps.dtype) @ eps).real)
         if exact_mode:
             err = 0.0
+        elif world > 1:
+            err = parallel.energy_statistics(eps.real[inverse], counts, 0, 1, group)["mc_error"]
         else:
             stream = eps.real[inverse]
             if n_chains > 1:
@@ -348,7 +372,14 @@ def train(config: TrainConfig, device=None) -> TrainResult:
                 lp_fmt, _ = ev.log_prob_packed(uniq)
                 lp64 = rbm.LogProbEvaluator(params, F64, RoundingMode.PER_OPERATION, dev).log_prob_packed(uniq)[0]
                 delta = lp_fmt - lp64
-                sigma_hat = float(delta.std()) if delta.numel() > 1 else 0.0
+                if world > 1:
+                    mom = torch.stack([delta.sum(), (delta * delta).sum(),
+                                       torch.tensor(float(delta.numel()), dtype=torch.float64, device=dev)])
+                    parallel.all_reduce_sum(mom, group)
+                    m1, m2, cnt_d = (float(x) for x in mom)
+                    sigma_hat = float(np.sqrt(max(m2 - m1 * m1 / cnt_d, 0.0) / (cnt_d - 1))) if cnt_d > 1 else 0.0
+                else:
+                    sigma_hat = float(delta.std()) if delta.numel() > 1 else 0.0
             record = {"step": step, "energy": energy, "mc_error": err, "acceptance": acceptance,
                       "sigma_hat": sigma_hat, "bound_pinsker": pinsker_tv_bound(sigma_hat),
                       "bound_theorem3": theorem3_gaussian_bound(sigma_hat, 0.0, 0.0), "kappa": update.kappa}

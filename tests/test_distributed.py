@@ -74,3 +74,50 @@ def test_gloo_world2_statistics():
         assert stats["acceptance"] == pytest.approx(30 / 200)
         assert stats["n_chains"] == N_CHAINS and stats["n_samples"] == N_SAMPLES
     assert results[0][3] == 0 and results[0][4] == results[1][3] and results[1][4] == N_SAMPLES
+
+
+def _stats_worker(rank, world, port, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    o, eps, w = _fake_vmc()
+    half = o.shape[0] // 2
+    sl = slice(0, half) if rank == 0 else slice(half, None)
+    f, s, e = parallel.sharded_statistics(o[sl], eps[sl], w[sl])
+    q.put((rank, f.numpy(), s.numpy(), float(e)))
+    dist.destroy_process_group()
+
+
+def _fake_vmc():
+    rng = np.random.default_rng(11)
+    o = torch.from_numpy(rng.normal(size=(40, 6)) + 1j * rng.normal(size=(40, 6)))
+    eps = torch.from_numpy(rng.normal(size=40) + 1j * rng.normal(size=40))
+    w = torch.from_numpy(rng.random(40))
+    w = w / w.sum()
+    return o, eps, w
+
+
+@pytest.mark.timeout(120)
+def test_gloo_sharded_forces_and_s_matrix():
+    """Two ranks holding halves of the samples reproduce the single-process
+    weighted forces and S-matrix (ref vmc.py:145-188)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stats_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=100) for _ in procs)
+    for p in procs:
+        p.join(timeout=30)
+        assert p.exitcode == 0
+    o, eps, w = _fake_vmc()
+    oc = np.conj(o.numpy())
+    wn, en = w.numpy(), eps.numpy()
+    f_ref = (oc * wn[:, None]).T @ en - (wn @ oc) * (wn @ en)
+    mean = wn @ o.numpy()
+    c = o.numpy() - mean[None, :]
+    s_ref = np.conj(c).T @ (c * wn[:, None])
+    s_ref = 0.5 * (s_ref + np.conj(s_ref).T)
+    for _, f, s, e in res:
+        assert np.allclose(f, f_ref, atol=1e-13)
+        assert np.allclose(s, s_ref, atol=1e-13)
+        assert e == pytest.approx(float((wn @ en).real), abs=1e-14)
