@@ -2,6 +2,7 @@
 // configuration and the small helper kernels.  No device allocation happens
 // here: every buffer is caller-owned.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -478,20 +479,29 @@ int mpv_rounded_log_prob(const uint8_t* bits, int64_t B, int N, int M, const dou
 
 size_t mpv_energy_tables_bytes(int N, int M, int ham, int n_bonds) {
   const int T = ham == MPV_HAM_TFIM ? N : n_bonds;
-  return 2 * (size_t)M * T * sizeof(double2) + 2 * (size_t)T * sizeof(double2) + (size_t)T * sizeof(int32_t) + 64;
+  return (size_t)M * T * sizeof(double2) + 2 * (size_t)T * sizeof(double2) + 2 * (size_t)T * sizeof(int32_t) + 128 +
+         (size_t)energy_w_rows(N) * energy_w_pitch(M) * sizeof(double);
 }
 
-static void energy_layout(int N, int M, int ham, int n_bonds, void* tables, double2** C, double2** S,
-                          double2** ea, int32_t** slow) {
+struct EnergyTables {
+  double2 *tau, *ea;
+  int32_t *ec, *slow;
+  double* wp;
+};
+static EnergyTables energy_layout(int N, int M, int ham, int n_bonds, void* tables) {
   const int T = ham == MPV_HAM_TFIM ? N : n_bonds;
   char* p = (char*)tables;
-  *C = (double2*)p;
+  EnergyTables e;
+  e.tau = (double2*)p;
   p += (size_t)M * T * sizeof(double2);
-  *S = (double2*)p;
-  p += (size_t)M * T * sizeof(double2);
-  *ea = (double2*)p;
+  e.ea = (double2*)p;
   p += 2 * (size_t)T * sizeof(double2);
-  *slow = (int32_t*)p;
+  e.ec = (int32_t*)p;
+  p += (size_t)T * sizeof(int32_t);
+  e.slow = (int32_t*)p;
+  p += (size_t)T * sizeof(int32_t);
+  e.wp = (double*)(((uintptr_t)p + 127) / 128 * 128);
+  return e;
 }
 
 int mpv_energy_prepare(int N, int M, const double* a, const double* b, const double* w_t, int ham,
@@ -502,12 +512,10 @@ int mpv_energy_prepare(int N, int M, const double* a, const double* b, const dou
   EnergyArgs e{};
   e.N = N; e.M = M; e.ham = ham; e.n_bonds = n_bonds; e.n_terms = ham == MPV_HAM_TFIM ? N : n_bonds;
   e.a = (const double2*)a; e.b = (const double2*)b; e.w_t = (const double2*)w_t; e.bonds = bonds;
-  double2 *C, *S, *ea;
-  int32_t* slow;
-  energy_layout(N, M, ham, n_bonds, tables, &C, &S, &ea, &slow);
+  const EnergyTables tb = energy_layout(N, M, ham, n_bonds, tables);
   const int64_t n = (int64_t)M * e.n_terms;
   const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  energy_tables_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(e, C, S, ea, slow);
+  energy_tables_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(e, tb.tau, tb.ea, tb.ec, tb.slow, tb.wp);
   return check_launch("energy_prepare");
 }
 
@@ -524,31 +532,44 @@ int mpv_local_energies(int N, int M, const double* a, const double* b, const dou
   e.n_terms = ham == MPV_HAM_TFIM ? N : n_bonds;
   e.a = (const double2*)a; e.b = (const double2*)b; e.w_t = (const double2*)w_t; e.bonds = bonds;
   e.J = J; e.h = h;
-  double2 *C, *S, *ea;
-  int32_t* slow;
-  energy_layout(N, M, ham, n_bonds, const_cast<void*>(tables), &C, &S, &ea, &slow);
-  e.C = C; e.S = S; e.ea = ea; e.slow = slow;
+  const EnergyTables tb = energy_layout(N, M, ham, n_bonds, const_cast<void*>(tables));
+  e.tau = tb.tau; e.ea = tb.ea; e.ec = tb.ec; e.slow = tb.slow; e.wp = tb.wp;
   e.bits = bits; e.B = B; e.out = (double2*)out_eps; e.status = status;
   const int T = e.n_terms;
-  const int TT = (T + 31) / 32 * 32;
-  if (TT > 512 || M > 512) return fail(MPV_ERR_ARGS, "local_energies: more than 512 terms or hidden units");
-  // staging buffer: a chunk of kRows C and S rows, or >= 8 W_t rows
-  const int stage = (int)std::max<size_t>((size_t)2 * kRows * T * sizeof(double2), (size_t)kRows * M * sizeof(double2));
-  auto smem_for = [&](int ng) {
-    return (size_t)kEnergyST * ng * M * sizeof(double2) + (size_t)kEnergyST * ng * 32 * sizeof(uint32_t) +
-           (size_t)((N + 3) / 4) * 4 * sizeof(uint32_t) + (size_t)kMaxSB * 16 * 2 * sizeof(double) +
-           2 * (size_t)stage + 16 + (size_t)N * kMaxSB * sizeof(double);
-  };
-  int NG = std::max(1, std::min(kMaxSB / kEnergyST, 512 / TT));  // sample groups per block (table reuse)
-  while (NG > 1 && smem_for(NG) > (size_t)max_smem_optin()) --NG;
-  const size_t smem = smem_for(NG);
-  if (smem > (size_t)max_smem_optin()) return fail(MPV_ERR_ARGS, "local_energies: n_hidden too large");
-  const int SB = kEnergyST * NG;
-  const int threads = std::max(std::max(32, NG * TT), (M + 31) / 32 * 32);
-  if (threads > 512) return fail(MPV_ERR_ARGS, "local_energies: block too large");
-  if (int rc = ensure_smem((const void*)&energy_kernel<kEnergyST>, smem)) return rc;
-  energy_kernel<kEnergyST><<<(unsigned)((B + SB - 1) / SB), threads, smem, (cudaStream_t)stream>>>(e, NG, stage);
-  return check_launch("local_energies");
+  if (T > 512 || M > 512) return fail(MPV_ERR_ARGS, "local_energies: more than 512 terms or hidden units");
+  // (ST samples per thread, SB samples per block): terms x groups flattened
+  // over <= 512 threads; prefer 16 samples per block (two DMMA m-tiles).
+  // Phase 1 runs in one pass: every warp owns <= KT of the ceil(M/4) n-tiles.
+  struct Cfg { int st, sb; };
+  const Cfg cfgs[] = {{4, 16}, {8, 16}, {8, 8}};
+  const size_t optin = (size_t)max_smem_optin();
+  const int NT = (M + 3) / 4;
+  for (const Cfg& cf : cfgs) {
+    int threads = std::max(32, ((cf.sb / cf.st) * T + 31) / 32 * 32);
+    int kt = 4;
+    if (32 * ((NT + 3) / 4) > threads) {
+      if (32 * ((NT + 3) / 4) <= 512) threads = 32 * ((NT + 3) / 4);
+      else { kt = 8; threads = std::max(threads, 32 * ((NT + 7) / 8)); }
+    }
+    if (threads > (cf.st == 4 ? kST4Threads : 512)) continue;
+    for (int nbt = 3; nbt >= 2; --nbt)
+      for (int rows = 12; rows >= 2; rows -= 2) {
+        EnergyPlan pl;
+        const size_t smem = energy_plan(N, M, T, cf.sb, rows, nbt, &pl);
+        static const int skip = getenv("MPV_ENERGY_SKIP") ? atoi(getenv("MPV_ENERGY_SKIP")) : 0;
+        pl.skip = skip;
+        if (smem > optin) continue;
+        const void* fn = cf.st == 4 ? (kt == 4 ? (const void*)&energy_kernel<4, 4> : (const void*)&energy_kernel<4, 8>)
+                                    : (kt == 4 ? (const void*)&energy_kernel<8, 4> : (const void*)&energy_kernel<8, 8>);
+        if (int rc = ensure_smem(fn, smem)) return rc;
+        const unsigned grid = (unsigned)((B + cf.sb - 1) / cf.sb);
+        void* args[] = {&e, &pl};
+        if (cudaLaunchKernel(fn, grid, threads, args, smem, (cudaStream_t)stream) != cudaSuccess)
+          return check_launch("local_energies");
+        return check_launch("local_energies");
+      }
+  }
+  return fail(MPV_ERR_ARGS, "local_energies: n_hidden / terms too large for shared memory");
 }
 
 int mpv_unpack_bits(const uint32_t* words, int64_t B, int N, uint8_t* out, void* stream) {

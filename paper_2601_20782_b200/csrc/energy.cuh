@@ -6,28 +6,32 @@
 //
 // The reference forms every connected x' and runs a full forward on it
 // (O(N * N * M) per sample).  Here a ratio is an O(M) product over hidden
-// units of cosh(theta_i + d w_i) / cosh(theta_i) = C_i + d tanh(theta_i) S_i
-// with C = cosh(w), S = sinh(w) tabulated once per parameter snapshot
-// (w = W_:k for a flip of k, w = W_:i - W_:j for a swap of bond (i,j); d = +-1),
-// times exp(d a_k) (or exp(d (a_i - a_j))).  theta and tanh(theta) are formed
-// once per sample.  Terms whose table has |Re w| > kSafeRe (where C - S would
-// cancel against tanh ~ +-1) use the log-cosh difference instead.
+// units of cosh(theta_i + d w_i) / cosh(theta_i) = cosh(w_i) (1 + d tanh(theta_i) tau_i),
+// tau = tanh(w), tabulated once per parameter snapshot (w = W_:k for a flip of
+// k, w = W_:i - W_:j for a swap of bond (i,j); d = +-1).  The term constant
+// exp(d a) prod_i cosh(w_i) (mantissa + binary exponent) is tabulated too, so a
+// factor costs one complex multiply plus one complex multiply-add (8 FP64
+// ops).  theta = b + W x is a 0/1 x f64 GEMM on the FP64 tensor cores (DMMA).
+// Terms with |Re w| > kSafeRe (tanh ~ +-1 cancels in 1 - tanh tanh) or
+// |cosh w| < kMinCosh (tau near a pole) use the log-cosh difference instead.
 #pragma once
 #include "common.cuh"
 
 namespace mpv {
 
 constexpr double kSafeRe = 4.0;
+constexpr double kMinCosh2 = 1.0 / 16.0;  // |cosh w|^2 below this -> slow path
 
 struct EnergyArgs {
   int N, M, words, ham, n_bonds, n_terms;
   const double2 *a, *b, *w_t;  // w_t [N][M]
   const int32_t* bonds;        // [n_bonds][2]
   double J, h;
-  const double2* C;  // [M][n_terms]
-  const double2* S;  // [M][n_terms]
-  const double2* ea; // [n_terms][2]: exp(+a_t), exp(-a_t)
+  const double2* tau;   // [M][n_terms]: tanh(w)
+  const double2* ea;    // [n_terms][2]: exp(+-a_t) prod_i cosh(w_it), mantissa
+  const int32_t* ec;    // [n_terms]: binary exponent of prod_i cosh(w_it)
   const int32_t* slow;  // [n_terms]
+  const double* wp;     // [roundup(N, 8)][2M + 8]: W_t in the staging layout
   const uint32_t* bits;
   int64_t B;
   double2* out;
@@ -73,40 +77,6 @@ __device__ __forceinline__ double2 clogcosh(double2 z) {
 }
 
 // ---- per-snapshot tables ----
-__global__ void energy_tables_kernel(const EnergyArgs a, double2* C, double2* S, double2* ea,
-                                     int32_t* slow) {
-  const int T = a.n_terms;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (int64_t)a.M * T;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(idx / T), t = (int)(idx % T);
-    double2 w;
-    if (a.ham == MPV_HAM_TFIM) {
-      w = a.w_t[(size_t)t * a.M + i];
-    } else {
-      const int p = a.bonds[2 * t], q = a.bonds[2 * t + 1];
-      const double2 wp = a.w_t[(size_t)p * a.M + i], wq = a.w_t[(size_t)q * a.M + i];
-      w = make_double2(wp.x - wq.x, wp.y - wq.y);
-    }
-    C[(size_t)i * T + t] = ccosh(w);
-    S[(size_t)i * T + t] = csinh(w);
-  }
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
-    double2 av;
-    int bad = 0;
-    if (a.ham == MPV_HAM_TFIM) {
-      av = a.a[t];
-      for (int i = 0; i < a.M; ++i) bad |= fabs(a.w_t[(size_t)t * a.M + i].x) > kSafeRe;
-    } else {
-      const int p = a.bonds[2 * t], q = a.bonds[2 * t + 1];
-      av = make_double2(a.a[p].x - a.a[q].x, a.a[p].y - a.a[q].y);
-      for (int i = 0; i < a.M; ++i)
-        bad |= fabs(a.w_t[(size_t)p * a.M + i].x - a.w_t[(size_t)q * a.M + i].x) > kSafeRe;
-    }
-    ea[2 * t] = cexp_(av);
-    ea[2 * t + 1] = cexp_(make_double2(-av.x, -av.y));
-    slow[t] = bad;
-  }
-}
 
 // Scale p by 2^-k (exact), k = biased-exponent of max(|re|, |im|) - 1023;
 // accumulate k.  Bit arithmetic only (no libm call).
@@ -121,297 +91,451 @@ __device__ __forceinline__ void renorm(double2& p, int& e) {
   e += k;
 }
 
-// One block = NG groups x ST samples x all terms (NG * ST = SB samples).
-// Thread (g, t) owns term t for the ST samples of group g: it keeps ST
-// running products in registers and streams its column of the C/S tables
-// (the NG threads of a term read the same addresses: one L1 fill).  theta
-// is formed per unit with one coalesced load of W_t[k][i] per (site, unit)
-// shared by all SB samples (per-site sample masks), then tanh(theta) sits in
-// shared memory, read as a broadcast.  Sums over terms are reduced in a fixed
-// order (deterministic).
-constexpr int kRows = 6;   // C/S rows per staged chunk
-constexpr int kMaxSB = 16;  // samples per block (NG * ST)
+__device__ __forceinline__ double2 term_w(const EnergyArgs& a, int t, int i) {
+  if (a.ham == MPV_HAM_TFIM) return a.w_t[(size_t)t * a.M + i];
+  const int p = a.bonds[2 * t], q = a.bonds[2 * t + 1];
+  const double2 wp = a.w_t[(size_t)p * a.M + i], wq = a.w_t[(size_t)q * a.M + i];
+  return make_double2(wp.x - wq.x, wp.y - wq.y);
+}
 
-// Bulk-async (TMA engine) staging of contiguous global chunks into a double
-// buffer in shared memory, one mbarrier per buffer.  Thread 0 issues; every
-// thread waits; a block barrier after consumption frees the buffer.
-struct Stager {
-  uint32_t buf_addr[2], bar_addr[2];
-  unsigned char* buf[2];
-  int uses[2];
-  __device__ void init(unsigned char* base, size_t bytes, uint64_t* bars, int tid) {
-    for (int b = 0; b < 2; ++b) {
-      buf[b] = base + b * bytes;
-      buf_addr[b] = (uint32_t)__cvta_generic_to_shared(buf[b]);
-      bar_addr[b] = (uint32_t)__cvta_generic_to_shared(bars + b);
-      uses[b] = 0;
-    }
-    if (tid == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_addr[0]));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_addr[1]));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+__global__ void energy_tables_kernel(const EnergyArgs a, double2* tau, double2* ea, int32_t* ec, int32_t* slow,
+                                     double* wp) {
+  const int T = a.n_terms;
+  // W_t copied to the staging layout: rows padded to a multiple of 8 (zero
+  // rows), pitch 2M + 8 doubles (zero pad)
+  const int pitch = 2 * a.M + 8, np = (a.N + 7) / 8 * 8;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (int64_t)np * pitch;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx / pitch), c = (int)(idx % pitch);
+    wp[idx] = (k < a.N && c < 2 * a.M) ? reinterpret_cast<const double*>(a.w_t)[(size_t)k * 2 * a.M + c] : 0.0;
   }
-  // one or two copies completing the same buffer
-  __device__ void issue(int b, const void* src1, uint32_t bytes1, const void* src2, uint32_t off2, uint32_t bytes2) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_addr[b]), "r"(bytes1 + bytes2)
-                 : "memory");
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (int64_t)a.M * T;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / T), t = (int)(idx % T);
+    tau[(size_t)i * T + t] = ctanh(term_w(a, t, i));
+  }
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    double2 av;
+    if (a.ham == MPV_HAM_TFIM) {
+      av = a.a[t];
+    } else {
+      const int p = a.bonds[2 * t], q = a.bonds[2 * t + 1];
+      av = make_double2(a.a[p].x - a.a[q].x, a.a[p].y - a.a[q].y);
+    }
+    int bad = 0, e = 0;
+    double2 cp = make_double2(1.0, 0.0);
+    for (int i = 0; i < a.M; ++i) {
+      const double2 w = term_w(a, t, i);
+      const double2 c = ccosh(w);
+      bad |= fabs(w.x) > kSafeRe || c.x * c.x + c.y * c.y < kMinCosh2;
+      cp = cmul(cp, c);
+      renorm(cp, e);
+    }
+    ea[2 * t] = cmul(cexp_(av), cp);
+    ea[2 * t + 1] = cmul(cexp_(make_double2(-av.x, -av.y)), cp);
+    ec[t] = e;
+    slow[t] = bad;
+  }
+}
+
+// Block layout (dynamic shared memory, 16-B aligned offsets):
+//   pool:  tt [M][SB] double2 (theta, then tanh theta) followed by nbt tau
+//          staging buffers of `rows` rows.  During phase 1 the whole pool is
+//          nbw W staging buffers of 8 padded rows; after phase 2 it holds the
+//          per-(sample, term) ratios [SB][T] double2.
+//   wsm [SB][32] packed sample bits, smask [energy_mask_pad(N)] per-site
+//   sample masks (zero beyond N), 16 mbarriers (two Pipes).
+constexpr int kMaxSB = 16;  // samples per block
+constexpr int kWRows = 8;   // W rows per staged chunk (two DMMA k-steps)
+
+struct EnergyPlan {
+  int SB, rows, nbt, nbw;          // samples/block, tau rows/chunk, tau buffers, W buffers
+  int tbuf_bytes, wbuf_bytes, pool_bytes;
+  int skip;  // profiling only (MPV_ENERGY_SKIP): bit 0 phase 1, bit 1 tanh, bit 2 phase 2
+};
+__host__ __device__ inline int energy_mask_pad(int N) { return (N + 15) / 16 * 16 + 16; }
+__host__ __device__ inline int energy_w_pitch(int M) { return 2 * M + 8; }  // doubles per staged W row
+__host__ __device__ inline int energy_w_rows(int N) { return (N + kWRows - 1) / kWRows * kWRows; }
+// fills pool/buffer sizes; returns the dynamic shared memory bytes
+inline size_t energy_plan(int N, int M, int T, int SB, int rows, int nbt, EnergyPlan* p) {
+  p->SB = SB;
+  p->rows = rows;
+  p->nbt = nbt;
+  p->tbuf_bytes = rows * T * 16;
+  p->wbuf_bytes = kWRows * energy_w_pitch(M) * 8;
+  size_t pool = (size_t)SB * M * 16 + (size_t)nbt * p->tbuf_bytes;
+  if ((size_t)SB * T * 16 > pool) pool = (size_t)SB * T * 16;
+  if ((size_t)2 * p->wbuf_bytes > pool) pool = (size_t)2 * p->wbuf_bytes;
+  pool = (pool + 127) / 128 * 128;
+  p->pool_bytes = (int)pool;
+  p->nbw = (int)(pool / p->wbuf_bytes);
+  if (p->nbw > 4) p->nbw = 4;
+  return pool + (size_t)SB * 32 * 4 + (size_t)energy_mask_pad(N) * 4 + 16 * 8;
+}
+
+// Bulk-async (TMA engine) ring of nb <= 4 buffers in shared memory.  Per
+// buffer a "full" mbarrier (count 1 + transaction bytes; thread 0 issues) and
+// an "empty" mbarrier (one arrival per warp once the warp has read the chunk).
+// Chunk c uses buffer c % nb, that buffer's (c / nb)-th completion, so waits
+// are on parity (c / nb) & 1 (tracked incrementally by Pos).  No block-wide barrier per chunk: only the
+// producer thread waits for the slowest warp before refilling a buffer.
+struct Pipe {
+  uint32_t buf_addr0, bar_addr0, bytes;  // bars: full[0..3], empty[0..3]
+  int nb;
+  __device__ void init(const unsigned char* base, uint32_t buf_bytes, int n_buf, const uint64_t* bars) {
+    buf_addr0 = (uint32_t)__cvta_generic_to_shared(base);
+    bar_addr0 = (uint32_t)__cvta_generic_to_shared(bars);
+    bytes = buf_bytes;
+    nb = n_buf;
+  }
+  __device__ static void init_bars(const uint64_t* bars, int n_pipes, int n_warps) {
+    const uint32_t b0 = (uint32_t)__cvta_generic_to_shared(bars);
+    for (int p = 0; p < n_pipes; ++p)
+      for (int k = 0; k < 8; ++k)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b0 + 8 * (8 * p + k)), "r"(k < 4 ? 1 : n_warps));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __device__ uint32_t full(int b) const { return bar_addr0 + 8 * b; }
+  __device__ uint32_t empty(int b) const { return bar_addr0 + 32 + 8 * b; }
+  __device__ uint32_t buf(int b) const { return buf_addr0 + b * bytes; }
+  __device__ void expect(int b, uint32_t total) const {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full(b)), "r"(total) : "memory");
+  }
+  __device__ void copy(int b, uint32_t dst_off, const void* src, uint32_t n) const {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     buf_addr[b]), "l"(src1), "r"(bytes1), "r"(bar_addr[b]) : "memory");
-    if (bytes2)
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       buf_addr[b] + off2), "l"(src2), "r"(bytes2), "r"(bar_addr[b]) : "memory");
+                     buf(b) + dst_off), "l"(src), "r"(n), "r"(full(b)) : "memory");
   }
-  __device__ void wait(int b) {
-    const uint32_t parity = uses[b] & 1;
+  __device__ static void wait_parity(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{.reg .pred p;\nWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
-            bar_addr[b]), "r"(parity) : "memory");
-    ++uses[b];
+            bar), "r"(parity) : "memory");
+  }
+  // consumers: chunk in buffer b, that buffer's use with parity ph
+  __device__ void wait_full(int b, uint32_t ph) const { wait_parity(full(b), ph); }
+  __device__ void release(int b, int lane) const {
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty(b)) : "memory");
+  }
+  // producer: buffer b was released by every warp for its use with parity ph
+  __device__ void wait_empty(int b, uint32_t ph) const { wait_parity(empty(b), ph); }
+  // ring position of a chunk sequence: slot and use parity, advanced per chunk
+  struct Pos {
+    int slot;
+    uint32_t ph;
+  };
+  __device__ void advance(Pos& p) const {
+    if (++p.slot == nb) {
+      p.slot = 0;
+      p.ph ^= 1u;
+    }
   }
 };
 
-// One block = NG groups x ST samples x all terms (SB = NG*ST samples).
-// Phase 1: theta = b + W x, thread i owns unit i for all SB samples; W_t
-// rows are staged by bulk copies and shared by the block (per-site sample
-// bit masks select the adds).  tanh(theta) goes to shared memory.
-// Phase 2: thread (g, t) owns term t for the ST samples of group g and keeps
-// ST running products of (C + d tanh(theta) S) in registers; C/S rows are
-// staged the same way and read conflict-free.  Sums over terms reduce in a
-// fixed order (deterministic).
-template <int ST>
-__global__ void __launch_bounds__(512) energy_kernel(const EnergyArgs a, int NG, int stage_bytes) {
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// tanh(x+iy) = (sinh 2x + i sin 2y) / (cosh 2x + cos 2y) with one expm1, one
+// sincos and one division: m = expm1(2|x|), sinh 2|x| = m (m + 2) / (2 (m + 1)),
+// cosh 2|x| = 1 + m^2 / (2 (m + 1)), 1 + cos 2y = 2 cos^2 y, so
+//   tanh = (m (m + 2) + i 4 (m + 1) sin y cos y) / (4 (m + 1) cos^2 y + m^2)
+// (a sum of non-negative terms in the denominator: no cancellation).
+__device__ __forceinline__ double2 ctanh_fast(double2 z) {
+  const double ax = fmin(fabs(z.x), 40.0);  // tanh(40) == 1 in f64
+  const double m = expm1(2.0 * ax);
+  double s, c;
+  sincos(z.y, &s, &c);
+  const double m1 = 4.0 * (m + 1.0);
+  const double inv = 1.0 / fma(m1 * c, c, m * m);
+  return make_double2(copysign(m * (m + 2.0) * inv, z.x), m1 * s * c * inv);
+}
+
+// Ratio of term t for one sample through the log-cosh difference (ref
+// formulation, rbm.py:130-140), theta recomputed from W: the path for terms
+// whose tau table would cancel or blow up (slow[t]).
+__device__ __noinline__ double2 slow_ratio(const EnergyArgs& a, const uint32_t* xbits, int t, double d) {
+  const int M = a.M, N = a.N;
+  double2 lsum = make_double2(0.0, 0.0);
+  for (int i = 0; i < M; ++i) {
+    double2 z = a.b[i];
+    for (int k = 0; k < N; ++k)
+      if ((xbits[k >> 5] >> (k & 31)) & 1u) {
+        const double2 e = a.w_t[(size_t)k * M + i];
+        z.x += e.x;
+        z.y += e.y;
+      }
+    const double2 w = term_w(a, t, i);
+    const double2 l1 = clogcosh(make_double2(z.x + d * w.x, z.y + d * w.y));
+    const double2 l0 = clogcosh(z);
+    lsum.x += l1.x - l0.x;
+    lsum.y += l1.y - l0.y;
+  }
+  double2 at;
+  if (a.ham == MPV_HAM_TFIM) {
+    at = a.a[t];
+  } else {
+    const int p = a.bonds[2 * t], q = a.bonds[2 * t + 1];
+    at = make_double2(a.a[p].x - a.a[q].x, a.a[p].y - a.a[q].y);
+  }
+  return cexp_(make_double2(lsum.x + d * at.x, lsum.y + d * at.y));
+}
+
+// One block = SB samples x all terms.  Thread (g, t) = (tid / T, tid % T)
+// owns term t for the ST samples of group g (groups and terms are flattened
+// over the block, so only the last warp has idle lanes).
+// Phase 1: theta[s][i] = b_i + sum_k x[s][k] W_t[k][i] as a real GEMM
+//   X[SB x N] (0/1) . Wr[N x 2M] on DMMA m8n8k4 tiles; W_t rows are staged by
+//   bulk copies into a padded pitch (2M + 8 doubles: the four k-rows of a
+//   fragment land on disjoint bank halves); A fragments come from the per-site
+//   sample masks.  The D fragment (row s, cols 2i, 2i+1) is exactly theta_i(s).
+//   tanh(theta) is then formed in place by one rolled loop.
+// Phase 2: each thread keeps ST running products of (1 + d tanh(theta) tau)
+//   in registers; tau rows are staged by bulk copies and read per lane,
+//   tanh(theta) as broadcasts.  Ratios go to shared memory and one warp per
+//   sample sums the terms in a fixed order (deterministic).
+constexpr int kST4Threads = 448;  // block size cap of the 4-samples-per-thread variant (2 blocks/SM)
+
+template <int ST, int KT>
+__global__ void __launch_bounds__(ST == 4 ? kST4Threads : 512, ST == 4 ? 2 : 1) energy_kernel(const EnergyArgs a, const EnergyPlan pl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int M = a.M, T = a.n_terms, words = a.words, N = a.N;
-  const int SB = ST * NG;
-  const int TT = (T + 31) / 32 * 32;  // threads per group
-  double2* tt = reinterpret_cast<double2*>(smem_raw);                  // [M][SB]
-  uint32_t* wsm = reinterpret_cast<uint32_t*>(tt + (size_t)SB * M);    // [SB][32]
-  uint32_t* smask = wsm + SB * 32;                                     // [N], padded to 16 B
-  double* red = reinterpret_cast<double*>(smask + ((N + 3) / 4) * 4);  // [SB][16 warps][2]
-  unsigned char* stage_base = reinterpret_cast<unsigned char*>(red + kMaxSB * 16 * 2);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_base + 2 * (size_t)stage_bytes);
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int SB = pl.SB, NG = SB / ST, rows = pl.rows;
+  double2* tt = reinterpret_cast<double2*>(smem_raw);  // [M][SB]
+  unsigned char* tstage = smem_raw + (size_t)SB * M * sizeof(double2);
+  uint32_t* wsm = reinterpret_cast<uint32_t*>(smem_raw + pl.pool_bytes);  // [SB][32]
+  uint32_t* smask = wsm + SB * 32;                                         // [energy_mask_pad(N)]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smask + energy_mask_pad(N));  // 16
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int64_t s0 = (int64_t)blockIdx.x * SB;
-  Stager st;
-  st.init(stage_base, stage_bytes, bars, tid);
+  if (tid == 0) Pipe::init_bars(bars, 2, nwarps);
+  Pipe pw, pt;
+  pw.init(smem_raw, (uint32_t)pl.wbuf_bytes, pl.nbw, bars);
+  pt.init(tstage, (uint32_t)pl.tbuf_bytes, pl.nbt, bars + 8);
+  const int pitch = energy_w_pitch(M);
+  const int nW = energy_w_rows(N) / kWRows;
+  auto issueW = [&](int c, int b) {
+    pw.expect(b, (uint32_t)pl.wbuf_bytes);
+    pw.copy(b, 0, a.wp + (size_t)c * kWRows * pitch, (uint32_t)pl.wbuf_bytes);
+  };
+  __syncthreads();  // barriers initialised
+  if (tid == 0 && !(pl.skip & 1))
+    for (int c = 0; c < min(pl.nbw, nW); ++c) issueW(c, c);
 
   for (int idx = tid; idx < SB * 32; idx += blockDim.x) {
     const int s = idx >> 5, w = idx & 31;
     wsm[idx] = (w < words && s0 + s < a.B) ? a.bits[(s0 + s) * words + w] : 0u;
   }
   __syncthreads();
-  for (int k = tid; k < N; k += blockDim.x) {
+  for (int k = tid; k < energy_mask_pad(N); k += blockDim.x) {
     uint32_t m = 0;
-    for (int s = 0; s < SB; ++s) m |= ((wsm[s * 32 + (k >> 5)] >> (k & 31)) & 1u) << s;
+    if (k < N)
+      for (int s = 0; s < SB; ++s) m |= ((wsm[s * 32 + (k >> 5)] >> (k & 31)) & 1u) << s;
     smask[k] = m;
   }
-  // 0/1 multipliers x[k][s] as doubles (theta phase uses DFMA, no selects)
-  double* xk = reinterpret_cast<double*>(stage_base + 2 * (size_t)stage_bytes + 16);  // [N][kMaxSB]
-  for (int idx = tid; idx < N * kMaxSB; idx += blockDim.x) {
-    const int k = idx / kMaxSB, s2 = idx % kMaxSB;
-    xk[idx] = (s2 < SB) ? (double)((wsm[s2 * 32 + (k >> 5)] >> (k & 31)) & 1u) : 0.0;
+  __syncthreads();
+  // ---- phase 1: theta on DMMA (one pass: the launch gives every warp <= KT tiles) ----
+  const int NT = (M + 3) / 4;  // n-tiles of 8 real columns (4 units)
+  const int MT = SB / 8;       // m-tiles of 8 samples
+  const int qr = lane & 3, qc = lane >> 2;
+  double acc[KT][2][2];
+  int col[KT];  // B column of tile j (clamped: surplus tiles compute and are dropped)
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    const int nt = warp + j * nwarps;
+    col[j] = min(nt, NT - 1) * 8 + qc;
+    const int i = nt * 4 + qr;
+    const double2 bi = i < M ? a.b[i] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int m = 0; m < 2; ++m) { acc[j][m][0] = bi.x; acc[j][m][1] = bi.y; }
   }
-  // ---- phase 1: theta ----
-  {
-    const int rW = stage_bytes / (M * (int)sizeof(double2));
-    const int nW = (N + rW - 1) / rW;
-    auto issueW = [&](int c) {
-      const int k0 = c * rW, nr = min(rW, N - k0);
-      st.issue(c & 1, a.w_t + (size_t)k0 * M, (uint32_t)(nr * M * sizeof(double2)), nullptr, 0, 0);
-    };
-    if (tid == 0) {
-      issueW(0);
-      if (nW > 1) issueW(1);
-    }
-    __syncthreads();  // masks ready
-    double zr[kMaxSB], zi[kMaxSB];
-    const int i = tid;
-    if (i < M) {
-      const double2 b = a.b[i];
+  Pipe::Pos wpos{0, 0u};
+  for (int c = 0; c < ((pl.skip & 1) ? 0 : nW); ++c) {
+    pw.wait_full(wpos.slot, wpos.ph);
+    const double* wbuf = reinterpret_cast<const double*>(smem_raw + (size_t)wpos.slot * pl.wbuf_bytes);
 #pragma unroll
-      for (int s = 0; s < kMaxSB; ++s) { zr[s] = b.x; zi[s] = b.y; }
-    }
-    for (int c = 0; c < nW; ++c) {
-      const int b = c & 1;
-      st.wait(b);
-      if (i < M) {
-        const double2* wr = reinterpret_cast<const double2*>(stage_base + (size_t)b * stage_bytes) + i;
-        const int k0 = c * rW, nr = min(rW, N - k0);
-        for (int r = 0; r < nr; ++r) {
-          const double2 w = wr[r * M];
-          const double* xr = xk + (k0 + r) * kMaxSB;
+    for (int kk = 0; kk < kWRows; kk += 4) {
+      const double* brow = wbuf + (kk + qr) * pitch;
+      double bf[KT];
 #pragma unroll
-          for (int s = 0; s < kMaxSB; ++s) {
-            const double x = xr[s];
-            zr[s] = fma(x, w.x, zr[s]);
-            zi[s] = fma(x, w.y, zi[s]);
-          }
-        }
+      for (int j = 0; j < KT; ++j) bf[j] = brow[col[j]];
+      const uint32_t mk = smask[c * kWRows + kk + qr];  // zero past N
+      double af[2];
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+        af[m] = __hiloint2double((int)(((mk >> (m * 8 + qc)) & 1u) * 0x3ff00000u), 0);
+#pragma unroll
+      for (int j = 0; j < KT; ++j) dmma_8x8x4(acc[j][0][0], acc[j][0][1], af[0], bf[j]);
+      if (MT > 1) {
+#pragma unroll
+        for (int j = 0; j < KT; ++j) dmma_8x8x4(acc[j][1][0], acc[j][1][1], af[1], bf[j]);
       }
-      __syncthreads();
-      if (tid == 0 && c + 2 < nW) issueW(c + 2);
     }
-    if (i < M) {
+    pw.release(wpos.slot, lane);
+    if (tid == 0 && c + pl.nbw < nW) {
+      pw.wait_empty(wpos.slot, wpos.ph);
+      issueW(c + pl.nbw, wpos.slot);
+    }
+    pw.advance(wpos);
+  }
+  __syncthreads();  // every W read done: the pool is free
+  const bool any_terms = (a.ham == MPV_HAM_HEISENBERG) || (a.h != 0.0);
+  const int nchunks = (M + rows - 1) / rows;
+  const uint32_t trow_bytes = (uint32_t)T * sizeof(double2);
+  auto issueT = [&](int c, int b) {
+    const int r0 = c * rows, nr = min(rows, M - r0);
+    pt.expect(b, nr * trow_bytes);
+    pt.copy(b, 0, a.tau + (size_t)r0 * T, nr * trow_bytes);
+  };
+  if (any_terms && !(pl.skip & 4) && tid == 0)
+    for (int c = 0; c < min(pl.nbt, nchunks); ++c) issueT(c, c);
+  // D fragment (row s = m*8 + qc, cols 2i, 2i+1) -> tanh(theta_i(s)) into tt[i][s]
 #pragma unroll
-      for (int s = 0; s < kMaxSB; ++s)
-        if (s < SB) tt[i * SB + s] = ctanh(make_double2(zr[s], zi[s]));
+  for (int j = 0; j < KT; ++j) {
+    const int nt = warp + j * nwarps, i = nt * 4 + qr;
+    if (nt < NT && i < M) {
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+        if (m < MT) tt[i * SB + m * 8 + qc] = make_double2(acc[j][m][0], acc[j][m][1]);
     }
+  }
+  __syncthreads();
+  // two independent tanh chains per iteration (latency-bound otherwise)
+  for (int idx = tid; idx < ((pl.skip & 2) ? 0 : M * SB); idx += 2 * blockDim.x) {
+    const int idx2 = idx + blockDim.x;
+    const double2 z0 = tt[idx], z1 = idx2 < M * SB ? tt[idx2] : make_double2(0.0, 0.0);
+    const double2 t0 = ctanh_fast(z0), t1 = ctanh_fast(z1);
+    tt[idx] = t0;
+    if (idx2 < M * SB) tt[idx2] = t1;
   }
   __syncthreads();
 
   auto bit_of = [&](int s, int k) -> int { return (wsm[s * 32 + (k >> 5)] >> (k & 31)) & 1u; };
-  const int g = tid / TT, t = tid % TT;
-  const bool any_terms = (a.ham == MPV_HAM_HEISENBERG) || (a.h != 0.0);
-  double2 ratio[ST];
-  double dd[ST];
+  const int g = tid / T, t = tid - g * T;
   double2 P[ST];
   int E[ST];
+  uint32_t sg[ST];  // sign bit of d on the high word (d = -1 -> flip tanh(theta))
+  uint32_t nz = 0;  // bit j: d_j != 0
 #pragma unroll
   for (int j = 0; j < ST; ++j) {
-    ratio[j] = make_double2(0.0, 0.0);
-    dd[j] = 0.0;
     P[j] = make_double2(1.0, 0.0);
     E[j] = 0;
+    sg[j] = 0;
   }
-  const bool active = any_terms && g < NG && t < T;
+  const bool active = any_terms && g < NG;
   bool slow = false;
   const double2* tg = tt;
-  int p = 0, q = 0;
   if (active) {
-    if (a.ham == MPV_HAM_TFIM) p = t;
-    else { p = a.bonds[2 * t]; q = a.bonds[2 * t + 1]; }
+    int p = t, q = 0;
+    if (a.ham != MPV_HAM_TFIM) { p = a.bonds[2 * t]; q = a.bonds[2 * t + 1]; }
 #pragma unroll
     for (int j = 0; j < ST; ++j) {
       const int s = g * ST + j;
-      dd[j] = (a.ham == MPV_HAM_TFIM) ? (double)(1 - 2 * bit_of(s, p)) : (double)(bit_of(s, q) - bit_of(s, p));
+      const int d = (a.ham == MPV_HAM_TFIM) ? 1 - 2 * bit_of(s, p) : bit_of(s, q) - bit_of(s, p);
+      sg[j] = d < 0 ? 0x80000000u : 0u;
+      nz |= (d != 0 ? 1u : 0u) << j;
     }
     slow = a.slow[t] != 0;
     tg = tt + g * ST;
   }
   // ---- phase 2: products over hidden units ----
-  if (any_terms) {
-    const int nchunks = (M + kRows - 1) / kRows;
-    const uint32_t row_bytes = (uint32_t)T * sizeof(double2);
-    auto issueCS = [&](int c) {
-      const int r0 = c * kRows, nr = min(kRows, M - r0);
-      st.issue(c & 1, a.C + (size_t)r0 * T, nr * row_bytes, a.S + (size_t)r0 * T, kRows * row_bytes, nr * row_bytes);
-    };
-    if (tid == 0) {
-      issueCS(0);
-      if (nchunks > 1) issueCS(1);
-    }
+  if (any_terms && !(pl.skip & 4)) {
+    Pipe::Pos tpos{0, 0u};
     for (int c = 0; c < nchunks; ++c) {
-      const int b = c & 1;
-      st.wait(b);
+      pt.wait_full(tpos.slot, tpos.ph);
       if (active && !slow) {
         // shared-space pointers derived from the dynamic smem array (LDS, not generic LD)
-        const double2* Cs = reinterpret_cast<const double2*>(stage_base + (size_t)b * stage_bytes) + t;
-        const double2* Ss = Cs + kRows * T;
-        const int r0 = c * kRows, nr = min(kRows, M - r0);
-        const double2* trow = tg + (size_t)r0 * SB;
-        for (int r = 0; r < nr; ++r, trow += SB) {
-          const double2 cv = Cs[r * T], sv = Ss[r * T];
-          // three independent phases over the ST samples: ts = tanh*S, f = C + d ts, P *= f
-          double2 f[ST];
+        const double2* tp = reinterpret_cast<const double2*>(tstage + (size_t)tpos.slot * pl.tbuf_bytes) + t;
+        const int r0 = c * rows, nr = min(rows, M - r0);
+        const double2* vp = tg + (size_t)r0 * SB;
+#pragma unroll 2
+        for (int r = 0; r < nr; ++r) {
+          // all loads of the row first (tau per lane, tanh(theta) broadcasts)
+          const double2 tau = *tp;
+          double2 tv[ST];
+#pragma unroll
+          for (int j = 0; j < ST; ++j) tv[j] = vp[j];
+          tp += T;
+          vp += SB;
+          // u = (d tanh theta) tau, P += P u
 #pragma unroll
           for (int j = 0; j < ST; ++j) {
-            const double2 tv = trow[j];
-            f[j] = make_double2(fma(tv.x, sv.x, -tv.y * sv.y), fma(tv.x, sv.y, tv.y * sv.x));
+            tv[j].x = __hiloint2double(__double2hiint(tv[j].x) ^ (int)sg[j], __double2loint(tv[j].x));
+            tv[j].y = __hiloint2double(__double2hiint(tv[j].y) ^ (int)sg[j], __double2loint(tv[j].y));
+            const double2 u = cmul(tv[j], tau);
+            const double px = P[j].x, py = P[j].y;
+            P[j].x = fma(px, u.x, fma(-py, u.y, px));
+            P[j].y = fma(px, u.y, fma(py, u.x, py));
           }
-#pragma unroll
-          for (int j = 0; j < ST; ++j) f[j] = make_double2(fma(dd[j], f[j].x, cv.x), fma(dd[j], f[j].y, cv.y));
-#pragma unroll
-          for (int j = 0; j < ST; ++j) P[j] = cmul(P[j], f[j]);
         }
-        if ((c & 3) == 3) {
+        if (c & 1) {
 #pragma unroll
           for (int j = 0; j < ST; ++j) renorm(P[j], E[j]);
         }
       }
-      __syncthreads();  // buffer b consumed by every thread
-      if (tid == 0 && c + 2 < nchunks) issueCS(c + 2);
+      pt.release(tpos.slot, lane);
+      if (tid == 0 && c + pl.nbt < nchunks) {
+        pt.wait_empty(tpos.slot, tpos.ph);
+        issueT(c + pl.nbt, tpos.slot);
+      }
+      pt.advance(tpos);
     }
   }
+  __syncthreads();  // all reads of tt and the staging buffers done
+  // ratios -> R [SB][T] (reuses tt + staging: all reads of them are done)
+  double2* R = tt;
   if (active) {
 #pragma unroll
     for (int j = 0; j < ST; ++j) {
       const int s = g * ST + j;
-      if (s0 + s >= a.B || dd[j] == 0.0) continue;
-      if (slow) {
-        // log-cosh difference (ref formulation) with theta recomputed here
-        double2 lsum = make_double2(0.0, 0.0);
-        for (int i = 0; i < M; ++i) {
-          double2 z = a.b[i];
-          for (int k = 0; k < N; ++k)
-            if (bit_of(s, k)) {
-              const double2 e = a.w_t[(size_t)k * M + i];
-              z.x += e.x;
-              z.y += e.y;
-            }
-          double2 w = a.w_t[(size_t)p * M + i];
-          if (a.ham != MPV_HAM_TFIM) {
-            const double2 w2 = a.w_t[(size_t)q * M + i];
-            w = make_double2(w.x - w2.x, w.y - w2.y);
+      double2 v = make_double2(0.0, 0.0);
+      if (s0 + s < a.B && ((nz >> j) & 1u)) {
+        if (slow) {
+          v = slow_ratio(a, wsm + s * 32, t, sg[j] ? -1.0 : 1.0);
+        } else {
+          v = cmul(a.ea[2 * t + (sg[j] ? 1 : 0)], P[j]);
+          const int k = E[j] + a.ec[t];
+          if (k >= -1022 && k <= 1023) {  // exact power-of-two scale (correctly rounded, like ldexp)
+            const double f = __longlong_as_double((long long)(k + 1023) << 52);
+            v.x *= f;
+            v.y *= f;
+          } else {
+            const int k1 = max(-1000, min(1000, k));
+            v.x = ldexp(ldexp(v.x, k1), k - k1);
+            v.y = ldexp(ldexp(v.y, k1), k - k1);
           }
-          const double2 l1 = clogcosh(make_double2(z.x + dd[j] * w.x, z.y + dd[j] * w.y));
-          const double2 l0 = clogcosh(z);
-          lsum.x += l1.x - l0.x;
-          lsum.y += l1.y - l0.y;
         }
-        double2 at;
-        if (a.ham == MPV_HAM_TFIM) at = a.a[p];
-        else at = make_double2(a.a[p].x - a.a[q].x, a.a[p].y - a.a[q].y);
-        ratio[j] = cexp_(make_double2(lsum.x + dd[j] * at.x, lsum.y + dd[j] * at.y));
-      } else {
-        const double2 e = a.ea[2 * t + (dd[j] > 0 ? 0 : 1)];
-        double2 v = cmul(e, P[j]);
-        const int k = E[j];
-        const int k1 = max(-1000, min(1000, k));
-        v.x = ldexp(v.x, k1);
-        v.y = ldexp(v.y, k1);
-        if (k != k1) {
-          v.x = ldexp(v.x, k - k1);
-          v.y = ldexp(v.y, k - k1);
-        }
-        ratio[j] = v;
       }
-    }
-  }
-  // fixed-order reduction: warp butterfly, then the group's warps in order
-  const int wg = t >> 5;  // warp index within the group
-#pragma unroll
-  for (int j = 0; j < ST; ++j) {
-    const double vr = segment_sum(ratio[j].x, 32), vi = segment_sum(ratio[j].y, 32);
-    if (lane == 0 && g < NG) {
-      red[((g * ST + j) * 16 + wg) * 2] = vr;
-      red[((g * ST + j) * 16 + wg) * 2 + 1] = vi;
+      R[s * T + t] = v;
     }
   }
   __syncthreads();
-  if (tid < SB && s0 + tid < a.B) {
-    const int s = tid;
+  // fixed-order sums: warp w takes samples w, w + nwarps, ...; lane l sums
+  // terms l, l + 32, ... then a butterfly
+  for (int s = warp; s < SB; s += nwarps) {
+    if (s0 + s >= a.B) continue;
     double er = 0.0, ei = 0.0;
     if (any_terms)
-      for (int w = 0; w < TT / 32; ++w) {
-        er += red[(s * 16 + w) * 2];
-        ei += red[(s * 16 + w) * 2 + 1];
+      for (int u = lane; u < T; u += 32) {
+        er += R[s * T + u].x;
+        ei += R[s * T + u].y;
       }
-    double diag = 0.0;  // ref vmc.py:52-57
-    for (int b = 0; b < a.n_bonds; ++b) {
-      const int xp = bit_of(s, a.bonds[2 * b]), xq = bit_of(s, a.bonds[2 * b + 1]);
-      diag += (double)((1 - 2 * xp) * (1 - 2 * xq));
-    }
-    const double coef = (a.ham == MPV_HAM_TFIM) ? a.h : 2.0 * a.J;
-    const double2 eps = make_double2(a.J * diag + coef * er, coef * ei);
-    a.out[s0 + s] = eps;
-    if ((!isfinite(eps.x) || !isfinite(eps.y)) && a.status) {
-      atomicMin((unsigned long long*)&a.status[1], (unsigned long long)(s0 + s));
-      atomicExch((unsigned long long*)&a.status[0], (unsigned long long)MPV_ERR_NONFINITE);
+    // ref vmc.py:52-57: sum_b s_p s_q = n_bonds - 2 #(anti-aligned bonds), exact in integers
+    int anti = 0;
+    for (int b = lane; b < a.n_bonds; b += 32) anti += bit_of(s, a.bonds[2 * b]) ^ bit_of(s, a.bonds[2 * b + 1]);
+    er = segment_sum(er, 32);
+    ei = segment_sum(ei, 32);
+    const double diag = (double)(a.n_bonds - 2 * __reduce_add_sync(0xffffffffu, anti));
+    if (lane == 0) {
+      const double coef = (a.ham == MPV_HAM_TFIM) ? a.h : 2.0 * a.J;
+      const double2 eps = make_double2(a.J * diag + coef * er, coef * ei);
+      a.out[s0 + s] = eps;
+      if ((!isfinite(eps.x) || !isfinite(eps.y)) && a.status) {
+        atomicMin((unsigned long long*)&a.status[1], (unsigned long long)(s0 + s));
+        atomicExch((unsigned long long*)&a.status[0], (unsigned long long)MPV_ERR_NONFINITE);
+      }
     }
   }
 }
-
-constexpr int kEnergyST = 8;  // samples per thread
 
 }  // namespace mpv
