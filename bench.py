@@ -209,7 +209,8 @@ def run_ours(args, rank, world, local_rank):
         if it > 0:
             e2e_ms += t0.elapsed_time(t1)
         snap = ev_e2e.snapshot
-        h2d = snap._table.numel() + snap._bias.numel() + snap._vis_im.numel() * 8 + samples.shape[0] * ens.words * 4
+        # snapshot upload + the uint8 sample rows re-uploaded by local_energies (packed on the device)
+        h2d = snap._table.numel() + snap._bias.numel() + snap._vis_im.numel() * 8 + samples.nbytes
         d2h = samples.nbytes + eps.nbytes + 3 * 16  # samples, eps, status words
     e2e_ms /= n_e2e
     if dist is not None:

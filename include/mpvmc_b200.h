@@ -77,6 +77,23 @@ typedef struct {
   double quantum; /* XI: table integers are multiples of this power of two */
 } mpv_snapshot;
 
+/* ---- snapshot build on the device (ref: rbm.py:91-101 round_parameters and
+ *      rbm.py:161-200 _PreparedRounded) ----
+ * mpv_snapshot_bytes: out[0] = bytes of the [table | vis] blob, out[1] = offset
+ * of vis in it, out[2] = bias bytes, for the layout (fmt, mode, variant, hidden_pad).
+ * mpv_snapshot_round: params = [a (N) | b (M) | w_t (N x M)] complex f64 (re, im)
+ * on the device; writes every component rounded RNE to fmt into `rounded` (same
+ * layout) and plan[0..3] = {finest power-of-two quantum of a_re, b, w (1 if all
+ * zero), max_i |b_re_i| + sum_k |w_re_ki|, the same for im, sum_k |a_re_k|}
+ * (`plan` >= 8 doubles of device scratch): the inputs of the exact-accumulator
+ * planner (paper_2601_20782_b200/rbm.py plan_exact).
+ * mpv_snapshot_fill: writes table/bias/vis (and vis_im if set) of `snap`, whose
+ * layout fields and buffers the caller has set, from `rounded`; split = X2 grid. */
+int mpv_snapshot_bytes(int n_visible, int hidden_pad, int fmt, int mode, int variant, size_t* out);
+int mpv_snapshot_round(int N, int M, int fmt, const double* params, double* rounded, double* plan,
+                       void* stream);
+int mpv_snapshot_fill(const mpv_snapshot* snap, const double* rounded, double split, void* stream);
+
 /* Chain state of one shard (device pointers; ref: sampler.py:55-65 state). */
 typedef struct {
   int64_t n_chains;     /* chains in this shard */

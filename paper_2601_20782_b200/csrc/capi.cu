@@ -9,6 +9,7 @@
 
 #include "energy.cuh"
 #include "perop.cuh"
+#include "snapshot.cuh"
 #include "sweep.cuh"
 
 namespace mpv {
@@ -254,6 +255,43 @@ int mpv_stream_uniforms(uint64_t key, int64_t n_chains, int64_t chain0, int64_t 
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   stream_uniforms_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(key, n_chains, chain0, t0, n_draws, out);
   return check_launch("stream_uniforms");
+}
+
+int mpv_snapshot_bytes(int n_visible, int hidden_pad, int fmt, int mode, int variant, size_t* out) {
+  if (n_visible < 1 || hidden_pad < 1 || fmt < MPV_FMT_F64 || fmt > MPV_FMT_BF16 || !out)
+    return fail(MPV_ERR_ARGS, "snapshot_bytes: bad args");
+  const bool f64arith = (fmt == MPV_FMT_F64) || (mode == MPV_MODE_STORAGE_ONLY);
+  const int kfmt = f64arith ? MPV_FMT_F64 : fmt, var = f64arith ? MPV_ACC_F64 : variant;
+  const size_t t16 = ((size_t)n_visible * hidden_pad * entry_bytes(kfmt, var) + 15) & ~(size_t)15;
+  out[0] = t16 + (((size_t)n_visible * vis_bytes(kfmt, var) + 15) & ~(size_t)15);  // [table | vis]
+  out[1] = t16;                                                                     // vis offset
+  out[2] = ((size_t)hidden_pad * entry_bytes(kfmt, var) + 15) & ~(size_t)15;        // bias
+  return MPV_OK;
+}
+
+int mpv_snapshot_round(int N, int M, int fmt, const double* params, double* rounded, double* plan, void* stream) {
+  if (N < 1 || M < 1 || fmt < MPV_FMT_F64 || fmt > MPV_FMT_BF16 || !params || !rounded || !plan)
+    return fail(MPV_ERR_ARGS, "snapshot_round: bad args");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(plan, 0, 8 * sizeof(double), st) != cudaSuccess) return check_launch("snapshot_round");
+  const int64_t n = 2 * ((int64_t)N + M + (int64_t)N * M);
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  snapshot_round_kernel<<<grid, 256, 0, st>>>(N, M, fmt, params, rounded, plan);
+  snapshot_bound_kernel<<<(M + 127) / 128, 128, 0, st>>>(N, M, rounded, plan);
+  return check_launch("snapshot_round");
+}
+
+int mpv_snapshot_fill(const mpv_snapshot* snap, const double* rounded, double split, void* stream) {
+  if (!snap || !rounded || !snap->table || !snap->bias || !snap->vis || snap->n_visible < 1 ||
+      snap->hidden_pad < snap->n_hidden || snap->n_hidden < 1)
+    return fail(MPV_ERR_ARGS, "snapshot_fill: bad args");
+  if (snap->variant == MPV_ACC_XI && !(snap->quantum > 0.0)) return fail(MPV_ERR_ARGS, "snapshot_fill: XI quantum");
+  if (snap->variant == MPV_ACC_X2 && snap->mode == MPV_MODE_NATIVE && !(split > 0.0))
+    return fail(MPV_ERR_ARGS, "snapshot_fill: X2 split");
+  const int64_t n = (int64_t)(snap->n_visible + 1) * snap->hidden_pad + snap->n_visible;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  snapshot_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(*snap, rounded, split);
+  return check_launch("snapshot_fill");
 }
 
 int mpv_chains_init(const mpv_chains* ch, uint64_t key, int proposal, int sector_weight, void* stream) {
@@ -552,8 +590,10 @@ int mpv_local_energies(int N, int M, const double* a, const double* b, const dou
       else { kt = 8; threads = std::max(threads, 32 * ((NT + 7) / 8)); }
     }
     if (threads > (cf.st == 4 ? kST4Threads : 512)) continue;
-    for (int nbt = 3; nbt >= 2; --nbt)
-      for (int rows = 12; rows >= 2; rows -= 2) {
+    static const int nbt0 = getenv("MPV_ENERGY_NBT") ? atoi(getenv("MPV_ENERGY_NBT")) : 3;
+    static const int rows0 = getenv("MPV_ENERGY_ROWS") ? atoi(getenv("MPV_ENERGY_ROWS")) : 12;
+    for (int nbt = nbt0; nbt >= 2; --nbt)
+      for (int rows = rows0; rows >= 2; rows -= 2) {
         EnergyPlan pl;
         const size_t smem = energy_plan(N, M, T, cf.sb, rows, nbt, &pl);
         static const int skip = getenv("MPV_ENERGY_SKIP") ? atoi(getenv("MPV_ENERGY_SKIP")) : 0;

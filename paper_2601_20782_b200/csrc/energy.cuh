@@ -147,6 +147,7 @@ __global__ void energy_tables_kernel(const EnergyArgs a, double2* tau, double2* 
 //   sample masks (zero beyond N), 16 mbarriers (two Pipes).
 constexpr int kMaxSB = 16;  // samples per block
 constexpr int kWRows = 8;   // W rows per staged chunk (two DMMA k-steps)
+constexpr int kMaxBufs = 8; // ring depth limit per Pipe
 
 struct EnergyPlan {
   int SB, rows, nbt, nbw;          // samples/block, tau rows/chunk, tau buffers, W buffers
@@ -169,18 +170,18 @@ inline size_t energy_plan(int N, int M, int T, int SB, int rows, int nbt, Energy
   pool = (pool + 127) / 128 * 128;
   p->pool_bytes = (int)pool;
   p->nbw = (int)(pool / p->wbuf_bytes);
-  if (p->nbw > 4) p->nbw = 4;
-  return pool + (size_t)SB * 32 * 4 + (size_t)energy_mask_pad(N) * 4 + 16 * 8;
+  if (p->nbw > kMaxBufs) p->nbw = kMaxBufs;
+  return pool + (size_t)SB * 32 * 4 + (size_t)energy_mask_pad(N) * 4 + 4 * kMaxBufs * 8;
 }
 
-// Bulk-async (TMA engine) ring of nb <= 4 buffers in shared memory.  Per
+// Bulk-async (TMA engine) ring of nb <= kMaxBufs buffers in shared memory.  Per
 // buffer a "full" mbarrier (count 1 + transaction bytes; thread 0 issues) and
 // an "empty" mbarrier (one arrival per warp once the warp has read the chunk).
 // Chunk c uses buffer c % nb, that buffer's (c / nb)-th completion, so waits
 // are on parity (c / nb) & 1 (tracked incrementally by Pos).  No block-wide barrier per chunk: only the
 // producer thread waits for the slowest warp before refilling a buffer.
 struct Pipe {
-  uint32_t buf_addr0, bar_addr0, bytes;  // bars: full[0..3], empty[0..3]
+  uint32_t buf_addr0, bar_addr0, bytes;  // bars: full[kMaxBufs], empty[kMaxBufs]
   int nb;
   __device__ void init(const unsigned char* base, uint32_t buf_bytes, int n_buf, const uint64_t* bars) {
     buf_addr0 = (uint32_t)__cvta_generic_to_shared(base);
@@ -191,12 +192,13 @@ struct Pipe {
   __device__ static void init_bars(const uint64_t* bars, int n_pipes, int n_warps) {
     const uint32_t b0 = (uint32_t)__cvta_generic_to_shared(bars);
     for (int p = 0; p < n_pipes; ++p)
-      for (int k = 0; k < 8; ++k)
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b0 + 8 * (8 * p + k)), "r"(k < 4 ? 1 : n_warps));
+      for (int k = 0; k < 2 * kMaxBufs; ++k)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b0 + 8 * (2 * kMaxBufs * p + k)),
+                     "r"(k < kMaxBufs ? 1 : n_warps));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __device__ uint32_t full(int b) const { return bar_addr0 + 8 * b; }
-  __device__ uint32_t empty(int b) const { return bar_addr0 + 32 + 8 * b; }
+  __device__ uint32_t empty(int b) const { return bar_addr0 + 8 * kMaxBufs + 8 * b; }
   __device__ uint32_t buf(int b) const { return buf_addr0 + b * bytes; }
   __device__ void expect(int b, uint32_t total) const {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full(b)), "r"(total) : "memory");
@@ -305,13 +307,13 @@ __global__ void __launch_bounds__(ST == 4 ? kST4Threads : 512, ST == 4 ? 2 : 1) 
   unsigned char* tstage = smem_raw + (size_t)SB * M * sizeof(double2);
   uint32_t* wsm = reinterpret_cast<uint32_t*>(smem_raw + pl.pool_bytes);  // [SB][32]
   uint32_t* smask = wsm + SB * 32;                                         // [energy_mask_pad(N)]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smask + energy_mask_pad(N));  // 16
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smask + energy_mask_pad(N));  // 4 * kMaxBufs
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int64_t s0 = (int64_t)blockIdx.x * SB;
   if (tid == 0) Pipe::init_bars(bars, 2, nwarps);
   Pipe pw, pt;
   pw.init(smem_raw, (uint32_t)pl.wbuf_bytes, pl.nbw, bars);
-  pt.init(tstage, (uint32_t)pl.tbuf_bytes, pl.nbt, bars + 8);
+  pt.init(tstage, (uint32_t)pl.tbuf_bytes, pl.nbt, bars + 2 * kMaxBufs);
   const int pitch = energy_w_pitch(M);
   const int nW = energy_w_rows(N) / kWRows;
   auto issueW = [&](int c, int b) {

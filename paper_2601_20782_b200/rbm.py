@@ -13,6 +13,7 @@ trip) so reference callers keep working.
 """
 from __future__ import annotations
 
+import ctypes
 import json
 import math
 from dataclasses import dataclass
@@ -160,16 +161,10 @@ class ExactPlan:
     split: float
 
 
-def plan_exact(snap: RbmParameters) -> ExactPlan:
-    a, b, w = snap.a, snap.b, snap.w
-    vals = np.concatenate([a.real, b.real, b.imag, w.real.ravel(), w.imag.ravel()])
-    q = finest_quantum(vals)
-    bound = max(
-        float(np.max(np.abs(b.real) + np.abs(w.real).sum(axis=1))),
-        float(np.max(np.abs(b.imag) + np.abs(w.imag).sum(axis=1))),
-        float(np.abs(a.real).sum()),
-    )
-    n_terms = snap.n_visible + 1
+def plan_from_bounds(q: float, bound_re: float, bound_im: float, bound_a: float, n_visible: int) -> ExactPlan:
+    """The planner's decision from the snapshot's quantum and bounds."""
+    bound = max(bound_re, bound_im, bound_a)
+    n_terms = n_visible + 1
     split = 2.0 ** math.floor(math.log2(2.0**25 * q / n_terms))
     if not (split >= q and bound + n_terms * split / 2 <= 2.0**24 * split):
         split = 0.0  # X2 not exact
@@ -182,35 +177,28 @@ def plan_exact(snap: RbmParameters) -> ExactPlan:
     return ExactPlan(nat.ACC_F64, q, bound, 0.0)
 
 
+def plan_exact(snap: RbmParameters) -> ExactPlan:
+    """Host planner on a rounded snapshot (the device computes the same four
+    numbers in mpv_snapshot_round)."""
+    a, b, w = snap.a, snap.b, snap.w
+    vals = np.concatenate([a.real, b.real, b.imag, w.real.ravel(), w.imag.ravel()])
+    return plan_from_bounds(finest_quantum(vals), float(np.max(np.abs(b.real) + np.abs(w.real).sum(axis=1))),
+                            float(np.max(np.abs(b.imag) + np.abs(w.imag).sum(axis=1))),
+                            float(np.abs(a.real).sum()), snap.n_visible)
+
+
 # ---------------------------------------------------------------------------
 # Device snapshot (kernel layout)
 # ---------------------------------------------------------------------------
 
-def _half_bits(x: np.ndarray, fmt: str) -> np.ndarray:
-    """uint16 bit patterns of values that are exactly representable in fmt."""
-    if fmt == "f16":
-        h = x.astype(np.float16)
-        return h.view(np.uint16)
-    f = x.astype(np.float32).view(np.uint32)
-    return (f >> np.uint32(16)).astype(np.uint16)
-
-
-def _pairs(re: np.ndarray, im: np.ndarray, fmt: str) -> np.ndarray:
-    """Entry array of (re, im) pairs in fmt: uint32 (f16/bf16) or float32x2."""
-    if fmt == "f32":
-        out = np.empty(re.shape + (2,), dtype=np.float32)
-        out[..., 0], out[..., 1] = re, im
-        return out
-    return _half_bits(re, fmt).astype(np.uint32) | (_half_bits(im, fmt).astype(np.uint32) << np.uint32(16))
-
-
-def _pad16(buf: bytes) -> bytes:
-    return buf + b"\0" * ((-len(buf)) % 16)
-
-
 class DeviceSnapshot:
     """Parameters of one evaluator in kernel layout, resident on the device
-    (the device counterpart of rbm.py:161-200 _PreparedRounded)."""
+    (the device counterpart of rbm.py:161-200 _PreparedRounded).
+
+    Built on the device: one upload of the f64 master parameters,
+    mpv_snapshot_round (RNE rounding to fmt + the planner's quantum/bounds),
+    the host planner's decision on those four numbers, then mpv_snapshot_fill
+    writes the table in the chosen layout."""
 
     def __init__(self, params: RbmParameters, fmt: FloatFormat, mode: RoundingMode, device=None,
                  variant: int | None = None):
@@ -220,22 +208,30 @@ class DeviceSnapshot:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.fmt, self.mode = fmt, mode
         f64arith = fmt.name == "f64" or mode is RoundingMode.STORAGE_ONLY
-        snap = round_parameters(params, fmt)
-        self.params = snap
-        N, M = snap.n_visible, snap.n_hidden
+        N, M = params.n_visible, params.n_hidden
         self.n_visible, self.n_hidden = N, M
-        wt = snap.w.T  # (N, M): column k of W is row k of the table
+        stream = nat.stream_handle(self.device)
+        # [a | b | w_t] as interleaved (re, im) f64, one pinned upload
+        host = torch.empty(2 * (N + M + N * M), dtype=torch.float64, pin_memory=True)
+        hv = host.numpy().view(np.complex128)
+        hv[:N], hv[N:N + M] = params.a, params.b
+        hv[N + M:].reshape(N, M)[:] = params.w.T
+        src = host.to(self.device, non_blocking=True)
+        self._rounded = torch.empty_like(src)
+        plan_dev = torch.empty(8, dtype=torch.float64, device=self.device)
+        nat.call("mpv_snapshot_round", N, M, fmt.code, src.data_ptr(), self._rounded.data_ptr(), plan_dev.data_ptr(),
+                 stream)
+        split = 0.0
+        quantum = 0.0
         if mode is RoundingMode.PER_OPERATION and not f64arith:
             G, U, Mpad = 1, M, M
             variant = nat.ACC_X1
-            table = _pairs(wt.real, wt.imag, fmt.name)
-            bias = _pairs(snap.b.real, snap.b.imag, fmt.name)
-            vis = snap.a.real.astype(np.float32)
         else:
             if f64arith:
                 variant = nat.ACC_F64
             else:
-                self.plan = plan_exact(snap)
+                pq = plan_dev.cpu().numpy()
+                self.plan = plan_from_bounds(float(pq[0]), float(pq[1]), float(pq[2]), float(pq[3]), N)
                 if variant is None:
                     variant = self.plan.variant
                 elif variant == nat.ACC_X1 and self.plan.variant != nat.ACC_X1:
@@ -244,59 +240,28 @@ class DeviceSnapshot:
                     raise ValueError("X2 accumulators are not exact for this snapshot")
                 elif variant == nat.ACC_XI and not self.plan.bound < 2.0**30 * self.plan.quantum:
                     raise ValueError("XI accumulators are not exact for this snapshot")
+                split = self.plan.split
+                if variant == nat.ACC_XI:
+                    quantum = self.plan.quantum
             G, U = nat.plan_layout(N, M, nat.FMT_F64 if f64arith else fmt.code, variant)
             Mpad = G * U
-            wpad = np.zeros((N, Mpad), dtype=np.complex128)
-            wpad[:, :M] = wt
-            bpad = np.zeros(Mpad, dtype=np.complex128)
-            bpad[:M] = snap.b
-            if variant == nat.ACC_F64:
-                table = np.stack([wpad.real, wpad.imag], axis=-1)
-                bias = np.stack([bpad.real, bpad.imag], axis=-1)
-                vis = snap.a.real.astype(np.float64)
-            elif variant == nat.ACC_X1:
-                table = _pairs(wpad.real, wpad.imag, fmt.name)
-                bias = _pairs(bpad.real, bpad.imag, fmt.name)
-                vis = snap.a.real.astype(np.float32)
-            elif variant == nat.ACC_XI:
-                q = self.plan.quantum
-
-                def ints(x):
-                    v = np.rint(x / q)
-                    assert np.array_equal(v * q, x), "XI: value not on the quantum grid"
-                    return v.astype(np.int32)
-
-                table = np.stack([ints(wpad.real), ints(wpad.imag)], axis=-1)
-                bias = np.stack([ints(bpad.real), ints(bpad.imag)], axis=-1)
-                vis = ints(snap.a.real)
-            else:
-                g = self.plan.split
-
-                def split(x):
-                    hi = np.rint(x / g) * g
-                    return hi, x - hi
-
-                whr, wlr = split(wpad.real)
-                whi, wli = split(wpad.imag)
-                bhr, blr = split(bpad.real)
-                bhi, bli = split(bpad.imag)
-                ahi, alo = split(snap.a.real)
-                th, tl = _pairs(whr, whi, fmt.name), _pairs(wlr, wli, fmt.name)
-                bh, bl = _pairs(bhr, bhi, fmt.name), _pairs(blr, bli, fmt.name)
-                table = np.stack([th, tl], axis=-2 if fmt.name == "f32" else -1)
-                bias = np.stack([bh, bl], axis=-2 if fmt.name == "f32" else -1)
-                vis = np.stack([ahi, alo], axis=-1).astype(np.float32)
         self.variant, self.lanes_per_chain, self.units_per_lane, self.hidden_pad = variant, G, U, Mpad
-        blob = _pad16(np.ascontiguousarray(table).tobytes()) + _pad16(np.ascontiguousarray(vis).tobytes())
-        self._table = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(self.device)
-        tbytes = len(_pad16(np.ascontiguousarray(table).tobytes()))
-        self._bias = torch.frombuffer(bytearray(_pad16(np.ascontiguousarray(bias).tobytes())),
-                                      dtype=torch.uint8).to(self.device)
-        self._vis_im = torch.from_numpy(np.ascontiguousarray(snap.a.imag, dtype=np.float64)).to(self.device)
+        sizes = (ctypes.c_size_t * 3)()
+        nat.call("mpv_snapshot_bytes", N, Mpad, fmt.code, mode.code, variant, sizes)
+        self._table = torch.zeros(int(sizes[0]), dtype=torch.uint8, device=self.device)  # zero padding
+        self._bias = torch.zeros(int(sizes[2]), dtype=torch.uint8, device=self.device)
+        self._vis_im = torch.empty(N, dtype=torch.float64, device=self.device)
         base = self._table.data_ptr()
-        quantum = self.plan.quantum if (variant == nat.ACC_XI) else 0.0
         self.struct = nat.Snapshot(N, M, Mpad, fmt.code, mode.code, variant, G, U,
-                                   base, self._bias.data_ptr(), base + tbytes, self._vis_im.data_ptr(), quantum)
+                                   base, self._bias.data_ptr(), base + int(sizes[1]), self._vis_im.data_ptr(), quantum)
+        nat.call("mpv_snapshot_fill", ctypes_byref(self.struct), self._rounded.data_ptr(), split, stream)
+
+    @property
+    def params(self) -> RbmParameters:
+        """The rounded snapshot (ref: rbm.py:91-101), read back from the device."""
+        r = self._rounded.cpu().numpy().view(np.complex128)
+        N, M = self.n_visible, self.n_hidden
+        return RbmParameters(r[:N].copy(), r[N:N + M].copy(), r[N + M:].reshape(N, M).T.copy())
 
     def scratch(self, n_chains: int):
         """Device scratch for the fused sweep over n_chains (work queue, parked theta)."""
@@ -328,7 +293,10 @@ def device_pack(bits, device):
 
     bits = np.ascontiguousarray(np.atleast_2d(bits), dtype=np.uint8)
     B, N = bits.shape
-    rows = torch.from_numpy(bits).to(device, non_blocking=False)
+    rows = torch.from_numpy(bits)
+    if B and not rows.is_pinned():  # stage through pinned memory (DMA instead of a pageable copy)
+        rows = torch.empty(rows.shape, dtype=torch.uint8, pin_memory=True).copy_(rows)
+    rows = rows.to(device, non_blocking=True)
     packed = torch.empty((B, (N + 31) // 32), dtype=torch.int32, device=device)
     if B:
         nat.call("mpv_pack_bits", rows.data_ptr(), B, N, packed.data_ptr(), nat.stream_handle(device))

@@ -257,13 +257,12 @@ class ChainEnsemble:
         if packed.shape[0]:
             nat.call("mpv_unpack_bits", packed.data_ptr(), packed.shape[0], self.n_sites, out.data_ptr(),
                      self._stream())
-        nbytes = out.numel()
-        if getattr(self, "_pinned", None) is None or self._pinned.numel() < nbytes:
-            self._pinned = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)  # reused across calls
-        host = self._pinned[:nbytes].view(out.shape)
+        # fresh pinned block from torch's caching host allocator (no host memcpy):
+        # the returned array keeps it alive, and device_pack() re-uploads it by DMA
+        host = torch.empty(out.shape, dtype=torch.uint8, pin_memory=True)
         host.copy_(out, non_blocking=True)
         torch.cuda.current_stream(self.device).synchronize()
-        return host.numpy().copy()
+        return host.numpy()
 
 
 def run_chains(n_chains, n_samples, burn_in_steps, thin_steps, seed, logprob, proposal: Proposal, n_sites):

@@ -90,8 +90,12 @@ def local_energies(spec, log_amplitude, bits) -> np.ndarray:
 
     packed = device_pack(bits, kern.device)
     out, status = kern.packed(packed)
-    eps = out.cpu().numpy()
-    st = status.cpu().numpy()
+    host = torch.empty((out.shape[0] + 1, 2), dtype=torch.float64, pin_memory=True)
+    host[:-1].copy_(out, non_blocking=True)
+    host[-1:].view(torch.int64).copy_(status.view(1, 2), non_blocking=True)
+    torch.cuda.current_stream(kern.device).synchronize()
+    eps = host[:-1].numpy()
+    st = host[-1:].view(torch.int64).numpy()[0]
     if st[0] != 0:
         bad = int(st[1])
         raise EvaluationFailureError("non-finite local energy", context={"bits": bits[bad].copy()})
