@@ -576,20 +576,24 @@ int mpv_local_energies(int N, int M, const double* a, const double* b, const dou
   const int T = e.n_terms;
   if (T > 512 || M > 512) return fail(MPV_ERR_ARGS, "local_energies: more than 512 terms or hidden units");
   // (ST samples per thread, SB samples per block): terms x groups flattened
-  // over <= 512 threads; prefer 16 samples per block (two DMMA m-tiles).
+  // over the block; 16 samples per block (two DMMA m-tiles) where it fits.
   // Phase 1 runs in one pass: every warp owns <= KT of the ceil(M/4) n-tiles.
-  struct Cfg { int st, sb; };
-  const Cfg cfgs[] = {{4, 16}, {8, 16}, {8, 8}};
+  struct Cfg { int st, sb, kt, tmax; const void* fn; };
+  const Cfg cfgs[] = {
+      {4, 16, 4, 448, (const void*)&energy_kernel<4, 4, 448, 2>},  // 2 blocks/SM, 72 regs (T <= 112)
+      {8, 16, 8, 256, (const void*)&energy_kernel<8, 8, 256, 2>},  // 2 blocks/SM, 128 regs (T <= 128)
+      {8, 16, 4, 512, (const void*)&energy_kernel<8, 4, 512, 1>},
+      {8, 16, 8, 512, (const void*)&energy_kernel<8, 8, 512, 1>},
+      {8, 8, 4, 512, (const void*)&energy_kernel<8, 4, 512, 1>},
+      {8, 8, 8, 512, (const void*)&energy_kernel<8, 8, 512, 1>},
+  };
+  static const int cfg0 = getenv("MPV_ENERGY_CFG") ? atoi(getenv("MPV_ENERGY_CFG")) : 0;  // profiling override
   const size_t optin = (size_t)max_smem_optin();
   const int NT = (M + 3) / 4;
-  for (const Cfg& cf : cfgs) {
-    int threads = std::max(32, ((cf.sb / cf.st) * T + 31) / 32 * 32);
-    int kt = 4;
-    if (32 * ((NT + 3) / 4) > threads) {
-      if (32 * ((NT + 3) / 4) <= 512) threads = 32 * ((NT + 3) / 4);
-      else { kt = 8; threads = std::max(threads, 32 * ((NT + 7) / 8)); }
-    }
-    if (threads > (cf.st == 4 ? kST4Threads : 512)) continue;
+  for (int ci = cfg0; ci < (int)(sizeof(cfgs) / sizeof(cfgs[0])); ++ci) {
+    const Cfg& cf = cfgs[ci];
+    const int threads = std::max(std::max(32, ((cf.sb / cf.st) * T + 31) / 32 * 32), 32 * ((NT + cf.kt - 1) / cf.kt));
+    if (threads > cf.tmax) continue;
     static const int nbt0 = getenv("MPV_ENERGY_NBT") ? atoi(getenv("MPV_ENERGY_NBT")) : 3;
     static const int rows0 = getenv("MPV_ENERGY_ROWS") ? atoi(getenv("MPV_ENERGY_ROWS")) : 12;
     for (int nbt = nbt0; nbt >= 2; --nbt)
@@ -599,12 +603,10 @@ int mpv_local_energies(int N, int M, const double* a, const double* b, const dou
         static const int skip = getenv("MPV_ENERGY_SKIP") ? atoi(getenv("MPV_ENERGY_SKIP")) : 0;
         pl.skip = skip;
         if (smem > optin) continue;
-        const void* fn = cf.st == 4 ? (kt == 4 ? (const void*)&energy_kernel<4, 4> : (const void*)&energy_kernel<4, 8>)
-                                    : (kt == 4 ? (const void*)&energy_kernel<8, 4> : (const void*)&energy_kernel<8, 8>);
-        if (int rc = ensure_smem(fn, smem)) return rc;
+        if (int rc = ensure_smem(cf.fn, smem)) return rc;
         const unsigned grid = (unsigned)((B + cf.sb - 1) / cf.sb);
         void* args[] = {&e, &pl};
-        if (cudaLaunchKernel(fn, grid, threads, args, smem, (cudaStream_t)stream) != cudaSuccess)
+        if (cudaLaunchKernel(cf.fn, grid, threads, args, smem, (cudaStream_t)stream) != cudaSuccess)
           return check_launch("local_energies");
         return check_launch("local_energies");
       }

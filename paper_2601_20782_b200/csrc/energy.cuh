@@ -296,10 +296,9 @@ __device__ __noinline__ double2 slow_ratio(const EnergyArgs& a, const uint32_t* 
 //   in registers; tau rows are staged by bulk copies and read per lane,
 //   tanh(theta) as broadcasts.  Ratios go to shared memory and one warp per
 //   sample sums the terms in a fixed order (deterministic).
-constexpr int kST4Threads = 448;  // block size cap of the 4-samples-per-thread variant (2 blocks/SM)
-
-template <int ST, int KT>
-__global__ void __launch_bounds__(ST == 4 ? kST4Threads : 512, ST == 4 ? 2 : 1) energy_kernel(const EnergyArgs a, const EnergyPlan pl) {
+// ST samples per thread, KT DMMA n-tiles per warp, launch bounds (TMAX threads, MINB blocks/SM)
+template <int ST, int KT, int TMAX, int MINB>
+__global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, const EnergyPlan pl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int M = a.M, T = a.n_terms, words = a.words, N = a.N;
   const int SB = pl.SB, NG = SB / ST, rows = pl.rows;
