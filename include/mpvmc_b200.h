@@ -166,6 +166,17 @@ int mpv_local_energies(int N, int M, const double* a, const double* b, const dou
                        int ham, const int32_t* bonds, int n_bonds, double J, double h,
                        const void* tables, const uint32_t* bits, int64_t B, double* out_eps,
                        int64_t* status, void* stream);
+/* General couplings (beyond the reference: J1-J2 bond classes, Marshall sign):
+ * eps(x) = sum_b bond_j[b] s_p s_q + sum_t term_coef[t] psi(x_t)/psi(x), with
+ * x_t the connected configuration of term t (TFIM: flip of site t; Heisenberg:
+ * swap of bond t).  NULL term_coef = h (TFIM) / 2J (Heisenberg) for every term,
+ * NULL bond_j = J for every bond (then identical to mpv_local_energies).
+ * Marshall sign: term_coef[t] = -2 J_t for bonds joining the two sublattices. */
+int mpv_local_energies_ex(int N, int M, const double* a, const double* b, const double* w_t,
+                          int ham, const int32_t* bonds, int n_bonds, double J, double h,
+                          const double* term_coef, const double* bond_j, const void* tables,
+                          const uint32_t* bits, int64_t B, double* out_eps, int64_t* status,
+                          void* stream);
 
 /* ---- helpers ---- */
 int mpv_unpack_bits(const uint32_t* words, int64_t B, int N, uint8_t* out, void* stream);

@@ -560,6 +560,14 @@ int mpv_energy_prepare(int N, int M, const double* a, const double* b, const dou
 int mpv_local_energies(int N, int M, const double* a, const double* b, const double* w_t, int ham,
                        const int32_t* bonds, int n_bonds, double J, double h, const void* tables,
                        const uint32_t* bits, int64_t B, double* out_eps, int64_t* status, void* stream) {
+  return mpv_local_energies_ex(N, M, a, b, w_t, ham, bonds, n_bonds, J, h, nullptr, nullptr, tables, bits, B,
+                               out_eps, status, stream);
+}
+
+int mpv_local_energies_ex(int N, int M, const double* a, const double* b, const double* w_t, int ham,
+                          const int32_t* bonds, int n_bonds, double J, double h, const double* term_coef,
+                          const double* bond_j, const void* tables, const uint32_t* bits, int64_t B,
+                          double* out_eps, int64_t* status, void* stream) {
   if (N < 1 || M < 1 || !a || !b || !w_t || !tables || !bits || !out_eps || B < 0)
     return fail(MPV_ERR_ARGS, "local_energies: bad args");
   if (ham != MPV_HAM_TFIM && ham != MPV_HAM_HEISENBERG) return fail(MPV_ERR_ARGS, "local_energies: ham");
@@ -569,7 +577,7 @@ int mpv_local_energies(int N, int M, const double* a, const double* b, const dou
   e.N = N; e.M = M; e.words = (N + 31) / 32; e.ham = ham; e.n_bonds = n_bonds;
   e.n_terms = ham == MPV_HAM_TFIM ? N : n_bonds;
   e.a = (const double2*)a; e.b = (const double2*)b; e.w_t = (const double2*)w_t; e.bonds = bonds;
-  e.J = J; e.h = h;
+  e.J = J; e.h = h; e.term_coef = term_coef; e.bond_j = bond_j;
   const EnergyTables tb = energy_layout(N, M, ham, n_bonds, const_cast<void*>(tables));
   e.tau = tb.tau; e.ea = tb.ea; e.ec = tb.ec; e.slow = tb.slow; e.wp = tb.wp;
   e.bits = bits; e.B = B; e.out = (double2*)out_eps; e.status = status;

@@ -31,6 +31,8 @@ struct EnergyArgs {
   const double2* ea;    // [n_terms][2]: exp(+-a_t) prod_i cosh(w_it), mantissa
   const int32_t* ec;    // [n_terms]: binary exponent of prod_i cosh(w_it)
   const int32_t* slow;  // [n_terms]
+  const double* term_coef;  // [n_terms] off-diagonal coefficient (NULL: h for TFIM, 2J for Heisenberg)
+  const double* bond_j;     // [n_bonds] diagonal couplings (NULL: J for every bond)
   const double* wp;     // [roundup(N, 8)][2M + 8]: W_t in the staging layout
   const uint32_t* bits;
   int64_t B;
@@ -507,7 +509,8 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
           }
         }
       }
-      R[s * T + t] = v;
+      const double ct = a.term_coef ? a.term_coef[t] : (a.ham == MPV_HAM_TFIM ? a.h : 2.0 * a.J);
+      R[s * T + t] = make_double2(ct * v.x, ct * v.y);
     }
   }
   __syncthreads();
@@ -521,15 +524,22 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
         er += R[s * T + u].x;
         ei += R[s * T + u].y;
       }
-    // ref vmc.py:52-57: sum_b s_p s_q = n_bonds - 2 #(anti-aligned bonds), exact in integers
-    int anti = 0;
-    for (int b = lane; b < a.n_bonds; b += 32) anti += bit_of(s, a.bonds[2 * b]) ^ bit_of(s, a.bonds[2 * b + 1]);
+    // ref vmc.py:52-57: J sum_b s_p s_q; uniform J: n_bonds - 2 #(anti-aligned bonds), exact in integers
+    double diag;
+    if (a.bond_j) {
+      double dj = 0.0;
+      for (int b = lane; b < a.n_bonds; b += 32)
+        dj += (bit_of(s, a.bonds[2 * b]) ^ bit_of(s, a.bonds[2 * b + 1])) ? -a.bond_j[b] : a.bond_j[b];
+      diag = segment_sum(dj, 32);
+    } else {
+      int anti = 0;
+      for (int b = lane; b < a.n_bonds; b += 32) anti += bit_of(s, a.bonds[2 * b]) ^ bit_of(s, a.bonds[2 * b + 1]);
+      diag = a.J * (double)(a.n_bonds - 2 * __reduce_add_sync(0xffffffffu, anti));
+    }
     er = segment_sum(er, 32);
     ei = segment_sum(ei, 32);
-    const double diag = (double)(a.n_bonds - 2 * __reduce_add_sync(0xffffffffu, anti));
     if (lane == 0) {
-      const double coef = (a.ham == MPV_HAM_TFIM) ? a.h : 2.0 * a.J;
-      const double2 eps = make_double2(a.J * diag + coef * er, coef * ei);
+      const double2 eps = make_double2(diag + er, ei);
       a.out[s0 + s] = eps;
       if ((!isfinite(eps.x) || !isfinite(eps.y)) && a.status) {
         atomicMin((unsigned long long*)&a.status[1], (unsigned long long)(s0 + s));

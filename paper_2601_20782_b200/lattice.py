@@ -73,6 +73,52 @@ class LatticeSpec:
     def bond_array(self) -> np.ndarray:
         return np.array(self.bonds, dtype=np.int64).reshape(-1, 2)
 
+    def next_nearest_bonds(self) -> np.ndarray:
+        """Next-nearest-neighbour (i<j) pairs, sorted, deduplicated, excluding
+        nearest-neighbour pairs (beyond the reference: J1-J2 models).  Chain:
+        (i, i+2); square: both diagonals; periodic wrap as for `bonds`."""
+        pairs = set()
+        if len(self.shape) == 1:
+            (n,) = self.shape
+            for i in range(n):
+                j = i + 2
+                if j >= n:
+                    if not self.periodic:
+                        continue
+                    j -= n
+                if i != j:
+                    pairs.add((min(i, j), max(i, j)))
+        else:
+            length = self.shape[0]
+            for r in range(length):
+                for c in range(length):
+                    for dc in (1, -1):
+                        rr, cc = r + 1, c + dc
+                        if not (0 <= cc < length and rr < length):
+                            if not self.periodic:
+                                continue
+                            rr, cc = rr % length, cc % length
+                        a, b = r * length + c, rr * length + cc
+                        if a != b:
+                            pairs.add((min(a, b), max(a, b)))
+        pairs -= set(self.bonds)
+        return np.array(sorted(pairs), dtype=np.int64).reshape(-1, 2)
+
+    def sublattice(self) -> np.ndarray:
+        """Checkerboard sublattice index (0/1) of every site; raises if the
+        nearest-neighbour bonds do not join the two sublattices (Marshall sign
+        needs a bipartite lattice: open, or periodic with even length)."""
+        if len(self.shape) == 1:
+            sub = np.arange(self.shape[0]) % 2
+        else:
+            length = self.shape[0]
+            r, c = np.divmod(np.arange(length * length), length)
+            sub = (r + c) % 2
+        bonds = self.bond_array()
+        if bonds.size and np.any(sub[bonds[:, 0]] == sub[bonds[:, 1]]):
+            raise ValueError("lattice is not bipartite (periodic with odd length)")
+        return sub.astype(np.int64)
+
 
 def enumerate_bits(n: int) -> np.ndarray:
     """(2^n, n) bit matrix in ascending code order (lattice.py:95-101)."""

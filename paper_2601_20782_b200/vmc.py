@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _native as nat
 from .errors import DegenerateInputError, EvaluationFailureError
-from .hamiltonians import HeisenbergSpec, TfimSpec
+from .hamiltonians import HeisenbergSpec, J1J2Spec, TfimSpec
 from .lattice import pack_bits
 
 
@@ -26,10 +26,16 @@ class EnergyKernel:
         import torch
 
         nat.require_cuda()
+        coef = bond_j = None
         if isinstance(spec, TfimSpec):
             self.ham, self.J, self.h = nat.HAM_TFIM, float(spec.j), float(spec.h)
-        elif isinstance(spec, HeisenbergSpec):
-            self.ham, self.J, self.h = nat.HAM_HEISENBERG, float(spec.j), 0.0
+            bonds = spec.lattice.bond_array()
+        elif isinstance(spec, (HeisenbergSpec, J1J2Spec)):
+            self.ham, self.h = nat.HAM_HEISENBERG, 0.0
+            self.J = float(spec.j) if isinstance(spec, HeisenbergSpec) else float(spec.j1)
+            bonds, jb, cf = spec.couplings()
+            if isinstance(spec, J1J2Spec) or spec.marshall:  # general couplings (mpv_local_energies_ex)
+                coef, bond_j = cf, jb
         else:
             raise TypeError(f"unknown Hamiltonian spec {type(spec).__name__}")
         n = spec.lattice.n_sites
@@ -41,8 +47,11 @@ class EnergyKernel:
         self.a = cplx(params.a)
         self.b = cplx(params.b)
         self.w_t = cplx(np.ascontiguousarray(params.w.T))
-        bonds = spec.lattice.bond_array().astype(np.int32)
+        bonds = bonds.astype(np.int32)
         self.n_bonds = bonds.shape[0]
+        f64 = lambda v: torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(self.device)
+        self.term_coef = f64(coef) if coef is not None else None
+        self.bond_j = f64(bond_j) if bond_j is not None else None
         self.bonds = torch.from_numpy(np.ascontiguousarray(bonds.reshape(-1))).to(self.device) if self.n_bonds else None
         nbytes = nat.load().mpv_energy_tables_bytes(self.N, self.M, self.ham, self.n_bonds)
         self.tables = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -59,9 +68,11 @@ class EnergyKernel:
         B = packed_bits.shape[0]
         out = torch.empty((B, 2), dtype=torch.float64, device=self.device)
         status = torch.tensor([0, 2**63 - 1], dtype=torch.int64, device=self.device)
-        nat.call("mpv_local_energies", self.N, self.M, self.a.data_ptr(), self.b.data_ptr(), self.w_t.data_ptr(),
-                 self.ham, self._bonds_ptr(), self.n_bonds, self.J, self.h, self.tables.data_ptr(),
-                 packed_bits.data_ptr(), B, out.data_ptr(), status.data_ptr(), nat.stream_handle(self.device))
+        ptr = lambda t: t.data_ptr() if t is not None else None
+        nat.call("mpv_local_energies_ex", self.N, self.M, self.a.data_ptr(), self.b.data_ptr(), self.w_t.data_ptr(),
+                 self.ham, self._bonds_ptr(), self.n_bonds, self.J, self.h, ptr(self.term_coef), ptr(self.bond_j),
+                 self.tables.data_ptr(), packed_bits.data_ptr(), B, out.data_ptr(), status.data_ptr(),
+                 nat.stream_handle(self.device))
         return out, status
 
 
@@ -71,7 +82,7 @@ def _energy_kernel(spec, log_amplitude):
     if not isinstance(log_amplitude, LogPsiEvaluator):
         raise TypeError("local_energies needs a device evaluator from rbm.log_psi_evaluator "
                         f"(got {type(log_amplitude).__name__}; there is no host-callable fallback)")
-    key = (type(spec).__name__, spec.lattice, float(spec.j), float(getattr(spec, "h", 0.0)))
+    key = spec  # frozen dataclasses: hashable, equal specs share the tables
     cache = log_amplitude._energy_cache
     if key not in cache:
         cache[key] = EnergyKernel(spec, log_amplitude.params, log_amplitude.device)

@@ -5,7 +5,7 @@ from fractions import Fraction
 import numpy as np
 import pytest
 
-from paper_2601_20782_b200 import precision, rbm
+from paper_2601_20782_b200 import hamiltonians, precision, rbm
 from paper_2601_20782_b200.lattice import LatticeSpec, pack_bits, unpack_bits
 from paper_2601_20782_b200.rng import counter_uniform, derive_key, mix64
 from paper_2601_20782_b200.sampler import Proposal, default_chain_count, pair_table
@@ -127,3 +127,14 @@ def test_parameters_io_roundtrip(tmp_path):
     assert p.n_params == 5 + 10 + 50
     with pytest.raises(ValueError):
         rbm.RbmParameters(np.zeros(3), np.zeros(3), np.zeros((2, 3)))
+
+
+def test_lattice_next_nearest_and_sublattice():
+    assert LatticeSpec.chain(10, periodic=True).next_nearest_bonds().shape == (10, 2)
+    assert LatticeSpec.square(4).next_nearest_bonds().shape == (32, 2)
+    assert LatticeSpec.square(4, periodic=False).next_nearest_bonds().shape == (18, 2)
+    assert LatticeSpec.square(10).next_nearest_bonds().shape == (200, 2)
+    with pytest.raises(ValueError):
+        LatticeSpec.square(3).sublattice()
+    with pytest.raises(ValueError):
+        hamiltonians.HeisenbergSpec(LatticeSpec.chain(9, periodic=True), 1.0, marshall=True)
