@@ -269,6 +269,41 @@ def run_ours(args, rank, world, local_rank):
             "config5_tfim16x16_a1_f16": rate(256, 1, F16, RoundingMode.NATIVE, flip, chains=4096 * 4),
         }
 
+        # BASELINE configs[4]: precision sweep on 16x16 TFIM, energy bias vs the
+        # paper's MH bias bound (same parameters, same sampler settings per format)
+        def bias_sweep(n_side=16, alpha=1, scale=0.05, chains=4096, per_chain=4, burn_sweeps=100):
+            from paper_2601_20782_b200 import bounds
+            from paper_2601_20782_b200.lattice import LatticeSpec as _LS
+
+            n = n_side * n_side
+            spec = TfimSpec(_LS.square(n_side), 1.0, 3.04)
+            p = rbm.random_parameters(n, alpha, derive_key(1, "init"), scale)
+            psi = rbm.log_psi_evaluator(p)
+            res = {}
+            for fmt, mode in ((F64, RoundingMode.PER_OPERATION), (F32, RoundingMode.NATIVE),
+                              (BF16, RoundingMode.NATIVE), (F16, RoundingMode.NATIVE)):
+                e = rbm.log_prob_evaluator(p, fmt, mode)
+                en = sampler.ChainEnsemble(chains, n, flip, e, derive_key(1, "chains"))
+                en.run_sweeps(burn_sweeps)
+                en.reset_counters()
+                smp = en.collect(chains * per_chain, n + 1)
+                eps = vmc.local_energies(spec, psi, smp).real
+                means = eps.reshape(chains, per_chain).mean(axis=1)
+                err = float(np.sqrt(means.var(ddof=1) / chains))
+                sig = float(np.std(e(smp) - rbm.log_prob_batch(p, smp, F64))) if fmt is not F64 else 0.0
+                res[fmt.name] = {"energy_per_site": float(eps.mean()) / n, "mc_error_per_site": err / n,
+                                 "sigma_hat": sig, "tv_bound_pinsker": float(bounds.pinsker_tv_bound(sig)),
+                                 "tv_bound_theorem3": float(bounds.theorem3_gaussian_bound(sig, 0.0, 0.0)),
+                                 "acceptance": en.acceptance_rate, "variant": e.snapshot.label}
+            e64 = res["f64"]["energy_per_site"]
+            for k, v in res.items():
+                v["bias_vs_f64_per_site"] = v["energy_per_site"] - e64
+            res["config"] = (f"rbm_a{alpha}_tfim{n_side}x{n_side}_h3.04_scale{scale}_c{chains}_s{chains * per_chain}"
+                             f"_burn{burn_sweeps}sweeps")
+            return res
+
+        extra["config5_precision_bias_16x16"] = bias_sweep()
+
     # ---- VMC iteration time at BASELINE configs[0] (N=20 open TFIM chain, alpha=1,
     # 4,096 samples, 1,024 chains, f16 sampling), reference: vmc.py:472-639 ----
     vmc_iter = None
