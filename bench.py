@@ -318,6 +318,20 @@ def run_ours(args, rank, world, local_rank):
                     "update_ms": 1e3 * float(np.median([r["update_seconds"] for r in recs])),
                     "energy_last": recs[-1]["energy"]}
         vmc_iter["iteration_ms"] = vmc_iter["sampling_ms"] + vmc_iter["update_ms"]
+        # BASELINE configs[1] (10x10 TFIM, alpha=2, 16,384 chains, 65,536 samples, f16
+        # sampling + f64 energies): the dense S (P = 20,300) does not fit the
+        # reference's solver; SR runs matrix-free (factored O, conjugate gradients)
+        cfg2 = vmc.TrainConfig(TfimSpec(_LS.square(10), 1.0, 3.04), alpha=2, n_steps=4, n_samples=4 * C,
+                               n_chains=C, sampling_format=F16, rounding_mode=RoundingMode.NATIVE,
+                               track_timings=True, sr_solver="cg", cg_tol=1e-8, burn_in_sweeps=200)
+        recs2 = vmc.train(cfg2).records[1:]
+        vmc_iter["config2"] = {
+            "config": "rbm_a2_tfim10x10_h3.04_s65536_c16384_f16native_f64energy_sr_cg(tol 1e-8, lambda 1e-3)",
+            "sampling_ms": 1e3 * float(np.median([r["sampling_seconds"] for r in recs2])),
+            "update_ms": 1e3 * float(np.median([r["update_seconds"] for r in recs2])),
+            "cg_iterations": int(np.median([r["cg_iterations"] for r in recs2])),
+            "energy_last": recs2[-1]["energy"]}
+        vmc_iter["config2"]["iteration_ms"] = vmc_iter["config2"]["sampling_ms"] + vmc_iter["config2"]["update_ms"]
 
     steps_per_step = chain_steps_per_step(C) * world
     value = steps_per_step / (ms / 1e3)

@@ -201,6 +201,7 @@ class SrUpdate:
     residual: float
     lambda_shift: float
     eta: float
+    iterations: int = 0  # conjugate-gradient iterations (matrix-free solver)
 
 
 def sr_step(f, s, lambda_shift: float, eta: float, compute_kappa: bool = True) -> SrUpdate:
@@ -229,6 +230,82 @@ def sr_step(f, s, lambda_shift: float, eta: float, compute_kappa: bool = True) -
     return SrUpdate(g, kappa, residual, lambda_shift, eta)
 
 
+class FactoredLogDerivatives:
+    """O(x) = [x, tanh(theta), tanh(theta) (x) x] (rbm.py:307-325) kept in factored
+    form: X (U, N) 0/1 and T = tanh(b + W x) (U, M) complex, never the (U, P)
+    matrix (P = N + M + M N is 20,300 at config 2: O would be 21 GB and S 6.6 GB).
+    Products with O and O^H are one (U, M, N) ZGEMM each (cuBLAS, f64):
+
+      O v   = X v_a + T v_b + rowsum(X * (T v_W))
+      O^H u = [X^T u, T^H u, T^H (u * X)  (row-major W block)]
+
+    `reduce` (optional) all-reduces sums over samples across ranks."""
+
+    def __init__(self, params, bits_u8, reduce=None):
+        import torch
+
+        dev = bits_u8.device
+        self.N, self.M = params.n_visible, params.n_hidden
+        self.x = bits_u8.to(torch.complex128)
+        self.t = torch.tanh(self.x @ _t(params.w, dev).T + _t(params.b, dev)[None, :])
+        self.reduce = reduce or (lambda z: z)
+
+    def o_v(self, v):
+        N, M = self.N, self.M
+        return self.x @ v[:N] + self.t @ v[N:N + M] + (self.x * (self.t @ v[N + M:].reshape(M, N))).sum(dim=1)
+
+    def oh_u(self, u):
+        """sum_s conj(O_s) u_s (local sums; callers reduce)."""
+        import torch
+
+        th = self.t.mH
+        return torch.cat([self.x.T @ u, th @ u, (th @ (u[:, None] * self.x)).reshape(-1)])
+
+
+def sr_step_cg(o: FactoredLogDerivatives, eps, weights, lambda_shift: float, eta: float,
+               tol: float = 1e-10, maxiter: int = 1000):
+    """SR update without forming S (matrix-free conjugate gradients on the
+    Hermitian positive-definite S + lambda I; beyond the
+    reference's dense Cholesky, vmc.py:202-229, which does not fit config 2).
+    Same estimators: F = sum_w conj(O) eps - (sum_w conj O)(sum_w eps),
+    S v = sum_w conj(O) (O v) - conj(Obar)(Obar v).  Returns (SrUpdate, F, energy)."""
+    import torch
+
+    if lambda_shift < 0:
+        raise ValueError("lambda must be >= 0")
+    if eta <= 0:
+        raise ValueError("eta must be > 0")
+    w = weights.to(torch.complex128)
+    s_oe = o.reduce(o.oh_u(w * eps))
+    s_o = o.reduce(o.oh_u(w))
+    e = o.reduce((w @ eps).reshape(1))[0]
+    f = s_oe - s_o * e
+    obar = s_o.conj()  # sum_w O
+
+    def apply(v):
+        return o.reduce(o.oh_u(w * o.o_v(v))) - obar.conj() * (obar @ v) + lambda_shift * v
+
+    g = torch.zeros_like(f)
+    r = f.clone()
+    pvec = r.clone()
+    rr = torch.vdot(r, r).real
+    fn = float(torch.linalg.norm(f))
+    it = 0
+    while it < maxiter and fn > 0 and float(rr) ** 0.5 > tol * fn:
+        ap = apply(pvec)
+        alpha = rr / torch.vdot(pvec, ap).real
+        g = g + alpha * pvec
+        r = r - alpha * ap
+        rr_new = torch.vdot(r, r).real
+        pvec = r + (rr_new / rr) * pvec
+        rr = rr_new
+        it += 1
+    residual = float(torch.linalg.norm(apply(g) - f)) / fn if fn > 0 else 0.0
+    if fn > 0 and residual > max(10 * tol, 1e-9):
+        raise SolverError(f"SR conjugate-gradient residual {residual:.3e} after {it} iterations")
+    return SrUpdate(g, float("nan"), residual, lambda_shift, eta, it), f, float(e.real)
+
+
 @dataclass
 class TrainConfig:
     """Reference TrainConfig (vmc.py:320-351) plus compute_kappa (the eigvalsh of
@@ -255,12 +332,17 @@ class TrainConfig:
     track_timings: bool = False
     reference_energy: float | None = None
     compute_kappa: bool = True
+    sr_solver: str = "dense"  # "dense" (reference: Cholesky on S) or "cg" (matrix-free, factored O)
+    cg_tol: float = 1e-10
+    cg_maxiter: int = 1000
 
     def __post_init__(self):
         if self.n_steps < 1 or self.n_samples < 2:
             raise ValueError("n_steps and n_samples must be positive")
         if self.sampling_mode not in ("mcmc", "exact"):
             raise ValueError(f"unknown sampling mode {self.sampling_mode!r}")
+        if self.sr_solver not in ("dense", "cg"):
+            raise ValueError(f"unknown SR solver {self.sr_solver!r}")
         if self.proposal is None:
             from .sampler import Proposal
 
@@ -356,15 +438,21 @@ def train(config: TrainConfig, device=None, group=None) -> TrainResult:
         eps = torch.complex(eps_ri[:, 0], eps_ri[:, 1])
         u8 = torch.empty((uniq.shape[0], n), dtype=torch.uint8, device=dev)
         nat.call("mpv_unpack_bits", uniq.data_ptr(), uniq.shape[0], n, u8.data_ptr(), nat.stream_handle(dev))
-        o = grad_log_psi_device(params, u8)
-        if world > 1:
-            f, s, e_glob = parallel.sharded_statistics(o, eps, est_w, group)
-            energy = float(e_glob)
+        if config.sr_solver == "cg":
+            red = (lambda z: parallel.all_reduce_sum(z, group)) if world > 1 else None
+            fo = FactoredLogDerivatives(params, u8, red)
+            update, f, energy = sr_step_cg(fo, eps, est_w, config.lambda_shift, config.eta, config.cg_tol,
+                                           config.cg_maxiter)
         else:
-            f = forces(o=o, eps=eps, weights=est_w)
-            s = s_matrix(o=o, weights=est_w)
-            energy = float((est_w.to(eps.dtype) @ eps).real)
-        update = sr_step(f, s, config.lambda_shift, config.eta, config.compute_kappa)
+            o = grad_log_psi_device(params, u8)
+            if world > 1:
+                f, s, e_glob = parallel.sharded_statistics(o, eps, est_w, group)
+                energy = float(e_glob)
+            else:
+                f = forces(o=o, eps=eps, weights=est_w)
+                s = s_matrix(o=o, weights=est_w)
+                energy = float((est_w.to(eps.dtype) @ eps).real)
+            update = sr_step(f, s, config.lambda_shift, config.eta, config.compute_kappa)
         theta = params.flatten() - config.eta * update.g.cpu().numpy()
         new_params = rbm.RbmParameters.from_flat(theta, params.n_visible, params.n_hidden)
         if exact_mode:
@@ -398,6 +486,8 @@ def train(config: TrainConfig, device=None, group=None) -> TrainResult:
             record = {"step": step, "energy": energy, "mc_error": err, "acceptance": acceptance,
                       "sigma_hat": sigma_hat, "bound_pinsker": pinsker_tv_bound(sigma_hat),
                       "bound_theorem3": theorem3_gaussian_bound(sigma_hat, 0.0, 0.0), "kappa": update.kappa}
+            if config.sr_solver == "cg":
+                record["cg_iterations"] = update.iterations
             if config.track_timings:
                 torch.cuda.synchronize(dev)
                 record["sampling_seconds"] = t_update - t_sample
