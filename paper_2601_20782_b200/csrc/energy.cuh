@@ -485,14 +485,25 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
     }
   }
   __syncthreads();  // all reads of tt and the staging buffers done
-  // ratios -> R [SB][T] (reuses tt + staging: all reads of them are done)
+  // R [SB][T] (reuses tt + staging: all reads of them are done): thread (g, t)
+  // writes coef_t * ratio_t plus the diagonal of bonds b = t, t + T, ...
+  // (ref vmc.py:52-57: J_b s_p s_q), so one fixed-order sum over t gives eps.
   double2* R = tt;
-  if (active) {
+  if (g < NG) {
+    int bp[2] = {0, 0}, bq[2] = {0, 0};
+    double bj[2] = {0.0, 0.0};
+    int nb = 0;
+    for (int b = t; b < a.n_bonds && nb < 2; b += T, ++nb) {
+      bp[nb] = a.bonds[2 * b];
+      bq[nb] = a.bonds[2 * b + 1];
+      bj[nb] = a.bond_j ? a.bond_j[b] : a.J;
+    }
+    const double ct = a.term_coef ? a.term_coef[t] : (a.ham == MPV_HAM_TFIM ? a.h : 2.0 * a.J);
 #pragma unroll
     for (int j = 0; j < ST; ++j) {
       const int s = g * ST + j;
       double2 v = make_double2(0.0, 0.0);
-      if (s0 + s < a.B && ((nz >> j) & 1u)) {
+      if (active && s0 + s < a.B && ((nz >> j) & 1u)) {
         if (slow) {
           v = slow_ratio(a, wsm + s * 32, t, sg[j] ? -1.0 : 1.0);
         } else {
@@ -509,8 +520,12 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
           }
         }
       }
-      const double ct = a.term_coef ? a.term_coef[t] : (a.ham == MPV_HAM_TFIM ? a.h : 2.0 * a.J);
-      R[s * T + t] = make_double2(ct * v.x, ct * v.y);
+      double dg = 0.0;
+      for (int q = 0; q < nb; ++q) dg += (bit_of(s, bp[q]) ^ bit_of(s, bq[q])) ? -bj[q] : bj[q];
+      for (int b = t + 2 * T; b < a.n_bonds; b += T)  // (more than two bonds per term: not in practice)
+        dg += (bit_of(s, a.bonds[2 * b]) ^ bit_of(s, a.bonds[2 * b + 1])) ? -(a.bond_j ? a.bond_j[b] : a.J)
+                                                                          : (a.bond_j ? a.bond_j[b] : a.J);
+      R[s * T + t] = make_double2(fma(ct, v.x, dg), ct * v.y);
     }
   }
   __syncthreads();
@@ -519,27 +534,14 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
   for (int s = warp; s < SB; s += nwarps) {
     if (s0 + s >= a.B) continue;
     double er = 0.0, ei = 0.0;
-    if (any_terms)
-      for (int u = lane; u < T; u += 32) {
-        er += R[s * T + u].x;
-        ei += R[s * T + u].y;
-      }
-    // ref vmc.py:52-57: J sum_b s_p s_q; uniform J: n_bonds - 2 #(anti-aligned bonds), exact in integers
-    double diag;
-    if (a.bond_j) {
-      double dj = 0.0;
-      for (int b = lane; b < a.n_bonds; b += 32)
-        dj += (bit_of(s, a.bonds[2 * b]) ^ bit_of(s, a.bonds[2 * b + 1])) ? -a.bond_j[b] : a.bond_j[b];
-      diag = segment_sum(dj, 32);
-    } else {
-      int anti = 0;
-      for (int b = lane; b < a.n_bonds; b += 32) anti += bit_of(s, a.bonds[2 * b]) ^ bit_of(s, a.bonds[2 * b + 1]);
-      diag = a.J * (double)(a.n_bonds - 2 * __reduce_add_sync(0xffffffffu, anti));
+    for (int u = lane; u < T; u += 32) {
+      er += R[s * T + u].x;
+      ei += R[s * T + u].y;
     }
     er = segment_sum(er, 32);
     ei = segment_sum(ei, 32);
     if (lane == 0) {
-      const double2 eps = make_double2(diag + er, ei);
+      const double2 eps = make_double2(er, ei);
       a.out[s0 + s] = eps;
       if ((!isfinite(eps.x) || !isfinite(eps.y)) && a.status) {
         atomicMin((unsigned long long*)&a.status[1], (unsigned long long)(s0 + s));
