@@ -193,7 +193,27 @@ def gen_train():
     save("train.npz", **arrays)
 
 
+def gen_formats():
+    """The reference's training-log writer (experiments.py:222-237, 611-624) on
+    fixed records -> tests/golden/training_log_ref.csv (formats.py parity)."""
+    from mpvmc import experiments as ex
+
+    recs = [{"step": 0, "energy": -1.2345678901234567, "mc_error": 0.01, "acceptance": 0.5, "sigma_hat": 0.0,
+             "bound_pinsker": 0.0, "bound_theorem3": 0.0, "kappa": float("nan"), "rel_error": 1e-3},
+            {"step": 1, "energy": np.float64(3.0), "mc_error": np.float32(0.25), "acceptance": 1,
+             "sigma_hat": 1e-300, "bound_pinsker": 5e-301, "bound_theorem3": 2.5, "kappa": 12.0,
+             "sampling_seconds": 0.5, "update_seconds": 0.25}]
+    rows = [ex._record_row(("f16",), r) for r in recs]
+    path = os.path.join(OUT, "training_log_ref.csv")
+    ex.write_csv(path, ["format", *ex._LOG_COLUMNS, "rel_error"], rows)
+    print(f"wrote {path}")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["formats"]:
+        gen_formats()
+        sys.exit(0)
+    gen_formats()
     gen_train()
     gen_rng()
     gen_forward()

@@ -138,3 +138,41 @@ def test_lattice_next_nearest_and_sublattice():
         LatticeSpec.square(3).sublattice()
     with pytest.raises(ValueError):
         hamiltonians.HeisenbergSpec(LatticeSpec.chain(9, periodic=True), 1.0, marshall=True)
+
+
+def test_training_log_format_matches_reference(tmp_path):
+    """formats.record_row/write_csv reproduce the reference's writer byte for
+    byte (golden file from experiments.py's own write_csv, make_golden.py)."""
+    import os
+
+    from paper_2601_20782_b200 import formats
+
+    recs = [{"step": 0, "energy": -1.2345678901234567, "mc_error": 0.01, "acceptance": 0.5, "sigma_hat": 0.0,
+             "bound_pinsker": 0.0, "bound_theorem3": 0.0, "kappa": float("nan"), "rel_error": 1e-3},
+            {"step": 1, "energy": np.float64(3.0), "mc_error": np.float32(0.25), "acceptance": 1,
+             "sigma_hat": 1e-300, "bound_pinsker": 5e-301, "bound_theorem3": 2.5, "kappa": 12.0,
+             "sampling_seconds": 0.5, "update_seconds": 0.25}]
+    out = formats.write_csv(tmp_path / "log.csv", ["format", *formats.LOG_COLUMNS, "rel_error"],
+                            [formats.record_row(("f16",), r) for r in recs])
+    golden = os.path.join(os.path.dirname(__file__), "golden", "training_log_ref.csv")
+    assert open(out).read() == open(golden).read()
+    back = formats.read_training_log(out)
+    assert back[0]["format"] == "f16" and back[1]["step"] == 1 and back[0]["energy"] == -1.23456789012346
+
+
+def test_training_log_sidecar_and_samples(tmp_path):
+    import json
+
+    from paper_2601_20782_b200 import formats
+
+    class R:
+        records = [{"step": 0, "energy": 1.0, "mc_error": 0.1, "acceptance": 0.5, "sigma_hat": 0.0,
+                    "bound_pinsker": 0.0, "bound_theorem3": 0.0, "kappa": 2.0}]
+
+    path = formats.write_training_log(tmp_path / "run", {"f64": R(), "f16": R()}, {"train": {"steps": 1}}, -1.5)
+    meta = json.load(open(f"{path}.meta.json"))
+    assert meta["reference_energy"] == -1.5 and meta["config"] == {"train": {"steps": 1}}
+    assert [r["format"] for r in formats.read_training_log(path)] == ["f64", "f16"]
+    smp = np.random.default_rng(0).integers(0, 2, size=(7, 5), dtype=np.uint8)
+    p = formats.save_samples(tmp_path / "s.npy", smp)
+    assert np.array_equal(formats.load_samples(p), smp)
