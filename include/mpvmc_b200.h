@@ -134,6 +134,17 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
                  uint32_t* samples, int64_t n_samples_total, int64_t n_chains_total,
                  int64_t round_offset, int64_t row0, void* stream);
 
+/* ---- MH sweep over a dense log-probability table (ref: sampler.py:254-268
+ *      table_log_prob / uniform_log_prob driven by ChainEnsemble.step) ----
+ * table: f64[2^n_sites] (device), indexed by the configuration code (bit k of
+ * the code = site k); n_sites <= 30, ch->words == 1.  Same draw schedule,
+ * sample layout and f64 accept test as mpv_mh_sweep; no finiteness check
+ * (the reference's table evaluator has none: -inf targets are never entered). */
+int mpv_table_sweep(const double* table, const mpv_chains* ch, uint64_t key, int proposal,
+                    int64_t init_draws, int64_t step_index, int64_t n_steps, int64_t thin,
+                    uint32_t* samples, int64_t n_samples_total, int64_t n_chains_total,
+                    int64_t round_offset, int64_t row0, void* stream);
+
 /* ---- batched log-probability / log-psi in the snapshot's arithmetic ----
  * bits: packed [B][words].  PER_OPERATION reproduces ref: _kernels.py:51-129
  * (rounded_forward / rounded_log_prob) bit for bit; F64/STORAGE_ONLY follow

@@ -166,6 +166,51 @@ __global__ void pack_kernel(const uint8_t* bits, int64_t B, int N, int nw, uint3
   }
 }
 
+// MH sweep over a dense log-probability table (ref: sampler.py:254-268
+// table_log_prob / uniform_log_prob as the evaluator of ChainEnsemble.step,
+// sampler.py:111-133): one thread per chain, configuration = its code (N <= 30),
+// the reference's draw schedule and f64 accept test (NaN / -inf reject).
+__global__ void table_sweep_kernel(const double* __restrict__ table, int N, mpv_chains ch, uint64_t key,
+                                   int proposal, int64_t init_draws, int64_t step_index, int64_t n_steps,
+                                   int64_t thin, uint32_t* samples, int64_t base, int64_t extra,
+                                   int64_t round_offset, int64_t row0) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ch.n_chains) return;
+  const int64_t gchain = ch.chain_offset + c;
+  const uint64_t s0 = mpv::stream_state(key, (uint64_t)gchain);
+  uint32_t word = ch.bits[c];
+  double lp = table[word];
+  const int64_t count_c = base + (gchain < extra ? 1 : 0);
+  const int64_t offset_c = gchain * base + (gchain < extra ? gchain : extra) - row0;
+  const double n_pairs = 0.5 * (double)N * (double)(N - 1);
+  int64_t n_acc = 0;
+  for (int64_t s = 0; s < n_steps; ++s) {
+    const uint64_t t = (uint64_t)(init_draws + 2 * (step_index + s));
+    const double us = mpv::stream_draw(s0, t), ua = mpv::stream_draw(s0, t + 1);
+    uint32_t prop = word;
+    if (proposal == MPV_PROPOSAL_FLIP) {
+      prop ^= 1u << (int)mpv::floor_scaled(us, (double)N);
+    } else {
+      int i, j;
+      mpv::pair_of(mpv::floor_scaled(us, n_pairs), N, i, j);
+      if (((word >> i) ^ (word >> j)) & 1u) prop ^= (1u << i) | (1u << j);
+    }
+    const double lp_new = table[prop];
+    if (log(ua) < lp_new - lp) {
+      word = prop;
+      lp = lp_new;
+      ++n_acc;
+    }
+    if (samples && thin > 0 && (s + 1) % thin == 0) {
+      const int64_t r = round_offset + (s + 1) / thin - 1;
+      if (r < count_c) samples[offset_c + r] = word;
+    }
+  }
+  ch.bits[c] = word;
+  ch.log_probs[c] = lp;
+  if (ch.accepted) ch.accepted[c] += n_acc;
+}
+
 __global__ void sum_i64_kernel(const int64_t* x, int64_t n, int64_t* out) {
   __shared__ long long part[32];
   long long acc = 0;
@@ -292,6 +337,26 @@ int mpv_snapshot_fill(const mpv_snapshot* snap, const double* rounded, double sp
   const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
   snapshot_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(*snap, rounded, split);
   return check_launch("snapshot_fill");
+}
+
+int mpv_table_sweep(const double* table, const mpv_chains* ch, uint64_t key, int proposal, int64_t init_draws,
+                    int64_t step_index, int64_t n_steps, int64_t thin, uint32_t* samples, int64_t n_samples_total,
+                    int64_t n_chains_total, int64_t round_offset, int64_t row0, void* stream) {
+  if (!table || !ch || ch->n_sites < 1 || ch->n_sites > 30 || ch->words != 1 || n_steps < 0 || thin < 0 ||
+      (proposal != MPV_PROPOSAL_FLIP && proposal != MPV_PROPOSAL_EXCHANGE) ||
+      (proposal == MPV_PROPOSAL_EXCHANGE && ch->n_sites < 2))
+    return fail(MPV_ERR_ARGS, "table_sweep: bad args (table evaluators need 1 <= n_sites <= 30)");
+  if (ch->n_chains == 0) return MPV_OK;
+  int64_t base = 0, extra = 0;
+  if (samples) {
+    if (n_chains_total < 1 || thin < 1) return fail(MPV_ERR_ARGS, "table_sweep: sample layout");
+    base = n_samples_total / n_chains_total;
+    extra = n_samples_total % n_chains_total;
+  }
+  table_sweep_kernel<<<(unsigned)((ch->n_chains + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      table, ch->n_sites, *ch, key, proposal, init_draws, step_index, n_steps, thin, samples, base, extra,
+      round_offset, row0);
+  return check_launch("table_sweep");
 }
 
 int mpv_chains_init(const mpv_chains* ch, uint64_t key, int proposal, int sector_weight, void* stream) {

@@ -55,12 +55,52 @@ def default_chain_count(n_samples: int) -> int:
     return max(1, n_samples // DEFAULT_SAMPLES_PER_CHAIN)
 
 
+class TableLogProb:
+    """Evaluator backed by a dense table of (unnormalised) log-probabilities
+    indexed by configuration code (ref: sampler.py:254-268 table_log_prob);
+    the table lives on the device and ChainEnsemble runs mpv_table_sweep.
+    Callable on uint8 rows like the reference evaluator."""
+
+    MAX_SITES = 30
+
+    def __init__(self, log_values, n_sites: int, device=None):
+        import torch
+
+        nat.require_cuda()
+        table = np.asarray(log_values, dtype=np.float64).reshape(-1)
+        if table.size != 1 << int(n_sites):
+            raise ValueError("table size must be 2^n")
+        if not 1 <= int(n_sites) <= self.MAX_SITES:
+            raise ValueError(f"table evaluators support 1..{self.MAX_SITES} sites")
+        self.n_visible = int(n_sites)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.table = torch.from_numpy(np.ascontiguousarray(table)).to(self.device)
+
+    def __call__(self, bits):
+        import torch
+
+        bits = np.atleast_2d(np.asarray(bits, dtype=np.uint8))
+        if bits.shape[1] != self.n_visible:
+            raise ValueError("bit matrix width differs from the table's site count")
+        rows = torch.from_numpy(bits).to(self.device).to(torch.int64)
+        codes = (rows << torch.arange(self.n_visible, device=self.device)).sum(dim=1)
+        return self.table[codes].cpu().numpy()
+
+
+def table_log_prob(log_values, n_sites: int) -> TableLogProb:
+    return TableLogProb(log_values, n_sites)
+
+
+def uniform_log_prob(n_sites: int) -> TableLogProb:
+    return TableLogProb(np.zeros(1 << n_sites), n_sites)
+
+
 def _device_evaluator(evaluator):
     from .rbm import LogProbEvaluator
 
-    if not isinstance(evaluator, LogProbEvaluator):
+    if not isinstance(evaluator, (LogProbEvaluator, TableLogProb)):
         raise TypeError(
-            f"ChainEnsemble needs a device evaluator from rbm.log_prob_evaluator, got "
+            f"ChainEnsemble needs a device evaluator (rbm.log_prob_evaluator, sampler.table_log_prob), got "
             f"{type(evaluator).__name__} (the B200 path has no host-callable fallback)")
     return evaluator
 
@@ -115,6 +155,8 @@ class ChainEnsemble:
 
     # -- internals ----------------------------------------------------------
     def _bind_scratch(self):
+        if isinstance(self._evaluator, TableLogProb):
+            return
         need = nat.load().mpv_sweep_scratch_bytes(ctypes.byref(self._evaluator.snapshot.struct), self.n_chains)
         if self._scratch is None or self._scratch.numel() < need:
             import torch
@@ -127,10 +169,15 @@ class ChainEnsemble:
         return nat.stream_handle(self.device)
 
     def _launch(self, n_steps, thin=0, samples=None, n_samples_total=0, round_offset=0, row0=0):
-        nat.call("mpv_mh_sweep", ctypes.byref(self._evaluator.snapshot.struct), ctypes.byref(self._chains),
-                 self.key, self.proposal.code, self.init_draws, self.steps_done, int(n_steps), int(thin),
-                 samples.data_ptr() if samples is not None else None, int(n_samples_total),
-                 self.n_chains_total, int(round_offset), int(row0), self._stream())
+        sp = samples.data_ptr() if samples is not None else None
+        if isinstance(self._evaluator, TableLogProb):
+            nat.call("mpv_table_sweep", self._evaluator.table.data_ptr(), ctypes.byref(self._chains), self.key,
+                     self.proposal.code, self.init_draws, self.steps_done, int(n_steps), int(thin), sp,
+                     int(n_samples_total), self.n_chains_total, int(round_offset), int(row0), self._stream())
+        else:
+            nat.call("mpv_mh_sweep", ctypes.byref(self._evaluator.snapshot.struct), ctypes.byref(self._chains),
+                     self.key, self.proposal.code, self.init_draws, self.steps_done, int(n_steps), int(thin), sp,
+                     int(n_samples_total), self.n_chains_total, int(round_offset), int(row0), self._stream())
         self.steps_done += int(n_steps)
         self.proposed += self.n_chains * int(n_steps)
 

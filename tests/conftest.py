@@ -35,6 +35,11 @@ def g_chains():
 
 
 @pytest.fixture(scope="session")
+def g_table():
+    return golden("table_chains.npz")
+
+
+@pytest.fixture(scope="session")
 def g_energy():
     return golden("energy.npz")
 

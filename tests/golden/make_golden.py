@@ -193,6 +193,34 @@ def gen_train():
     save("train.npz", **arrays)
 
 
+def gen_table():
+    """Reference ChainEnsemble / run_chains driven by table_log_prob evaluators
+    (sampler.py:254-268) -> tests/golden/table_chains.npz."""
+    from mpvmc.sampler import table_log_prob, uniform_log_prob
+
+    arrays = {}
+    n = 6
+    table = np.random.default_rng(11).normal(0.0, 1.5, 1 << n)
+    table[5] = -np.inf  # an unreachable state
+    arrays["table"] = table
+    key = derive_key(8, "chains")
+    arrays["key"] = np.uint64(key)
+    for kind, weight in (("flip", None), ("exchange", 3)):
+        ens = ChainEnsemble(40, n, Proposal(kind, weight), table_log_prob(table, n), key)
+        done = 0
+        for cp in (0, 1, 50, 400):
+            ens.run_steps(cp - done)
+            done = cp
+            arrays[f"{kind}_bits_{cp}"] = ens.bits
+            arrays[f"{kind}_logp_{cp}"] = ens.log_probs
+            arrays[f"{kind}_acc_{cp}"] = np.array(ens.accepted)
+    samples, rate = run_chains(8, 64, 5, 1, 42, uniform_log_prob(4), Proposal("flip"), 4)
+    arrays["uniform_samples"], arrays["uniform_rate"] = samples, np.array(rate)
+    samples, rate = run_chains(16, 64, 10, 3, 4, table_log_prob(table, n), Proposal("exchange", 3), n)
+    arrays["exchange_samples"], arrays["exchange_rate"] = samples, np.array(rate)
+    save("table_chains.npz", **arrays)
+
+
 def gen_formats():
     """The reference's training-log writer (experiments.py:222-237, 611-624) on
     fixed records -> tests/golden/training_log_ref.csv (formats.py parity)."""
@@ -213,7 +241,11 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["formats"]:
         gen_formats()
         sys.exit(0)
+    if sys.argv[1:] == ["table"]:
+        gen_table()
+        sys.exit(0)
     gen_formats()
+    gen_table()
     gen_train()
     gen_rng()
     gen_forward()
