@@ -75,6 +75,13 @@ typedef struct {
   const void* vis;
   const double* vis_im;
   double quantum; /* XI: table integers are multiples of this power of two */
+  /* Frozen Gaussian log-density noise (ref: rbm.py:333-352 NoiseField,
+   * rbm.py:408-416 noisy_log_prob_evaluator): log p(x) += noise_sigma *
+   * ndtri(counter_uniform(noise_key, code(x))) with code(x) = sum_k bit_k 2^k
+   * (rng.py:56-60, 86-96).  noise_sigma == 0 disables it; only for f64
+   * arithmetic (fmt F64 / STORAGE_ONLY) and n_visible <= 64. */
+  uint64_t noise_key;
+  double noise_sigma;
 } mpv_snapshot;
 
 /* ---- snapshot build on the device (ref: rbm.py:91-101 round_parameters and

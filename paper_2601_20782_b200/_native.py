@@ -32,6 +32,7 @@ class Snapshot(ctypes.Structure):
         ("fmt", _i32), ("mode", _i32), ("variant", _i32),
         ("lanes_per_chain", _i32), ("units_per_lane", _i32),
         ("table", _vp), ("bias", _vp), ("vis", _vp), ("vis_im", _vp), ("quantum", _f64),
+        ("noise_key", _u64), ("noise_sigma", _f64),
     ]
 
 

@@ -211,6 +211,14 @@ __global__ void table_sweep_kernel(const double* __restrict__ table, int N, mpv_
   if (ch.accepted) ch.accepted[c] += n_acc;
 }
 
+__global__ void noise_add_kernel(const uint32_t* bits, int64_t B, int words, uint64_t key, double sigma,
+                                 double* out) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < B; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t code = (uint64_t)bits[r * words] | (words > 1 ? (uint64_t)bits[r * words + 1] << 32 : 0ull);
+    out[r] += mpv::noise_zeta(key, code, sigma);
+  }
+}
+
 __global__ void sum_i64_kernel(const int64_t* x, int64_t n, int64_t* out) {
   __shared__ long long part[32];
   long long acc = 0;
@@ -400,6 +408,7 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
   const int fmt = snap->fmt, mode = snap->mode;
 
   if (mode == MPV_MODE_PER_OPERATION && fmt != MPV_FMT_F64) {
+    if (snap->noise_sigma != 0.0) return fail(MPV_ERR_ARGS, "mh_sweep: log-density noise needs f64 arithmetic");
     PerOpSweepArgs a{};
     a.f.N = snap->n_visible; a.f.M = snap->n_hidden; a.f.Mpad = snap->hidden_pad; a.f.words = ch->words;
     a.f.table = snap->table; a.f.bias = snap->bias; a.f.vis = snap->vis; a.f.vis_im = snap->vis_im;
@@ -424,6 +433,8 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
 
   // fused sweep; f64 and storage-only run the f64 arithmetic
   const bool f64arith = (fmt == MPV_FMT_F64) || (mode == MPV_MODE_STORAGE_ONLY);
+  if (snap->noise_sigma != 0.0 && (!f64arith || snap->n_visible > 64))
+    return fail(MPV_ERR_ARGS, "mh_sweep: log-density noise needs f64 arithmetic and n_visible <= 64");
   const int kfmt = f64arith ? MPV_FMT_F64 : fmt;
   const int variant = f64arith ? MPV_ACC_F64 : snap->variant;
   const int G = snap->lanes_per_chain, U = snap->units_per_lane;
@@ -467,6 +478,8 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
   a.seg_len = seg_len; a.n_groups = n_groups; a.n_items = n_groups * n_segments;
   a.queue = queue; a.done = done; a.save = save; a.vis_save = vsave;
   a.xi_scale = (float)snap->quantum;
+  a.noise_key = snap->noise_key;
+  a.noise_sigma = snap->noise_sigma;
   if (variant == MPV_ACC_XI && !(snap->quantum > 0.0)) return fail(MPV_ERR_ARGS, "mh_sweep: XI needs quantum > 0");
   // flip kernels: 512-thread blocks (one staged table per 16 warps, <= 128 regs);
   // exchange kernels need more registers: 256-thread blocks
@@ -536,6 +549,13 @@ int mpv_snapshot_forward(const mpv_snapshot* snap, const uint32_t* bits, int64_t
   const unsigned grid = (unsigned)std::min<int64_t>((B + nw - 1) / nw, 148 * 32);
   const cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, st);
   if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("snapshot_forward: ") + cudaGetErrorString(e));
+  if (snap->noise_sigma != 0.0) {
+    if (snap->n_visible > 64 || !(fmt == MPV_FMT_F64 || mode == MPV_MODE_STORAGE_ONLY))
+      return fail(MPV_ERR_ARGS, "snapshot_forward: log-density noise needs f64 arithmetic and n_visible <= 64");
+    noise_add_kernel<<<(unsigned)std::min<int64_t>((B + 255) / 256, 148 * 8), 256, 0, st>>>(
+        bits, B, words, snap->noise_key, snap->noise_sigma, out_lp);
+    return check_launch("snapshot_forward noise");
+  }
   return MPV_OK;
 }
 

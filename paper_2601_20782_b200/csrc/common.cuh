@@ -172,6 +172,14 @@ template <> struct Half<MPV_FMT_BF16> {
 
 // Warp-segment (width G) xor-butterfly sum.  Commutativity of IEEE addition
 // makes every lane of the segment end with the identical value.
+// Frozen Gaussian log-density noise of a configuration code (ref: rng.py:56-60
+// counter_uniform, rng.py:86-96 gaussian_field): sigma * ndtri(u), u =
+// uniform_from_bits(mix64((code + 1) * G ^ key)).
+__device__ __forceinline__ double noise_zeta(uint64_t key, uint64_t code, double sigma) {
+  const double u = uniform_from_bits(mix64(((code + 1ull) * 0x9E3779B97F4A7C15ull) ^ key));
+  return sigma * normcdfinv(u);
+}
+
 template <typename T>
 __device__ __forceinline__ T segment_sum(T v, int G) {
   for (int off = G >> 1; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off, G);

@@ -42,7 +42,16 @@ struct SweepArgs {
   int* done;          // [n_groups] segments finished, zero at launch
   float* save;        // [n_groups][save_words][32] theta between segments
   void* vis_save;     // [n_chains] visible term between segments
+  uint64_t noise_key;  // frozen log-density noise (f64 arithmetic, N <= 64); sigma 0 = off
+  double noise_sigma;
 };
+
+// code(x) of the configuration spread over a segment's lanes (word w in lane w)
+__device__ __forceinline__ uint64_t segment_code(uint32_t word, int words, int G) {
+  const uint32_t w0 = __shfl_sync(kFull, word, 0, G);
+  const uint32_t w1 = __shfl_sync(kFull, word, 1 % G, G);
+  return (uint64_t)w0 | (words > 1 ? (uint64_t)w1 << 32 : 0ull);
+}
 
 // ------------------------------------------------------------------------
 // Unit evaluators: Re log cosh of one hidden unit in the snapshot's arithmetic.
@@ -511,6 +520,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, 1) sw
       }
       h0 = segment_sum(h0, G);
       lp = E::finalize(vis, h0, sc);
+      if (a.noise_sigma != 0.0) lp = (Lp)((double)lp + noise_zeta(a.noise_key, segment_code(myword, words, G), a.noise_sigma));
       if (!isfinite(lp)) {
         if (live && gl == 0) report_nonfinite(a.status, 0, cidx);
         lp = Lp(NAN);  // NaN marks a frozen chain
@@ -628,7 +638,9 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, 1) sw
       h = segment_sum(h, G);
       VisT vnew = vis_add(vis, visv[k1], dsign);
       if (PROP == MPV_PROPOSAL_EXCHANGE) vnew = vis_add(vnew, visv[k2], -dsign);
-      const Lp lp_new = E::finalize(vnew, h, sc);
+      Lp lp_new = E::finalize(vnew, h, sc);
+      if (a.noise_sigma != 0.0)
+        lp_new = (Lp)((double)lp_new + noise_zeta(a.noise_key, segment_code(myword ^ flip, words, G), a.noise_sigma));
       // ref sampler.py:128-129: NaN compares false (reject); the reference raises
       // EvaluationFailureError on any non-finite proposal (rbm.py:242-251): the
       // chain freezes and the first failure is reported.

@@ -25,7 +25,7 @@ from . import _native as nat
 from .errors import EvaluationFailureError
 from .lattice import pack_bits
 from .precision import F64, FloatFormat, RoundingMode, make_rounder
-from .rng import gaussian_field
+from .rng import derive_key, gaussian_field
 
 
 @dataclass(frozen=True)
@@ -396,6 +396,44 @@ def _raise_nonfinite(status, bits, what):
         bad = int(st[1])
         raise EvaluationFailureError(f"non-finite {what} for configuration bits {bits[bad].tolist()}",
                                      context={"bits": bits[bad].copy()})
+
+
+@dataclass(frozen=True)
+class NoiseField:
+    """Frozen Gaussian log-density noise: std sigma, fixed per (seed, x)
+    (rbm.py:333-352).  On the device it is added inside the f64 sweep and the
+    forward (mpv_snapshot noise_key / noise_sigma)."""
+
+    sigma: float
+    seed: int
+
+    def __post_init__(self):
+        if self.sigma < 0:
+            raise ValueError("sigma must be >= 0")
+
+    @property
+    def key(self):
+        return derive_key(self.seed, "noise-field")
+
+    def zeta(self, codes) -> np.ndarray:
+        """delta(x) = zeta(x) for configuration codes (host; rbm.py:347-352)."""
+        codes = np.asarray(codes, dtype=np.uint64)
+        if self.sigma == 0.0:
+            return np.zeros(codes.shape)
+        return gaussian_field(self.key, codes, self.sigma)
+
+
+def noisy_log_prob_evaluator(params, noise: NoiseField, device=None) -> LogProbEvaluator:
+    """f64 log-probability plus the frozen noise field (rbm.py:408-416), as a
+    device evaluator: ChainEnsemble runs the fused f64 sweep with the noise
+    added to every proposal's log p (N <= 64, like the reference's codes)."""
+    if params.n_visible > 64:
+        raise ValueError("noise fields are keyed by 64-bit configuration codes (n_visible <= 64)")
+    ev = LogProbEvaluator(params, F64, RoundingMode.PER_OPERATION, device)
+    ev.noise = noise
+    ev.snapshot.struct.noise_key = int(noise.key)
+    ev.snapshot.struct.noise_sigma = float(noise.sigma)
+    return ev
 
 
 def log_prob_evaluator(params, fmt: FloatFormat = F64, mode: RoundingMode = RoundingMode.PER_OPERATION,

@@ -221,6 +221,29 @@ def gen_table():
     save("table_chains.npz", **arrays)
 
 
+def gen_noisy():
+    """Reference ChainEnsemble with noisy_log_prob_evaluator (rbm.py:333-352,
+    408-416) -> tests/golden/noisy_chains.npz."""
+    arrays = {}
+    n = 10
+    p = rbm.random_parameters(n, 2, derive_key(3, "noisy"), 0.3)
+    arrays["a"], arrays["b"], arrays["w"] = p.a, p.b, p.w
+    noise = rbm.NoiseField(0.4, 5)
+    key = derive_key(6, "chains")
+    arrays["key"] = np.uint64(key)
+    ev = rbm.noisy_log_prob_evaluator(p, noise)
+    bits = np.random.default_rng(4).integers(0, 2, size=(64, n), dtype=np.uint8)
+    arrays["eval_bits"], arrays["eval_lp"] = bits, ev(bits)
+    ens = ChainEnsemble(64, n, Proposal("flip"), ev, key)
+    done = 0
+    for cp in (0, 1, 50, 300):
+        ens.run_steps(cp - done)
+        done = cp
+        arrays[f"bits_{cp}"], arrays[f"logp_{cp}"] = ens.bits, ens.log_probs
+        arrays[f"acc_{cp}"] = np.array(ens.accepted)
+    save("noisy_chains.npz", **arrays)
+
+
 def gen_formats():
     """The reference's training-log writer (experiments.py:222-237, 611-624) on
     fixed records -> tests/golden/training_log_ref.csv (formats.py parity)."""
@@ -244,8 +267,12 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["table"]:
         gen_table()
         sys.exit(0)
+    if sys.argv[1:] == ["noisy"]:
+        gen_noisy()
+        sys.exit(0)
     gen_formats()
     gen_table()
+    gen_noisy()
     gen_train()
     gen_rng()
     gen_forward()
