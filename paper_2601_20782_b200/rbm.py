@@ -482,3 +482,52 @@ def log_psi_batch(params, bits, fmt: FloatFormat = F64, mode: RoundingMode = Rou
     out = re.cpu().numpy() + 1j * im.cpu().numpy()
     _raise_nonfinite(status, bits, "log psi")
     return out
+
+
+# ---------------------------------------------------------------------------
+# delta-distribution studies (rbm.py:429-492): delta(x) = log p_fmt - log p_f64
+# evaluated on the device over the full enumeration; summaries on the host.
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class DeltaSummary:
+    """Moments of delta over the enumerated space plus its Shapiro-Wilk W."""
+
+    mean: float
+    std: float
+    skewness: float
+    excess_kurtosis: float
+    shapiro_wilk_w: float
+    shapiro_n: int
+
+
+def precision_delta(params, fmt, mode, bits) -> np.ndarray:
+    """delta on an arbitrary batch (rbm.py:472-474), both evaluations on the device."""
+    return log_prob_batch(params, bits, fmt, mode) - log_prob_batch(params, bits, F64)
+
+
+def delta_distribution(params, fmt, mode, lattice_spec):
+    """(DeltaSummary, delta vector) over the full enumeration (rbm.py:440-469);
+    Shapiro-Wilk on the standardised field, deterministically subsampled to
+    5000 points by the reference's counter-based order."""
+    from .lattice import enumerate_bits
+    from .normality import shapiro_wilk, standardize
+    from .rng import counter_uniform
+
+    bits = enumerate_bits(lattice_spec.n_sites)
+    delta = precision_delta(params, fmt, mode, bits)
+    mean, std = float(delta.mean()), float(delta.std())
+    if std == 0.0:
+        return DeltaSummary(mean, 0.0, 0.0, 0.0, float("nan"), 0), delta
+    z = standardize(delta)
+    sample = z
+    if sample.size > 5000:
+        order = np.argsort(counter_uniform(derive_key(0, "sw-subsample"), np.arange(sample.size)))
+        sample = sample[order[:5000]]
+    report = shapiro_wilk(sample)
+    return DeltaSummary(mean, std, float((z**3).mean()), float((z**4).mean() - 3.0), report.w, report.n), delta
+
+
+def delta_for_noise(params, noise: NoiseField, n: int) -> np.ndarray:
+    """delta induced by a frozen noise field over the full enumeration (rbm.py:477-480)."""
+    return noise.zeta(np.arange(1 << n, dtype=np.uint64))

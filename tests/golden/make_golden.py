@@ -244,6 +244,29 @@ def gen_noisy():
     save("noisy_chains.npz", **arrays)
 
 
+def gen_delta():
+    """rbm.delta_distribution (rbm.py:440-469) and normality.shapiro_wilk on
+    fixed inputs -> tests/golden/delta.npz."""
+    from mpvmc import normality
+    from mpvmc.lattice import LatticeSpec as RefLattice
+
+    arrays = {}
+    for tag, (n, alpha, seed, scale, fmt) in {
+            "f16_n12": (12, 1, 16, 0.05, F16), "bf16_n8": (8, 2, 15, 0.3, BF16), "f32_n8": (8, 2, 15, 0.3, F32),
+            "f16_n14": (14, 1, 3, 0.2, F16)}.items():
+        p = rbm.random_parameters(n, alpha, derive_key(seed, "delta"), scale)
+        summary, delta = rbm.delta_distribution(p, fmt, PER_OP, RefLattice.chain(n))
+        arrays[f"{tag}_delta"] = delta
+        arrays[f"{tag}_summary"] = np.array([summary.mean, summary.std, summary.skewness, summary.excess_kurtosis,
+                                             summary.shapiro_wilk_w, summary.shapiro_n])
+        arrays[f"{tag}_meta"] = np.array([n, alpha, seed, scale])
+    x = np.random.default_rng(5).standard_t(5, size=777)
+    arrays["sw_x"] = x
+    arrays["sw_w"] = np.array(normality.shapiro_wilk(x).w)
+    arrays["sw_a20"] = normality._sw_coefficients(20)
+    save("delta.npz", **arrays)
+
+
 def gen_formats():
     """The reference's training-log writer (experiments.py:222-237, 611-624) on
     fixed records -> tests/golden/training_log_ref.csv (formats.py parity)."""
@@ -270,9 +293,13 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["noisy"]:
         gen_noisy()
         sys.exit(0)
+    if sys.argv[1:] == ["delta"]:
+        gen_delta()
+        sys.exit(0)
     gen_formats()
     gen_table()
     gen_noisy()
+    gen_delta()
     gen_train()
     gen_rng()
     gen_forward()

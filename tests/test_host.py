@@ -176,3 +176,15 @@ def test_training_log_sidecar_and_samples(tmp_path):
     smp = np.random.default_rng(0).integers(0, 2, size=(7, 5), dtype=np.uint8)
     p = formats.save_samples(tmp_path / "s.npy", smp)
     assert np.array_equal(formats.load_samples(p), smp)
+
+
+def test_shapiro_wilk_matches_reference():
+    """normality.shapiro_wilk / sw_coefficients equal the reference's
+    (golden from normality.py itself, tests/golden/make_golden.py gen_delta)."""
+    import os
+
+    from paper_2601_20782_b200 import normality
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "delta.npz"))
+    np.testing.assert_allclose(normality.sw_coefficients(20), g["sw_a20"], rtol=1e-14, atol=1e-15)
+    assert normality.shapiro_wilk(g["sw_x"]).w == pytest.approx(float(g["sw_w"]), rel=1e-13)
