@@ -196,6 +196,20 @@ int mpv_local_energies_ex(int N, int M, const double* a, const double* b, const 
                           const uint32_t* bits, int64_t B, double* out_eps, int64_t* status,
                           void* stream);
 
+/* ---- products with the log-derivative matrix O (ref: rbm.py:307-325
+ *      grad_log_psi_batch, O(x) = [x, tanh theta, tanh theta (x) x]; the SR
+ *      estimators of vmc.py:145-229 evaluated matrix-free) ----
+ * t: tanh(theta) complex [U][M]; bits: packed [U][ceil(N/32)]; v, out:
+ * complex P-vectors (P = N + M + M N, order a, b, W row-major); q, u:
+ * complex U-vectors.  mpv_logderiv_ov: q = O v.  mpv_logderiv_ohu:
+ * out = O^H u = sum_s conj(O_s) u_s (deterministic: fixed-order chunk sums).
+ * `scratch` >= mpv_logderiv_scratch_bytes(U, N, M).  N <= 256, M <= 512. */
+size_t mpv_logderiv_scratch_bytes(int64_t U, int N, int M);
+int mpv_logderiv_ov(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* v,
+                    double* q, void* scratch, void* stream);
+int mpv_logderiv_ohu(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* u,
+                     double* out, void* scratch, void* stream);
+
 /* ---- helpers ---- */
 int mpv_unpack_bits(const uint32_t* words, int64_t B, int N, uint8_t* out, void* stream);
 int mpv_pack_bits(const uint8_t* bits, int64_t B, int N, uint32_t* out, void* stream);

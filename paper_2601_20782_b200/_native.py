@@ -52,6 +52,9 @@ _SIGNATURES = {
     "mpv_snapshot_fill": (ctypes.c_int, [ctypes.POINTER(Snapshot), _vp, ctypes.c_double, _vp]),
     "mpv_table_sweep": (ctypes.c_int, [_vp, ctypes.POINTER(Chains), _u64, ctypes.c_int, _i64, _i64, _i64, _i64, _vp,
                                        _i64, _i64, _i64, _i64, _vp]),
+    "mpv_logderiv_scratch_bytes": (ctypes.c_size_t, [_i64, ctypes.c_int, ctypes.c_int]),
+    "mpv_logderiv_ov": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    "mpv_logderiv_ohu": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
     "mpv_chains_init": (ctypes.c_int, [ctypes.POINTER(Chains), _u64, ctypes.c_int, ctypes.c_int, _vp]),
     "mpv_mh_sweep": (ctypes.c_int, [ctypes.POINTER(Snapshot), ctypes.POINTER(Chains), _u64, ctypes.c_int,
                                     _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),

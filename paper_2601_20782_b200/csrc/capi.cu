@@ -8,6 +8,7 @@
 #include <unordered_map>
 
 #include "energy.cuh"
+#include "logderiv.cuh"
 #include "perop.cuh"
 #include "snapshot.cuh"
 #include "sweep.cuh"
@@ -705,6 +706,53 @@ int mpv_local_energies_ex(int N, int M, const double* a, const double* b, const 
       }
   }
   return fail(MPV_ERR_ARGS, "local_energies: n_hidden / terms too large for shared memory");
+}
+
+static size_t ld_ov_bytes(int N, int M) { return ((size_t)ld_rows(N) * ld_pitch(M) * sizeof(double) + 255) / 256 * 256; }
+
+size_t mpv_logderiv_scratch_bytes(int64_t U, int N, int M) {
+  const int64_t chunks = (U + kLdChunk - 1) / kLdChunk;
+  return ld_ov_bytes(N, M) + (size_t)chunks * ld_rows_a(M) * ld_col_groups(N) * 8 * kLdNT * sizeof(double);
+}
+
+int mpv_logderiv_ov(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* v, double* q,
+                    void* scratch, void* stream) {
+  if (!t || !bits || !v || !q || !scratch || U < 0 || N < 1 || N > 256 || M < 1 || M > 512)
+    return fail(MPV_ERR_ARGS, "logderiv_ov: bad args (N <= 256, M <= 512)");
+  if (U == 0) return MPV_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  double* vwt = (double*)scratch;
+  const int64_t n = (int64_t)ld_rows(N) * ld_pitch(M);
+  ld_transpose_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, st>>>(
+      (const double2*)v, N, M, vwt);
+  const int NT = (M + 3) / 4, kt = (NT + 7) / 8;
+  const unsigned grid = (unsigned)((U + kLdSB - 1) / kLdSB);
+  const int words = (N + 31) / 32;
+  const double2* T = (const double2*)t;
+  if (kt <= 2) ld_ov_kernel<2><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, (const double2*)v, vwt, (double2*)q);
+  else if (kt <= 4) ld_ov_kernel<4><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, (const double2*)v, vwt, (double2*)q);
+  else if (kt <= 8) ld_ov_kernel<8><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, (const double2*)v, vwt, (double2*)q);
+  else ld_ov_kernel<16><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, (const double2*)v, vwt, (double2*)q);
+  return check_launch("logderiv_ov");
+}
+
+int mpv_logderiv_ohu(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* u, double* out,
+                     void* scratch, void* stream) {
+  if (!t || !bits || !u || !out || !scratch || U < 0 || N < 1 || N > 256 || M < 1)
+    return fail(MPV_ERR_ARGS, "logderiv_ohu: bad args (N <= 256)");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int P = N + M + M * N;
+  if (U == 0) {
+    if (cudaMemsetAsync(out, 0, (size_t)P * 2 * sizeof(double), st) != cudaSuccess) return check_launch("logderiv_ohu");
+    return MPV_OK;
+  }
+  double* partial = (double*)((char*)scratch + ld_ov_bytes(N, M));
+  const int chunks = (int)((U + kLdChunk - 1) / kLdChunk);
+  const dim3 grid((unsigned)(ld_rows_a(M) / 64), (unsigned)chunks, (unsigned)ld_col_groups(N));
+  ld_ohu_kernel<<<grid, 256, 0, st>>>((const double2*)t, bits, U, N, M, (N + 31) / 32, (const double2*)u, partial);
+  ld_ohu_reduce_kernel<<<(unsigned)std::min(148 * 8, (P + 255) / 256), 256, 0, st>>>(partial, chunks, N, M,
+                                                                                      (double2*)out);
+  return check_launch("logderiv_ohu");
 }
 
 int mpv_unpack_bits(const uint32_t* words, int64_t B, int N, uint8_t* out, void* stream) {

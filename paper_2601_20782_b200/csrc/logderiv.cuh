@@ -1,0 +1,230 @@
+// Products with the RBM log-derivative matrix O (ref: rbm.py:307-325
+// grad_log_psi_batch: O(x) = [x, tanh theta, tanh theta (x) x], columns a, b,
+// W row-major) without forming O: the SR solve (vmc.py:145-229 estimators,
+// solved matrix-free) needs O v and O^H u per conjugate-gradient iteration.
+// X (samples x sites) is 0/1 and arrives bit-packed, T = tanh(theta) is a
+// complex (U, M) matrix; both products are GEMMs over X on the FP64 tensor
+// cores (DMMA m8n8k4), with the rest fused into their epilogues:
+//
+//   ov:  q_s = sum_k x_sk va_k + sum_i t_si (vb_i + (X vW^T)_si)
+//        block = 16 samples; (X vW^T) as the energy kernel's theta GEMM
+//        (A = sample bits, B = vW^T in the padded staging layout); the
+//        epilogue multiplies by t and reduces over units in a fixed order.
+//   ohu: out = [X^T u, T^H u, (conj(T) * u)^T X]  ==  A' B' with
+//        A' rows (2i, 2i+1) = Re/Im conj(t_si) u_s, rows (2M, 2M+1) = Re/Im u_s,
+//        B' = [X | 1]; split over sample chunks (K), partial sums reduced in a
+//        fixed chunk order (deterministic).
+#pragma once
+#include "common.cuh"
+
+namespace mpv {
+
+constexpr int kLdSB = 16;       // samples per ov block
+constexpr int kLdChunk = 1024;  // samples per ohu K-chunk
+
+__device__ __forceinline__ void ld_dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__host__ __device__ inline int ld_pitch(int M) { return 2 * M + 8; }  // doubles per vW^T row
+__host__ __device__ inline int ld_rows(int N) { return (N + 3) / 4 * 4; }
+
+// vW (row-major [M][N] complex, the W block of v) -> vWt[k][2i + c] padded
+__global__ void ld_transpose_kernel(const double2* __restrict__ v, int N, int M, double* __restrict__ vwt) {
+  const int pitch = ld_pitch(M), rows = ld_rows(N);
+  const double2* vw = v + N + M;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (int64_t)rows * pitch;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx / pitch), c = (int)(idx % pitch);
+    double val = 0.0;
+    if (k < N && c < 2 * M) {
+      const double2 z = vw[(size_t)(c >> 1) * N + k];
+      val = (c & 1) ? z.y : z.x;
+    }
+    vwt[idx] = val;
+  }
+}
+
+template <int KT>
+__global__ void __launch_bounds__(256) ld_ov_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
+                                                    int64_t U, int N, int M, int words, const double2* __restrict__ v,
+                                                    const double* __restrict__ vwt, double2* __restrict__ q) {
+  __shared__ uint32_t smask[256 + 8];        // per-site masks of the block's 16 samples (N <= 256)
+  __shared__ double2 red[8][kLdSB];          // per-warp partial q
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t s0 = (int64_t)blockIdx.x * kLdSB;
+  const int pitch = ld_pitch(M), rows = ld_rows(N);
+  for (int k = tid; k < rows; k += blockDim.x) {
+    uint32_t m = 0;
+    if (k < N)
+      for (int s = 0; s < kLdSB; ++s)
+        if (s0 + s < U) m |= ((bits[(s0 + s) * words + (k >> 5)] >> (k & 31)) & 1u) << s;
+    smask[k] = m;
+  }
+  __syncthreads();
+  const int NT = (M + 3) / 4;
+  const int qr = lane & 3, qc = lane >> 2;
+  double acc[KT][2][2];
+  int col[KT];
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    col[j] = min(warp + j * 8, NT - 1) * 8 + qc;
+    acc[j][0][0] = acc[j][0][1] = acc[j][1][0] = acc[j][1][1] = 0.0;
+  }
+  for (int k0 = 0; k0 < rows; k0 += 4) {
+    const double* brow = vwt + (size_t)(k0 + qr) * pitch;
+    double bf[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) bf[j] = __ldg(brow + col[j]);
+    const uint32_t mk = smask[k0 + qr];
+    const double a0 = __hiloint2double((int)(((mk >> qc) & 1u) * 0x3ff00000u), 0);
+    const double a1 = __hiloint2double((int)(((mk >> (8 + qc)) & 1u) * 0x3ff00000u), 0);
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      ld_dmma(acc[j][0][0], acc[j][0][1], a0, bf[j]);
+      ld_dmma(acc[j][1][0], acc[j][1][1], a1, bf[j]);
+    }
+  }
+  // epilogue: D fragment (sample m*8 + qc, unit nt*4 + qr) -> t * (Y + vb), summed over units
+  double2 part[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    const int nt = warp + j * 8, i = nt * 4 + qr;
+    if (nt < NT && i < M) {
+      const double2 vb = v[N + i];
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int64_t s = s0 + m * 8 + qc;
+        if (s < U) {
+          const double2 ts = t[s * M + i];
+          const double yr = acc[j][m][0] + vb.x, yi = acc[j][m][1] + vb.y;
+          part[m].x = fma(ts.x, yr, fma(-ts.y, yi, part[m].x));
+          part[m].y = fma(ts.x, yi, fma(ts.y, yr, part[m].y));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    for (int off = 1; off < 4; off <<= 1) {
+      part[m].x += __shfl_xor_sync(kFull, part[m].x, off);
+      part[m].y += __shfl_xor_sync(kFull, part[m].y, off);
+    }
+    if (qr == 0) red[warp][m * 8 + qc] = part[m];
+  }
+  __syncthreads();
+  if (tid < kLdSB && s0 + tid < U) {
+    const int64_t s = s0 + tid;
+    double2 acc2 = make_double2(0.0, 0.0);
+    for (int k = 0; k < N; ++k)  // sum_k x_sk va_k, ascending k
+      if ((smask[k] >> tid) & 1u) {
+        acc2.x += v[k].x;
+        acc2.y += v[k].y;
+      }
+    for (int w = 0; w < 8; ++w) {
+      acc2.x += red[w][tid].x;
+      acc2.y += red[w][tid].y;
+    }
+    q[s] = acc2;
+  }
+}
+
+// ohu partials: block (row group x, chunk y, column group z); warp = one
+// m-tile (8 rows of A'), kLdNT n-tiles (64 columns of B' = [X | 1]).
+constexpr int kLdNT = 8;
+__host__ __device__ inline int ld_col_groups(int N) { return (N + 1 + 8 * kLdNT - 1) / (8 * kLdNT); }
+__host__ __device__ inline int ld_rows_a(int M) { return (2 * M + 2 + 63) / 64 * 64; }  // A' rows, whole blocks
+
+constexpr int kLdTile = 64;  // samples staged per ohu sub-tile
+
+__global__ void __launch_bounds__(256) ld_ohu_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
+                                                     int64_t U, int N, int M, int words, const double2* __restrict__ u,
+                                                     double* __restrict__ partial) {
+  // A' tile [64 rows][kLdTile samples] (+1 pad against bank conflicts) and the samples' bits
+  __shared__ double as[64][kLdTile + 1];
+  __shared__ uint32_t bs[kLdTile][9];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows_a = 2 * M + 2;
+  const int r0 = blockIdx.x * 64;                // first A' row of this block (32 units)
+  const int64_t k_begin = (int64_t)blockIdx.y * kLdChunk;
+  const int64_t k_end = min(U, k_begin + kLdChunk);
+  const int c0 = blockIdx.z * 8 * kLdNT;         // first B' column of this block
+  const int qr = lane & 3, qc = lane >> 2;
+  double acc[kLdNT][2];
+#pragma unroll
+  for (int j = 0; j < kLdNT; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int64_t sb = k_begin; sb < k_end; sb += kLdTile) {
+    __syncthreads();
+    // stage: thread -> (sample, unit pair); unit loads are contiguous per sample
+    for (int idx = tid; idx < kLdTile * 32; idx += blockDim.x) {
+      const int ls = idx >> 5, lu = idx & 31;  // local sample, local unit
+      const int64_t s = sb + ls;
+      const int ui = (r0 >> 1) + lu;
+      double re = 0.0, im = 0.0;
+      if (s < k_end) {
+        const double2 us = u[s];
+        if (ui < M) {
+          const double2 ts = t[s * M + ui];  // conj(t) u
+          re = fma(ts.x, us.x, ts.y * us.y);
+          im = fma(ts.x, us.y, -ts.y * us.x);
+        } else if (2 * ui < rows_a) {  // rows 2M, 2M+1: u itself (a-part)
+          re = us.x;
+          im = us.y;
+        }
+      }
+      as[2 * lu][ls] = re;
+      as[2 * lu + 1][ls] = im;
+    }
+    for (int idx = tid; idx < kLdTile * words; idx += blockDim.x) {
+      const int ls = idx / words, w = idx % words;
+      bs[ls][w] = (sb + ls < k_end) ? bits[(sb + ls) * words + w] : 0u;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k0 = 0; k0 < kLdTile; k0 += 4) {
+      const double av = as[warp * 8 + qc][k0 + qr];
+      const uint32_t* bw = bs[k0 + qr];
+      const bool valid = sb + k0 + qr < k_end;
+#pragma unroll
+      for (int j = 0; j < kLdNT; ++j) {
+        const int n = c0 + j * 8 + qc;  // B' column of this lane
+        const uint32_t bit = n < N ? ((bw[n >> 5] >> (n & 31)) & 1u) : (n == N && valid ? 1u : 0u);
+        ld_dmma(acc[j][0], acc[j][1], av, __hiloint2double((int)(bit * 0x3ff00000u), 0));
+      }
+    }
+  }
+  // D fragment: row r0 + warp*8 + qc, columns c0 + j*8 + 2*qr (+1) -> partial[chunk][row][col]
+  const int cols = ld_col_groups(N) * 8 * kLdNT;
+  double* out = partial + (size_t)blockIdx.y * ld_rows_a(M) * cols;
+  const int row = r0 + warp * 8 + qc;
+  if (row < ld_rows_a(M)) {
+#pragma unroll
+    for (int j = 0; j < kLdNT; ++j) {
+      out[(size_t)row * cols + c0 + j * 8 + 2 * qr] = acc[j][0];
+      out[(size_t)row * cols + c0 + j * 8 + 2 * qr + 1] = acc[j][1];
+    }
+  }
+}
+
+// fixed-order reduction of the chunk partials -> out (complex P-vector)
+__global__ void ld_ohu_reduce_kernel(const double* __restrict__ partial, int chunks, int N, int M,
+                                     double2* __restrict__ out) {
+  const int rows_pad = ld_rows_a(M), cols = ld_col_groups(N) * 8 * kLdNT;
+  const int P = N + M + M * N;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < P; idx += gridDim.x * blockDim.x) {
+    int r, c;  // (row pair, column) of the entry
+    if (idx < N) { r = M; c = idx; }                       // a-part: rows 2M, 2M+1 (u), column k
+    else if (idx < N + M) { r = idx - N; c = N; }          // b-part: unit i, ones column
+    else { r = (idx - N - M) / N; c = (idx - N - M) % N; }  // W-part: unit i, site k
+    double re = 0.0, im = 0.0;
+    for (int ch = 0; ch < chunks; ++ch) {
+      const double* p = partial + (size_t)ch * rows_pad * cols;
+      re += p[(size_t)(2 * r) * cols + c];
+      im += p[(size_t)(2 * r + 1) * cols + c];
+    }
+    out[idx] = make_double2(re, im);
+  }
+}
+
+}  // namespace mpv

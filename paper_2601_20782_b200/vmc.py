@@ -232,34 +232,48 @@ def sr_step(f, s, lambda_shift: float, eta: float, compute_kappa: bool = True) -
 
 class FactoredLogDerivatives:
     """O(x) = [x, tanh(theta), tanh(theta) (x) x] (rbm.py:307-325) kept in factored
-    form: X (U, N) 0/1 and T = tanh(b + W x) (U, M) complex, never the (U, P)
-    matrix (P = N + M + M N is 20,300 at config 2: O would be 21 GB and S 6.6 GB).
-    Products with O and O^H are one (U, M, N) ZGEMM each (cuBLAS, f64):
-
-      O v   = X v_a + T v_b + rowsum(X * (T v_W))
-      O^H u = [X^T u, T^H u, T^H (u * X)  (row-major W block)]
-
+    form: the packed sample bits X and T = tanh(b + W x) (U, M) complex, never
+    the (U, P) matrix (P = N + M + M N is 20,300 at config 2: O would be 21 GB
+    and S 6.6 GB).  O v and O^H u run in csrc/logderiv.cuh as DMMA GEMMs over
+    the bits with fused epilogues (mpv_logderiv_ov / mpv_logderiv_ohu).
     `reduce` (optional) all-reduces sums over samples across ranks."""
 
-    def __init__(self, params, bits_u8, reduce=None):
+    def __init__(self, params, bits_u8, packed=None, reduce=None):
         import torch
 
         dev = bits_u8.device
         self.N, self.M = params.n_visible, params.n_hidden
-        self.x = bits_u8.to(torch.complex128)
-        self.t = torch.tanh(self.x @ _t(params.w, dev).T + _t(params.b, dev)[None, :])
+        self.U = bits_u8.shape[0]
+        if packed is None:
+            packed = torch.empty((self.U, (self.N + 31) // 32), dtype=torch.int32, device=dev)
+            if self.U:
+                nat.call("mpv_pack_bits", bits_u8.data_ptr(), self.U, self.N, packed.data_ptr(), nat.stream_handle(dev))
+        self.packed = packed.contiguous()
+        x = bits_u8.to(torch.complex128)
+        self.t = torch.tanh(x @ _t(params.w, dev).T + _t(params.b, dev)[None, :]).contiguous()
+        self.scratch = torch.empty(nat.load().mpv_logderiv_scratch_bytes(self.U, self.N, self.M), dtype=torch.uint8,
+                                   device=dev)
         self.reduce = reduce or (lambda z: z)
+        self.device = dev
 
     def o_v(self, v):
-        N, M = self.N, self.M
-        return self.x @ v[:N] + self.t @ v[N:N + M] + (self.x * (self.t @ v[N + M:].reshape(M, N))).sum(dim=1)
+        import torch
+
+        v = v.contiguous()
+        q = torch.empty(self.U, dtype=torch.complex128, device=self.device)
+        nat.call("mpv_logderiv_ov", self.t.data_ptr(), self.packed.data_ptr(), self.U, self.N, self.M, v.data_ptr(),
+                 q.data_ptr(), self.scratch.data_ptr(), nat.stream_handle(self.device))
+        return q
 
     def oh_u(self, u):
         """sum_s conj(O_s) u_s (local sums; callers reduce)."""
         import torch
 
-        th = self.t.mH
-        return torch.cat([self.x.T @ u, th @ u, (th @ (u[:, None] * self.x)).reshape(-1)])
+        u = u.contiguous()
+        out = torch.empty(self.N + self.M + self.M * self.N, dtype=torch.complex128, device=self.device)
+        nat.call("mpv_logderiv_ohu", self.t.data_ptr(), self.packed.data_ptr(), self.U, self.N, self.M, u.data_ptr(),
+                 out.data_ptr(), self.scratch.data_ptr(), nat.stream_handle(self.device))
+        return out
 
 
 def sr_step_cg(o: FactoredLogDerivatives, eps, weights, lambda_shift: float, eta: float,
@@ -440,7 +454,7 @@ def train(config: TrainConfig, device=None, group=None) -> TrainResult:
         nat.call("mpv_unpack_bits", uniq.data_ptr(), uniq.shape[0], n, u8.data_ptr(), nat.stream_handle(dev))
         if config.sr_solver == "cg":
             red = (lambda z: parallel.all_reduce_sum(z, group)) if world > 1 else None
-            fo = FactoredLogDerivatives(params, u8, red)
+            fo = FactoredLogDerivatives(params, u8, uniq, red)
             update, f, energy = sr_step_cg(fo, eps, est_w, config.lambda_shift, config.eta, config.cg_tol,
                                            config.cg_maxiter)
         else:

@@ -25,18 +25,20 @@ def _setup(n=20, alpha=1, U=1500, scale=0.3, seed=0):
     return p, bits, w, eps
 
 
-def test_factored_products_match_materialised_o(cuda):
+@pytest.mark.parametrize("n,alpha,U", [(20, 1, 1500), (37, 2, 2049), (100, 2, 3000), (8, 4, 5)])
+def test_factored_products_match_materialised_o(cuda, n, alpha, U):
     import torch
 
-    p, bits, w, _ = _setup()
+    p, bits, w, _ = _setup(n=n, alpha=alpha, U=U)
     o = vmc.grad_log_psi_device(p, bits)
     fo = vmc.FactoredLogDerivatives(p, bits)
     rng = np.random.default_rng(1)
     P = o.shape[1]
     v = torch.complex(torch.from_numpy(rng.normal(size=P)), torch.from_numpy(rng.normal(size=P))).cuda()
     u = torch.complex(torch.from_numpy(rng.normal(size=o.shape[0])), torch.from_numpy(rng.normal(size=o.shape[0]))).cuda()
-    torch.testing.assert_close(fo.o_v(v), o @ v, rtol=1e-12, atol=1e-12)
-    torch.testing.assert_close(fo.oh_u(u), o.conj().T @ u, rtol=1e-12, atol=1e-12)
+    torch.testing.assert_close(fo.o_v(v), o @ v, rtol=1e-12, atol=1e-11)
+    torch.testing.assert_close(fo.oh_u(u), o.conj().T @ u, rtol=1e-12, atol=1e-11)
+    torch.testing.assert_close(fo.oh_u(u), fo.oh_u(u), rtol=0, atol=0)  # deterministic
 
 
 @pytest.mark.parametrize("lam", [1e-3, 1e-1])
