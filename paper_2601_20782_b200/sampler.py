@@ -181,8 +181,12 @@ class ChainEnsemble:
         self.steps_done += int(n_steps)
         self.proposed += self.n_chains * int(n_steps)
 
-    def _check(self):
-        st = self._status.cpu().numpy()
+    def _check(self, st=None):
+        """Raise the first recorded evaluation failure.  The status words are
+        sticky (first non-finite (step, chain)), so a check after several
+        unchecked launches reports the same failure as immediate checking."""
+        if st is None:
+            st = self._status.cpu().numpy()
         if st[0] != 0:
             key = int(st[1])
             step, chain = key >> 32, key & 0xFFFFFFFF
@@ -209,15 +213,18 @@ class ChainEnsemble:
         return x
 
     # -- reference API ------------------------------------------------------
-    def set_evaluator(self, evaluator):
-        """Swap the target; refreshes every chain's cached log-probability (sampler.py:90-93)."""
+    def set_evaluator(self, evaluator, check: bool = True):
+        """Swap the target; refreshes every chain's cached log-probability
+        (sampler.py:90-93).  check=False defers the failure check to the next
+        checked call (no host synchronisation here)."""
         ev = _device_evaluator(evaluator)
         if ev.n_visible != self.n_sites:
             raise ValueError("evaluator and ensemble disagree on the number of sites")
         self._evaluator = ev
         self._bind_scratch()
         self._launch(0)
-        self._check()
+        if check:
+            self._check()
 
     def reset_counters(self):
         self._acc.zero_()
@@ -299,16 +306,20 @@ class ChainEnsemble:
         (sampler.py:142-167); returns this shard's uint8 rows."""
         import torch
 
-        packed = self.collect_packed(n_samples, thin_steps)
+        packed = self.collect_packed(n_samples, thin_steps, check=False)
         out = torch.empty((packed.shape[0], self.n_sites), dtype=torch.uint8, device=self.device)
         if packed.shape[0]:
             nat.call("mpv_unpack_bits", packed.data_ptr(), packed.shape[0], self.n_sites, out.data_ptr(),
                      self._stream())
         # fresh pinned block from torch's caching host allocator (no host memcpy):
-        # the returned array keeps it alive, and device_pack() re-uploads it by DMA
+        # the returned array keeps it alive, and device_pack() re-uploads it by DMA.
+        # The status words ride along: one synchronisation for samples + check.
         host = torch.empty(out.shape, dtype=torch.uint8, pin_memory=True)
+        st = torch.empty(2, dtype=torch.int64, pin_memory=True)
         host.copy_(out, non_blocking=True)
+        st.copy_(self._status, non_blocking=True)
         torch.cuda.current_stream(self.device).synchronize()
+        self._check(st.numpy())
         return host.numpy()
 
 

@@ -290,3 +290,28 @@ def test_nonfinite_log_prob_raises_with_context(cuda):
             ens = sampler.ChainEnsemble(8, 3, sampler.Proposal("flip"), ev, derive_key(0, "chains"))
             ens.run_steps(50)
         assert err.value.context["bits"][:2].tolist() == [1, 1]
+
+
+def test_deferred_failure_check_reports_the_same_failure(cuda):
+    """run_sweeps/set_evaluator(check=False) skip the host synchronisation; the
+    sticky status words make the next checked call (collect) raise the same
+    first failure (step, chain, configuration) as immediate checking."""
+    from paper_2601_20782_b200.errors import EvaluationFailureError
+
+    p = rbm.RbmParameters(np.array([6e307, 6e307, 0], complex), np.zeros(2, complex), np.zeros((2, 3), complex))
+    ev = rbm.log_prob_evaluator(p, F64)
+    ctx = []
+    for deferred in (False, True):
+        p0 = rbm.RbmParameters(np.zeros(3, complex), np.zeros(2, complex), np.zeros((2, 3), complex))
+        ens = sampler.ChainEnsemble(8, 3, sampler.Proposal("flip"), rbm.log_prob_evaluator(p0, F64),
+                                    derive_key(0, "chains"))
+        with pytest.raises(EvaluationFailureError) as err:
+            if deferred:
+                ens.set_evaluator(ev, check=False)
+                ens.run_steps(50, check=False)
+                ens.collect(16, 4)
+            else:
+                ens.set_evaluator(ev)
+                ens.run_steps(50)
+        ctx.append((err.value.context["step"], err.value.context["chain"], err.value.context["bits"].tolist()))
+    assert ctx[0] == ctx[1]
