@@ -313,7 +313,7 @@ def run_ours(args, rank, world, local_rank):
 
         cfg = vmc.TrainConfig(TfimSpec(_LS.chain(20), 1.0, 1.0), alpha=1, n_steps=10, n_samples=4096, n_chains=1024,
                               sampling_format=F16, rounding_mode=RoundingMode.NATIVE, track_timings=True)
-        recs = vmc.train(cfg).records[2:]
+        recs = vmc.train(cfg, local=True).records[2:]  # rank 0 alone (other ranks idle)
         vmc_iter = {"config": "tfim_chain20_open_h1_a1_s4096_c1024_f16native",
                     "sampling_ms": 1e3 * float(np.median([r["sampling_seconds"] for r in recs])),
                     "update_ms": 1e3 * float(np.median([r["update_seconds"] for r in recs])),
@@ -325,7 +325,7 @@ def run_ours(args, rank, world, local_rank):
         cfg2 = vmc.TrainConfig(TfimSpec(_LS.square(10), 1.0, 3.04), alpha=2, n_steps=4, n_samples=4 * C,
                                n_chains=C, sampling_format=F16, rounding_mode=RoundingMode.NATIVE,
                                track_timings=True, sr_solver="cg", cg_tol=1e-8, burn_in_sweeps=200)
-        recs2 = vmc.train(cfg2).records[1:]
+        recs2 = vmc.train(cfg2, local=True).records[1:]
         vmc_iter["config2"] = {
             "config": "rbm_a2_tfim10x10_h3.04_s65536_c16384_f16native_f64energy_sr_cg(tol 1e-8, lambda 1e-3)",
             "sampling_ms": 1e3 * float(np.median([r["sampling_seconds"] for r in recs2])),
@@ -479,8 +479,16 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # BENCH_TEST_ONE_GPU=1 (control-flow check only, never a measurement):
+        # every rank on cuda:0 over gloo, so the N>1 path can run on one GPU
+        if os.environ.get("BENCH_TEST_ONE_GPU") == "1":
+            os.environ["LOCAL_RANK"] = "0"
+            local_rank = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out))

@@ -370,7 +370,7 @@ class TrainResult:
     force_history: list = field(default_factory=list)
 
 
-def train(config: TrainConfig, device=None, group=None) -> TrainResult:
+def train(config: TrainConfig, device=None, group=None, local: bool = False) -> TrainResult:
     """Two-copy mixed-precision SR training (vmc.py:472-639) on the device.
 
     Under torch.distributed (world > 1) each rank samples its contiguous slice
@@ -392,7 +392,8 @@ def train(config: TrainConfig, device=None, group=None) -> TrainResult:
 
     nat.require_cuda()
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    world = tdist.get_world_size(group) if (tdist.is_available() and tdist.is_initialized()) else 1
+    # local=True: a single-process run even inside an initialised process group
+    world = tdist.get_world_size(group) if (not local and tdist.is_available() and tdist.is_initialized()) else 1
     rank = tdist.get_rank(group) if world > 1 else 0
     spec = config.hamiltonian
     n = spec.lattice.n_sites
