@@ -130,7 +130,7 @@ def run_ours(args, rank, world, local_rank):
 
     def device_step(record=None):
         """Inputs resident in HBM: snapshot already built; returns device scalars."""
-        ens.set_evaluator(ev)  # refresh launch (set_evaluator semantics)
+        ens.set_evaluator(ev, check=False)  # refresh launch (set_evaluator semantics); checked at the end
         ens.reset_counters()
         ens.run_sweeps(REBURN_SWEEPS, check=False)
         if record is not None:
@@ -139,7 +139,11 @@ def run_ours(args, rank, world, local_rank):
         if record is not None:
             record[1].record(stream)
         kern = vmc._energy_kernel(spec, psi)
+        if record is not None:
+            record[2].record(stream)
         eps, status = kern.packed(packed)
+        if record is not None:
+            record[3].record(stream)
         e_sum = eps[:, 0].sum()
         acc = ens.accepted_per_chain.sum()
         launches["n"] = 6  # refresh, re-burn sweep, collect sweep, energy, (2 torch reductions not ours)
@@ -155,6 +159,7 @@ def run_ours(args, rank, world, local_rank):
     time.sleep(0.3)
     total_ms = 0.0
     sweep_ms = 0.0
+    energy_ms = 0.0
     energies = []
     accs = []
     for _ in range(args.steps):
@@ -164,8 +169,9 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        e_sum, acc, rows = device_step((s0, s1))
+        e_sum, acc, rows = device_step((s0, s1, g0, g1))
         if dist is not None:
             red = torch.stack([e_sum, acc.to(torch.float64), torch.tensor(float(rows), device=dev, dtype=torch.float64)])
             dist.all_reduce(red)
@@ -174,16 +180,17 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
         sweep_ms += s0.elapsed_time(s1)
+        energy_ms += g0.elapsed_time(g1)
         energies.append(float(e_sum) / float(rows))
         accs.append(float(acc))
     clocks.stop()
     ms = total_ms / args.steps
     if dist is not None:
-        t = torch.tensor([ms, sweep_ms / args.steps], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms, sweep_ms / args.steps, energy_ms / args.steps], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, sweep_avg = float(t[0]), float(t[1])
+        ms, sweep_avg, energy_avg = float(t[0]), float(t[1]), float(t[2])
     else:
-        sweep_avg = sweep_ms / args.steps
+        sweep_avg, energy_avg = sweep_ms / args.steps, energy_ms / args.steps
 
     # ---- end-to-end through the public API (host buffers, copies inside) ----
     e2e_ms = 0.0
@@ -341,6 +348,8 @@ def run_ours(args, rank, world, local_rank):
     mufu_peak = 16 * 148 * sm_mhz * 1e6  # MUFU lane-ops/s at the measured SM clock
     collect_steps = C * SAMPLES_PER_CHAIN * (N_SITES + 1)
     achieved_mufu = 3 * params.n_hidden * collect_steps / (sweep_avg / 1e3)
+    fp64_peak = 64 * 148 * sm_mhz * 1e6
+    fp64_ops = n_samples_total / world * (N_SITES * params.n_hidden * 8 + N_SITES * 2 * params.n_hidden)
     out = {
         "metric": "MCMC chain-steps/sec (f16 sampling + f64 local energies), whole job",
         "value": value,
@@ -365,6 +374,14 @@ def run_ours(args, rank, world, local_rank):
                      "peak": mufu_peak / 1e12, "unit": "Tmufu-op/s", "frac": achieved_mufu / mufu_peak,
                      "traffic": None, "algorithmic": "3 MUFU ops (ex2, cos, lg2) per hidden unit per chain-step, M=200",
                      "peak_basis": "16 MUFU/clk/SM (measured, tools/microbench) x 148 SMs x measured median SM clock"},
+        # second-largest kernel of the step: the f64 local energies (FP64 pipe: DFMA and DMMA)
+        "roofline_energy": {"bound": "fp64", "kernel": "energy_kernel", "ms": energy_avg,
+                            "achieved": fp64_ops / (energy_avg / 1e3) / 1e12, "peak": fp64_peak / 1e12,
+                            "unit": "TFP64-op/s", "frac": fp64_ops / (energy_avg / 1e3) / fp64_peak,
+                            "algorithmic": "per sample: terms x M x 8 FP64 ops (ratio products) + N x 2M "
+                                           "multiply-adds (theta GEMM on DMMA); 65,536 samples, 100 terms, M=200",
+                            "peak_basis": "64 FP64 FMA/clk/SM (measured, tools/microbench/fp64lat.cu, dmma.cu) x 148 "
+                                          "SMs x measured median SM clock"},
         "clocks": clk,
         "gpu_launches": launches["n"],
         "e2e": {"value": steps_per_step / (e2e_ms / 1e3), "unit": "chain-steps/s", "ms_per_step": e2e_ms,
@@ -380,6 +397,7 @@ def run_ours(args, rank, world, local_rank):
         with open(tr) as f:
             out["roofline"]["traffic"] = json.load(f)["sweep_kernel"]["dram_bytes_per_launch"]
             out["roofline"]["traffic_unit"] = "bytes/launch (ncu --set full, profiles/r01)"
+            out["roofline_energy"]["traffic"] = json.load(open(tr))["energy_kernel"]["dram_bytes_per_launch"]
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, sample_chains=C)
     return out
