@@ -154,7 +154,7 @@ constexpr int kMaxBufs = 8; // ring depth limit per Pipe
 struct EnergyPlan {
   int SB, rows, nbt, nbw;          // samples/block, tau rows/chunk, tau buffers, W buffers
   int tbuf_bytes, wbuf_bytes, pool_bytes;
-  int skip;  // profiling only (MPV_ENERGY_SKIP): bit 0 phase 1, bit 1 tanh, bit 2 phase 2
+  int skip;  // profiling only (MPV_ENERGY_SKIP): bit 0 phase 1, bit 1 tanh, bit 2 phase 2, bit 3 ratios, bit 4 sums
 };
 __host__ __device__ inline int energy_mask_pad(int N) { return (N + 15) / 16 * 16 + 16; }
 __host__ __device__ inline int energy_w_pitch(int M) { return 2 * M + 8; }  // doubles per staged W row
@@ -258,30 +258,36 @@ __device__ __forceinline__ double2 ctanh_fast(double2 z) {
 // Ratio of term t for one sample through the log-cosh difference (ref
 // formulation, rbm.py:130-140), theta recomputed from W: the path for terms
 // whose tau table would cancel or blow up (slow[t]).
-__device__ __noinline__ double2 slow_ratio(const EnergyArgs& a, const uint32_t* xbits, int t, double d) {
-  const int M = a.M, N = a.N;
+__device__ __noinline__ double2 slow_ratio(int N, int M, int ham, const double2* __restrict__ av,
+                                           const double2* __restrict__ bv, const double2* __restrict__ w_t,
+                                           const int32_t* __restrict__ bonds, const uint32_t* xbits, int t, double d) {
   double2 lsum = make_double2(0.0, 0.0);
+  int p = t, q = 0;
+  if (ham != MPV_HAM_TFIM) {
+    p = bonds[2 * t];
+    q = bonds[2 * t + 1];
+  }
   for (int i = 0; i < M; ++i) {
-    double2 z = a.b[i];
+    double2 z = bv[i];
     for (int k = 0; k < N; ++k)
       if ((xbits[k >> 5] >> (k & 31)) & 1u) {
-        const double2 e = a.w_t[(size_t)k * M + i];
+        const double2 e = w_t[(size_t)k * M + i];
         z.x += e.x;
         z.y += e.y;
       }
-    const double2 w = term_w(a, t, i);
+    double2 w = w_t[(size_t)p * M + i];
+    if (ham != MPV_HAM_TFIM) {
+      const double2 w2 = w_t[(size_t)q * M + i];
+      w = make_double2(w.x - w2.x, w.y - w2.y);
+    }
     const double2 l1 = clogcosh(make_double2(z.x + d * w.x, z.y + d * w.y));
     const double2 l0 = clogcosh(z);
     lsum.x += l1.x - l0.x;
     lsum.y += l1.y - l0.y;
   }
   double2 at;
-  if (a.ham == MPV_HAM_TFIM) {
-    at = a.a[t];
-  } else {
-    const int p = a.bonds[2 * t], q = a.bonds[2 * t + 1];
-    at = make_double2(a.a[p].x - a.a[q].x, a.a[p].y - a.a[q].y);
-  }
+  if (ham == MPV_HAM_TFIM) at = av[t];
+  else at = make_double2(av[p].x - av[q].x, av[p].y - av[q].y);
   return cexp_(make_double2(lsum.x + d * at.x, lsum.y + d * at.y));
 }
 
@@ -418,7 +424,8 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
   double2 P[ST];
   int E[ST];
   uint32_t sg[ST];  // sign bit of d on the high word (d = -1 -> flip tanh(theta))
-  uint32_t nz = 0;  // bit j: d_j != 0
+  uint32_t nz = 0;       // bit j: d_j != 0
+  uint32_t sg_bits = 0;  // bit j: d_j < 0
 #pragma unroll
   for (int j = 0; j < ST; ++j) {
     P[j] = make_double2(1.0, 0.0);
@@ -436,6 +443,7 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
       const int s = g * ST + j;
       const int d = (a.ham == MPV_HAM_TFIM) ? 1 - 2 * bit_of(s, p) : bit_of(s, q) - bit_of(s, p);
       sg[j] = d < 0 ? 0x80000000u : 0u;
+      sg_bits |= (d < 0 ? 1u : 0u) << j;
       nz |= (d != 0 ? 1u : 0u) << j;
     }
     slow = a.slow[t] != 0;
@@ -489,26 +497,44 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
   // writes coef_t * ratio_t plus the diagonal of bonds b = t, t + T, ...
   // (ref vmc.py:52-57: J_b s_p s_q), so one fixed-order sum over t gives eps.
   double2* R = tt;
-  if (g < NG) {
-    int bp[2] = {0, 0}, bq[2] = {0, 0};
-    double bj[2] = {0.0, 0.0};
-    int nb = 0;
-    for (int b = t; b < a.n_bonds && nb < 2; b += T, ++nb) {
-      bp[nb] = a.bonds[2 * b];
-      bq[nb] = a.bonds[2 * b + 1];
-      bj[nb] = a.bond_j ? a.bond_j[b] : a.J;
-    }
+  if (g < NG && !(pl.skip & 8)) {
+    // the first two bonds of this term in registers (TFIM: 2N bonds over N terms)
+    const int b0 = t, b1 = t + T;
+    const bool h0 = b0 < a.n_bonds, h1 = b1 < a.n_bonds;
+    const int p0 = h0 ? a.bonds[2 * b0] : 0, q0 = h0 ? a.bonds[2 * b0 + 1] : 0;
+    const int p1 = h1 ? a.bonds[2 * b1] : 0, q1 = h1 ? a.bonds[2 * b1 + 1] : 0;
+    const double j0 = h0 ? (a.bond_j ? a.bond_j[b0] : a.J) : 0.0;
+    const double j1 = h1 ? (a.bond_j ? a.bond_j[b1] : a.J) : 0.0;
     const double ct = a.term_coef ? a.term_coef[t] : (a.ham == MPV_HAM_TFIM ? a.h : 2.0 * a.J);
+    const double2 eap = a.ea[2 * t], eam = a.ea[2 * t + 1];
+    const int ect = a.ec[t];
+    // diagonal of bonds t, t + T (and further bonds, not in practice)
+    auto diag = [&](int s) {
+      double dg = 0.0;
+      if (h0) dg += (bit_of(s, p0) ^ bit_of(s, q0)) ? -j0 : j0;
+      if (h1) dg += (bit_of(s, p1) ^ bit_of(s, q1)) ? -j1 : j1;
+      for (int b = t + 2 * T; b < a.n_bonds; b += T)
+        dg += (bit_of(s, a.bonds[2 * b]) ^ bit_of(s, a.bonds[2 * b + 1])) ? -(a.bond_j ? a.bond_j[b] : a.J)
+                                                                          : (a.bond_j ? a.bond_j[b] : a.J);
+      return dg;
+    };
+    if (active && slow) {
+#pragma unroll 1
+      for (int j = 0; j < ST; ++j) {  // rolled: one call site, results straight to R
+        const int s = g * ST + j;
+        double2 v = make_double2(0.0, 0.0);
+        if (s0 + s < a.B && ((nz >> j) & 1u)) v = slow_ratio(a.N, a.M, a.ham, a.a, a.b, a.w_t, a.bonds, wsm + s * 32, t,
+                                                                ((sg_bits >> j) & 1u) ? -1.0 : 1.0);
+        R[s * T + t] = make_double2(fma(ct, v.x, diag(s)), ct * v.y);
+      }
+    } else {
 #pragma unroll
-    for (int j = 0; j < ST; ++j) {
-      const int s = g * ST + j;
-      double2 v = make_double2(0.0, 0.0);
-      if (active && s0 + s < a.B && ((nz >> j) & 1u)) {
-        if (slow) {
-          v = slow_ratio(a, wsm + s * 32, t, sg[j] ? -1.0 : 1.0);
-        } else {
-          v = cmul(a.ea[2 * t + (sg[j] ? 1 : 0)], P[j]);
-          const int k = E[j] + a.ec[t];
+      for (int j = 0; j < ST; ++j) {
+        const int s = g * ST + j;
+        double2 v = make_double2(0.0, 0.0);
+        if (active && ((nz >> j) & 1u)) {
+          v = cmul(sg[j] ? eam : eap, P[j]);
+          const int k = E[j] + ect;
           if (k >= -1022 && k <= 1023) {  // exact power-of-two scale (correctly rounded, like ldexp)
             const double f = __longlong_as_double((long long)(k + 1023) << 52);
             v.x *= f;
@@ -519,19 +545,14 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
             v.y = ldexp(ldexp(v.y, k1), k - k1);
           }
         }
+        R[s * T + t] = make_double2(fma(ct, v.x, diag(s)), ct * v.y);
       }
-      double dg = 0.0;
-      for (int q = 0; q < nb; ++q) dg += (bit_of(s, bp[q]) ^ bit_of(s, bq[q])) ? -bj[q] : bj[q];
-      for (int b = t + 2 * T; b < a.n_bonds; b += T)  // (more than two bonds per term: not in practice)
-        dg += (bit_of(s, a.bonds[2 * b]) ^ bit_of(s, a.bonds[2 * b + 1])) ? -(a.bond_j ? a.bond_j[b] : a.J)
-                                                                          : (a.bond_j ? a.bond_j[b] : a.J);
-      R[s * T + t] = make_double2(fma(ct, v.x, dg), ct * v.y);
     }
   }
   __syncthreads();
   // fixed-order sums: warp w takes samples w, w + nwarps, ...; lane l sums
   // terms l, l + 32, ... then a butterfly
-  for (int s = warp; s < SB; s += nwarps) {
+  for (int s = warp; s < ((pl.skip & 16) ? 0 : SB); s += nwarps) {
     if (s0 + s >= a.B) continue;
     double er = 0.0, ei = 0.0;
     for (int u = lane; u < T; u += 32) {
