@@ -234,6 +234,52 @@ class ChainEnsemble:
     def evaluator(self):
         return self._evaluator
 
+    # -- checkpoint / resume (beyond the reference, which has none: SURVEY §5) --
+    def state_dict(self) -> dict:
+        """Everything that determines the continuation: packed configurations,
+        cached log p, per-chain acceptance counters, the draw counter
+        (steps_done) and the stream key / proposal / shard.  The theta
+        accumulators are a function of the bits (refreshed at every launch),
+        so they are not stored."""
+        self._check()
+        return {"format": "mpv-chains-v1", "n_sites": self.n_sites, "n_chains": self.n_chains,
+                "chain_offset": self.chain_offset, "n_chains_total": self.n_chains_total, "key": self.key,
+                "proposal": self.proposal.kind, "sector_weight": self.proposal.sector_weight,
+                "init_draws": self.init_draws, "steps_done": self.steps_done, "proposed": self.proposed,
+                "bits": self._bits.cpu().numpy().copy(), "log_probs": self._logp.cpu().numpy().copy(),
+                "accepted": self._acc.cpu().numpy().copy()}
+
+    def load_state_dict(self, state: dict):
+        """Resume from state_dict(): the continuation is bit-identical to an
+        uninterrupted run (draws depend only on (key, chain, draw counter))."""
+        import torch
+
+        if state.get("format") != "mpv-chains-v1":
+            raise ValueError("not an mpv-chains-v1 state")
+        for k in ("n_sites", "n_chains", "chain_offset", "n_chains_total", "key", "init_draws"):
+            if int(state[k]) != int(getattr(self, k)):
+                raise ValueError(f"state mismatch in {k}: {state[k]} vs {getattr(self, k)}")
+        if state["proposal"] != self.proposal.kind:
+            raise ValueError("state was recorded with a different proposal")
+        self._bits.copy_(torch.from_numpy(np.asarray(state["bits"], dtype=np.int32)))
+        self._logp.copy_(torch.from_numpy(np.asarray(state["log_probs"], dtype=np.float64)))
+        self._acc.copy_(torch.from_numpy(np.asarray(state["accepted"], dtype=np.int64)))
+        self.steps_done = int(state["steps_done"])
+        self.proposed = int(state["proposed"])
+
+    def save_state(self, path):
+        st = self.state_dict()
+        np.savez(path, **{k: np.asarray(v) if not isinstance(v, str) else np.array(v) for k, v in st.items()
+                          if v is not None}, has_weight=np.array(st["sector_weight"] is not None))
+        return path
+
+    def load_state(self, path):
+        with np.load(path, allow_pickle=False) as z:
+            st = {k: z[k] for k in z.files}
+        st = {k: (str(v) if v.dtype.kind == "U" else (v if v.ndim else v.item())) for k, v in st.items()}
+        st.setdefault("sector_weight", None)
+        self.load_state_dict(st)
+
     @property
     def bits(self) -> np.ndarray:
         return unpack_bits(self._bits.cpu().numpy().view(np.uint32), self.n_sites)

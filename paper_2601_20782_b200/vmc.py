@@ -417,6 +417,8 @@ def train(config: TrainConfig, device=None, group=None, local: bool = False) -> 
     for step in range(config.n_steps):
         torch.cuda.synchronize(dev)
         t_sample = time.perf_counter()
+        nvtx = torch.cuda.nvtx  # phase ranges for nsys/ncu timelines (no-ops without a profiler)
+        nvtx.range_push(f"vmc step {step}: sampling")
         if exact_mode:
             lp = rbm.LogProbEvaluator(params, F64, RoundingMode.PER_OPERATION, dev).log_prob_packed(all_packed)[0]
             weights = torch.softmax(lp, dim=0)
@@ -446,6 +448,8 @@ def train(config: TrainConfig, device=None, group=None, local: bool = False) -> 
             est_w = cnt.to(torch.float64) / config.n_samples
         torch.cuda.synchronize(dev)
         t_update = time.perf_counter()
+        nvtx.range_pop()
+        nvtx.range_push(f"vmc step {step}: energies + SR update")
         psi = rbm.log_psi_evaluator(params, dev)
         eps_ri, status = _energy_kernel(spec, psi).packed(uniq)
         if int(status[0]) != 0:
@@ -469,6 +473,7 @@ def train(config: TrainConfig, device=None, group=None, local: bool = False) -> 
                 energy = float((est_w.to(eps.dtype) @ eps).real)
             update = sr_step(f, s, config.lambda_shift, config.eta, config.compute_kappa)
         theta = params.flatten() - config.eta * update.g.cpu().numpy()
+        nvtx.range_pop()
         new_params = rbm.RbmParameters.from_flat(theta, params.n_visible, params.n_hidden)
         if exact_mode:
             err = 0.0

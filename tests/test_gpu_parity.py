@@ -315,3 +315,26 @@ def test_deferred_failure_check_reports_the_same_failure(cuda):
                 ens.run_steps(50)
         ctx.append((err.value.context["step"], err.value.context["chain"], err.value.context["bits"].tolist()))
     assert ctx[0] == ctx[1]
+
+
+@pytest.mark.parametrize("kind,weight", [("flip", None), ("exchange", 5)])
+def test_checkpoint_resume_is_bit_identical(cuda, tmp_path, kind, weight):
+    """state_dict / save_state -> a fresh ensemble continues exactly like the
+    uninterrupted run (bits, log p, counters, collected samples)."""
+    p = rbm.random_parameters(10, 2, derive_key(1, "ckpt"), 0.3)
+    ev = rbm.log_prob_evaluator(p, F16, NATIVE)
+    key = derive_key(2, "chains")
+    ref = sampler.ChainEnsemble(64, 10, sampler.Proposal(kind, weight), ev, key)
+    ref.run_steps(137)
+    path = ref.save_state(tmp_path / "chains.npz")
+    ref.run_steps(91)
+    s_ref = ref.collect(256, 11)
+    res = sampler.ChainEnsemble(64, 10, sampler.Proposal(kind, weight), ev, key)
+    res.run_steps(3)  # diverged state, overwritten by the checkpoint
+    res.load_state(path)
+    res.run_steps(91)
+    s_res = res.collect(256, 11)
+    np.testing.assert_array_equal(s_res, s_ref)
+    np.testing.assert_array_equal(res.bits, ref.bits)
+    np.testing.assert_array_equal(res.log_probs, ref.log_probs)
+    assert res.accepted == ref.accepted and res.proposed == ref.proposed
