@@ -711,8 +711,8 @@ int mpv_local_energies_ex(int N, int M, const double* a, const double* b, const 
 static size_t ld_ov_bytes(int N, int M) { return ((size_t)ld_rows(N) * ld_pitch(M) * sizeof(double) + 255) / 256 * 256; }
 
 size_t mpv_logderiv_scratch_bytes(int64_t U, int N, int M) {
-  const int64_t chunks = (U + kLdChunk - 1) / kLdChunk;
-  return ld_ov_bytes(N, M) + (size_t)chunks * ld_rows_a(M) * ld_col_groups(N) * 8 * kLdNT * sizeof(double);
+  const int64_t chunk = ld_chunk(std::max<int64_t>(U, 1), N, M), chunks = (U + chunk - 1) / chunk;
+  return ld_ov_bytes(N, M) + (size_t)std::max<int64_t>(chunks, 1) * ld_rows_a(M) * ld_cols(N) * sizeof(double);
 }
 
 int mpv_logderiv_ov(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* v, double* q,
@@ -747,9 +747,17 @@ int mpv_logderiv_ohu(const double* t, const uint32_t* bits, int64_t U, int N, in
     return MPV_OK;
   }
   double* partial = (double*)((char*)scratch + ld_ov_bytes(N, M));
-  const int chunks = (int)((U + kLdChunk - 1) / kLdChunk);
-  const dim3 grid((unsigned)(ld_rows_a(M) / 64), (unsigned)chunks, (unsigned)ld_col_groups(N));
-  ld_ohu_kernel<<<grid, 256, 0, st>>>((const double2*)t, bits, U, N, M, (N + 31) / 32, (const double2*)u, partial);
+  const int64_t chunk = ld_chunk(U, N, M);
+  const int chunks = (int)((U + chunk - 1) / chunk);
+  const int ntc = ld_ntc(N);
+  const dim3 grid((unsigned)(ld_rows_a(M) / 64), (unsigned)chunks, (unsigned)(ld_cols(N) / (8 * ntc)));
+  const int words = (N + 31) / 32;
+  const double2* T = (const double2*)t;
+  const double2* Uv = (const double2*)u;
+  if (ntc == 16) ld_ohu_kernel<16><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk);
+  else if (ntc == 13) ld_ohu_kernel<13><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk);
+  else if (ntc == 8) ld_ohu_kernel<8><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk);
+  else ld_ohu_kernel<4><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk);
   ld_ohu_reduce_kernel<<<(unsigned)std::min(148 * 8, (P + 255) / 256), 256, 0, st>>>(partial, chunks, N, M,
                                                                                       (double2*)out);
   return check_launch("logderiv_ohu");

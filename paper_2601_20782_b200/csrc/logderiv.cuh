@@ -15,12 +15,13 @@
 //        B' = [X | 1]; split over sample chunks (K), partial sums reduced in a
 //        fixed chunk order (deterministic).
 #pragma once
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace mpv {
 
 constexpr int kLdSB = 16;       // samples per ov block
-constexpr int kLdChunk = 1024;  // samples per ohu K-chunk
 
 __device__ __forceinline__ void ld_dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -131,86 +132,115 @@ __global__ void __launch_bounds__(256) ld_ov_kernel(const double2* __restrict__ 
 }
 
 // ohu partials: block (row group x, chunk y, column group z); warp = one
-// m-tile (8 rows of A'), kLdNT n-tiles (64 columns of B' = [X | 1]).
-constexpr int kLdNT = 8;
-__host__ __device__ inline int ld_col_groups(int N) { return (N + 1 + 8 * kLdNT - 1) / (8 * kLdNT); }
+// m-tile (8 rows of A'), NTC n-tiles (8*NTC columns of B' = [X | 1]).  The
+// A' values of the next 64-sample tile are loaded into registers while the
+// current tile's DMMAs run (double-buffered shared memory).
+constexpr int kLdTile = 32;  // samples staged per sub-tile
 __host__ __device__ inline int ld_rows_a(int M) { return (2 * M + 2 + 63) / 64 * 64; }  // A' rows, whole blocks
+// n-tiles per column group: the smallest padding of N + 1 columns
+__host__ __device__ inline int ld_ntc(int N) {
+  const int c = N + 1;
+  int best = 16, waste = 1 << 30;
+  const int opts[4] = {16, 13, 8, 4};
+  for (int k = 0; k < 4; ++k) {
+    const int w = (c + 8 * opts[k] - 1) / (8 * opts[k]) * 8 * opts[k] - c;
+    if (w < waste) { waste = w; best = opts[k]; }
+  }
+  return best;
+}
+__host__ __device__ inline int ld_cols(int N) { const int g = 8 * ld_ntc(N); return (N + 1 + g - 1) / g * g; }
+// samples per K-chunk: about two blocks per SM over the (row, chunk, column) grid
+inline int64_t ld_chunk(int64_t U, int N, int M) {
+  const int64_t other = (int64_t)(ld_rows_a(M) / 64) * (ld_cols(N) / (8 * ld_ntc(N)));
+  const int64_t target = std::max<int64_t>(1, 2 * 148 / std::max<int64_t>(1, other));
+  const int64_t c = (U + target - 1) / target;
+  return std::max<int64_t>(kLdTile, (c + kLdTile - 1) / kLdTile * kLdTile);
+}
 
-constexpr int kLdTile = 64;  // samples staged per ohu sub-tile
-
+template <int NTC>
 __global__ void __launch_bounds__(256) ld_ohu_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
                                                      int64_t U, int N, int M, int words, const double2* __restrict__ u,
-                                                     double* __restrict__ partial) {
-  // A' tile [64 rows][kLdTile samples] (+1 pad against bank conflicts) and the samples' bits
-  __shared__ double as[64][kLdTile + 1];
-  __shared__ uint32_t bs[kLdTile][9];
+                                                     double* __restrict__ partial, int64_t chunk) {
+  __shared__ double as[2][64][kLdTile + 1];  // A' tiles [row][sample] (+1 pad: conflict-free column reads)
+  __shared__ uint32_t bs[2][kLdTile][9];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rows_a = 2 * M + 2;
-  const int r0 = blockIdx.x * 64;                // first A' row of this block (32 units)
-  const int64_t k_begin = (int64_t)blockIdx.y * kLdChunk;
-  const int64_t k_end = min(U, k_begin + kLdChunk);
-  const int c0 = blockIdx.z * 8 * kLdNT;         // first B' column of this block
+  const int u0 = blockIdx.x * 32;  // first unit of this block (64 A' rows)
+  const int64_t k_begin = (int64_t)blockIdx.y * chunk;
+  const int64_t k_end = min(U, k_begin + chunk);
+  const int c0 = blockIdx.z * 8 * NTC;  // first B' column of this block
   const int qr = lane & 3, qc = lane >> 2;
-  double acc[kLdNT][2];
+  constexpr int kPer = kLdTile * 32 / 256;  // (sample, unit) pairs staged per thread
+  double2 pt[kPer], pu[kPer];
+  uint32_t pb = 0;
+  auto load = [&](int64_t sb) {  // global -> registers for the tile at sb
 #pragma unroll
-  for (int j = 0; j < kLdNT; ++j) acc[j][0] = acc[j][1] = 0.0;
-  for (int64_t sb = k_begin; sb < k_end; sb += kLdTile) {
-    __syncthreads();
-    // stage: thread -> (sample, unit pair); unit loads are contiguous per sample
-    for (int idx = tid; idx < kLdTile * 32; idx += blockDim.x) {
-      const int ls = idx >> 5, lu = idx & 31;  // local sample, local unit
+    for (int r = 0; r < kPer; ++r) {
+      const int idx = tid + r * 256, ls = idx >> 5, lu = idx & 31;
       const int64_t s = sb + ls;
-      const int ui = (r0 >> 1) + lu;
-      double re = 0.0, im = 0.0;
+      const int ui = u0 + lu;
+      pt[r] = make_double2(0.0, 0.0);
+      pu[r] = make_double2(0.0, 0.0);
       if (s < k_end) {
-        const double2 us = u[s];
-        if (ui < M) {
-          const double2 ts = t[s * M + ui];  // conj(t) u
-          re = fma(ts.x, us.x, ts.y * us.y);
-          im = fma(ts.x, us.y, -ts.y * us.x);
-        } else if (2 * ui < rows_a) {  // rows 2M, 2M+1: u itself (a-part)
-          re = us.x;
-          im = us.y;
-        }
+        pu[r] = u[s];
+        pt[r] = ui < M ? t[s * M + ui] : make_double2(2 * ui < rows_a ? 1.0 : 0.0, 0.0);  // rows 2M, 2M+1: u itself
       }
-      as[2 * lu][ls] = re;
-      as[2 * lu + 1][ls] = im;
     }
-    for (int idx = tid; idx < kLdTile * words; idx += blockDim.x) {
-      const int ls = idx / words, w = idx % words;
-      bs[ls][w] = (sb + ls < k_end) ? bits[(sb + ls) * words + w] : 0u;
+    if (tid < kLdTile * words) {
+      const int ls = tid / words, w = tid % words;
+      pb = (sb + ls < k_end) ? bits[(sb + ls) * words + w] : 0u;
     }
-    __syncthreads();
+  };
+  auto store = [&](int buf) {  // registers -> shared: A' = (Re, Im) conj(t) u
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int idx = tid + r * 256, ls = idx >> 5, lu = idx & 31;
+      as[buf][2 * lu][ls] = fma(pt[r].x, pu[r].x, pt[r].y * pu[r].y);
+      as[buf][2 * lu + 1][ls] = fma(pt[r].x, pu[r].y, -pt[r].y * pu[r].x);
+    }
+    if (tid < kLdTile * words) bs[buf][tid / words][tid % words] = pb;
+  };
+  double acc[NTC][2];
+#pragma unroll
+  for (int j = 0; j < NTC; ++j) acc[j][0] = acc[j][1] = 0.0;
+  int cur = 0;
+  load(k_begin);
+  store(0);
+  __syncthreads();
+  for (int64_t sb = k_begin; sb < k_end; sb += kLdTile) {
+    const bool more = sb + kLdTile < k_end;
+    if (more) load(sb + kLdTile);  // in flight during the DMMAs below
 #pragma unroll 4
     for (int k0 = 0; k0 < kLdTile; k0 += 4) {
-      const double av = as[warp * 8 + qc][k0 + qr];
-      const uint32_t* bw = bs[k0 + qr];
+      const double av = as[cur][warp * 8 + qc][k0 + qr];
+      const uint32_t* bw = bs[cur][k0 + qr];
       const bool valid = sb + k0 + qr < k_end;
 #pragma unroll
-      for (int j = 0; j < kLdNT; ++j) {
+      for (int j = 0; j < NTC; ++j) {
         const int n = c0 + j * 8 + qc;  // B' column of this lane
         const uint32_t bit = n < N ? ((bw[n >> 5] >> (n & 31)) & 1u) : (n == N && valid ? 1u : 0u);
         ld_dmma(acc[j][0], acc[j][1], av, __hiloint2double((int)(bit * 0x3ff00000u), 0));
       }
     }
+    if (more) store(cur ^ 1);
+    __syncthreads();
+    cur ^= 1;
   }
-  // D fragment: row r0 + warp*8 + qc, columns c0 + j*8 + 2*qr (+1) -> partial[chunk][row][col]
-  const int cols = ld_col_groups(N) * 8 * kLdNT;
+  // D fragment: row 2*u0 + warp*8 + qc, columns c0 + j*8 + 2*qr (+1) -> partial[chunk][row][col]
+  const int cols = ld_cols(N);
   double* out = partial + (size_t)blockIdx.y * ld_rows_a(M) * cols;
-  const int row = r0 + warp * 8 + qc;
-  if (row < ld_rows_a(M)) {
+  const int row = 2 * u0 + warp * 8 + qc;
 #pragma unroll
-    for (int j = 0; j < kLdNT; ++j) {
-      out[(size_t)row * cols + c0 + j * 8 + 2 * qr] = acc[j][0];
-      out[(size_t)row * cols + c0 + j * 8 + 2 * qr + 1] = acc[j][1];
-    }
+  for (int j = 0; j < NTC; ++j) {
+    out[(size_t)row * cols + c0 + j * 8 + 2 * qr] = acc[j][0];
+    out[(size_t)row * cols + c0 + j * 8 + 2 * qr + 1] = acc[j][1];
   }
 }
 
 // fixed-order reduction of the chunk partials -> out (complex P-vector)
 __global__ void ld_ohu_reduce_kernel(const double* __restrict__ partial, int chunks, int N, int M,
                                      double2* __restrict__ out) {
-  const int rows_pad = ld_rows_a(M), cols = ld_col_groups(N) * 8 * kLdNT;
+  const int rows_pad = ld_rows_a(M), cols = ld_cols(N);
   const int P = N + M + M * N;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < P; idx += gridDim.x * blockDim.x) {
     int r, c;  // (row pair, column) of the entry
