@@ -146,7 +146,7 @@ def run_ours(args, rank, world, local_rank):
             record[3].record(stream)
         e_sum = eps[:, 0].sum()
         acc = ens.accepted_per_chain.sum()
-        launches["n"] = 6  # refresh, re-burn sweep, collect sweep, energy, (2 torch reductions not ours)
+        launches["n"] = 4  # ours: refresh sweep, re-burn sweep, collect sweep, local energies (+ 2 torch reductions)
         return e_sum, acc, packed.shape[0]
 
     # warmup
