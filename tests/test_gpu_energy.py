@@ -100,3 +100,20 @@ def test_large_lattice_against_oracle(cuda):
     eps = vmc.local_energies(spec, rbm.log_psi_evaluator(p), bits)
     want = port.local_energies(port.Params(p.a, p.b, p.w), "tfim", spec.lattice.bond_array(), 1.0, 3.04, bits)
     assert np.max(np.abs(eps - want) / np.maximum(1, np.abs(want))) < 1e-11
+
+
+@pytest.mark.parametrize("n,alpha,B", [(3, "1/3", 5), (5, "3/5", 17), (7, 3, 33), (12, "5/4", 49), (33, 1, 20),
+                                       (65, "6/5", 21), (40, 6, 9)])
+def test_odd_shapes_against_oracle(cuda, n, alpha, B):
+    """M not a multiple of 4 (DMMA tile edges), N across word boundaries, sample
+    counts not a multiple of the 16-sample block, many hidden units (M = 240)."""
+    from fractions import Fraction
+
+    p = rbm.random_parameters(n, Fraction(alpha), derive_key(n, "odd"), 0.4)
+    bits = np.random.default_rng(n).integers(0, 2, size=(B, n), dtype=np.uint8)
+    for spec, ham in ((TfimSpec(LatticeSpec.chain(n, n >= 3), 0.7, 1.3), "tfim"),
+                      (HeisenbergSpec(LatticeSpec.chain(n, n >= 3), 1.1), "heisenberg")):
+        eps = vmc.local_energies(spec, rbm.log_psi_evaluator(p), bits)
+        want = port.local_energies(port.Params(p.a, p.b, p.w), ham, spec.lattice.bond_array(), spec.j,
+                                   getattr(spec, "h", 0.0), bits)
+        assert np.max(np.abs(eps - want) / np.maximum(1, np.abs(want))) < 1e-10, (n, alpha, ham)
