@@ -681,19 +681,17 @@ int mpv_local_energies_ex(int N, int M, const double* a, const double* b, const 
       {8, 8, 4, 512, (const void*)&energy_kernel<8, 4, 512, 1>},
       {8, 8, 8, 512, (const void*)&energy_kernel<8, 8, 512, 1>},
   };
-  static const int cfg0 = getenv("MPV_ENERGY_CFG") ? atoi(getenv("MPV_ENERGY_CFG")) : 0;  // profiling override
   const size_t optin = (size_t)max_smem_optin();
   const int NT = (M + 3) / 4;
-  for (int ci = cfg0; ci < (int)(sizeof(cfgs) / sizeof(cfgs[0])); ++ci) {
+  for (int ci = 0; ci < (int)(sizeof(cfgs) / sizeof(cfgs[0])); ++ci) {
     const Cfg& cf = cfgs[ci];
     const int threads = std::max(std::max(32, ((cf.sb / cf.st) * T + 31) / 32 * 32), 32 * ((NT + cf.kt - 1) / cf.kt));
     if (threads > cf.tmax) continue;
-    static const int nbt0 = getenv("MPV_ENERGY_NBT") ? atoi(getenv("MPV_ENERGY_NBT")) : 3;
-    static const int rows0 = getenv("MPV_ENERGY_ROWS") ? atoi(getenv("MPV_ENERGY_ROWS")) : 12;
-    for (int nbt = nbt0; nbt >= 2; --nbt)
-      for (int rows = rows0; rows >= 2; rows -= 2) {
+    for (int nbt = 3; nbt >= 2; --nbt)
+      for (int rows = 12; rows >= 2; rows -= 2) {
         EnergyPlan pl;
         const size_t smem = energy_plan(N, M, T, cf.sb, rows, nbt, &pl);
+        // profiling only: MPV_ENERGY_SKIP bit mask drops kernel phases (profiles/r01/README.md)
         static const int skip = getenv("MPV_ENERGY_SKIP") ? atoi(getenv("MPV_ENERGY_SKIP")) : 0;
         pl.skip = skip;
         if (smem > optin) continue;
