@@ -130,7 +130,7 @@ def run_ours(args, rank, world, local_rank):
 
     def device_step(record=None):
         """Inputs resident in HBM: snapshot already built; returns device scalars."""
-        ens.set_evaluator(ev, check=False)  # refresh launch (set_evaluator semantics); checked at the end
+        ens.set_evaluator(ev, check=False)  # the refresh rides on the re-burn launch; checked at the end
         ens.reset_counters()
         ens.run_sweeps(REBURN_SWEEPS, check=False)
         if record is not None:
@@ -146,7 +146,7 @@ def run_ours(args, rank, world, local_rank):
             record[3].record(stream)
         e_sum = eps[:, 0].sum()
         acc = ens.accepted_per_chain.sum()
-        launches["n"] = 4  # ours: refresh sweep, re-burn sweep, collect sweep, local energies (+ 2 torch reductions)
+        launches["n"] = 3  # ours: re-burn sweep (refreshes first), collect sweep, local energies (+ 2 torch reductions)
         return e_sum, acc, packed.shape[0]
 
     # warmup

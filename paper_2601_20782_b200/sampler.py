@@ -169,6 +169,7 @@ class ChainEnsemble:
         return nat.stream_handle(self.device)
 
     def _launch(self, n_steps, thin=0, samples=None, n_samples_total=0, round_offset=0, row0=0):
+        self._refresh_pending = False  # every launch refreshes the cached log p from the bits first
         sp = samples.data_ptr() if samples is not None else None
         if isinstance(self._evaluator, TableLogProb):
             nat.call("mpv_table_sweep", self._evaluator.table.data_ptr(), ctypes.byref(self._chains), self.key,
@@ -186,6 +187,7 @@ class ChainEnsemble:
         sticky (first non-finite (step, chain)), so a check after several
         unchecked launches reports the same failure as immediate checking."""
         if st is None:
+            self._flush_refresh()
             st = self._status.cpu().numpy()
         if st[0] != 0:
             key = int(st[1])
@@ -215,16 +217,26 @@ class ChainEnsemble:
     # -- reference API ------------------------------------------------------
     def set_evaluator(self, evaluator, check: bool = True):
         """Swap the target; refreshes every chain's cached log-probability
-        (sampler.py:90-93).  check=False defers the failure check to the next
-        checked call (no host synchronisation here)."""
+        (sampler.py:90-93).  check=False defers both the refresh and the failure
+        check: every sweep launch recomputes the cached log p from the bits at
+        its start, so the refresh rides on the next launch (a zero-step launch
+        runs first only if log_probs / state is read before any sweep), and a
+        non-finite refreshed value is reported by the next checked call with
+        step 0, as an immediate check would."""
         ev = _device_evaluator(evaluator)
         if ev.n_visible != self.n_sites:
             raise ValueError("evaluator and ensemble disagree on the number of sites")
         self._evaluator = ev
         self._bind_scratch()
-        self._launch(0)
         if check:
+            self._launch(0)
             self._check()
+        else:
+            self._refresh_pending = True
+
+    def _flush_refresh(self):
+        if getattr(self, "_refresh_pending", False):
+            self._launch(0)
 
     def reset_counters(self):
         self._acc.zero_()
@@ -241,6 +253,7 @@ class ChainEnsemble:
         (steps_done) and the stream key / proposal / shard.  The theta
         accumulators are a function of the bits (refreshed at every launch),
         so they are not stored."""
+        self._flush_refresh()
         self._check()
         return {"format": "mpv-chains-v1", "n_sites": self.n_sites, "n_chains": self.n_chains,
                 "chain_offset": self.chain_offset, "n_chains_total": self.n_chains_total, "key": self.key,
@@ -291,6 +304,7 @@ class ChainEnsemble:
 
     @property
     def log_probs(self) -> np.ndarray:
+        self._flush_refresh()
         return self._logp.cpu().numpy().copy()
 
     @property
