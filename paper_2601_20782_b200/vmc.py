@@ -249,11 +249,13 @@ class FactoredLogDerivatives:
             if self.U:
                 nat.call("mpv_pack_bits", bits_u8.data_ptr(), self.U, self.N, packed.data_ptr(), nat.stream_handle(dev))
         self.packed = packed.contiguous()
+        self.packed_u8 = bits_u8
         x = bits_u8.to(torch.complex128)
         self.t = torch.tanh(x @ _t(params.w, dev).T + _t(params.b, dev)[None, :]).contiguous()
         self.scratch = torch.empty(nat.load().mpv_logderiv_scratch_bytes(self.U, self.N, self.M), dtype=torch.uint8,
                                    device=dev)
         self.reduce = reduce or (lambda z: z)
+        self.reduce_is_local = reduce is None
         self.device = dev
 
     def o_v(self, v):
@@ -320,6 +322,51 @@ def sr_step_cg(o: FactoredLogDerivatives, eps, weights, lambda_shift: float, eta
     return SrUpdate(g, float("nan"), residual, lambda_shift, eta, it), f, float(e.real)
 
 
+def sr_step_minsr(o: FactoredLogDerivatives, eps, weights, lambda_shift: float, eta: float):
+    """The same SR update solved in sample space (minSR; beyond the reference).
+
+    With O~ = W^{1/2} (O - 1 obar^T) the reference's estimators are S = O~^H O~
+    and F = O~^H e~ (e~ = W^{1/2} (eps - ebar)), and the push-through identity
+    gives g = (S + lambda)^-1 F = O~^H (O~ O~^H + lambda)^-1 e~ exactly: a U x U
+    Cholesky instead of a P x P one (cheaper whenever U < P).  The Gram matrix
+    never needs O: O O^H = X X^T + (T T^H) * (1 + X X^T) (elementwise), one real
+    and one complex GEMM (cuBLAS); O^H y runs in csrc/logderiv.cuh.
+    Single process only (the U x U system couples every rank's samples)."""
+    import torch
+
+    if lambda_shift < 0:
+        raise ValueError("lambda must be >= 0")
+    if eta <= 0:
+        raise ValueError("eta must be > 0")
+    if not o.reduce_is_local:
+        raise ValueError("minSR couples all samples: use sr_solver='cg' or 'dense' across ranks")
+    w = weights.to(torch.float64)
+    wc = w.to(torch.complex128)
+    obar = o.oh_u(wc).conj()  # sum_w O
+    e = wc @ eps
+    xr = o.packed_u8.to(torch.float64)
+    xx = xr @ xr.T
+    gram = xx.to(torch.complex128) + (o.t @ o.t.mH) * (1.0 + xx)
+    c = o.o_v(obar.conj())  # c_s = sum_j O_sj conj(obar_j)
+    ones = torch.ones_like(c)
+    k = gram - c[:, None] * ones[None, :] - ones[:, None] * c.conj()[None, :] + torch.vdot(obar, obar).real
+    sw = torch.sqrt(w).to(torch.complex128)
+    k = sw[:, None] * k * sw[None, :]
+    k = 0.5 * (k + k.mH)
+    k += lambda_shift * torch.eye(k.shape[0], dtype=k.dtype, device=k.device)
+    et = sw * (eps - e)
+    L, info = torch.linalg.cholesky_ex(k)
+    if int(info) != 0:
+        raise SolverError("sample-space matrix O~ O~^H + lambda I is not positive definite")
+    y = torch.cholesky_solve(et[:, None], L)[:, 0]
+    y = y + torch.cholesky_solve((et - k @ y)[:, None], L)[:, 0]  # one refinement pass
+    z = sw * y
+    g = o.oh_u(z) - obar.conj() * z.sum()
+    f = o.oh_u(wc * eps) - o.oh_u(wc) * e
+    residual = float(torch.linalg.norm(k @ y - et) / max(float(torch.linalg.norm(et)), 1e-300))
+    return SrUpdate(g, float("nan"), residual, lambda_shift, eta), f, float(e.real)
+
+
 @dataclass
 class TrainConfig:
     """Reference TrainConfig (vmc.py:320-351) plus compute_kappa (the eigvalsh of
@@ -346,7 +393,7 @@ class TrainConfig:
     track_timings: bool = False
     reference_energy: float | None = None
     compute_kappa: bool = True
-    sr_solver: str = "dense"  # "dense" (reference: Cholesky on S) or "cg" (matrix-free, factored O)
+    sr_solver: str = "dense"  # "dense" (reference: Cholesky on S), "cg" (matrix-free) or "minsr" (sample space)
     cg_tol: float = 1e-10
     cg_maxiter: int = 1000
 
@@ -355,7 +402,7 @@ class TrainConfig:
             raise ValueError("n_steps and n_samples must be positive")
         if self.sampling_mode not in ("mcmc", "exact"):
             raise ValueError(f"unknown sampling mode {self.sampling_mode!r}")
-        if self.sr_solver not in ("dense", "cg"):
+        if self.sr_solver not in ("dense", "cg", "minsr"):
             raise ValueError(f"unknown SR solver {self.sr_solver!r}")
         if self.proposal is None:
             from .sampler import Proposal
@@ -462,6 +509,11 @@ def train(config: TrainConfig, device=None, group=None, local: bool = False) -> 
             fo = FactoredLogDerivatives(params, u8, uniq, red)
             update, f, energy = sr_step_cg(fo, eps, est_w, config.lambda_shift, config.eta, config.cg_tol,
                                            config.cg_maxiter)
+        elif config.sr_solver == "minsr":
+            if world > 1:
+                raise ValueError("sr_solver='minsr' is single-process (use 'cg' or 'dense' across ranks)")
+            update, f, energy = sr_step_minsr(FactoredLogDerivatives(params, u8, uniq), eps, est_w,
+                                              config.lambda_shift, config.eta)
         else:
             o = grad_log_psi_device(params, u8)
             if world > 1:

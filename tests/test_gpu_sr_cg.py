@@ -67,3 +67,27 @@ def test_train_cg_matches_dense(cuda):
         assert abs(a["energy"] - b["energy"]) <= 1e-9 * max(1.0, abs(a["energy"]))
         assert a["acceptance"] == b["acceptance"]
     np.testing.assert_allclose(cg.params.w, dense.params.w, rtol=1e-8, atol=1e-10)
+
+
+@pytest.mark.parametrize("lam,n,alpha,U", [(1e-3, 20, 2, 500), (1e-1, 12, 3, 200), (1e-3, 37, 1, 1200)])
+def test_minsr_step_equals_dense_step(cuda, lam, n, alpha, U):
+    """Sample-space solve == the reference's parameter-space SR step (push-through identity)."""
+    import torch
+
+    p, bits, w, eps = _setup(n=n, alpha=alpha, U=U)
+    o = vmc.grad_log_psi_device(p, bits)
+    dense = vmc.sr_step(vmc.forces(o=o, eps=eps, weights=w), vmc.s_matrix(o=o, weights=w), lam, 0.02)
+    ms, f_ms, _ = vmc.sr_step_minsr(vmc.FactoredLogDerivatives(p, bits), eps, w, lam, 0.02)
+    torch.testing.assert_close(f_ms, vmc.forces(o=o, eps=eps, weights=w), rtol=1e-11, atol=1e-12)
+    err = float(torch.linalg.norm(ms.g - dense.g) / torch.linalg.norm(dense.g))
+    assert err < 1e-8, err
+
+
+def test_train_minsr_matches_dense(cuda):
+    common = dict(hamiltonian=TfimSpec(LatticeSpec.chain(8), 1.0, 1.0), n_steps=5, n_samples=256, n_chains=64,
+                  eta=0.02, seed=3, sampling_format=F64)
+    dense = vmc.train(vmc.TrainConfig(**common))
+    ms = vmc.train(vmc.TrainConfig(**common, sr_solver="minsr"))
+    for a, b in zip(dense.records, ms.records):
+        assert abs(a["energy"] - b["energy"]) <= 1e-9 * max(1.0, abs(a["energy"]))
+    np.testing.assert_allclose(ms.params.w, dense.params.w, rtol=1e-8, atol=1e-10)
