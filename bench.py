@@ -312,6 +312,40 @@ def run_ours(args, rank, world, local_rank):
 
         extra["config5_precision_bias_16x16"] = bias_sweep()
 
+        # f64 local-energy throughput for the Hamiltonians of configs[1..3] (65,536 samples each)
+        def energy_rate(spec, alpha, n=N_SITES, samples=65536):
+            from paper_2601_20782_b200.lattice import pack_bits
+
+            p = rbm.random_parameters(n, alpha, derive_key(3, "init"), 0.05)
+            kern = vmc._energy_kernel(spec, rbm.log_psi_evaluator(p))
+            rng = np.random.default_rng(0)
+            bits = rng.integers(0, 2, size=(samples, n), dtype=np.uint8)
+            if not isinstance(spec, TfimSpec):  # Sz = 0 sector, as the exchange sampler produces
+                bits = np.zeros((samples, n), dtype=np.uint8)
+                idx = np.argsort(rng.random((samples, n)), axis=1)[:, : n // 2]
+                np.put_along_axis(bits, idx, 1, axis=1)
+            packed = torch.from_numpy(pack_bits(bits)).to(dev)
+            for _ in range(2):
+                kern.packed(packed)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(5):
+                kern.packed(packed)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            ms_ = a0.elapsed_time(a1) / 5
+            return {"ms_per_65536_samples": ms_, "samples_per_s": samples / (ms_ / 1e3)}
+
+        from paper_2601_20782_b200.hamiltonians import HeisenbergSpec, J1J2Spec
+        from paper_2601_20782_b200.lattice import LatticeSpec as _LS2
+
+        extra["local_energies_f64"] = {
+            "config2_tfim10x10_h3.04_a2": energy_rate(TfimSpec(_LS2.square(10), 1.0, 3.04), 2),
+            "config3_heisenberg10x10_marshall_a4": energy_rate(HeisenbergSpec(_LS2.square(10), 1.0, marshall=True), 4),
+            "config4_j1j2_10x10_j2_0.5_marshall_a1": energy_rate(J1J2Spec(_LS2.square(10), 1.0, 0.5, marshall=True), 1),
+        }
+
     # ---- VMC iteration time at BASELINE configs[0] (N=20 open TFIM chain, alpha=1,
     # 4,096 samples, 1,024 chains, f16 sampling), reference: vmc.py:472-639 ----
     vmc_iter = None
