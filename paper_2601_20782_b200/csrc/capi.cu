@@ -33,10 +33,11 @@ void* sweep_kernel_ptr(int fmt, int variant, int G, int U, int prop, int smem) {
            : variant == MPV_ACC_X2 ? sweep_kernel_ptr_bf16_x2(G, U, prop, smem)
            : variant == MPV_ACC_XI ? sweep_kernel_ptr_bf16_xi(G, U, prop, smem)
                                    : sweep_kernel_ptr_bf16_f64(G, U, prop, smem);
-    case MPV_FMT_F32:
-      return variant == MPV_ACC_X1 ? sweep_kernel_ptr_f32_x1(G, U, prop, smem)
-           : variant == MPV_ACC_X2 ? sweep_kernel_ptr_f32_x2(G, U, prop, smem)
-                                   : sweep_kernel_ptr_f32_f64(G, U, prop, smem);
+    case MPV_FMT_F32:  // (no integer accumulators for f32 snapshots)
+      return variant == MPV_ACC_X1    ? sweep_kernel_ptr_f32_x1(G, U, prop, smem)
+           : variant == MPV_ACC_X2    ? sweep_kernel_ptr_f32_x2(G, U, prop, smem)
+           : variant == MPV_ACC_F64   ? sweep_kernel_ptr_f32_f64(G, U, prop, smem)
+                                      : nullptr;
     default:
       return sweep_kernel_ptr_f64_f64(G, U, prop, smem);
   }

@@ -161,8 +161,10 @@ class ExactPlan:
     split: float
 
 
-def plan_from_bounds(q: float, bound_re: float, bound_im: float, bound_a: float, n_visible: int) -> ExactPlan:
-    """The planner's decision from the snapshot's quantum and bounds."""
+def plan_from_bounds(q: float, bound_re: float, bound_im: float, bound_a: float, n_visible: int,
+                     allow_xi: bool = True) -> ExactPlan:
+    """The planner's decision from the snapshot's quantum and bounds (XI, the
+    integer accumulators, exists for the f16/bf16 kernels only: allow_xi)."""
     bound = max(bound_re, bound_im, bound_a)
     n_terms = n_visible + 1
     split = 2.0 ** math.floor(math.log2(2.0**25 * q / n_terms))
@@ -170,21 +172,21 @@ def plan_from_bounds(q: float, bound_re: float, bound_im: float, bound_a: float,
         split = 0.0  # X2 not exact
     if bound <= 2.0**24 * q:
         return ExactPlan(nat.ACC_X1, q, bound, split)
-    if bound < 2.0**30 * q:
+    if allow_xi and bound < 2.0**30 * q:
         return ExactPlan(nat.ACC_XI, q, bound, split)
     if split > 0.0:
         return ExactPlan(nat.ACC_X2, q, bound, split)
     return ExactPlan(nat.ACC_F64, q, bound, 0.0)
 
 
-def plan_exact(snap: RbmParameters) -> ExactPlan:
+def plan_exact(snap: RbmParameters, allow_xi: bool = True) -> ExactPlan:
     """Host planner on a rounded snapshot (the device computes the same four
     numbers in mpv_snapshot_round)."""
     a, b, w = snap.a, snap.b, snap.w
     vals = np.concatenate([a.real, b.real, b.imag, w.real.ravel(), w.imag.ravel()])
     return plan_from_bounds(finest_quantum(vals), float(np.max(np.abs(b.real) + np.abs(w.real).sum(axis=1))),
                             float(np.max(np.abs(b.imag) + np.abs(w.imag).sum(axis=1))),
-                            float(np.abs(a.real).sum()), snap.n_visible)
+                            float(np.abs(a.real).sum()), snap.n_visible, allow_xi)
 
 
 # ---------------------------------------------------------------------------
@@ -231,13 +233,16 @@ class DeviceSnapshot:
                 variant = nat.ACC_F64
             else:
                 pq = plan_dev.cpu().numpy()
-                self.plan = plan_from_bounds(float(pq[0]), float(pq[1]), float(pq[2]), float(pq[3]), N)
+                self.plan = plan_from_bounds(float(pq[0]), float(pq[1]), float(pq[2]), float(pq[3]), N,
+                                             allow_xi=fmt.name in ("f16", "bf16"))
                 if variant is None:
                     variant = self.plan.variant
                 elif variant == nat.ACC_X1 and self.plan.variant != nat.ACC_X1:
                     raise ValueError("X1 accumulators are not exact for this snapshot")
                 elif variant == nat.ACC_X2 and self.plan.split == 0.0:
                     raise ValueError("X2 accumulators are not exact for this snapshot")
+                elif variant == nat.ACC_XI and fmt.name not in ("f16", "bf16"):
+                    raise ValueError("XI accumulators exist for f16/bf16 snapshots only")
                 elif variant == nat.ACC_XI and not self.plan.bound < 2.0**30 * self.plan.quantum:
                     raise ValueError("XI accumulators are not exact for this snapshot")
                 split = self.plan.split

@@ -338,3 +338,48 @@ def test_checkpoint_resume_is_bit_identical(cuda, tmp_path, kind, weight):
     np.testing.assert_array_equal(res.bits, ref.bits)
     np.testing.assert_array_equal(res.log_probs, ref.log_probs)
     assert res.accepted == ref.accepted and res.proposed == ref.proposed
+
+
+@pytest.mark.parametrize("n,alpha,chains,kind", [(1, 2, 5, "flip"), (2, 3, 7, "exchange"), (31, 1, 33, "flip"),
+                                                 (32, "1/2", 64, "exchange"), (33, "3/11", 3, "flip"),
+                                                 (65, "1/5", 40, "flip"), (97, 1, 1, "exchange")])
+@pytest.mark.parametrize("fmt", ["f16", "bf16", "f32"])
+def test_edge_shapes_per_op_bitwise(cuda, n, alpha, chains, kind, fmt):
+    """Per-operation chains bit-identical to the oracle at edge shapes: one site,
+    word boundaries (31/32/33, 65, 97 sites), tiny M, odd chain counts, one chain."""
+    from fractions import Fraction
+
+    p = rbm.random_parameters(n, Fraction(alpha), derive_key(n, "edge"), 0.4)
+    key = derive_key(n + 1, "chains")
+    prop = sampler.Proposal(kind, None if kind == "flip" else max(1, n // 2))
+    ev = rbm.log_prob_evaluator(p, FORMATS[fmt], PER_OP)
+    ens = sampler.ChainEnsemble(chains, n, prop, ev, key)
+    snap = rbm.round_parameters(p, FORMATS[fmt])
+    ref = port.PortEnsemble(chains, n, kind, None if kind == "flip" else max(1, n // 2),
+                            port.Params(snap.a, snap.b, snap.w), fmt, int(key))
+    ens.run_steps(150)
+    ref.run_steps(150)
+    np.testing.assert_array_equal(ens.bits, ref.bits)
+    np.testing.assert_array_equal(ens.log_probs, ref.logp)
+    assert ens.accepted == ref.accepted
+
+
+@pytest.mark.parametrize("n,alpha", [(1, 3), (2, "5/2"), (31, 1), (33, "3/11"), (65, "1/5"), (97, 2), (200, 1)])
+@pytest.mark.parametrize("fmt", ["f16", "bf16", "f32"])
+def test_edge_shapes_native_model(cuda, n, alpha, fmt):
+    """NATIVE fused-sweep evaluation at edge shapes (lane layouts with padded
+    hidden units, word boundaries, M = 1..200) against the arithmetic model,
+    and a short chain run stays consistent with its own re-evaluation."""
+    from fractions import Fraction
+
+    from oracle import model
+
+    p = rbm.random_parameters(n, Fraction(alpha), derive_key(n, "edge-native"), 0.3)
+    snap = rbm.round_parameters(p, FORMATS[fmt])
+    bits = np.random.default_rng(n).integers(0, 2, size=(37, n), dtype=np.uint8)
+    ev = rbm.log_prob_evaluator(p, FORMATS[fmt], NATIVE)
+    want, tol = model.native_log_prob(snap.a, snap.b, snap.w, bits, fmt)
+    assert np.all(np.abs(ev(bits) - want) <= tol), ev.snapshot.label
+    ens = sampler.ChainEnsemble(19, n, sampler.Proposal("flip"), ev, derive_key(3, "chains"))
+    ens.run_steps(120)
+    np.testing.assert_array_equal(ens.log_probs, ev(ens.bits))  # cached log p == fresh evaluation
