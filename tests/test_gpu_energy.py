@@ -117,3 +117,23 @@ def test_odd_shapes_against_oracle(cuda, n, alpha, B):
         want = port.local_energies(port.Params(p.a, p.b, p.w), ham, spec.lattice.bond_array(), spec.j,
                                    getattr(spec, "h", 0.0), bits)
         assert np.max(np.abs(eps - want) / np.maximum(1, np.abs(want))) < 1e-10, (n, alpha, ham)
+
+
+@pytest.mark.parametrize("spec,alpha", [(TfimSpec(LatticeSpec.chain(140, True), 1.0, 0.8), "1/2"),
+                                        (HeisenbergSpec(LatticeSpec.square(12), 1.0), "1/3"),
+                                        (TfimSpec(LatticeSpec.square(16), 1.0, 3.0), "1/8")],
+                         ids=["tfim140", "heis12x12_288bonds", "tfim16x16_M32"])
+def test_many_terms_launch_configs(cuda, spec, alpha):
+    """Term counts beyond the 4-samples-per-thread block (T > 112) and beyond
+    256 (one 8-sample group per block) against the oracle."""
+    from fractions import Fraction
+
+    n = spec.lattice.n_sites
+    p = rbm.random_parameters(n, Fraction(alpha), derive_key(n, "many"), 0.2)
+    rng = np.random.default_rng(n)
+    bits = rng.integers(0, 2, size=(19, n), dtype=np.uint8)
+    eps = vmc.local_energies(spec, rbm.log_psi_evaluator(p), bits)
+    ham = "tfim" if isinstance(spec, TfimSpec) else "heisenberg"
+    want = port.local_energies(port.Params(p.a, p.b, p.w), ham, spec.lattice.bond_array(), spec.j,
+                               getattr(spec, "h", 0.0), bits)
+    assert np.max(np.abs(eps - want) / np.maximum(1, np.abs(want))) < 1e-10

@@ -380,6 +380,10 @@ def test_edge_shapes_native_model(cuda, n, alpha, fmt):
     ev = rbm.log_prob_evaluator(p, FORMATS[fmt], NATIVE)
     want, tol = model.native_log_prob(snap.a, snap.b, snap.w, bits, fmt)
     assert np.all(np.abs(ev(bits) - want) <= tol), ev.snapshot.label
-    ens = sampler.ChainEnsemble(19, n, sampler.Proposal("flip"), ev, derive_key(3, "chains"))
-    ens.run_steps(120)
-    np.testing.assert_array_equal(ens.log_probs, ev(ens.bits))  # cached log p == fresh evaluation
+    kinds = [("flip", None)] + ([("exchange", n // 2)] if n >= 2 else [])
+    for kind, weight in kinds:
+        ens = sampler.ChainEnsemble(19, n, sampler.Proposal(kind, weight), ev, derive_key(3, "chains"))
+        ens.run_steps(120)
+        np.testing.assert_array_equal(ens.log_probs, ev(ens.bits))  # cached log p == fresh evaluation
+        if kind == "exchange":
+            assert np.all(ens.bits.sum(axis=1) == n // 2)

@@ -91,3 +91,18 @@ def test_train_minsr_matches_dense(cuda):
     for a, b in zip(dense.records, ms.records):
         assert abs(a["energy"] - b["energy"]) <= 1e-9 * max(1.0, abs(a["energy"]))
     np.testing.assert_allclose(ms.params.w, dense.params.w, rtol=1e-8, atol=1e-10)
+
+
+def test_factored_products_at_the_size_limits(cuda):
+    """N = 256 sites (8 words), M = 512 hidden units: the largest shapes the
+    O-product kernels accept, against the materialised O."""
+    import torch
+
+    p, bits, w, _ = _setup(n=256, alpha=2, U=300, scale=0.05)
+    o = vmc.grad_log_psi_device(p, bits)
+    fo = vmc.FactoredLogDerivatives(p, bits)
+    rng = np.random.default_rng(5)
+    v = torch.complex(torch.from_numpy(rng.normal(size=o.shape[1])), torch.from_numpy(rng.normal(size=o.shape[1]))).cuda()
+    u = torch.complex(torch.from_numpy(rng.normal(size=300)), torch.from_numpy(rng.normal(size=300))).cuda()
+    torch.testing.assert_close(fo.o_v(v), o @ v, rtol=1e-11, atol=1e-10)
+    torch.testing.assert_close(fo.oh_u(u), o.conj().T @ u, rtol=1e-11, atol=1e-10)
