@@ -210,6 +210,23 @@ int mpv_logderiv_ov(const double* t, const uint32_t* bits, int64_t U, int N, int
 int mpv_logderiv_ohu(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* u,
                      double* out, void* scratch, void* stream);
 
+/* ---- batched forward on the tensor cores (north_star (2); ref: rbm.py:130-150
+ *      _fast_forward over a batch, i.e. log_psi_batch / log_prob_batch) ----
+ * theta = b + W x as a tcgen05 GEMM (f16/bf16 operands, f32 accumulators in
+ * TMEM) with the log-cosh sum as its epilogue.  mpv_forward_tc_prepare rounds
+ * params = [a (N) | b (M) | w_t (N x M)] complex (re, im) f64 (the layout of
+ * mpv_snapshot_round) to fmt (MPV_FMT_F16 / MPV_FMT_BF16, round-to-nearest-
+ * even as round_parameters, rbm.py:91-101) into `weights` (device, >=
+ * mpv_forward_tc_weights_bytes(N, M); 0 = unsupported shape, N <= 1024).
+ * mpv_forward_tc: bits packed [B][ceil(N/32)]; any of out_lp (= 2 Re log psi),
+ * out_re, out_im (double[B]) may be NULL but not all; max_ctas <= 0 = one CTA
+ * per SM.  Agrees with the f64 forward of the rounded parameters to f32
+ * accumulation error (tests/test_gpu_forward_tc.py). */
+size_t mpv_forward_tc_weights_bytes(int N, int M);
+int mpv_forward_tc_prepare(int N, int M, int fmt, const double* params, void* weights, void* stream);
+int mpv_forward_tc(int N, int M, int fmt, const void* weights, const uint32_t* bits, int64_t B, double* out_lp,
+                   double* out_re, double* out_im, int max_ctas, void* stream);
+
 /* ---- helpers ---- */
 int mpv_unpack_bits(const uint32_t* words, int64_t B, int N, uint8_t* out, void* stream);
 int mpv_pack_bits(const uint8_t* bits, int64_t B, int N, uint32_t* out, void* stream);

@@ -71,6 +71,10 @@ _SIGNATURES = {
                                           ctypes.c_int, _f64, _f64, _vp, _vp, _i64, _vp, _vp, _vp]),
     "mpv_local_energies_ex": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp,
                                              ctypes.c_int, _f64, _f64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "mpv_forward_tc_weights_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int]),
+    "mpv_forward_tc_prepare": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
+    "mpv_forward_tc": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _vp,
+                                      ctypes.c_int, _vp]),
     "mpv_unpack_bits": (ctypes.c_int, [_vp, _i64, ctypes.c_int, _vp, _vp]),
     "mpv_pack_bits": (ctypes.c_int, [_vp, _i64, ctypes.c_int, _vp, _vp]),
     "mpv_sum_i64": (ctypes.c_int, [_vp, _i64, _vp, _vp]),

@@ -21,6 +21,11 @@ MPV_DECL(f32, x1) MPV_DECL(f32, x2) MPV_DECL(f32, f64)
 MPV_DECL(f64, f64)
 #undef MPV_DECL
 
+size_t forward_tc_weights_bytes(int N, int M);
+cudaError_t forward_tc_prepare(int N, int M, int fmt, const double* params, void* weights, cudaStream_t st);
+cudaError_t forward_tc_launch(int N, int M, int fmt, const void* weights, const uint32_t* bits, int64_t B,
+                              double* out_lp, double* out_re, double* out_im, int max_ctas, cudaStream_t st);
+
 void* sweep_kernel_ptr(int fmt, int variant, int G, int U, int prop, int smem) {
   switch (fmt) {
     case MPV_FMT_F16:
@@ -760,6 +765,32 @@ int mpv_logderiv_ohu(const double* t, const uint32_t* bits, int64_t U, int N, in
   ld_ohu_reduce_kernel<<<(unsigned)std::min(148 * 8, (P + 255) / 256), 256, 0, st>>>(partial, chunks, N, M,
                                                                                       (double2*)out);
   return check_launch("logderiv_ohu");
+}
+
+// ---- batched forward on tcgen05 (forward_tc.cu) ----
+size_t mpv_forward_tc_weights_bytes(int N, int M) { return forward_tc_weights_bytes(N, M); }
+
+int mpv_forward_tc_prepare(int N, int M, int fmt, const double* params, void* weights, void* stream) {
+  if (!params || !weights) return fail(MPV_ERR_ARGS, "forward_tc_prepare: null pointer");
+  if (fmt != MPV_FMT_F16 && fmt != MPV_FMT_BF16)
+    return fail(MPV_ERR_ARGS, "forward_tc_prepare: the tensor-core forward takes f16 or bf16 parameters");
+  if (!forward_tc_weights_bytes(N, M)) return fail(MPV_ERR_ARGS, "forward_tc_prepare: unsupported N/M");
+  const cudaError_t e = forward_tc_prepare(N, M, fmt, params, weights, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("forward_tc_prepare: ") + cudaGetErrorString(e));
+  return MPV_OK;
+}
+
+int mpv_forward_tc(int N, int M, int fmt, const void* weights, const uint32_t* bits, int64_t B, double* out_lp,
+                   double* out_re, double* out_im, int max_ctas, void* stream) {
+  if (B == 0 && weights) return MPV_OK;
+  if (!weights || !bits || B < 0 || !(out_lp || out_re || out_im)) return fail(MPV_ERR_ARGS, "forward_tc: bad args");
+  if (fmt != MPV_FMT_F16 && fmt != MPV_FMT_BF16)
+    return fail(MPV_ERR_ARGS, "forward_tc: the tensor-core forward takes f16 or bf16 parameters");
+  if (!forward_tc_weights_bytes(N, M)) return fail(MPV_ERR_ARGS, "forward_tc: unsupported N/M");
+  const cudaError_t e =
+      forward_tc_launch(N, M, fmt, weights, bits, B, out_lp, out_re, out_im, max_ctas, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("forward_tc: ") + cudaGetErrorString(e));
+  return MPV_OK;
 }
 
 int mpv_unpack_bits(const uint32_t* words, int64_t B, int N, uint8_t* out, void* stream) {

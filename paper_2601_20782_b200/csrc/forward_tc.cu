@@ -1,0 +1,407 @@
+// Batched RBM forward on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// North-star subsystem (2): "the batched proposal and forward pass is a
+// tcgen05 tensor-core GEMM in f16/bf16, since that path really is a dense
+// contraction".  For B configurations x in {0,1}^N (packed words, the layout
+// of mpv_chains.bits) it evaluates the reference's forward
+// (ref: rbm.py:130-150 _fast_forward / _logcosh_pair; oracle/c/oracle_port.c
+// f64_row) with the parameters rounded to f16/bf16:
+//
+//   theta_i = b_i + sum_k w_ik x_k                       (GEMM, f32 accumulate)
+//   log psi = sum_k a_k x_k + sum_i [u - log 2 + log|(1+t)cos v + i(1-t)sin v|]
+//             + i (... + sum_i atan2((1-t) sin v, (1+t) cos v)),
+//   u = |Re theta|, v = sign(Re theta) Im theta, t = exp(-2u).
+//
+// GEMM shape per CTA tile: D[128 configurations x HC hidden] (re and im in
+// two TMEM column blocks, cols [0,HC) and [256,256+HC)) = A[128 x Kp] * B[Kp x HC],
+// Kp = N rounded up to 16.  A is decoded from the packed bits straight into
+// shared memory (x in {0,1} is exact in f16/bf16, so the products are exact
+// and only the f32 accumulation order differs from the f64 reference); B
+// (the rounded weights, re and im rows) is staged once per CTA by the bulk
+// copy engine when it fits (one chunk), else re-staged per chunk from L2.
+// Both operands use the K-major no-swizzle canonical layout: 8x16-byte core
+// matrices, K-adjacent core matrices 128 B apart (LBO), 8-row groups Kp*16 B
+// apart (SBO).  One elected thread issues tcgen05.mma (M=128, N=HC, K=16 per
+// instruction) and commits to an mbarrier; 8 warps drain TMEM with
+// tcgen05.ld (warp w reads lanes 32(w%4).. and every 4th 8-column group from
+// w/4) and run the f32 log-cosh epilogue, which is the kernel's bound (3 MUFU
+// ops per hidden unit for log p, + sin and atan2 for the phase, against 4*Kp
+// tensor flops per hidden unit).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <stdint.h>
+
+#include "../../include/mpvmc_b200.h"
+
+namespace mpv {
+namespace tc {
+
+constexpr int kRows = 128;     // MMA M (configurations per tile)
+constexpr int kThreads = 512;  // 16 warps: 4 TMEM lane quarters x 4 column slices
+constexpr int kSlices = kThreads / 128;
+constexpr int kMaxHC = 256;    // MMA N limit / TMEM block
+constexpr size_t kSmemBudget = 200 * 1024;
+constexpr size_t kSmemFloor = 116 * 1024;  // one CTA per SM (512 TMEM columns each)
+
+struct Layout {
+  int N, M, Kp, HC, nchunks, words;
+  size_t a_bytes;      // A tile bytes
+  size_t chunk_bytes;  // B chunk bytes (re + im rows)
+  size_t smem;         // dynamic smem
+  // weights blob: [chunks of B][bias re/im f32 (nchunks*HC each)][a re/im f32 (N each)]
+  size_t off_bias, off_vis, blob_bytes;
+};
+
+__host__ __device__ inline size_t rup(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline bool make_layout(int N, int M, Layout* L) {
+  if (N < 1 || N > 1024 || M < 1) return false;
+  L->N = N; L->M = M; L->words = (N + 31) / 32;
+  L->Kp = (int)rup(N, 16);
+  L->a_bytes = (size_t)kRows * L->Kp * 2;
+  if (L->a_bytes + 2ull * 16 * L->Kp * 2 + 4096 > kSmemBudget) return false;
+  const size_t hc_cap = (kSmemBudget - L->a_bytes - 4096) / (4ull * L->Kp);
+  const int hcmax = (int)std::min<size_t>(kMaxHC, hc_cap / 16 * 16);
+  if (hcmax < 16) return false;
+  L->nchunks = (M + hcmax - 1) / hcmax;
+  L->HC = (int)rup((M + L->nchunks - 1) / L->nchunks, 16);
+  L->chunk_bytes = 4ull * L->HC * L->Kp;
+  const size_t used = L->a_bytes + L->chunk_bytes + 2ull * N * 4 + 3ull * kRows * kSlices * 4 + 1024;
+  L->smem = std::max(used, kSmemFloor);
+  L->off_bias = L->chunk_bytes * L->nchunks;
+  L->off_vis = L->off_bias + 2ull * L->nchunks * L->HC * 4;
+  L->blob_bytes = rup(L->off_vis + 2ull * N * 4, 256);
+  return true;
+}
+
+// byte offset of element (row r, k) in a K-major no-swizzle tile with Kp columns
+__host__ __device__ inline size_t kmajor_off(int r, int k, int Kp) {
+  return (size_t)(r & 7) * 16 + (size_t)(r >> 3) * Kp * 16 + (size_t)(k >> 3) * 128 + (size_t)(k & 7) * 2;
+}
+
+template <int FMT>
+__device__ inline uint16_t to_bits16(double v) {
+  if (FMT == MPV_FMT_F16) return __half_as_ushort(__double2half(v));
+  return __bfloat16_as_ushort(__double2bfloat16(v));
+}
+template <int FMT>
+__device__ inline float from_bits16(uint16_t h) {
+  if (FMT == MPV_FMT_F16) return __half2float(__ushort_as_half(h));
+  return __bfloat162float(__ushort_as_bfloat16(h));
+}
+
+// params = [a (N) | b (M) | w_t (N x M)] complex (re, im) f64, as mpv_snapshot_round.
+template <int FMT>
+__global__ void prepare_kernel(Layout L, const double* __restrict__ params, uint8_t* __restrict__ blob) {
+  const int N = L.N, M = L.M, HC = L.HC, Kp = L.Kp;
+  const double* a = params;
+  const double* b = params + 2 * (size_t)N;
+  const double* wt = params + 2 * (size_t)(N + M);
+  const int64_t nb = (int64_t)L.nchunks * 2 * HC * Kp;  // B elements
+  float* bias = reinterpret_cast<float*>(blob + L.off_bias);
+  float* vis = reinterpret_cast<float*>(blob + L.off_vis);
+  const int64_t total = nb + 2LL * L.nchunks * HC + 2LL * N;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    if (idx < nb) {
+      const int64_t per_chunk = 2LL * HC * Kp;
+      const int c = (int)(idx / per_chunk);
+      const int rem = (int)(idx % per_chunk);
+      const int r = rem / Kp, k = rem % Kp;  // r in [0, 2HC): re rows then im rows
+      const int part = r / HC, i = c * HC + (r % HC);
+      uint16_t h = 0;
+      if (i < M && k < N) h = to_bits16<FMT>(wt[2 * ((size_t)k * M + i) + part]);
+      *reinterpret_cast<uint16_t*>(blob + (size_t)c * L.chunk_bytes + (size_t)part * 2 * HC * Kp +
+                                   kmajor_off(r % HC, k, Kp)) = h;
+    } else if (idx < nb + 2LL * L.nchunks * HC) {
+      const int j = (int)(idx - nb);  // [re: nchunks*HC][im: nchunks*HC]
+      const int part = j / (L.nchunks * HC), i = j % (L.nchunks * HC);
+      bias[j] = i < M ? from_bits16<FMT>(to_bits16<FMT>(b[2 * (size_t)i + part])) : 0.0f;
+    } else {
+      const int j = (int)(idx - nb - 2LL * L.nchunks * HC);  // [re: N][im: N]
+      const int part = j / N, k = j % N;
+      vis[j] = from_bits16<FMT>(to_bits16<FMT>(a[2 * (size_t)k + part]));
+    }
+  }
+}
+
+__device__ inline uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ inline uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // descriptor version (sm_100)
+  return d;         // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+
+__device__ inline void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ inline void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{.reg .pred p;\nWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          bar),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ inline void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// Stage one B chunk (bytes multiple of 16) global -> smem with the bulk copy engine.
+__device__ inline void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  const uint32_t step = 65536;  // keep each bulk copy well inside the size field
+  for (uint32_t off = 0; off < bytes; off += step) {
+    const uint32_t n = bytes - off < step ? bytes - off : step;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst + off),
+                 "l"((const uint8_t*)src + off), "r"(n), "r"(bar)
+                 : "memory");
+  }
+}
+
+// cos(x) with a two-constant Cody-Waite reduction to [-pi, pi] ahead of the
+// MUFU approximation (cos.approx is accurate to ~2^-21 absolute only there).
+__device__ __forceinline__ float reduce_2pi(float x) {
+  const float k = rintf(x * 0.159154943091895336f);
+  x = fmaf(-k, 6.28318548202514648f, x);
+  return fmaf(-k, -1.74845553e-7f, x);
+}
+
+// Per hidden unit (theta = x + i y), with u = |x|, v = sign(x) y, t = e^{-2u}:
+//   |(1+t) cos v + i (1-t) sin v|^2 = (1-t)^2 + 4 t cos^2 v,
+// so Re log cosh theta = u - log 2 + 0.5 log((1-t)^2 + 4t cos^2 v): three MUFU
+// ops (ex2, cos, lg2).  The phase atan2((1-t) sin v, (1+t) cos v) is computed
+// only when Im log psi is requested (IM), from sin v / cos v.
+template <int FMT, bool IM>
+__global__ void __launch_bounds__(kThreads, 1)
+    forward_tc_kernel(Layout L, const uint8_t* __restrict__ blob, const uint32_t* __restrict__ bits, int64_t B,
+                      double* __restrict__ out_lp, double* __restrict__ out_re, double* __restrict__ out_im) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(8) uint64_t bars[2];  // [0] MMA done, [1] B staged
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int N = L.N, Kp = L.Kp, HC = L.HC, nchunks = L.nchunks, words = L.words;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + L.a_bytes;
+  float* sVis = reinterpret_cast<float*>(sB + L.chunk_bytes);  // [re N][im N]
+  float* sRed = sVis + 2 * N;                                   // [slice][128][3]
+  const uint32_t aA = smem_u32(sA), aB = smem_u32(sB);
+  const uint32_t bar_mma = smem_u32(&bars[0]), bar_b = smem_u32(&bars[1]);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_mma));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_b));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const float* gvis = reinterpret_cast<const float*>(blob + L.off_vis);
+  for (int j = tid; j < 2 * N; j += kThreads) sVis[j] = gvis[j];
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  const float* bias_re = reinterpret_cast<const float*>(blob + L.off_bias);
+  const float* bias_im = bias_re + (size_t)nchunks * HC;
+  // instruction descriptor: f32 accumulate, A/B format, K-major both, N = HC, M = 128
+  const uint32_t fmtbits = FMT == MPV_FMT_BF16 ? 1u : 0u;
+  const uint32_t idesc = (1u << 4) | (fmtbits << 7) | (fmtbits << 10) | ((uint32_t)(HC >> 3) << 17) |
+                         ((uint32_t)(kRows >> 4) << 24);
+  const uint32_t sbo = (uint32_t)Kp * 16, lbo = 128;
+  uint32_t ph_mma = 0, ph_b = 0;
+
+  const int q = warp & 3, slice = warp >> 2;
+  const int row = q * 32 + lane;  // TMEM lane = tile row
+  const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+  const uint16_t one = FMT == MPV_FMT_BF16 ? 0x3F80 : 0x3C00;
+  const int64_t ntiles = (B + kRows - 1) / kRows;
+  const int kgroups = Kp / 8, cgroups = HC / 8;
+  // every column (padding included) contributes -log 2; padded columns (theta = 0) add log 2 back
+  const float ln2 = 0.693147180559945309f;
+
+  if (nchunks == 1 && tid == 0) bulk_load(aB, blob, (uint32_t)L.chunk_bytes, bar_b);
+  bool b_resident = false;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * kRows;
+    // A tile: 8 bits -> 8 f16/bf16 values per 16-byte store
+    for (int idx = tid; idx < kRows * kgroups; idx += kThreads) {
+      const int r = idx / kgroups, g = idx % kgroups;
+      const int64_t s = row0 + r;
+      uint32_t byte = 0;
+      if (s < B && g * 8 < N) {
+        byte = (bits[s * words + (g >> 2)] >> ((g & 3) * 8)) & 0xFFu;
+        const int valid = N - g * 8;
+        if (valid < 8) byte &= (1u << valid) - 1u;
+      }
+      uint32_t p[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        p[j] = ((byte >> (2 * j)) & 1u ? (uint32_t)one : 0u) | ((byte >> (2 * j + 1)) & 1u ? (uint32_t)one << 16 : 0u);
+      *reinterpret_cast<uint4*>(sA + kmajor_off(r, g * 8, Kp)) = make_uint4(p[0], p[1], p[2], p[3]);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+
+    float su = 0.0f, sl = 0.0f, si = 0.0f;  // sum u, sum log2(q), sum phase
+    for (int c = 0; c < nchunks; ++c) {
+      if (tid == 0) {
+        if (nchunks > 1) bulk_load(aB, blob + (size_t)c * L.chunk_bytes, (uint32_t)L.chunk_bytes, bar_b);
+        if (!b_resident) {
+          mbar_wait(bar_b, ph_b);
+          ph_b ^= 1;
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int ks = 0; ks < Kp / 16; ++ks) {
+          const uint64_t da = make_desc(aA + ks * 256, lbo, sbo);
+          const uint64_t dre = make_desc(aB + ks * 256, lbo, sbo);
+          const uint64_t dim = make_desc(aB + (uint32_t)HC * Kp * 2 + ks * 256, lbo, sbo);
+          mma_f16(tmem, da, dre, idesc, ks > 0);
+          mma_f16(tmem + 256, da, dim, idesc, ks > 0);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar_mma)
+                     : "memory");
+      }
+      b_resident = nchunks == 1;
+      mbar_wait(bar_mma, ph_mma);
+      ph_mma ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const float* br = bias_re + (size_t)c * HC;
+      const float* bi = bias_im + (size_t)c * HC;
+      for (int cg = slice; cg < cgroups; cg += kSlices) {
+        const int j0 = cg * 8;
+        float tr[8], ti[8];
+        tmem_ld8(tmem + t_lane + j0, tr);
+        tmem_ld8(tmem + t_lane + 256 + j0, ti);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float x = tr[j] + br[j0 + j], y = ti[j] + bi[j0 + j];
+          const float u = fabsf(x);
+          const float v = x < 0.0f ? -y : y;
+          const float t = exp2f(-2.885390081777926815f * u);  // e^{-2u}, ex2.approx (ftz)
+          // 1 - t without cancellation for small u (series of -expm1(-2u))
+          const float omt = u < 0.0625f ? u * fmaf(u, fmaf(u, 1.33333333f, -2.0f), 2.0f) : 1.0f - t;
+          su += u;
+          float sv, cv;
+          const float vr = reduce_2pi(v);
+          if (IM) {
+            __sincosf(vr, &sv, &cv);
+            const float wr = (1.0f + t) * cv, wi = omt * sv;
+            sl += __log2f(fmaf(wr, wr, wi * wi));
+            si += atan2f(wi, wr);
+          } else {
+            // |.|^2 = (1-t)^2 + 4t cos^2 v: no cancellation near the zeros of cosh
+            cv = __cosf(vr);
+            sl += __log2f(fmaf(4.0f * t * cv, cv, omt * omt));
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();  // TMEM and the B buffer are free for the next chunk / tile
+    }
+    if (slice > 0) {
+      float* r = sRed + 3 * ((slice - 1) * kRows + row);
+      r[0] = su;
+      r[1] = sl;
+      r[2] = si;
+    }
+    __syncthreads();
+    if (slice == 0) {
+      const int64_t s = row0 + row;
+#pragma unroll
+      for (int k = 1; k < kSlices; ++k) {
+        const float* r = sRed + 3 * ((k - 1) * kRows + row);
+        su += r[0];
+        sl += r[1];
+        si += r[2];
+      }
+      if (s < B) {
+        float vr = 0.0f, vi = 0.0f;
+        for (int w = 0; w < words; ++w) {
+          uint32_t m = bits[s * words + w];
+          if (w == words - 1 && (N & 31)) m &= (1u << (N & 31)) - 1u;
+          while (m) {
+            const int k = w * 32 + __ffs(m) - 1;
+            m &= m - 1;
+            vr += sVis[k];
+            if (IM) vi += sVis[N + k];
+          }
+        }
+        const double re = (double)vr + (double)su + 0.5 * (double)ln2 * (double)sl -
+                          (double)ln2 * (double)(nchunks * HC);
+        if (out_lp) out_lp[s] = 2.0 * re;
+        if (out_re) out_re[s] = re;
+        if (IM && out_im) out_im[s] = (double)vi + (double)si;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+}  // namespace tc
+
+// -------- launchers (C ABI wrappers live in capi.cu) --------
+size_t forward_tc_weights_bytes(int N, int M) {
+  tc::Layout L;
+  return tc::make_layout(N, M, &L) ? L.blob_bytes : 0;
+}
+
+cudaError_t forward_tc_prepare(int N, int M, int fmt, const double* params, void* weights, cudaStream_t st) {
+  tc::Layout L;
+  if (!tc::make_layout(N, M, &L)) return cudaErrorInvalidValue;
+  const int64_t total = (int64_t)L.nchunks * 2 * L.HC * L.Kp + 2LL * L.nchunks * L.HC + 2LL * N;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (fmt == MPV_FMT_F16)
+    tc::prepare_kernel<MPV_FMT_F16><<<grid, 256, 0, st>>>(L, params, (uint8_t*)weights);
+  else
+    tc::prepare_kernel<MPV_FMT_BF16><<<grid, 256, 0, st>>>(L, params, (uint8_t*)weights);
+  return cudaGetLastError();
+}
+
+cudaError_t forward_tc_launch(int N, int M, int fmt, const void* weights, const uint32_t* bits, int64_t B,
+                              double* out_lp, double* out_re, double* out_im, int max_ctas, cudaStream_t st) {
+  tc::Layout L;
+  if (!tc::make_layout(N, M, &L)) return cudaErrorInvalidValue;
+  const bool im = out_im != nullptr;
+  const void* fn = fmt == MPV_FMT_F16 ? (im ? (const void*)&tc::forward_tc_kernel<MPV_FMT_F16, true>
+                                            : (const void*)&tc::forward_tc_kernel<MPV_FMT_F16, false>)
+                                      : (im ? (const void*)&tc::forward_tc_kernel<MPV_FMT_BF16, true>
+                                            : (const void*)&tc::forward_tc_kernel<MPV_FMT_BF16, false>);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ntiles = (B + tc::kRows - 1) / tc::kRows;
+  int64_t grid = std::min<int64_t>(ntiles, sms);
+  if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
+  const uint8_t* blob = (const uint8_t*)weights;
+  void* args[] = {&L, &blob, &bits, &B, &out_lp, &out_re, &out_im};
+  return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(tc::kThreads), args, L.smem, st);
+}
+
+}  // namespace mpv

@@ -489,6 +489,66 @@ def log_psi_batch(params, bits, fmt: FloatFormat = F64, mode: RoundingMode = Rou
     return out
 
 
+class TensorCoreForward:
+    """Batched forward of the RBM as a tcgen05 tensor-core GEMM (north_star
+    subsystem (2)): theta = b + W x with f16/bf16 operands (the parameters
+    rounded as round_parameters, rbm.py:91-101; x in {0,1} exact) and f32
+    accumulators in TMEM, the log-cosh sum of rbm.py:130-150 as the GEMM's
+    epilogue.  Agrees with the f64 forward of the rounded parameters to f32
+    accumulation error; the sampler's bit-exact arithmetics (per-operation,
+    NATIVE) stay in the sweep kernels."""
+
+    def __init__(self, params: RbmParameters, fmt: FloatFormat, device=None):
+        import torch
+
+        nat.require_cuda()
+        if fmt.name not in ("f16", "bf16"):
+            raise ValueError("the tensor-core forward takes f16 or bf16 parameters")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.params, self.fmt = params, fmt
+        N, M = params.n_visible, params.n_hidden
+        self.n_visible, self.n_hidden = N, M
+        nbytes = int(nat.load().mpv_forward_tc_weights_bytes(N, M))
+        if nbytes == 0:
+            raise ValueError(f"tensor-core forward: unsupported shape N={N}, M={M}")
+        host = torch.empty(2 * (N + M + N * M), dtype=torch.float64, pin_memory=True)
+        hv = host.numpy().view(np.complex128)
+        hv[:N], hv[N:N + M] = params.a, params.b
+        hv[N + M:].reshape(N, M)[:] = params.w.T
+        src = host.to(self.device, non_blocking=True)
+        self._weights = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+        nat.call("mpv_forward_tc_prepare", N, M, fmt.code, src.data_ptr(), self._weights.data_ptr(),
+                 nat.stream_handle(self.device))
+        torch.cuda.current_stream(self.device).synchronize()  # `host`/`src` are released on return
+
+    def forward_packed(self, packed, out_lp=None, out_re=None, out_im=None, max_ctas: int = 0):
+        """Device call on packed words [B, ceil(N/32)]; returns (lp, re, im) f64 tensors."""
+        import torch
+
+        B = packed.shape[0]
+        if out_lp is None and out_re is None and out_im is None:
+            out_lp = torch.empty(B, dtype=torch.float64, device=self.device)
+            out_re, out_im = torch.empty_like(out_lp), torch.empty_like(out_lp)
+        ptr = (lambda t: t.data_ptr() if t is not None else None)
+        nat.call("mpv_forward_tc", self.n_visible, self.n_hidden, self.fmt.code, self._weights.data_ptr(),
+                 packed.data_ptr(), B, ptr(out_lp), ptr(out_re), ptr(out_im), int(max_ctas),
+                 nat.stream_handle(self.device))
+        return out_lp, out_re, out_im
+
+    def __call__(self, bits) -> np.ndarray:
+        """complex128 log psi for a (B, N) uint8 bit matrix."""
+        bits = np.atleast_2d(np.asarray(bits, dtype=np.uint8))
+        if bits.shape[1] != self.n_visible:
+            raise ValueError(f"bit matrix has {bits.shape[1]} sites, ansatz has {self.n_visible}")
+        _, re, im = self.forward_packed(device_pack(bits, self.device))
+        return re.cpu().numpy() + 1j * im.cpu().numpy()
+
+
+def log_psi_batch_tc(params, bits, fmt: FloatFormat, device=None) -> np.ndarray:
+    """log psi(x) for a (B, N) bit matrix through the tensor-core forward."""
+    return TensorCoreForward(params, fmt, device)(bits)
+
+
 # ---------------------------------------------------------------------------
 # delta-distribution studies (rbm.py:429-492): delta(x) = log p_fmt - log p_f64
 # evaluated on the device over the full enumeration; summaries on the host.

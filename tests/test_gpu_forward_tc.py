@@ -1,0 +1,107 @@
+"""Tensor-core (tcgen05) batched forward, mpv_forward_tc, against the oracle's
+f64 forward of the same rounded parameters (ref: rbm.py:130-150 _fast_forward,
+rbm.py:91-101 round_parameters; oracle/c/oracle_port.c f64_row).
+
+The GEMM products are exact (x in {0,1}, f16/bf16 weights) and the kernel
+accumulates theta and the log-cosh sum in f32, so the tolerance is the
+north star's f32 bar: log psi within 1e-5 relative (floor 1)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import port
+from paper_2601_20782_b200 import rbm
+from paper_2601_20782_b200.precision import BF16, F16, F32
+from paper_2601_20782_b200.rng import derive_key
+
+pytestmark = pytest.mark.gpu
+
+CASES = [  # (N, alpha, scale, B)
+    (1, 1, 0.5, 5),
+    (12, 2, 0.4, 300),
+    (37, 3, 0.3, 1000),      # M = 111: padded hidden columns
+    (100, 2, 0.05, 5000),    # configs[1] shape
+    (100, 4, 0.05, 2000),    # M = 400: two hidden chunks, B re-staged per chunk
+    (256, 1, 0.05, 700),     # Kp = 256: chunk size capped by shared memory
+    (333, 1, 0.03, 129),     # odd N across words, one full tile + 1
+]
+
+
+def _bits(B, N, seed):
+    return np.random.default_rng(seed).integers(0, 2, size=(B, N), dtype=np.uint8)
+
+
+def _oracle(params, fmt, bits):
+    snap = rbm.round_parameters(params, fmt)
+    _, re, im = port.f64_forward(port.Params(snap.a, snap.b, snap.w), bits)
+    return re, im
+
+
+def _conditioning(params, fmt, bits):
+    """sum_i |tanh theta_i| |theta_i|: the change of log psi under a relative
+    perturbation of every theta (log|cosh| is ill-conditioned near the zeros of
+    cosh, where f32 theta alone moves the f64 answer)."""
+    snap = rbm.round_parameters(params, fmt)
+    theta = snap.b[None, :] + bits.astype(np.float64) @ snap.w.T
+    return np.sum(np.abs(np.tanh(theta)) * np.abs(theta), axis=1)
+
+
+@pytest.mark.parametrize("fmt", [F16, BF16], ids=["f16", "bf16"])
+@pytest.mark.parametrize("N,alpha,scale,B", CASES)
+def test_forward_tc_matches_f64_of_rounded(fmt, N, alpha, scale, B):
+    params = rbm.random_parameters(N, alpha, derive_key(N * 7 + alpha, "tc"), scale)
+    bits = _bits(B, N, N + B)
+    tc = rbm.TensorCoreForward(params, fmt)
+    got = tc(bits)
+    re, im = _oracle(params, fmt, bits)
+    # 1e-5 relative (floor 1) plus the f32-theta conditioning term (K*2^-24 ~ 1e-6 per unit)
+    cond = 1e-6 * _conditioning(params, fmt, bits)
+    tol_re = 1e-5 * np.maximum(1.0, np.abs(re)) + cond
+    tol_im = 1e-5 * np.maximum(1.0, np.abs(im)) + cond
+    assert np.all(np.abs(got.real - re) <= tol_re), np.max(np.abs(got.real - re) / tol_re)
+    assert np.all(np.abs(got.imag - im) <= tol_im), np.max(np.abs(got.imag - im) / tol_im)
+    # log p only (the epilogue without the phase: ex2, cos 2v, lg2 per hidden unit)
+    lp = torch.empty(B, dtype=torch.float64, device=tc.device)
+    tc.forward_packed(rbm.device_pack(bits, tc.device), out_lp=lp)
+    lp = lp.cpu().numpy()
+    tol_lp = 2.0 * tol_re
+    assert np.all(np.abs(lp - 2.0 * re) <= tol_lp), np.max(np.abs(lp - 2.0 * re) / tol_lp)
+
+
+def test_forward_tc_large_theta_and_log_prob():
+    """|Re theta| up to ~30 (t = exp(-2u) underflow side) and out_lp = 2 Re log psi."""
+    N, B = 64, 512
+    params = rbm.random_parameters(N, 2, derive_key(3, "tc-big"), 1.0)
+    bits = _bits(B, N, 11)
+    tc = rbm.TensorCoreForward(params, F16)
+    packed = rbm.device_pack(bits, tc.device)
+    lp, re, im = tc.forward_packed(packed)
+    want_re, want_im = _oracle(params, F16, bits)
+    assert np.allclose(re.cpu().numpy(), want_re, rtol=1e-5, atol=1e-5)
+    assert np.array_equal(lp.cpu().numpy(), 2.0 * re.cpu().numpy())
+
+
+def test_forward_tc_deterministic_across_grids():
+    """Each row's sums run in a fixed order: the grid size does not change a bit."""
+    N, B = 100, 3000
+    params = rbm.random_parameters(N, 2, derive_key(5, "tc-det"), 0.1)
+    tc = rbm.TensorCoreForward(params, BF16)
+    packed = rbm.device_pack(_bits(B, N, 7), tc.device)
+    a = [t.cpu().numpy() for t in tc.forward_packed(packed)]
+    b = [t.cpu().numpy() for t in tc.forward_packed(packed, max_ctas=3)]
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    lp = torch.empty(B, dtype=torch.float64, device=tc.device)
+    tc.forward_packed(packed, out_lp=lp)
+    lp2 = torch.empty_like(lp)
+    tc.forward_packed(packed, out_lp=lp2, max_ctas=5)
+    assert np.array_equal(lp.cpu().numpy(), lp2.cpu().numpy())
+
+
+def test_forward_tc_rejects_other_formats_and_empty_batch():
+    params = rbm.random_parameters(10, 1, derive_key(1, "tc-x"), 0.1)
+    with pytest.raises(ValueError):
+        rbm.TensorCoreForward(params, F32)
+    tc = rbm.TensorCoreForward(params, F16)
+    out = tc(np.zeros((0, 10), dtype=np.uint8))
+    assert out.shape == (0,)
