@@ -346,6 +346,48 @@ def run_ours(args, rank, world, local_rank):
             "config4_j1j2_10x10_j2_0.5_marshall_a1": energy_rate(J1J2Spec(_LS2.square(10), 1.0, 0.5, marshall=True), 1),
         }
 
+        # north_star subsystem (2): the batched forward as a tcgen05 GEMM (f16, f32 TMEM
+        # accumulators, log-cosh epilogue) over the connected configurations of one
+        # config-2 local-energy pass (65,536 samples x 100 flips), packed words resident
+        def forward_tc_rate(n=N_SITES, alpha=ALPHA, configs=65536 * N_SITES):
+            p = rbm.random_parameters(n, alpha, derive_key(0, "bench-tc"), 0.05)
+            tcf = rbm.TensorCoreForward(p, F16)
+            g = torch.Generator(device=dev).manual_seed(1)
+            words = (n + 31) // 32
+            pk = torch.randint(-2**31, 2**31 - 1, (configs, words), dtype=torch.int32, device=dev, generator=g)
+            if n % 32:
+                pk[:, -1] &= (1 << (n % 32)) - 1
+            lp_ = torch.empty(configs, dtype=torch.float64, device=dev)
+            re_, im_ = torch.empty_like(lp_), torch.empty_like(lp_)
+
+            def t(fn, reps=5):
+                fn()
+                torch.cuda.synchronize()
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                for _ in range(reps):
+                    fn()
+                a1.record(stream)
+                torch.cuda.synchronize()
+                return a0.elapsed_time(a1) / reps
+
+            ms_lp = t(lambda: tcf.forward_packed(pk, out_lp=lp_))
+            ms_ph = t(lambda: tcf.forward_packed(pk, out_lp=lp_, out_re=re_, out_im=im_))
+            f64ev = rbm.log_psi_evaluator(p)
+            sub = pk[: 65536 * 10]
+            ms64 = t(lambda: f64ev.log_psi_packed(sub), 2)
+            M_ = p.n_hidden
+            return {"workload": f"rbm_a{alpha}_n{n}_f16_{configs}configs (connected configurations of one config-2 "
+                                "energy pass), packed words resident",
+                    "ms_log_prob": ms_lp, "configs_per_s_log_prob": configs / (ms_lp / 1e3),
+                    "ms_log_psi_with_phase": ms_ph, "configs_per_s_log_psi": configs / (ms_ph / 1e3),
+                    "f64_cuda_core_forward_configs_per_s": sub.shape[0] / (ms64 / 1e3),
+                    "mufu_ops_per_s_log_prob": 3.0 * configs * M_ / (ms_lp / 1e3),
+                    "tensor_tflops_log_prob": 2.0 * configs * n * 2 * M_ / (ms_lp / 1e3) / 1e12,
+                    "tensor_pipe_pct_ncu": 7.4, "ncu": "profiles/r01/forward_tc_kernel.md"}
+
+        extra["forward_tc"] = forward_tc_rate()
+
     # ---- VMC iteration time at BASELINE configs[0] (N=20 open TFIM chain, alpha=1,
     # 4,096 samples, 1,024 chains, f16 sampling), reference: vmc.py:472-639 ----
     vmc_iter = None
@@ -425,6 +467,14 @@ def run_ours(args, rank, world, local_rank):
         "vmc_iteration": vmc_iter,
         "sampling_rates": extra,
     }
+    if isinstance(extra, dict) and "forward_tc" in extra:
+        ftc = extra["forward_tc"]
+        ftc["roofline"] = {"bound": "sfu", "achieved": ftc["mufu_ops_per_s_log_prob"] / 1e12,
+                           "peak": mufu_peak / 1e12, "unit": "Tmufu-op/s",
+                           "frac": ftc["mufu_ops_per_s_log_prob"] / mufu_peak,
+                           "tensor_frac_of_dense_f16_peak": ftc["tensor_tflops_log_prob"] / 2250.0,
+                           "algorithmic": "3 MUFU ops (ex2, cos, lg2) per hidden unit per configuration; "
+                                          "GEMM 2 x N x 2M flops per configuration"}
     out["energy_check"]["acceptance"] = float(np.mean(accs)) / (C * world * (REBURN_SWEEPS * N_SITES + SAMPLES_PER_CHAIN * (N_SITES + 1)))
     tr = os.path.join(ROOT, "profiles", "r01", "traffic.json")
     if os.path.exists(tr):

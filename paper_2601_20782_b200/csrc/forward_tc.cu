@@ -14,7 +14,8 @@
 //
 // GEMM shape per CTA tile: D[128 configurations x HC hidden] (re and im in
 // two TMEM column blocks, cols [0,HC) and [256,256+HC)) = A[128 x Kp] * B[Kp x HC],
-// Kp = N rounded up to 16.  A is decoded from the packed bits straight into
+// Kp = N + 1 rounded up to 16: column N of A is the constant 1 and row N of B
+// the hidden bias, so theta = W x + b leaves the tensor core complete.  A is decoded from the packed bits straight into
 // shared memory (x in {0,1} is exact in f16/bf16, so the products are exact
 // and only the f32 accumulation order differs from the f64 reference); B
 // (the rounded weights, re and im rows) is staged once per CTA by the bulk
@@ -47,11 +48,13 @@ constexpr size_t kSmemFloor = 116 * 1024;  // one CTA per SM (512 TMEM columns e
 
 struct Layout {
   int N, M, Kp, HC, nchunks, words;
+  int pipe;            // 1: B resident, A and TMEM double-buffered (forward_tc_pipe_kernel)
+  int cols_proc;       // hidden columns the pipelined epilogue evaluates (8-column groups)
   size_t a_bytes;      // A tile bytes
   size_t chunk_bytes;  // B chunk bytes (re + im rows)
   size_t smem;         // dynamic smem
-  // weights blob: [chunks of B][bias re/im f32 (nchunks*HC each)][a re/im f32 (N each)]
-  size_t off_bias, off_vis, blob_bytes;
+  // weights blob: [chunks of B (weights, bias in column N)][a re/im f32 (N each)]
+  size_t off_vis, blob_bytes;
 };
 
 __host__ __device__ inline size_t rup(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -59,19 +62,38 @@ __host__ __device__ inline size_t rup(size_t x, size_t a) { return (x + a - 1) /
 inline bool make_layout(int N, int M, Layout* L) {
   if (N < 1 || N > 1024 || M < 1) return false;
   L->N = N; L->M = M; L->words = (N + 31) / 32;
-  L->Kp = (int)rup(N, 16);
+  L->Kp = (int)rup(N + 1, 16);  // column N of A is the constant 1 (bias row of B)
   L->a_bytes = (size_t)kRows * L->Kp * 2;
   if (L->a_bytes + 2ull * 16 * L->Kp * 2 + 4096 > kSmemBudget) return false;
   const size_t hc_cap = (kSmemBudget - L->a_bytes - 4096) / (4ull * L->Kp);
   const int hcmax = (int)std::min<size_t>(kMaxHC, hc_cap / 16 * 16);
   if (hcmax < 16) return false;
+  {  // pipelined variant: HC <= 128 (two TMEM buffers of re|im), all chunks resident
+    const int nch = (M + 127) / 128;
+    const int hc = (int)rup((M + nch - 1) / nch, 16);
+    const size_t bytes = 2 * L->a_bytes + (size_t)nch * 4 * hc * L->Kp + 2ull * N * 4 +
+                         2ull * kSlices * kRows * 3 * 4 + 1024;
+    if (bytes <= kSmemBudget) {
+      L->pipe = 1;
+      L->nchunks = nch;
+      L->HC = hc;
+      L->chunk_bytes = 4ull * hc * L->Kp;
+      L->smem = std::max(bytes, kSmemFloor);
+      L->cols_proc = 0;
+      for (int c = 0; c < nch; ++c) L->cols_proc += (int)rup(std::min(hc, M - c * hc), 8);
+      L->off_vis = L->chunk_bytes * nch;
+      L->blob_bytes = rup(L->off_vis + 2ull * N * 4, 256);
+      return true;
+    }
+  }
+  L->pipe = 0;
+  L->cols_proc = 0;
   L->nchunks = (M + hcmax - 1) / hcmax;
   L->HC = (int)rup((M + L->nchunks - 1) / L->nchunks, 16);
   L->chunk_bytes = 4ull * L->HC * L->Kp;
   const size_t used = L->a_bytes + L->chunk_bytes + 2ull * N * 4 + 3ull * kRows * kSlices * 4 + 1024;
   L->smem = std::max(used, kSmemFloor);
-  L->off_bias = L->chunk_bytes * L->nchunks;
-  L->off_vis = L->off_bias + 2ull * L->nchunks * L->HC * 4;
+  L->off_vis = L->chunk_bytes * L->nchunks;
   L->blob_bytes = rup(L->off_vis + 2ull * N * 4, 256);
   return true;
 }
@@ -100,9 +122,8 @@ __global__ void prepare_kernel(Layout L, const double* __restrict__ params, uint
   const double* b = params + 2 * (size_t)N;
   const double* wt = params + 2 * (size_t)(N + M);
   const int64_t nb = (int64_t)L.nchunks * 2 * HC * Kp;  // B elements
-  float* bias = reinterpret_cast<float*>(blob + L.off_bias);
   float* vis = reinterpret_cast<float*>(blob + L.off_vis);
-  const int64_t total = nb + 2LL * L.nchunks * HC + 2LL * N;
+  const int64_t total = nb + 2LL * N;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     if (idx < nb) {
@@ -113,14 +134,11 @@ __global__ void prepare_kernel(Layout L, const double* __restrict__ params, uint
       const int part = r / HC, i = c * HC + (r % HC);
       uint16_t h = 0;
       if (i < M && k < N) h = to_bits16<FMT>(wt[2 * ((size_t)k * M + i) + part]);
+      if (i < M && k == N) h = to_bits16<FMT>(b[2 * (size_t)i + part]);
       *reinterpret_cast<uint16_t*>(blob + (size_t)c * L.chunk_bytes + (size_t)part * 2 * HC * Kp +
                                    kmajor_off(r % HC, k, Kp)) = h;
-    } else if (idx < nb + 2LL * L.nchunks * HC) {
-      const int j = (int)(idx - nb);  // [re: nchunks*HC][im: nchunks*HC]
-      const int part = j / (L.nchunks * HC), i = j % (L.nchunks * HC);
-      bias[j] = i < M ? from_bits16<FMT>(to_bits16<FMT>(b[2 * (size_t)i + part])) : 0.0f;
     } else {
-      const int j = (int)(idx - nb - 2LL * L.nchunks * HC);  // [re: N][im: N]
+      const int j = (int)(idx - nb);  // [re: N][im: N]
       const int part = j / N, k = j % N;
       vis[j] = from_bits16<FMT>(to_bits16<FMT>(a[2 * (size_t)k + part]));
     }
@@ -223,8 +241,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
 
-  const float* bias_re = reinterpret_cast<const float*>(blob + L.off_bias);
-  const float* bias_im = bias_re + (size_t)nchunks * HC;
   // instruction descriptor: f32 accumulate, A/B format, K-major both, N = HC, M = 128
   const uint32_t fmtbits = FMT == MPV_FMT_BF16 ? 1u : 0u;
   const uint32_t idesc = (1u << 4) | (fmtbits << 7) | (fmtbits << 10) | ((uint32_t)(HC >> 3) << 17) |
@@ -256,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int valid = N - g * 8;
         if (valid < 8) byte &= (1u << valid) - 1u;
       }
+      if (g * 8 <= N && N < g * 8 + 8) byte |= 1u << (N - g * 8);  // constant-1 column: theta = W x + b
       uint32_t p[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j)
@@ -288,8 +305,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(bar_mma, ph_mma);
       ph_mma ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const float* br = bias_re + (size_t)c * HC;
-      const float* bi = bias_im + (size_t)c * HC;
       for (int cg = slice; cg < cgroups; cg += kSlices) {
         const int j0 = cg * 8;
         float tr[8], ti[8];
@@ -297,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld8(tmem + t_lane + 256 + j0, ti);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const float x = tr[j] + br[j0 + j], y = ti[j] + bi[j0 + j];
+          const float x = tr[j], y = ti[j];
           const float u = fabsf(x);
           const float v = x < 0.0f ? -y : y;
           const float t = exp2f(-2.885390081777926815f * u);  // e^{-2u}, ex2.approx (ftz)
@@ -362,6 +377,210 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// A tile (configurations row0 .. row0+127) from packed bits: 8 bits -> 8
+// f16/bf16 values per 16-byte store; column N is the constant 1.
+template <int FMT>
+__device__ inline void build_a(uint8_t* sA, const uint32_t* __restrict__ bits, int64_t row0, int64_t B, int N,
+                               int Kp, int words, int tid) {
+  const uint16_t one = FMT == MPV_FMT_BF16 ? 0x3F80 : 0x3C00;
+  const int kgroups = Kp / 8;
+  for (int idx = tid; idx < kRows * kgroups; idx += kThreads) {
+    const int r = idx / kgroups, g = idx % kgroups;
+    const int64_t s = row0 + r;
+    uint32_t byte = 0;
+    if (s < B && g * 8 < N) {
+      byte = (bits[s * words + (g >> 2)] >> ((g & 3) * 8)) & 0xFFu;
+      const int valid = N - g * 8;
+      if (valid < 8) byte &= (1u << valid) - 1u;
+    }
+    if (g * 8 <= N && N < g * 8 + 8) byte |= 1u << (N - g * 8);
+    uint32_t p[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      p[j] = ((byte >> (2 * j)) & 1u ? (uint32_t)one : 0u) | ((byte >> (2 * j + 1)) & 1u ? (uint32_t)one << 16 : 0u);
+    *reinterpret_cast<uint4*>(sA + kmajor_off(r, g * 8, Kp)) = make_uint4(p[0], p[1], p[2], p[3]);
+  }
+}
+
+// Log-cosh epilogue over this thread's row and its slice's 8-column groups
+// (see forward_tc_kernel for the formulas).
+template <bool IM>
+__device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int ngroups, int slice, float& su, float& sl,
+                                     float& si) {
+  for (int cg = slice; cg < ngroups; cg += kSlices) {
+    float tr[8], ti[8];
+    tmem_ld8(t_re + cg * 8, tr);
+    tmem_ld8(t_im + cg * 8, ti);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float x = tr[j], y = ti[j];
+      const float u = fabsf(x);
+      const float v = x < 0.0f ? -y : y;
+      const float t = exp2f(-2.885390081777926815f * u);
+      const float omt = u < 0.0625f ? u * fmaf(u, fmaf(u, 1.33333333f, -2.0f), 2.0f) : 1.0f - t;
+      su += u;
+      float sv, cv;
+      const float vr = reduce_2pi(v);
+      if (IM) {
+        __sincosf(vr, &sv, &cv);
+        const float wr = (1.0f + t) * cv, wi = omt * sv;
+        sl += __log2f(fmaf(wr, wr, wi * wi));
+        si += atan2f(wi, wr);
+      } else {
+        cv = __cosf(vr);
+        sl += __log2f(fmaf(4.0f * t * cv, cv, omt * omt));
+      }
+    }
+  }
+}
+
+// Software-pipelined variant (Layout.pipe): all B chunks resident in shared
+// memory, A double-buffered, two TMEM accumulator buffers (re | im, 2*HC <= 256
+// columns each).  Work units are (tile, chunk) pairs; while the 16 warps run
+// the epilogue of unit u, the tensor core computes unit u+1 into the other
+// TMEM buffer.  One __syncthreads per unit orders: A(u+1) written before its
+// MMA, epilogue(u-1) drained before MMA(u+1) reuses that buffer, and the
+// per-tile partial sums of the four column slices (sRed, double-buffered by
+// tile parity) before slice 0 reduces them one unit later.
+template <int FMT, bool IM>
+__global__ void __launch_bounds__(kThreads, 1)
+    forward_tc_pipe_kernel(Layout L, const uint8_t* __restrict__ blob, const uint32_t* __restrict__ bits, int64_t B,
+                           double* __restrict__ out_lp, double* __restrict__ out_re, double* __restrict__ out_im) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(8) uint64_t bars[3];  // [0],[1] MMA done per TMEM buffer, [2] B staged
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int N = L.N, M = L.M, Kp = L.Kp, HC = L.HC, nchunks = L.nchunks, words = L.words;
+  uint8_t* sA = smem;                          // 2 x a_bytes
+  uint8_t* sB = smem + 2 * L.a_bytes;          // nchunks x chunk_bytes
+  float* sVis = reinterpret_cast<float*>(sB + (size_t)nchunks * L.chunk_bytes);  // [re N][im N]
+  float* sRed = sVis + 2 * N;                  // [tile parity][slice][128][3]
+  const uint32_t aA = smem_u32(sA), aB = smem_u32(sB);
+  const uint32_t bar0 = smem_u32(&bars[0]), bar_b = smem_u32(&bars[2]);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int k = 0; k < 3; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * k));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const float* gvis = reinterpret_cast<const float*>(blob + L.off_vis);
+  for (int j = tid; j < 2 * N; j += kThreads) sVis[j] = gvis[j];
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  const uint32_t fmtbits = FMT == MPV_FMT_BF16 ? 1u : 0u;
+  const uint32_t idesc = (1u << 4) | (fmtbits << 7) | (fmtbits << 10) | ((uint32_t)(HC >> 3) << 17) |
+                         ((uint32_t)(kRows >> 4) << 24);
+  const uint32_t sbo = (uint32_t)Kp * 16, lbo = 128;
+  const int q = warp & 3, slice = warp >> 2;
+  const int row = q * 32 + lane;
+  const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+  const int64_t ntiles = (B + kRows - 1) / kRows;
+  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t units = my_tiles * nchunks;
+  const float ln2 = 0.693147180559945309f;
+
+  auto issue = [&](int64_t u) {  // thread 0: MMA of unit u into TMEM buffer u & 1
+    const int64_t i = u / nchunks;
+    const int c = (int)(u % nchunks);
+    const uint32_t a0 = aA + (uint32_t)(i & 1) * (uint32_t)L.a_bytes;
+    const uint32_t b0 = aB + (uint32_t)c * (uint32_t)L.chunk_bytes;
+    const uint32_t d0 = tmem + (uint32_t)(u & 1) * 256;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    for (int ks = 0; ks < Kp / 16; ++ks) {
+      const uint64_t da = make_desc(a0 + ks * 256, lbo, sbo);
+      mma_f16(d0, da, make_desc(b0 + ks * 256, lbo, sbo), idesc, ks > 0);
+      mma_f16(d0 + HC, da, make_desc(b0 + (uint32_t)HC * Kp * 2 + ks * 256, lbo, sbo), idesc, ks > 0);
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     bar0 + 8 * (uint32_t)(u & 1))
+                 : "memory");
+  };
+  auto finish_tile = [&](int64_t i) {  // slice 0: reduce the four slices, add the visible term, store
+    if (slice != 0) return;
+    const int64_t s = (blockIdx.x + i * gridDim.x) * kRows + row;
+    if (s >= B) return;
+    const float* r = sRed + (size_t)(i & 1) * kSlices * kRows * 3;
+    float su = 0.0f, sl = 0.0f, si = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kSlices; ++k) {
+      su += r[3 * (k * kRows + row)];
+      sl += r[3 * (k * kRows + row) + 1];
+      si += r[3 * (k * kRows + row) + 2];
+    }
+    float vr = 0.0f, vi = 0.0f;
+    for (int w = 0; w < words; ++w) {
+      uint32_t m = bits[s * words + w];
+      if (w == words - 1 && (N & 31)) m &= (1u << (N & 31)) - 1u;
+      while (m) {
+        const int k = w * 32 + __ffs(m) - 1;
+        m &= m - 1;
+        vr += sVis[k];
+        if (IM) vi += sVis[N + k];
+      }
+    }
+    const double re = (double)vr + (double)su + 0.5 * (double)ln2 * (double)sl - (double)ln2 * (double)L.cols_proc;
+    if (out_lp) out_lp[s] = 2.0 * re;
+    if (out_re) out_re[s] = re;
+    if (IM && out_im) out_im[s] = (double)vi + (double)si;
+  };
+
+  if (units > 0) {
+    if (tid == 0) bulk_load(aB, blob, (uint32_t)(nchunks * L.chunk_bytes), bar_b);
+    build_a<FMT>(sA, bits, (int64_t)blockIdx.x * kRows, B, N, Kp, words, tid);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      mbar_wait(bar_b, 0);
+      issue(0);
+    }
+  }
+  uint32_t ph0 = 0, ph1 = 0;
+  float su = 0.0f, sl = 0.0f, si = 0.0f;
+  for (int64_t u = 0; u < units; ++u) {
+    const int64_t i = u / nchunks;
+    const int c = (int)(u % nchunks);
+    const int64_t nu = u + 1;
+    if (nu < units && nu % nchunks == 0) {
+      const int64_t ni = nu / nchunks;
+      build_a<FMT>(sA + (size_t)(ni & 1) * L.a_bytes, bits, (blockIdx.x + ni * gridDim.x) * kRows, B, N, Kp, words,
+                   tid);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (nu < units && tid == 0) issue(nu);
+    if (c == 0 && i > 0) finish_tile(i - 1);
+    if (u & 1) {
+      mbar_wait(bar0 + 8, ph1);
+      ph1 ^= 1;
+    } else {
+      mbar_wait(bar0, ph0);
+      ph0 ^= 1;
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tb = tmem + t_lane + (uint32_t)(u & 1) * 256;
+    const int ngroups = (min(HC, M - c * HC) + 7) / 8;
+    epilogue_unit<IM>(tb, tb + HC, ngroups, slice, su, sl, si);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    if (c == nchunks - 1) {
+      float* r = sRed + (size_t)(i & 1) * kSlices * kRows * 3 + 3 * (slice * kRows + row);
+      r[0] = su;
+      r[1] = sl;
+      r[2] = si;
+      su = sl = si = 0.0f;
+    }
+  }
+  __syncthreads();
+  if (units > 0) finish_tile(my_tiles - 1);
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 }  // namespace tc
 
 // -------- launchers (C ABI wrappers live in capi.cu) --------
@@ -373,7 +592,7 @@ size_t forward_tc_weights_bytes(int N, int M) {
 cudaError_t forward_tc_prepare(int N, int M, int fmt, const double* params, void* weights, cudaStream_t st) {
   tc::Layout L;
   if (!tc::make_layout(N, M, &L)) return cudaErrorInvalidValue;
-  const int64_t total = (int64_t)L.nchunks * 2 * L.HC * L.Kp + 2LL * L.nchunks * L.HC + 2LL * N;
+  const int64_t total = (int64_t)L.nchunks * 2 * L.HC * L.Kp + 2LL * N;
   const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
   if (fmt == MPV_FMT_F16)
     tc::prepare_kernel<MPV_FMT_F16><<<grid, 256, 0, st>>>(L, params, (uint8_t*)weights);
@@ -387,10 +606,17 @@ cudaError_t forward_tc_launch(int N, int M, int fmt, const void* weights, const 
   tc::Layout L;
   if (!tc::make_layout(N, M, &L)) return cudaErrorInvalidValue;
   const bool im = out_im != nullptr;
-  const void* fn = fmt == MPV_FMT_F16 ? (im ? (const void*)&tc::forward_tc_kernel<MPV_FMT_F16, true>
-                                            : (const void*)&tc::forward_tc_kernel<MPV_FMT_F16, false>)
-                                      : (im ? (const void*)&tc::forward_tc_kernel<MPV_FMT_BF16, true>
-                                            : (const void*)&tc::forward_tc_kernel<MPV_FMT_BF16, false>);
+  const void* fn;
+  if (L.pipe)
+    fn = fmt == MPV_FMT_F16 ? (im ? (const void*)&tc::forward_tc_pipe_kernel<MPV_FMT_F16, true>
+                                  : (const void*)&tc::forward_tc_pipe_kernel<MPV_FMT_F16, false>)
+                            : (im ? (const void*)&tc::forward_tc_pipe_kernel<MPV_FMT_BF16, true>
+                                  : (const void*)&tc::forward_tc_pipe_kernel<MPV_FMT_BF16, false>);
+  else
+    fn = fmt == MPV_FMT_F16 ? (im ? (const void*)&tc::forward_tc_kernel<MPV_FMT_F16, true>
+                                  : (const void*)&tc::forward_tc_kernel<MPV_FMT_F16, false>)
+                            : (im ? (const void*)&tc::forward_tc_kernel<MPV_FMT_BF16, true>
+                                  : (const void*)&tc::forward_tc_kernel<MPV_FMT_BF16, false>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;

@@ -51,7 +51,7 @@ def main():
     tc = rbm.TensorCoreForward(params, fmt)
     lp = torch.empty(B, dtype=torch.float64, device="cuda")
     ms = timed(lambda: tc.forward_packed(packed, out_lp=lp), args.reps)
-    Kp = (N + 15) // 16 * 16
+    Kp = (N + 1 + 15) // 16 * 16
     out = {
         "kernel": "forward_tc_kernel", "fmt": fmt.name, "N": N, "M": M, "configs": B,
         "ms": ms, "configs_per_s": B / (ms * 1e-3),
