@@ -47,7 +47,7 @@ constexpr size_t kSmemBudget = 200 * 1024;
 constexpr size_t kSmemFloor = 116 * 1024;  // one CTA per SM (512 TMEM columns each)
 
 struct Layout {
-  int N, M, Kp, HC, nchunks, words;
+  int N, M, Kp, HC, HCB, nchunks, words;  // HCB: B rows (MMA N) per re/im block
   int pipe;            // 1: B resident, A and TMEM double-buffered (forward_tc_pipe_kernel)
   int cols_proc;       // hidden columns the pipelined epilogue evaluates (8-column groups)
   size_t a_bytes;      // A tile bytes
@@ -68,19 +68,21 @@ inline bool make_layout(int N, int M, Layout* L) {
   const size_t hc_cap = (kSmemBudget - L->a_bytes - 4096) / (4ull * L->Kp);
   const int hcmax = (int)std::min<size_t>(kMaxHC, hc_cap / 16 * 16);
   if (hcmax < 16) return false;
-  {  // pipelined variant: HC <= 128 (two TMEM buffers of re|im), all chunks resident
-    const int nch = (M + 127) / 128;
+  {  // pipelined variant: HC <= 112 hidden + 16 rows (row HC = visible biases) per
+     // re/im block, two TMEM buffers of re|im (2 x 128 columns), all chunks resident
+    const int nch = (M + 111) / 112;
     const int hc = (int)rup((M + nch - 1) / nch, 16);
-    const size_t bytes = 2 * L->a_bytes + (size_t)nch * 4 * hc * L->Kp + 2ull * N * 4 +
-                         2ull * kSlices * kRows * 3 * 4 + 1024;
+    const size_t bytes = 2 * L->a_bytes + (size_t)nch * 4 * (hc + 16) * L->Kp + 2ull * N * 4 +
+                         2ull * kSlices * kRows * 3 * 4 + 2ull * kRows * 2 * 4 + 1024;
     if (bytes <= kSmemBudget) {
       L->pipe = 1;
       L->nchunks = nch;
       L->HC = hc;
-      L->chunk_bytes = 4ull * hc * L->Kp;
+      L->HCB = hc + 16;
+      L->chunk_bytes = 4ull * L->HCB * L->Kp;
       L->smem = std::max(bytes, kSmemFloor);
       L->cols_proc = 0;
-      for (int c = 0; c < nch; ++c) L->cols_proc += (int)rup(std::min(hc, M - c * hc), 8);
+      for (int c = 0; c < nch; ++c) L->cols_proc += (int)rup(std::min(hc, M - c * hc), 4);
       L->off_vis = L->chunk_bytes * nch;
       L->blob_bytes = rup(L->off_vis + 2ull * N * 4, 256);
       return true;
@@ -90,6 +92,7 @@ inline bool make_layout(int N, int M, Layout* L) {
   L->cols_proc = 0;
   L->nchunks = (M + hcmax - 1) / hcmax;
   L->HC = (int)rup((M + L->nchunks - 1) / L->nchunks, 16);
+  L->HCB = L->HC;
   L->chunk_bytes = 4ull * L->HC * L->Kp;
   const size_t used = L->a_bytes + L->chunk_bytes + 2ull * N * 4 + 3ull * kRows * kSlices * 4 + 1024;
   L->smem = std::max(used, kSmemFloor);
@@ -117,26 +120,30 @@ __device__ inline float from_bits16(uint16_t h) {
 // params = [a (N) | b (M) | w_t (N x M)] complex (re, im) f64, as mpv_snapshot_round.
 template <int FMT>
 __global__ void prepare_kernel(Layout L, const double* __restrict__ params, uint8_t* __restrict__ blob) {
-  const int N = L.N, M = L.M, HC = L.HC, Kp = L.Kp;
+  const int N = L.N, M = L.M, HC = L.HC, HCB = L.HCB, Kp = L.Kp;
   const double* a = params;
   const double* b = params + 2 * (size_t)N;
   const double* wt = params + 2 * (size_t)(N + M);
-  const int64_t nb = (int64_t)L.nchunks * 2 * HC * Kp;  // B elements
+  const int64_t nb = (int64_t)L.nchunks * 2 * HCB * Kp;  // B elements
   float* vis = reinterpret_cast<float*>(blob + L.off_vis);
   const int64_t total = nb + 2LL * N;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     if (idx < nb) {
-      const int64_t per_chunk = 2LL * HC * Kp;
+      const int64_t per_chunk = 2LL * HCB * Kp;
       const int c = (int)(idx / per_chunk);
       const int rem = (int)(idx % per_chunk);
-      const int r = rem / Kp, k = rem % Kp;  // r in [0, 2HC): re rows then im rows
-      const int part = r / HC, i = c * HC + (r % HC);
+      const int r = rem / Kp, k = rem % Kp;  // r in [0, 2HCB): re rows then im rows
+      const int part = r / HCB, rr = r % HCB, i = c * HC + rr;
       uint16_t h = 0;
-      if (i < M && k < N) h = to_bits16<FMT>(wt[2 * ((size_t)k * M + i) + part]);
-      if (i < M && k == N) h = to_bits16<FMT>(b[2 * (size_t)i + part]);
-      *reinterpret_cast<uint16_t*>(blob + (size_t)c * L.chunk_bytes + (size_t)part * 2 * HC * Kp +
-                                   kmajor_off(r % HC, k, Kp)) = h;
+      if (rr < HC) {
+        if (i < M && k < N) h = to_bits16<FMT>(wt[2 * ((size_t)k * M + i) + part]);
+        if (i < M && k == N) h = to_bits16<FMT>(b[2 * (size_t)i + part]);
+      } else if (rr == HC && c == 0 && k < N) {  // pipelined layout: a . x from the tensor core
+        h = to_bits16<FMT>(a[2 * (size_t)k + part]);
+      }
+      *reinterpret_cast<uint16_t*>(blob + (size_t)c * L.chunk_bytes + (size_t)part * 2 * HCB * Kp +
+                                   kmajor_off(rr, k, Kp)) = h;
     } else {
       const int j = (int)(idx - nb);  // [re: N][im: N]
       const int part = j / N, k = j % N;
@@ -404,15 +411,42 @@ __device__ inline void build_a(uint8_t* sA, const uint32_t* __restrict__ bits, i
 
 // Log-cosh epilogue over this thread's row and its slice's 8-column groups
 // (see forward_tc_kernel for the formulas).
-template <bool IM>
-__device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int ngroups, int slice, float& su, float& sl,
-                                     float& si) {
-  for (int cg = slice; cg < ngroups; cg += kSlices) {
-    float tr[8], ti[8];
-    tmem_ld8(t_re + cg * 8, tr);
-    tmem_ld8(t_im + cg * 8, ti);
+__device__ inline void tmem_ld4(uint32_t taddr, float* v) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < 4; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+__device__ inline void tmem_ld4_pair(uint32_t a0, uint32_t a1, float* v0, float* v1) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a0));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(a1));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    v0[j] = __uint_as_float(r[j]);
+    v1[j] = __uint_as_float(r[4 + j]);
+  }
+}
+
+// 4-column groups, group j to slice (j - rot) mod 4: the rotation (tile index +
+// chunk) evens out the remainder groups across slices over consecutive units.
+template <bool IM>
+__device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int nquads, int slice, int rot, float& su,
+                                     float& sl, float& si) {
+  for (int cq = (slice + rot) & (kSlices - 1); cq < nquads; cq += kSlices) {
+    float tr[4], ti[4];
+    tmem_ld4_pair(t_re + cq * 4, t_im + cq * 4, tr, ti);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
       const float x = tr[j], y = ti[j];
       const float u = fabsf(x);
       const float v = x < 0.0f ? -y : y;
@@ -451,11 +485,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t bars[3];  // [0],[1] MMA done per TMEM buffer, [2] B staged
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int N = L.N, M = L.M, Kp = L.Kp, HC = L.HC, nchunks = L.nchunks, words = L.words;
+  const int N = L.N, M = L.M, Kp = L.Kp, HC = L.HC, HCB = L.HCB, nchunks = L.nchunks;
   uint8_t* sA = smem;                          // 2 x a_bytes
   uint8_t* sB = smem + 2 * L.a_bytes;          // nchunks x chunk_bytes
   float* sVis = reinterpret_cast<float*>(sB + (size_t)nchunks * L.chunk_bytes);  // [re N][im N]
   float* sRed = sVis + 2 * N;                  // [tile parity][slice][128][3]
+  float* sAx = sRed + 2 * kSlices * kRows * 3; // [tile parity][128][2]: a . x (re, im)
   const uint32_t aA = smem_u32(sA), aB = smem_u32(sB);
   const uint32_t bar0 = smem_u32(&bars[0]), bar_b = smem_u32(&bars[2]);
 
@@ -475,11 +510,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = tmem_slot;
 
   const uint32_t fmtbits = FMT == MPV_FMT_BF16 ? 1u : 0u;
-  const uint32_t idesc = (1u << 4) | (fmtbits << 7) | (fmtbits << 10) | ((uint32_t)(HC >> 3) << 17) |
+  const uint32_t idesc = (1u << 4) | (fmtbits << 7) | (fmtbits << 10) | ((uint32_t)(HCB >> 3) << 17) |
                          ((uint32_t)(kRows >> 4) << 24);
   const uint32_t sbo = (uint32_t)Kp * 16, lbo = 128;
   const int q = warp & 3, slice = warp >> 2;
   const int row = q * 32 + lane;
+  const int words = L.words;
   const uint32_t t_lane = (uint32_t)(q * 32) << 16;
   const int64_t ntiles = (B + kRows - 1) / kRows;
   const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -496,13 +532,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int ks = 0; ks < Kp / 16; ++ks) {
       const uint64_t da = make_desc(a0 + ks * 256, lbo, sbo);
       mma_f16(d0, da, make_desc(b0 + ks * 256, lbo, sbo), idesc, ks > 0);
-      mma_f16(d0 + HC, da, make_desc(b0 + (uint32_t)HC * Kp * 2 + ks * 256, lbo, sbo), idesc, ks > 0);
+      mma_f16(d0 + HCB, da, make_desc(b0 + (uint32_t)HCB * Kp * 2 + ks * 256, lbo, sbo), idesc, ks > 0);
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      bar0 + 8 * (uint32_t)(u & 1))
                  : "memory");
   };
-  auto finish_tile = [&](int64_t i) {  // slice 0: reduce the four slices, add the visible term, store
+  auto finish_tile = [&](int64_t i) {  // slice 0: reduce the four slices (+ a . x), store
     if (slice != 0) return;
     const int64_t s = (blockIdx.x + i * gridDim.x) * kRows + row;
     if (s >= B) return;
@@ -514,17 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       sl += r[3 * (k * kRows + row) + 1];
       si += r[3 * (k * kRows + row) + 2];
     }
-    float vr = 0.0f, vi = 0.0f;
-    for (int w = 0; w < words; ++w) {
-      uint32_t m = bits[s * words + w];
-      if (w == words - 1 && (N & 31)) m &= (1u << (N & 31)) - 1u;
-      while (m) {
-        const int k = w * 32 + __ffs(m) - 1;
-        m &= m - 1;
-        vr += sVis[k];
-        if (IM) vi += sVis[N + k];
-      }
-    }
+    const float vr = sAx[2 * ((i & 1) * kRows + row)], vi = sAx[2 * ((i & 1) * kRows + row) + 1];
     const double re = (double)vr + (double)su + 0.5 * (double)ln2 * (double)sl - (double)ln2 * (double)L.cols_proc;
     if (out_lp) out_lp[s] = 2.0 * re;
     if (out_re) out_re[s] = re;
@@ -555,6 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();
     if (nu < units && tid == 0) issue(nu);
+
     if (c == 0 && i > 0) finish_tile(i - 1);
     if (u & 1) {
       mbar_wait(bar0 + 8, ph1);
@@ -565,8 +592,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tb = tmem + t_lane + (uint32_t)(u & 1) * 256;
-    const int ngroups = (min(HC, M - c * HC) + 7) / 8;
-    epilogue_unit<IM>(tb, tb + HC, ngroups, slice, su, sl, si);
+    const int nquads = (min(HC, M - c * HC) + 3) / 4;
+    // rotation keyed by the global tile index: each row's summation order is grid-independent
+    const int rot = (int)((blockIdx.x + i * gridDim.x + c) & 3);
+    epilogue_unit<IM>(tb, tb + HCB, nquads, slice, rot, su, sl, si);
+    if (c == 0 && slice == 0) {  // column HC of chunk 0: the visible term a . x
+      float ar[4], ai[4];
+      tmem_ld4(tb + HC, ar);
+      tmem_ld4(tb + HCB + HC, ai);
+      sAx[2 * ((i & 1) * kRows + row)] = ar[0];
+      sAx[2 * ((i & 1) * kRows + row) + 1] = ai[0];
+    }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     if (c == nchunks - 1) {
       float* r = sRed + (size_t)(i & 1) * kSlices * kRows * 3 + 3 * (slice * kRows + row);
@@ -592,7 +628,7 @@ size_t forward_tc_weights_bytes(int N, int M) {
 cudaError_t forward_tc_prepare(int N, int M, int fmt, const double* params, void* weights, cudaStream_t st) {
   tc::Layout L;
   if (!tc::make_layout(N, M, &L)) return cudaErrorInvalidValue;
-  const int64_t total = (int64_t)L.nchunks * 2 * L.HC * L.Kp + 2LL * N;
+  const int64_t total = (int64_t)L.nchunks * 2 * L.HCB * L.Kp + 2LL * N;
   const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
   if (fmt == MPV_FMT_F16)
     tc::prepare_kernel<MPV_FMT_F16><<<grid, 256, 0, st>>>(L, params, (uint8_t*)weights);
