@@ -40,8 +40,10 @@ namespace mpv {
 namespace tc {
 
 constexpr int kRows = 128;     // MMA M (configurations per tile)
-constexpr int kThreads = 512;  // 16 warps: 4 TMEM lane quarters x 4 column slices
+constexpr int kThreads = 512;  // 16 epilogue warps: 4 TMEM lane quarters x 4 column slices
 constexpr int kSlices = kThreads / 128;
+constexpr int kProducers = 4;  // producer warps of the pipelined kernel (A build, MMA issue)
+constexpr int kRowsPerLane = kRows / (32 * kProducers);
 constexpr int kMaxHC = 256;    // MMA N limit / TMEM block
 constexpr size_t kSmemBudget = 200 * 1024;
 constexpr size_t kSmemFloor = 116 * 1024;  // one CTA per SM (512 TMEM columns each)
@@ -72,7 +74,7 @@ inline bool make_layout(int N, int M, Layout* L) {
      // re/im block, two TMEM buffers of re|im (2 x 128 columns), all chunks resident
     const int nch = (M + 111) / 112;
     const int hc = (int)rup((M + nch - 1) / nch, 16);
-    const size_t bytes = 2 * L->a_bytes + (size_t)nch * 4 * (hc + 16) * L->Kp + 2ull * N * 4 +
+    const size_t bytes = 2 * L->a_bytes + (size_t)nch * 4 * (hc + 16) * L->Kp +
                          2ull * kSlices * kRows * 3 * 4 + 2ull * kRows * 2 * 4 + 1024;
     if (bytes <= kSmemBudget) {
       L->pipe = 1;
@@ -409,6 +411,49 @@ __device__ inline void build_a(uint8_t* sA, const uint32_t* __restrict__ bits, i
   }
 }
 
+// A tile built by the producer warps of the pipelined kernel: lane l of
+// producer warp pw owns rows l + 32 (pw + kProducers rr); their packed words are loaded first (up to 4 per
+// row in registers), then expanded into 16-byte stores (each 8-lane group
+// writes one 128-byte core matrix: conflict-free).
+template <int FMT>
+__device__ inline void build_a_warp(uint8_t* sA, const uint32_t* __restrict__ bits, int64_t row0, int64_t B, int N,
+                                    int Kp, int words, int lane, int pw) {
+  const uint32_t one = FMT == MPV_FMT_BF16 ? 0x3F80u : 0x3C00u;
+  const int kgroups = Kp / 8, nw = (kgroups + 3) / 4;
+  uint32_t wv[kRowsPerLane][4];
+#pragma unroll
+  for (int rr = 0; rr < kRowsPerLane; ++rr) {
+    const int64_t s = row0 + lane + 32 * (pw + kProducers * rr);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) wv[rr][w] = (s < B && w < words) ? __ldg(bits + s * words + w) : 0u;
+  }
+  auto expand = [&](int r, uint32_t word, int w) {
+    if (w == words - 1 && (N & 31)) word &= (1u << (N & 31)) - 1u;
+#pragma unroll
+    for (int g4 = 0; g4 < 4; ++g4) {
+      const int g = w * 4 + g4;
+      if (g < kgroups) {
+        uint32_t byte = (word >> (8 * g4)) & 0xFFu;
+        if (g * 8 <= N && N < g * 8 + 8) byte |= 1u << (N - g * 8);
+        uint32_t p[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          p[j] = ((byte >> (2 * j)) & 1u ? one : 0u) | ((byte >> (2 * j + 1)) & 1u ? one << 16 : 0u);
+        *reinterpret_cast<uint4*>(sA + kmajor_off(r, g * 8, Kp)) = make_uint4(p[0], p[1], p[2], p[3]);
+      }
+    }
+  };
+#pragma unroll
+  for (int rr = 0; rr < kRowsPerLane; ++rr) {
+    const int r = lane + 32 * (pw + kProducers * rr);
+    const int64_t s = row0 + r;
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+      if (w < nw) expand(r, wv[rr][w], w);
+    for (int w = 4; w < nw; ++w) expand(r, (s < B && w < words) ? __ldg(bits + s * words + w) : 0u, w);
+  }
+}
+
 // Log-cosh epilogue over this thread's row and its slice's 8-column groups
 // (see forward_tc_kernel for the formulas).
 __device__ inline void tmem_ld4(uint32_t taddr, float* v) {
@@ -442,7 +487,7 @@ __device__ inline void tmem_ld4_pair(uint32_t a0, uint32_t a1, float* v0, float*
 template <bool IM>
 __device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int nquads, int slice, int rot, float& su,
                                      float& sl, float& si) {
-  for (int cq = (slice + rot) & (kSlices - 1); cq < nquads; cq += kSlices) {
+  for (int cq = (slice + rot) % kSlices; cq < nquads; cq += kSlices) {
     float tr[4], ti[4];
     tmem_ld4_pair(t_re + cq * 4, t_im + cq * 4, tr, ti);
 #pragma unroll
@@ -477,7 +522,7 @@ __device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int nquads, i
 // per-tile partial sums of the four column slices (sRed, double-buffered by
 // tile parity) before slice 0 reduces them one unit later.
 template <int FMT, bool IM>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads + 32 * kProducers, 1)
     forward_tc_pipe_kernel(Layout L, const uint8_t* __restrict__ blob, const uint32_t* __restrict__ bits, int64_t B,
                            double* __restrict__ out_lp, double* __restrict__ out_re, double* __restrict__ out_im) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -488,9 +533,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int N = L.N, M = L.M, Kp = L.Kp, HC = L.HC, HCB = L.HCB, nchunks = L.nchunks;
   uint8_t* sA = smem;                          // 2 x a_bytes
   uint8_t* sB = smem + 2 * L.a_bytes;          // nchunks x chunk_bytes
-  float* sVis = reinterpret_cast<float*>(sB + (size_t)nchunks * L.chunk_bytes);  // [re N][im N]
-  float* sRed = sVis + 2 * N;                  // [tile parity][slice][128][3]
+  float* sRed = reinterpret_cast<float*>(sB + (size_t)nchunks * L.chunk_bytes);  // [tile parity][slice][128][3]
   float* sAx = sRed + 2 * kSlices * kRows * 3; // [tile parity][128][2]: a . x (re, im)
+  const bool producer = warp >= kThreads / 32;  // build A tiles; producer warp 0 issues the MMAs
+  const int pw = warp - kThreads / 32;
+  const bool issuer = pw == 0 && lane == 0;
   const uint32_t aA = smem_u32(sA), aB = smem_u32(sB);
   const uint32_t bar0 = smem_u32(&bars[0]), bar_b = smem_u32(&bars[2]);
 
@@ -502,8 +549,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int k = 0; k < 3; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * k));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const float* gvis = reinterpret_cast<const float*>(blob + L.off_vis);
-  for (int j = tid; j < 2 * N; j += kThreads) sVis[j] = gvis[j];
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -557,15 +602,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (IM && out_im) out_im[s] = (double)vi + (double)si;
   };
 
-  if (units > 0) {
-    if (tid == 0) bulk_load(aB, blob, (uint32_t)(nchunks * L.chunk_bytes), bar_b);
-    build_a<FMT>(sA, bits, (int64_t)blockIdx.x * kRows, B, N, Kp, words, tid);
+  // Producer warp: A(tile 0) and the B staging before the first barrier, then per
+  // iteration u (after the barrier): issue MMA(u+1) and build the A tile that
+  // MMA(u+2) needs.  Its A buffer was last read by the MMAs of two tiles back,
+  // whose completion it checks on the MMA barrier of unit u (parity (u>>1)&1:
+  // unit u is the (u>>1)-th use of buffer u&1, and MMA(u+2) is issued later).
+  auto tile_row0 = [&](int64_t t) { return (blockIdx.x + t * gridDim.x) * (int64_t)kRows; };
+  if (producer && units > 0) {
+    if (issuer) bulk_load(aB, blob, (uint32_t)(nchunks * L.chunk_bytes), bar_b);
+    build_a_warp<FMT>(sA, bits, tile_row0(0), B, N, Kp, words, lane, pw);
+    if (units > 1 && nchunks == 1) build_a_warp<FMT>(sA + L.a_bytes, bits, tile_row0(1), B, N, Kp, words, lane, pw);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      mbar_wait(bar_b, 0);
-      issue(0);
-    }
+  }
+  __syncthreads();
+  if (units > 0 && issuer) {
+    mbar_wait(bar_b, 0);
+    issue(0);
   }
   uint32_t ph0 = 0, ph1 = 0;
   float su = 0.0f, sl = 0.0f, si = 0.0f;
@@ -573,14 +625,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t i = u / nchunks;
     const int c = (int)(u % nchunks);
     const int64_t nu = u + 1;
-    if (nu < units && nu % nchunks == 0) {
-      const int64_t ni = nu / nchunks;
-      build_a<FMT>(sA + (size_t)(ni & 1) * L.a_bytes, bits, (blockIdx.x + ni * gridDim.x) * kRows, B, N, Kp, words,
-                   tid);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
     __syncthreads();
-    if (nu < units && tid == 0) issue(nu);
+    if (producer) {
+      if (nu < units && issuer) issue(nu);
+      const int64_t bu = u + 2;
+      if (bu < units && bu % nchunks == 0) {
+        // nchunks == 1: the buffer's last reader is MMA(u), possibly in flight;
+        // nchunks >= 2: its last reader completed before this iteration's barrier
+        if (nchunks == 1) mbar_wait(bar0 + 8 * (uint32_t)(u & 1), (uint32_t)((u >> 1) & 1));
+        build_a_warp<FMT>(sA + (size_t)((bu / nchunks) & 1) * L.a_bytes, bits, tile_row0(bu / nchunks), B, N, Kp,
+                          words, lane, pw);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      continue;
+    }
 
     if (c == 0 && i > 0) finish_tile(i - 1);
     if (u & 1) {
@@ -594,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tb = tmem + t_lane + (uint32_t)(u & 1) * 256;
     const int nquads = (min(HC, M - c * HC) + 3) / 4;
     // rotation keyed by the global tile index: each row's summation order is grid-independent
-    const int rot = (int)((blockIdx.x + i * gridDim.x + c) & 3);
+    const int rot = (int)((blockIdx.x + i * gridDim.x + c) % kSlices);
     epilogue_unit<IM>(tb, tb + HCB, nquads, slice, rot, su, sl, si);
     if (c == 0 && slice == 0) {  // column HC of chunk 0: the visible term a . x
       float ar[4], ai[4];
@@ -613,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   __syncthreads();
-  if (units > 0) finish_tile(my_tiles - 1);
+  if (units > 0 && !producer) finish_tile(my_tiles - 1);
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
@@ -663,7 +721,8 @@ cudaError_t forward_tc_launch(int N, int M, int fmt, const void* weights, const 
   if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
   const uint8_t* blob = (const uint8_t*)weights;
   void* args[] = {&L, &blob, &bits, &B, &out_lp, &out_re, &out_im};
-  return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(tc::kThreads), args, L.smem, st);
+  const unsigned block = L.pipe ? tc::kThreads + 32 * tc::kProducers : tc::kThreads;  // + the producer warps
+  return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(block), args, L.smem, st);
 }
 
 }  // namespace mpv
