@@ -89,3 +89,23 @@ def test_product_has_no_cpu_fallback():
             text = open(os.path.join(pkg, fn)).read()
             assert "oracle" not in text.replace("oracle/", ""), fn
             assert "numba" not in text, fn
+
+
+def test_forward_tc_layout_and_argument_checks():
+    """Host-side contract of the tensor-core forward (no GPU needed): the
+    weights blob size, the supported shapes, and the format check that fails
+    before any launch."""
+    lib = nat.load()
+    n100 = lib.mpv_forward_tc_weights_bytes(100, 200)
+    assert n100 > 0 and n100 % 256 == 0
+    # B rows: (112 hidden + 16) per re/im block per chunk x Kp = 112 f16, two chunks, + a (re, im) f32
+    assert n100 >= 2 * 2 * 128 * 112 * 2
+    assert lib.mpv_forward_tc_weights_bytes(1, 1) > 0
+    assert lib.mpv_forward_tc_weights_bytes(100, 400) > lib.mpv_forward_tc_weights_bytes(100, 200)
+    assert lib.mpv_forward_tc_weights_bytes(2000, 10) == 0  # A tile beyond shared memory
+    assert lib.mpv_forward_tc_weights_bytes(0, 10) == 0
+    rc = lib.mpv_forward_tc_prepare(10, 10, nat.FMT_F32, ctypes.c_void_p(8), ctypes.c_void_p(8), None)
+    assert rc == nat.MPV_ERR_ARGS and b"f16 or bf16" in lib.mpv_last_error()
+    rc = lib.mpv_forward_tc(10, 10, nat.FMT_F16, ctypes.c_void_p(8), ctypes.c_void_p(8), 4, None, None, None, 0, None)
+    assert rc == nat.MPV_ERR_ARGS  # no output requested
+    assert lib.mpv_forward_tc(10, 10, nat.FMT_F16, ctypes.c_void_p(8), None, 0, None, None, None, 0, None) == nat.MPV_OK

@@ -105,3 +105,27 @@ def test_forward_tc_rejects_other_formats_and_empty_batch():
     tc = rbm.TensorCoreForward(params, F16)
     out = tc(np.zeros((0, 10), dtype=np.uint8))
     assert out.shape == (0,)
+
+
+def test_forward_tc_full_size_subsample():
+    """configs[1]-sized batch (65,536 samples x 100 flips = 6,553,600 configurations):
+    a seeded subsample against the oracle, and log p == 2 Re log psi of the
+    phase epilogue over the whole batch (two different epilogues, same GEMM)."""
+    N, B = 100, 65536 * 100
+    params = rbm.random_parameters(N, 2, derive_key(9, "tc-full"), 0.05)
+    tc = rbm.TensorCoreForward(params, F16)
+    g = torch.Generator(device=tc.device).manual_seed(3)
+    packed = torch.randint(-2**31, 2**31 - 1, (B, 4), dtype=torch.int32, device=tc.device, generator=g)
+    packed[:, -1] &= (1 << (N % 32)) - 1
+    lp, re, im = tc.forward_packed(packed)
+    lp_only = torch.empty_like(lp)
+    tc.forward_packed(packed, out_lp=lp_only)
+    assert torch.all(torch.abs(lp_only - lp) <= 4e-5 * torch.clamp(torch.abs(lp), min=1.0))
+    rows = np.random.default_rng(5).choice(B, size=3000, replace=False)
+    words = packed[torch.from_numpy(rows).to(tc.device)].cpu().numpy().view(np.uint32)
+    bits = ((words[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(len(rows), -1)[:, :N].astype(np.uint8)
+    want_re, want_im = _oracle(params, F16, bits)
+    got_re = re.cpu().numpy()[rows]
+    got_im = im.cpu().numpy()[rows]
+    assert np.all(np.abs(got_re - want_re) <= 1e-5 * np.maximum(1.0, np.abs(want_re)))
+    assert np.all(np.abs(got_im - want_im) <= 1e-5 * np.maximum(1.0, np.abs(want_im)))
