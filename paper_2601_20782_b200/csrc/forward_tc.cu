@@ -204,6 +204,29 @@ __device__ inline void bulk_load(uint32_t dst, const void* src, uint32_t bytes, 
   }
 }
 
+// MUFU approximations without the denormal fix-ups of the non-ftz intrinsics
+// (arguments are kept >= FLT_MIN where it matters: the lg2 input is clamped).
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float cos_ftz(float x) {
+  float y;
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sin_ftz(float x) {
+  float y;
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // cos(x) with a two-constant Cody-Waite reduction to [-pi, pi] ahead of the
 // MUFU approximation (cos.approx is accurate to ~2^-21 absolute only there).
 __device__ __forceinline__ float reduce_2pi(float x) {
@@ -217,6 +240,10 @@ __device__ __forceinline__ float reduce_2pi(float x) {
 // so Re log cosh theta = u - log 2 + 0.5 log((1-t)^2 + 4t cos^2 v): three MUFU
 // ops (ex2, cos, lg2).  The phase atan2((1-t) sin v, (1+t) cos v) is computed
 // only when Im log psi is requested (IM), from sin v / cos v.
+template <bool IM>
+__device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int nquads, int slice, int rot, float& su,
+                                     float& sl, float& si);
+
 template <int FMT, bool IM>
 __global__ void __launch_bounds__(kThreads, 1)
     forward_tc_kernel(Layout L, const uint8_t* __restrict__ blob, const uint32_t* __restrict__ bits, int64_t B,
@@ -262,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t t_lane = (uint32_t)(q * 32) << 16;
   const uint16_t one = FMT == MPV_FMT_BF16 ? 0x3F80 : 0x3C00;
   const int64_t ntiles = (B + kRows - 1) / kRows;
-  const int kgroups = Kp / 8, cgroups = HC / 8;
+  const int kgroups = Kp / 8;
   // every column (padding included) contributes -log 2; padded columns (theta = 0) add log 2 back
   const float ln2 = 0.693147180559945309f;
 
@@ -314,34 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(bar_mma, ph_mma);
       ph_mma ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      for (int cg = slice; cg < cgroups; cg += kSlices) {
-        const int j0 = cg * 8;
-        float tr[8], ti[8];
-        tmem_ld8(tmem + t_lane + j0, tr);
-        tmem_ld8(tmem + t_lane + 256 + j0, ti);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float x = tr[j], y = ti[j];
-          const float u = fabsf(x);
-          const float v = x < 0.0f ? -y : y;
-          const float t = exp2f(-2.885390081777926815f * u);  // e^{-2u}, ex2.approx (ftz)
-          // 1 - t without cancellation for small u (series of -expm1(-2u))
-          const float omt = u < 0.0625f ? u * fmaf(u, fmaf(u, 1.33333333f, -2.0f), 2.0f) : 1.0f - t;
-          su += u;
-          float sv, cv;
-          const float vr = reduce_2pi(v);
-          if (IM) {
-            __sincosf(vr, &sv, &cv);
-            const float wr = (1.0f + t) * cv, wi = omt * sv;
-            sl += __log2f(fmaf(wr, wr, wi * wi));
-            si += atan2f(wi, wr);
-          } else {
-            // |.|^2 = (1-t)^2 + 4t cos^2 v: no cancellation near the zeros of cosh
-            cv = __cosf(vr);
-            sl += __log2f(fmaf(4.0f * t * cv, cv, omt * omt));
-          }
-        }
-      }
+      epilogue_unit<IM>(tmem + t_lane, tmem + t_lane + 256, HC / 4, slice, 0, su, sl, si);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncthreads();  // TMEM and the B buffer are free for the next chunk / tile
     }
@@ -495,19 +495,20 @@ __device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int nquads, i
       const float x = tr[j], y = ti[j];
       const float u = fabsf(x);
       const float v = x < 0.0f ? -y : y;
-      const float t = exp2f(-2.885390081777926815f * u);
+      const float t = ex2_ftz(-2.885390081777926815f * u);  // e^{-2u}
+      // 1 - t without cancellation for small u (series of -expm1(-2u))
       const float omt = u < 0.0625f ? u * fmaf(u, fmaf(u, 1.33333333f, -2.0f), 2.0f) : 1.0f - t;
       su += u;
-      float sv, cv;
       const float vr = reduce_2pi(v);
       if (IM) {
-        __sincosf(vr, &sv, &cv);
+        const float sv = sin_ftz(vr), cv = cos_ftz(vr);
         const float wr = (1.0f + t) * cv, wi = omt * sv;
-        sl += __log2f(fmaf(wr, wr, wi * wi));
+        sl += lg2_ftz(fmaxf(fmaf(wr, wr, wi * wi), 1.17549435e-38f));
         si += atan2f(wi, wr);
       } else {
-        cv = __cosf(vr);
-        sl += __log2f(fmaf(4.0f * t * cv, cv, omt * omt));
+        // |.|^2 = (1-t)^2 + 4t cos^2 v: no cancellation near the zeros of cosh
+        const float cv = cos_ftz(vr);
+        sl += lg2_ftz(fmaxf(fmaf(4.0f * t * cv, cv, omt * omt), 1.17549435e-38f));
       }
     }
   }
