@@ -12,22 +12,24 @@
 //             + i (... + sum_i atan2((1-t) sin v, (1+t) cos v)),
 //   u = |Re theta|, v = sign(Re theta) Im theta, t = exp(-2u).
 //
-// GEMM shape per CTA tile: D[128 configurations x HC hidden] (re and im in
-// two TMEM column blocks, cols [0,HC) and [256,256+HC)) = A[128 x Kp] * B[Kp x HC],
-// Kp = N + 1 rounded up to 16: column N of A is the constant 1 and row N of B
-// the hidden bias, so theta = W x + b leaves the tensor core complete.  A is decoded from the packed bits straight into
+// GEMM per CTA tile: D[128 configurations x (HC hidden + 16)] for the re and
+// the im block = A[128 x Kp] * B[Kp x (HC+16)], Kp = N + 1 rounded up to 16:
+// column N of A is the constant 1 and row N of B the hidden bias, so theta =
+// W x + b leaves the tensor core complete (row HC of the first chunk's blocks
+// holds a, giving a . x).  A is decoded from the packed bits straight into
 // shared memory (x in {0,1} is exact in f16/bf16, so the products are exact
-// and only the f32 accumulation order differs from the f64 reference); B
-// (the rounded weights, re and im rows) is staged once per CTA by the bulk
-// copy engine when it fits (one chunk), else re-staged per chunk from L2.
-// Both operands use the K-major no-swizzle canonical layout: 8x16-byte core
+// and only the f32 accumulation order differs from the f64 reference); B (the
+// rounded weights) is staged once per CTA by the bulk copy engine.  Both
+// operands use the K-major no-swizzle canonical layout: 8x16-byte core
 // matrices, K-adjacent core matrices 128 B apart (LBO), 8-row groups Kp*16 B
-// apart (SBO).  One elected thread issues tcgen05.mma (M=128, N=HC, K=16 per
-// instruction) and commits to an mbarrier; 8 warps drain TMEM with
-// tcgen05.ld (warp w reads lanes 32(w%4).. and every 4th 8-column group from
-// w/4) and run the f32 log-cosh epilogue, which is the kernel's bound (3 MUFU
-// ops per hidden unit for log p, + sin and atan2 for the phase, against 4*Kp
-// tensor flops per hidden unit).
+// apart (SBO).  forward_tc_pipe_kernel: 4 producer warps build A and one of
+// their threads issues tcgen05.mma (M=128, K=16 per instruction) into one of
+// two TMEM buffers and commits to an mbarrier; 16 epilogue warps drain the
+// other buffer with tcgen05.ld and run the f32 log-cosh epilogue, which is the
+// kernel's bound (3 MUFU ops per hidden unit for log p, + sin and atan2 for
+// the phase, against 4*Kp tensor flops per hidden unit).  forward_tc_kernel is
+// the unpipelined fallback for weights beyond shared memory (B re-staged per
+// chunk from L2, visible term from a bit loop).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -180,17 +182,6 @@ __device__ inline void mbar_wait(uint32_t bar, uint32_t phase) {
       : "memory");
 }
 
-__device__ inline void tmem_ld8(uint32_t taddr, float* v) {
-  uint32_t r[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                 "=r"(r[7])
-               : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(r[j]);
-}
-
 // Stage one B chunk (bytes multiple of 16) global -> smem with the bulk copy engine.
 __device__ inline void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -240,6 +231,9 @@ __device__ __forceinline__ float reduce_2pi(float x) {
 // so Re log cosh theta = u - log 2 + 0.5 log((1-t)^2 + 4t cos^2 v): three MUFU
 // ops (ex2, cos, lg2).  The phase atan2((1-t) sin v, (1+t) cos v) is computed
 // only when Im log psi is requested (IM), from sin v / cos v.
+template <int FMT>
+__device__ inline void build_a(uint8_t* sA, const uint32_t* __restrict__ bits, int64_t row0, int64_t B, int N,
+                               int Kp, int words, int tid);
 template <bool IM>
 __device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int nquads, int slice, int rot, float& su,
                                      float& sl, float& si);
@@ -287,9 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int q = warp & 3, slice = warp >> 2;
   const int row = q * 32 + lane;  // TMEM lane = tile row
   const uint32_t t_lane = (uint32_t)(q * 32) << 16;
-  const uint16_t one = FMT == MPV_FMT_BF16 ? 0x3F80 : 0x3C00;
   const int64_t ntiles = (B + kRows - 1) / kRows;
-  const int kgroups = Kp / 8;
   // every column (padding included) contributes -log 2; padded columns (theta = 0) add log 2 back
   const float ln2 = 0.693147180559945309f;
 
@@ -298,23 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * kRows;
-    // A tile: 8 bits -> 8 f16/bf16 values per 16-byte store
-    for (int idx = tid; idx < kRows * kgroups; idx += kThreads) {
-      const int r = idx / kgroups, g = idx % kgroups;
-      const int64_t s = row0 + r;
-      uint32_t byte = 0;
-      if (s < B && g * 8 < N) {
-        byte = (bits[s * words + (g >> 2)] >> ((g & 3) * 8)) & 0xFFu;
-        const int valid = N - g * 8;
-        if (valid < 8) byte &= (1u << valid) - 1u;
-      }
-      if (g * 8 <= N && N < g * 8 + 8) byte |= 1u << (N - g * 8);  // constant-1 column: theta = W x + b
-      uint32_t p[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        p[j] = ((byte >> (2 * j)) & 1u ? (uint32_t)one : 0u) | ((byte >> (2 * j + 1)) & 1u ? (uint32_t)one << 16 : 0u);
-      *reinterpret_cast<uint4*>(sA + kmajor_off(r, g * 8, Kp)) = make_uint4(p[0], p[1], p[2], p[3]);
-    }
+    build_a<FMT>(sA, bits, row0, B, N, Kp, words, tid);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
 
@@ -494,20 +470,19 @@ __device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int nquads, i
     for (int j = 0; j < 4; ++j) {
       const float x = tr[j], y = ti[j];
       const float u = fabsf(x);
-      const float v = x < 0.0f ? -y : y;
       const float t = ex2_ftz(-2.885390081777926815f * u);  // e^{-2u}
       // 1 - t without cancellation for small u (series of -expm1(-2u))
       const float omt = u < 0.0625f ? u * fmaf(u, fmaf(u, 1.33333333f, -2.0f), 2.0f) : 1.0f - t;
       su += u;
-      const float vr = reduce_2pi(v);
       if (IM) {
+        const float vr = reduce_2pi(x < 0.0f ? -y : y);  // v = sign(x) y
         const float sv = sin_ftz(vr), cv = cos_ftz(vr);
         const float wr = (1.0f + t) * cv, wi = omt * sv;
         sl += lg2_ftz(fmaxf(fmaf(wr, wr, wi * wi), 1.17549435e-38f));
         si += atan2f(wi, wr);
       } else {
-        // |.|^2 = (1-t)^2 + 4t cos^2 v: no cancellation near the zeros of cosh
-        const float cv = cos_ftz(vr);
+        // |.|^2 = (1-t)^2 + 4t cos^2 v: no cancellation near the zeros of cosh; cos is even, so v -> y
+        const float cv = cos_ftz(reduce_2pi(y));
         sl += lg2_ftz(fmaxf(fmaf(4.0f * t * cv, cv, omt * omt), 1.17549435e-38f));
       }
     }
