@@ -26,7 +26,7 @@
 // their threads issues tcgen05.mma (M=128, K=16 per instruction) into one of
 // two TMEM buffers and commits to an mbarrier; 16 epilogue warps drain the
 // other buffer with tcgen05.ld and run the f32 log-cosh epilogue, which is the
-// kernel's bound (3 MUFU ops per hidden unit for log p, + sin and atan2 for
+// kernel's bound (3 MUFU ops per hidden unit for log p, + sin and a minimax atan2 for
 // the phase, against 4*Kp tensor flops per hidden unit).  forward_tc_kernel is
 // the unpipelined fallback for weights beyond shared memory (B re-staged per
 // chunk from L2, visible term from a bit loop).
@@ -216,6 +216,36 @@ __device__ __forceinline__ float sin_ftz(float x) {
   float y;
   asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// atan2(y, x) for finite arguments: a = min/max through MUFU rcp, atan(a) as
+// a * p(a^2), p the degree-7 f32 minimax fit (max |error| 1.3e-7 on [0,1],
+// evaluated in f32 Horner, the f32 rounding floor; fit by tools/fit_atan.py),
+// then the octant/quadrant fix-ups.  The result takes y's sign, so signed
+// zeros give +-0 / +-pi as libm's atan2f does.
+__device__ __forceinline__ float atan2_fast(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  const float a = mx > 0.0f ? mn * rcp_ftz(mx) : 0.0f;
+  const float s = a * a;
+  float p = -0.004054425284266472f;
+  p = fmaf(p, s, 0.02186243049800396f);
+  p = fmaf(p, s, -0.05591154471039772f);
+  p = fmaf(p, s, 0.09642138332128525f);
+  p = fmaf(p, s, -0.139086052775383f);
+  p = fmaf(p, s, 0.19946560263633728f);
+  p = fmaf(p, s, -0.33329859375953674f);
+  p = fmaf(p, s, 0.9999993443489075f);
+  float r = p * a;
+  if (ay > ax) r = 1.57079632679489662f - r;
+  if (x < 0.0f || (x == 0.0f && __float_as_uint(x) != 0u)) r = 3.14159265358979324f - r;
+  return copysignf(r, y);
 }
 
 // cos(x) with a two-constant Cody-Waite reduction to [-pi, pi] ahead of the
@@ -479,7 +509,7 @@ __device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int nquads, i
         const float sv = sin_ftz(vr), cv = cos_ftz(vr);
         const float wr = (1.0f + t) * cv, wi = omt * sv;
         sl += lg2_ftz(fmaxf(fmaf(wr, wr, wi * wi), 1.17549435e-38f));
-        si += atan2f(wi, wr);
+        si += atan2_fast(wi, wr);
       } else {
         // |.|^2 = (1-t)^2 + 4t cos^2 v: no cancellation near the zeros of cosh; cos is even, so v -> y
         const float cv = cos_ftz(reduce_2pi(y));
