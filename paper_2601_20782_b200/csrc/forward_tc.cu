@@ -77,7 +77,7 @@ inline bool make_layout(int N, int M, Layout* L) {
     const int nch = (M + 111) / 112;
     const int hc = (int)rup((M + nch - 1) / nch, 16);
     const size_t bytes = 2 * L->a_bytes + (size_t)nch * 4 * (hc + 16) * L->Kp +
-                         2ull * kSlices * kRows * 3 * 4 + 2ull * kRows * 2 * 4 + 1024;
+                         3ull * kSlices * kRows * 3 * 4 + 2ull * kRows * 2 * 4 + 1024;
     if (bytes <= kSmemBudget) {
       L->pipe = 1;
       L->nchunks = nch;
@@ -488,13 +488,18 @@ __device__ inline void tmem_ld4_pair(uint32_t a0, uint32_t a1, float* v0, float*
   }
 }
 
+// Floor of a unit's |cosh|^2 factor.  The smallest factor finite f32 theta can
+// give is ~4e-14 (u = 0, v one f32 ulp from pi/2), so the floor never binds
+// short of an exact zero of cosh; it keeps the product of two factors normal.
+constexpr float kFactorFloor = 2.16840434e-19f;  // 2^-62
+
 // 4-column groups, group j to slice (j - rot) mod 4: the rotation (tile index +
 // chunk) evens out the remainder groups across slices over consecutive units.
 template <bool IM>
 __device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int nquads, int slice, int rot, float& su,
                                      float& sl, float& si) {
   for (int cq = (slice + rot) % kSlices; cq < nquads; cq += kSlices) {
-    float tr[4], ti[4];
+    float tr[4], ti[4], f[4];
     tmem_ld4_pair(t_re + cq * 4, t_im + cq * 4, tr, ti);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -508,51 +513,72 @@ __device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int nquads, i
         const float vr = reduce_2pi(x < 0.0f ? -y : y);  // v = sign(x) y
         const float sv = sin_ftz(vr), cv = cos_ftz(vr);
         const float wr = (1.0f + t) * cv, wi = omt * sv;
-        sl += lg2_ftz(fmaxf(fmaf(wr, wr, wi * wi), 1.17549435e-38f));
+        f[j] = fmaxf(fmaf(wr, wr, wi * wi), kFactorFloor);
         si += atan2_fast(wi, wr);
       } else {
         // |.|^2 = (1-t)^2 + 4t cos^2 v: no cancellation near the zeros of cosh; cos is even, so v -> y
         const float cv = cos_ftz(reduce_2pi(y));
-        sl += lg2_ftz(fmaxf(fmaf(4.0f * t * cv, cv, omt * omt), 1.17549435e-38f));
+        f[j] = fmaxf(fmaf(4.0f * t * cv, cv, omt * omt), kFactorFloor);
       }
     }
+    // one lg2 per pair of units: each factor lies in [2^-62, 4], so the product stays normal
+    sl += lg2_ftz(f[0] * f[1]) + lg2_ftz(f[2] * f[3]);
   }
+}
+
+__device__ inline void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ inline void commit_to(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
 // Software-pipelined variant (Layout.pipe): all B chunks resident in shared
 // memory, A double-buffered, two TMEM accumulator buffers (re | im, 2*HC <= 256
 // columns each).  Work units are (tile, chunk) pairs; while the 16 warps run
 // the epilogue of unit u, the tensor core computes unit u+1 into the other
-// TMEM buffer.  One __syncthreads per unit orders: A(u+1) written before its
-// MMA, epilogue(u-1) drained before MMA(u+1) reuses that buffer, and the
-// per-tile partial sums of the four column slices (sRed, double-buffered by
-// tile parity) before slice 0 reduces them one unit later.
+// TMEM buffer.  No CTA-wide barrier inside the loop: mbarriers hand off
+//   full[b]       MMA of the unit in TMEM buffer b done (tcgen05.commit),
+//   tmem_empty[b] all 512 epilogue threads drained buffer b (the issuer waits
+//                 on it before MMA(u+2) reuses the buffer),
+//   a_empty[b]    the MMAs of the tile in A buffer b done (A(t+2) may be built),
+//   red_full[k]   slices 1..3 wrote their per-tile partial sums into sRed[k]
+//                 (k = tile mod 3; slice 0 reduces tile i at the start of tile
+//                 i+1, and a writer of tile i+3 is held back by tmem_empty until
+//                 slice 0 has drained tile i+1, so three buffers never collide),
+// so a slow epilogue warp only stalls the issuer two units later, not its peers.
 template <int FMT, bool IM>
 __global__ void __launch_bounds__(kThreads + 32 * kProducers, 1)
     forward_tc_pipe_kernel(Layout L, const uint8_t* __restrict__ blob, const uint32_t* __restrict__ bits, int64_t B,
                            double* __restrict__ out_lp, double* __restrict__ out_re, double* __restrict__ out_im) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tmem_slot;
-  __shared__ __align__(8) uint64_t bars[3];  // [0],[1] MMA done per TMEM buffer, [2] B staged
+  // [0,1] full, [2,3] tmem_empty, [4,5] a_empty, [6,7,8] red_full, [9] B staged
+  __shared__ __align__(8) uint64_t bars[10];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = L.N, M = L.M, Kp = L.Kp, HC = L.HC, HCB = L.HCB, nchunks = L.nchunks;
   uint8_t* sA = smem;                          // 2 x a_bytes
   uint8_t* sB = smem + 2 * L.a_bytes;          // nchunks x chunk_bytes
-  float* sRed = reinterpret_cast<float*>(sB + (size_t)nchunks * L.chunk_bytes);  // [tile parity][slice][128][3]
-  float* sAx = sRed + 2 * kSlices * kRows * 3; // [tile parity][128][2]: a . x (re, im)
+  float* sRed = reinterpret_cast<float*>(sB + (size_t)nchunks * L.chunk_bytes);  // [tile % 3][slice][128][3]
+  float* sAx = sRed + 3 * kSlices * kRows * 3; // [tile parity][128][2]: a . x (re, im)
   const bool producer = warp >= kThreads / 32;  // build A tiles; producer warp 0 issues the MMAs
   const int pw = warp - kThreads / 32;
   const bool issuer = pw == 0 && lane == 0;
   const uint32_t aA = smem_u32(sA), aB = smem_u32(sB);
-  const uint32_t bar0 = smem_u32(&bars[0]), bar_b = smem_u32(&bars[2]);
+  const uint32_t bar0 = smem_u32(&bars[0]);
+  const uint32_t bar_full = bar0, bar_tempty = bar0 + 16, bar_aempty = bar0 + 32, bar_red = bar0 + 48,
+                 bar_b = bar0 + 72;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int k = 0; k < 3; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * k));
+    for (int k = 0; k < 10; ++k) {
+      const uint32_t count = (k == 2 || k == 3) ? kThreads : (k >= 6 && k <= 8) ? kThreads - 128 : 1;
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar0 + 8 * k), "r"(count));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -573,111 +599,101 @@ __global__ void __launch_bounds__(kThreads + 32 * kProducers, 1)
   const int64_t units = my_tiles * nchunks;
   const float ln2 = 0.693147180559945309f;
 
-  auto issue = [&](int64_t u) {  // thread 0: MMA of unit u into TMEM buffer u & 1
-    const int64_t i = u / nchunks;
-    const int c = (int)(u % nchunks);
-    const uint32_t a0 = aA + (uint32_t)(i & 1) * (uint32_t)L.a_bytes;
-    const uint32_t b0 = aB + (uint32_t)c * (uint32_t)L.chunk_bytes;
-    const uint32_t d0 = tmem + (uint32_t)(u & 1) * 256;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    for (int ks = 0; ks < Kp / 16; ++ks) {
-      const uint64_t da = make_desc(a0 + ks * 256, lbo, sbo);
-      mma_f16(d0, da, make_desc(b0 + ks * 256, lbo, sbo), idesc, ks > 0);
-      mma_f16(d0 + HCB, da, make_desc(b0 + (uint32_t)HCB * Kp * 2 + ks * 256, lbo, sbo), idesc, ks > 0);
-    }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     bar0 + 8 * (uint32_t)(u & 1))
-                 : "memory");
-  };
-  auto finish_tile = [&](int64_t i) {  // slice 0: reduce the four slices (+ a . x), store
-    if (slice != 0) return;
-    const int64_t s = (blockIdx.x + i * gridDim.x) * kRows + row;
-    if (s >= B) return;
-    const float* r = sRed + (size_t)(i & 1) * kSlices * kRows * 3;
-    float su = 0.0f, sl = 0.0f, si = 0.0f;
-#pragma unroll
-    for (int k = 0; k < kSlices; ++k) {
-      su += r[3 * (k * kRows + row)];
-      sl += r[3 * (k * kRows + row) + 1];
-      si += r[3 * (k * kRows + row) + 2];
-    }
-    const float vr = sAx[2 * ((i & 1) * kRows + row)], vi = sAx[2 * ((i & 1) * kRows + row) + 1];
-    const double re = (double)vr + (double)su + 0.5 * (double)ln2 * (double)sl - (double)ln2 * (double)L.cols_proc;
-    if (out_lp) out_lp[s] = 2.0 * re;
-    if (out_re) out_re[s] = re;
-    if (IM && out_im) out_im[s] = (double)vi + (double)si;
-  };
-
-  // Producer warp: A(tile 0) and the B staging before the first barrier, then per
-  // iteration u (after the barrier): issue MMA(u+1) and build the A tile that
-  // MMA(u+2) needs.  Its A buffer was last read by the MMAs of two tiles back,
-  // whose completion it checks on the MMA barrier of unit u (parity (u>>1)&1:
-  // unit u is the (u>>1)-th use of buffer u&1, and MMA(u+2) is issued later).
   auto tile_row0 = [&](int64_t t) { return (blockIdx.x + t * gridDim.x) * (int64_t)kRows; };
-  if (producer && units > 0) {
-    if (issuer) bulk_load(aB, blob, (uint32_t)(nchunks * L.chunk_bytes), bar_b);
-    build_a_warp<FMT>(sA, bits, tile_row0(0), B, N, Kp, words, lane, pw);
-    if (units > 1 && nchunks == 1) build_a_warp<FMT>(sA + L.a_bytes, bits, tile_row0(1), B, N, Kp, words, lane, pw);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-  if (units > 0 && issuer) {
-    mbar_wait(bar_b, 0);
-    issue(0);
-  }
-  uint32_t ph0 = 0, ph1 = 0;
-  float su = 0.0f, sl = 0.0f, si = 0.0f;
-  for (int64_t u = 0; u < units; ++u) {
-    const int64_t i = u / nchunks;
-    const int c = (int)(u % nchunks);
-    const int64_t nu = u + 1;
-    __syncthreads();
-    if (producer) {
-      if (nu < units && issuer) issue(nu);
-      const int64_t bu = u + 2;
-      if (bu < units && bu % nchunks == 0) {
-        // nchunks == 1: the buffer's last reader is MMA(u), possibly in flight;
-        // nchunks >= 2: its last reader completed before this iteration's barrier
-        if (nchunks == 1) mbar_wait(bar0 + 8 * (uint32_t)(u & 1), (uint32_t)((u >> 1) & 1));
-        build_a_warp<FMT>(sA + (size_t)((bu / nchunks) & 1) * L.a_bytes, bits, tile_row0(bu / nchunks), B, N, Kp,
-                          words, lane, pw);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (producer) {
+    // per tile t: wait until the MMAs of tile t-2 released A buffer t&1, build
+    // A(t) (4 warps), then the issuer issues the tile's units, each once the
+    // epilogue has drained the TMEM buffer it overwrites (unit u-2)
+    for (int64_t t = 0; t < my_tiles; ++t) {
+      if (t >= 2) mbar_wait(bar_aempty + 8 * (uint32_t)(t & 1), (uint32_t)(((t - 2) >> 1) & 1));
+      build_a_warp<FMT>(sA + (size_t)(t & 1) * L.a_bytes, bits, tile_row0(t), B, N, Kp, words, lane, pw);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kProducers) : "memory");
+      if (issuer) {
+        if (t == 0) {
+          bulk_load(aB, blob, (uint32_t)(nchunks * L.chunk_bytes), bar_b);
+          mbar_wait(bar_b, 0);
+        }
+        for (int c = 0; c < nchunks; ++c) {
+          const int64_t u = t * nchunks + c;
+          const uint32_t b = (uint32_t)(u & 1);
+          if (u >= 2) mbar_wait(bar_tempty + 8 * b, (uint32_t)(((u >> 1) + 1) & 1));
+          const uint32_t a0 = aA + (uint32_t)(t & 1) * (uint32_t)L.a_bytes;
+          const uint32_t b0 = aB + (uint32_t)c * (uint32_t)L.chunk_bytes;
+          const uint32_t d0 = tmem + b * 256;
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          for (int ks = 0; ks < Kp / 16; ++ks) {
+            const uint64_t da = make_desc(a0 + ks * 256, lbo, sbo);
+            mma_f16(d0, da, make_desc(b0 + ks * 256, lbo, sbo), idesc, ks > 0);
+            mma_f16(d0 + HCB, da, make_desc(b0 + (uint32_t)HCB * Kp * 2 + ks * 256, lbo, sbo), idesc, ks > 0);
+          }
+          commit_to(bar_full + 8 * b);
+          if (c == nchunks - 1) commit_to(bar_aempty + 8 * (uint32_t)(t & 1));
+        }
       }
-      continue;
+      __syncwarp();
     }
-
-    if (c == 0 && i > 0) finish_tile(i - 1);
-    if (u & 1) {
-      mbar_wait(bar0 + 8, ph1);
-      ph1 ^= 1;
-    } else {
-      mbar_wait(bar0, ph0);
-      ph0 ^= 1;
+  } else {
+    auto finish_tile = [&](int64_t i) {  // slice 0: reduce the four slices (+ a . x), store
+      if (slice != 0) return;
+      mbar_wait(bar_red + 8 * (uint32_t)(i % 3), (uint32_t)((i / 3) & 1));
+      const int64_t s = (blockIdx.x + i * gridDim.x) * kRows + row;
+      if (s >= B) return;
+      const float* r = sRed + (size_t)(i % 3) * kSlices * kRows * 3;
+      float su = 0.0f, sl = 0.0f, si = 0.0f;
+#pragma unroll
+      for (int k = 0; k < kSlices; ++k) {
+        su += r[3 * (k * kRows + row)];
+        sl += r[3 * (k * kRows + row) + 1];
+        si += r[3 * (k * kRows + row) + 2];
+      }
+      const float vr = sAx[2 * ((i & 1) * kRows + row)], vi = sAx[2 * ((i & 1) * kRows + row) + 1];
+      const double re =
+          (double)vr + (double)su + 0.5 * (double)ln2 * (double)sl - (double)ln2 * (double)L.cols_proc;
+      if (out_lp) out_lp[s] = 2.0 * re;
+      if (out_re) out_re[s] = re;
+      if (IM && out_im) out_im[s] = (double)vi + (double)si;
+    };
+    uint32_t ph0 = 0, ph1 = 0;
+    float su = 0.0f, sl = 0.0f, si = 0.0f;
+    for (int64_t u = 0; u < units; ++u) {
+      const int64_t i = u / nchunks;
+      const int c = (int)(u % nchunks);
+      if (c == 0 && i > 0) finish_tile(i - 1);
+      if (u & 1) {
+        mbar_wait(bar_full + 8, ph1);
+        ph1 ^= 1;
+      } else {
+        mbar_wait(bar_full, ph0);
+        ph0 ^= 1;
+      }
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tb = tmem + t_lane + (uint32_t)(u & 1) * 256;
+      const int nquads = (min(HC, M - c * HC) + 3) / 4;
+      // rotation keyed by the global tile index: each row's summation order is grid-independent
+      const int rot = (int)((blockIdx.x + i * gridDim.x + c) % kSlices);
+      epilogue_unit<IM>(tb, tb + HCB, nquads, slice, rot, su, sl, si);
+      if (c == 0 && slice == 0) {  // column HC of chunk 0: the visible term a . x
+        float ar[4], ai[4];
+        tmem_ld4(tb + HC, ar);
+        tmem_ld4(tb + HCB + HC, ai);
+        sAx[2 * ((i & 1) * kRows + row)] = ar[0];
+        sAx[2 * ((i & 1) * kRows + row) + 1] = ai[0];
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(bar_tempty + 8 * (uint32_t)(u & 1));
+      if (c == nchunks - 1) {
+        float* r = sRed + (size_t)(i % 3) * kSlices * kRows * 3 + 3 * (slice * kRows + row);
+        r[0] = su;
+        r[1] = sl;
+        r[2] = si;
+        su = sl = si = 0.0f;
+        if (slice != 0) mbar_arrive(bar_red + 8 * (uint32_t)(i % 3));
+      }
     }
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tb = tmem + t_lane + (uint32_t)(u & 1) * 256;
-    const int nquads = (min(HC, M - c * HC) + 3) / 4;
-    // rotation keyed by the global tile index: each row's summation order is grid-independent
-    const int rot = (int)((blockIdx.x + i * gridDim.x + c) % kSlices);
-    epilogue_unit<IM>(tb, tb + HCB, nquads, slice, rot, su, sl, si);
-    if (c == 0 && slice == 0) {  // column HC of chunk 0: the visible term a . x
-      float ar[4], ai[4];
-      tmem_ld4(tb + HC, ar);
-      tmem_ld4(tb + HCB + HC, ai);
-      sAx[2 * ((i & 1) * kRows + row)] = ar[0];
-      sAx[2 * ((i & 1) * kRows + row) + 1] = ai[0];
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    if (c == nchunks - 1) {
-      float* r = sRed + (size_t)(i & 1) * kSlices * kRows * 3 + 3 * (slice * kRows + row);
-      r[0] = su;
-      r[1] = sl;
-      r[2] = si;
-      su = sl = si = 0.0f;
-    }
+    if (units > 0) finish_tile(my_tiles - 1);
   }
   __syncthreads();
-  if (units > 0 && !producer) finish_tile(my_tiles - 1);
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
