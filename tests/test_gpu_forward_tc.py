@@ -98,6 +98,28 @@ def test_forward_tc_deterministic_across_grids():
     assert np.array_equal(lp.cpu().numpy(), lp2.cpu().numpy())
 
 
+@pytest.mark.parametrize("N,alpha,B,ctas", [
+    (37, 3, 2100, 2),   # M = 111: one hidden chunk per tile, 9 tiles per CTA (the tightest mbarrier hand-off)
+    (12, 20, 1900, 2),  # M = 240: three hidden chunks per tile, ragged last tile
+    (100, 2, 1000, 1),  # a single CTA runs every tile of the batch
+])
+def test_forward_tc_many_tiles_per_cta(N, alpha, B, ctas):
+    """Pipelined kernel with many tiles per CTA (A, TMEM and partial-sum buffers
+    wrap many times): equal to the oracle and bit-equal to the full grid."""
+    params = rbm.random_parameters(N, alpha, derive_key(N * 13 + alpha, "tc-wrap"), 0.2)
+    bits = _bits(B, N, N * 3 + B)
+    tc = rbm.TensorCoreForward(params, F16)
+    packed = rbm.device_pack(bits, tc.device)
+    few = [t.cpu().numpy() for t in tc.forward_packed(packed, max_ctas=ctas)]
+    full = [t.cpu().numpy() for t in tc.forward_packed(packed)]
+    for x, y in zip(few, full):
+        assert np.array_equal(x, y)
+    re, im = _oracle(params, F16, bits)
+    cond = 1e-6 * _conditioning(params, F16, bits)
+    assert np.all(np.abs(few[1] - re) <= 1e-5 * np.maximum(1.0, np.abs(re)) + cond)
+    assert np.all(np.abs(few[2] - im) <= 1e-5 * np.maximum(1.0, np.abs(im)) + cond)
+
+
 def test_forward_tc_rejects_other_formats_and_empty_batch():
     params = rbm.random_parameters(10, 1, derive_key(1, "tc-x"), 0.1)
     with pytest.raises(ValueError):
