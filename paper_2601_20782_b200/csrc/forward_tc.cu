@@ -505,20 +505,23 @@ __device__ inline void epilogue_unit(uint32_t t_re, uint32_t t_im, int nquads, i
     for (int j = 0; j < 4; ++j) {
       const float x = tr[j], y = ti[j];
       const float u = fabsf(x);
-      const float t = ex2_ftz(-2.885390081777926815f * u);  // e^{-2u}
-      // 1 - t without cancellation for small u (series of -expm1(-2u))
-      const float omt = u < 0.0625f ? u * fmaf(u, fmaf(u, 1.33333333f, -2.0f), 2.0f) : 1.0f - t;
       su += u;
       if (IM) {
+        const float t = ex2_ftz(-2.885390081777926815f * u);  // e^{-2u}
+        // 1 - t without cancellation for small u (series of -expm1(-2u))
+        const float omt = u < 0.0625f ? u * fmaf(u, fmaf(u, 1.33333333f, -2.0f), 2.0f) : 1.0f - t;
         const float vr = reduce_2pi(x < 0.0f ? -y : y);  // v = sign(x) y
         const float sv = sin_ftz(vr), cv = cos_ftz(vr);
         const float wr = (1.0f + t) * cv, wi = omt * sv;
         f[j] = fmaxf(fmaf(wr, wr, wi * wi), kFactorFloor);
         si += atan2_fast(wi, wr);
       } else {
-        // |.|^2 = (1-t)^2 + 4t cos^2 v: no cancellation near the zeros of cosh; cos is even, so v -> y
+        // |.|^2 = (1-t)^2 + 4t cos^2 v: no cancellation near the zeros of cosh; cos is even, so v -> y.
+        // The 4 rides in the exponent: t4 = 4t = 2^(2 - 2u log2 e).
+        const float t4 = ex2_ftz(fmaf(-2.885390081777926815f, u, 2.0f));
+        const float omt = u < 0.0625f ? u * fmaf(u, fmaf(u, 1.33333333f, -2.0f), 2.0f) : fmaf(t4, -0.25f, 1.0f);
         const float cv = cos_ftz(reduce_2pi(y));
-        f[j] = fmaxf(fmaf(4.0f * t * cv, cv, omt * omt), kFactorFloor);
+        f[j] = fmaxf(fmaf(t4 * cv, cv, omt * omt), kFactorFloor);
       }
     }
     // one lg2 per pair of units: each factor lies in [2^-62, 4], so the product stays normal
