@@ -41,6 +41,8 @@ REBURN_SWEEPS = 2
 BURN_IN_SWEEPS = 10 * N_SITES // 10  # 100 sweeps of initial equilibration (untimed)
 INIT_SCALE = 0.01  # reference default init (vmc.py:338)
 WORKLOAD = "rbm_a2_tfim10x10_h3.04_c16384_f16native_f64energy"
+METRIC = "MCMC chain-steps/sec (f16 sampling + f64 local energies), whole job"
+DATA = "synthetic (random_parameters scale 0.01, reference streams derive_key(0,'chains'))"
 
 
 def chain_steps_per_step(chains):
@@ -417,6 +419,31 @@ def run_ours(args, rank, world, local_rank):
             "energy_last": recs2[-1]["energy"]}
         vmc_iter["config2"]["iteration_ms"] = vmc_iter["config2"]["sampling_ms"] + vmc_iter["config2"]["update_ms"]
 
+        # north_star precision leg: the ground-state search on the 10x10 TFIM (h=3.04,
+        # alpha=1) with f16 NATIVE vs f64 sampling, same seed and protocol (minSR in
+        # sample space: U = 4,096 < P = 10,200); plateau = mean of the last 100 steps
+        def plateau(fmt):
+            mode = RoundingMode.NATIVE if fmt is not F64 else RoundingMode.PER_OPERATION
+            c = vmc.TrainConfig(TfimSpec(_LS.square(10), 1.0, 3.04), alpha=1, n_steps=300, n_samples=4096,
+                                n_chains=1024, sampling_format=fmt, rounding_mode=mode, sr_solver="minsr",
+                                compute_kappa=False, eta=0.02, burn_in_sweeps=100)
+            t0 = time.perf_counter()
+            r = vmc.train(c, local=True).records
+            e = np.array([x["energy"] for x in r[-100:]])
+            return {"plateau_energy_per_site": float(e.mean()) / 100, "plateau_std_per_site": float(e.std()) / 100,
+                    "mean_mc_error_per_site": float(np.mean([x["mc_error"] for x in r[-100:]])) / 100,
+                    "sigma_hat": float(np.mean([x["sigma_hat"] for x in r[-100:]])),
+                    "tv_bound": float(np.mean([min(x["bound_pinsker"], x["bound_theorem3"]) for x in r[-100:]])),
+                    "wall_s": time.perf_counter() - t0}
+
+        from paper_2601_20782_b200 import F64
+
+        p16, p64 = plateau(F16), plateau(F64)
+        vmc_iter["precision_leg_10x10"] = {
+            "config": "tfim10x10_h3.04_a1_s4096_c1024_minsr_eta0.02_300steps (plateau: last 100 steps)",
+            "f16_native": p16, "f64": p64,
+            "delta_per_site": p16["plateau_energy_per_site"] - p64["plateau_energy_per_site"]}
+
     steps_per_step = chain_steps_per_step(C) * world
     value = steps_per_step / (ms / 1e3)
     clk = clocks.summary()
@@ -427,7 +454,7 @@ def run_ours(args, rank, world, local_rank):
     fp64_peak = 64 * 148 * sm_mhz * 1e6
     fp64_ops = n_samples_total / world * (N_SITES * params.n_hidden * 8 + N_SITES * 2 * params.n_hidden)
     out = {
-        "metric": "MCMC chain-steps/sec (f16 sampling + f64 local energies), whole job",
+        "metric": METRIC,
         "value": value,
         "unit": "chain-steps/s",
         "n_gpus": world,
@@ -438,11 +465,10 @@ def run_ours(args, rank, world, local_rank):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f16",
-        "data": "synthetic (random_parameters scale 0.01, reference streams derive_key(0,'chains'))",
-        "config": {"workload": WORKLOAD, "chains_per_gpu": C, "n_sites": N_SITES, "alpha": ALPHA, "h": H_FIELD,
-                   "samples_per_step": n_samples_total, "thin_steps": thin, "reburn_sweeps": REBURN_SWEEPS,
-                   "chain_steps_per_step": steps_per_step, "variant": ev.snapshot.label,
-                   "l2": "flushed between timed steps (256 MB write)", "parallelism": f"chains sharded x{world}"},
+        "data": DATA,
+        "config": bench_config(),
+        "run": {"chain_steps_per_step": steps_per_step, "variant": ev.snapshot.label,
+                "parallelism": f"chains sharded x{world}"},
         "sampling_sweep_ms": sweep_avg,
         "sampling_chain_steps_per_s": collect_steps * world / (sweep_avg / 1e3),
         "energy_check": {"mean_energy": float(np.mean(energies)), "acceptance": None},
@@ -483,46 +509,95 @@ def run_ours(args, rank, world, local_rank):
             out["roofline"]["traffic_unit"] = "bytes/launch (ncu --set full, profiles/r01)"
             out["roofline_energy"]["traffic"] = json.load(open(tr))["energy_kernel"]["dram_bytes_per_launch"]
     if rank == 0 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args, sample_chains=C)
+        out["cpu_baseline"] = cpu_baseline()
     return out
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle restatement of the reference CPU path
-# (per-operation f16 evaluator, full forward per proposal; f64 local energies)
+# CPU baseline / reference arm: the oracle's restatement of the reference CPU
+# path (oracle/c/oracle_port.c: per-operation f16 evaluator with a full forward
+# per proposal, as numba runs _kernels.rounded_log_prob; f64 local energies with
+# a full forward per connected configuration, vmc.py:60-108), OpenMP over the
+# chains on every host core.  Parameters come from the oracle's own restatement
+# of rbm.random_parameters / round_parameters (pinned to the reference's output,
+# tests/test_oracle.py), never from the package under test.
 # ---------------------------------------------------------------------------
-def cpu_baseline(args, sample_chains=CHAINS_PER_GPU, threads=None, sample_steps=4, energy_samples=256):
-    from oracle import port
-    from paper_2601_20782_b200 import F16, rbm
-    from paper_2601_20782_b200.lattice import LatticeSpec
-    from paper_2601_20782_b200.rng import derive_key
+REF_SAMPLE_DIV = 16  # each reference step is 1/16 of the workload step (1,024 chains)
 
+
+class ReferenceWorkload:
+    """One bounded sample of the bench step on the CPU: C/16 chains through the
+    reference's per-iteration sampling phase (vmc.py:531-564): set_evaluator with
+    the f16 snapshot, re-burn 2 sweeps, collect 4 samples per chain at thinning
+    N+1, f64 local energies of every sample, energy mean and acceptance.  Work
+    proportions equal the GPU step's, so chain-steps/s are comparable."""
+
+    def __init__(self, chains, threads):
+        from oracle import port
+        from oracle import rng as orng
+
+        self.port, self.chains, self.threads = port, int(chains), int(threads)
+        a, b, w = port.random_parameters(N_SITES, ALPHA, orng.derive_key(0, "init"), INIT_SCALE)
+        self.p64 = port.Params(a, b, w)
+        self.p16 = port.Params(*port.round_parameters(a, b, w, "f16"))
+        self.ens = port.PortEnsemble(self.chains, N_SITES, "flip", None, self.p16, "f16",
+                                     int(orng.derive_key(0, "chains")), nthreads=self.threads)
+        self.ens.run_steps(2 * N_SITES)  # untimed equilibration (per-op cost does not depend on the state)
+        self.bonds = _square_bonds(L)
+
+    def chain_steps(self):
+        return chain_steps_per_step(self.chains)
+
+    def step(self):
+        ens = self.ens
+        ens.set_params(self.p16, "f16")  # the iteration's snapshot (set_evaluator refresh)
+        ens.reset_counters()
+        ens.run_steps(REBURN_SWEEPS * N_SITES)
+        samples = ens.collect(self.chains * SAMPLES_PER_CHAIN, N_SITES + 1)
+        eps = self.port.local_energies(self.p64, "tfim", self.bonds, 1.0, H_FIELD, samples, nthreads=self.threads)
+        return float(eps.real.mean()), ens.accepted / ens.proposed
+
+
+def _square_bonds(length):
+    """Periodic square-lattice bonds (i < j), row-major sites (lattice.py:118-182)."""
+    out = set()
+    for r in range(length):
+        for c in range(length):
+            i = r * length + c
+            for j in (r * length + (c + 1) % length, ((r + 1) % length) * length + c):
+                out.add((min(i, j), max(i, j)))
+    return np.array(sorted(out), dtype=np.int64)
+
+
+def _time_reference_steps(n_warmup, n_steps, threads, chains):
+    wl = ReferenceWorkload(chains, threads)
+    times = []
+    for i in range(n_warmup + n_steps):
+        t0 = time.perf_counter()
+        wl.step()
+        dt = time.perf_counter() - t0
+        if i >= n_warmup:
+            times.append(dt)
+    return wl, times
+
+
+def cpu_baseline(threads=None, steps=3):
+    """Reported CPU baseline of our arm's JSON line (rank 0, N=1): a few timed
+    reference steps of the bounded sample (about 10-20 s of CPU work)."""
     threads = threads or len(os.sched_getaffinity(0))
-    params = rbm.random_parameters(N_SITES, ALPHA, derive_key(0, "init"), INIT_SCALE)
-    snap = rbm.round_parameters(params, F16)
-    P = port.Params(snap.a, snap.b, snap.w)
-    ens = port.PortEnsemble(sample_chains, N_SITES, "flip", None, P, "f16", int(derive_key(0, "chains")),
-                            nthreads=threads)
-    ens.run_steps(1)
-    t0 = time.perf_counter()
-    ens.run_steps(sample_steps)
-    t_s = time.perf_counter() - t0
-    rate_s = sample_chains * sample_steps / t_s
-    bonds = LatticeSpec.square(L).bond_array()
-    P64 = port.Params(params.a, params.b, params.w)
-    bits = ens.bits[:energy_samples]
-    t0 = time.perf_counter()
-    port.local_energies(P64, "tfim", bonds, 1.0, H_FIELD, bits, nthreads=threads)
-    t_e = time.perf_counter() - t0
-    rate_e = energy_samples / t_e
-    C = CHAINS_PER_GPU
-    total_steps = chain_steps_per_step(C)
-    t_job = total_steps / rate_s + C * SAMPLES_PER_CHAIN / rate_e
-    return {"value": total_steps / t_job, "unit": "chain-steps/s", "cores": threads, "kind": "port",
-            "sample": f"{sample_steps} MH steps x {sample_chains} chains (per-op f16, full forward per proposal) "
-                      f"+ f64 local energies of {energy_samples} samples; extrapolated to one workload step",
-            "sampling_chain_steps_per_s": rate_s, "local_energy_samples_per_s": rate_e,
-            "cpu_model": _cpu_model()}
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+    chains = CHAINS_PER_GPU // REF_SAMPLE_DIV
+    wl, times = _time_reference_steps(1, steps, threads, chains)
+    sec = float(np.median(times))
+    return {"value": wl.chain_steps() / sec, "unit": "chain-steps/s", "cores": threads, "kind": "port",
+            "sample": _reference_sample_text(chains), "sec_per_sample_step": sec, "cpu_model": _cpu_model()}
+
+
+def _reference_sample_text(chains):
+    return (f"1/{REF_SAMPLE_DIV} of the workload step per step: {chains} chains x "
+            f"{REBURN_SWEEPS * N_SITES + SAMPLES_PER_CHAIN * (N_SITES + 1)} per-op f16 MH steps "
+            f"(full forward per proposal) + f64 local energies of {chains * SAMPLES_PER_CHAIN} samples "
+            "(oracle C port of the reference, OpenMP)")
 
 
 def _cpu_model():
@@ -536,25 +611,32 @@ def _cpu_model():
     return "unknown"
 
 
+def bench_config():
+    return {"workload": WORKLOAD, "chains_per_gpu": CHAINS_PER_GPU, "n_sites": N_SITES, "alpha": ALPHA,
+            "h": H_FIELD, "samples_per_step": CHAINS_PER_GPU * SAMPLES_PER_CHAIN, "thin_steps": N_SITES + 1,
+            "reburn_sweeps": REBURN_SWEEPS, "l2": "flushed between timed steps (256 MB write)"}
+
+
 def run_reference(args, rank):
+    """--impl reference: every counted step is one timed bounded sample (1/16) of
+    the workload step, run by the oracle's restatement of the reference's CPU
+    path on all host cores; ms_per_step is that sample's measured wall time."""
     if rank != 0:
         return None
     threads = len(os.sched_getaffinity(0))
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
-    rates = []
+    chains = CHAINS_PER_GPU // REF_SAMPLE_DIV
     t_start = time.perf_counter()
-    for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(args, sample_chains=4096, threads=threads, sample_steps=2, energy_samples=64)
-        if i >= args.warmup:
-            rates.append(cb["value"])
-    value = float(np.median(rates))
-    cb["value"] = value
-    ms = chain_steps_per_step(CHAINS_PER_GPU) / value * 1e3
-    return {"metric": "MCMC chain-steps/sec (f16 sampling + f64 local energies), whole job", "value": value,
-            "unit": "chain-steps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "chains_per_gpu": CHAINS_PER_GPU},
-            "impl": "reference", "cpu_baseline": cb,
+    wl, times = _time_reference_steps(args.warmup, args.steps, threads, chains)
+    total = float(sum(times))
+    value = wl.chain_steps() * len(times) / total
+    ms = 1e3 * total / len(times)
+    cb = {"value": value, "unit": "chain-steps/s", "cores": threads, "kind": "port",
+          "sample": _reference_sample_text(chains), "cpu_model": _cpu_model()}
+    return {"metric": METRIC, "value": value, "unit": "chain-steps/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f16", "data": DATA, "config": bench_config(), "impl": "reference",
+            "cpu_baseline": cb,
             "e2e": {"value": value, "unit": "chain-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": time.perf_counter() - t_start}
 

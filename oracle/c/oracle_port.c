@@ -10,6 +10,7 @@
  * What is restated (each function cites the reference lines it follows):
  *   orc_mix64 / orc_stream_uniform   rng.py:21-27, 50-53, 63-77 (closed form of StreamSet)
  *   orc_quantize                     _kernels.py:27-48 (Veltkamp split + magic-constant RNE)
+ *   orc_quantize_array               rbm.py:91-101 (round_parameters, elementwise)
  *   orc_rounded_forward              _kernels.py:51-92
  *   orc_rounded_log_prob             _kernels.py:95-129
  *   orc_f64_forward                  rbm.py:130-150 (_logcosh_pair / _fast_forward; the
@@ -99,6 +100,13 @@ static qfmt make_qfmt(int fmt) {
 double orc_quantize_fmt(double v, int fmt) {
   qfmt q = make_qfmt(fmt);
   return orc_quantize(v, &q);
+}
+
+/* Elementwise RNE rounding of an array to fmt: the two-copy snapshot of
+ * rbm.round_parameters (rbm.py:91-101), applied to Re and Im separately. */
+void orc_quantize_array(const double* in, int64_t n, int fmt, double* out) {
+  qfmt q = make_qfmt(fmt);
+  for (int64_t i = 0; i < n; ++i) out[i] = orc_quantize(in[i], &q);
 }
 
 /* One row of _kernels.rounded_forward (_kernels.py:58-92); im lanes skipped when

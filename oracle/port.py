@@ -47,6 +47,7 @@ def lib():
                                           ctypes.c_int64, ctypes.c_int64, _dp]
         L.orc_quantize_fmt.restype = ctypes.c_double
         L.orc_quantize_fmt.argtypes = [ctypes.c_double, ctypes.c_int]
+        L.orc_quantize_array.argtypes = [_dp, ctypes.c_int64, ctypes.c_int, _dp]
         L.orc_rounded_forward.argtypes = [_u8p, ctypes.c_int64, ctypes.c_int, ctypes.c_int] + [_dp] * 6 + [
             ctypes.c_int, _dp, _dp, _dp, ctypes.c_int]
         L.orc_rounded_log_prob.argtypes = [_u8p, ctypes.c_int64, ctypes.c_int, ctypes.c_int] + [_dp] * 5 + [
@@ -107,6 +108,40 @@ def quantize(v, fmt):
     return lib().orc_quantize_fmt(float(v), FMT_CODES[fmt])
 
 
+def quantize_array(values, fmt):
+    """Elementwise RNE rounding to fmt (f64 arrays)."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    out = np.empty_like(v)
+    lib().orc_quantize_array(_d(v), v.size, FMT_CODES[fmt], _d(out))
+    return out
+
+
+def random_parameters(n_visible, alpha, key, scale=0.01):
+    """rbm.random_parameters (rbm.py:78-88): Re and Im i.i.d. N(0, scale^2) from the
+    counter-based Gaussian field, order [a | b | W row-major] (re block, then im
+    block).  Returns complex (a, b, w) with w of shape (M, N)."""
+    from fractions import Fraction
+
+    from oracle.rng import gaussian_field
+
+    m = Fraction(alpha) * n_visible
+    if m.denominator != 1 or m <= 0:
+        raise ValueError("alpha*N must be a positive integer")
+    m = int(m)
+    count = n_visible + m + m * n_visible
+    draws = scale * gaussian_field(key, np.arange(2 * count), 1.0)
+    z = draws[:count] + 1j * draws[count:]
+    return z[:n_visible], z[n_visible:n_visible + m], z[n_visible + m:].reshape(m, n_visible)
+
+
+def round_parameters(a, b, w, fmt):
+    """rbm.round_parameters (rbm.py:91-101): Re and Im rounded RNE to fmt."""
+    if fmt == "f64":
+        return a, b, w
+    q = lambda z: quantize_array(z.real, fmt) + 1j * quantize_array(z.imag, fmt)  # noqa: E731
+    return q(a), q(b), q(w)
+
+
 def rounded_forward(params: Params, bits, fmt, nthreads=None):
     """_kernels.rounded_forward: (lp, re, im) in per-operation rounding."""
     bits = np.ascontiguousarray(np.atleast_2d(bits), dtype=np.uint8)
@@ -157,6 +192,15 @@ class PortEnsemble:
                             self.nthreads)
         self.acc = np.zeros(self.n_chains, dtype=np.int64)
         self.proposed = 0
+
+    def set_params(self, params: Params, fmt=None):
+        """ChainEnsemble.set_evaluator (sampler.py:90-93): new target, cached log p
+        refreshed with one batched evaluation of every chain."""
+        self.params = params
+        self.fmt = fmt if fmt is not None else self.fmt
+        self._model = params.model(self.fmt)
+        lib().orc_log_probs(ctypes.byref(self._model), _u8(self.bits), self.n_chains, _d(self.logp),
+                            self.nthreads)
 
     @property
     def accepted(self):

@@ -47,3 +47,15 @@ def stream_uniforms(key, chains, t):
     with np.errstate(over="ignore"):
         s0 = mix64(np.uint64(key) ^ ((chains + np.uint64(1)) * GOLDEN))
         return uniform_from_bits(mix64(s0 + (t + np.uint64(1)) * GOLDEN))
+
+
+def counter_uniform(key, counters):  # rng.py:56-60
+    c = np.asarray(counters, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return uniform_from_bits(mix64(((c + np.uint64(1)) * GOLDEN) ^ np.uint64(key)))
+
+
+def gaussian_field(key, codes, sigma):  # rng.py:86-96
+    from scipy.special import ndtri
+
+    return sigma * ndtri(counter_uniform(key, codes))

@@ -525,7 +525,17 @@ class TensorCoreForward:
         """Device call on packed words [B, ceil(N/32)]; returns (lp, re, im) f64 tensors."""
         import torch
 
+        words = (self.n_visible + 31) // 32
+        if packed.dtype not in (torch.int32, torch.uint32) or packed.dim() != 2 or packed.shape[1] != words:
+            raise ValueError(f"packed configurations must be an int32 [B, {words}] tensor, got "
+                             f"{packed.dtype} {tuple(packed.shape)}")
+        if not packed.is_contiguous() or packed.device != self.device:
+            raise ValueError("packed configurations must be contiguous and on the evaluator's device")
         B = packed.shape[0]
+        for t in (out_lp, out_re, out_im):
+            if t is not None and (t.dtype != torch.float64 or t.numel() < B or not t.is_contiguous()
+                                  or t.device != self.device):
+                raise ValueError("outputs must be contiguous float64 device tensors with >= B elements")
         if out_lp is None and out_re is None and out_im is None:
             out_lp = torch.empty(B, dtype=torch.float64, device=self.device)
             out_re, out_im = torch.empty_like(out_lp), torch.empty_like(out_lp)

@@ -441,13 +441,18 @@ def train(config: TrainConfig, device=None, group=None, local: bool = False) -> 
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     # local=True: a single-process run even inside an initialised process group
     world = tdist.get_world_size(group) if (not local and tdist.is_available() and tdist.is_initialized()) else 1
+    exact_mode = config.sampling_mode == "exact"
+    if exact_mode:
+        # every rank enumerates the whole space with globally normalised weights;
+        # summing those across ranks would count each configuration `world` times,
+        # so exact mode runs the (identical) single-process update on every rank
+        world = 1
     rank = tdist.get_rank(group) if world > 1 else 0
     spec = config.hamiltonian
     n = spec.lattice.n_sites
     params = rbm.random_parameters(n, Fraction(config.alpha), derive_key(config.seed, "init"), config.init_scale)
     n_chains = config.n_chains or default_chain_count(config.n_samples)
     burn_in = config.burn_in_sweeps if config.burn_in_sweeps is not None else 10 * n
-    exact_mode = config.sampling_mode == "exact"
     words = (n + 31) // 32
     if exact_mode:
         from .lattice import pack_bits

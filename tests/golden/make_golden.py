@@ -283,7 +283,46 @@ def gen_formats():
     print(f"wrote {path}")
 
 
+def gen_params():
+    """rbm.random_parameters / round_parameters of the reference at the bench's
+    shapes: full arrays at configs[0] (N=20, alpha=1), SHA-256 digests of the
+    arrays' bytes at configs[1] (N=100, alpha=2) and configs[2] (alpha=4)."""
+    import hashlib
+
+    out = {}
+    p = rbm.random_parameters(20, 1, derive_key(0, "init"), 0.01)
+    out["c20_a"], out["c20_b"], out["c20_w"] = p.a, p.b, p.w
+    for f in ("f32", "f16", "bf16"):
+        r = rbm.round_parameters(p, FMTS[f])
+        out[f"c20_{f}_w"] = r.w
+    for alpha in (2, 4):
+        p = rbm.random_parameters(100, alpha, derive_key(0, "init"), 0.01)
+        for f in ("f64", "f32", "f16", "bf16"):
+            r = rbm.round_parameters(p, FMTS[f])
+            h = hashlib.sha256()
+            for arr in (r.a, r.b, r.w):
+                h.update(np.ascontiguousarray(arr, dtype=np.complex128).tobytes())
+            out[f"c100a{alpha}_{f}_sha256"] = np.array(h.hexdigest())
+    save("params.npz", **out)
+
+
+def gen_ed():
+    """Exact ground-state energies (hamiltonians.exact_ground_state) that pin
+    the oracle's dense diagonalisation (the VMC precision gate's E0)."""
+    cases = {"tfim_chain10_h0.5": TfimSpec(LatticeSpec.chain(10), 1.0, 0.5),
+             "tfim_chain10_h1": TfimSpec(LatticeSpec.chain(10), 1.0, 1.0),
+             "tfim_sq3_h3.04": TfimSpec(LatticeSpec.square(3), 1.0, 3.04),
+             "heis_chain8": HeisenbergSpec(LatticeSpec.chain(8), 1.0)}
+    save("ed.npz", **{k: np.float64(exact_ground_state(v)[0]) for k, v in cases.items()})
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["ed"]:
+        gen_ed()
+        sys.exit(0)
+    if sys.argv[1:] == ["params"]:
+        gen_params()
+        sys.exit(0)
     if sys.argv[1:] == ["formats"]:
         gen_formats()
         sys.exit(0)
@@ -296,6 +335,8 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["delta"]:
         gen_delta()
         sys.exit(0)
+    gen_ed()
+    gen_params()
     gen_formats()
     gen_table()
     gen_noisy()

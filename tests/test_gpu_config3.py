@@ -1,0 +1,96 @@
+"""BASELINE configs[2] instance: RBM alpha=4 on the 10x10 Heisenberg model with
+the Marshall sign, zero-magnetisation exchange moves, bf16 NATIVE sampling.
+
+At N=100, M=400 the planner picks the XI (int32) accumulators, and the
+320 KB table exceeds shared memory, so the fused sweep reads it from global
+memory (L1/L2).  That exact kernel instance is checked here:
+  * model parity: log p of the device == the numpy model of the NATIVE
+    arithmetic (oracle/model.py) within its per-row tolerance, and a chain's
+    cached log p == a fresh evaluation after many exchange moves;
+  * energy gate: the bf16 chains' Marshall-Heisenberg energy
+    agrees with the f64 chains of the oracle's restatement of the reference
+    ChainEnsemble (same key, chains and schedule) within 3 combined
+    split-chain errors; the device f64 chains take the oracle's decisions.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import model, port
+from paper_2601_20782_b200 import BF16, F64, RoundingMode, _native, parallel, rbm, sampler, vmc
+from paper_2601_20782_b200.hamiltonians import HeisenbergSpec
+from paper_2601_20782_b200.lattice import LatticeSpec
+from paper_2601_20782_b200.rng import derive_key
+
+pytestmark = pytest.mark.gpu
+N, ALPHA = 100, 4
+SMEM_LIMIT = 227 * 1024
+
+
+def _sz0_bits(rows, seed):
+    rng = np.random.default_rng(seed)
+    bits = np.zeros((rows, N), dtype=np.uint8)
+    np.put_along_axis(bits, np.argsort(rng.random((rows, N)), axis=1)[:, : N // 2], 1, axis=1)
+    return bits
+
+
+def _params(scale=0.01):
+    return rbm.random_parameters(N, ALPHA, derive_key(0, "init"), scale)
+
+
+@pytest.mark.parametrize("scale", [0.01, 0.3])
+def test_config3_xi_global_table_matches_model(cuda, scale):
+    p = _params(scale)
+    ev = rbm.log_prob_evaluator(p, BF16, RoundingMode.NATIVE)
+    snap = ev.snapshot
+    assert snap.variant == _native.ACC_XI, snap.label
+    assert snap._table.numel() > SMEM_LIMIT  # global-table (L1/L2) sweep instance
+    bits = _sz0_bits(3000, 1)
+    r = rbm.round_parameters(p, BF16)
+    want, tol = model.native_log_prob(r.a, r.b, r.w, bits, "bf16")
+    got = ev(bits)
+    assert np.all(np.abs(got - want) <= tol), np.max(np.abs(got - want) - tol)
+    ens = sampler.ChainEnsemble(1000, N, sampler.Proposal("exchange", N // 2), ev, derive_key(1, "chains"))
+    ens.run_steps(3000)
+    x = ens.bits
+    assert np.all(x.sum(axis=1) == N // 2)
+    np.testing.assert_array_equal(ens.log_probs, ev(x))  # the cached log p after 3000 moves
+
+
+def test_config3_bf16_energy_vs_reference_f64_chains(cuda):
+    p = _params(0.01)
+    spec = HeisenbergSpec(LatticeSpec.square(10), 1.0, marshall=True)
+    psi = rbm.log_psi_evaluator(p)
+    chains, per_chain, burn_sweeps, thin = 1024, 8, 30, N + 1
+    key = derive_key(7, "chains")
+    prop = sampler.Proposal("exchange", N // 2)
+    n_samples = chains * per_chain
+    counts = parallel.chain_counts(n_samples, chains, 0, chains)
+    ids = np.repeat(np.arange(chains), counts)
+
+    def stats(samples):
+        eps = vmc.local_energies(spec, psi, samples).real
+        means = np.bincount(ids, weights=eps) / counts
+        return float(eps.mean()), float(np.sqrt(means.var(ddof=1) / chains))
+
+    # the reference's f64 ChainEnsemble (oracle restatement, CPU)
+    ref = port.PortEnsemble(chains, N, "exchange", N // 2, port.Params(p.a, p.b, p.w), "f64", int(key))
+    ref.run_steps(burn_sweeps * N)
+    ref_samples = ref.collect(n_samples, thin)
+    e_ref, err_ref = stats(ref_samples)
+    # the device f64 chains take the same decisions (up to near-threshold ties)
+    dev64 = sampler.ChainEnsemble(chains, N, prop, rbm.log_prob_evaluator(p, F64), key)
+    dev64.run_steps(burn_sweeps * N)
+    s64 = dev64.collect(n_samples, thin)
+    assert np.mean(np.all(s64 == ref_samples, axis=1)) > 0.99
+    # bf16 NATIVE, identical sampler settings
+    ev = rbm.log_prob_evaluator(p, BF16, RoundingMode.NATIVE)
+    ens = sampler.ChainEnsemble(chains, N, prop, ev, key)
+    ens.run_steps(burn_sweeps * N)
+    s16 = ens.collect(n_samples, thin)
+    e16, err16 = stats(s16)
+    sigma_hat = float(np.std(ev(s16) - rbm.log_prob_batch(p, s16, F64)))
+    print(f"\n[config3] E_bf16 {e16:.6f} +- {err16:.6f}  E_ref(f64) {e_ref:.6f} +- {err_ref:.6f}  "
+          f"sigma_hat {sigma_hat:.3e}")
+    assert abs(e16 - e_ref) <= 3 * math.hypot(err16, err_ref), (e16, e_ref, err16, err_ref)

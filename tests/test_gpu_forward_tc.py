@@ -164,3 +164,22 @@ def test_forward_tc_full_size_subsample():
     cond = 1e-6 * _conditioning(params, F16, bits)
     assert np.all(np.abs(got_re - want_re) <= 1e-5 * np.maximum(1.0, np.abs(want_re)) + cond)
     assert np.all(np.abs(got_im - want_im) <= 1e-5 * np.maximum(1.0, np.abs(want_im)) + cond)
+
+
+def test_forward_tc_small_u_near_cosh_zero():
+    """|Re theta| just below the 1/16 series threshold of 1 - e^{-2u} with Im theta
+    near pi/2 (where the phase is most sensitive to that factor): theta = b is
+    exact in f32 for the all-zero configuration, so the epilogue alone is checked
+    against the f64 forward, at the 1e-5 relative bar with no conditioning term."""
+    M = 128
+    i = np.arange(M)
+    u = np.where(i % 2 == 0, 0.06, 0.0305) * np.where(i % 4 < 2, 1.0, -1.0)
+    v = np.pi / 2 + np.linspace(-0.09, 0.09, M)
+    b = u + 1j * v
+    params = rbm.RbmParameters(np.zeros(1, complex), b, np.zeros((M, 1), complex))
+    bits = np.zeros((256, 1), dtype=np.uint8)
+    for fmt in (F16, BF16):
+        got = rbm.TensorCoreForward(params, fmt)(bits)
+        re, im = _oracle(params, fmt, bits)
+        assert np.all(np.abs(got.real - re) <= 1e-5 * np.maximum(1.0, np.abs(re)))
+        assert np.all(np.abs(got.imag - im) <= 1e-5 * np.maximum(1.0, np.abs(im))), np.max(np.abs(got.imag - im))

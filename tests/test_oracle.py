@@ -107,3 +107,40 @@ def test_local_energies(g_energy, tag):
     eps = port.local_energies(p, ham, g_energy[f"{tag}_bonds"], J, h, g_energy[f"{tag}_bits"])
     ref = g_energy[f"{tag}_eps"]
     assert np.max(np.abs(eps - ref) / np.maximum(1, np.abs(ref))) < 1e-11
+
+
+def test_oracle_parameters_match_reference():
+    """oracle random_parameters / round_parameters (the reference arm's inputs)
+    == the reference's rbm.random_parameters / round_parameters (golden)."""
+    import hashlib
+
+    from conftest import golden
+
+    g = golden("params.npz")
+    a, b, w = port.random_parameters(20, 1, orng.derive_key(0, "init"), 0.01)
+    assert np.array_equal(a, g["c20_a"]) and np.array_equal(b, g["c20_b"]) and np.array_equal(w, g["c20_w"])
+    for f in ("f32", "f16", "bf16"):
+        assert np.array_equal(port.round_parameters(a, b, w, f)[2], g[f"c20_{f}_w"])
+    for alpha in (2, 4):
+        a, b, w = port.random_parameters(100, alpha, orng.derive_key(0, "init"), 0.01)
+        for f in ("f64", "f32", "f16", "bf16"):
+            h = hashlib.sha256()
+            for arr in port.round_parameters(a, b, w, f):
+                h.update(np.ascontiguousarray(arr, dtype=np.complex128).tobytes())
+            assert h.hexdigest() == str(g[f"c100a{alpha}_{f}_sha256"]), (alpha, f)
+
+
+def test_oracle_exact_diagonalisation_matches_reference():
+    from conftest import golden
+
+    from oracle import ed
+    from paper_2601_20782_b200.lattice import LatticeSpec
+
+    g = golden("ed.npz")
+    chain10 = LatticeSpec.chain(10).bond_array()
+    assert ed.ground_energy("tfim", 10, chain10, 1.0, 0.5) == pytest.approx(float(g["tfim_chain10_h0.5"]), abs=1e-10)
+    assert ed.ground_energy("tfim", 10, chain10, 1.0, 1.0) == pytest.approx(float(g["tfim_chain10_h1"]), abs=1e-10)
+    assert ed.ground_energy("tfim", 9, LatticeSpec.square(3).bond_array(), 1.0, 3.04) == pytest.approx(
+        float(g["tfim_sq3_h3.04"]), abs=1e-10)
+    assert ed.ground_energy("heisenberg", 8, LatticeSpec.chain(8).bond_array(), 1.0) == pytest.approx(
+        float(g["heis_chain8"]), abs=1e-10)
