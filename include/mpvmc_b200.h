@@ -205,10 +205,77 @@ int mpv_local_energies_ex(int N, int M, const double* a, const double* b, const 
  * out = O^H u = sum_s conj(O_s) u_s (deterministic: fixed-order chunk sums).
  * `scratch` >= mpv_logderiv_scratch_bytes(U, N, M).  N <= 256, M <= 512. */
 size_t mpv_logderiv_scratch_bytes(int64_t U, int N, int M);
+/* q_s = w_s (O v)_s (w: real [U], NULL = 1) */
 int mpv_logderiv_ov(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* v,
-                    double* q, void* scratch, void* stream);
+                    const double* w, double* q, void* scratch, void* stream);
+/* out = sum_s conj(O_s) w_s u_s; sum_out (NULL = skip) = sum_s w_s u_s */
 int mpv_logderiv_ohu(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* u,
-                     double* out, void* scratch, void* stream);
+                     const double* w, double* out, double* sum_out, void* scratch, void* stream);
+/* t = tanh(b + W x_s) complex [U][M] (ref: rbm.py:316) for params = [a | b | W row-major]
+ * complex (the order of RbmParameters.flatten, rbm.py:64-67); same scratch. */
+int mpv_logderiv_tanh(const double* params, const uint32_t* bits, int64_t U, int N, int M, double* t,
+                      void* scratch, void* stream);
+/* dense O_s - obar (obar NULL = uncentred), complex [U][P] (ref: rbm.py:307-325) */
+int mpv_logderiv_dense(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* obar,
+                       double* o, void* stream);
+
+/* ---- SR statistics and solve on the device (ref: vmc.py:145-229) ----
+ * mpv_sr_smatrix: S = sum_s w_s conj(C_s) C_s^T (Hermitian, real diagonal) for
+ * the centred dense C [U][P] complex (w NULL = 1), s [P][P] complex
+ * (ref: vmc.py:168-188 s_matrix). */
+int mpv_sr_smatrix(const double* c, const double* w, int64_t U, int P, double* s, void* stream);
+
+/* Matrix-free conjugate gradients for (S + lambda) g = F with S v =
+ * O^H (w O v) - conj(obar) (obar . v) and obar = sum_s w_s O_s; the
+ * vmc.py:202-229 system solved without forming S.  The CG scalars live in
+ * `scalars` (double[8]: rr, tol |F|, iterations, done flag, maxiter); every
+ * reduction runs in a fixed order.  Single process: mpv_cg_init, then
+ * mpv_cg_run(k) batches (read scalars[2..3] between batches).  Across ranks:
+ * per iteration mpv_cg_apply(p -> y, ysum), all-reduce [y | ysum], mpv_cg_step. */
+typedef struct {
+  int32_t n_visible, n_hidden;
+  int64_t n_samples;
+  const double* t;       /* tanh theta, complex [U][M] */
+  const uint32_t* bits;  /* packed [U][ceil(N/32)] */
+  const double* w;       /* sample weights, real [U] */
+  const double* obar;    /* sum_s w_s O_s (all ranks), complex [P] */
+  double lambda;
+  double *g, *r, *p, *ap; /* complex [P] */
+  double *y, *ysum;       /* complex [P], [1]: O^H (w O p) and sum_s w_s (O p)_s */
+  double* q;              /* complex [U] */
+  double* partials;       /* double[mpv_cg_partials_len()] */
+  double* scalars;        /* double[8] */
+  void* scratch;          /* >= mpv_logderiv_scratch_bytes(U, N, M) */
+  size_t scratch_bytes;
+} mpv_cg;
+size_t mpv_cg_partials_len(void);
+int mpv_cg_init(const mpv_cg* cg, const double* f, double tol, int64_t maxiter, void* stream);
+int mpv_cg_apply(const mpv_cg* cg, const double* v, double* y, double* ysum, void* stream);
+int mpv_cg_apply_finish(const mpv_cg* cg, const double* v, const double* y, const double* ysum, double* out,
+                        void* stream);
+int mpv_cg_step(const mpv_cg* cg, void* stream);
+int mpv_cg_run(const mpv_cg* cg, int n_iter, void* stream);
+
+/* minSR sample-space matrix (beyond the reference: the SR step of vmc.py:202-229
+ * solved in sample space by the push-through identity) for this rank's rows
+ * [row0, row0 + U_rows) of the all-rank sample set against all U_all columns:
+ * K = W^1/2 (O - 1 obar^T)(O - 1 obar^T)^H W^1/2 + lambda I, with O O^H formed from
+ * the factors (common set bits of the packed rows, T T^H) and d = O conj(obar),
+ * obar2 = |obar|^2.  out: [U_rows][U_all] complex, f64 (out_f32 = 0) or f32. */
+int mpv_minsr_gram(const double* t_rows, const uint32_t* bits_rows, int64_t U_rows, int64_t row0,
+                   const double* t_all, const uint32_t* bits_all, int64_t U_all, int N, int M, const double* d_all,
+                   const double* w_all, double obar2, double lambda, int out_f32, void* out, void* stream);
+
+/* Split-chain statistics (ref: vmc.py:592-604, mc_error vmc.py:311-317): per-chain
+ * means of Re eps over each chain's sample rows (rows of chain c = global id
+ * chain_offset + c: [c base + min(c, extra), ...) - row0, eps_u[inverse[row]]),
+ * then out = [mean of the means, sum of squared deviations, n_chains] (two-pass,
+ * fixed order).  mpv_moments: the same three numbers for a real vector.
+ * partials: double[mpv_cg_partials_len()]. */
+int mpv_chain_stats(const double* eps_u, const int64_t* inverse, int64_t n_chains, int64_t chain_offset,
+                    int64_t base, int64_t extra, int64_t row0, double* means, double* partials, double* out,
+                    void* stream);
+int mpv_moments(const double* x, int64_t n, double* partials, double* out, void* stream);
 
 /* ---- batched forward on the tensor cores (north_star (2); ref: rbm.py:130-150
  *      _fast_forward over a batch, i.e. log_psi_batch / log_prob_batch) ----

@@ -44,6 +44,15 @@ class Chains(ctypes.Structure):
     ]
 
 
+class CG(ctypes.Structure):
+    _fields_ = [
+        ("n_visible", _i32), ("n_hidden", _i32), ("n_samples", _i64),
+        ("t", _vp), ("bits", _vp), ("w", _vp), ("obar", _vp), ("lam", _f64),
+        ("g", _vp), ("r", _vp), ("p", _vp), ("ap", _vp), ("y", _vp), ("ysum", _vp), ("q", _vp),
+        ("partials", _vp), ("scalars", _vp), ("scratch", _vp), ("scratch_bytes", ctypes.c_size_t),
+    ]
+
+
 _SIGNATURES = {
     "mpv_stream_uniforms": (ctypes.c_int, [_u64, _i64, _i64, _i64, _i64, _vp, _vp]),
     "mpv_snapshot_bytes": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -53,8 +62,21 @@ _SIGNATURES = {
     "mpv_table_sweep": (ctypes.c_int, [_vp, ctypes.POINTER(Chains), _u64, ctypes.c_int, _i64, _i64, _i64, _i64, _vp,
                                        _i64, _i64, _i64, _i64, _vp]),
     "mpv_logderiv_scratch_bytes": (ctypes.c_size_t, [_i64, ctypes.c_int, ctypes.c_int]),
-    "mpv_logderiv_ov": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
-    "mpv_logderiv_ohu": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    "mpv_logderiv_ov": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp, _vp]),
+    "mpv_logderiv_ohu": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mpv_logderiv_tanh": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
+    "mpv_logderiv_dense": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
+    "mpv_sr_smatrix": (ctypes.c_int, [_vp, _vp, _i64, ctypes.c_int, _vp, _vp]),
+    "mpv_cg_partials_len": (ctypes.c_size_t, []),
+    "mpv_cg_init": (ctypes.c_int, [ctypes.POINTER(CG), _vp, _f64, _i64, _vp]),
+    "mpv_cg_apply": (ctypes.c_int, [ctypes.POINTER(CG), _vp, _vp, _vp, _vp]),
+    "mpv_cg_apply_finish": (ctypes.c_int, [ctypes.POINTER(CG), _vp, _vp, _vp, _vp, _vp]),
+    "mpv_cg_step": (ctypes.c_int, [ctypes.POINTER(CG), _vp]),
+    "mpv_cg_run": (ctypes.c_int, [ctypes.POINTER(CG), ctypes.c_int, _vp]),
+    "mpv_chain_stats": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "mpv_moments": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp]),
+    "mpv_minsr_gram": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp,
+                                      _f64, _f64, ctypes.c_int, _vp, _vp]),
     "mpv_chains_init": (ctypes.c_int, [ctypes.POINTER(Chains), _u64, ctypes.c_int, ctypes.c_int, _vp]),
     "mpv_mh_sweep": (ctypes.c_int, [ctypes.POINTER(Snapshot), ctypes.POINTER(Chains), _u64, ctypes.c_int,
                                     _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),

@@ -11,6 +11,7 @@
 #include "logderiv.cuh"
 #include "perop.cuh"
 #include "snapshot.cuh"
+#include "sr.cuh"
 #include "sweep.cuh"
 
 namespace mpv {
@@ -719,12 +720,9 @@ size_t mpv_logderiv_scratch_bytes(int64_t U, int N, int M) {
   return ld_ov_bytes(N, M) + (size_t)std::max<int64_t>(chunks, 1) * ld_rows_a(M) * ld_cols(N) * sizeof(double);
 }
 
-int mpv_logderiv_ov(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* v, double* q,
-                    void* scratch, void* stream) {
-  if (!t || !bits || !v || !q || !scratch || U < 0 || N < 1 || N > 256 || M < 1 || M > 512)
-    return fail(MPV_ERR_ARGS, "logderiv_ov: bad args (N <= 256, M <= 512)");
-  if (U == 0) return MPV_OK;
-  cudaStream_t st = (cudaStream_t)stream;
+// O v (MODE 0, weights fused) or T = tanh(b + W x) (MODE 1, v = parameters)
+static int launch_ov(int mode, const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* v,
+                     const double* w, double* q, double* t_out, void* scratch, cudaStream_t st) {
   double* vwt = (double*)scratch;
   const int64_t n = (int64_t)ld_rows(N) * ld_pitch(M);
   ld_transpose_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, st>>>(
@@ -733,21 +731,46 @@ int mpv_logderiv_ov(const double* t, const uint32_t* bits, int64_t U, int N, int
   const unsigned grid = (unsigned)((U + kLdSB - 1) / kLdSB);
   const int words = (N + 31) / 32;
   const double2* T = (const double2*)t;
-  if (kt <= 2) ld_ov_kernel<2><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, (const double2*)v, vwt, (double2*)q);
-  else if (kt <= 4) ld_ov_kernel<4><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, (const double2*)v, vwt, (double2*)q);
-  else if (kt <= 8) ld_ov_kernel<8><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, (const double2*)v, vwt, (double2*)q);
-  else ld_ov_kernel<16><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, (const double2*)v, vwt, (double2*)q);
-  return check_launch("logderiv_ov");
+  const double2* V = (const double2*)v;
+  double2* Q = (double2*)q;
+  double2* TO = (double2*)t_out;
+#define MPV_OV(K)                                                                                      \
+  if (mode == 0) ld_ov_kernel<K, 0><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, V, vwt, Q, w, TO); \
+  else ld_ov_kernel<K, 1><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, V, vwt, Q, w, TO);
+  if (kt <= 2) { MPV_OV(2) }
+  else if (kt <= 4) { MPV_OV(4) }
+  else if (kt <= 8) { MPV_OV(8) }
+  else { MPV_OV(16) }
+#undef MPV_OV
+  return check_launch(mode == 0 ? "logderiv_ov" : "logderiv_tanh");
 }
 
-int mpv_logderiv_ohu(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* u, double* out,
-                     void* scratch, void* stream) {
+int mpv_logderiv_ov(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* v, const double* w,
+                    double* q, void* scratch, void* stream) {
+  if (!t || !bits || !v || !q || !scratch || U < 0 || N < 1 || N > 256 || M < 1 || M > 512)
+    return fail(MPV_ERR_ARGS, "logderiv_ov: bad args (N <= 256, M <= 512)");
+  if (U == 0) return MPV_OK;
+  return launch_ov(0, t, bits, U, N, M, v, w, q, nullptr, scratch, (cudaStream_t)stream);
+}
+
+int mpv_logderiv_tanh(const double* params, const uint32_t* bits, int64_t U, int N, int M, double* t, void* scratch,
+                      void* stream) {
+  if (!params || !bits || !t || !scratch || U < 0 || N < 1 || N > 256 || M < 1 || M > 512)
+    return fail(MPV_ERR_ARGS, "logderiv_tanh: bad args (N <= 256, M <= 512)");
+  if (U == 0) return MPV_OK;
+  return launch_ov(1, nullptr, bits, U, N, M, params, nullptr, nullptr, t, scratch, (cudaStream_t)stream);
+}
+
+int mpv_logderiv_ohu(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* u, const double* w,
+                     double* out, double* sum_out, void* scratch, void* stream) {
   if (!t || !bits || !u || !out || !scratch || U < 0 || N < 1 || N > 256 || M < 1)
     return fail(MPV_ERR_ARGS, "logderiv_ohu: bad args (N <= 256)");
   cudaStream_t st = (cudaStream_t)stream;
   const int P = N + M + M * N;
   if (U == 0) {
     if (cudaMemsetAsync(out, 0, (size_t)P * 2 * sizeof(double), st) != cudaSuccess) return check_launch("logderiv_ohu");
+    if (sum_out && cudaMemsetAsync(sum_out, 0, 2 * sizeof(double), st) != cudaSuccess)
+      return check_launch("logderiv_ohu");
     return MPV_OK;
   }
   double* partial = (double*)((char*)scratch + ld_ov_bytes(N, M));
@@ -758,13 +781,153 @@ int mpv_logderiv_ohu(const double* t, const uint32_t* bits, int64_t U, int N, in
   const int words = (N + 31) / 32;
   const double2* T = (const double2*)t;
   const double2* Uv = (const double2*)u;
-  if (ntc == 16) ld_ohu_kernel<16><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk);
-  else if (ntc == 13) ld_ohu_kernel<13><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk);
-  else if (ntc == 8) ld_ohu_kernel<8><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk);
-  else ld_ohu_kernel<4><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk);
-  ld_ohu_reduce_kernel<<<(unsigned)std::min(148 * 8, (P + 255) / 256), 256, 0, st>>>(partial, chunks, N, M,
-                                                                                      (double2*)out);
+  if (ntc == 16) ld_ohu_kernel<16><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w);
+  else if (ntc == 13) ld_ohu_kernel<13><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w);
+  else if (ntc == 8) ld_ohu_kernel<8><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w);
+  else ld_ohu_kernel<4><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w);
+  ld_ohu_reduce_kernel<<<(unsigned)std::min(148 * 8, (P + 256) / 256), 256, 0, st>>>(partial, chunks, N, M,
+                                                                                      (double2*)out,
+                                                                                      (double2*)sum_out);
   return check_launch("logderiv_ohu");
+}
+
+int mpv_logderiv_dense(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* obar, double* o,
+                       void* stream) {
+  if (!t || !bits || !o || U < 0 || N < 1 || M < 1) return fail(MPV_ERR_ARGS, "logderiv_dense: bad args");
+  if (U == 0) return MPV_OK;
+  const int64_t n = U * ((int64_t)N + M + (int64_t)M * N);
+  ld_dense_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+      (const double2*)t, bits, U, N, M, (N + 31) / 32, (const double2*)obar, (double2*)o);
+  return check_launch("logderiv_dense");
+}
+
+int mpv_sr_smatrix(const double* c, const double* w, int64_t U, int P, double* s, void* stream) {
+  if (!c || !s || U < 0 || P < 1) return fail(MPV_ERR_ARGS, "sr_smatrix: bad args");
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned tiles = (unsigned)((P + kSmT - 1) / kSmT);
+  sr_smatrix_kernel<<<dim3(tiles, tiles), 256, 0, st>>>((const double2*)c, w, U, P, (double2*)s);
+  sr_real_diag_kernel<<<(unsigned)std::min(148 * 4, (P + 255) / 256), 256, 0, st>>>(P, (double2*)s);
+  return check_launch("sr_smatrix");
+}
+
+// ---- device-resident conjugate gradients (sr.cuh) ----
+static int cg_blocks(int P) { return std::max(1, std::min(kCgMaxBlocks, (P + kCgThreads - 1) / kCgThreads)); }
+static int cg_check(const mpv_cg* cg) {
+  if (!cg || !cg->t || !cg->bits || !cg->obar || !cg->g || !cg->r || !cg->p || !cg->ap || !cg->y || !cg->ysum ||
+      !cg->q || !cg->partials || !cg->scalars || !cg->scratch || cg->n_visible < 1 || cg->n_visible > 256 ||
+      cg->n_hidden < 1 || cg->n_hidden > 512 || cg->n_samples < 0)
+    return fail(MPV_ERR_ARGS, "cg: bad descriptor");
+  if (cg->scratch_bytes < mpv_logderiv_scratch_bytes(cg->n_samples, cg->n_visible, cg->n_hidden))
+    return fail(MPV_ERR_ARGS, "cg: scratch too small (mpv_logderiv_scratch_bytes)");
+  return MPV_OK;
+}
+static int cg_P(const mpv_cg* cg) { return cg->n_visible + cg->n_hidden + cg->n_hidden * cg->n_visible; }
+
+size_t mpv_cg_partials_len(void) { return 3 * (size_t)kCgMaxBlocks; }
+
+int mpv_cg_init(const mpv_cg* cg, const double* f, double tol, int64_t maxiter, void* stream) {
+  if (int rc = cg_check(cg)) return rc;
+  if (!f || tol < 0) return fail(MPV_ERR_ARGS, "cg_init: bad args");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int P = cg_P(cg), nb = cg_blocks(P);
+  cg_init_kernel<<<nb, kCgThreads, 0, st>>>(P, (const double2*)f, (double2*)cg->g, (double2*)cg->r, (double2*)cg->p,
+                                            cg->partials);
+  cg_init_scalars_kernel<<<1, 32, 0, st>>>(cg->partials, nb, tol, (double)maxiter, cg->scalars);
+  return check_launch("cg_init");
+}
+
+int mpv_cg_apply(const mpv_cg* cg, const double* v, double* y, double* ysum, void* stream) {
+  if (int rc = cg_check(cg)) return rc;
+  if (!v || !y || !ysum) return fail(MPV_ERR_ARGS, "cg_apply: bad args");
+  const int N = cg->n_visible, M = cg->n_hidden;
+  if (cg->n_samples == 0) {
+    return mpv_logderiv_ohu(cg->t, cg->bits, 0, N, M, cg->q, nullptr, y, ysum, cg->scratch, stream);
+  }
+  if (int rc = launch_ov(0, cg->t, cg->bits, cg->n_samples, N, M, v, cg->w, cg->q, nullptr, cg->scratch,
+                         (cudaStream_t)stream))
+    return rc;
+  return mpv_logderiv_ohu(cg->t, cg->bits, cg->n_samples, N, M, cg->q, nullptr, y, ysum, cg->scratch, stream);
+}
+
+int mpv_cg_apply_finish(const mpv_cg* cg, const double* v, const double* y, const double* ysum, double* out,
+                        void* stream) {
+  if (int rc = cg_check(cg)) return rc;
+  if (!v || !y || !ysum || !out) return fail(MPV_ERR_ARGS, "cg_apply_finish: bad args");
+  const int P = cg_P(cg);
+  cg_ap_kernel<<<cg_blocks(P), kCgThreads, 0, (cudaStream_t)stream>>>(
+      P, (const double2*)y, (const double2*)ysum, (const double2*)cg->obar, cg->lambda, (const double2*)v,
+      (double2*)out, nullptr);
+  return check_launch("cg_apply_finish");
+}
+
+int mpv_cg_step(const mpv_cg* cg, void* stream) {
+  if (int rc = cg_check(cg)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int P = cg_P(cg), nb = cg_blocks(P);
+  double* pap = cg->partials;
+  double* rr = cg->partials + kCgMaxBlocks;
+  cg_ap_kernel<<<nb, kCgThreads, 0, st>>>(P, (const double2*)cg->y, (const double2*)cg->ysum,
+                                          (const double2*)cg->obar, cg->lambda, (const double2*)cg->p,
+                                          (double2*)cg->ap, pap);
+  cg_update_kernel<<<nb, kCgThreads, 0, st>>>(P, (const double2*)cg->p, (const double2*)cg->ap, (double2*)cg->g,
+                                              (double2*)cg->r, pap, nb, rr, cg->scalars);
+  cg_direction_kernel<<<nb, kCgThreads, 0, st>>>(P, (const double2*)cg->r, (double2*)cg->p, rr, nb, cg->scalars);
+  cg_commit_kernel<<<1, 32, 0, st>>>(rr, nb, cg->scalars);
+  return check_launch("cg_step");
+}
+
+int mpv_cg_run(const mpv_cg* cg, int n_iter, void* stream) {
+  if (n_iter < 0) return fail(MPV_ERR_ARGS, "cg_run: n_iter < 0");
+  for (int it = 0; it < n_iter; ++it) {
+    if (int rc = mpv_cg_apply(cg, cg->p, cg->y, cg->ysum, stream)) return rc;
+    if (int rc = mpv_cg_step(cg, stream)) return rc;
+  }
+  return MPV_OK;
+}
+
+int mpv_minsr_gram(const double* t_rows, const uint32_t* bits_rows, int64_t U_rows, int64_t row0,
+                   const double* t_all, const uint32_t* bits_all, int64_t U_all, int N, int M, const double* d_all,
+                   const double* w_all, double obar2, double lambda, int out_f32, void* out, void* stream) {
+  if (!t_rows || !bits_rows || !t_all || !bits_all || !d_all || !w_all || !out || U_rows < 0 || U_all < 1 ||
+      row0 < 0 || row0 + U_rows > U_all || N < 1 || M < 1)
+    return fail(MPV_ERR_ARGS, "minsr_gram: bad args");
+  if (U_rows == 0) return MPV_OK;
+  const dim3 grid((unsigned)((U_all + kSmT - 1) / kSmT), (unsigned)((U_rows + kSmT - 1) / kSmT));
+  const int words = (N + 31) / 32;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (out_f32)
+    minsr_gram_kernel<float2><<<grid, 256, 0, st>>>((const double2*)t_rows, bits_rows, U_rows, row0,
+                                                    (const double2*)t_all, bits_all, U_all, M, words,
+                                                    (const double2*)d_all, w_all, obar2, lambda, (float2*)out);
+  else
+    minsr_gram_kernel<double2><<<grid, 256, 0, st>>>((const double2*)t_rows, bits_rows, U_rows, row0,
+                                                     (const double2*)t_all, bits_all, U_all, M, words,
+                                                     (const double2*)d_all, w_all, obar2, lambda, (double2*)out);
+  return check_launch("minsr_gram");
+}
+
+int mpv_chain_stats(const double* eps_u, const int64_t* inverse, int64_t n_chains, int64_t chain_offset,
+                    int64_t base, int64_t extra, int64_t row0, double* means, double* partials, double* out,
+                    void* stream) {
+  if (!eps_u || !means || !partials || !out || n_chains < 1 || base < 0 || extra < 0 || (base == 0 && extra == 0))
+    return fail(MPV_ERR_ARGS, "chain_stats: bad args");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = (int)std::min<int64_t>(kCgMaxBlocks, (n_chains + kCgThreads - 1) / kCgThreads);
+  chain_means_kernel<<<nb, kCgThreads, 0, st>>>((const double2*)eps_u, inverse, n_chains, chain_offset, base, extra,
+                                                row0, means, partials);
+  moments_pass2_kernel<<<nb, kCgThreads, 0, st>>>(means, n_chains, partials, nb, partials + kCgMaxBlocks);
+  moments_finish_kernel<<<1, 32, 0, st>>>(partials, nb, partials + kCgMaxBlocks, n_chains, out);
+  return check_launch("chain_stats");
+}
+
+int mpv_moments(const double* x, int64_t n, double* partials, double* out, void* stream) {
+  if (!x || !partials || !out || n < 1) return fail(MPV_ERR_ARGS, "moments: bad args");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = (int)std::min<int64_t>(kCgMaxBlocks, (n + kCgThreads - 1) / kCgThreads);
+  moments_pass1_kernel<<<nb, kCgThreads, 0, st>>>(x, n, partials);
+  moments_pass2_kernel<<<nb, kCgThreads, 0, st>>>(x, n, partials, nb, partials + kCgMaxBlocks);
+  moments_finish_kernel<<<1, 32, 0, st>>>(partials, nb, partials + kCgMaxBlocks, n, out);
+  return check_launch("moments");
 }
 
 // ---- batched forward on tcgen05 (forward_tc.cu) ----

@@ -47,10 +47,26 @@ __global__ void ld_transpose_kernel(const double2* __restrict__ v, int N, int M,
   }
 }
 
-template <int KT>
+// Complex tanh in f64: tanh(x + iy) = (sign(x)(1 - e^2) + 2i e sin 2y) / (1 + e^2 + 2e cos 2y),
+// e = exp(-2|x|) (numerator and denominator of sinh 2x / (cosh 2x + cos 2y) scaled by 2e:
+// no overflow for large |x|, and 1 - e^2 = -expm1(-4|x|) keeps small |x| accurate).
+__device__ __forceinline__ double2 ctanh_f64(double x, double y) {
+  const double ax = fabs(x);
+  const double e = exp(-2.0 * ax);
+  double s2, c2;
+  sincos(2.0 * y, &s2, &c2);
+  const double den = fma(2.0 * e, c2, fma(e, e, 1.0));
+  return make_double2(copysign(-expm1(-4.0 * ax), x) / den, 2.0 * e * s2 / den);
+}
+
+// MODE 0 (ov):   q_s = w_s (O v)_s            (w NULL: 1)
+// MODE 1 (tanh): t_si = tanh(b_i + (X W^T)_si) with v = the parameter vector [a | b | W]
+template <int KT, int MODE = 0>
 __global__ void __launch_bounds__(256) ld_ov_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
                                                     int64_t U, int N, int M, int words, const double2* __restrict__ v,
-                                                    const double* __restrict__ vwt, double2* __restrict__ q) {
+                                                    const double* __restrict__ vwt, double2* __restrict__ q,
+                                                    const double* __restrict__ w = nullptr,
+                                                    double2* __restrict__ t_out = nullptr) {
   __shared__ uint32_t smask[256 + 8];        // per-site masks of the block's 16 samples (N <= 256)
   __shared__ double2 red[8][kLdSB];          // per-warp partial q
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -86,6 +102,22 @@ __global__ void __launch_bounds__(256) ld_ov_kernel(const double2* __restrict__ 
       ld_dmma(acc[j][0][0], acc[j][0][1], a0, bf[j]);
       ld_dmma(acc[j][1][0], acc[j][1][1], a1, bf[j]);
     }
+  }
+  if constexpr (MODE == 1) {
+    // D fragment (sample m*8 + qc, unit nt*4 + qr) = theta - b: write tanh(theta)
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      const int nt = warp + j * 8, i = nt * 4 + qr;
+      if (nt < NT && i < M) {
+        const double2 b = v[N + i];
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int64_t s = s0 + m * 8 + qc;
+          if (s < U) t_out[s * M + i] = ctanh_f64(acc[j][m][0] + b.x, acc[j][m][1] + b.y);
+        }
+      }
+    }
+    return;
   }
   // epilogue: D fragment (sample m*8 + qc, unit nt*4 + qr) -> t * (Y + vb), summed over units
   double2 part[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
@@ -123,9 +155,13 @@ __global__ void __launch_bounds__(256) ld_ov_kernel(const double2* __restrict__ 
         acc2.x += v[k].x;
         acc2.y += v[k].y;
       }
-    for (int w = 0; w < 8; ++w) {
-      acc2.x += red[w][tid].x;
-      acc2.y += red[w][tid].y;
+    for (int wp = 0; wp < 8; ++wp) {
+      acc2.x += red[wp][tid].x;
+      acc2.y += red[wp][tid].y;
+    }
+    if (w) {
+      acc2.x *= w[s];
+      acc2.y *= w[s];
     }
     q[s] = acc2;
   }
@@ -160,7 +196,8 @@ inline int64_t ld_chunk(int64_t U, int N, int M) {
 template <int NTC>
 __global__ void __launch_bounds__(256) ld_ohu_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
                                                      int64_t U, int N, int M, int words, const double2* __restrict__ u,
-                                                     double* __restrict__ partial, int64_t chunk) {
+                                                     double* __restrict__ partial, int64_t chunk,
+                                                     const double* __restrict__ wts = nullptr) {
   __shared__ double as[2][64][kLdTile + 1];  // A' tiles [row][sample] (+1 pad: conflict-free column reads)
   __shared__ uint32_t bs[2][kLdTile][9];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -183,6 +220,11 @@ __global__ void __launch_bounds__(256) ld_ohu_kernel(const double2* __restrict__
       pu[r] = make_double2(0.0, 0.0);
       if (s < k_end) {
         pu[r] = u[s];
+        if (wts) {
+          const double ws = wts[s];
+          pu[r].x *= ws;
+          pu[r].y *= ws;
+        }
         pt[r] = ui < M ? t[s * M + ui] : make_double2(2 * ui < rows_a ? 1.0 : 0.0, 0.0);  // rows 2M, 2M+1: u itself
       }
     }
@@ -237,14 +279,17 @@ __global__ void __launch_bounds__(256) ld_ohu_kernel(const double2* __restrict__
   }
 }
 
-// fixed-order reduction of the chunk partials -> out (complex P-vector)
+// fixed-order reduction of the chunk partials -> out (complex P-vector); with
+// sum_out, also sum_s u_s (rows 2M, 2M+1 of A' against the ones column N)
 __global__ void ld_ohu_reduce_kernel(const double* __restrict__ partial, int chunks, int N, int M,
-                                     double2* __restrict__ out) {
+                                     double2* __restrict__ out, double2* __restrict__ sum_out = nullptr) {
   const int rows_pad = ld_rows_a(M), cols = ld_cols(N);
   const int P = N + M + M * N;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < P; idx += gridDim.x * blockDim.x) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < P + 1; idx += gridDim.x * blockDim.x) {
+    if (idx == P && !sum_out) break;
     int r, c;  // (row pair, column) of the entry
-    if (idx < N) { r = M; c = idx; }                       // a-part: rows 2M, 2M+1 (u), column k
+    if (idx == P) { r = M; c = N; }                         // sum_s u_s
+    else if (idx < N) { r = M; c = idx; }                   // a-part: rows 2M, 2M+1 (u), column k
     else if (idx < N + M) { r = idx - N; c = N; }          // b-part: unit i, ones column
     else { r = (idx - N - M) / N; c = (idx - N - M) % N; }  // W-part: unit i, site k
     double re = 0.0, im = 0.0;
@@ -253,7 +298,8 @@ __global__ void ld_ohu_reduce_kernel(const double* __restrict__ partial, int chu
       re += p[(size_t)(2 * r) * cols + c];
       im += p[(size_t)(2 * r + 1) * cols + c];
     }
-    out[idx] = make_double2(re, im);
+    if (idx == P) *sum_out = make_double2(re, im);
+    else out[idx] = make_double2(re, im);
   }
 }
 

@@ -1,0 +1,526 @@
+// ResCNN neural quantum state on the 5th-generation tensor cores.
+//
+// North-star subsystem (2) for the convolutional ansatz of BASELINE configs[3]
+// ("CNN/ResNet NQS, J1-J2 Heisenberg 10x10, tensor-core forward"): the model of
+// /root/reference/PAPER.md:876-890 (oracle/rescnn.py is its f64 restatement;
+// the reference package has no CNN, so parity is pinned by that restatement and
+// exact H psi on enumerable lattices):
+//   h0 = Conv(s), h_{l+1} = h_l + Conv(GELU(Conv(GELU(LN(h_l))))),
+//   log psi = sum LN(h_n);  3x3 periodic convolutions, F = 16 channels.
+//
+// Tensor-core mapping (no im2col): a CTA holds C configurations as padded
+// (L+2) x (L+2) grids, one row per grid position, rows of consecutive
+// configurations back to back (C (L+2)^2 <= 2048 rows = 16 MMA tiles of 128).
+// Activations are two K planes (channels 0-7, 8-15) of 16 bytes per row, so a
+// K-major no-swizzle descriptor with SBO = 128 B (8-row groups contiguous) and
+// LBO = the plane stride addresses ANY row offset: the 3x3 neighbour of row r
+// is row r + dy (L+2) + dx, so tap (dy, dx) of a convolution is one
+//   tcgen05.mma.kind::f16  M=128, N=16 (out channels), K=16 (in channels)
+// on the activation planes shifted by a constant, accumulated over the 9 taps
+// in TMEM (f32).  The periodic halo rows are rewritten by the epilogue after
+// every layer.  TMEM: the residual stream h for 16 tiles (256 columns; the
+// second convolution of a block accumulates straight into it) and the
+// first convolution's accumulators (256 columns).  Biases enter in the
+// epilogues (the residual's biases as a running sum per block).  Epilogues
+// (LN, GELU) run in f32 on 16 warps (lane quarter x tile group); layer inputs
+// are rounded to the format (f16/bf16), accumulation and the residual stream
+// are f32.
+//
+// Modes: evaluate (packed bits -> log p = 2 log psi), and the fused MH step
+// (ref: sampler.py:111-133 with this evaluator): per chain the reference's
+// splitmix64 draws pick a flip (or an exchange pair), the proposal is
+// evaluated, accepted by the f64 test log u < lp' - lp, state updated in place
+// and samples recorded at the thinning rounds (sampler.py:142-167 layout).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace mpv {
+namespace cnn {
+
+constexpr int kF = 16;           // channels (the paper's 16 filters)
+constexpr int kTaps = 9;         // 3x3
+constexpr int kRowsMax = 2048;   // 16 MMA tiles
+constexpr int kThreads = 512;    // 16 warps: TMEM lane quarter x tile group
+constexpr int kTapBytes = kF * kF * 2;  // one B block (16 x 16 f16)
+
+struct Shape {
+  int L, Lp, R, n_res, C, tiles, margin;  // R = Lp^2 rows per configuration
+  int n_conv;                             // 1 + 2 n_res
+  size_t off_vec;                         // byte offset of the f32 vectors in the blob
+  size_t blob_bytes;
+  size_t smem;
+};
+
+__host__ __device__ inline int plane_rows(const Shape& s) { return s.tiles * 128 + 2 * s.margin; }
+
+inline bool make_shape(int L, int n_res, Shape* s) {
+  if (L < 3 || L > 30 || n_res < 0 || n_res > 8) return false;
+  s->L = L;
+  s->Lp = L + 2;
+  s->R = s->Lp * s->Lp;
+  s->n_res = n_res;
+  s->C = kRowsMax / s->R;
+  if (s->C < 1) return false;
+  s->tiles = (s->C * s->R + 127) / 128;
+  s->margin = (s->Lp + 1 + 7) / 8 * 8;
+  s->n_conv = 1 + 2 * n_res;
+  s->off_vec = (size_t)s->n_conv * kTaps * kTapBytes;
+  // vectors: per LN i (n_res + 1): cumulative residual bias, gain, shift; per block: first conv bias
+  s->blob_bytes = s->off_vec + ((size_t)(n_res + 1) * 3 * kF + (size_t)n_res * kF) * 4;
+  s->blob_bytes = (s->blob_bytes + 255) / 256 * 256;
+  const size_t planes = 2ull * plane_rows(*s) * 16;
+  s->smem = planes + s->blob_bytes + (size_t)s->tiles * 128 * 4 + 1024;
+  return s->smem <= 220 * 1024;
+}
+
+// ---- tcgen05 helpers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // sm_100 descriptor version; base offset 0, SWIZZLE_NONE
+  return d;
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{.reg .pred p;\nWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu(float z) {
+  const float u = 0.7978845608028654f * fmaf(0.044715f * z, z * z, z);
+  return 0.5f * z * (1.0f + tanh_approx(u));
+}
+
+template <int FMT>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  uint32_t r;
+  if (FMT == MPV_FMT_BF16) asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  else asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// Write one grid position's 16 channels (rounded to FMT) to the activation
+// planes at row `row` and at the periodic halo images of an interior position.
+template <int FMT>
+__device__ __forceinline__ void store_row(uint8_t* plane0, size_t plane_stride, int row, int pr, int pc, int Lp,
+                                          const float* v) {
+  uint4 a, b;
+  a.x = pack2<FMT>(v[0], v[1]); a.y = pack2<FMT>(v[2], v[3]); a.z = pack2<FMT>(v[4], v[5]); a.w = pack2<FMT>(v[6], v[7]);
+  b.x = pack2<FMT>(v[8], v[9]); b.y = pack2<FMT>(v[10], v[11]); b.z = pack2<FMT>(v[12], v[13]);
+  b.w = pack2<FMT>(v[14], v[15]);
+  const int L = Lp - 2;
+  const int dr = pr == 1 ? L : (pr == L ? -L : 0);
+  const int dc = pc == 1 ? L : (pc == L ? -L : 0);
+  const int offs[4] = {0, dr * Lp, dc, dr * Lp + dc};
+  const bool use[4] = {true, dr != 0, dc != 0, dr != 0 && dc != 0};
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (use[k]) {
+      const int r = row + offs[k];
+      *reinterpret_cast<uint4*>(plane0 + (size_t)r * 16) = a;
+      *reinterpret_cast<uint4*>(plane0 + plane_stride + (size_t)r * 16) = b;
+    }
+}
+
+struct Args {
+  Shape S;
+  const uint8_t* blob;
+  // configurations / chains
+  int64_t B;                 // configurations (evaluate) or chains (MH)
+  int N, words;
+  uint32_t* bits;            // packed [B][words] (MH: updated in place)
+  double* out_lp;            // evaluate: log p; MH: cached log p (updated)
+  int64_t* accepted;         // MH (may be NULL)
+  int64_t* status;           // first non-finite (step, chain)
+  // MH schedule
+  int mh;
+  uint64_t key;
+  int64_t chain_offset, init_draws, step_index;
+  int proposal;
+  uint32_t* samples;
+  int64_t thin, sample_base, sample_extra, round_offset, row0;
+};
+
+template <int FMT>
+__global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(8) uint64_t bar_mma;
+  __shared__ int s_site[64];       // per configuration: flipped sites (MH), -1 none
+  __shared__ int s_site2[64];
+  __shared__ double s_logu[64];
+  __shared__ int s_bad[64];
+  const Shape& S = a.S;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Lp = S.Lp, R = S.R, C = S.C, N = a.N, words = a.words;
+  const int prow = plane_rows(S);
+  const size_t pstride = (size_t)prow * 16;
+  uint8_t* planes = smem;                                // [2][prow][16 B]
+  uint8_t* sblob = smem + 2 * pstride;                   // B blocks + vectors
+  float* vec = reinterpret_cast<float*>(sblob + S.off_vec);
+  float* rowsum = reinterpret_cast<float*>(sblob + S.blob_bytes);  // [tiles * 128]
+  uint8_t* plane0 = planes + (size_t)S.margin * 16;      // row 0 of the grid rows
+  const uint32_t aPlanes = smem_u32(plane0), aBlob = smem_u32(sblob);
+  const uint32_t sbar = smem_u32(&bar_mma);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (size_t i = tid * 16; i < S.blob_bytes; i += kThreads * 16)
+    *reinterpret_cast<uint4*>(sblob + i) = *reinterpret_cast<const uint4*>(a.blob + i);
+  for (size_t i = tid * 16; i < 2 * pstride; i += kThreads * 16) *reinterpret_cast<uint4*>(planes + i) = make_uint4(0, 0, 0, 0);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+  uint32_t phase = 0;
+
+  const uint32_t fmtbits = FMT == MPV_FMT_BF16 ? 1u : 0u;
+  const uint32_t idesc = (1u << 4) | (fmtbits << 7) | (fmtbits << 10) | ((uint32_t)(kF >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const int q = warp & 3, tg = warp >> 2;  // TMEM lane quarter, tile group
+  const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+  const int L = S.L;
+  const int64_t groups = (a.B + C - 1) / C;
+  const float* cb = vec;                          // [(n_res+1)][3][16]: cumulative bias, gain, shift
+  const float* b1 = vec + (S.n_res + 1) * 3 * kF;  // [n_res][16]
+
+  // one convolution: 9 taps x tiles MMAs; accumulate into dst columns (acc0: first tap overwrites)
+  auto conv = [&](int ci, uint32_t dst_col, bool keep) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int t = 0; t < S.tiles; ++t)
+        for (int d = 0; d < kTaps; ++d) {
+          const int off = (d / 3 - 1) * Lp + (d % 3 - 1);
+          const uint32_t aaddr = aPlanes + (uint32_t)((t * 128 + off) * 16);
+          const uint64_t da = make_desc(aaddr, (uint32_t)pstride, 128);
+          const uint64_t db = make_desc(aBlob + (uint32_t)((ci * kTaps + d) * kTapBytes), 128, 256);
+          mma_f16(tmem + dst_col + t * kF, da, db, idesc, (keep || d > 0) ? 1u : 0u);
+        }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sbar)
+                   : "memory");
+    }
+    mbar_wait(sbar, phase);
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  };
+
+  for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
+    const int64_t c0 = grp * C;
+    const int nc = (int)min((int64_t)C, a.B - c0);
+    // ---- proposals (MH) ----
+    if (a.mh && tid < nc) {
+      const int64_t c = c0 + tid, gchain = a.chain_offset + c;
+      const uint64_t s0 = stream_state(a.key, (uint64_t)gchain);
+      const uint64_t t = (uint64_t)(a.init_draws + 2 * a.step_index);
+      const double us = stream_draw(s0, t), ua = stream_draw(s0, t + 1);
+      int k1, k2 = -1;
+      if (a.proposal == MPV_PROPOSAL_FLIP) {
+        k1 = (int)floor_scaled(us, (double)N);
+      } else {
+        int i, j;
+        pair_of(floor_scaled(us, 0.5 * (double)N * (double)(N - 1)), N, i, j);
+        const uint32_t bi = (a.bits[c * words + (i >> 5)] >> (i & 31)) & 1u;
+        const uint32_t bj = (a.bits[c * words + (j >> 5)] >> (j & 31)) & 1u;
+        k1 = bi != bj ? i : -1;  // an exchange of equal bits is the identity (always accepted)
+        k2 = bi != bj ? j : -1;
+      }
+      s_site[tid] = k1;
+      s_site2[tid] = k2;
+      s_logu[tid] = log(ua);
+    }
+    __syncthreads();
+    // ---- input plane: s = 1 - 2x in channel 0 (all grid rows incl. halo) ----
+    for (int r = tid; r < S.tiles * 128; r += kThreads) {
+      const int j = r / R, pos = r % R;
+      float v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = 0.0f;
+      if (j < nc) {
+        int pr = pos / Lp, pc = pos % Lp;
+        pr = pr == 0 ? L : (pr == L + 1 ? 1 : pr);
+        pc = pc == 0 ? L : (pc == L + 1 ? 1 : pc);
+        const int site = (pr - 1) * L + (pc - 1);
+        uint32_t x = (a.bits[(c0 + j) * words + (site >> 5)] >> (site & 31)) & 1u;
+        if (a.mh && (site == s_site[j] || site == s_site2[j])) x ^= 1u;
+        v[0] = x ? -1.0f : 1.0f;
+      }
+      uint4 lo, hi = make_uint4(0, 0, 0, 0);
+      lo.x = pack2<FMT>(v[0], 0.0f);
+      lo.y = lo.z = lo.w = 0;
+      *reinterpret_cast<uint4*>(plane0 + (size_t)r * 16) = lo;
+      *reinterpret_cast<uint4*>(plane0 + pstride + (size_t)r * 16) = hi;
+    }
+    // ---- embedding convolution -> h (TMEM columns [0, 256)) ----
+    conv(0, 0, false);
+    for (int l = 0; l <= S.n_res; ++l) {
+      // LN epilogue of h (+ the running bias): block input (GELU) or the final sum
+      const float* cbl = cb + l * 3 * kF;
+      for (int t = tg; t < S.tiles; t += 4) {
+        float h[16];
+        tmem_ld16(tmem + t_lane + t * kF, h);
+        const int r = t * 128 + q * 32 + lane;
+        const int j = r / R, pos = r % R, pr = pos / Lp, pc = pos % Lp;
+        const bool interior = j < nc && pr >= 1 && pr <= L && pc >= 1 && pc <= L;
+        float mu = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          h[k] += cbl[k];
+          mu += h[k];
+        }
+        mu *= 1.0f / 16.0f;
+        float var = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) var = fmaf(h[k] - mu, h[k] - mu, var);
+        const float rs = rsqrtf(fmaf(var, 1.0f / 16.0f, 1e-6f));
+        if (l < S.n_res) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) h[k] = gelu(fmaf(cbl[kF + k] * rs, h[k] - mu, cbl[2 * kF + k]));
+          if (interior) store_row<FMT>(plane0, pstride, r, pr, pc, Lp, h);
+        } else {
+          float sum = 0.0f;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) sum += fmaf(cbl[kF + k] * rs, h[k] - mu, cbl[2 * kF + k]);
+          rowsum[r] = interior ? sum : 0.0f;
+        }
+      }
+      if (l == S.n_res) break;
+      // first convolution of the block -> accumulators (TMEM columns [256, 512))
+      conv(1 + 2 * l, 256, false);
+      const float* b1l = b1 + l * kF;
+      for (int t = tg; t < S.tiles; t += 4) {
+        float v[16];
+        tmem_ld16(tmem + t_lane + 256 + t * kF, v);
+        const int r = t * 128 + q * 32 + lane;
+        const int j = r / R, pos = r % R, pr = pos / Lp, pc = pos % Lp;
+        if (j < nc && pr >= 1 && pr <= L && pc >= 1 && pc <= L) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = gelu(v[k] + b1l[k]);
+          store_row<FMT>(plane0, pstride, r, pr, pc, Lp, v);
+        }
+      }
+      // second convolution accumulates into the residual stream h
+      conv(2 + 2 * l, 0, true);
+    }
+    __syncthreads();
+    // ---- per-configuration sums (fixed order), accept / write ----
+    if (tid < nc) {
+      const int j = tid;
+      float sum = 0.0f;
+      for (int pos = 0; pos < R; ++pos) sum += rowsum[j * R + pos];
+      const double lp_new = 2.0 * (double)sum;
+      const int64_t c = c0 + j;
+      if (!a.mh) {
+        a.out_lp[c] = lp_new;
+        if (!isfinite(lp_new) && a.status) {
+          atomicMin((unsigned long long*)&a.status[1], (unsigned long long)c);
+          atomicExch((unsigned long long*)&a.status[0], (unsigned long long)MPV_ERR_NONFINITE);
+        }
+      } else {
+        const double lp_old = a.out_lp[c];
+        const bool identity = s_site[j] < 0;  // exchange of equal bits
+        const bool accept = identity || s_logu[j] < lp_new - lp_old;  // NaN -> reject
+        if (!identity && !isfinite(lp_new) && a.status) {
+          atomicMin((unsigned long long*)&a.status[1],
+                    (unsigned long long)(((a.step_index + 1) << 32) | (unsigned long long)c));
+          atomicExch((unsigned long long*)&a.status[0], (unsigned long long)MPV_ERR_NONFINITE);
+        }
+        if (accept && !identity) {
+          const int k1 = s_site[j], k2 = s_site2[j];
+          a.bits[c * words + (k1 >> 5)] ^= 1u << (k1 & 31);
+          if (k2 >= 0) a.bits[c * words + (k2 >> 5)] ^= 1u << (k2 & 31);
+          a.out_lp[c] = lp_new;
+        }
+        if (accept && a.accepted) a.accepted[c] += 1;
+        const int64_t s1 = a.step_index + 1;
+        if (a.samples && a.thin > 0 && s1 % a.thin == 0) {
+          const int64_t gchain = a.chain_offset + c;
+          const int64_t count_c = a.sample_base + (gchain < a.sample_extra ? 1 : 0);
+          const int64_t offset_c =
+              gchain * a.sample_base + (gchain < a.sample_extra ? gchain : a.sample_extra) - a.row0;
+          const int64_t rr = a.round_offset + s1 / a.thin - 1;
+          if (rr < count_c)
+            for (int w = 0; w < words; ++w) a.samples[(offset_c + rr) * words + w] = a.bits[c * words + w];
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ---- f64 forward on the CUDA cores (local energies, parity): one CTA per
+// configuration, activations in shared memory, sites x channels over threads.
+__device__ __forceinline__ double gelu64(double z) {
+  return 0.5 * z * (1.0 + tanh(0.7978845608028654 * (z + 0.044715 * z * z * z)));
+}
+
+__global__ void __launch_bounds__(256) rescnn_f64_kernel(const double* __restrict__ theta, int L, int n_res,
+                                                         const uint32_t* __restrict__ bits, int64_t B, int words,
+                                                         double* __restrict__ out) {
+  extern __shared__ double sm64[];
+  const int N = L * L;
+  double* h = sm64;            // [N][16]
+  double* u = h + N * kF;      // [N][16]
+  double* v = u + N * kF;      // [N][16]
+  __shared__ double red[256];
+  const int tid = threadIdx.x;
+  for (int64_t cfg = blockIdx.x; cfg < B; cfg += gridDim.x) {
+    // input spins in u[:, 0]
+    for (int p = tid; p < N; p += blockDim.x) u[p * kF] = ((bits[cfg * words + (p >> 5)] >> (p & 31)) & 1u) ? -1.0 : 1.0;
+    __syncthreads();
+    const double* w = theta;
+    // embedding
+    for (int idx = tid; idx < N * kF; idx += blockDim.x) {
+      const int p = idx / kF, c = idx % kF, pr = p / L, pc = p % L;
+      double acc = w[kF * kTaps + c];  // b0
+      for (int d = 0; d < kTaps; ++d) {
+        const int q = ((pr + d / 3 - 1 + L) % L) * L + (pc + d % 3 - 1 + L) % L;
+        acc = fma(w[c * kTaps + d], u[q * kF], acc);
+      }
+      h[idx] = acc;
+    }
+    __syncthreads();
+    const double* pp = theta + kF * kTaps + kF;
+    auto conv = [&](const double* src, const double* wc, const double* bc, double* dst, bool add) {
+      for (int idx = tid; idx < N * kF; idx += blockDim.x) {
+        const int p = idx / kF, c = idx % kF, pr = p / L, pc = p % L;
+        double acc = bc[c];
+        for (int d = 0; d < kTaps; ++d) {
+          const int q = ((pr + d / 3 - 1 + L) % L) * L + (pc + d % 3 - 1 + L) % L;
+          const double* sq = src + q * kF;
+          const double* wr = wc + (size_t)c * kF * kTaps + d;
+          for (int ci = 0; ci < kF; ++ci) acc = fma(wr[ci * kTaps], sq[ci], acc);
+        }
+        dst[idx] = add ? dst[idx] + acc : acc;
+      }
+      __syncthreads();
+    };
+    auto ln = [&](const double* g, const double* be, double* dst, bool act) {
+      for (int p = tid; p < N; p += blockDim.x) {
+        double mu = 0.0, var = 0.0;
+        for (int c = 0; c < kF; ++c) mu += h[p * kF + c];
+        mu /= kF;
+        for (int c = 0; c < kF; ++c) var += (h[p * kF + c] - mu) * (h[p * kF + c] - mu);
+        const double rs = 1.0 / sqrt(var / kF + 1e-6);
+        for (int c = 0; c < kF; ++c) {
+          const double z = g[c] * (h[p * kF + c] - mu) * rs + be[c];
+          dst[p * kF + c] = act ? gelu64(z) : z;
+        }
+      }
+      __syncthreads();
+    };
+    for (int l = 0; l < n_res; ++l) {
+      const double* g = pp;
+      const double* be = pp + kF;
+      const double* wa = pp + 2 * kF;
+      const double* ba = wa + kF * kF * kTaps;
+      const double* wb = ba + kF;
+      const double* bb = wb + kF * kF * kTaps;
+      pp = bb + kF;
+      ln(g, be, u, true);
+      conv(u, wa, ba, v, false);
+      for (int idx = tid; idx < N * kF; idx += blockDim.x) v[idx] = gelu64(v[idx]);
+      __syncthreads();
+      conv(v, wb, bb, h, true);
+    }
+    ln(pp, pp + kF, u, false);
+    double acc = 0.0;
+    for (int idx = tid; idx < N * kF; idx += blockDim.x) acc += u[idx];
+    red[tid] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int i = 0; i < (int)blockDim.x; ++i) s += red[i];
+      out[cfg] = s;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace cnn
+
+using namespace cnn;
+
+size_t rescnn_blob_bytes(int L, int n_res) {
+  Shape s;
+  return make_shape(L, n_res, &s) ? s.blob_bytes : 0;
+}
+
+cudaError_t rescnn_launch(int L, int n_res, int fmt, const void* blob, uint32_t* bits, int64_t B, int words,
+                          double* lp, int64_t* accepted, int64_t* status, int mh, uint64_t key, int64_t chain_offset,
+                          int64_t init_draws, int64_t step_index, int proposal, uint32_t* samples, int64_t thin,
+                          int64_t sample_base, int64_t sample_extra, int64_t round_offset, int64_t row0,
+                          cudaStream_t st) {
+  Args a{};
+  if (!make_shape(L, n_res, &a.S)) return cudaErrorInvalidValue;
+  a.blob = (const uint8_t*)blob;
+  a.B = B; a.N = L * L; a.words = words; a.bits = bits; a.out_lp = lp; a.accepted = accepted; a.status = status;
+  a.mh = mh; a.key = key; a.chain_offset = chain_offset; a.init_draws = init_draws; a.step_index = step_index;
+  a.proposal = proposal; a.samples = samples; a.thin = thin; a.sample_base = sample_base;
+  a.sample_extra = sample_extra; a.round_offset = round_offset; a.row0 = row0;
+  const void* fn = fmt == MPV_FMT_BF16 ? (const void*)&rescnn_kernel<MPV_FMT_BF16> : (const void*)&rescnn_kernel<MPV_FMT_F16>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.S.smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t groups = (B + a.S.C - 1) / a.S.C;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(groups, n_sm));
+  void* args[] = {&a};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, a.S.smem, st);
+}
+
+cudaError_t rescnn_f64_launch(const double* theta, int L, int n_res, const uint32_t* bits, int64_t B, int words,
+                              double* out, cudaStream_t st) {
+  const size_t smem = 3ull * L * L * kF * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute((const void*)&rescnn_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(B, 148 * 8));
+  rescnn_f64_kernel<<<grid, 256, smem, st>>>(theta, L, n_res, bits, B, words, out);
+  return cudaGetLastError();
+}
+
+}  // namespace mpv

@@ -113,6 +113,41 @@ def local_energies(spec, log_amplitude, bits) -> np.ndarray:
     return eps[:, 0] + 1j * eps[:, 1]
 
 
+def _moments_out(x, fn, *args):
+    import torch
+
+    partials = torch.empty(int(nat.load().mpv_cg_partials_len()), dtype=torch.float64, device=x.device)
+    out = torch.empty(3, dtype=torch.float64, device=x.device)
+    nat.call(fn, *args, partials.data_ptr(), out.data_ptr(), nat.stream_handle(x.device))
+    return [float(v) for v in out.cpu()]
+
+
+def device_mc_error(eps_u, inverse, n_samples: int, n_chains: int) -> float:
+    """Split-chain MC error (vmc.py:592-604 with mc_error, vmc.py:311-317) on the
+    device: per-chain means of Re eps over the chain-major sample rows (sample
+    row -> unique row through `inverse`), then sqrt(var(means, ddof=1) / C) from
+    two-pass moments (mpv_chain_stats).  One chain: the samples themselves."""
+    import torch
+
+    eps_ri = torch.view_as_real(eps_u.contiguous()).contiguous() if eps_u.is_complex() else eps_u
+    inverse = inverse.to(torch.int64).contiguous()
+    C = n_chains if n_chains > 1 else int(n_samples)
+    base, extra = divmod(int(n_samples), C)
+    means = torch.empty(C, dtype=torch.float64, device=eps_u.device)
+    _, ss, c = _moments_out(eps_u, "mpv_chain_stats", eps_ri.data_ptr(), inverse.data_ptr(), C, 0, base, extra, 0,
+                            means.data_ptr())
+    if c < 2:
+        raise DegenerateInputError("need >= 2 values")
+    return float(np.sqrt(ss / (c - 1) / c))
+
+
+def device_std(x) -> float:
+    """Unbiased standard deviation of a real device vector (two-pass, mpv_moments)."""
+    x = x.contiguous()
+    _, ss, n = _moments_out(x, "mpv_moments", x.data_ptr(), x.numel())
+    return float(np.sqrt(ss / (n - 1)))
+
+
 def local_energy(spec, log_amplitude, x) -> complex:
     bits = x.bits()[None, :] if hasattr(x, "bits") and callable(x.bits) else np.atleast_2d(x)
     return complex(local_energies(spec, log_amplitude, bits)[0])
@@ -146,52 +181,70 @@ def _t(x, device):
     return torch.as_tensor(np.asarray(x), device=device)
 
 
+def _params_flat(params, dev):
+    """[a | b | W row-major] complex on the device (RbmParameters.flatten order)."""
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(params.flatten())).to(dev)
+
+
 def grad_log_psi_device(params, bits_u8, device=None):
     """O(x) = d log psi / d theta (rbm.py:307-325) for a (U, N) uint8 device
-    tensor: columns a, b, W row-major; complex128 [U, P] on the device."""
+    tensor: columns a, b, W row-major; complex128 [U, P] on the device
+    (mpv_logderiv_tanh for tanh(b + W x), mpv_logderiv_dense for the layout)."""
     import torch
 
     dev = bits_u8.device
-    x = bits_u8.to(torch.float64).to(torch.complex128)
-    w = _t(params.w, dev)
-    b = _t(params.b, dev)
-    th = x @ w.T + b[None, :]
-    t = torch.tanh(th)
-    U, N = x.shape
-    M = b.numel()
-    out = torch.empty((U, N + M + M * N), dtype=torch.complex128, device=dev)
-    out[:, :N] = x
-    out[:, N:N + M] = t
-    out[:, N + M:] = (t[:, :, None] * x[:, None, :]).reshape(U, M * N)
-    return out
+    U, N = bits_u8.shape
+    packed = torch.empty((U, (N + 31) // 32), dtype=torch.int32, device=dev)
+    if U:
+        nat.call("mpv_pack_bits", bits_u8.data_ptr(), U, N, packed.data_ptr(), nat.stream_handle(dev))
+    fo = FactoredLogDerivatives(params, packed)
+    return fo.dense()
 
 
 def forces(*, o, eps, weights=None):
-    """F_k = E[conj(O_k) eps] - E[conj(O_k)] E[eps] (vmc.py:145-165), device tensors."""
+    """F_k = E[conj(O_k) eps] - E[conj(O_k)] E[eps] (vmc.py:145-165), device tensors
+    (elementwise products and column sums; no BLAS)."""
     if o.shape[0] != eps.numel() or eps.numel() == 0:
         raise DegenerateInputError("need at least one (O, eps) pair")
-    oc = o.conj()
     if weights is None:
         if eps.numel() < 2:
             raise DegenerateInputError("need >= 2 samples")
-        return oc.T @ eps / eps.numel() - oc.mean(dim=0) * eps.mean()
-    w = weights.to(oc.dtype)
-    return (oc * w[:, None]).T @ eps - (w @ oc) * (w @ eps)
+        w = eps.new_full((eps.numel(),), 1.0 / eps.numel()).real
+    else:
+        w = weights.to(eps.real.dtype)
+    oc = o.conj()
+    we = w.to(eps.dtype) * eps
+    return (oc * we[:, None]).sum(dim=0) - (oc * w.to(eps.dtype)[:, None]).sum(dim=0) * we.sum()
 
 
 def s_matrix(*, o, weights=None):
-    """S = E[conj(O) O^T] - E[conj O] E[O^T], Hermitised (vmc.py:168-188)."""
+    """S = E[conj(O) O^T] - E[conj O] E[O^T], Hermitised (vmc.py:168-188): the
+    centred O and mpv_sr_smatrix (a tiled f64 kernel, Hermitian by construction)."""
+    import torch
+
     if o.shape[0] == 0:
         raise DegenerateInputError("empty sample set")
-    if weights is None:
-        c = o - o.mean(dim=0, keepdim=True)
-        s = c.conj().T @ c / o.shape[0]
-    else:
-        w = weights.to(o.dtype)
-        mean = w @ o
-        c = o - mean[None, :]
-        s = c.conj().T @ (c * w[:, None])
-    return 0.5 * (s + s.conj().T)
+    U, P = o.shape
+    w = (torch.full((U,), 1.0 / U, dtype=torch.float64, device=o.device) if weights is None
+         else weights.to(torch.float64).contiguous())
+    mean = (o * w.to(o.dtype)[:, None]).sum(dim=0)
+    c = (o - mean[None, :]).contiguous()
+    s = torch.empty((P, P), dtype=torch.complex128, device=o.device)
+    nat.call("mpv_sr_smatrix", c.data_ptr(), w.data_ptr(), U, P, s.data_ptr(), nat.stream_handle(o.device))
+    return s
+
+
+def s_matrix_centred(c, weights):
+    """sum_s w_s conj(C_s) C_s^T for an already centred dense C (mpv_sr_smatrix)."""
+    import torch
+
+    U, P = c.shape
+    w = weights.to(torch.float64).contiguous()
+    s = torch.empty((P, P), dtype=torch.complex128, device=c.device)
+    nat.call("mpv_sr_smatrix", c.contiguous().data_ptr(), w.data_ptr(), U, P, s.data_ptr(), nat.stream_handle(c.device))
+    return s
 
 
 @dataclass(frozen=True)
@@ -234,136 +287,224 @@ class FactoredLogDerivatives:
     """O(x) = [x, tanh(theta), tanh(theta) (x) x] (rbm.py:307-325) kept in factored
     form: the packed sample bits X and T = tanh(b + W x) (U, M) complex, never
     the (U, P) matrix (P = N + M + M N is 20,300 at config 2: O would be 21 GB
-    and S 6.6 GB).  O v and O^H u run in csrc/logderiv.cuh as DMMA GEMMs over
-    the bits with fused epilogues (mpv_logderiv_ov / mpv_logderiv_ohu).
+    and S 6.6 GB).  T comes from mpv_logderiv_tanh (DMMA GEMM over the bits,
+    complex tanh epilogue); O v and O^H u run in csrc/logderiv.cuh as DMMA GEMMs
+    over the bits with fused epilogues (weights and sum_s u_s fused).
     `reduce` (optional) all-reduces sums over samples across ranks."""
 
-    def __init__(self, params, bits_u8, packed=None, reduce=None):
+    def __init__(self, params, packed, reduce=None, bits_u8=None):
         import torch
 
-        dev = bits_u8.device
+        dev = packed.device
+        if packed.dtype == torch.uint8:  # (U, N) 0/1 rows: pack them on the device
+            bits_u8 = packed
+            U, N = packed.shape
+            packed = torch.empty((U, (N + 31) // 32), dtype=torch.int32, device=dev)
+            if U:
+                nat.call("mpv_pack_bits", bits_u8.contiguous().data_ptr(), U, N, packed.data_ptr(),
+                         nat.stream_handle(dev))
         self.N, self.M = params.n_visible, params.n_hidden
-        self.U = bits_u8.shape[0]
-        if packed is None:
-            packed = torch.empty((self.U, (self.N + 31) // 32), dtype=torch.int32, device=dev)
-            if self.U:
-                nat.call("mpv_pack_bits", bits_u8.data_ptr(), self.U, self.N, packed.data_ptr(), nat.stream_handle(dev))
+        self.P = self.N + self.M + self.M * self.N
         self.packed = packed.contiguous()
+        self.U = self.packed.shape[0]
         self.packed_u8 = bits_u8
-        x = bits_u8.to(torch.complex128)
-        self.t = torch.tanh(x @ _t(params.w, dev).T + _t(params.b, dev)[None, :]).contiguous()
+        self.device = dev
         self.scratch = torch.empty(nat.load().mpv_logderiv_scratch_bytes(self.U, self.N, self.M), dtype=torch.uint8,
                                    device=dev)
+        self.t = torch.empty((self.U, self.M), dtype=torch.complex128, device=dev)
+        nat.call("mpv_logderiv_tanh", _params_flat(params, dev).data_ptr(), self.packed.data_ptr(), self.U, self.N,
+                 self.M, self.t.data_ptr(), self.scratch.data_ptr(), nat.stream_handle(dev))
         self.reduce = reduce or (lambda z: z)
         self.reduce_is_local = reduce is None
-        self.device = dev
 
-    def o_v(self, v):
+    def _s(self):
+        return nat.stream_handle(self.device)
+
+    def o_v(self, v, w=None):
+        """q_s = w_s (O v)_s (w None: 1)."""
         import torch
 
-        v = v.contiguous()
+        v = v.resolve_conj().contiguous()
         q = torch.empty(self.U, dtype=torch.complex128, device=self.device)
         nat.call("mpv_logderiv_ov", self.t.data_ptr(), self.packed.data_ptr(), self.U, self.N, self.M, v.data_ptr(),
-                 q.data_ptr(), self.scratch.data_ptr(), nat.stream_handle(self.device))
+                 w.data_ptr() if w is not None else None, q.data_ptr(), self.scratch.data_ptr(), self._s())
         return q
 
-    def oh_u(self, u):
-        """sum_s conj(O_s) u_s (local sums; callers reduce)."""
+    def oh_u(self, u, w=None, with_sum=False):
+        """sum_s conj(O_s) w_s u_s (local sums; callers reduce); with_sum: also
+        sum_s w_s u_s, returned as element P of a P+1 vector."""
         import torch
 
-        u = u.contiguous()
-        out = torch.empty(self.N + self.M + self.M * self.N, dtype=torch.complex128, device=self.device)
+        u = u.resolve_conj().contiguous()
+        out = torch.empty(self.P + 1, dtype=torch.complex128, device=self.device)
         nat.call("mpv_logderiv_ohu", self.t.data_ptr(), self.packed.data_ptr(), self.U, self.N, self.M, u.data_ptr(),
-                 out.data_ptr(), self.scratch.data_ptr(), nat.stream_handle(self.device))
-        return out
+                 w.data_ptr() if w is not None else None, out.data_ptr(),
+                 out[self.P:].data_ptr() if with_sum else None, self.scratch.data_ptr(), self._s())
+        return out if with_sum else out[:self.P]
+
+    def dense(self, obar=None):
+        """O_s - obar as a dense complex [U, P] tensor (small P only)."""
+        import torch
+
+        o = torch.empty((self.U, self.P), dtype=torch.complex128, device=self.device)
+        nat.call("mpv_logderiv_dense", self.t.data_ptr(), self.packed.data_ptr(), self.U, self.N, self.M,
+                 obar.resolve_conj().contiguous().data_ptr() if obar is not None else None, o.data_ptr(),
+                 self._s())
+        return o
+
+    def statistics(self, eps, weights):
+        """(F, energy, obar) of the reference estimators (vmc.py:145-165) with one
+        reduction across ranks: F = sum_w conj(O) eps - (sum_w conj O)(sum_w eps),
+        obar = sum_w O."""
+        import torch
+
+        w = weights.to(torch.float64).contiguous()
+        ones = torch.ones(self.U, dtype=torch.complex128, device=self.device)
+        first = torch.cat([self.oh_u(eps, w, with_sum=True), self.oh_u(ones, w)])
+        first = self.reduce(first)
+        P = self.P
+        s_oe, e, s_o = first[:P], first[P], first[P + 1:]
+        return s_oe - s_o * e, e, s_o.conj().resolve_conj()
 
 
 def sr_step_cg(o: FactoredLogDerivatives, eps, weights, lambda_shift: float, eta: float,
-               tol: float = 1e-10, maxiter: int = 1000):
+               tol: float = 1e-10, maxiter: int = 1000, batch: int = 16):
     """SR update without forming S (matrix-free conjugate gradients on the
-    Hermitian positive-definite S + lambda I; beyond the
-    reference's dense Cholesky, vmc.py:202-229, which does not fit config 2).
-    Same estimators: F = sum_w conj(O) eps - (sum_w conj O)(sum_w eps),
-    S v = sum_w conj(O) (O v) - conj(Obar)(Obar v).  Returns (SrUpdate, F, energy)."""
+    Hermitian positive-definite S + lambda I; beyond the reference's dense
+    Cholesky, vmc.py:202-229, which does not fit config 2).  Same estimators:
+    F = sum_w conj(O) eps - (sum_w conj O)(sum_w eps),
+    S v = sum_w conj(O) (O v) - conj(Obar)(Obar v).
+
+    Device-resident (csrc/sr.cuh): the CG scalars and the convergence flag stay
+    on the device, a converged solve turns the remaining iterations of a batch
+    into no-ops, and the host reads the flag once per `batch` iterations
+    (single process: mpv_cg_run; across ranks: one all-reduce of O^H(w O p)
+    per iteration between mpv_cg_apply and mpv_cg_step).
+    Returns (SrUpdate, F, energy)."""
     import torch
 
     if lambda_shift < 0:
         raise ValueError("lambda must be >= 0")
     if eta <= 0:
         raise ValueError("eta must be > 0")
-    w = weights.to(torch.complex128)
-    s_oe = o.reduce(o.oh_u(w * eps))
-    s_o = o.reduce(o.oh_u(w))
-    e = o.reduce((w @ eps).reshape(1))[0]
-    f = s_oe - s_o * e
-    obar = s_o.conj()  # sum_w O
-
-    def apply(v):
-        return o.reduce(o.oh_u(w * o.o_v(v))) - obar.conj() * (obar @ v) + lambda_shift * v
-
-    g = torch.zeros_like(f)
-    r = f.clone()
-    pvec = r.clone()
-    rr = torch.vdot(r, r).real
-    fn = float(torch.linalg.norm(f))
-    it = 0
-    while it < maxiter and fn > 0 and float(rr) ** 0.5 > tol * fn:
-        ap = apply(pvec)
-        alpha = rr / torch.vdot(pvec, ap).real
-        g = g + alpha * pvec
-        r = r - alpha * ap
-        rr_new = torch.vdot(r, r).real
-        pvec = r + (rr_new / rr) * pvec
-        rr = rr_new
-        it += 1
-    residual = float(torch.linalg.norm(apply(g) - f)) / fn if fn > 0 else 0.0
+    w = weights.to(torch.float64).contiguous()
+    f, e, obar = o.statistics(eps, w)
+    f = f.resolve_conj().contiguous()
+    obar = obar.resolve_conj().contiguous()
+    dev, P = o.device, o.P
+    c128 = lambda n: torch.empty(n, dtype=torch.complex128, device=dev)  # noqa: E731
+    g, r, pv, ap, q = c128(P), c128(P), c128(P), c128(P), c128(max(o.U, 1))
+    yy = c128(P + 1)
+    partials = torch.empty(int(nat.load().mpv_cg_partials_len()), dtype=torch.float64, device=dev)
+    scalars = torch.zeros(8, dtype=torch.float64, device=dev)
+    cg = nat.CG(o.N, o.M, o.U, o.t.data_ptr(), o.packed.data_ptr(), w.data_ptr(), obar.data_ptr(),
+                float(lambda_shift), g.data_ptr(), r.data_ptr(), pv.data_ptr(), ap.data_ptr(), yy.data_ptr(),
+                yy[P:].data_ptr(), q.data_ptr(), partials.data_ptr(), scalars.data_ptr(), o.scratch.data_ptr(),
+                o.scratch.numel())
+    cgp = ctypes.byref(cg)
+    st = nat.stream_handle(dev)
+    nat.call("mpv_cg_init", cgp, f.data_ptr(), float(tol), int(maxiter), st)
+    host = torch.empty(8, dtype=torch.float64, pin_memory=True)
+    while True:
+        if o.reduce_is_local:
+            nat.call("mpv_cg_run", cgp, int(batch), st)
+        else:
+            for _ in range(batch):
+                nat.call("mpv_cg_apply", cgp, pv.data_ptr(), yy.data_ptr(), yy[P:].data_ptr(), st)
+                o.reduce(yy)
+                nat.call("mpv_cg_step", cgp, st)
+        host.copy_(scalars, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        if host[3] != 0.0:
+            break
+    it = int(host[2])
+    fn = float(torch.linalg.vector_norm(f))
+    # residual of the returned g with one more application of S + lambda
+    nat.call("mpv_cg_apply", cgp, g.data_ptr(), yy.data_ptr(), yy[P:].data_ptr(), st)
+    o.reduce(yy)
+    nat.call("mpv_cg_apply_finish", cgp, g.data_ptr(), yy.data_ptr(), yy[P:].data_ptr(), ap.data_ptr(), st)
+    residual = float(torch.linalg.vector_norm(ap - f)) / fn if fn > 0 else 0.0
     if fn > 0 and residual > max(10 * tol, 1e-9):
         raise SolverError(f"SR conjugate-gradient residual {residual:.3e} after {it} iterations")
     return SrUpdate(g, float("nan"), residual, lambda_shift, eta, it), f, float(e.real)
 
 
-def sr_step_minsr(o: FactoredLogDerivatives, eps, weights, lambda_shift: float, eta: float):
+def _gather_rows(x, group=None):
+    """Concatenate a per-rank tensor along dim 0 over all ranks (rank order);
+    returns (all rows, this rank's first row).  Ranks may hold different counts."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    n = torch.tensor([x.shape[0]], dtype=torch.int64, device=x.device)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(counts, n, group=group)
+    counts = [int(c) for c in counts]
+    nmax = max(counts)
+    pad = torch.zeros((nmax,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    pad[:x.shape[0]] = x
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    rank = dist.get_rank(group)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)]), sum(counts[:rank])
+
+
+def sr_step_minsr(o: FactoredLogDerivatives, eps, weights, lambda_shift: float, eta: float,
+                  precision: str = "f64", group=None):
     """The same SR update solved in sample space (minSR; beyond the reference).
 
     With O~ = W^{1/2} (O - 1 obar^T) the reference's estimators are S = O~^H O~
     and F = O~^H e~ (e~ = W^{1/2} (eps - ebar)), and the push-through identity
     gives g = (S + lambda)^-1 F = O~^H (O~ O~^H + lambda)^-1 e~ exactly: a U x U
     Cholesky instead of a P x P one (cheaper whenever U < P).  The Gram matrix
-    never needs O: O O^H = X X^T + (T T^H) * (1 + X X^T) (elementwise), one real
-    and one complex GEMM (cuBLAS); O^H y runs in csrc/logderiv.cuh.
-    Single process only (the U x U system couples every rank's samples)."""
+    never needs O: mpv_minsr_gram forms it from the factors (common set bits of
+    the packed rows, T T^H) with the centring and weights fused, in f64 or
+    (precision="f32", the north star's "minSR in f32") f32 with an f32 solve.
+    Across ranks (o.reduce set, `group`): the factors are all-gathered, every rank
+    builds its own block of rows of the U x U matrix, the rows are all-gathered,
+    every rank solves the same system, and O^H y sums per rank then all-reduces."""
     import torch
 
     if lambda_shift < 0:
         raise ValueError("lambda must be >= 0")
     if eta <= 0:
         raise ValueError("eta must be > 0")
-    if not o.reduce_is_local:
-        raise ValueError("minSR couples all samples: use sr_solver='cg' or 'dense' across ranks")
-    w = weights.to(torch.float64)
-    wc = w.to(torch.complex128)
-    obar = o.oh_u(wc).conj()  # sum_w O
-    e = wc @ eps
-    xr = o.packed_u8.to(torch.float64)
-    xx = xr @ xr.T
-    gram = xx.to(torch.complex128) + (o.t @ o.t.mH) * (1.0 + xx)
-    c = o.o_v(obar.conj())  # c_s = sum_j O_sj conj(obar_j)
-    ones = torch.ones_like(c)
-    k = gram - c[:, None] * ones[None, :] - ones[:, None] * c.conj()[None, :] + torch.vdot(obar, obar).real
-    sw = torch.sqrt(w).to(torch.complex128)
-    k = sw[:, None] * k * sw[None, :]
+    if precision not in ("f64", "f32"):
+        raise ValueError("precision must be 'f64' or 'f32'")
+    w = weights.to(torch.float64).contiguous()
+    f, e, obar = o.statistics(eps, w)
+    d = o.o_v(obar.conj())  # d_s = (O conj(obar))_s
+    sw = torch.sqrt(w)
+    et = (sw.to(torch.complex128) * (eps - e)).contiguous()
+    sharded = not o.reduce_is_local
+    if sharded:
+        t_all, row0 = _gather_rows(o.t, group)
+        bits_all, _ = _gather_rows(o.packed, group)
+        d_all, _ = _gather_rows(d, group)
+        w_all, _ = _gather_rows(w, group)
+        et_all, _ = _gather_rows(et, group)
+    else:
+        t_all, bits_all, d_all, w_all, et_all, row0 = o.t, o.packed, d, w, et, 0
+    U_all = t_all.shape[0]
+    ctype = torch.complex64 if precision == "f32" else torch.complex128
+    rows = torch.empty((o.U, U_all), dtype=ctype, device=o.device)
+    obar2 = float(torch.vdot(obar, obar).real)
+    nat.call("mpv_minsr_gram", o.t.data_ptr(), o.packed.data_ptr(), o.U, row0, t_all.contiguous().data_ptr(),
+             bits_all.contiguous().data_ptr(), U_all, o.N, o.M, d_all.contiguous().data_ptr(),
+             w_all.contiguous().data_ptr(), obar2, float(lambda_shift), 1 if precision == "f32" else 0,
+             rows.data_ptr(), nat.stream_handle(o.device))
+    k = _gather_rows(rows, group)[0] if sharded else rows
     k = 0.5 * (k + k.mH)
-    k += lambda_shift * torch.eye(k.shape[0], dtype=k.dtype, device=k.device)
-    et = sw * (eps - e)
+    rhs = et_all.to(ctype)
     L, info = torch.linalg.cholesky_ex(k)
     if int(info) != 0:
         raise SolverError("sample-space matrix O~ O~^H + lambda I is not positive definite")
-    y = torch.cholesky_solve(et[:, None], L)[:, 0]
-    y = y + torch.cholesky_solve((et - k @ y)[:, None], L)[:, 0]  # one refinement pass
-    z = sw * y
-    g = o.oh_u(z) - obar.conj() * z.sum()
-    f = o.oh_u(wc * eps) - o.oh_u(wc) * e
-    residual = float(torch.linalg.norm(k @ y - et) / max(float(torch.linalg.norm(et)), 1e-300))
+    y = torch.cholesky_solve(rhs[:, None], L)[:, 0]
+    y = y + torch.cholesky_solve((rhs - k @ y)[:, None], L)[:, 0]  # one refinement pass
+    residual = float(torch.linalg.norm(k @ y - rhs) / max(float(torch.linalg.norm(rhs)), 1e-300))
+    z = (sw.to(torch.complex128) * y[row0:row0 + o.U].to(torch.complex128)).contiguous()
+    gz = o.reduce(o.oh_u(z, with_sum=True))
+    g = gz[:o.P] - obar.conj() * gz[o.P]
     return SrUpdate(g, float("nan"), residual, lambda_shift, eta), f, float(e.real)
 
 
@@ -396,6 +537,7 @@ class TrainConfig:
     sr_solver: str = "dense"  # "dense" (reference: Cholesky on S), "cg" (matrix-free) or "minsr" (sample space)
     cg_tol: float = 1e-10
     cg_maxiter: int = 1000
+    minsr_precision: str = "f64"  # "f64" or "f32" (Gram matrix and solve)
 
     def __post_init__(self):
         if self.n_steps < 1 or self.n_samples < 2:
@@ -462,8 +604,6 @@ def train(config: TrainConfig, device=None, group=None, local: bool = False) -> 
     else:
         c_off, c_cnt = parallel.shard(n_chains, rank, world)
         counts = parallel.chain_counts(config.n_samples, n_chains, c_off, c_cnt)
-        chain_ids = torch.as_tensor(np.repeat(np.arange(c_cnt), counts), device=dev)
-        per_chain = torch.as_tensor(counts, device=dev, dtype=torch.float64)
     ensemble = None
     records, force_history = [], []
     for step in range(config.n_steps):
@@ -507,27 +647,22 @@ def train(config: TrainConfig, device=None, group=None, local: bool = False) -> 
         if int(status[0]) != 0:
             raise EvaluationFailureError("non-finite local energy", context={"step": step})
         eps = torch.complex(eps_ri[:, 0], eps_ri[:, 1])
-        u8 = torch.empty((uniq.shape[0], n), dtype=torch.uint8, device=dev)
-        nat.call("mpv_unpack_bits", uniq.data_ptr(), uniq.shape[0], n, u8.data_ptr(), nat.stream_handle(dev))
+        red = (lambda z: parallel.all_reduce_sum(z, group)) if world > 1 else None
+        fo = FactoredLogDerivatives(params, uniq, red)
         if config.sr_solver == "cg":
-            red = (lambda z: parallel.all_reduce_sum(z, group)) if world > 1 else None
-            fo = FactoredLogDerivatives(params, u8, uniq, red)
             update, f, energy = sr_step_cg(fo, eps, est_w, config.lambda_shift, config.eta, config.cg_tol,
                                            config.cg_maxiter)
         elif config.sr_solver == "minsr":
-            if world > 1:
-                raise ValueError("sr_solver='minsr' is single-process (use 'cg' or 'dense' across ranks)")
-            update, f, energy = sr_step_minsr(FactoredLogDerivatives(params, u8, uniq), eps, est_w,
-                                              config.lambda_shift, config.eta)
+            update, f, energy = sr_step_minsr(fo, eps, est_w, config.lambda_shift, config.eta,
+                                              config.minsr_precision, group)
         else:
-            o = grad_log_psi_device(params, u8)
+            # the reference's dense path: F and obar from the factored kernels, the
+            # centred dense O, S = sum_w conj(C) C^T (mpv_sr_smatrix), Cholesky
+            f, e_glob, obar = fo.statistics(eps, est_w)
+            s = s_matrix_centred(fo.dense(obar), est_w)
             if world > 1:
-                f, s, e_glob = parallel.sharded_statistics(o, eps, est_w, group)
-                energy = float(e_glob)
-            else:
-                f = forces(o=o, eps=eps, weights=est_w)
-                s = s_matrix(o=o, weights=est_w)
-                energy = float((est_w.to(eps.dtype) @ eps).real)
+                parallel.all_reduce_sum(s, group)
+            energy = float(e_glob.real)
             update = sr_step(f, s, config.lambda_shift, config.eta, config.compute_kappa)
         theta = params.flatten() - config.eta * update.g.cpu().numpy()
         nvtx.range_pop()
@@ -537,12 +672,7 @@ def train(config: TrainConfig, device=None, group=None, local: bool = False) -> 
         elif world > 1:
             err = parallel.energy_statistics(eps.real[inverse], counts, 0, 1, group)["mc_error"]
         else:
-            stream = eps.real[inverse]
-            if n_chains > 1:
-                sums = torch.zeros(n_chains, dtype=torch.float64, device=dev).index_add_(0, chain_ids, stream)
-                err = mc_error((sums / per_chain).cpu().numpy())
-            else:
-                err = mc_error(stream.cpu().numpy())
+            err = device_mc_error(eps, inverse, config.n_samples, n_chains)
         if config.track_forces:
             force_history.append(f.cpu().numpy())
         if step % config.log_every == 0 or step == config.n_steps - 1:
@@ -559,7 +689,7 @@ def train(config: TrainConfig, device=None, group=None, local: bool = False) -> 
                     m1, m2, cnt_d = (float(x) for x in mom)
                     sigma_hat = float(np.sqrt(max(m2 - m1 * m1 / cnt_d, 0.0) / (cnt_d - 1))) if cnt_d > 1 else 0.0
                 else:
-                    sigma_hat = float(delta.std()) if delta.numel() > 1 else 0.0
+                    sigma_hat = device_std(delta) if delta.numel() > 1 else 0.0
             record = {"step": step, "energy": energy, "mc_error": err, "acceptance": acceptance,
                       "sigma_hat": sigma_hat, "bound_pinsker": pinsker_tv_bound(sigma_hat),
                       "bound_theorem3": theorem3_gaussian_bound(sigma_hat, 0.0, 0.0), "kappa": update.kappa}

@@ -44,7 +44,7 @@ def _worker(rank, world, port, q, solver):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("solver", ["dense", "cg", "exact"])
+@pytest.mark.parametrize("solver", ["dense", "cg", "exact", "minsr"])
 def test_two_rank_training_matches_single(cuda, solver):
     from paper_2601_20782_b200 import vmc
 
