@@ -294,6 +294,30 @@ int mpv_forward_tc_prepare(int N, int M, int fmt, const double* params, void* we
 int mpv_forward_tc(int N, int M, int fmt, const void* weights, const uint32_t* bits, int64_t B, double* out_lp,
                    double* out_re, double* out_im, int max_ctas, void* stream);
 
+/* ---- ResCNN ansatz (beyond the reference: PAPER.md:876-890, BASELINE configs[3]) ----
+ * log psi(x) = sum LN(h_n), h_0 = Conv(1 - 2x), h_{l+1} = h_l + Conv(GELU(Conv(GELU(LN(h_l)))))
+ * on an L x L periodic lattice (3 <= L <= 30), 16 channels, 3x3 kernels, n_res <= 8 blocks.
+ * `blob` (>= mpv_rescnn_blob_bytes(L, n_res), built by rescnn.py from the f64
+ * parameters): per convolution and tap a 16 x 16 f16/bf16 B operand in the
+ * tcgen05 K-major core-matrix layout, then f32 vectors (per LN: running
+ * residual bias, gain, shift; per block: the first convolution's bias).
+ * mpv_rescnn_forward: tcgen05 forward (f16/bf16 operands, f32 accumulation),
+ * out_lp = 2 log psi.  mpv_rescnn_forward_f64: the f64 forward on the CUDA cores
+ * (theta = the flat parameter vector of oracle/rescnn.py), out = log psi.
+ * mpv_rescnn_mh_sweep: n_steps MH steps (ref: sampler.py:111-133, the
+ * reference's streams and f64 accept test) with the tcgen05 evaluator, one
+ * fused propose / evaluate / accept launch per step, samples recorded as
+ * mpv_mh_sweep does; the cached log p is refreshed first. */
+size_t mpv_rescnn_blob_bytes(int L, int n_res);
+int mpv_rescnn_forward(int L, int n_res, int fmt, const void* blob, const uint32_t* bits, int64_t B, double* out_lp,
+                       int64_t* status, void* stream);
+int mpv_rescnn_forward_f64(const double* theta, int L, int n_res, const uint32_t* bits, int64_t B, double* out,
+                           void* stream);
+int mpv_rescnn_mh_sweep(int L, int n_res, int fmt, const void* blob, const mpv_chains* ch, uint64_t key, int proposal,
+                        int64_t init_draws, int64_t step_index, int64_t n_steps, int64_t thin, uint32_t* samples,
+                        int64_t n_samples_total, int64_t n_chains_total, int64_t round_offset, int64_t row0,
+                        void* stream);
+
 /* ---- helpers ---- */
 int mpv_unpack_bits(const uint32_t* words, int64_t B, int N, uint8_t* out, void* stream);
 int mpv_pack_bits(const uint8_t* bits, int64_t B, int N, uint32_t* out, void* stream);

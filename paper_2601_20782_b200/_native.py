@@ -97,6 +97,11 @@ _SIGNATURES = {
     "mpv_forward_tc_prepare": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
     "mpv_forward_tc": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _vp,
                                       ctypes.c_int, _vp]),
+    "mpv_rescnn_blob_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int]),
+    "mpv_rescnn_forward": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "mpv_rescnn_forward_f64": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _i64, _vp, _vp]),
+    "mpv_rescnn_mh_sweep": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.POINTER(Chains), _u64,
+                                           ctypes.c_int, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),
     "mpv_unpack_bits": (ctypes.c_int, [_vp, _i64, ctypes.c_int, _vp, _vp]),
     "mpv_pack_bits": (ctypes.c_int, [_vp, _i64, ctypes.c_int, _vp, _vp]),
     "mpv_sum_i64": (ctypes.c_int, [_vp, _i64, _vp, _vp]),

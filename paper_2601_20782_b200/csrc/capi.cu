@@ -23,6 +23,14 @@ MPV_DECL(f64, f64)
 #undef MPV_DECL
 
 size_t forward_tc_weights_bytes(int N, int M);
+size_t rescnn_blob_bytes(int L, int n_res);
+cudaError_t rescnn_launch(int L, int n_res, int fmt, const void* blob, uint32_t* bits, int64_t B, int words,
+                          double* lp, int64_t* accepted, int64_t* status, int mh, uint64_t key, int64_t chain_offset,
+                          int64_t init_draws, int64_t step_index, int proposal, uint32_t* samples, int64_t thin,
+                          int64_t sample_base, int64_t sample_extra, int64_t round_offset, int64_t row0,
+                          int64_t local_step1, cudaStream_t st);
+cudaError_t rescnn_f64_launch(const double* theta, int L, int n_res, const uint32_t* bits, int64_t B, int words,
+                              double* out, cudaStream_t st);
 cudaError_t forward_tc_prepare(int N, int M, int fmt, const double* params, void* weights, cudaStream_t st);
 cudaError_t forward_tc_launch(int N, int M, int fmt, const void* weights, const uint32_t* bits, int64_t B,
                               double* out_lp, double* out_re, double* out_im, int max_ctas, cudaStream_t st);
@@ -953,6 +961,57 @@ int mpv_forward_tc(int N, int M, int fmt, const void* weights, const uint32_t* b
   const cudaError_t e =
       forward_tc_launch(N, M, fmt, weights, bits, B, out_lp, out_re, out_im, max_ctas, (cudaStream_t)stream);
   if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("forward_tc: ") + cudaGetErrorString(e));
+  return MPV_OK;
+}
+
+// ---- ResCNN (rescnn.cu) ----
+size_t mpv_rescnn_blob_bytes(int L, int n_res) { return rescnn_blob_bytes(L, n_res); }
+
+int mpv_rescnn_forward(int L, int n_res, int fmt, const void* blob, const uint32_t* bits, int64_t B, double* out_lp,
+                       int64_t* status, void* stream) {
+  if (!blob || !bits || !out_lp || B < 0 || (fmt != MPV_FMT_F16 && fmt != MPV_FMT_BF16) || !rescnn_blob_bytes(L, n_res))
+    return fail(MPV_ERR_ARGS, "rescnn_forward: bad args (f16/bf16, 3 <= L <= 30, n_res <= 8)");
+  if (B == 0) return MPV_OK;
+  const cudaError_t e = rescnn_launch(L, n_res, fmt, blob, const_cast<uint32_t*>(bits), B, (L * L + 31) / 32, out_lp,
+                                      nullptr, status, 0, 0, 0, 0, 0, 0, nullptr, 0, 0, 0, 0, 0, 0, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("rescnn_forward: ") + cudaGetErrorString(e));
+  return MPV_OK;
+}
+
+int mpv_rescnn_forward_f64(const double* theta, int L, int n_res, const uint32_t* bits, int64_t B, double* out,
+                           void* stream) {
+  if (!theta || !bits || !out || B < 0 || L < 3 || L > 30 || n_res < 0 || n_res > 8)
+    return fail(MPV_ERR_ARGS, "rescnn_forward_f64: bad args");
+  if (B == 0) return MPV_OK;
+  const cudaError_t e = rescnn_f64_launch(theta, L, n_res, bits, B, (L * L + 31) / 32, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("rescnn_forward_f64: ") + cudaGetErrorString(e));
+  return MPV_OK;
+}
+
+int mpv_rescnn_mh_sweep(int L, int n_res, int fmt, const void* blob, const mpv_chains* ch, uint64_t key, int proposal,
+                        int64_t init_draws, int64_t step_index, int64_t n_steps, int64_t thin, uint32_t* samples,
+                        int64_t n_samples_total, int64_t n_chains_total, int64_t round_offset, int64_t row0,
+                        void* stream) {
+  if (!blob || !ch || !ch->bits || !ch->log_probs || ch->n_sites != L * L || ch->words != (L * L + 31) / 32 ||
+      n_steps < 0 || thin < 0 || (samples && thin < 1) || (fmt != MPV_FMT_F16 && fmt != MPV_FMT_BF16) ||
+      !rescnn_blob_bytes(L, n_res) || (proposal != MPV_PROPOSAL_FLIP && proposal != MPV_PROPOSAL_EXCHANGE))
+    return fail(MPV_ERR_ARGS, "rescnn_mh_sweep: bad args");
+  if (ch->n_chains == 0) return MPV_OK;
+  int64_t base = 0, extra = 0;
+  if (samples) {
+    if (n_chains_total < 1) return fail(MPV_ERR_ARGS, "rescnn_mh_sweep: n_chains_total");
+    base = n_samples_total / n_chains_total;
+    extra = n_samples_total % n_chains_total;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  // the cached log p of the current configurations (set_evaluator semantics)
+  cudaError_t e = rescnn_launch(L, n_res, fmt, blob, ch->bits, ch->n_chains, ch->words, ch->log_probs, nullptr,
+                                ch->status, 0, 0, 0, 0, 0, 0, nullptr, 0, 0, 0, 0, 0, 0, st);
+  for (int64_t s = 0; e == cudaSuccess && s < n_steps; ++s)
+    e = rescnn_launch(L, n_res, fmt, blob, ch->bits, ch->n_chains, ch->words, ch->log_probs, ch->accepted,
+                      ch->status, 1, key, ch->chain_offset, init_draws, step_index + s, proposal, samples, thin, base,
+                      extra, round_offset, row0, s + 1, st);
+  if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("rescnn_mh_sweep: ") + cudaGetErrorString(e));
   return MPV_OK;
 }
 

@@ -47,6 +47,7 @@ constexpr int kTaps = 9;         // 3x3
 constexpr int kRowsMax = 2048;   // 16 MMA tiles
 constexpr int kThreads = 512;    // 16 warps: TMEM lane quarter x tile group
 constexpr int kTapBytes = kF * kF * 2;  // one B block (16 x 16 f16)
+constexpr int kMaxC = 96;        // configurations per CTA (L >= 3: <= 81)
 
 struct Shape {
   int L, Lp, R, n_res, C, tiles, margin;  // R = Lp^2 rows per configuration
@@ -65,7 +66,7 @@ inline bool make_shape(int L, int n_res, Shape* s) {
   s->R = s->Lp * s->Lp;
   s->n_res = n_res;
   s->C = kRowsMax / s->R;
-  if (s->C < 1) return false;
+  if (s->C < 1 || s->C > kMaxC) return false;
   s->tiles = (s->C * s->R + 127) / 128;
   s->margin = (s->Lp + 1 + 7) / 8 * 8;
   s->n_conv = 1 + 2 * n_res;
@@ -170,6 +171,7 @@ struct Args {
   int proposal;
   uint32_t* samples;
   int64_t thin, sample_base, sample_extra, round_offset, row0;
+  int64_t local_step1;       // 1-based step within the recording launch
 };
 
 template <int FMT>
@@ -177,10 +179,9 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bar_mma;
-  __shared__ int s_site[64];       // per configuration: flipped sites (MH), -1 none
-  __shared__ int s_site2[64];
-  __shared__ double s_logu[64];
-  __shared__ int s_bad[64];
+  __shared__ int s_site[kMaxC];    // per configuration: flipped sites (MH), -1 none
+  __shared__ int s_site2[kMaxC];
+  __shared__ double s_logu[kMaxC];
   const Shape& S = a.S;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Lp = S.Lp, R = S.R, C = S.C, N = a.N, words = a.words;
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
           a.out_lp[c] = lp_new;
         }
         if (accept && a.accepted) a.accepted[c] += 1;
-        const int64_t s1 = a.step_index + 1;
+        const int64_t s1 = a.local_step1;
         if (a.samples && a.thin > 0 && s1 % a.thin == 0) {
           const int64_t gchain = a.chain_offset + c;
           const int64_t count_c = a.sample_base + (gchain < a.sample_extra ? 1 : 0);
@@ -492,14 +493,14 @@ cudaError_t rescnn_launch(int L, int n_res, int fmt, const void* blob, uint32_t*
                           double* lp, int64_t* accepted, int64_t* status, int mh, uint64_t key, int64_t chain_offset,
                           int64_t init_draws, int64_t step_index, int proposal, uint32_t* samples, int64_t thin,
                           int64_t sample_base, int64_t sample_extra, int64_t round_offset, int64_t row0,
-                          cudaStream_t st) {
+                          int64_t local_step1, cudaStream_t st) {
   Args a{};
   if (!make_shape(L, n_res, &a.S)) return cudaErrorInvalidValue;
   a.blob = (const uint8_t*)blob;
   a.B = B; a.N = L * L; a.words = words; a.bits = bits; a.out_lp = lp; a.accepted = accepted; a.status = status;
   a.mh = mh; a.key = key; a.chain_offset = chain_offset; a.init_draws = init_draws; a.step_index = step_index;
   a.proposal = proposal; a.samples = samples; a.thin = thin; a.sample_base = sample_base;
-  a.sample_extra = sample_extra; a.round_offset = round_offset; a.row0 = row0;
+  a.sample_extra = sample_extra; a.round_offset = round_offset; a.row0 = row0; a.local_step1 = local_step1;
   const void* fn = fmt == MPV_FMT_BF16 ? (const void*)&rescnn_kernel<MPV_FMT_BF16> : (const void*)&rescnn_kernel<MPV_FMT_F16>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.S.smem);
   if (e != cudaSuccess) return e;

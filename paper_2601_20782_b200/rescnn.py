@@ -1,0 +1,277 @@
+"""ResCNN neural quantum state on the B200 (beyond the reference: the
+convolutional ansatz of /root/reference/PAPER.md:876-890, used for BASELINE
+configs[3]; the reference package has none, so parity is pinned by the f64
+restatement oracle/rescnn.py and by exact H psi on enumerable lattices).
+
+    s = 1 - 2x,  h0 = Conv(s),  h_{l+1} = h_l + Conv(GELU(Conv(GELU(LN(h_l))))),
+    log psi(x) = sum_{sites, channels} LN(h_n)           (real; log p = 2 log psi)
+
+3x3 periodic convolutions with bias, 16 channels, LN over the channels of a
+site (learned gain / shift, eps 1e-6), GELU in its tanh form.  Evaluation runs
+in the CUDA library (csrc/rescnn.cu): a tcgen05 tensor-core forward with
+f16/bf16 operands and f32 accumulation (the sampler's evaluator, fused with the
+MH step), and an f64 CUDA-core forward (local energies, parity).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .errors import EvaluationFailureError
+from .precision import FloatFormat, make_rounder
+from .rng import gaussian_field
+
+FILTERS = 16
+TAPS = 9
+
+
+def param_layout(n_res: int):
+    """(name, shape) of the flat parameter vector, in order (oracle/rescnn.py)."""
+    F, T = FILTERS, TAPS
+    out = [("w0", (F, 1, T)), ("b0", (F,))]
+    for i in range(n_res):
+        out += [(f"g{i}", (F,)), (f"be{i}", (F,)), (f"w{i}a", (F, F, T)), (f"b{i}a", (F,)),
+                (f"w{i}b", (F, F, T)), (f"b{i}b", (F,))]
+    return out + [("gf", (F,)), ("bef", (F,))]
+
+
+def n_params(n_res: int) -> int:
+    return int(sum(np.prod(s) for _, s in param_layout(n_res)))
+
+
+@dataclass(frozen=True)
+class ResCnnParameters:
+    """Flat real f64 parameters of a ResCNN on an L x L periodic lattice."""
+
+    theta: np.ndarray
+    L: int
+    n_res: int = 4
+
+    def __post_init__(self):
+        th = np.ascontiguousarray(self.theta, dtype=np.float64)
+        if th.shape != (n_params(self.n_res),):
+            raise ValueError(f"expected {n_params(self.n_res)} parameters, got {th.shape}")
+        if not np.all(np.isfinite(th)):
+            raise ValueError("non-finite parameters")
+        if not 3 <= self.L <= 30:
+            raise ValueError("3 <= L <= 30")
+        object.__setattr__(self, "theta", th)
+
+    @property
+    def n_visible(self) -> int:
+        return self.L * self.L
+
+    def unflatten(self) -> dict:
+        out, k = {}, 0
+        for name, shape in param_layout(self.n_res):
+            size = int(np.prod(shape))
+            out[name] = self.theta[k:k + size].reshape(shape)
+            k += size
+        return out
+
+
+def random_parameters(L: int, n_res: int, key, scale: float = 1.0) -> ResCnnParameters:
+    """Counter-based Gaussian init (the rbm.random_parameters field, rng.py:86-96):
+    conv weights N(0, scale^2 / fan_in), biases N(0, (0.1 scale)^2), LN gains
+    1 + N(0, 0.1^2), shifts N(0, 0.1^2)."""
+    z = gaussian_field(key, np.arange(n_params(n_res)), 1.0)
+    theta = np.empty_like(z)
+    k = 0
+    for name, shape in param_layout(n_res):
+        size = int(np.prod(shape))
+        v = z[k:k + size]
+        if name.startswith("w"):
+            fan_in = shape[1] * shape[2]
+            v = v * scale / np.sqrt(fan_in)
+        elif name.startswith("g"):
+            v = 1.0 + 0.1 * v
+        elif name.startswith("be"):
+            v = 0.1 * v
+        else:
+            v = 0.1 * scale * v
+        theta[k:k + size] = v
+        k += size
+    return ResCnnParameters(theta, L, n_res)
+
+
+def _bits16(values, fmt: FloatFormat) -> np.ndarray:
+    """RNE rounding to f16/bf16 (round_parameters semantics), as uint16 bit patterns."""
+    v = np.asarray(values, dtype=np.float64)
+    if fmt.name == "f16":
+        return v.astype(np.float16).view(np.uint16)
+    r = make_rounder(fmt)(v).astype(np.float32)  # exact bf16 values
+    return (r.view(np.uint32) >> 16).astype(np.uint16)
+
+
+def rounded_parameters(params: ResCnnParameters, fmt: FloatFormat) -> ResCnnParameters:
+    """The parameters the tensor-core forward uses: convolution weights rounded
+    to fmt (RNE), vectors rounded to f32 (the epilogue's precision)."""
+    out = params.theta.copy()
+    k = 0
+    rnd = make_rounder(fmt)
+    for name, shape in param_layout(params.n_res):
+        size = int(np.prod(shape))
+        seg = out[k:k + size]
+        out[k:k + size] = rnd(seg) if name.startswith("w") else seg.astype(np.float32).astype(np.float64)
+        k += size
+    return ResCnnParameters(out, params.L, params.n_res)
+
+
+def make_blob(params: ResCnnParameters, fmt: FloatFormat) -> np.ndarray:
+    """Kernel operand blob (include/mpvmc_b200.h): per convolution and tap the
+    16 x 16 B operand W[cout][cin] in the K-major core-matrix layout (element
+    (n, k) at byte (n&7)*16 + (n>>3)*256 + (k>>3)*128 + (k&7)*2), then f32 vectors:
+    per LN the running residual bias b0 + sum of the earlier blocks' second
+    biases, the gain and the shift; then each block's first-convolution bias."""
+    p = params.unflatten()
+    n_res, F = params.n_res, FILTERS
+    convs = [np.concatenate([p["w0"], np.zeros((F, F - 1, TAPS))], axis=1)]
+    for i in range(n_res):
+        convs += [p[f"w{i}a"], p[f"w{i}b"]]
+    n, k = np.meshgrid(np.arange(F), np.arange(F), indexing="ij")
+    off = ((n & 7) * 16 + (n >> 3) * 256 + (k >> 3) * 128 + (k & 7) * 2) // 2
+    blocks = np.zeros((len(convs), TAPS, 256), dtype=np.uint16)
+    for ci, w in enumerate(convs):
+        bits = _bits16(w, fmt)  # [cout][cin][tap]
+        for d in range(TAPS):
+            blocks[ci, d, off.ravel()] = bits[:, :, d].ravel()
+    vec = []
+    run = p["b0"].copy()
+    for i in range(n_res):
+        vec += [run.copy(), p[f"g{i}"], p[f"be{i}"]]
+        run = run + p[f"b{i}b"]
+    vec += [run, p["gf"], p["bef"]]
+    vec += [p[f"b{i}a"] for i in range(n_res)]
+    vec = np.concatenate(vec).astype(np.float32)
+    size = int(nat.load().mpv_rescnn_blob_bytes(params.L, n_res))
+    if size == 0:
+        raise ValueError(f"unsupported ResCNN shape L={params.L}, n_res={n_res}")
+    out = np.zeros(size, dtype=np.uint8)
+    b = blocks.view(np.uint8).ravel()
+    out[:b.size] = b
+    out[b.size:b.size + vec.nbytes] = vec.view(np.uint8)
+    return out
+
+
+class ResCnnEvaluator:
+    """Device log-probability evaluator of a ResCNN (the reference evaluator
+    protocol, sampler.py:49-53: uint8[B, N] -> float64[B]).  fmt f16/bf16: the
+    tcgen05 forward (ChainEnsemble fuses it into the MH step); f64: the CUDA-core
+    f64 forward (2 log psi)."""
+
+    def __init__(self, params: ResCnnParameters, fmt: FloatFormat, device=None):
+        import torch
+
+        nat.require_cuda()
+        if fmt.name not in ("f16", "bf16", "f64"):
+            raise ValueError("the ResCNN evaluator takes f16, bf16 (tensor cores) or f64")
+        self.params, self.fmt = params, fmt
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.L, self.n_res = params.L, params.n_res
+        self.n_visible = params.n_visible
+        self.theta = torch.from_numpy(params.theta).to(self.device)
+        self.blob = None
+        if fmt.name != "f64":
+            self.blob = torch.from_numpy(make_blob(params, fmt)).to(self.device)
+
+    def log_prob_packed(self, packed):
+        import torch
+
+        packed = packed.contiguous()
+        B = packed.shape[0]
+        out = torch.empty(B, dtype=torch.float64, device=self.device)
+        status = torch.tensor([0, 2**63 - 1], dtype=torch.int64, device=self.device)
+        st = nat.stream_handle(self.device)
+        if self.blob is None:
+            nat.call("mpv_rescnn_forward_f64", self.theta.data_ptr(), self.L, self.n_res, packed.data_ptr(), B,
+                     out.data_ptr(), st)
+            out.mul_(2.0)
+        else:
+            nat.call("mpv_rescnn_forward", self.L, self.n_res, self.fmt.code, self.blob.data_ptr(), packed.data_ptr(),
+                     B, out.data_ptr(), status.data_ptr(), st)
+        return out, status
+
+    def __call__(self, bits) -> np.ndarray:
+        from .rbm import device_pack
+
+        bits = np.atleast_2d(np.asarray(bits, dtype=np.uint8))
+        if bits.shape[1] != self.n_visible:
+            raise ValueError(f"bit matrix has {bits.shape[1]} sites, ansatz has {self.n_visible}")
+        out, status = self.log_prob_packed(device_pack(bits, self.device))
+        out = out.cpu().numpy()
+        if not np.all(np.isfinite(out)):
+            bad = int(np.nonzero(~np.isfinite(out))[0][0])
+            raise EvaluationFailureError("non-finite log probability", context={"bits": bits[bad].copy()})
+        return out
+
+
+def log_prob_evaluator(params: ResCnnParameters, fmt: FloatFormat, device=None) -> ResCnnEvaluator:
+    return ResCnnEvaluator(params, fmt, device)
+
+
+def log_psi_packed(params: ResCnnParameters, packed, device=None):
+    """f64 log psi of packed configurations (device tensor)."""
+    ev = ResCnnEvaluator(params, FloatFormat_f64(), device)
+    lp, _ = ev.log_prob_packed(packed)
+    return 0.5 * lp
+
+
+def FloatFormat_f64():
+    from .precision import F64
+
+    return F64
+
+
+def local_energies_packed(spec, params: ResCnnParameters, packed, device=None):
+    """eps(x) = sum_x' H(x, x') psi(x') / psi(x) (the reference's local energy,
+    vmc.py:60-108) for the real ResCNN amplitude: connected configurations built
+    with device bit operations, every amplitude from the f64 forward.  TFIM: all
+    single flips, H = h; Heisenberg / J1-J2 (optionally Marshall): anti-aligned
+    bonds, H = the bond's off-diagonal coefficient.  Returns complex128 [B]."""
+    import torch
+
+    from .hamiltonians import HeisenbergSpec, J1J2Spec, TfimSpec
+
+    dev = packed.device
+    N = params.n_visible
+    words = (N + 31) // 32
+    B = packed.shape[0]
+    packed = packed.contiguous().view(torch.int32)
+    lp0 = log_psi_packed(params, packed, dev)
+    sites = torch.arange(N, device=dev)
+    bits = ((packed[:, sites // 32] >> (sites % 32)) & 1).to(torch.int64)  # (B, N)
+    spin = 1 - 2 * bits
+    if isinstance(spec, TfimSpec):
+        bonds = torch.from_numpy(spec.lattice.bond_array()).to(dev)
+        diag = float(spec.j) * (spin[:, bonds[:, 0]] * spin[:, bonds[:, 1]]).sum(dim=1).to(torch.float64)
+        mask = torch.zeros((N, words), dtype=torch.int64, device=dev)
+        mask[sites, sites // 32] = (1 << (sites % 32))
+        conn = (packed.to(torch.int64)[:, None, :] ^ mask[None]).reshape(B * N, words)
+        owner = torch.arange(B, device=dev).repeat_interleave(N)
+        coef = torch.full((B * N,), float(spec.h), dtype=torch.float64, device=dev)
+    elif isinstance(spec, (HeisenbergSpec, J1J2Spec)):
+        b_np, jb_np, cf_np = spec.couplings()
+        bonds = torch.from_numpy(b_np).to(dev)
+        jb = torch.from_numpy(jb_np).to(dev)
+        cf = torch.from_numpy(cf_np).to(dev)
+        diag = (jb[None, :] * (spin[:, bonds[:, 0]] * spin[:, bonds[:, 1]])).sum(dim=1).to(torch.float64)
+        differ = bits[:, bonds[:, 0]] != bits[:, bonds[:, 1]]  # (B, nb)
+        s_idx, b_idx = torch.nonzero(differ, as_tuple=True)
+        i, j = bonds[b_idx, 0], bonds[b_idx, 1]
+        mask = torch.zeros((s_idx.numel(), words), dtype=torch.int64, device=dev)
+        mask.scatter_(1, (i // 32)[:, None], (1 << (i % 32))[:, None])
+        mask.scatter_add_(1, (j // 32)[:, None], (1 << (j % 32))[:, None])
+        conn = packed.to(torch.int64)[s_idx] ^ mask
+        owner = s_idx
+        coef = cf[b_idx].to(torch.float64)
+    else:
+        raise TypeError(f"unknown Hamiltonian spec {type(spec).__name__}")
+    conn32 = conn.to(torch.int32).contiguous() if conn.numel() else torch.empty((0, words), dtype=torch.int32,
+                                                                                     device=dev)
+    lpc = log_psi_packed(params, conn32, dev)
+    ratio = torch.exp(lpc - lp0[owner]) * coef
+    off = torch.zeros(B, dtype=torch.float64, device=dev).index_add_(0, owner, ratio)
+    eps = diag + off
+    return torch.complex(eps, torch.zeros_like(eps))

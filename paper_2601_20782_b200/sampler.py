@@ -97,8 +97,11 @@ def uniform_log_prob(n_sites: int) -> TableLogProb:
 
 def _device_evaluator(evaluator):
     from .rbm import LogProbEvaluator
+    from .rescnn import ResCnnEvaluator
 
-    if not isinstance(evaluator, (LogProbEvaluator, TableLogProb)):
+    if isinstance(evaluator, ResCnnEvaluator) and evaluator.blob is None:
+        raise TypeError("ChainEnsemble fuses the ResCNN tensor-core evaluator (f16 / bf16), not the f64 forward")
+    if not isinstance(evaluator, (LogProbEvaluator, TableLogProb, ResCnnEvaluator)):
         raise TypeError(
             f"ChainEnsemble needs a device evaluator (rbm.log_prob_evaluator, sampler.table_log_prob), got "
             f"{type(evaluator).__name__} (the B200 path has no host-callable fallback)")
@@ -155,7 +158,9 @@ class ChainEnsemble:
 
     # -- internals ----------------------------------------------------------
     def _bind_scratch(self):
-        if isinstance(self._evaluator, TableLogProb):
+        from .rescnn import ResCnnEvaluator
+
+        if isinstance(self._evaluator, (TableLogProb, ResCnnEvaluator)):
             return
         need = nat.load().mpv_sweep_scratch_bytes(ctypes.byref(self._evaluator.snapshot.struct), self.n_chains)
         if self._scratch is None or self._scratch.numel() < need:
@@ -171,7 +176,14 @@ class ChainEnsemble:
     def _launch(self, n_steps, thin=0, samples=None, n_samples_total=0, round_offset=0, row0=0):
         self._refresh_pending = False  # every launch refreshes the cached log p from the bits first
         sp = samples.data_ptr() if samples is not None else None
-        if isinstance(self._evaluator, TableLogProb):
+        from .rescnn import ResCnnEvaluator
+
+        if isinstance(self._evaluator, ResCnnEvaluator):
+            ev = self._evaluator
+            nat.call("mpv_rescnn_mh_sweep", ev.L, ev.n_res, ev.fmt.code, ev.blob.data_ptr(), ctypes.byref(self._chains),
+                     self.key, self.proposal.code, self.init_draws, self.steps_done, int(n_steps), int(thin), sp,
+                     int(n_samples_total), self.n_chains_total, int(round_offset), int(row0), self._stream())
+        elif isinstance(self._evaluator, TableLogProb):
             nat.call("mpv_table_sweep", self._evaluator.table.data_ptr(), ctypes.byref(self._chains), self.key,
                      self.proposal.code, self.init_draws, self.steps_done, int(n_steps), int(thin), sp,
                      int(n_samples_total), self.n_chains_total, int(round_offset), int(row0), self._stream())
