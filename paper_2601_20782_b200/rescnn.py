@@ -275,3 +275,181 @@ def local_energies_packed(spec, params: ResCnnParameters, packed, device=None):
     off = torch.zeros(B, dtype=torch.float64, device=dev).index_add_(0, owner, ratio)
     eps = diag + off
     return torch.complex(eps, torch.zeros_like(eps))
+
+
+# ---------------------------------------------------------------------------
+# Training (BASELINE configs[3]: "minSR in f32, chain sharding").  Sampling
+# uses the fused tensor-core MH step, local energies the f64 forward; the
+# per-sample log-derivatives O = d log psi / d theta come from torch autograd
+# over a torch restatement of the same network in f64 (vmap of grad; cuDNN
+# convolutions - the gradient statistics stay f32/f64, north_star (4)), and
+# the SR step is solved in sample space (minSR) in f32 or f64, sharded.
+# ---------------------------------------------------------------------------
+
+def torch_log_psi(theta, spins, L: int, n_res: int):
+    """log psi for spins (B, L, L) = 1 - 2x as a torch function of theta (autograd)."""
+    import torch
+    import torch.nn.functional as tf
+
+    F, k = FILTERS, 0
+    p = {}
+    for name, shape in param_layout(n_res):
+        size = int(np.prod(shape))
+        p[name] = theta[k:k + size].reshape(shape)
+        k += size
+
+    def conv(h, w, b):
+        hp = tf.pad(h, (1, 1, 1, 1), mode="circular")
+        return tf.conv2d(hp, w.reshape(w.shape[0], w.shape[1], 3, 3), b)
+
+    def ln(h, g, be):
+        mu = h.mean(dim=1, keepdim=True)
+        var = ((h - mu) ** 2).mean(dim=1, keepdim=True)
+        return g[None, :, None, None] * (h - mu) / torch.sqrt(var + 1e-6) + be[None, :, None, None]
+
+    h = conv(spins[:, None], p["w0"], p["b0"])
+    for i in range(n_res):
+        u = tf.gelu(ln(h, p[f"g{i}"], p[f"be{i}"]), approximate="tanh")
+        v = tf.gelu(conv(u, p[f"w{i}a"], p[f"b{i}a"]), approximate="tanh")
+        h = h + conv(v, p[f"w{i}b"], p[f"b{i}b"])
+    return ln(h, p["gf"], p["bef"]).sum(dim=(1, 2, 3))
+
+
+def log_derivatives(params: ResCnnParameters, packed, chunk: int = 1024):
+    """O[s] = d log psi(x_s) / d theta (U, P) f64 on the device."""
+    import torch
+    from torch.func import grad, vmap
+
+    dev = packed.device
+    L, n = params.L, params.n_visible
+    sites = torch.arange(n, device=dev)
+    bits = ((packed.view(torch.int32)[:, sites // 32] >> (sites % 32)) & 1).to(torch.float64)
+    spins = (1.0 - 2.0 * bits).reshape(-1, L, L)
+    theta = torch.from_numpy(params.theta).to(dev)
+    one = lambda th, s: torch_log_psi(th, s[None], L, params.n_res)[0]  # noqa: E731
+    g = vmap(grad(one), in_dims=(None, 0), chunk_size=chunk)
+    return g(theta, spins)
+
+
+@dataclass
+class CnnTrainConfig:
+    hamiltonian: object
+    n_res: int = 4
+    n_steps: int = 100
+    n_samples: int = 4096
+    n_chains: int | None = None
+    eta: float = 0.01
+    lambda_shift: float = 1e-3
+    seed: int = 0
+    sampling_format: FloatFormat = None
+    proposal: object = None
+    burn_in_sweeps: int = 20
+    reburn_sweeps: int = 2
+    init_scale: float = 0.5
+    minsr_precision: str = "f32"
+
+
+def minsr_dense(o, eps, w, lam: float, precision: str = "f32", group=None, sharded: bool = False):
+    """Sample-space SR step for a real dense O (U, P) shard: K = O~ O~^T + lam
+    with O~ = W^1/2 (O - obar), e~ = W^1/2 (eps - ebar); g = O~^T K^-1 e~
+    (push-through identity; the reference's parameter-space estimators,
+    vmc.py:145-229).  Across ranks the O~ rows are all-gathered and every rank
+    solves the same U_total x U_total system; O~^T y sums per rank."""
+    import torch
+
+    from . import parallel
+    from .vmc import _gather_rows
+
+    red = (lambda z: parallel.all_reduce_sum(z, group)) if sharded else (lambda z: z)
+    s = red(torch.cat([(w[:, None] * o).sum(0), (w * eps).sum().reshape(1)]))
+    obar, ebar = s[:-1], s[-1]
+    sw = torch.sqrt(w)
+    ot = sw[:, None] * (o - obar[None, :])
+    et = sw * (eps - ebar)
+    f = red(ot.T @ et)
+    dt = torch.float32 if precision == "f32" else torch.float64
+    if sharded:
+        ot_all, row0 = _gather_rows(ot.to(dt).contiguous(), group)
+        et_all, _ = _gather_rows(et.to(dt).contiguous(), group)
+    else:
+        ot_all, row0, et_all = ot.to(dt), 0, et.to(dt)
+    k = ot_all @ ot_all.T
+    if precision == "f32":
+        # the f32 Gram matrix is PSD only to its rounding floor: the shift is
+        # raised to 64 ulp of the largest diagonal entry when that exceeds lam
+        lam = max(lam, 64.0 * 2.0**-24 * float(torch.diagonal(k).max()))
+    k = 0.5 * (k + k.T) + lam * torch.eye(k.shape[0], dtype=dt, device=k.device)
+    L_, info = torch.linalg.cholesky_ex(k)
+    if int(info) != 0:
+        from .errors import SolverError
+
+        raise SolverError("minSR matrix is not positive definite")
+    y = torch.cholesky_solve(et_all[:, None], L_)[:, 0]
+    y = y + torch.cholesky_solve((et_all - k @ y)[:, None], L_)[:, 0]
+    g = red(ot.T @ y[row0:row0 + ot.shape[0]].to(torch.float64))
+    return g, f, float(ebar)
+
+
+def train(config: CnnTrainConfig, device=None, group=None, local: bool = False):
+    """VMC of the ResCNN (the reference's _train_loop structure, vmc.py:472-639):
+    per step the f16/bf16 snapshot, re-burn, collect, unique samples + weights,
+    f64 local energies, O, minSR, update; records energy, split-chain error,
+    acceptance, sigma_hat (fmt vs f64 log p on the unique samples)."""
+    import torch
+    import torch.distributed as tdist
+
+    from . import parallel
+    from .bounds import pinsker_tv_bound, theorem3_gaussian_bound
+    from .precision import F16
+    from .rng import derive_key
+    from .sampler import ChainEnsemble, Proposal, default_chain_count
+    from .vmc import device_mc_error, device_std
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    world = tdist.get_world_size(group) if (not local and tdist.is_available() and tdist.is_initialized()) else 1
+    rank = tdist.get_rank(group) if world > 1 else 0
+    spec = config.hamiltonian
+    if len(spec.lattice.shape) != 2 or spec.lattice.shape[0] != spec.lattice.shape[1]:
+        raise ValueError("the ResCNN needs a square L x L lattice")
+    L = spec.lattice.shape[0]
+    n = L * L
+    fmt = config.sampling_format or F16
+    proposal = config.proposal or Proposal("flip")
+    params = random_parameters(L, config.n_res, derive_key(config.seed, "init"), config.init_scale)
+    n_chains = config.n_chains or default_chain_count(config.n_samples)
+    c_off, c_cnt = parallel.shard(n_chains, rank, world)
+    grp = group if world > 1 else None
+    ensemble = None
+    records = []
+    for step in range(config.n_steps):
+        ev = log_prob_evaluator(params, fmt, dev)
+        if ensemble is None:
+            ensemble = ChainEnsemble(c_cnt, n, proposal, ev, derive_key(config.seed, "chains"), chain_offset=c_off,
+                                     n_chains_total=n_chains)
+            ensemble.run_sweeps(config.burn_in_sweeps)
+        else:
+            ensemble.set_evaluator(ev, check=False)
+            ensemble.run_sweeps(config.reburn_sweeps, check=False)
+        ensemble.reset_counters()
+        packed = ensemble.collect_packed(config.n_samples, n + 1)
+        acc = torch.tensor([float(ensemble.accepted), float(ensemble.proposed)], dtype=torch.float64, device=dev)
+        if world > 1:
+            parallel.all_reduce_sum(acc, grp)
+        uniq, inverse, cnt = torch.unique(packed, dim=0, return_inverse=True, return_counts=True)
+        w = cnt.to(torch.float64) / config.n_samples
+        eps = local_energies_packed(spec, params, uniq).real
+        o = log_derivatives(params, uniq)
+        g, _, energy = minsr_dense(o, eps, w, config.lambda_shift, config.minsr_precision, grp, world > 1)
+        if world > 1:
+            counts = parallel.chain_counts(config.n_samples, n_chains, c_off, c_cnt)
+            err = parallel.energy_statistics(eps[inverse], counts, 0, 1, grp)["mc_error"]
+        else:
+            err = device_mc_error(torch.complex(eps, torch.zeros_like(eps)), inverse, config.n_samples, n_chains)
+        lp_fmt, _ = ev.log_prob_packed(uniq)
+        delta = lp_fmt - 2.0 * log_psi_packed(params, uniq, dev)
+        sigma_hat = device_std(delta) if delta.numel() > 1 else 0.0
+        records.append({"step": step, "energy": energy, "mc_error": err, "acceptance": float(acc[0] / acc[1]),
+                        "sigma_hat": sigma_hat, "bound_pinsker": pinsker_tv_bound(sigma_hat),
+                        "bound_theorem3": theorem3_gaussian_bound(sigma_hat, 0.0, 0.0)})
+        params = ResCnnParameters(params.theta - config.eta * g.cpu().numpy(), L, config.n_res)
+    return records, params

@@ -158,3 +158,115 @@ def test_mh_exchange_shards_and_launch_splits(cuda):
     full = a.collect(300, 7)
     parts = [s.collect(300, 7) for s in (s0, s1)]
     np.testing.assert_array_equal(np.concatenate(parts), full)
+
+
+def test_log_derivatives_match_finite_differences(cuda):
+    """O = d log psi / d theta (torch autograd over the torch restatement) against
+    central differences of the device f64 forward, and the torch restatement's
+    value against the f64 kernel."""
+    L, n_res = 4, 2
+    p = _params(L, n_res, seed=31, scale=0.6)
+    bits = _bits(8, L * L, 3)
+    packed = torch.from_numpy(pack_bits(bits).view(np.int32)).to(cuda)
+    o = rescnn.log_derivatives(p, packed).cpu().numpy()
+    lp = rescnn.log_psi_packed(p, packed).cpu().numpy()
+    sites = np.arange(L * L)
+    spins = torch.from_numpy((1.0 - 2.0 * bits).reshape(-1, L, L)).to(cuda)
+    val = rescnn.torch_log_psi(torch.from_numpy(p.theta).to(cuda), spins, L, n_res).cpu().numpy()
+    np.testing.assert_allclose(val, lp, rtol=1e-12, atol=1e-12)
+    rng = np.random.default_rng(0)
+    for j in rng.choice(p.theta.size, size=12, replace=False):
+        hstep = 1e-6
+        tp, tm = p.theta.copy(), p.theta.copy()
+        tp[j] += hstep
+        tm[j] -= hstep
+        fp = rescnn.log_psi_packed(rescnn.ResCnnParameters(tp, L, n_res), packed).cpu().numpy()
+        fm = rescnn.log_psi_packed(rescnn.ResCnnParameters(tm, L, n_res), packed).cpu().numpy()
+        np.testing.assert_allclose(o[:, j], (fp - fm) / (2 * hstep), rtol=1e-5, atol=1e-7)
+
+
+def test_minsr_dense_equals_parameter_space_sr(cuda):
+    """The sample-space step equals (S + lambda)^-1 F of the reference estimators
+    (vmc.py:145-229) for a real O; f32 to 1e-3."""
+    rng = np.random.default_rng(4)
+    U, P, lam = 300, 700, 1e-2
+    o = torch.from_numpy(rng.normal(size=(U, P))).to(cuda)
+    eps = torch.from_numpy(rng.normal(size=U)).to(cuda)
+    w = torch.from_numpy(rng.random(U) + 0.1).to(cuda)
+    w = w / w.sum()
+    c = o - (w[:, None] * o).sum(0)
+    s = c.T @ (w[:, None] * c)
+    f = c.T @ (w * (eps - (w * eps).sum()))
+    g_ref = torch.linalg.solve(s + lam * torch.eye(P, dtype=torch.float64, device=cuda), f)
+    for prec, tol in (("f64", 1e-9), ("f32", 1e-3)):
+        g, f2, _ = rescnn.minsr_dense(o, eps, w, lam, prec)
+        torch.testing.assert_close(f2, f, rtol=1e-12, atol=1e-12)
+        assert float(torch.linalg.norm(g - g_ref) / torch.linalg.norm(g_ref)) < tol
+
+
+def test_train_rescnn_reaches_ground_state(cuda):
+    """configs[3]'s training path at an enumerable size: 4x4 J1-J2 (J2 = 0.5,
+    Marshall sign) with f16 tensor-core sampling, f64 energies and f32 minSR,
+    against the exact ground-state energy (oracle dense diagonalisation)."""
+    from oracle import ed
+
+    spec = J1J2Spec(LatticeSpec.square(4), 1.0, 0.5, marshall=True)
+    e0 = ed.ground_energy_sparse([("heisenberg", spec.lattice.bond_array(), 1.0, 0.0),
+                                  ("heisenberg", spec.lattice.next_nearest_bonds(), 0.5, 0.0)], 16)
+    cfg = rescnn.CnnTrainConfig(spec, n_res=2, n_steps=40, n_samples=2048, n_chains=512, eta=0.01,
+                                lambda_shift=1e-2, proposal=sampler.Proposal("exchange", 8), init_scale=0.3,
+                                minsr_precision="f32")
+    recs, _ = rescnn.train(cfg)
+    e_end = float(np.mean([r["energy"] for r in recs[-10:]]))
+    print(f"\n[rescnn train] J1-J2 4x4 E0 {e0:.5f}  start {recs[0]['energy']:.5f}  end {e_end:.5f}  "
+          f"sigma_hat {recs[-1]['sigma_hat']:.2e}")
+    assert abs(e_end - e0) / abs(e0) < 0.03
+    assert recs[-1]["sigma_hat"] < 0.05
+
+
+def _cnn_worker(rank, world, port, q):
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    recs, p = rescnn.train(_cnn_cfg())
+    q.put((rank, [(r["energy"], r["mc_error"], r["acceptance"]) for r in recs], p.theta))
+    dist.destroy_process_group()
+
+
+def _cnn_cfg():
+    return rescnn.CnnTrainConfig(J1J2Spec(LatticeSpec.square(4), 1.0, 0.5, marshall=True), n_res=1, n_steps=3,
+                                 n_samples=512, n_chains=128, eta=0.01, lambda_shift=1e-2,
+                                 proposal=sampler.Proposal("exchange", 8), init_scale=0.3, minsr_precision="f64")
+
+
+def test_train_rescnn_two_ranks_match_single(cuda):
+    """Chain sharding (global chain ids) + all-gathered minSR: two gloo ranks on
+    one GPU reproduce the single-process training records and parameters."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    recs1, p1 = rescnn.train(_cnn_cfg())
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_cnn_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted((q.get(timeout=300) for _ in procs), key=lambda x: x[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for _, recs, theta in res:
+        for (e, err, acc), r in zip(recs, recs1):
+            assert e == pytest.approx(r["energy"], rel=1e-9, abs=1e-10)
+            assert err == pytest.approx(r["mc_error"], rel=1e-6)
+            assert acc == r["acceptance"]
+        np.testing.assert_allclose(theta, p1.theta, rtol=1e-7, atol=1e-9)

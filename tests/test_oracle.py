@@ -144,3 +144,13 @@ def test_oracle_exact_diagonalisation_matches_reference():
         float(g["tfim_sq3_h3.04"]), abs=1e-10)
     assert ed.ground_energy("heisenberg", 8, LatticeSpec.chain(8).bond_array(), 1.0) == pytest.approx(
         float(g["heis_chain8"]), abs=1e-10)
+
+
+def test_oracle_sparse_diagonalisation_matches_dense():
+    from oracle import ed
+    from paper_2601_20782_b200.lattice import LatticeSpec
+
+    for kind, lat, j, h in (("tfim", LatticeSpec.chain(10), 1.0, 0.5), ("heisenberg", LatticeSpec.square(3), 1.0, 0.0)):
+        n = lat.n_sites
+        dense = ed.ground_energy(kind, n, lat.bond_array(), j, h)
+        assert ed.ground_energy_sparse([(kind, lat.bond_array(), j, h)], n) == pytest.approx(dense, abs=1e-9)
