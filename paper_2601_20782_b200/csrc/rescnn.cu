@@ -391,90 +391,127 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-// ---- f64 forward on the CUDA cores (local energies, parity): one CTA per
-// configuration, activations in shared memory, sites x channels over threads.
+// ---- f64 forward on the CUDA cores (local energies, parity).  A CTA holds G
+// configurations; thread = (configuration, site) keeps its site's residual
+// stream h[16] in registers and computes all 16 output channels of a
+// convolution (16 FMA per activation load; the weights of the current
+// convolution are staged in shared memory and read warp-uniformly).  Two
+// activation buffers per configuration (layer input / first-convolution
+// output) hold the neighbours' values.
 __device__ __forceinline__ double gelu64(double z) {
   return 0.5 * z * (1.0 + tanh(0.7978845608028654 * (z + 0.044715 * z * z * z)));
 }
 
-__global__ void __launch_bounds__(256) rescnn_f64_kernel(const double* __restrict__ theta, int L, int n_res,
-                                                         const uint32_t* __restrict__ bits, int64_t B, int words,
-                                                         double* __restrict__ out) {
+constexpr int kF64Threads = 512;
+
+__global__ void __launch_bounds__(kF64Threads) rescnn_f64_kernel(const double* __restrict__ theta, int L, int n_res,
+                                                                  const uint32_t* __restrict__ bits, int64_t B,
+                                                                  int words, int G, double* __restrict__ out) {
   extern __shared__ double sm64[];
   const int N = L * L;
-  double* h = sm64;            // [N][16]
-  double* u = h + N * kF;      // [N][16]
-  double* v = u + N * kF;      // [N][16]
-  __shared__ double red[256];
+  double* wsm = sm64;                 // [16 cout][16 cin][9]
+  double* bufA = wsm + kF * kF * kTaps;  // [G][N][16]
+  double* bufB = bufA + (size_t)G * N * kF;
+  __shared__ double red[kF64Threads];
   const int tid = threadIdx.x;
-  for (int64_t cfg = blockIdx.x; cfg < B; cfg += gridDim.x) {
-    // input spins in u[:, 0]
-    for (int p = tid; p < N; p += blockDim.x) u[p * kF] = ((bits[cfg * words + (p >> 5)] >> (p & 31)) & 1u) ? -1.0 : 1.0;
+  const int g = tid / N, p = tid % N;  // configuration slot, site
+  const bool active = g < G;
+  const int pr = p / L, pc = p % L;
+  int nb[kTaps];
+#pragma unroll
+  for (int d = 0; d < kTaps; ++d) nb[d] = ((pr + d / 3 - 1 + L) % L) * L + (pc + d % 3 - 1 + L) % L;
+  // parameter offsets (oracle/rescnn.py order)
+  const size_t blk = 2 * kF + 2 * (kF * kF * kTaps + kF);
+
+  auto stage = [&](const double* w) {  // one 16x16x9 convolution's weights
     __syncthreads();
-    const double* w = theta;
-    // embedding
-    for (int idx = tid; idx < N * kF; idx += blockDim.x) {
-      const int p = idx / kF, c = idx % kF, pr = p / L, pc = p % L;
-      double acc = w[kF * kTaps + c];  // b0
-      for (int d = 0; d < kTaps; ++d) {
-        const int q = ((pr + d / 3 - 1 + L) % L) * L + (pc + d % 3 - 1 + L) % L;
-        acc = fma(w[c * kTaps + d], u[q * kF], acc);
+    for (int i = tid; i < kF * kF * kTaps; i += blockDim.x) wsm[i] = w[i];
+    __syncthreads();
+  };
+  // out[c] = bias[c] + sum_{tap, cin} w[c][cin][tap] src[nb(tap)][cin]
+  auto conv = [&](const double* src, const double* bias, double* o) {
+#pragma unroll
+    for (int c = 0; c < kF; ++c) o[c] = bias[c];
+    for (int d = 0; d < kTaps; ++d) {
+      const double* sq = src + (size_t)nb[d] * kF;
+      for (int ci = 0; ci < kF; ++ci) {
+        const double a = sq[ci];
+#pragma unroll
+        for (int c = 0; c < kF; ++c) o[c] = fma(wsm[(c * kF + ci) * kTaps + d], a, o[c]);
       }
-      h[idx] = acc;
     }
+  };
+  auto ln = [&](const double* h, const double* gm, const double* be, double* z) {
+    double mu = 0.0, var = 0.0;
+#pragma unroll
+    for (int c = 0; c < kF; ++c) mu += h[c];
+    mu /= kF;
+#pragma unroll
+    for (int c = 0; c < kF; ++c) var += (h[c] - mu) * (h[c] - mu);
+    const double rs = 1.0 / sqrt(var / kF + 1e-6);
+#pragma unroll
+    for (int c = 0; c < kF; ++c) z[c] = gm[c] * (h[c] - mu) * rs + be[c];
+  };
+
+  for (int64_t cfg0 = (int64_t)blockIdx.x * G; cfg0 < B; cfg0 += (int64_t)gridDim.x * G) {
+    const int64_t cfg = cfg0 + g;
+    const bool live = active && cfg < B;
+    double* A = bufA + (size_t)g * N * kF;
+    double* Bv = bufB + (size_t)g * N * kF;
+    double h[kF], t[kF];
+    if (live) A[p * kF] = ((bits[cfg * words + (p >> 5)] >> (p & 31)) & 1u) ? -1.0 : 1.0;
     __syncthreads();
+    // embedding (one input channel)
+    if (live) {
+      const double* w0 = theta;
+      const double* b0 = theta + kF * kTaps;
+#pragma unroll
+      for (int c = 0; c < kF; ++c) h[c] = b0[c];
+      for (int d = 0; d < kTaps; ++d) {
+        const double sv = A[nb[d] * kF];
+#pragma unroll
+        for (int c = 0; c < kF; ++c) h[c] = fma(w0[c * kTaps + d], sv, h[c]);
+      }
+    }
     const double* pp = theta + kF * kTaps + kF;
-    auto conv = [&](const double* src, const double* wc, const double* bc, double* dst, bool add) {
-      for (int idx = tid; idx < N * kF; idx += blockDim.x) {
-        const int p = idx / kF, c = idx % kF, pr = p / L, pc = p % L;
-        double acc = bc[c];
-        for (int d = 0; d < kTaps; ++d) {
-          const int q = ((pr + d / 3 - 1 + L) % L) * L + (pc + d % 3 - 1 + L) % L;
-          const double* sq = src + q * kF;
-          const double* wr = wc + (size_t)c * kF * kTaps + d;
-          for (int ci = 0; ci < kF; ++ci) acc = fma(wr[ci * kTaps], sq[ci], acc);
-        }
-        dst[idx] = add ? dst[idx] + acc : acc;
-      }
-      __syncthreads();
-    };
-    auto ln = [&](const double* g, const double* be, double* dst, bool act) {
-      for (int p = tid; p < N; p += blockDim.x) {
-        double mu = 0.0, var = 0.0;
-        for (int c = 0; c < kF; ++c) mu += h[p * kF + c];
-        mu /= kF;
-        for (int c = 0; c < kF; ++c) var += (h[p * kF + c] - mu) * (h[p * kF + c] - mu);
-        const double rs = 1.0 / sqrt(var / kF + 1e-6);
-        for (int c = 0; c < kF; ++c) {
-          const double z = g[c] * (h[p * kF + c] - mu) * rs + be[c];
-          dst[p * kF + c] = act ? gelu64(z) : z;
-        }
-      }
-      __syncthreads();
-    };
-    for (int l = 0; l < n_res; ++l) {
-      const double* g = pp;
+    for (int l = 0; l < n_res; ++l, pp += blk) {
+      const double* gm = pp;
       const double* be = pp + kF;
       const double* wa = pp + 2 * kF;
       const double* ba = wa + kF * kF * kTaps;
       const double* wb = ba + kF;
       const double* bb = wb + kF * kF * kTaps;
-      pp = bb + kF;
-      ln(g, be, u, true);
-      conv(u, wa, ba, v, false);
-      for (int idx = tid; idx < N * kF; idx += blockDim.x) v[idx] = gelu64(v[idx]);
+      stage(wa);  // (also orders the previous block's reads of A before the writes below)
+      if (live) {
+        ln(h, gm, be, t);
+#pragma unroll
+        for (int c = 0; c < kF; ++c) A[p * kF + c] = gelu64(t[c]);
+      }
       __syncthreads();
-      conv(v, wb, bb, h, true);
+      if (live) {
+        conv(A, ba, t);
+#pragma unroll
+        for (int c = 0; c < kF; ++c) Bv[p * kF + c] = gelu64(t[c]);
+      }
+      stage(wb);
+      if (live) {
+        conv(Bv, bb, t);
+#pragma unroll
+        for (int c = 0; c < kF; ++c) h[c] += t[c];
+      }
     }
-    ln(pp, pp + kF, u, false);
-    double acc = 0.0;
-    for (int idx = tid; idx < N * kF; idx += blockDim.x) acc += u[idx];
-    red[tid] = acc;
+    double sum = 0.0;
+    if (live) {
+      ln(h, pp, pp + kF, t);
+#pragma unroll
+      for (int c = 0; c < kF; ++c) sum += t[c];
+    }
+    red[tid] = sum;
     __syncthreads();
-    if (tid == 0) {
-      double s = 0.0;
-      for (int i = 0; i < (int)blockDim.x; ++i) s += red[i];
-      out[cfg] = s;
+    if (live && p == 0) {
+      double acc = 0.0;
+      for (int i = 0; i < N; ++i) acc += red[g * N + i];
+      out[cfg] = acc;
     }
     __syncthreads();
   }
@@ -515,12 +552,17 @@ cudaError_t rescnn_launch(int L, int n_res, int fmt, const void* blob, uint32_t*
 
 cudaError_t rescnn_f64_launch(const double* theta, int L, int n_res, const uint32_t* bits, int64_t B, int words,
                               double* out, cudaStream_t st) {
-  const size_t smem = 3ull * L * L * kF * sizeof(double);
+  const int N = L * L;
+  if (N > kF64Threads) return cudaErrorInvalidValue;
+  const int G = kF64Threads / N;
+  const size_t smem = ((size_t)kF * kF * kTaps + 2ull * G * N * kF) * sizeof(double);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute((const void*)&rescnn_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(B, 148 * 8));
-  rescnn_f64_kernel<<<grid, 256, smem, st>>>(theta, L, n_res, bits, B, words, out);
+  const int64_t groups = (B + G - 1) / G;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(groups, 148 * 4));
+  rescnn_f64_kernel<<<grid, kF64Threads, smem, st>>>(theta, L, n_res, bits, B, words, G, out);
   return cudaGetLastError();
 }
 
