@@ -390,6 +390,56 @@ def run_ours(args, rank, world, local_rank):
 
         extra["forward_tc"] = forward_tc_rate()
 
+        # BASELINE configs[3]: ResCNN (4 residual blocks, 16 filters, 3x3) on the 10x10
+        # J1-J2 model (J2 = 0.5, Marshall sign): tcgen05 forward, fused MH sampling with
+        # exchange moves (16,384 chains, f16), one VMC iteration (4,096 samples, f32 minSR)
+        def rescnn_rates():
+            from paper_2601_20782_b200 import rescnn
+            from paper_2601_20782_b200.hamiltonians import J1J2Spec
+            from paper_2601_20782_b200.lattice import LatticeSpec as _LS3
+
+            pc = rescnn.random_parameters(10, 4, derive_key(0, "init"), 0.5)
+            B = 65536
+            pk = torch.randint(-2**31, 2**31 - 1, (B, 4), dtype=torch.int32, device=dev)
+            pk[:, -1] &= (1 << (N_SITES % 32)) - 1
+            evc = rescnn.log_prob_evaluator(pc, F16)
+            evc.log_prob_packed(pk)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(5):
+                evc.log_prob_packed(pk)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            ms_f = a0.elapsed_time(a1) / 5
+            useful = N_SITES * (16 * 9 + 8 * 16 * 16 * 9) * 2
+            ens_c = sampler.ChainEnsemble(C, N_SITES, sampler.Proposal("exchange", N_SITES // 2), evc,
+                                          derive_key(0, "chains"))
+            ens_c.run_steps(20)
+            torch.cuda.synchronize()
+            a0.record(stream)
+            ens_c.run_steps(200, check=False)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            spec_c = J1J2Spec(_LS3.square(10), 1.0, 0.5, marshall=True)
+            cfgc = rescnn.CnnTrainConfig(spec_c, n_res=4, n_steps=3, n_samples=4096, n_chains=1024, eta=0.01,
+                                         lambda_shift=1e-2, proposal=sampler.Proposal("exchange", N_SITES // 2),
+                                         init_scale=0.3, burn_in_sweeps=0)
+            t0 = time.perf_counter()
+            rescnn.train(cfgc)
+            torch.cuda.synchronize()
+            return {"config": "rescnn_4x16_3x3_j1j2_10x10_j2_0.5_marshall",
+                    "forward_f16_configs_per_s": B / (ms_f / 1e3),
+                    "forward_f16_useful_tflops": useful * B / (ms_f / 1e3) / 1e12,
+                    "sampling_exchange_f16_chain_steps_per_s": C * 200 / (a0.elapsed_time(a1) / 1e3),
+                    "acceptance": ens_c.acceptance_rate,
+                    "vmc_iteration_s4096_c1024_minsr_f32_seconds": (time.perf_counter() - t0) / 3}
+
+        try:
+            extra["config4_rescnn"] = rescnn_rates()
+        except Exception as exc:
+            extra["config4_rescnn"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     # ---- VMC iteration time at BASELINE configs[0] (N=20 open TFIM chain, alpha=1,
     # 4,096 samples, 1,024 chains, f16 sampling), reference: vmc.py:472-639 ----
     vmc_iter = None
