@@ -742,9 +742,14 @@ static int launch_ov(int mode, const double* t, const uint32_t* bits, int64_t U,
   const double2* V = (const double2*)v;
   double2* Q = (double2*)q;
   double2* TO = (double2*)t_out;
-#define MPV_OV(K)                                                                                      \
-  if (mode == 0) ld_ov_kernel<K, 0><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, V, vwt, Q, w, TO); \
-  else ld_ov_kernel<K, 1><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, V, vwt, Q, w, TO);
+  const size_t tbytes = (size_t)kLdSB * M * 16;  // MODE 0: the block's T rows in shared memory
+#define MPV_OV(K)                                                                                             \
+  if (mode == 0) {                                                                                            \
+    if (int rc = ensure_smem((const void*)&ld_ov_kernel<K, 0>, tbytes)) return rc;                           \
+    ld_ov_kernel<K, 0><<<grid, 256, tbytes, st>>>(T, bits, U, N, M, words, V, vwt, Q, w, TO);               \
+  } else {                                                                                                    \
+    ld_ov_kernel<K, 1><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, V, vwt, Q, w, TO);                    \
+  }
   if (kt <= 2) { MPV_OV(2) }
   else if (kt <= 4) { MPV_OV(4) }
   else if (kt <= 8) { MPV_OV(8) }

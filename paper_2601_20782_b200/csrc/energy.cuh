@@ -398,24 +398,19 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
   };
   if (any_terms && !(pl.skip & 4) && tid == 0)
     for (int c = 0; c < min(pl.nbt, nchunks); ++c) issueT(c, c);
-  // D fragment (row s = m*8 + qc, cols 2i, 2i+1) -> tanh(theta_i(s)) into tt[i][s]
+  // D fragment (row s = m*8 + qc, cols 2i, 2i+1) = theta_i(s): tanh formed in
+  // registers (the lane's 2 KT fragments are independent chains) -> tt[i][s]
 #pragma unroll
   for (int j = 0; j < KT; ++j) {
     const int nt = warp + j * nwarps, i = nt * 4 + qr;
     if (nt < NT && i < M) {
 #pragma unroll
       for (int m = 0; m < 2; ++m)
-        if (m < MT) tt[i * SB + m * 8 + qc] = make_double2(acc[j][m][0], acc[j][m][1]);
+        if (m < MT) {
+          const double2 z = make_double2(acc[j][m][0], acc[j][m][1]);
+          tt[i * SB + m * 8 + qc] = (pl.skip & 2) ? z : ctanh_fast(z);
+        }
     }
-  }
-  __syncthreads();
-  // two independent tanh chains per iteration (latency-bound otherwise)
-  for (int idx = tid; idx < ((pl.skip & 2) ? 0 : M * SB); idx += 2 * blockDim.x) {
-    const int idx2 = idx + blockDim.x;
-    const double2 z0 = tt[idx], z1 = idx2 < M * SB ? tt[idx2] : make_double2(0.0, 0.0);
-    const double2 t0 = ctanh_fast(z0), t1 = ctanh_fast(z1);
-    tt[idx] = t0;
-    if (idx2 < M * SB) tt[idx2] = t1;
   }
   __syncthreads();
 

@@ -62,16 +62,35 @@ __device__ __forceinline__ double2 ctanh_f64(double x, double y) {
 // MODE 0 (ov):   q_s = w_s (O v)_s            (w NULL: 1)
 // MODE 1 (tanh): t_si = tanh(b_i + (X W^T)_si) with v = the parameter vector [a | b | W]
 template <int KT, int MODE = 0>
-__global__ void __launch_bounds__(256) ld_ov_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
+__global__ void __launch_bounds__(256, KT >= 16 ? 1 : 2) ld_ov_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
                                                     int64_t U, int N, int M, int words, const double2* __restrict__ v,
                                                     const double* __restrict__ vwt, double2* __restrict__ q,
                                                     const double* __restrict__ w = nullptr,
                                                     double2* __restrict__ t_out = nullptr) {
   __shared__ uint32_t smask[256 + 8];        // per-site masks of the block's 16 samples (N <= 256)
   __shared__ double2 red[8][kLdSB];          // per-warp partial q
+  __shared__ __align__(8) uint64_t tbar;
+  extern __shared__ __align__(16) double2 tsm[];  // MODE 0: the block's T rows [16][M], bulk-copied
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t s0 = (int64_t)blockIdx.x * kLdSB;
   const int pitch = ld_pitch(M), rows = ld_rows(N);
+  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(&tbar);
+  if constexpr (MODE == 0) {
+    // the epilogue's T rows stream in (TMA engine) under the GEMM
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint32_t bytes = (uint32_t)((min((int64_t)kLdSB, U - s0)) * M * 16);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(bytes) : "memory");
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(tsm);
+      for (uint32_t off = 0; off < bytes; off += 65536u) {
+        const uint32_t n = min(bytes - off, 65536u);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         dst + off), "l"((const char*)(t + s0 * M) + off), "r"(n), "r"(sbar)
+                     : "memory");
+      }
+    }
+  }
   for (int k = tid; k < rows; k += blockDim.x) {
     uint32_t m = 0;
     if (k < N)
@@ -89,19 +108,29 @@ __global__ void __launch_bounds__(256) ld_ov_kernel(const double2* __restrict__ 
     col[j] = min(warp + j * 8, NT - 1) * 8 + qc;
     acc[j][0][0] = acc[j][0][1] = acc[j][1][0] = acc[j][1][1] = 0.0;
   }
-  for (int k0 = 0; k0 < rows; k0 += 4) {
-    const double* brow = vwt + (size_t)(k0 + qr) * pitch;
-    double bf[KT];
+  // B fragments are prefetched one k-step ahead (L2 latency); n-tiles past NT
+  // (clamped duplicates) are skipped (warp-uniform)
+  double bf[KT], bn[KT];
 #pragma unroll
-    for (int j = 0; j < KT; ++j) bf[j] = __ldg(brow + col[j]);
+  for (int j = 0; j < KT; ++j) bf[j] = __ldg(vwt + (size_t)qr * pitch + col[j]);
+  for (int k0 = 0; k0 < rows; k0 += 4) {
+    if (k0 + 4 < rows) {
+      const double* brow = vwt + (size_t)(k0 + 4 + qr) * pitch;
+#pragma unroll
+      for (int j = 0; j < KT; ++j) bn[j] = __ldg(brow + col[j]);
+    }
     const uint32_t mk = smask[k0 + qr];
     const double a0 = __hiloint2double((int)(((mk >> qc) & 1u) * 0x3ff00000u), 0);
     const double a1 = __hiloint2double((int)(((mk >> (8 + qc)) & 1u) * 0x3ff00000u), 0);
 #pragma unroll
     for (int j = 0; j < KT; ++j) {
-      ld_dmma(acc[j][0][0], acc[j][0][1], a0, bf[j]);
-      ld_dmma(acc[j][1][0], acc[j][1][1], a1, bf[j]);
+      if (warp + j * 8 < NT) {
+        ld_dmma(acc[j][0][0], acc[j][0][1], a0, bf[j]);
+        ld_dmma(acc[j][1][0], acc[j][1][1], a1, bf[j]);
+      }
     }
+#pragma unroll
+    for (int j = 0; j < KT; ++j) bf[j] = bn[j];
   }
   if constexpr (MODE == 1) {
     // D fragment (sample m*8 + qc, unit nt*4 + qr) = theta - b: write tanh(theta)
@@ -120,6 +149,9 @@ __global__ void __launch_bounds__(256) ld_ov_kernel(const double2* __restrict__ 
     return;
   }
   // epilogue: D fragment (sample m*8 + qc, unit nt*4 + qr) -> t * (Y + vb), summed over units
+  asm volatile(
+      "{.reg .pred p;\nWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(sbar)
+      : "memory");
   double2 part[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
 #pragma unroll
   for (int j = 0; j < KT; ++j) {
@@ -130,7 +162,7 @@ __global__ void __launch_bounds__(256) ld_ov_kernel(const double2* __restrict__ 
       for (int m = 0; m < 2; ++m) {
         const int64_t s = s0 + m * 8 + qc;
         if (s < U) {
-          const double2 ts = t[s * M + i];
+          const double2 ts = tsm[(m * 8 + qc) * M + i];
           const double yr = acc[j][m][0] + vb.x, yi = acc[j][m][1] + vb.y;
           part[m].x = fma(ts.x, yr, fma(-ts.y, yi, part[m].x));
           part[m].y = fma(ts.x, yi, fma(ts.y, yr, part[m].y));
@@ -194,7 +226,7 @@ inline int64_t ld_chunk(int64_t U, int N, int M) {
 }
 
 template <int NTC>
-__global__ void __launch_bounds__(256) ld_ohu_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
+__global__ void __launch_bounds__(256, 2) ld_ohu_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
                                                      int64_t U, int N, int M, int words, const double2* __restrict__ u,
                                                      double* __restrict__ partial, int64_t chunk,
                                                      const double* __restrict__ wts = nullptr) {
