@@ -91,20 +91,33 @@ __device__ __forceinline__ float lc_near_zero(float x, float y) {
   return 0.34657359027997264f * lg2_approx(fmaf(sh, sh, sr * sr));
 }
 
-// f32 NATIVE: accurate single-precision regime-split form:
-// |cosh z|² = 1 + sinh²x - sin²y = sinh²x + cos²y.
+// f32 NATIVE: Re log cosh(x + iy) = 1/2 log(sinh^2 x + cos^2 y):
+// both terms are computed to a few f32 ulps *relative*, so the sum has no
+// cancellation, near the zeros of cosh included; branch-free (the lanes of a
+// warp hold different units).  sinh: odd series through x^9 for |x| < 1/2,
+// (e - 1/e)/2 from MUFU ex2 / rcp above (relative error < 3e-7 there);
+// cos^2 y: Cody-Waite reduction to [-pi/4, pi/4] and the quadrant's sin or cos
+// polynomial (< 1 ulp); log through MUFU lg2 (absolute error ~6e-8 per unit).
+// |x| > 40: |x| - ln 2 (the correction is < 1e-34).  (A two-MUFU variant with
+// the e^{-2|x|}-scaled form above |x| = 1/2 measured 13% slower: issue-bound.)
 __device__ __forceinline__ float lc_f32(float x, float y) {
   const float ax = fabsf(x);
-  float s, c;
-  sincosf(y, &s, &c);
-  if (ax > 9.0f) {
-    const float t = expf(-2.0f * ax);
-    const float c2 = fmaf(2.0f * c, c, -1.0f);
-    return ax - 0.69314718055994531f + 0.5f * log1pf(t * (t + 2.0f * c2));
-  }
-  const float sh = sinhf(ax);
-  if (c * c >= 0.5f) return 0.5f * log1pf(fmaf(sh, sh, -s * s));
-  return 0.5f * logf(fmaf(sh, sh, c * c));
+  const float x2 = ax * ax;
+  const float sh_s =
+      ax * fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, 2.7557319e-6f, 1.9841270e-4f), 8.3333333e-3f), 0.16666667f), 1.0f);
+  const float e = ex2_approx(ax * 1.4426950408889634f);
+  const float sh_l = 0.5f * (e - rcp_approx(e));
+  const float sh = ax < 0.5f ? sh_s : sh_l;
+  const float k = rintf(y * 0.63661977236758134f);  // y / (pi/2)
+  float r = fmaf(-k, 1.5707963705062866f, y);
+  r = fmaf(-k, -4.3711388286737929e-8f, r);
+  const float r2 = r * r;
+  const float sr = r * fmaf(r2, fmaf(r2, fmaf(r2, -1.9841270e-4f, 8.3333333e-3f), -0.16666667f), 1.0f);
+  const float cr = fmaf(r2, fmaf(r2, fmaf(r2, fmaf(r2, 2.4801587e-5f, -1.3888889e-3f), 4.1666667e-2f), -0.5f), 1.0f);
+  const float cy = (((int)k) & 1) ? sr : cr;  // |cos y|
+  const float v = fmaf(sh, sh, cy * cy);
+  const float lc = 0.34657359027997264f * lg2_approx(v);
+  return ax > 40.0f ? ax - 0.69314718055994531f : lc;
 }
 
 // f64: the reference formula op for op (rbm.py:130-140 / _kernels.py:101-106).
@@ -378,7 +391,8 @@ __device__ __forceinline__ void report_nonfinite(int64_t* status, int64_t step, 
 // ------------------------------------------------------------------------
 
 template <int FMT, int VAR, int G, int U, int PROP, bool SMEM>
-__global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, 1) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP == MPV_PROPOSAL_FLIP || SMEM) ? 1 : 2)
+    sweep_kernel(const SweepArgs a) {
   using A = Acc<FMT, VAR>;
   using E = Eval<FMT, VAR>;
   using Entry = typename A::Entry;
