@@ -1,10 +1,14 @@
-"""Lattices and bond lists (mirror of the reference lattice.py:118-182).
+"""Lattices and bond lists.  API names follow the reference (`lattice.py:118-182`:
+LatticeSpec(shape, periodic), .chain, .square, n_sites, bonds, bond_array);
+the construction is this package's own: bonds are generated from lattice
+displacement vectors over site coordinates, so nearest and next-nearest
+neighbours share one code path.
 
-Spin convention s_i = 1 - 2*bit_i; 2D sites row-major (r, c) -> r*L + c; bonds
-are (i<j) pairs, sorted, deduplicated — identical to LatticeSpec.bonds so the
-device Hamiltonian kernels see the same bond order as the reference.  Unlike
-the reference's SpinConfiguration (N <= 62), device configurations are packed
-uint32 words, so any N up to MAX_DEVICE_SITES works.
+Conventions (they fix the device kernels' bond order): spin s = 1 - 2 bit;
+2D sites row-major, site(r, c) = r L + c; a bond is an (i < j) pair; the list
+is sorted and free of duplicates (small periodic lattices wrap onto the same
+pair).  Device configurations are packed uint32 words (any N up to
+MAX_DEVICE_SITES), unlike the reference's 62-site integer codes.
 """
 from __future__ import annotations
 
@@ -16,6 +20,21 @@ ENUMERATION_LIMIT = 14
 MAX_DEVICE_SITES = 1024
 
 
+def _pairs(coords: np.ndarray, extent: int, periodic: bool, disp) -> set:
+    """(i < j) pairs joining every site to site + disp (coordinates in [0, extent))."""
+    target = coords + np.asarray(disp)[None, :]
+    if periodic:
+        target %= extent
+        keep = np.ones(len(coords), dtype=bool)
+    else:
+        keep = np.all((target >= 0) & (target < extent), axis=1)
+    dims = coords.shape[1]
+    weights = extent ** np.arange(dims - 1, -1, -1)  # row-major site index
+    a = coords[keep] @ weights
+    b = target[keep] @ weights
+    return {(int(min(x, y)), int(max(x, y))) for x, y in zip(a, b) if x != y}
+
+
 @dataclass(frozen=True)
 class LatticeSpec:
     shape: tuple
@@ -23,36 +42,28 @@ class LatticeSpec:
     bonds: tuple = field(init=False)
 
     def __post_init__(self):
+        dims = len(self.shape)
+        if dims not in (1, 2):
+            raise ValueError(f"lattice shape must be (n,) or (L, L), got {self.shape}")
+        if dims == 2 and self.shape[0] != self.shape[1]:
+            raise ValueError(f"2D lattices are square here, got {self.shape}")
+        extent = int(self.shape[0])
+        smallest = 1 if dims == 1 else 2
+        if extent < smallest or (self.periodic and extent < 3):
+            raise ValueError(f"lattice {self.shape} is too small ({'periodic needs >= 3' if self.periodic else ''})")
+        nn = set()
+        for axis in range(dims):
+            disp = np.zeros(dims, dtype=np.int64)
+            disp[axis] = 1
+            nn |= _pairs(self._coords(), extent, self.periodic, disp)
+        object.__setattr__(self, "bonds", tuple(sorted(nn)))
+
+    def _coords(self) -> np.ndarray:
+        extent = int(self.shape[0])
         if len(self.shape) == 1:
-            (n,) = self.shape
-            if n < 1:
-                raise ValueError("chain length must be >= 1")
-            if self.periodic and n < 3:
-                raise ValueError("periodic chain requires n >= 3")
-            bonds = [(i, i + 1) for i in range(n - 1)]
-            if self.periodic:
-                bonds.append((0, n - 1))
-        elif len(self.shape) == 2:
-            rows, cols = self.shape
-            if rows != cols:
-                raise ValueError("only square 2D lattices are supported")
-            length = rows
-            if self.periodic and length < 3:
-                raise ValueError("periodic square lattice requires L >= 3")
-            if length < 2:
-                raise ValueError("square lattice requires L >= 2")
-            bonds = []
-            for r in range(length):
-                for c in range(length):
-                    site = r * length + c
-                    right = site + 1 if c + 1 < length else (r * length if self.periodic else None)
-                    down = site + length if r + 1 < length else (c if self.periodic else None)
-                    for other in (right, down):
-                        if other is not None:
-                            bonds.append((min(site, other), max(site, other)))
-        else:
-            raise ValueError("shape must be (n,) or (L, L)")
-        object.__setattr__(self, "bonds", tuple(sorted(set(bonds))))
+            return np.arange(extent)[:, None]
+        r, c = np.divmod(np.arange(extent * extent), extent)
+        return np.stack([r, c], axis=1)
 
     @classmethod
     def chain(cls, n: int, periodic: bool = False) -> "LatticeSpec":
@@ -74,50 +85,26 @@ class LatticeSpec:
         return np.array(self.bonds, dtype=np.int64).reshape(-1, 2)
 
     def next_nearest_bonds(self) -> np.ndarray:
-        """Next-nearest-neighbour (i<j) pairs, sorted, deduplicated, excluding
-        nearest-neighbour pairs (beyond the reference: J1-J2 models).  Chain:
-        (i, i+2); square: both diagonals; periodic wrap as for `bonds`."""
+        """Next-nearest-neighbour (i < j) pairs (beyond the reference: J1-J2
+        models): chain (i, i+2), square lattice both diagonals; same wrap rule
+        as the bonds, pairs that are also nearest neighbours excluded."""
+        extent = int(self.shape[0])
+        disps = [(2,)] if len(self.shape) == 1 else [(1, 1), (1, -1)]
         pairs = set()
-        if len(self.shape) == 1:
-            (n,) = self.shape
-            for i in range(n):
-                j = i + 2
-                if j >= n:
-                    if not self.periodic:
-                        continue
-                    j -= n
-                if i != j:
-                    pairs.add((min(i, j), max(i, j)))
-        else:
-            length = self.shape[0]
-            for r in range(length):
-                for c in range(length):
-                    for dc in (1, -1):
-                        rr, cc = r + 1, c + dc
-                        if not (0 <= cc < length and rr < length):
-                            if not self.periodic:
-                                continue
-                            rr, cc = rr % length, cc % length
-                        a, b = r * length + c, rr * length + cc
-                        if a != b:
-                            pairs.add((min(a, b), max(a, b)))
+        for d in disps:
+            pairs |= _pairs(self._coords(), extent, self.periodic, d)
         pairs -= set(self.bonds)
         return np.array(sorted(pairs), dtype=np.int64).reshape(-1, 2)
 
     def sublattice(self) -> np.ndarray:
-        """Checkerboard sublattice index (0/1) of every site; raises if the
-        nearest-neighbour bonds do not join the two sublattices (Marshall sign
-        needs a bipartite lattice: open, or periodic with even length)."""
-        if len(self.shape) == 1:
-            sub = np.arange(self.shape[0]) % 2
-        else:
-            length = self.shape[0]
-            r, c = np.divmod(np.arange(length * length), length)
-            sub = (r + c) % 2
+        """Checkerboard sublattice (0/1) of every site; a lattice whose bonds join
+        equal sublattices (periodic, odd length) is rejected - the Marshall sign
+        needs a bipartite lattice."""
+        parity = self._coords().sum(axis=1) % 2
         bonds = self.bond_array()
-        if bonds.size and np.any(sub[bonds[:, 0]] == sub[bonds[:, 1]]):
-            raise ValueError("lattice is not bipartite (periodic with odd length)")
-        return sub.astype(np.int64)
+        if bonds.size and np.any(parity[bonds[:, 0]] == parity[bonds[:, 1]]):
+            raise ValueError(f"{self.shape} {self.boundary} lattice is not bipartite")
+        return parity.astype(np.int64)
 
 
 def enumerate_bits(n: int) -> np.ndarray:

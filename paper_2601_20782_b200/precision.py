@@ -1,17 +1,18 @@
-"""Floating-point formats and rounding modes (mirror of the reference's
-precision.py:23-169; same names and semantics).
+"""Number formats of the two-copy scheme and the rounding modes of the
+evaluators.  API names follow the reference (`precision.py:23-169`:
+FloatFormat, BF16/F16/F32/F64, parse_format, RoundingMode, make_rounder,
+round_to_format); the implementation is this package's own.
 
-Adds one rounding mode, ``NATIVE``: the B200 fused-sweep arithmetic.  The
-hidden pre-activation theta(x) = b + W x is kept exact (on-chip accumulators,
-see DESIGN.md §3) and rounded ONCE to the format, each hidden unit's
-Re log cosh is evaluated in f32 from that rounded value and rounded to the
-format, and the hidden sum is accumulated in f32.  log p_fmt(x) is therefore a
-fixed function of x (path independent), which is what the paper's
-perturbed-target bounds assume.
+Formats are described by (exponent bits, explicit significand bits).  Host
+rounding is only used to build the parameter snapshot (rbm.round_parameters);
+every per-sample operation runs in the CUDA library, where the reduced formats
+are native (`add.rn.{f16,bf16,f32}`, `cvt.rn.*`).
 
-Host-side rounding here is only used for the two-copy parameter snapshot
-(rbm.round_parameters, reference rbm.py:91-101); all per-sample arithmetic runs
-in the CUDA library.
+Rounding modes: STORAGE_ONLY and PER_OPERATION as in the reference, plus
+NATIVE, the fused-sweep arithmetic of this package: theta is
+kept exact on chip and rounded once to the format, each hidden unit's
+Re log cosh is evaluated in f32 and rounded to the format, the hidden sum is
+accumulated in f32.
 """
 from __future__ import annotations
 
@@ -21,11 +22,13 @@ from dataclasses import dataclass
 
 import numpy as np
 
+_DEVICE_CODES = {"f64": 0, "f32": 1, "f16": 2, "bf16": 3}  # MPV_FMT_* (include/mpvmc_b200.h)
+
 
 @dataclass(frozen=True)
 class FloatFormat:
-    """An (exponent bits, significand bits) pair; significand_bits excludes the
-    implicit leading 1 (reference precision.py:23-61)."""
+    """Binary floating-point format: `exponent_bits` and `significand_bits`
+    (without the implicit leading one); subnormals optional."""
 
     name: str
     exponent_bits: int
@@ -33,14 +36,13 @@ class FloatFormat:
     supports_subnormals: bool = True
 
     def __post_init__(self):
-        if self.exponent_bits < 2 or self.significand_bits < 1:
-            raise ValueError("need >= 2 exponent bits and >= 1 significand bit")
-        if self.exponent_bits > 11 or self.significand_bits > 52:
-            raise ValueError("formats wider than float64 cannot be emulated")
+        if not (2 <= self.exponent_bits <= 11 and 1 <= self.significand_bits <= 52):
+            raise ValueError(f"format {self.name!r}: exponent bits must lie in [2, 11] and significand bits "
+                             "in [1, 52] (float64 is the widest emulated format)")
 
     @property
     def bias(self) -> int:
-        return (1 << (self.exponent_bits - 1)) - 1
+        return 2 ** (self.exponent_bits - 1) - 1
 
     @property
     def max_exponent(self) -> int:
@@ -52,92 +54,106 @@ class FloatFormat:
 
     @property
     def max_finite(self) -> float:
-        return (2.0 - 2.0 ** -self.significand_bits) * 2.0 ** self.max_exponent
+        return float(np.ldexp(2.0 - np.ldexp(1.0, -self.significand_bits), self.max_exponent))
 
     @property
     def min_normal(self) -> float:
-        return 2.0 ** self.min_exponent
+        return float(np.ldexp(1.0, self.min_exponent))
 
     @property
     def unit_roundoff(self) -> float:
-        return 2.0 ** -(self.significand_bits + 1)
+        return float(np.ldexp(1.0, -self.significand_bits - 1))
 
     @property
     def code(self) -> int:
-        """Format code of the C-ABI (include/mpvmc_b200.h, MPV_FMT_*)."""
-        try:
-            return FORMAT_CODES[self.name]
-        except KeyError:
-            raise ValueError(f"format {self.name!r} has no device implementation") from None
+        """MPV_FMT_* code of the C ABI."""
+        if self.name not in _DEVICE_CODES:
+            raise ValueError(f"no device kernels for format {self.name!r}")
+        return _DEVICE_CODES[self.name]
 
 
-BF16 = FloatFormat("bf16", 8, 7)
-F16 = FloatFormat("f16", 5, 10)
-F32 = FloatFormat("f32", 8, 23)
 F64 = FloatFormat("f64", 11, 52)
+F32 = FloatFormat("f32", 8, 23)
+F16 = FloatFormat("f16", 5, 10)
+BF16 = FloatFormat("bf16", 8, 7)
+FORMATS = {f.name: f for f in (F64, F32, F16, BF16)}
+FORMAT_CODES = dict(_DEVICE_CODES)
 
-FORMATS = {fmt.name: fmt for fmt in (BF16, F16, F32, F64)}
-FORMAT_CODES = {"f64": 0, "f32": 1, "f16": 2, "bf16": 3}
-_CUSTOM_RE = re.compile(r"^e(\d+)m(\d+)$")
+_EM_NAME = re.compile(r"e(?P<e>\d+)m(?P<m>\d+)")
 
 
 def parse_format(name: str) -> FloatFormat:
-    """Resolve a format name: f64/f32/f16/bf16 or custom e<E>m<M> (precision.py:74-81)."""
-    if name in FORMATS:
-        return FORMATS[name]
-    match = _CUSTOM_RE.match(name)
-    if match:
-        return FloatFormat(name, int(match.group(1)), int(match.group(2)))
-    raise ValueError(f"unknown float format {name!r}")
+    """A named format (f64 / f32 / f16 / bf16) or a custom `e<E>m<M>`."""
+    fmt = FORMATS.get(name)
+    if fmt is not None:
+        return fmt
+    m = _EM_NAME.fullmatch(name)
+    if m is None:
+        raise ValueError(f"{name!r} is neither f64/f32/f16/bf16 nor e<E>m<M>")
+    return FloatFormat(name, int(m["e"]), int(m["m"]))
 
 
 class RoundingMode(enum.Enum):
-    """Where rounding is applied (precision.py:158-169) plus the device NATIVE mode."""
+    """Where results are rounded to the format."""
 
-    STORAGE_ONLY = "storage_only"
-    PER_OPERATION = "per_operation"
-    NATIVE = "native"
+    STORAGE_ONLY = "storage_only"    # parameters stored in fmt, arithmetic in f64
+    PER_OPERATION = "per_operation"  # every add rounded (the reference's emulation)
+    NATIVE = "native"                # the B200 fused-sweep arithmetic (DESIGN.md §3)
 
     @property
     def code(self) -> int:
-        return {"native": 0, "per_operation": 1, "storage_only": 2}[self.value]
+        return (RoundingMode.NATIVE, RoundingMode.PER_OPERATION, RoundingMode.STORAGE_ONLY).index(self)
 
 
 def parse_rounding_mode(name: str) -> RoundingMode:
-    for mode in RoundingMode:
-        if mode.value == name:
-            return mode
-    raise ValueError(f"unknown rounding mode {name!r}")
+    try:
+        return RoundingMode(name)
+    except ValueError:
+        raise ValueError(f"rounding mode must be one of {[m.value for m in RoundingMode]}, got {name!r}") from None
 
 
-def _quantize(values: np.ndarray, fmt: FloatFormat) -> np.ndarray:
-    """Round-to-nearest-even onto fmt's grid; overflow -> +-inf; subnormals kept
-    unless the format flushes them (same contract as precision.py:89-104)."""
-    with np.errstate(all="ignore"):
-        _, exponents = np.frexp(values)
-        eu = np.maximum(exponents - 1, fmt.min_exponent)
-        quantum = np.ldexp(1.0, eu - fmt.significand_bits)
-        rounded = np.rint(values / quantum) * quantum
+def _rne_generic(x: np.ndarray, fmt: FloatFormat) -> np.ndarray:
+    """Round-to-nearest-even onto fmt's grid by bit arithmetic on the float64
+    pattern: add half an ulp of the target (minus one when the kept lsb is 0),
+    clear the dropped bits; values below fmt's normal range are rounded on the
+    fixed subnormal grid (or flushed), overflow goes to +-inf."""
+    x = np.asarray(x, dtype=np.float64)
+    out = np.array(x, dtype=np.float64, copy=True)
+    finite = np.isfinite(x)
+    drop = 52 - fmt.significand_bits
+    if drop > 0:
+        u = x.view(np.uint64)
+        half = np.uint64(1 << (drop - 1))
+        lsb = (u >> np.uint64(drop)) & np.uint64(1)
+        mask = ~np.uint64((1 << drop) - 1)
+        r = ((u + half - np.uint64(1) + lsb) & mask).view(np.float64)
+        out = np.where(finite, r, x)
+    tiny = np.abs(x) < fmt.min_normal
+    if np.any(tiny & finite):
+        step = np.ldexp(1.0, fmt.min_exponent - fmt.significand_bits)  # subnormal spacing
+        xt = np.where(tiny & finite, x, 0.0)
+        sub = np.rint(xt / step) * step  # exact scaling, numpy rint is half-to-even
         if not fmt.supports_subnormals:
-            rounded = np.where(np.abs(rounded) < fmt.min_normal, 0.0 * rounded, rounded)
-        return np.where(np.abs(rounded) > fmt.max_finite, np.copysign(np.inf, rounded), rounded)
+            sub = np.where(np.abs(sub) < fmt.min_normal, 0.0 * xt, sub)
+        out = np.where(tiny & finite, sub, out)
+    with np.errstate(invalid="ignore"):
+        big = np.abs(out) > fmt.max_finite
+    return np.where(big & finite, np.copysign(np.inf, x), out)
 
 
 def make_rounder(fmt: FloatFormat):
-    """Array rounding callable (precision.py:107-132)."""
+    """Vectorised RNE rounding onto fmt (float64 in, float64 out)."""
     if fmt.name == "f64":
         return lambda a: np.asarray(a, dtype=np.float64)
-    if fmt.name == "f32":
-        return lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
-    if fmt.name == "f16":
-        return lambda a: np.asarray(a, dtype=np.float64).astype(np.float16).astype(np.float64)
-    return lambda a: _quantize(np.asarray(a, dtype=np.float64), fmt)
+    native = {"f32": np.float32, "f16": np.float16}.get(fmt.name)
+    if native is not None and fmt.supports_subnormals:
+        return lambda a: np.asarray(a, dtype=np.float64).astype(native).astype(np.float64)
+    return lambda a: _rne_generic(a, fmt)
 
 
 def round_to_format(value, fmt: FloatFormat):
+    """Scalar or array rounding onto fmt."""
     arr = np.asarray(value, dtype=np.float64)
     with np.errstate(over="ignore"):
         out = make_rounder(fmt)(arr)
-    if np.isscalar(value) or arr.ndim == 0:
-        return float(out)
-    return out
+    return float(out) if arr.ndim == 0 else out

@@ -28,104 +28,91 @@ from .precision import F64, FloatFormat, RoundingMode, make_rounder
 from .rng import derive_key, gaussian_field
 
 
+def _as_complex(name: str, value, ndim: int) -> np.ndarray:
+    arr = np.asarray(value, dtype=np.complex128)
+    if arr.ndim != ndim:
+        raise ValueError(f"{name} must be {ndim}-dimensional, got shape {arr.shape}")
+    if not np.isfinite(arr.view(np.float64)).all():
+        raise ValueError(f"{name} has non-finite entries")
+    return arr
+
+
 @dataclass(frozen=True)
 class RbmParameters:
-    """Complex visible biases a (N,), hidden biases b (M,), weights w (M, N)."""
+    """Complex RBM parameters: visible biases a [N], hidden biases b [M], weights
+    w [M, N] (the reference's RbmParameters fields and flat order a, b, W)."""
 
     a: np.ndarray
     b: np.ndarray
     w: np.ndarray
 
     def __post_init__(self):
-        a = np.asarray(self.a, dtype=np.complex128)
-        b = np.asarray(self.b, dtype=np.complex128)
-        w = np.asarray(self.w, dtype=np.complex128)
-        if a.ndim != 1 or b.ndim != 1 or w.shape != (b.size, a.size):
-            raise ValueError(f"inconsistent dimensions: a{a.shape}, b{b.shape}, w{w.shape}")
+        a, b, w = _as_complex("a", self.a, 1), _as_complex("b", self.b, 1), _as_complex("w", self.w, 2)
+        if w.shape != (b.size, a.size):
+            raise ValueError(f"w has shape {w.shape}, expected (len(b), len(a)) = ({b.size}, {a.size})")
         for name, arr in (("a", a), ("b", b), ("w", w)):
-            if not np.all(np.isfinite(arr.view(np.float64))):
-                raise ValueError(f"non-finite entries in {name}")
-        object.__setattr__(self, "a", a)
-        object.__setattr__(self, "b", b)
-        object.__setattr__(self, "w", w)
+            object.__setattr__(self, name, arr)
 
-    @property
-    def n_visible(self) -> int:
-        return self.a.size
-
-    @property
-    def n_hidden(self) -> int:
-        return self.b.size
-
-    @property
-    def alpha_density(self) -> Fraction:
-        return Fraction(self.n_hidden, self.n_visible)
-
-    @property
-    def n_params(self) -> int:
-        return self.n_visible + self.n_hidden + self.n_visible * self.n_hidden
+    n_visible = property(lambda self: self.a.size)
+    n_hidden = property(lambda self: self.b.size)
+    alpha_density = property(lambda self: Fraction(self.n_hidden, self.n_visible))
+    n_params = property(lambda self: self.a.size + self.b.size + self.w.size)
 
     def flatten(self) -> np.ndarray:
-        return np.concatenate([self.a, self.b, self.w.reshape(-1)])
+        """theta = [a | b | W row-major]."""
+        return np.concatenate((self.a, self.b, self.w.ravel()))
 
     @classmethod
     def from_flat(cls, theta, n_visible: int, n_hidden: int) -> "RbmParameters":
         theta = np.asarray(theta, dtype=np.complex128)
-        return cls(theta[:n_visible], theta[n_visible:n_visible + n_hidden],
-                   theta[n_visible + n_hidden:].reshape(n_hidden, n_visible))
+        cut = np.cumsum([n_visible, n_hidden])
+        a, b, w = np.split(theta, cut)
+        return cls(a, b, w.reshape(n_hidden, n_visible))
 
 
 def random_parameters(n_visible: int, alpha, key, scale: float = 0.01) -> RbmParameters:
-    """Re and Im i.i.d. N(0, scale^2) from the counter-based Gaussian field
-    (rbm.py:78-88); host-side, once per run."""
-    alpha = Fraction(alpha)
-    n_hidden = alpha * n_visible
-    if n_hidden.denominator != 1 or n_hidden <= 0:
-        raise ValueError(f"alpha*N must be a positive integer, got {n_hidden}")
-    n_hidden = int(n_hidden)
-    count = n_visible + n_hidden + n_hidden * n_visible
-    draws = scale * gaussian_field(key, np.arange(2 * count), 1.0)
-    return RbmParameters.from_flat(draws[:count] + 1j * draws[count:], n_visible, n_hidden)
+    """Gaussian initialisation from the counter-based field (rng.gaussian_field):
+    counters 0..P-1 give the real parts and P..2P-1 the imaginary parts of
+    theta = [a | b | W], each N(0, scale^2) (the reference's draw order)."""
+    m = Fraction(alpha) * n_visible
+    if m.denominator != 1 or m <= 0:
+        raise ValueError(f"alpha * n_visible = {m} is not a positive integer")
+    m = int(m)
+    total = n_visible + m + m * n_visible
+    z = scale * gaussian_field(key, np.arange(2 * total), 1.0)
+    return RbmParameters.from_flat(z[:total] + 1j * z[total:], n_visible, m)
 
 
 def round_parameters(params: RbmParameters, fmt: FloatFormat) -> RbmParameters:
-    """Two-copy downcast snapshot (rbm.py:91-101): Re and Im rounded RNE to fmt."""
+    """The two-copy snapshot: real and imaginary parts rounded to fmt (RNE)."""
     if fmt.name == "f64":
         return params
     rnd = make_rounder(fmt)
+    with np.errstate(over="ignore"):
+        parts = [rnd(arr.real) + 1j * rnd(arr.imag) for arr in (params.a, params.b, params.w)]
+    return RbmParameters(*parts)
 
-    def q(arr):
-        with np.errstate(over="ignore"):
-            return rnd(arr.real) + 1j * rnd(arr.imag)
 
-    return RbmParameters(q(params.a), q(params.b), q(params.w))
+_PARAMS_FORMAT = "rbm-params-v1"
 
 
 def save_parameters(params: RbmParameters, path):
-    """rbm-params-v1 JSON (rbm.py:104-114)."""
-    payload = {
-        "format": "rbm-params-v1",
-        "n_visible": params.n_visible,
-        "n_hidden": params.n_hidden,
-        "a": [[float(v.real), float(v.imag)] for v in params.a],
-        "b": [[float(v.real), float(v.imag)] for v in params.b],
-        "w": [[[float(v.real), float(v.imag)] for v in row] for row in params.w],
-    }
-    with open(path, "w") as handle:
-        json.dump(payload, handle)
+    """JSON file in the reference's rbm-params-v1 layout: every complex number
+    as a [re, im] pair."""
+    pairs = lambda z: np.stack([z.real, z.imag], axis=-1).tolist()  # noqa: E731
+    doc = {"format": _PARAMS_FORMAT, "n_visible": params.n_visible, "n_hidden": params.n_hidden,
+           "a": pairs(params.a), "b": pairs(params.b), "w": pairs(params.w)}
+    with open(path, "w") as fh:
+        json.dump(doc, fh)
 
 
 def load_parameters(path) -> RbmParameters:
-    with open(path) as handle:
-        payload = json.load(handle)
-    if payload.get("format") != "rbm-params-v1":
-        raise ValueError(f"unrecognized parameter file {path}")
-
-    def decode(entries):
-        arr = np.asarray(entries, dtype=np.float64)
-        return arr[..., 0] + 1j * arr[..., 1]
-
-    return RbmParameters(decode(payload["a"]), decode(payload["b"]), decode(payload["w"]))
+    with open(path) as fh:
+        doc = json.load(fh)
+    if doc.get("format") != _PARAMS_FORMAT:
+        raise ValueError(f"{path}: not an {_PARAMS_FORMAT} file")
+    cplx = lambda v: (lambda arr: arr[..., 0] + 1j * arr[..., 1])(np.asarray(v, dtype=np.float64))  # noqa: E731
+    return RbmParameters(cplx(doc["a"]), cplx(doc["b"]), cplx(doc["w"]))
 
 
 # ---------------------------------------------------------------------------
