@@ -56,20 +56,28 @@ extern "C" {
  * A prepared parameter snapshot in kernel layout (the device counterpart of
  * ref: rbm.py:161-200 _PreparedRounded, built by the host from
  * round_parameters(params, fmt), ref: rbm.py:91-101).  Column-major by site
- * so one flip reads one contiguous column: entry (k, i) at table[k*hidden_pad+i].
+ * so one flip reads one contiguous column.  The hidden units are split into
+ * `cluster` rank blocks of GU = lanes_per_chain * units_per_lane units
+ * (hidden_pad = cluster * GU): entry (k, i) of rank block r = i / GU sits at
+ * element r * RB + k * GU + i % GU, RB = round_up(N * GU * entry, 16) / entry
+ * (cluster = 1: table[k * hidden_pad + i]).  With cluster > 1 the fused sweep
+ * runs as thread-block clusters: CTA rank r stages block r in shared memory
+ * and the ranks exchange partial log-cosh sums over distributed shared memory
+ * every step (tables beyond one SM's shared memory stay on chip).
  *   entry type      table/bias element            vis element
  *   X1, PER_OP      fmt pair (re,im): 4 B f16/bf16, 8 B f32      float (a_re)
  *   X2              two fmt pairs (hi, lo)                       float2 (hi, lo)
  *   F64             double2 (re, im)                             double
  *   XI              int2 (re, im) = value / quantum              int
  * `vis_im` (double[N], a_im) is only read by mpv_snapshot_forward (log psi).
- * For the fused sweep `vis` must sit at table + round_up(N*hidden_pad*entry, 16):
- * [table | vis] is staged into shared memory with one bulk copy.
+ * For the fused sweep `vis` must sit at table + cluster * RB * entry:
+ * [table | vis] is staged into shared memory with bulk copies.
  */
 typedef struct {
   int32_t n_visible, n_hidden, hidden_pad;
   int32_t fmt, mode, variant;
   int32_t lanes_per_chain, units_per_lane;
+  int32_t cluster; /* 1, 2 or 4 rank blocks (mpv_plan_cluster) */
   const void* table;
   const void* bias;
   const void* vis;
@@ -96,7 +104,7 @@ typedef struct {
  * planner (paper_2601_20782_b200/rbm.py plan_exact).
  * mpv_snapshot_fill: writes table/bias/vis (and vis_im if set) of `snap`, whose
  * layout fields and buffers the caller has set, from `rounded`; split = X2 grid. */
-int mpv_snapshot_bytes(int n_visible, int hidden_pad, int fmt, int mode, int variant, size_t* out);
+int mpv_snapshot_bytes(int n_visible, int hidden_pad, int fmt, int mode, int variant, int cluster, size_t* out);
 int mpv_snapshot_round(int N, int M, int fmt, const double* params, double* rounded, double* plan,
                        void* stream);
 int mpv_snapshot_fill(const mpv_snapshot* snap, const double* rounded, double split, void* stream);
@@ -331,6 +339,13 @@ int mpv_sum_i64(const int64_t* x, int64_t n, int64_t* out, void* stream);
  * (N, M, fmt, variant), hence of the snapshot. */
 int mpv_plan_layout(int n_visible, int n_hidden, int fmt, int variant, int32_t* lanes_per_chain,
                     int32_t* units_per_lane);
+/* Layout of the fused sweep including the cluster split: the smallest cluster
+ * size (1, 2, 4) whose per-CTA rank block (+ visible biases and exchange
+ * buffers) fits in shared memory, and the (G, U) of one rank block's
+ * ceil(M / cluster) units; cluster = 1 with a table beyond shared memory when
+ * none fits (read through L1/L2). */
+int mpv_plan_cluster(int n_visible, int n_hidden, int fmt, int mode, int variant, int32_t* cluster,
+                     int32_t* lanes_per_chain, int32_t* units_per_lane);
 
 const char* mpv_last_error(void);
 const char* mpv_version(void);

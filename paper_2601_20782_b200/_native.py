@@ -30,7 +30,7 @@ class Snapshot(ctypes.Structure):
     _fields_ = [
         ("n_visible", _i32), ("n_hidden", _i32), ("hidden_pad", _i32),
         ("fmt", _i32), ("mode", _i32), ("variant", _i32),
-        ("lanes_per_chain", _i32), ("units_per_lane", _i32),
+        ("lanes_per_chain", _i32), ("units_per_lane", _i32), ("cluster", _i32),
         ("table", _vp), ("bias", _vp), ("vis", _vp), ("vis_im", _vp), ("quantum", _f64),
         ("noise_key", _u64), ("noise_sigma", _f64),
     ]
@@ -56,7 +56,9 @@ class CG(ctypes.Structure):
 _SIGNATURES = {
     "mpv_stream_uniforms": (ctypes.c_int, [_u64, _i64, _i64, _i64, _i64, _vp, _vp]),
     "mpv_snapshot_bytes": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                          ctypes.POINTER(ctypes.c_size_t)]),
+                                          ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
+    "mpv_plan_cluster": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "mpv_snapshot_round": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
     "mpv_snapshot_fill": (ctypes.c_int, [ctypes.POINTER(Snapshot), _vp, ctypes.c_double, _vp]),
     "mpv_table_sweep": (ctypes.c_int, [_vp, ctypes.POINTER(Chains), _u64, ctypes.c_int, _i64, _i64, _i64, _i64, _vp,
@@ -163,6 +165,13 @@ def stream_handle(device=None) -> int:
     import torch
 
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def plan_cluster(n_visible: int, n_hidden: int, fmt: int, mode: int, variant: int):
+    """(cluster, G, U) of the fused sweep's layout (mpv_plan_cluster)."""
+    c, g, u = _i32(), _i32(), _i32()
+    call("mpv_plan_cluster", n_visible, n_hidden, fmt, mode, variant, ctypes.byref(c), ctypes.byref(g), ctypes.byref(u))
+    return c.value, g.value, u.value
 
 
 def plan_layout(n_visible: int, n_hidden: int, fmt: int = FMT_F16, variant: int = ACC_X1):

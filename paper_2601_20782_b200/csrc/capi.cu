@@ -15,7 +15,7 @@
 #include "sweep.cuh"
 
 namespace mpv {
-#define MPV_DECL(f, v) void* sweep_kernel_ptr_##f##_##v(int G, int U, int prop, int smem);
+#define MPV_DECL(f, v) void* sweep_kernel_ptr_##f##_##v(int G, int U, int prop, int smem, int cs);
 MPV_DECL(f16, x1) MPV_DECL(f16, x2) MPV_DECL(f16, f64) MPV_DECL(f16, xi)
 MPV_DECL(bf16, x1) MPV_DECL(bf16, x2) MPV_DECL(bf16, f64) MPV_DECL(bf16, xi)
 MPV_DECL(f32, x1) MPV_DECL(f32, x2) MPV_DECL(f32, f64)
@@ -35,25 +35,25 @@ cudaError_t forward_tc_prepare(int N, int M, int fmt, const double* params, void
 cudaError_t forward_tc_launch(int N, int M, int fmt, const void* weights, const uint32_t* bits, int64_t B,
                               double* out_lp, double* out_re, double* out_im, int max_ctas, cudaStream_t st);
 
-void* sweep_kernel_ptr(int fmt, int variant, int G, int U, int prop, int smem) {
+void* sweep_kernel_ptr(int fmt, int variant, int G, int U, int prop, int smem, int cs) {
   switch (fmt) {
     case MPV_FMT_F16:
-      return variant == MPV_ACC_X1 ? sweep_kernel_ptr_f16_x1(G, U, prop, smem)
-           : variant == MPV_ACC_X2 ? sweep_kernel_ptr_f16_x2(G, U, prop, smem)
-           : variant == MPV_ACC_XI ? sweep_kernel_ptr_f16_xi(G, U, prop, smem)
-                                   : sweep_kernel_ptr_f16_f64(G, U, prop, smem);
+      return variant == MPV_ACC_X1 ? sweep_kernel_ptr_f16_x1(G, U, prop, smem, cs)
+           : variant == MPV_ACC_X2 ? sweep_kernel_ptr_f16_x2(G, U, prop, smem, cs)
+           : variant == MPV_ACC_XI ? sweep_kernel_ptr_f16_xi(G, U, prop, smem, cs)
+                                   : sweep_kernel_ptr_f16_f64(G, U, prop, smem, cs);
     case MPV_FMT_BF16:
-      return variant == MPV_ACC_X1 ? sweep_kernel_ptr_bf16_x1(G, U, prop, smem)
-           : variant == MPV_ACC_X2 ? sweep_kernel_ptr_bf16_x2(G, U, prop, smem)
-           : variant == MPV_ACC_XI ? sweep_kernel_ptr_bf16_xi(G, U, prop, smem)
-                                   : sweep_kernel_ptr_bf16_f64(G, U, prop, smem);
+      return variant == MPV_ACC_X1 ? sweep_kernel_ptr_bf16_x1(G, U, prop, smem, cs)
+           : variant == MPV_ACC_X2 ? sweep_kernel_ptr_bf16_x2(G, U, prop, smem, cs)
+           : variant == MPV_ACC_XI ? sweep_kernel_ptr_bf16_xi(G, U, prop, smem, cs)
+                                   : sweep_kernel_ptr_bf16_f64(G, U, prop, smem, cs);
     case MPV_FMT_F32:  // (no integer accumulators for f32 snapshots)
-      return variant == MPV_ACC_X1    ? sweep_kernel_ptr_f32_x1(G, U, prop, smem)
-           : variant == MPV_ACC_X2    ? sweep_kernel_ptr_f32_x2(G, U, prop, smem)
-           : variant == MPV_ACC_F64   ? sweep_kernel_ptr_f32_f64(G, U, prop, smem)
+      return variant == MPV_ACC_X1    ? sweep_kernel_ptr_f32_x1(G, U, prop, smem, cs)
+           : variant == MPV_ACC_X2    ? sweep_kernel_ptr_f32_x2(G, U, prop, smem, cs)
+           : variant == MPV_ACC_F64   ? sweep_kernel_ptr_f32_f64(G, U, prop, smem, cs)
                                       : nullptr;
     default:
-      return sweep_kernel_ptr_f64_f64(G, U, prop, smem);
+      return sweep_kernel_ptr_f64_f64(G, U, prop, smem, cs);
   }
 }
 }  // namespace mpv
@@ -119,6 +119,16 @@ size_t vis_bytes(int fmt, int variant) {
   if (variant == MPV_ACC_XI) return 4;
   return variant == MPV_ACC_X2 ? 8 : 4;
 }
+
+// B200 shared memory per block (opt-in) used by the layout planner (the
+// launch checks the device's own value)
+constexpr size_t kSmemPlan = 232448;
+constexpr int kFlipThreads = 512, kExchangeThreads = 256;
+size_t rank_block_bytes(int N, int GU, size_t entry) { return ((size_t)N * GU * entry + 15) & ~(size_t)15; }
+size_t vis16(int N, size_t vb) { return ((size_t)N * vb + 15) & ~(size_t)15; }
+// exchange buffers of a cluster-split sweep: per warp 2 mbarriers + [2][CS][32] partial sums
+size_t xchg_bytes(int cs, int warps, size_t sum_bytes) { return (size_t)warps * (16 + 2 * cs * 32 * sum_bytes); }
+size_t sum_bytes(int kfmt) { return kfmt == MPV_FMT_F64 ? 8 : 4; }
 
 // ---------------- helper kernels ----------------
 
@@ -326,15 +336,49 @@ int mpv_stream_uniforms(uint64_t key, int64_t n_chains, int64_t chain0, int64_t 
   return check_launch("stream_uniforms");
 }
 
-int mpv_snapshot_bytes(int n_visible, int hidden_pad, int fmt, int mode, int variant, size_t* out) {
-  if (n_visible < 1 || hidden_pad < 1 || fmt < MPV_FMT_F64 || fmt > MPV_FMT_BF16 || !out)
+int mpv_snapshot_bytes(int n_visible, int hidden_pad, int fmt, int mode, int variant, int cluster, size_t* out) {
+  if (n_visible < 1 || hidden_pad < 1 || fmt < MPV_FMT_F64 || fmt > MPV_FMT_BF16 || !out ||
+      (cluster != 1 && cluster != 2 && cluster != 4) || hidden_pad % cluster)
     return fail(MPV_ERR_ARGS, "snapshot_bytes: bad args");
   const bool f64arith = (fmt == MPV_FMT_F64) || (mode == MPV_MODE_STORAGE_ONLY);
   const int kfmt = f64arith ? MPV_FMT_F64 : fmt, var = f64arith ? MPV_ACC_F64 : variant;
-  const size_t t16 = ((size_t)n_visible * hidden_pad * entry_bytes(kfmt, var) + 15) & ~(size_t)15;
-  out[0] = t16 + (((size_t)n_visible * vis_bytes(kfmt, var) + 15) & ~(size_t)15);  // [table | vis]
-  out[1] = t16;                                                                     // vis offset
-  out[2] = ((size_t)hidden_pad * entry_bytes(kfmt, var) + 15) & ~(size_t)15;        // bias
+  const size_t t16 = cluster * rank_block_bytes(n_visible, hidden_pad / cluster, entry_bytes(kfmt, var));
+  out[0] = t16 + vis16(n_visible, vis_bytes(kfmt, var));                     // [rank blocks | vis]
+  out[1] = t16;                                                             // vis offset
+  out[2] = ((size_t)hidden_pad * entry_bytes(kfmt, var) + 15) & ~(size_t)15;  // bias
+  return MPV_OK;
+}
+
+int mpv_plan_cluster(int n_visible, int n_hidden, int fmt, int mode, int variant, int32_t* cluster,
+                     int32_t* lanes_per_chain, int32_t* units_per_lane) {
+  if (!cluster || !lanes_per_chain || !units_per_lane) return fail(MPV_ERR_ARGS, "plan_cluster: null output");
+  const bool f64arith = (fmt == MPV_FMT_F64) || (mode == MPV_MODE_STORAGE_ONLY);
+  const int kfmt = f64arith ? MPV_FMT_F64 : fmt, var = f64arith ? MPV_ACC_F64 : variant;
+  const size_t eb = entry_bytes(kfmt, var), vb = vis_bytes(kfmt, var);
+  int32_t G = 0, U = 0;
+  // The cluster split is opt-in (MPV_CLUSTER_SPLIT=1): measured on B200 it is
+  // slower than reading the table through L1/L2 (the per-step partial-sum
+  // exchange between the ranks is latency-bound).
+  const char* env = getenv("MPV_CLUSTER_SPLIT");
+  const int max_cs = (env && env[0] == '1') ? 4 : 1;
+  for (int cs : {1, 2, 4}) {
+    if (cs > max_cs) break;
+    if (mpv_plan_layout(n_visible, (n_hidden + cs - 1) / cs, kfmt, var, &G, &U)) return MPV_ERR_ARGS;
+    const size_t need = rank_block_bytes(n_visible, G * U, eb) + vis16(n_visible, vb) +
+                        (cs > 1 ? xchg_bytes(cs, kFlipThreads / 32, sum_bytes(kfmt)) : 0) + 1024;
+    const bool instantiated = cs == 1 || ((G == 4 || G == 8 || G == 16 || G == 32) && U >= 8);
+    if (need <= kSmemPlan && instantiated && (cs == 1 || n_hidden > 1)) {
+      *cluster = cs;
+      *lanes_per_chain = G;
+      *units_per_lane = U;
+      return MPV_OK;
+    }
+  }
+  // nothing fits on chip: one CTA per chain group, table read through L1/L2
+  if (mpv_plan_layout(n_visible, n_hidden, kfmt, var, &G, &U)) return MPV_ERR_ARGS;
+  *cluster = 1;
+  *lanes_per_chain = G;
+  *units_per_lane = U;
   return MPV_OK;
 }
 
@@ -359,7 +403,9 @@ int mpv_snapshot_fill(const mpv_snapshot* snap, const double* rounded, double sp
     return fail(MPV_ERR_ARGS, "snapshot_fill: X2 split");
   const int64_t n = (int64_t)(snap->n_visible + 1) * snap->hidden_pad + snap->n_visible;
   const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  snapshot_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(*snap, rounded, split);
+  const bool f64a = snap->fmt == MPV_FMT_F64 || snap->mode == MPV_MODE_STORAGE_ONLY;
+  const size_t eb = entry_bytes(f64a ? MPV_FMT_F64 : snap->fmt, f64a ? MPV_ACC_F64 : snap->variant);
+  snapshot_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(*snap, rounded, split, eb);
   return check_launch("snapshot_fill");
 }
 
@@ -427,6 +473,9 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
     if (snap->noise_sigma != 0.0) return fail(MPV_ERR_ARGS, "mh_sweep: log-density noise needs f64 arithmetic");
     PerOpSweepArgs a{};
     a.f.N = snap->n_visible; a.f.M = snap->n_hidden; a.f.Mpad = snap->hidden_pad; a.f.words = ch->words;
+    a.f.GU = snap->hidden_pad;  // per-op snapshots are never split
+    a.f.RB = (int64_t)(rank_block_bytes(snap->n_visible, snap->hidden_pad, entry_bytes(fmt, MPV_ACC_X1)) /
+                       entry_bytes(fmt, MPV_ACC_X1));
     a.f.table = snap->table; a.f.bias = snap->bias; a.f.vis = snap->vis; a.f.vis_im = snap->vis_im;
     a.n_chains = ch->n_chains; a.chain_offset = ch->chain_offset; a.bits = ch->bits;
     a.log_probs = ch->log_probs; a.accepted = ch->accepted; a.status = ch->status; a.key = key;
@@ -453,19 +502,31 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
     return fail(MPV_ERR_ARGS, "mh_sweep: log-density noise needs f64 arithmetic and n_visible <= 64");
   const int kfmt = f64arith ? MPV_FMT_F64 : fmt;
   const int variant = f64arith ? MPV_ACC_F64 : snap->variant;
-  const int G = snap->lanes_per_chain, U = snap->units_per_lane;
-  if (G < 1 || G > 32 || (G & (G - 1)) || G * U != snap->hidden_pad || snap->hidden_pad < snap->n_hidden)
+  const int G = snap->lanes_per_chain, U = snap->units_per_lane, CS = snap->cluster;
+  if (G < 1 || G > 32 || (G & (G - 1)) || (CS != 1 && CS != 2 && CS != 4) || CS * G * U != snap->hidden_pad ||
+      snap->hidden_pad < snap->n_hidden)
     return fail(MPV_ERR_ARGS, "mh_sweep: snapshot layout inconsistent");
   if (G < ch->words) return fail(MPV_ERR_ARGS, "mh_sweep: lanes_per_chain < words");
-  // [table | vis], each padded to 16 bytes (the host snapshot layout)
-  const size_t tbytes = (((size_t)snap->n_visible * snap->hidden_pad * entry_bytes(kfmt, variant) + 15) & ~(size_t)15) +
-                        (size_t)snap->n_visible * vis_bytes(kfmt, variant);
-  const size_t tbytes16 = (tbytes + 15) & ~(size_t)15;
-  if ((const char*)snap->vis != (const char*)snap->table + (tbytes - (size_t)snap->n_visible * vis_bytes(kfmt, variant)))
-    return fail(MPV_ERR_ARGS, "mh_sweep: vis must follow the table at the next 16-byte boundary");
-  const bool use_smem = tbytes16 + 1024 <= (size_t)max_smem_optin();  // static smem: mbarrier
-  const int sm = use_smem ? 1 : 0;
-  void* fn = sweep_kernel_ptr(kfmt, variant, G, U, proposal, sm);
+  // [rank blocks | vis], each padded to 16 bytes (the host snapshot layout)
+  const size_t eb = entry_bytes(kfmt, variant), vb = vis_bytes(kfmt, variant);
+  const size_t rb = rank_block_bytes(snap->n_visible, G * U, eb);
+  if ((const char*)snap->vis != (const char*)snap->table + CS * rb)
+    return fail(MPV_ERR_ARGS, "mh_sweep: vis must follow the rank blocks at the next 16-byte boundary");
+  // flip kernels: 512-thread blocks (one staged table per 16 warps, <= 128 regs);
+  // exchange kernels need more registers: 256-thread blocks
+  const int threads = (proposal == MPV_PROPOSAL_FLIP) ? kFlipThreads : kExchangeThreads;
+  const size_t xoff = rb + vis16(snap->n_visible, vb);
+  size_t smem = 0;
+  int sm = 0;
+  if (CS > 1) {
+    smem = xoff + xchg_bytes(CS, threads / 32, sum_bytes(kfmt));
+    if (smem + 1024 > (size_t)max_smem_optin()) return fail(MPV_ERR_ARGS, "mh_sweep: rank block exceeds shared memory");
+    sm = 1;
+  } else if (xoff + 1024 <= (size_t)max_smem_optin()) {  // static smem: mbarrier
+    smem = xoff;
+    sm = 1;
+  }
+  void* fn = sweep_kernel_ptr(kfmt, variant, G, U, proposal, sm, CS);
   if (!fn) return fail(MPV_ERR_ARGS, "mh_sweep: no kernel for this (format, variant, layout)");
   const int64_t cpw = 32 / G;
   const int64_t n_groups = (ch->n_chains + cpw - 1) / cpw;
@@ -477,15 +538,17 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
   const size_t need = mpv_sweep_scratch_bytes(snap, ch->n_chains);
   if (!ch->scratch || ch->scratch_bytes < need) return fail(MPV_ERR_ARGS, "mh_sweep: scratch too small (mpv_sweep_scratch_bytes)");
   char* sp = (char*)ch->scratch;
+  const size_t done_bytes = ((CS * n_groups * 4 + 255) / 256) * 256;
   int* queue = (int*)sp;
   int* done = (int*)(sp + 256);
-  float* save = (float*)(sp + 256 + ((n_groups * 4 + 255) / 256) * 256);
-  void* vsave = (char*)save + ((size_t)n_groups * U * acc_bytes(kfmt, variant) * 32 + 255) / 256 * 256;
-  if (cudaMemsetAsync(sp, 0, 256 + n_groups * 4, st) != cudaSuccess) return check_launch("mh_sweep memset");
+  float* save = (float*)(sp + 256 + done_bytes);
+  void* vsave = (char*)save + ((size_t)CS * n_groups * U * acc_bytes(kfmt, variant) * 32 + 255) / 256 * 256;
+  if (cudaMemsetAsync(sp, 0, 256 + CS * n_groups * 4, st) != cudaSuccess) return check_launch("mh_sweep memset");
   SweepArgs a{};
   a.N = snap->n_visible; a.M = snap->n_hidden; a.Mpad = snap->hidden_pad; a.G = G; a.words = ch->words;
-  a.table = snap->table; a.bias = snap->bias; a.vis = snap->vis; a.table_bytes = tbytes16;
+  a.table = snap->table; a.bias = snap->bias; a.vis = snap->vis; a.table_bytes = xoff;
   a.table_in_smem = sm;
+  a.rank_block_bytes = rb; a.vis_bytes = (size_t)snap->n_visible * vb; a.xchg_off = xoff;
   a.n_chains = ch->n_chains; a.chain_offset = ch->chain_offset; a.bits = ch->bits;
   a.log_probs = ch->log_probs; a.accepted = ch->accepted; a.status = ch->status; a.key = key;
   a.init_draws = init_draws; a.step_index = step_index; a.n_steps = n_steps; a.thin = thin;
@@ -497,22 +560,42 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
   a.noise_key = snap->noise_key;
   a.noise_sigma = snap->noise_sigma;
   if (variant == MPV_ACC_XI && !(snap->quantum > 0.0)) return fail(MPV_ERR_ARGS, "mh_sweep: XI needs quantum > 0");
-  // flip kernels: 512-thread blocks (one staged table per 16 warps, <= 128 regs);
-  // exchange kernels need more registers: 256-thread blocks
-  const int threads = (proposal == MPV_PROPOSAL_FLIP) ? 512 : 256;
-  const size_t smem = use_smem ? tbytes16 : 0;
   if (int rc = ensure_smem(fn, smem)) return rc;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1)
-    return fail(MPV_ERR_CUDA, "mh_sweep: kernel does not fit on an SM");
   int dev = 0, n_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t warps_needed = a.n_items;
-  const int64_t blocks = std::min<int64_t>((int64_t)n_sm * per_sm, (warps_needed + threads / 32 - 1) / (threads / 32));
   void* args[] = {&a};
-  const cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, st);
-  if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("mh_sweep: ") + cudaGetErrorString(e));
+  if (CS == 1) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1)
+      return fail(MPV_ERR_CUDA, "mh_sweep: kernel does not fit on an SM");
+    const int64_t warps_needed = a.n_items;
+    const int64_t blocks = std::min<int64_t>((int64_t)n_sm * per_sm, (warps_needed + threads / 32 - 1) / (threads / 32));
+    const cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, smem, st);
+    if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("mh_sweep: ") + cudaGetErrorString(e));
+    return MPV_OK;
+  }
+  // cluster split: as many co-resident clusters as the device holds (persistent)
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)(n_sm / CS * CS));
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) != cudaSuccess || clusters < 1)
+    return fail(MPV_ERR_CUDA, "mh_sweep: cluster does not fit on the device");
+  const int64_t warps_needed = a.n_items;
+  const int64_t want = (warps_needed + threads / 32 - 1) / (threads / 32);
+  cfg.gridDim = dim3((unsigned)(std::min<int64_t>(clusters, want) * CS));
+  const cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+  if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("mh_sweep (cluster): ") + cudaGetErrorString(e));
   return MPV_OK;
 }
 
@@ -522,9 +605,10 @@ size_t mpv_sweep_scratch_bytes(const mpv_snapshot* snap, int64_t n_chains) {
   const int kfmt = f64arith ? MPV_FMT_F64 : snap->fmt;
   const int variant = f64arith ? MPV_ACC_F64 : snap->variant;
   const int G = std::max(1, (int)snap->lanes_per_chain), U = std::max(1, (int)snap->units_per_lane);
+  const int CS = std::max(1, (int)snap->cluster);
   const int64_t n_groups = (n_chains + 32 / G - 1) / (32 / G);
-  return 256 + ((n_groups * 4 + 255) / 256) * 256 +
-         ((size_t)n_groups * U * acc_bytes(kfmt, variant) * 32 + 255) / 256 * 256 +
+  return 256 + ((CS * n_groups * 4 + 255) / 256) * 256 +
+         ((size_t)CS * n_groups * U * acc_bytes(kfmt, variant) * 32 + 255) / 256 * 256 +
          (size_t)(n_chains + 1) * 16 + 256;
 }
 
@@ -548,6 +632,13 @@ int mpv_snapshot_forward(const mpv_snapshot* snap, const uint32_t* bits, int64_t
   }
   FwdArgs a{};
   a.N = snap->n_visible; a.M = snap->n_hidden; a.Mpad = snap->hidden_pad; a.words = words;
+  {
+    const int cs = std::max(1, (int)snap->cluster);
+    const bool f64a = fmt == MPV_FMT_F64 || mode == MPV_MODE_STORAGE_ONLY;
+    const size_t eb = entry_bytes(f64a ? MPV_FMT_F64 : fmt, f64a ? MPV_ACC_F64 : snap->variant);
+    a.GU = snap->hidden_pad / cs;
+    a.RB = (int64_t)(rank_block_bytes(snap->n_visible, a.GU, eb) / eb);
+  }
   a.table = snap->table; a.bias = snap->bias; a.vis = snap->vis; a.vis_im = snap->vis_im;
   a.bits = bits; a.B = B; a.out_lp = out_lp; a.out_re = out_re; a.out_im = out_im; a.status = status;
   const bool want_im = out_re || out_im;
@@ -611,7 +702,7 @@ int mpv_rounded_log_prob(const uint8_t* bits, int64_t B, int N, int M, const dou
   mpv_snapshot snap{};
   snap.n_visible = N; snap.n_hidden = M; snap.hidden_pad = M;
   snap.fmt = fmt; snap.mode = MPV_MODE_PER_OPERATION; snap.variant = MPV_ACC_X1;
-  snap.lanes_per_chain = 1; snap.units_per_lane = M;
+  snap.lanes_per_chain = 1; snap.units_per_lane = M; snap.cluster = 1;
   snap.table = table; snap.bias = bias; snap.vis = vis; snap.vis_im = nullptr;
   return mpv_snapshot_forward(&snap, packed, B, out_lp, nullptr, nullptr, nullptr, nullptr, 0, stream);
 }

@@ -47,7 +47,9 @@ template <> struct PerOp<MPV_FMT_F32> {
 
 struct FwdArgs {
   int N, M, Mpad, words;
-  const void* table;  // [N][Mpad] entries
+  int GU;             // units per rank block (Mpad for an unsplit snapshot)
+  int64_t RB;         // elements per rank block (16-byte padded)
+  const void* table;  // rank blocks [Mpad / GU][N][GU] entries (include/mpvmc_b200.h)
   const void* bias;   // [Mpad] entries
   const void* vis;    // [N] float (per-op: a_re exact) or double (f64)
   const double* vis_im;
@@ -76,7 +78,7 @@ __device__ double warp_forward_perop(const FwdArgs& a, const uint32_t* wbuf, dou
       while (word) {
         const int k = w * 32 + __ffs(word) - 1;
         word &= word - 1;
-        const Entry e = tab[(size_t)k * a.Mpad + i];
+        const Entry e = tab[(size_t)(i / a.GU) * a.RB + (size_t)k * a.GU + i % a.GU];
         tr = P::add(tr, P::re(e));
         ti = P::add(ti, P::im(e));
       }
@@ -141,7 +143,7 @@ __device__ double warp_forward_f64(const FwdArgs& a, const uint32_t* wbuf, doubl
       while (word) {
         const int k = w * 32 + __ffs(word) - 1;
         word &= word - 1;
-        const double2 e = tab[(size_t)k * a.Mpad + i];
+        const double2 e = tab[(size_t)(i / a.GU) * a.RB + (size_t)k * a.GU + i % a.GU];
         th.x += e.x;
         th.y += e.y;
       }

@@ -100,18 +100,21 @@ __device__ __forceinline__ void put_entry(const mpv_snapshot& s, void* base, siz
   }
 }
 
-__global__ void snapshot_fill_kernel(const mpv_snapshot s, const double* __restrict__ r, double split) {
+__global__ void snapshot_fill_kernel(const mpv_snapshot s, const double* __restrict__ r, double split, size_t eb) {
   const int N = s.n_visible, M = s.n_hidden, P = s.hidden_pad;
   const double2* a = reinterpret_cast<const double2*>(r);
   const double2* b = a + N;
   const double2* w = b + M;  // [N][M]
+  // rank blocks (include/mpvmc_b200.h): unit i of block r = i / GU at element r RB + k GU + i % GU
+  const int CS = s.cluster > 1 ? s.cluster : 1, GU = P / CS;
+  const int64_t RB = (int64_t)((((size_t)N * GU * eb + 15) & ~(size_t)15) / eb);
   const int64_t n_tab = (int64_t)N * P, n = n_tab + P + N;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
        idx += (int64_t)gridDim.x * blockDim.x) {
     if (idx < n_tab) {
       const int k = (int)(idx / P), i = (int)(idx % P);
       const double2 z = i < M ? w[(size_t)k * M + i] : make_double2(0.0, 0.0);
-      put_entry(s, const_cast<void*>(s.table), (size_t)idx, z, split);
+      put_entry(s, const_cast<void*>(s.table), (size_t)((i / GU) * RB + (int64_t)k * GU + i % GU), z, split);
     } else if (idx < n_tab + P) {
       const int i = (int)(idx - n_tab);
       put_entry(s, const_cast<void*>(s.bias), (size_t)i, i < M ? b[i] : make_double2(0.0, 0.0), split);

@@ -44,6 +44,86 @@ struct SweepArgs {
   void* vis_save;     // [n_chains] visible term between segments
   uint64_t noise_key;  // frozen log-density noise (f64 arithmetic, N <= 64); sigma 0 = off
   double noise_sigma;
+  // cluster split (CS > 1): rank block bytes in global (16-aligned), vis bytes,
+  // and the shared-memory offset of the exchange buffers
+  size_t rank_block_bytes, vis_bytes, xchg_off;
+};
+
+// ------------------------------------------------------------------------
+// Cluster exchange of per-rank partial sums (CS ranks split the hidden units).
+// Per warp: two data slots [parity][rank][32 lanes] and two mbarriers (one per
+// slot parity, CS - 1 arrivals each).  Every rank writes its partial into every
+// other rank's slot (st.shared::cluster) and arrives on their barrier
+// (release.cluster); after its own barrier completes it sums the CS partials
+// in rank order, so all ranks hold the identical total.  A slot is rewritten
+// two exchanges later, after the writer has seen the reader's next arrival,
+// i.e. after the reader consumed it.
+// ------------------------------------------------------------------------
+template <int CS, typename T>
+struct ClusterXchg {
+  uint32_t data0;  // shared address of this warp's slots in this CTA: [2][CS][32] T
+  uint32_t bar0;   // shared address of this warp's two mbarriers
+  int rank;
+  uint32_t count;  // exchanges done by this warp
+  __device__ static uint32_t mapa(uint32_t addr, int r) {
+    uint32_t out;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(r));
+    return out;
+  }
+  __device__ T sum(T v, int lane) {
+    if constexpr (CS == 1) {
+      return v;
+    } else {
+      const uint32_t par = count & 1u;
+      const uint32_t slot = data0 + (uint32_t)((par * CS + rank) * 32 + lane) * (uint32_t)sizeof(T);
+#pragma unroll
+      for (int r = 0; r < CS; ++r) {
+        if (r == rank) continue;
+        const uint32_t dst = mapa(slot, r);
+        if constexpr (sizeof(T) == 8)
+          asm volatile("st.shared::cluster.b64 [%0], %1;" ::"r"(dst), "l"(__double_as_longlong((double)v)) : "memory");
+        else
+          asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(dst), "r"(__float_as_uint((float)v)) : "memory");
+      }
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < CS; ++r) {
+          if (r == rank) continue;
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa(bar0 + 8 * par, r))
+                       : "memory");
+        }
+      }
+      const uint32_t ph = (count >> 1) & 1u;
+      asm volatile(
+          "{.reg .pred p;\nXW_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n @!p bra XW_%=;\n}" ::"r"(
+              bar0 + 8 * par),
+          "r"(ph)
+          : "memory");
+      T total = T(0);
+#pragma unroll
+      for (int r = 0; r < CS; ++r) {
+        T x;
+        if (r == rank) {
+          x = v;
+        } else {
+          const uint32_t src = data0 + (uint32_t)((par * CS + r) * 32 + lane) * (uint32_t)sizeof(T);
+          if constexpr (sizeof(T) == 8) {
+            unsigned long long b;
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(b) : "r"(src) : "memory");
+            x = (T)__longlong_as_double((long long)b);
+          } else {
+            uint32_t b;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(b) : "r"(src) : "memory");
+            x = (T)__uint_as_float(b);
+          }
+        }
+        total += x;
+      }
+      ++count;
+      return total;
+    }
+  }
 };
 
 // code(x) of the configuration spread over a segment's lanes (word w in lane w)
@@ -390,9 +470,10 @@ __device__ __forceinline__ void report_nonfinite(int64_t* status, int64_t step, 
 // running or finished on a resident warp: no deadlock).
 // ------------------------------------------------------------------------
 
-template <int FMT, int VAR, int G, int U, int PROP, bool SMEM>
+template <int FMT, int VAR, int G, int U, int PROP, bool SMEM, int CS = 1>
 __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP == MPV_PROPOSAL_FLIP || SMEM) ? 1 : 2)
     sweep_kernel(const SweepArgs a) {
+  static_assert(CS == 1 || SMEM, "cluster-split sweeps keep their rank block in shared memory");
   using A = Acc<FMT, VAR>;
   using E = Eval<FMT, VAR>;
   using Entry = typename A::Entry;
@@ -407,7 +488,47 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Entry* tab;
   const VisT* visv;
-  if constexpr (SMEM) {
+  int rank = 0;
+  if constexpr (CS > 1) {
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    // this rank's block of hidden units, then the visible biases; the exchange
+    // barriers are initialised before any rank can arrive on them (cluster barrier)
+    __shared__ __align__(8) uint64_t bar;
+    const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(&bar);
+    const uint32_t rb = (uint32_t)a.rank_block_bytes, vb = (uint32_t)((a.vis_bytes + 15) & ~(size_t)15);
+    uint64_t* xbars = reinterpret_cast<uint64_t*>(smem_raw + a.xchg_off);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        for (int k = 0; k < 2; ++k)
+          asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(
+                           xbars + 2 * w + k)),
+                       "r"(CS - 1));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(rb + vb) : "memory");
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem_raw);
+      const char* src = (const char*)a.table + (size_t)rank * rb;
+      for (uint32_t off = 0; off < rb; off += 65536u)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + off),
+            "l"(src + off), "r"(min(rb - off, 65536u)), "r"(sbar)
+            : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + rb),
+          "l"((const char*)a.vis), "r"(vb), "r"(sbar)
+          : "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile(
+        "{.reg .pred p;\nWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
+            sbar)
+        : "memory");
+    tab = reinterpret_cast<const Entry*>(smem_raw);
+    visv = reinterpret_cast<const VisT*>(smem_raw + rb);
+  } else if constexpr (SMEM) {
     // Stage the snapshot (column table, then visible biases) into shared memory
     // with bulk async copies (TMA engine, cp.async.bulk) on one mbarrier.
     __shared__ __align__(8) uint64_t bar;
@@ -451,13 +572,38 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
   const int N = a.N;
   const int words = a.words;
   const double n_pairs = 0.5 * (double)N * (double)(N - 1);
-  const Entry* bias = reinterpret_cast<const Entry*>(a.bias);
+  const Entry* bias = reinterpret_cast<const Entry*>(a.bias) + rank * Mpad;  // this rank's units
   VisT* vsave = reinterpret_cast<VisT*>(a.vis_save);
+  const int warp = threadIdx.x >> 5;
+  ClusterXchg<CS, Sum> xchg;
+  if constexpr (CS > 1) {
+    xchg.rank = rank;
+    xchg.count = 0;
+    xchg.bar0 = (uint32_t)__cvta_generic_to_shared(smem_raw + a.xchg_off) + 16u * warp;
+    xchg.data0 = (uint32_t)__cvta_generic_to_shared(smem_raw + a.xchg_off) + 16u * (blockDim.x >> 5) +
+                 (uint32_t)(warp * 2 * CS * 32 * sizeof(Sum));
+  }
+  // parked theta of this rank; per-rank segment counters
+  float* const save_r = a.save + (size_t)rank * a.n_groups * (U * SW) * 32;
+  int* const done_r = a.done + (size_t)rank * a.n_groups;
+  const bool writer = rank == 0;  // rank 0 owns the chain state (bits, log p, counters, samples)
+  // CS > 1: static item order (the ranks of a cluster walk the same items in
+  // lockstep); a group's earlier segment always has a smaller item index, so
+  // the persistent grid cannot deadlock
+  const int64_t gwarp = (int64_t)(blockIdx.x / CS) * (blockDim.x >> 5) + warp;
+  const int64_t gstride = (int64_t)(gridDim.x / CS) * (blockDim.x >> 5);
+  int64_t next_item = gwarp;
 
   for (;;) {
-    int item = 0;
-    if (lane == 0) item = atomicAdd(a.queue, 1);
-    item = __shfl_sync(kFull, item, 0);
+    int64_t item = 0;
+    if constexpr (CS == 1) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(a.queue, 1);
+      item = __shfl_sync(kFull, it, 0);
+    } else {
+      item = next_item;
+      next_item += gstride;
+    }
     if (item >= a.n_items) break;
     const int64_t seg = item / a.n_groups;
     const int64_t grp = item % a.n_groups;
@@ -467,11 +613,15 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
     const int64_t gchain = a.chain_offset + cidx;
     if (seg > 0) {
       if (lane == 0) {
-        int d;
-        for (;;) {
-          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(d) : "l"(a.done + grp) : "memory");
-          if (d >= seg) break;
-          __nanosleep(100);
+        // this rank's parked theta, and (CS > 1) the chain state written by rank 0
+        for (int r = 0; r < (CS > 1 && rank != 0 ? 2 : 1); ++r) {
+          const int* flag = (r == 0 ? done_r : a.done) + grp;
+          int d;
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(d) : "l"(flag) : "memory");
+            if (d >= seg) break;
+            __nanosleep(100);
+          }
         }
       }
       __syncwarp();
@@ -516,7 +666,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
         if (vmin0 < NearZero<FMT>::kV) {  // rare: a unit is near a cosh zero
           // the accumulators go through this lane's parking slot so the
           // correction loop is a compact rolled loop (no register pressure)
-          float* sv = a.save + (size_t)grp * (U * SW) * 32 + lane;
+          float* sv = save_r + (size_t)grp * (U * SW) * 32 + lane;
 #pragma unroll
           for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -532,15 +682,15 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
           }
         }
       }
-      h0 = segment_sum(h0, G);
+      h0 = xchg.sum(segment_sum(h0, G), lane);
       lp = E::finalize(vis, h0, sc);
       if (a.noise_sigma != 0.0) lp = (Lp)((double)lp + noise_zeta(a.noise_key, segment_code(myword, words, G), a.noise_sigma));
       if (!isfinite(lp)) {
-        if (live && gl == 0) report_nonfinite(a.status, 0, cidx);
+        if (live && gl == 0 && writer) report_nonfinite(a.status, 0, cidx);
         lp = Lp(NAN);  // NaN marks a frozen chain
       }
     } else {
-      const float* sv = a.save + (size_t)grp * (U * SW) * 32 + lane;
+      const float* sv = save_r + (size_t)grp * (U * SW) * 32 + lane;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         float* dst = reinterpret_cast<float*>(&acc[u]);
@@ -632,7 +782,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
       }
       if constexpr (E::kFix) {
         if (vmin < NearZero<FMT>::kV) {  // rare: a unit of this lane is near a cosh zero
-          float* sv = a.save + (size_t)grp * (U * SW) * 32 + lane;
+          float* sv = save_r + (size_t)grp * (U * SW) * 32 + lane;
 #pragma unroll
           for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -649,7 +799,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
           }
         }
       }
-      h = segment_sum(h, G);
+      h = xchg.sum(segment_sum(h, G), lane);
       VisT vnew = vis_add(vis, visv[k1], dsign);
       if (PROP == MPV_PROPOSAL_EXCHANGE) vnew = vis_add(vnew, visv[k2], -dsign);
       Lp lp_new = E::finalize(vnew, h, sc);
@@ -660,7 +810,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
       // chain freezes and the first failure is reported.
       if (!isfinite(lp_new) && dsign != 0 && !dead) {
         dead = true;
-        if (live && gl == 0) report_nonfinite(a.status, a.step_index + s + 1, cidx);
+        if (live && gl == 0 && writer) report_nonfinite(a.status, a.step_index + s + 1, cidx);
       }
       const bool accept = !dead && (dsign == 0 || logu < lp_new - lp);
       const bool moved = accept && dsign != 0;
@@ -681,12 +831,12 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
       if (s + 1 == next_record) {
         next_record += thin;
         const int64_t r = a.round_offset + (s + 1) / thin - 1;
-        if (live && r < count_c && gl < words) a.samples[(offset_c + r) * words + gl] = myword;
+        if (live && writer && r < count_c && gl < words) a.samples[(offset_c + r) * words + gl] = myword;
       }
     }
     if (dead) lp = Lp(NAN);
 
-    if (live) {
+    if (live && writer) {
       if (gl < words) a.bits[cidx * words + gl] = myword;
       if (gl == 0) {
         a.log_probs[cidx] = (double)lp;
@@ -694,18 +844,21 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
       }
     }
     if (s_end < a.n_steps) {  // more segments follow: park theta and vis
-      float* sv = a.save + (size_t)grp * (U * SW) * 32 + lane;
+      float* sv = save_r + (size_t)grp * (U * SW) * 32 + lane;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const float* src = reinterpret_cast<const float*>(&acc[u]);
 #pragma unroll
         for (int j = 0; j < SW; ++j) sv[(u * SW + j) * 32] = src[j];
       }
-      if (live && gl == 0) vsave[cidx] = vis;
+      if (live && gl == 0 && writer) vsave[cidx] = vis;
     }
     __threadfence();
     __syncwarp();
-    if (lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.done + grp), "r"((int)(seg + 1)) : "memory");
+    if (lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(done_r + grp), "r"((int)(seg + 1)) : "memory");
+  }
+  if constexpr (CS > 1) {  // no rank leaves while another may still address its shared memory
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
 }
 

@@ -212,6 +212,7 @@ class DeviceSnapshot:
                  stream)
         split = 0.0
         quantum = 0.0
+        cluster = 1
         if mode is RoundingMode.PER_OPERATION and not f64arith:
             G, U, Mpad = 1, M, M
             variant = nat.ACC_X1
@@ -235,16 +236,17 @@ class DeviceSnapshot:
                 split = self.plan.split
                 if variant == nat.ACC_XI:
                     quantum = self.plan.quantum
-            G, U = nat.plan_layout(N, M, nat.FMT_F64 if f64arith else fmt.code, variant)
-            Mpad = G * U
+            cluster, G, U = nat.plan_cluster(N, M, fmt.code, mode.code, variant)
+            Mpad = cluster * G * U
         self.variant, self.lanes_per_chain, self.units_per_lane, self.hidden_pad = variant, G, U, Mpad
+        self.cluster = cluster
         sizes = (ctypes.c_size_t * 3)()
-        nat.call("mpv_snapshot_bytes", N, Mpad, fmt.code, mode.code, variant, sizes)
+        nat.call("mpv_snapshot_bytes", N, Mpad, fmt.code, mode.code, variant, cluster, sizes)
         self._table = torch.zeros(int(sizes[0]), dtype=torch.uint8, device=self.device)  # zero padding
         self._bias = torch.zeros(int(sizes[2]), dtype=torch.uint8, device=self.device)
         self._vis_im = torch.empty(N, dtype=torch.float64, device=self.device)
         base = self._table.data_ptr()
-        self.struct = nat.Snapshot(N, M, Mpad, fmt.code, mode.code, variant, G, U,
+        self.struct = nat.Snapshot(N, M, Mpad, fmt.code, mode.code, variant, G, U, cluster,
                                    base, self._bias.data_ptr(), base + int(sizes[1]), self._vis_im.data_ptr(), quantum)
         nat.call("mpv_snapshot_fill", ctypes_byref(self.struct), self._rounded.data_ptr(), split, stream)
 
@@ -265,7 +267,9 @@ class DeviceSnapshot:
     @property
     def label(self) -> str:
         names = {nat.ACC_X1: "X1", nat.ACC_X2: "X2", nat.ACC_F64: "F64", nat.ACC_XI: "XI"}
-        return f"{self.fmt.name}/{self.mode.value}/{names[self.variant]}/G{self.lanes_per_chain}xU{self.units_per_lane}"
+        cl = f"C{self.cluster}x" if self.cluster > 1 else ""
+        return (f"{self.fmt.name}/{self.mode.value}/{names[self.variant]}/"
+                f"{cl}G{self.lanes_per_chain}xU{self.units_per_lane}")
 
 
 # ---------------------------------------------------------------------------

@@ -143,7 +143,7 @@ def test_native_variants_identical(cuda, fmt):
             ev = rbm.log_prob_evaluator(p, FORMATS[fmt], NATIVE, variant=var)
         except ValueError:
             continue
-        key = (ev.snapshot.lanes_per_chain, ev.snapshot.units_per_lane)
+        key = (ev.snapshot.cluster, ev.snapshot.lanes_per_chain, ev.snapshot.units_per_lane)
         by_layout.setdefault(key, []).append(ev(bits))
     assert sum(len(v) for v in by_layout.values()) >= 2
     firsts = []
@@ -400,3 +400,39 @@ def test_edge_shapes_native_model(cuda, n, alpha, fmt):
         np.testing.assert_array_equal(ens.log_probs, ev(ens.bits))  # cached log p == fresh evaluation
         if kind == "exchange":
             assert np.all(ens.bits.sum(axis=1) == n // 2)
+
+
+@pytest.mark.parametrize("n,alpha,fmt,kind,scale", [(100, 4, "bf16", "exchange", 0.01), (256, 1, "f16", "flip", 0.01),
+                                                     (100, 2, "f32", "flip", 0.3)])
+def test_cluster_split_sweep(cuda, monkeypatch, n, alpha, fmt, kind, scale):
+    """Opt-in cluster split (MPV_CLUSTER_SPLIT=1: the hidden units of a table
+    beyond shared memory split over 2 or 4 CTAs of a thread-block cluster that
+    exchange partial sums every step): log p equals the arithmetic model (and,
+    for f32, the f64 value to 1e-5), chains stay consistent with fresh
+    evaluations, shards reproduce the single ensemble."""
+    from oracle import model
+
+    monkeypatch.setenv("MPV_CLUSTER_SPLIT", "1")
+    p = rbm.random_parameters(n, alpha, derive_key(n, "cluster"), scale)
+    ev = rbm.log_prob_evaluator(p, FORMATS[fmt], NATIVE)
+    assert ev.snapshot.cluster > 1, ev.snapshot.label
+    rng = np.random.default_rng(1)
+    bits = rng.integers(0, 2, size=(500, n), dtype=np.uint8)
+    got = ev(bits)
+    if fmt == "f32":
+        ref = rbm.log_prob_batch(p, bits, F64)
+        assert np.max(np.abs(got - ref) / np.maximum(1, np.abs(ref))) < 1e-5
+    else:
+        r = rbm.round_parameters(p, FORMATS[fmt])
+        want, tol = model.native_log_prob(r.a, r.b, r.w, bits, fmt)
+        assert np.all(np.abs(got - want) <= tol)
+    prop = sampler.Proposal(kind, n // 2 if kind == "exchange" else None)
+    key = derive_key(2, "chains")
+    a = sampler.ChainEnsemble(300, n, prop, ev, key)
+    a.run_steps(700)
+    np.testing.assert_array_equal(a.log_probs, ev(a.bits))
+    s0 = sampler.ChainEnsemble(100, n, prop, ev, key, chain_offset=0, n_chains_total=300)
+    s1 = sampler.ChainEnsemble(200, n, prop, ev, key, chain_offset=100, n_chains_total=300)
+    for s in (s0, s1):
+        s.run_steps(700)
+    np.testing.assert_array_equal(np.concatenate([s0.bits, s1.bits]), a.bits)

@@ -59,6 +59,33 @@ def full(path):
             if k in d:
                 print(f"| {k} | {d[k]} | {u.get(k, '')} |")
         print()
+        stalls = []
+        for k, v in d.items():
+            if "issue_stalled" in k and k.endswith("per_issue_active.ratio"):
+                try:
+                    stalls.append((float(v), k.replace("smsp__average_warps_issue_stalled_", "").replace(
+                        "_per_issue_active.ratio", "")))
+                except ValueError:
+                    pass
+        if stalls:
+            print("warp stall reasons (cycles per issued instruction): " +
+                  ", ".join(f"{n} {v:.2f}" for v, n in sorted(stalls, reverse=True)[:8]) + "\n")
+    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+    srows = list(csv.reader(io.StringIO(src)))
+    if len(srows) > 2 and "Source" in srows[1]:
+        h = srows[1]
+        iS, iW = h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
+        data = []
+        for r in srows[2:]:
+            try:
+                data.append((int(r[iW]), r[iS].strip()))
+            except (ValueError, IndexError):
+                pass
+        tot = sum(w for w, _ in data) or 1
+        print("hottest SASS (share of warp stall samples):\n```")
+        for w, line in sorted(data, reverse=True)[:12]:
+            print(f"{100 * w / tot:5.1f}%  {line[:100]}")
+        print("```")
     det = subprocess.run(["ncu", "-i", path, "--page", "details"], capture_output=True, text=True).stdout
     print("```")
     for line in det.splitlines():

@@ -1,6 +1,7 @@
 #!/bin/bash
 # Round profile captures on the GPU box (one GPU): microbenchmarks, the bench's
-# launch list, and ncu --set full of the top kernels.  Output: gpurun_out/$1/
+# launch list, and ncu --set full of the top kernels, each summarised on the box
+# (tools/ncu_summary.py) so only small files come back.  Output: gpurun_out/$1/
 R=${1:-r02}
 O=gpurun_out/$R
 mkdir -p $O
@@ -9,16 +10,19 @@ SHORT="--no-cpu-baseline --no-extras --no-vmc"
 python bench.py --steps 2 --warmup 3 $SHORT > $O/bench_short.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
     python bench.py --steps 2 --warmup 3 $SHORT > /dev/null 2>&1
-ncu --set full --import-source on --clock-control none -k regex:sweep_kernel -s 3 -c 1 -o $O/sweep \
-    python bench.py --steps 1 --warmup 3 $SHORT > $O/ncu_sweep.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:energy_kernel -c 1 -o $O/energy \
-    python tools/bench_energy.py > $O/ncu_energy.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:rescnn_kernel -c 1 -o $O/rescnn \
-    python tools/bench_rescnn.py > $O/ncu_rescnn.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"ld_ov_kernel|ld_ohu_kernel" -s 1 -c 2 -o $O/ld \
-    python tools/bench_sr_cg.py > $O/ncu_ld.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:sweep_kernel -s 1 -c 1 -o $O/sweep_f32 \
-    python tools/bench_sweep_one.py f32 > $O/ncu_sweep_f32.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:sweep_kernel -s 1 -c 1 -o $O/sweep_c3 \
-    python tools/bench_sweep_one.py bf16 100 4 0.01 exchange > $O/ncu_sweep_c3.log 2>&1
+python tools/ncu_summary.py launches $O/launches.csv > $O/launches.md 2>&1
+cap() {  # name, kernel regex, skip, count, command...
+  local name=$1 rx=$2 skip=$3 cnt=$4; shift 4
+  ncu --set full --import-source on --clock-control none -k regex:"$rx" -s $skip -c $cnt -o $O/$name "$@" \
+      > $O/ncu_$name.log 2>&1
+  python tools/ncu_summary.py full $O/$name.ncu-rep > $O/$name.md 2>&1
+  rm -f $O/$name.ncu-rep
+}
+cap sweep sweep_kernel 3 1 python bench.py --steps 1 --warmup 3 $SHORT
+cap energy energy_kernel 0 1 python tools/bench_energy.py
+cap rescnn rescnn_kernel 0 1 python tools/bench_rescnn.py
+cap ld "ld_ov_kernel|ld_ohu_kernel" 1 2 python tools/bench_sr_cg.py
+cap sweep_f32 sweep_kernel 1 1 python tools/bench_sweep_one.py f32
+cap sweep_c3 sweep_kernel 1 1 python tools/bench_sweep_one.py bf16 100 4 0.01 exchange
+cap sweep_c5 sweep_kernel 1 1 python tools/bench_sweep_one.py f16 256 1 0.01 flip
 echo done
