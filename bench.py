@@ -555,11 +555,11 @@ def run_ours(args, rank, world, local_rank):
                            "algorithmic": "2.5 MUFU ops per hidden unit per configuration (ex2, cos each; one lg2 per pair of units); "
                                           "GEMM 2 x N x 2M flops per configuration"}
     out["energy_check"]["acceptance"] = float(np.mean(accs)) / (C * world * (REBURN_SWEEPS * N_SITES + SAMPLES_PER_CHAIN * (N_SITES + 1)))
-    tr = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+    tr = os.path.join(ROOT, "profiles", "r02", "traffic.json")
     if os.path.exists(tr):
         with open(tr) as f:
             out["roofline"]["traffic"] = json.load(f)["sweep_kernel"]["dram_bytes_per_launch"]
-            out["roofline"]["traffic_unit"] = "bytes/launch (ncu --set full, profiles/r01)"
+            out["roofline"]["traffic_unit"] = "bytes/launch (ncu --set full, profiles/r02)"
             out["roofline_energy"]["traffic"] = json.load(open(tr))["energy_kernel"]["dram_bytes_per_launch"]
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline()

@@ -366,7 +366,7 @@ int mpv_plan_cluster(int n_visible, int n_hidden, int fmt, int mode, int variant
     if (mpv_plan_layout(n_visible, (n_hidden + cs - 1) / cs, kfmt, var, &G, &U)) return MPV_ERR_ARGS;
     const size_t need = rank_block_bytes(n_visible, G * U, eb) + vis16(n_visible, vb) +
                         (cs > 1 ? xchg_bytes(cs, kFlipThreads / 32, sum_bytes(kfmt)) : 0) + 1024;
-    const bool instantiated = cs == 1 || ((G == 4 || G == 8 || G == 16 || G == 32) && U >= 8);
+    const bool instantiated = cs == 1 || (G == 8 && (U == 8 || U == 13 || U == 25));  // tools/gen_sweep_instances.py
     if (need <= kSmemPlan && instantiated && (cs == 1 || n_hidden > 1)) {
       *cluster = cs;
       *lanes_per_chain = G;
