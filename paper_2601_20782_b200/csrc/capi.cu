@@ -779,14 +779,20 @@ int mpv_local_energies_ex(int N, int M, const double* a, const double* b, const 
   // over the block; 16 samples per block (two DMMA m-tiles) where it fits.
   // Phase 1 runs in one pass: every warp owns <= KT of the ceil(M/4) n-tiles.
   struct Cfg { int st, sb, kt, tmax; const void* fn; };
+  // TFIM: every (sample, term) pair is active; Heisenberg / J1-J2: the active
+  // pairs are compacted per block (COMPACT kernels)
+  const bool cmp = ham != MPV_HAM_TFIM;
+#define MPV_EK(ST, KT, TM, MB) (cmp ? (const void*)&energy_kernel<ST, KT, TM, MB, true> \
+                                    : (const void*)&energy_kernel<ST, KT, TM, MB, false>)
   const Cfg cfgs[] = {
-      {4, 16, 4, 448, (const void*)&energy_kernel<4, 4, 448, 2>},  // 2 blocks/SM, 72 regs (T <= 112)
-      {8, 16, 8, 256, (const void*)&energy_kernel<8, 8, 256, 2>},  // 2 blocks/SM, 128 regs (T <= 128)
-      {8, 16, 4, 512, (const void*)&energy_kernel<8, 4, 512, 1>},
-      {8, 16, 8, 512, (const void*)&energy_kernel<8, 8, 512, 1>},
-      {8, 8, 4, 512, (const void*)&energy_kernel<8, 4, 512, 1>},
-      {8, 8, 8, 512, (const void*)&energy_kernel<8, 8, 512, 1>},
+      {4, 16, 4, 448, MPV_EK(4, 4, 448, 2)},  // 2 blocks/SM, 72 regs (T <= 112)
+      {8, 16, 8, 256, MPV_EK(8, 8, 256, 2)},  // 2 blocks/SM, 128 regs (T <= 128)
+      {8, 16, 4, 512, MPV_EK(8, 4, 512, 1)},
+      {8, 16, 8, 512, MPV_EK(8, 8, 512, 1)},
+      {8, 8, 4, 512, MPV_EK(8, 4, 512, 1)},
+      {8, 8, 8, 512, MPV_EK(8, 8, 512, 1)},
   };
+#undef MPV_EK
   const size_t optin = (size_t)max_smem_optin();
   const int NT = (M + 3) / 4;
   for (int ci = 0; ci < (int)(sizeof(cfgs) / sizeof(cfgs[0])); ++ci) {

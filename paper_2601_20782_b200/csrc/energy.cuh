@@ -173,7 +173,8 @@ inline size_t energy_plan(int N, int M, int T, int SB, int rows, int nbt, Energy
   p->pool_bytes = (int)pool;
   p->nbw = (int)(pool / p->wbuf_bytes);
   if (p->nbw > kMaxBufs) p->nbw = kMaxBufs;
-  return pool + (size_t)SB * 32 * 4 + (size_t)energy_mask_pad(N) * 4 + 4 * kMaxBufs * 8;
+  // + the Heisenberg compaction's per-term active masks and unit offsets
+  return pool + (size_t)SB * 32 * 4 + (size_t)energy_mask_pad(N) * 4 + 4 * kMaxBufs * 8 + (size_t)(2 * T + 1) * 4;
 }
 
 // Bulk-async (TMA engine) ring of nb <= kMaxBufs buffers in shared memory.  Per
@@ -305,7 +306,7 @@ __device__ __noinline__ double2 slow_ratio(int N, int M, int ham, const double2*
 //   tanh(theta) as broadcasts.  Ratios go to shared memory and one warp per
 //   sample sums the terms in a fixed order (deterministic).
 // ST samples per thread, KT DMMA n-tiles per warp, launch bounds (TMAX threads, MINB blocks/SM)
-template <int ST, int KT, int TMAX, int MINB>
+template <int ST, int KT, int TMAX, int MINB, bool COMPACT>
 __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, const EnergyPlan pl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int M = a.M, T = a.n_terms, words = a.words, N = a.N;
@@ -415,7 +416,73 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
   __syncthreads();
 
   auto bit_of = [&](int s, int k) -> int { return (wsm[s * 32 + (k >> 5)] >> (k & 31)) & 1u; };
-  const int g = tid / T, t = tid - g * T;
+  // Heisenberg / J1-J2: a (sample, bond) pair with aligned spins (d = 0) has no
+  // off-diagonal term (about half of them).  The active pairs of each bond are
+  // packed into units of ST samples, term-major, one unit per thread, so whole
+  // warps at the end of the block idle instead of half the lanes of every warp.
+  // TFIM: every pair is active; thread (g, t) takes samples g ST .. g ST + ST - 1.
+  constexpr bool compact = COMPACT;  // launched for Heisenberg / J1-J2 terms
+  uint32_t* cmask = reinterpret_cast<uint32_t*>(bars + 4 * kMaxBufs);  // [T] active samples per term
+  int* coff = reinterpret_cast<int*>(cmask + T);                       // [T + 1] first unit per term
+  if constexpr (compact) {
+    for (int x = tid; x < T; x += blockDim.x) {
+      const int p = a.bonds[2 * x], q = a.bonds[2 * x + 1];
+      uint32_t m = 0;
+      for (int ss = 0; ss < SB; ++ss)
+        if (s0 + ss < a.B && bit_of(ss, p) != bit_of(ss, q)) m |= 1u << ss;
+      cmask[x] = m;
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of ceil(active / ST) over the terms
+      int carry = 0;
+      for (int x0 = 0; x0 < T; x0 += 32) {
+        const int x = x0 + lane;
+        const int cnt = x < T ? (__popc(cmask[x]) + ST - 1) / ST : 0;
+        int inc = cnt;
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y = __shfl_up_sync(kFull, inc, off);
+          if (lane >= off) inc += y;
+        }
+        if (x < T) coff[x] = carry + inc - cnt;
+        carry += __shfl_sync(kFull, inc, 31);
+      }
+      if (lane == 0) coff[T] = carry;
+    }
+    __syncthreads();
+  }
+  int g = 0, t = 0;
+  int sidx[ST];       // block sample of slot j
+  uint32_t live = 0;  // bit j: slot j carries an active pair
+  bool have = false;
+  if constexpr (compact) {
+    if (tid < coff[T]) {
+      int lo = 0, hi = T - 1;  // last term whose first unit is <= tid
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (coff[mid] <= tid) lo = mid;
+        else hi = mid - 1;
+      }
+      t = lo;
+      have = true;
+      uint32_t m = cmask[t];
+      for (int k = (tid - coff[t]) * ST; k > 0; --k) m &= m - 1;
+#pragma unroll
+      for (int j = 0; j < ST; ++j) {
+        sidx[j] = m ? __ffs(m) - 1 : 0;
+        live |= (m ? 1u : 0u) << j;
+        m &= m - 1;
+      }
+    }
+  } else {
+    g = tid / T;
+    t = tid - g * T;
+    have = g < NG;
+#pragma unroll
+    for (int j = 0; j < ST; ++j) {
+      sidx[j] = g * ST + j;
+      live |= 1u << j;
+    }
+  }
   double2 P[ST];
   int E[ST];
   uint32_t sg[ST];  // sign bit of d on the high word (d = -1 -> flip tanh(theta))
@@ -427,22 +494,20 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
     E[j] = 0;
     sg[j] = 0;
   }
-  const bool active = any_terms && g < NG;
+  const bool active = any_terms && have;
   bool slow = false;
-  const double2* tg = tt;
   if (active) {
     int p = t, q = 0;
     if (a.ham != MPV_HAM_TFIM) { p = a.bonds[2 * t]; q = a.bonds[2 * t + 1]; }
 #pragma unroll
     for (int j = 0; j < ST; ++j) {
-      const int s = g * ST + j;
+      const int s = sidx[j];
       const int d = (a.ham == MPV_HAM_TFIM) ? 1 - 2 * bit_of(s, p) : bit_of(s, q) - bit_of(s, p);
       sg[j] = d < 0 ? 0x80000000u : 0u;
       sg_bits |= (d < 0 ? 1u : 0u) << j;
-      nz |= (d != 0 ? 1u : 0u) << j;
+      nz |= (d != 0 && ((live >> j) & 1u) ? 1u : 0u) << j;
     }
     slow = a.slow[t] != 0;
-    tg = tt + g * ST;
   }
   // ---- phase 2: products over hidden units ----
   if (any_terms && !(pl.skip & 4)) {
@@ -453,14 +518,14 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
         // shared-space pointers derived from the dynamic smem array (LDS, not generic LD)
         const double2* tp = reinterpret_cast<const double2*>(tstage + (size_t)tpos.slot * pl.tbuf_bytes) + t;
         const int r0 = c * rows, nr = min(rows, M - r0);
-        const double2* vp = tg + (size_t)r0 * SB;
+        const double2* vp = tt + (size_t)r0 * SB + (compact ? 0 : g * ST);
 #pragma unroll 2
         for (int r = 0; r < nr; ++r) {
           // all loads of the row first (tau per lane, tanh(theta) broadcasts)
           const double2 tau = *tp;
           double2 tv[ST];
 #pragma unroll
-          for (int j = 0; j < ST; ++j) tv[j] = vp[j];
+          for (int j = 0; j < ST; ++j) tv[j] = vp[compact ? sidx[j] : j];
           tp += T;
           vp += SB;
           // u = (d tanh theta) tau, P += P u
@@ -492,7 +557,21 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
   // writes coef_t * ratio_t plus the diagonal of bonds b = t, t + T, ...
   // (ref vmc.py:52-57: J_b s_p s_q), so one fixed-order sum over t gives eps.
   double2* R = tt;
-  if (g < NG && !(pl.skip & 8)) {
+  // diagonal of bonds x, x + T, ... (bond x's J s_p s_q rides on term x's entry)
+  auto diag_of = [&](int s, int x) {
+    double dg = 0.0;
+    for (int b = x; b < a.n_bonds; b += T)
+      dg += (bit_of(s, a.bonds[2 * b]) ^ bit_of(s, a.bonds[2 * b + 1])) ? -(a.bond_j ? a.bond_j[b] : a.J)
+                                                                        : (a.bond_j ? a.bond_j[b] : a.J);
+    return dg;
+  };
+  if (COMPACT && !(pl.skip & 8)) {  // pairs without an off-diagonal term: the diagonal only
+    for (int idx = tid; idx < SB * T; idx += blockDim.x) {
+      const int ss = idx / T, x = idx - ss * T;
+      if (!((cmask[x] >> ss) & 1u)) R[ss * T + x] = make_double2(diag_of(ss, x), 0.0);
+    }
+  }
+  if (have && !(pl.skip & 8)) {
     // the first two bonds of this term in registers (TFIM: 2N bonds over N terms)
     const int b0 = t, b1 = t + T;
     const bool h0 = b0 < a.n_bonds, h1 = b1 < a.n_bonds;
@@ -516,7 +595,8 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
     if (active && slow) {
 #pragma unroll 1
       for (int j = 0; j < ST; ++j) {  // rolled: one call site, results straight to R
-        const int s = g * ST + j;
+        if (!((live >> j) & 1u)) continue;
+        const int s = sidx[j];
         double2 v = make_double2(0.0, 0.0);
         if (s0 + s < a.B && ((nz >> j) & 1u)) v = slow_ratio(a.N, a.M, a.ham, a.a, a.b, a.w_t, a.bonds, wsm + s * 32, t,
                                                                 ((sg_bits >> j) & 1u) ? -1.0 : 1.0);
@@ -525,7 +605,8 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
     } else {
 #pragma unroll
       for (int j = 0; j < ST; ++j) {
-        const int s = g * ST + j;
+        if (!((live >> j) & 1u)) continue;
+        const int s = sidx[j];
         double2 v = make_double2(0.0, 0.0);
         if (active && ((nz >> j) & 1u)) {
           v = cmul(sg[j] ? eam : eap, P[j]);
