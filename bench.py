@@ -425,6 +425,10 @@ def run_ours(args, rank, world, local_rank):
             cfgc = rescnn.CnnTrainConfig(spec_c, n_res=4, n_steps=3, n_samples=4096, n_chains=1024, eta=0.01,
                                          lambda_shift=1e-2, proposal=sampler.Proposal("exchange", N_SITES // 2),
                                          init_scale=0.3, burn_in_sweeps=0)
+            cfgc.n_steps = 1
+            rescnn.train(cfgc)  # warm-up: autograd / cuDNN plans, allocator
+            cfgc.n_steps = 3
+            torch.cuda.synchronize()
             t0 = time.perf_counter()
             rescnn.train(cfgc)
             torch.cuda.synchronize()

@@ -48,6 +48,7 @@ constexpr int kRowsMax = 2048;   // 16 MMA tiles
 constexpr int kThreads = 512;    // 16 warps: TMEM lane quarter x tile group
 constexpr int kTapBytes = kF * kF * 2;  // one B block (16 x 16 f16)
 constexpr int kMaxC = 96;        // configurations per CTA (L >= 3: <= 81)
+constexpr int kIssuers = 4;      // threads issuing a convolution's MMAs
 
 struct Shape {
   int L, Lp, R, n_res, C, tiles, margin;  // R = Lp^2 rows per configuration
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sbar), "r"(kIssuers));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (size_t i = tid * 16; i < S.blob_bytes; i += kThreads * 16)
@@ -226,9 +227,11 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (tid == 0) {
+    // kIssuers threads (lane 0 of warps 0..kIssuers-1, one per SM sub-partition)
+    // issue the tiles round-robin; each commits its own MMAs to the barrier
+    if (lane == 0 && warp < kIssuers) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      for (int t = 0; t < S.tiles; ++t)
+      for (int t = warp; t < S.tiles; t += kIssuers)
         for (int d = 0; d < kTaps; ++d) {
           const int off = (d / 3 - 1) * Lp + (d % 3 - 1);
           const uint32_t aaddr = aPlanes + (uint32_t)((t * 128 + off) * 16);

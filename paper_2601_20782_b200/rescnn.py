@@ -328,7 +328,8 @@ def log_derivatives(params: ResCnnParameters, packed, chunk: int = 1024):
     theta = torch.from_numpy(params.theta).to(dev)
     one = lambda th, s: torch_log_psi(th, s[None], L, params.n_res)[0]  # noqa: E731
     g = vmap(grad(one), in_dims=(None, 0), chunk_size=chunk)
-    return g(theta, spins)
+    with torch.backends.cudnn.flags(enabled=True, deterministic=True, benchmark=False):
+        return g(theta, spins)  # reproducible training runs
 
 
 @dataclass

@@ -213,7 +213,7 @@ def test_train_rescnn_reaches_ground_state(cuda):
     spec = J1J2Spec(LatticeSpec.square(4), 1.0, 0.5, marshall=True)
     e0 = ed.ground_energy_sparse([("heisenberg", spec.lattice.bond_array(), 1.0, 0.0),
                                   ("heisenberg", spec.lattice.next_nearest_bonds(), 0.5, 0.0)], 16)
-    cfg = rescnn.CnnTrainConfig(spec, n_res=2, n_steps=40, n_samples=2048, n_chains=512, eta=0.01,
+    cfg = rescnn.CnnTrainConfig(spec, n_res=2, n_steps=30, n_samples=2048, n_chains=512, eta=0.01,
                                 lambda_shift=1e-2, proposal=sampler.Proposal("exchange", 8), init_scale=0.3,
                                 minsr_precision="f32")
     recs, _ = rescnn.train(cfg)
