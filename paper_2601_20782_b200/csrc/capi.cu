@@ -827,11 +827,12 @@ size_t mpv_logderiv_scratch_bytes(int64_t U, int N, int M) {
 
 // O v (MODE 0, weights fused) or T = tanh(b + W x) (MODE 1, v = parameters)
 static int launch_ov(int mode, const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* v,
-                     const double* w, double* q, double* t_out, void* scratch, cudaStream_t st) {
+                     const double* w, double* q, double* t_out, void* scratch, cudaStream_t st,
+                     const double* skip = nullptr) {
   double* vwt = (double*)scratch;
   const int64_t n = (int64_t)ld_rows(N) * ld_pitch(M);
   ld_transpose_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, st>>>(
-      (const double2*)v, N, M, vwt);
+      (const double2*)v, N, M, vwt, skip);
   const int NT = (M + 3) / 4, kt = (NT + 7) / 8;
   const unsigned grid = (unsigned)((U + kLdSB - 1) / kLdSB);
   const int words = (N + 31) / 32;
@@ -843,7 +844,7 @@ static int launch_ov(int mode, const double* t, const uint32_t* bits, int64_t U,
 #define MPV_OV(K)                                                                                             \
   if (mode == 0) {                                                                                            \
     if (int rc = ensure_smem((const void*)&ld_ov_kernel<K, 0>, tbytes)) return rc;                           \
-    ld_ov_kernel<K, 0><<<grid, 256, tbytes, st>>>(T, bits, U, N, M, words, V, vwt, Q, w, TO);               \
+    ld_ov_kernel<K, 0><<<grid, 256, tbytes, st>>>(T, bits, U, N, M, words, V, vwt, Q, w, TO, skip);         \
   } else {                                                                                                    \
     ld_ov_kernel<K, 1><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, V, vwt, Q, w, TO);                    \
   }
@@ -871,11 +872,20 @@ int mpv_logderiv_tanh(const double* params, const uint32_t* bits, int64_t U, int
   return launch_ov(1, nullptr, bits, U, N, M, params, nullptr, nullptr, t, scratch, (cudaStream_t)stream);
 }
 
+static int launch_ohu(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* u,
+                      const double* w, double* out, double* sum_out, void* scratch, cudaStream_t st,
+                      const double* skip);
+
 int mpv_logderiv_ohu(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* u, const double* w,
                      double* out, double* sum_out, void* scratch, void* stream) {
   if (!t || !bits || !u || !out || !scratch || U < 0 || N < 1 || N > 256 || M < 1)
     return fail(MPV_ERR_ARGS, "logderiv_ohu: bad args (N <= 256)");
-  cudaStream_t st = (cudaStream_t)stream;
+  return launch_ohu(t, bits, U, N, M, u, w, out, sum_out, scratch, (cudaStream_t)stream, nullptr);
+}
+
+static int launch_ohu(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* u,
+                      const double* w, double* out, double* sum_out, void* scratch, cudaStream_t st,
+                      const double* skip) {
   const int P = N + M + M * N;
   if (U == 0) {
     if (cudaMemsetAsync(out, 0, (size_t)P * 2 * sizeof(double), st) != cudaSuccess) return check_launch("logderiv_ohu");
@@ -891,13 +901,13 @@ int mpv_logderiv_ohu(const double* t, const uint32_t* bits, int64_t U, int N, in
   const int words = (N + 31) / 32;
   const double2* T = (const double2*)t;
   const double2* Uv = (const double2*)u;
-  if (ntc == 16) ld_ohu_kernel<16><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w);
-  else if (ntc == 13) ld_ohu_kernel<13><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w);
-  else if (ntc == 8) ld_ohu_kernel<8><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w);
-  else ld_ohu_kernel<4><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w);
+  if (ntc == 16) ld_ohu_kernel<16><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w, skip);
+  else if (ntc == 13) ld_ohu_kernel<13><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w, skip);
+  else if (ntc == 8) ld_ohu_kernel<8><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w, skip);
+  else ld_ohu_kernel<4><<<grid, 256, 0, st>>>(T, bits, U, N, M, words, Uv, partial, chunk, w, skip);
   ld_ohu_reduce_kernel<<<(unsigned)std::min(148 * 8, (P + 256) / 256), 256, 0, st>>>(partial, chunks, N, M,
                                                                                       (double2*)out,
-                                                                                      (double2*)sum_out);
+                                                                                      (double2*)sum_out, skip);
   return check_launch("logderiv_ohu");
 }
 
@@ -946,17 +956,22 @@ int mpv_cg_init(const mpv_cg* cg, const double* f, double tol, int64_t maxiter, 
   return check_launch("cg_init");
 }
 
-int mpv_cg_apply(const mpv_cg* cg, const double* v, double* y, double* ysum, void* stream) {
-  if (int rc = cg_check(cg)) return rc;
-  if (!v || !y || !ysum) return fail(MPV_ERR_ARGS, "cg_apply: bad args");
+static int cg_apply(const mpv_cg* cg, const double* v, double* y, double* ysum, void* stream, const double* skip) {
   const int N = cg->n_visible, M = cg->n_hidden;
   if (cg->n_samples == 0) {
     return mpv_logderiv_ohu(cg->t, cg->bits, 0, N, M, cg->q, nullptr, y, ysum, cg->scratch, stream);
   }
   if (int rc = launch_ov(0, cg->t, cg->bits, cg->n_samples, N, M, v, cg->w, cg->q, nullptr, cg->scratch,
-                         (cudaStream_t)stream))
+                         (cudaStream_t)stream, skip))
     return rc;
-  return mpv_logderiv_ohu(cg->t, cg->bits, cg->n_samples, N, M, cg->q, nullptr, y, ysum, cg->scratch, stream);
+  return launch_ohu(cg->t, cg->bits, cg->n_samples, N, M, cg->q, nullptr, y, ysum, cg->scratch, (cudaStream_t)stream,
+                    skip);
+}
+
+int mpv_cg_apply(const mpv_cg* cg, const double* v, double* y, double* ysum, void* stream) {
+  if (int rc = cg_check(cg)) return rc;
+  if (!v || !y || !ysum) return fail(MPV_ERR_ARGS, "cg_apply: bad args");
+  return cg_apply(cg, v, y, ysum, stream, nullptr);
 }
 
 int mpv_cg_apply_finish(const mpv_cg* cg, const double* v, const double* y, const double* ysum, double* out,
@@ -988,8 +1003,12 @@ int mpv_cg_step(const mpv_cg* cg, void* stream) {
 
 int mpv_cg_run(const mpv_cg* cg, int n_iter, void* stream) {
   if (n_iter < 0) return fail(MPV_ERR_ARGS, "cg_run: n_iter < 0");
+  if (int rc = cg_check(cg)) return rc;
+  // once the device flag reports convergence the products of the batch's
+  // remaining iterations return at once (the updates are no-ops anyway)
+  const double* done = cg->scalars + kCgDone;
   for (int it = 0; it < n_iter; ++it) {
-    if (int rc = mpv_cg_apply(cg, cg->p, cg->y, cg->ysum, stream)) return rc;
+    if (int rc = cg_apply(cg, cg->p, cg->y, cg->ysum, stream, done)) return rc;
     if (int rc = mpv_cg_step(cg, stream)) return rc;
   }
   return MPV_OK;

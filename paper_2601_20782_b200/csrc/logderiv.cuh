@@ -32,7 +32,11 @@ __host__ __device__ inline int ld_pitch(int M) { return 2 * M + 8; }  // doubles
 __host__ __device__ inline int ld_rows(int N) { return (N + 3) / 4 * 4; }
 
 // vW (row-major [M][N] complex, the W block of v) -> vWt[k][2i + c] padded
-__global__ void ld_transpose_kernel(const double2* __restrict__ v, int N, int M, double* __restrict__ vwt) {
+// `skip` (optional): a device flag; non-zero = the launch is a no-op (a converged
+// CG solve's remaining batch iterations)
+__global__ void ld_transpose_kernel(const double2* __restrict__ v, int N, int M, double* __restrict__ vwt,
+                                    const double* __restrict__ skip = nullptr) {
+  if (skip && *skip != 0.0) return;
   const int pitch = ld_pitch(M), rows = ld_rows(N);
   const double2* vw = v + N + M;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (int64_t)rows * pitch;
@@ -66,7 +70,9 @@ __global__ void __launch_bounds__(256, KT >= 16 ? 1 : 2) ld_ov_kernel(const doub
                                                     int64_t U, int N, int M, int words, const double2* __restrict__ v,
                                                     const double* __restrict__ vwt, double2* __restrict__ q,
                                                     const double* __restrict__ w = nullptr,
-                                                    double2* __restrict__ t_out = nullptr) {
+                                                    double2* __restrict__ t_out = nullptr,
+                                                    const double* __restrict__ skip = nullptr) {
+  if (skip && *skip != 0.0) return;
   __shared__ uint32_t smask[256 + 8];        // per-site masks of the block's 16 samples (N <= 256)
   __shared__ double2 red[8][kLdSB];          // per-warp partial q
   __shared__ __align__(8) uint64_t tbar;
@@ -229,7 +235,9 @@ template <int NTC>
 __global__ void __launch_bounds__(256, 2) ld_ohu_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
                                                      int64_t U, int N, int M, int words, const double2* __restrict__ u,
                                                      double* __restrict__ partial, int64_t chunk,
-                                                     const double* __restrict__ wts = nullptr) {
+                                                     const double* __restrict__ wts = nullptr,
+                                                     const double* __restrict__ skip = nullptr) {
+  if (skip && *skip != 0.0) return;
   __shared__ double as[2][64][kLdTile + 1];  // A' tiles [row][sample] (+1 pad: conflict-free column reads)
   __shared__ uint32_t bs[2][kLdTile][9];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -314,7 +322,9 @@ __global__ void __launch_bounds__(256, 2) ld_ohu_kernel(const double2* __restric
 // fixed-order reduction of the chunk partials -> out (complex P-vector); with
 // sum_out, also sum_s u_s (rows 2M, 2M+1 of A' against the ones column N)
 __global__ void ld_ohu_reduce_kernel(const double* __restrict__ partial, int chunks, int N, int M,
-                                     double2* __restrict__ out, double2* __restrict__ sum_out = nullptr) {
+                                     double2* __restrict__ out, double2* __restrict__ sum_out = nullptr,
+                                     const double* __restrict__ skip = nullptr) {
+  if (skip && *skip != 0.0) return;
   const int rows_pad = ld_rows_a(M), cols = ld_cols(N);
   const int P = N + M + M * N;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < P + 1; idx += gridDim.x * blockDim.x) {
