@@ -263,7 +263,7 @@ def run_ours(args, rank, world, local_rank):
             en.run_steps(k, check=False)
             a1.record(stream)
             torch.cuda.synchronize()
-            return {"chain_steps_per_s": chains * k / (a0.elapsed_time(a1) / 1e3), "variant": e.snapshot.label}
+            return {"chain_steps_per_s": chains * k / (a0.elapsed_time(a1) / 1e3), "variant": en.layout_label}
 
         flip = sampler.Proposal("flip")
         extra = {"precision_sweep_a2_10x10": {

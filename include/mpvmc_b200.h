@@ -346,6 +346,13 @@ int mpv_plan_layout(int n_visible, int n_hidden, int fmt, int variant, int32_t* 
  * none fits (read through L1/L2). */
 int mpv_plan_cluster(int n_visible, int n_hidden, int fmt, int mode, int variant, int32_t* cluster,
                      int32_t* lanes_per_chain, int32_t* units_per_lane);
+/* As mpv_plan_cluster with at least `min_lanes` lanes per chain (a power of
+ * two <= 32).  Exchange sweeps plan with 32: a warp then holds one chain, and
+ * a step whose exchange swaps equal bits (about half of them in a balanced
+ * sector) is skipped by the whole warp.  The f32 summation order of NATIVE
+ * log p follows the layout, so it is a function of (snapshot, min_lanes). */
+int mpv_plan_cluster_ex(int n_visible, int n_hidden, int fmt, int mode, int variant, int min_lanes,
+                        int32_t* cluster, int32_t* lanes_per_chain, int32_t* units_per_lane);
 
 const char* mpv_last_error(void);
 const char* mpv_version(void);

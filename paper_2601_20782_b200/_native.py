@@ -59,6 +59,9 @@ _SIGNATURES = {
                                           ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
     "mpv_plan_cluster": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
+    "mpv_plan_cluster_ex": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                                           ctypes.POINTER(_i32)]),
     "mpv_snapshot_round": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
     "mpv_snapshot_fill": (ctypes.c_int, [ctypes.POINTER(Snapshot), _vp, ctypes.c_double, _vp]),
     "mpv_table_sweep": (ctypes.c_int, [_vp, ctypes.POINTER(Chains), _u64, ctypes.c_int, _i64, _i64, _i64, _i64, _vp,
@@ -167,10 +170,11 @@ def stream_handle(device=None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def plan_cluster(n_visible: int, n_hidden: int, fmt: int, mode: int, variant: int):
-    """(cluster, G, U) of the fused sweep's layout (mpv_plan_cluster)."""
+def plan_cluster(n_visible: int, n_hidden: int, fmt: int, mode: int, variant: int, min_lanes: int = 1):
+    """(cluster, G, U) of the fused sweep's layout (mpv_plan_cluster_ex)."""
     c, g, u = _i32(), _i32(), _i32()
-    call("mpv_plan_cluster", n_visible, n_hidden, fmt, mode, variant, ctypes.byref(c), ctypes.byref(g), ctypes.byref(u))
+    call("mpv_plan_cluster_ex", n_visible, n_hidden, fmt, mode, variant, min_lanes, ctypes.byref(c), ctypes.byref(g),
+         ctypes.byref(u))
     return c.value, g.value, u.value
 
 

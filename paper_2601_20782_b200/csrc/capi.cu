@@ -308,13 +308,14 @@ static int units_cap(int fmt, int variant) {
   return fmt == MPV_FMT_F32 ? 13 : 16;
 }
 
-int mpv_plan_layout(int n_visible, int n_hidden, int fmt, int variant, int32_t* lanes_per_chain,
-                    int32_t* units_per_lane) {
-  if (n_visible < 1 || n_visible > 1024 || n_hidden < 1 || !lanes_per_chain || !units_per_lane)
+static int plan_layout(int n_visible, int n_hidden, int fmt, int variant, int min_lanes, int32_t* lanes_per_chain,
+                       int32_t* units_per_lane) {
+  if (n_visible < 1 || n_visible > 1024 || n_hidden < 1 || !lanes_per_chain || !units_per_lane ||
+      min_lanes < 1 || min_lanes > 32 || (min_lanes & (min_lanes - 1)))
     return fail(MPV_ERR_ARGS, "plan: bad args");
   const int words = (n_visible + 31) / 32;
   const int cap = units_cap(fmt, variant);
-  int G = 1;
+  int G = min_lanes;
   while (G < 32 && ((n_hidden + G - 1) / G > cap || G < words)) G *= 2;
   const int need = (n_hidden + G - 1) / G;
   for (int u : kUnits)
@@ -324,6 +325,11 @@ int mpv_plan_layout(int n_visible, int n_hidden, int fmt, int variant, int32_t* 
       return MPV_OK;
     }
   return fail(MPV_ERR_ARGS, "plan: too many hidden units for the fused sweep");
+}
+
+int mpv_plan_layout(int n_visible, int n_hidden, int fmt, int variant, int32_t* lanes_per_chain,
+                    int32_t* units_per_lane) {
+  return plan_layout(n_visible, n_hidden, fmt, variant, 1, lanes_per_chain, units_per_lane);
 }
 
 int mpv_stream_uniforms(uint64_t key, int64_t n_chains, int64_t chain0, int64_t t0, int64_t n_draws,
@@ -351,6 +357,11 @@ int mpv_snapshot_bytes(int n_visible, int hidden_pad, int fmt, int mode, int var
 
 int mpv_plan_cluster(int n_visible, int n_hidden, int fmt, int mode, int variant, int32_t* cluster,
                      int32_t* lanes_per_chain, int32_t* units_per_lane) {
+  return mpv_plan_cluster_ex(n_visible, n_hidden, fmt, mode, variant, 1, cluster, lanes_per_chain, units_per_lane);
+}
+
+int mpv_plan_cluster_ex(int n_visible, int n_hidden, int fmt, int mode, int variant, int min_lanes, int32_t* cluster,
+                        int32_t* lanes_per_chain, int32_t* units_per_lane) {
   if (!cluster || !lanes_per_chain || !units_per_lane) return fail(MPV_ERR_ARGS, "plan_cluster: null output");
   const bool f64arith = (fmt == MPV_FMT_F64) || (mode == MPV_MODE_STORAGE_ONLY);
   const int kfmt = f64arith ? MPV_FMT_F64 : fmt, var = f64arith ? MPV_ACC_F64 : variant;
@@ -363,7 +374,7 @@ int mpv_plan_cluster(int n_visible, int n_hidden, int fmt, int mode, int variant
   const int max_cs = (env && env[0] == '1') ? 4 : 1;
   for (int cs : {1, 2, 4}) {
     if (cs > max_cs) break;
-    if (mpv_plan_layout(n_visible, (n_hidden + cs - 1) / cs, kfmt, var, &G, &U)) return MPV_ERR_ARGS;
+    if (plan_layout(n_visible, (n_hidden + cs - 1) / cs, kfmt, var, min_lanes, &G, &U)) return MPV_ERR_ARGS;
     const size_t need = rank_block_bytes(n_visible, G * U, eb) + vis16(n_visible, vb) +
                         (cs > 1 ? xchg_bytes(cs, kFlipThreads / 32, sum_bytes(kfmt)) : 0) + 1024;
     const bool instantiated = cs == 1 || (G == 8 && (U == 8 || U == 13 || U == 25));  // tools/gen_sweep_instances.py
@@ -375,7 +386,7 @@ int mpv_plan_cluster(int n_visible, int n_hidden, int fmt, int mode, int variant
     }
   }
   // nothing fits on chip: one CTA per chain group, table read through L1/L2
-  if (mpv_plan_layout(n_visible, n_hidden, kfmt, var, &G, &U)) return MPV_ERR_ARGS;
+  if (plan_layout(n_visible, n_hidden, kfmt, var, min_lanes, &G, &U)) return MPV_ERR_ARGS;
   *cluster = 1;
   *lanes_per_chain = G;
   *units_per_lane = U;
@@ -795,12 +806,17 @@ int mpv_local_energies_ex(int N, int M, const double* a, const double* b, const 
 #undef MPV_EK
   const size_t optin = (size_t)max_smem_optin();
   const int NT = (M + 3) / 4;
+  // profiling only: MPV_ENERGY_CFG=ci[,nbt,rows] forces a configuration
+  static const char* force = getenv("MPV_ENERGY_CFG");
+  int f_ci = -1, f_nbt = 0, f_rows = 0;
+  if (force) sscanf(force, "%d,%d,%d", &f_ci, &f_nbt, &f_rows);
   for (int ci = 0; ci < (int)(sizeof(cfgs) / sizeof(cfgs[0])); ++ci) {
     const Cfg& cf = cfgs[ci];
+    if (f_ci >= 0 && ci != f_ci) continue;
     const int threads = std::max(std::max(32, ((cf.sb / cf.st) * T + 31) / 32 * 32), 32 * ((NT + cf.kt - 1) / cf.kt));
     if (threads > cf.tmax) continue;
-    for (int nbt = 3; nbt >= 2; --nbt)
-      for (int rows = 12; rows >= 2; rows -= 2) {
+    for (int nbt = f_nbt ? f_nbt : 3; nbt >= 2; --nbt)
+      for (int rows = f_rows ? f_rows : 12; rows >= 2; rows -= 2) {
         EnergyPlan pl;
         const size_t smem = energy_plan(N, M, T, cf.sb, rows, nbt, &pl);
         // profiling only: MPV_ENERGY_SKIP bit mask drops kernel phases (profiles/r01/README.md)

@@ -756,6 +756,19 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
       // exchange of equal bits (dsign == 0) is accepted unconditionally: the
       // reference evaluator returns the cached value, Δ = 0, log u < 0
       // (sampler.py:119-131).
+      // A warp whose chains all drew an exchange of equal bits has nothing to
+      // evaluate this step: every chain accepts without moving (the reference
+      // returns the cached value, sampler.py:119-131); only the counters and the
+      // sample record advance.  (Flip proposals always have dsign != 0.)
+      if (PROP == MPV_PROPOSAL_EXCHANGE && !__any_sync(kFull, dsign != 0)) {
+        n_acc += dead ? 0 : 1;
+        if (s + 1 == next_record) {
+          next_record += thin;
+          const int64_t r = a.round_offset + (s + 1) / thin - 1;
+          if (live && writer && r < count_c && gl < words) a.samples[(offset_c + r) * words + gl] = myword;
+        }
+        continue;
+      }
       const Sign d = A::sign(dsign);
       const Sign md = A::sign(-dsign);
       const Entry* c1 = tab + (size_t)k1 * Mpad + gl;

@@ -238,6 +238,18 @@ class DeviceSnapshot:
                     quantum = self.plan.quantum
             cluster, G, U = nat.plan_cluster(N, M, fmt.code, mode.code, variant)
             Mpad = cluster * G * U
+        self._split, self._quantum = split, quantum
+        self._layouts = {}
+        self._fill(variant, cluster, G, U, Mpad)
+
+    def _fill(self, variant, cluster, G, U, Mpad):
+        """Table, bias and visible terms in the layout (cluster, G, U), filled on
+        the device from the rounded parameters."""
+        import torch
+
+        N, M, fmt, mode = self.n_visible, self.n_hidden, self.fmt, self.mode
+        stream = nat.stream_handle(self.device)
+        split, quantum = self._split, self._quantum
         self.variant, self.lanes_per_chain, self.units_per_lane, self.hidden_pad = variant, G, U, Mpad
         self.cluster = cluster
         sizes = (ctypes.c_size_t * 3)()
@@ -249,6 +261,31 @@ class DeviceSnapshot:
         self.struct = nat.Snapshot(N, M, Mpad, fmt.code, mode.code, variant, G, U, cluster,
                                    base, self._bias.data_ptr(), base + int(sizes[1]), self._vis_im.data_ptr(), quantum)
         nat.call("mpv_snapshot_fill", ctypes_byref(self.struct), self._rounded.data_ptr(), split, stream)
+
+    def for_proposal(self, kind: str) -> "DeviceSnapshot":
+        """The snapshot in the layout the fused sweep uses for `kind`.  Exchange
+        sweeps run one chain per warp (32 lanes per chain, mpv_plan_cluster_ex)
+        so a step that swaps equal bits is skipped by the whole warp; the table
+        is re-filled once from the same rounded parameters and cached."""
+        if kind != "exchange":
+            return self
+        f64arith = self.fmt.name == "f64" or self.mode is RoundingMode.STORAGE_ONLY
+        if self.mode is RoundingMode.PER_OPERATION and not f64arith:
+            return self  # the per-operation kernels do not use the lane layout
+        if self.cluster > 1:
+            return self  # opt-in cluster split (instantiated for G = 8 only)
+        cluster, G, U = nat.plan_cluster(self.n_visible, self.n_hidden, self.fmt.code, self.mode.code, self.variant,
+                                         32)
+        if (cluster, G, U) == (self.cluster, self.lanes_per_chain, self.units_per_lane):
+            return self
+        key = (cluster, G, U)
+        if key not in self._layouts:
+            other = object.__new__(DeviceSnapshot)
+            other.__dict__.update({k: v for k, v in self.__dict__.items() if k != "_layouts"})
+            other._layouts = {}
+            other._fill(self.variant, cluster, G, U, cluster * G * U)
+            self._layouts[key] = other
+        return self._layouts[key]
 
     @property
     def params(self) -> RbmParameters:
@@ -316,6 +353,19 @@ class LogProbEvaluator:
     @property
     def n_visible(self):
         return self.snapshot.n_visible
+
+    def for_proposal(self, kind: str) -> "LogProbEvaluator":
+        """This evaluator in the lane layout an ensemble with `kind` proposals
+        sweeps with (DeviceSnapshot.for_proposal).  With NATIVE arithmetic the
+        f32 summation order of the hidden sum follows the layout, so a chain's
+        cached log p equals this view's evaluation bit for bit."""
+        snap = self.snapshot.for_proposal(kind)
+        if snap is self.snapshot:
+            return self
+        view = object.__new__(type(self))
+        view.__dict__.update(self.__dict__)
+        view.snapshot = snap
+        return view
 
     def log_prob_packed(self, packed):
         """Device path: packed uint32 [B, words] tensor -> float64 [B] tensor."""

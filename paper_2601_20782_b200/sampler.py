@@ -162,13 +162,27 @@ class ChainEnsemble:
 
         if isinstance(self._evaluator, (TableLogProb, ResCnnEvaluator)):
             return
-        need = nat.load().mpv_sweep_scratch_bytes(ctypes.byref(self._evaluator.snapshot.struct), self.n_chains)
+        need = nat.load().mpv_sweep_scratch_bytes(ctypes.byref(self._snapshot().struct), self.n_chains)
         if self._scratch is None or self._scratch.numel() < need:
             import torch
 
             self._scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
             self._chains.scratch = self._scratch.data_ptr()
             self._chains.scratch_bytes = self._scratch.numel()
+
+    def _snapshot(self):
+        """The evaluator's snapshot in this ensemble's sweep layout (exchange: one
+        chain per warp, DeviceSnapshot.for_proposal)."""
+        return self._evaluator.snapshot.for_proposal(self.proposal.kind)
+
+    @property
+    def layout_label(self) -> str:
+        """Format / arithmetic / accumulator / lane layout of this ensemble's sweep."""
+        from .rescnn import ResCnnEvaluator
+
+        if isinstance(self._evaluator, (TableLogProb, ResCnnEvaluator)):
+            return type(self._evaluator).__name__
+        return self._snapshot().label
 
     def _stream(self):
         return nat.stream_handle(self.device)
@@ -188,7 +202,7 @@ class ChainEnsemble:
                      self.proposal.code, self.init_draws, self.steps_done, int(n_steps), int(thin), sp,
                      int(n_samples_total), self.n_chains_total, int(round_offset), int(row0), self._stream())
         else:
-            nat.call("mpv_mh_sweep", ctypes.byref(self._evaluator.snapshot.struct), ctypes.byref(self._chains),
+            nat.call("mpv_mh_sweep", ctypes.byref(self._snapshot().struct), ctypes.byref(self._chains),
                      self.key, self.proposal.code, self.init_draws, self.steps_done, int(n_steps), int(thin), sp,
                      int(n_samples_total), self.n_chains_total, int(round_offset), int(row0), self._stream())
         self.steps_done += int(n_steps)

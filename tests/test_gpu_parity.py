@@ -397,7 +397,8 @@ def test_edge_shapes_native_model(cuda, n, alpha, fmt):
     for kind, weight in kinds:
         ens = sampler.ChainEnsemble(19, n, sampler.Proposal(kind, weight), ev, derive_key(3, "chains"))
         ens.run_steps(120)
-        np.testing.assert_array_equal(ens.log_probs, ev(ens.bits))  # cached log p == fresh evaluation
+        # cached log p == fresh evaluation (in the sweep's lane layout)
+        np.testing.assert_array_equal(ens.log_probs, ev.for_proposal(kind)(ens.bits))
         if kind == "exchange":
             assert np.all(ens.bits.sum(axis=1) == n // 2)
 
@@ -430,7 +431,7 @@ def test_cluster_split_sweep(cuda, monkeypatch, n, alpha, fmt, kind, scale):
     key = derive_key(2, "chains")
     a = sampler.ChainEnsemble(300, n, prop, ev, key)
     a.run_steps(700)
-    np.testing.assert_array_equal(a.log_probs, ev(a.bits))
+    np.testing.assert_array_equal(a.log_probs, ev.for_proposal(kind)(a.bits))
     s0 = sampler.ChainEnsemble(100, n, prop, ev, key, chain_offset=0, n_chains_total=300)
     s1 = sampler.ChainEnsemble(200, n, prop, ev, key, chain_offset=100, n_chains_total=300)
     for s in (s0, s1):

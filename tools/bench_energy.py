@@ -11,10 +11,16 @@ for name, spec, alpha in (("tfim10x10 a2", TfimSpec(LatticeSpec.square(10), 1.0,
     p = rbm.random_parameters(100, alpha, derive_key(0, "init"), 0.01)
     psi = rbm.log_psi_evaluator(p)
     kern = vmc._energy_kernel(spec, psi)
+    if len(sys.argv) > 1 and sys.argv[1] not in name:
+        continue
     bits = np.random.default_rng(0).integers(0, 2, size=(65536, 100), dtype=np.uint8)
     packed = torch.from_numpy(pack_bits(bits)).cuda()
-    for _ in range(3):
-        kern.packed(packed)
+    try:
+        for _ in range(3):
+            kern.packed(packed)
+    except ValueError as exc:
+        print(f"{name}: {exc}")
+        continue
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()

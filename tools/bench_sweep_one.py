@@ -21,4 +21,4 @@ en.run_steps(4 * n)
 torch.cuda.synchronize()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record(); en.run_steps(4 * (n + 1), check=False); b.record(); torch.cuda.synchronize()
-print(f"{fmt.name} {ev.snapshot.label} {chains * 4 * (n + 1) / (a.elapsed_time(b) / 1e3):.3e} chain-steps/s")
+print(f"{fmt.name} {en.layout_label} {chains * 4 * (n + 1) / (a.elapsed_time(b) / 1e3):.3e} chain-steps/s")
