@@ -315,8 +315,12 @@ int mpv_forward_tc(int N, int M, int fmt, const void* weights, const uint32_t* b
  * mpv_rescnn_mh_sweep: n_steps MH steps (ref: sampler.py:111-133, the
  * reference's streams and f64 accept test) with the tcgen05 evaluator, one
  * fused propose / evaluate / accept launch per step, samples recorded as
- * mpv_mh_sweep does; the cached log p is refreshed first. */
+ * mpv_mh_sweep does; the cached log p is refreshed first.  Exchange steps
+ * with ch->scratch of >= mpv_rescnn_mh_scratch_bytes(n_chains) bytes first
+ * settle the chains whose swap exchanges equal bits (the identity, always
+ * accepted) and evaluate only the others on the tensor cores. */
 size_t mpv_rescnn_blob_bytes(int L, int n_res);
+size_t mpv_rescnn_mh_scratch_bytes(int64_t n_chains);
 int mpv_rescnn_forward(int L, int n_res, int fmt, const void* blob, const uint32_t* bits, int64_t B, double* out_lp,
                        int64_t* status, void* stream);
 int mpv_rescnn_forward_f64(const double* theta, int L, int n_res, const uint32_t* bits, int64_t B, double* out,

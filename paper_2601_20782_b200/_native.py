@@ -103,6 +103,7 @@ _SIGNATURES = {
     "mpv_forward_tc": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _vp,
                                       ctypes.c_int, _vp]),
     "mpv_rescnn_blob_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int]),
+    "mpv_rescnn_mh_scratch_bytes": (ctypes.c_size_t, [_i64]),
     "mpv_rescnn_forward": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _vp]),
     "mpv_rescnn_forward_f64": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _i64, _vp, _vp]),
     "mpv_rescnn_mh_sweep": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.POINTER(Chains), _u64,

@@ -28,7 +28,8 @@ cudaError_t rescnn_launch(int L, int n_res, int fmt, const void* blob, uint32_t*
                           double* lp, int64_t* accepted, int64_t* status, int mh, uint64_t key, int64_t chain_offset,
                           int64_t init_draws, int64_t step_index, int proposal, uint32_t* samples, int64_t thin,
                           int64_t sample_base, int64_t sample_extra, int64_t round_offset, int64_t row0,
-                          int64_t local_step1, cudaStream_t st);
+                          int64_t local_step1, cudaStream_t st, int32_t* list = nullptr,
+                          int32_t* count = nullptr);
 cudaError_t rescnn_f64_launch(const double* theta, int L, int n_res, const uint32_t* bits, int64_t B, int words,
                               double* out, cudaStream_t st);
 cudaError_t forward_tc_prepare(int N, int M, int fmt, const double* params, void* weights, cudaStream_t st);
@@ -1125,6 +1126,8 @@ int mpv_rescnn_forward_f64(const double* theta, int L, int n_res, const uint32_t
   return MPV_OK;
 }
 
+size_t mpv_rescnn_mh_scratch_bytes(int64_t n_chains) { return 16 + 4 * (size_t)std::max<int64_t>(n_chains, 0); }
+
 int mpv_rescnn_mh_sweep(int L, int n_res, int fmt, const void* blob, const mpv_chains* ch, uint64_t key, int proposal,
                         int64_t init_draws, int64_t step_index, int64_t n_steps, int64_t thin, uint32_t* samples,
                         int64_t n_samples_total, int64_t n_chains_total, int64_t round_offset, int64_t row0,
@@ -1141,13 +1144,22 @@ int mpv_rescnn_mh_sweep(int L, int n_res, int fmt, const void* blob, const mpv_c
     extra = n_samples_total % n_chains_total;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  // exchange steps evaluate only the chains whose swap changes the configuration
+  // (list + two step counters in the chains' scratch, mpv_rescnn_mh_scratch_bytes)
+  int32_t *list = nullptr, *count = nullptr;
+  if (proposal == MPV_PROPOSAL_EXCHANGE && ch->scratch &&
+      ch->scratch_bytes >= mpv_rescnn_mh_scratch_bytes(ch->n_chains)) {
+    count = (int32_t*)ch->scratch;
+    list = count + 4;
+    if (cudaMemsetAsync(count, 0, 4 * sizeof(int32_t), st) != cudaSuccess) return check_launch("rescnn_mh_sweep");
+  }
   // the cached log p of the current configurations (set_evaluator semantics)
   cudaError_t e = rescnn_launch(L, n_res, fmt, blob, ch->bits, ch->n_chains, ch->words, ch->log_probs, nullptr,
                                 ch->status, 0, 0, 0, 0, 0, 0, nullptr, 0, 0, 0, 0, 0, 0, st);
   for (int64_t s = 0; e == cudaSuccess && s < n_steps; ++s)
     e = rescnn_launch(L, n_res, fmt, blob, ch->bits, ch->n_chains, ch->words, ch->log_probs, ch->accepted,
                       ch->status, 1, key, ch->chain_offset, init_draws, step_index + s, proposal, samples, thin, base,
-                      extra, round_offset, row0, s + 1, st);
+                      extra, round_offset, row0, s + 1, st, list, count);
   if (e != cudaSuccess) return fail(MPV_ERR_CUDA, std::string("rescnn_mh_sweep: ") + cudaGetErrorString(e));
   return MPV_OK;
 }

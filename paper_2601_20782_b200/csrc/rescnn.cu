@@ -173,6 +173,9 @@ struct Args {
   uint32_t* samples;
   int64_t thin, sample_base, sample_extra, round_offset, row0;
   int64_t local_step1;       // 1-based step within the recording launch
+  // compacted MH step (exchange): the chains to evaluate, list[0 .. *count)
+  const int32_t* list;
+  const int32_t* count;
 };
 
 template <int FMT>
@@ -218,7 +221,6 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
   const int q = warp & 3, tg = warp >> 2;  // TMEM lane quarter, tile group
   const uint32_t t_lane = (uint32_t)(q * 32) << 16;
   const int L = S.L;
-  const int64_t groups = (a.B + C - 1) / C;
   const float* cb = vec;                          // [(n_res+1)][3][16]: cumulative bias, gain, shift
   const float* b1 = vec + (S.n_res + 1) * 3 * kF;  // [n_res][16]
 
@@ -247,12 +249,14 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   };
 
-  for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
+  const int64_t B = a.list ? (int64_t)*a.count : a.B;  // compacted: only the chains that move
+  auto chain_of = [&](int64_t idx) -> int64_t { return a.list ? (int64_t)a.list[idx] : idx; };
+  for (int64_t grp = blockIdx.x; grp < (B + C - 1) / C; grp += gridDim.x) {
     const int64_t c0 = grp * C;
-    const int nc = (int)min((int64_t)C, a.B - c0);
+    const int nc = (int)min((int64_t)C, B - c0);
     // ---- proposals (MH) ----
     if (a.mh && tid < nc) {
-      const int64_t c = c0 + tid, gchain = a.chain_offset + c;
+      const int64_t c = chain_of(c0 + tid), gchain = a.chain_offset + c;
       const uint64_t s0 = stream_state(a.key, (uint64_t)gchain);
       const uint64_t t = (uint64_t)(a.init_draws + 2 * a.step_index);
       const double us = stream_draw(s0, t), ua = stream_draw(s0, t + 1);
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
         pr = pr == 0 ? L : (pr == L + 1 ? 1 : pr);
         pc = pc == 0 ? L : (pc == L + 1 ? 1 : pc);
         const int site = (pr - 1) * L + (pc - 1);
-        uint32_t x = (a.bits[(c0 + j) * words + (site >> 5)] >> (site & 31)) & 1u;
+        uint32_t x = (a.bits[chain_of(c0 + j) * words + (site >> 5)] >> (site & 31)) & 1u;
         if (a.mh && (site == s_site[j] || site == s_site2[j])) x ^= 1u;
         v[0] = x ? -1.0f : 1.0f;
       }
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
       float sum = 0.0f;
       for (int pos = 0; pos < R; ++pos) sum += rowsum[j * R + pos];
       const double lp_new = 2.0 * (double)sum;
-      const int64_t c = c0 + j;
+      const int64_t c = chain_of(c0 + j);
       if (!a.mh) {
         a.out_lp[c] = lp_new;
         if (!isfinite(lp_new) && a.status) {
@@ -529,11 +533,43 @@ size_t rescnn_blob_bytes(int L, int n_res) {
   return make_shape(L, n_res, &s) ? s.blob_bytes : 0;
 }
 
+// Exchange MH step, part 1: the reference's draws of every chain; a swap of
+// equal bits is the identity (always accepted, sampler.py:119-131): its
+// counter and sample record are written here, and only the other chains are
+// appended to the list the tensor-core step evaluates (their order does not
+// matter: each configuration's log p is independent of its tile slot).
+// count[step & 1] collects this step; count[(step + 1) & 1] is cleared for the next.
+__global__ void rescnn_propose_kernel(const Args a, int32_t* list, int32_t* count) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (threadIdx.x == 0 && blockIdx.x == 0) count[(a.step_index + 1) & 1] = 0;
+  if (c >= a.B) return;
+  const int64_t gchain = a.chain_offset + c;
+  const uint64_t s0 = stream_state(a.key, (uint64_t)gchain);
+  const double us = stream_draw(s0, (uint64_t)(a.init_draws + 2 * a.step_index));
+  int i, j;
+  pair_of(floor_scaled(us, 0.5 * (double)a.N * (double)(a.N - 1)), a.N, i, j);
+  const uint32_t bi = (a.bits[c * a.words + (i >> 5)] >> (i & 31)) & 1u;
+  const uint32_t bj = (a.bits[c * a.words + (j >> 5)] >> (j & 31)) & 1u;
+  if (bi != bj) {
+    list[atomicAdd(&count[a.step_index & 1], 1)] = (int32_t)c;
+    return;
+  }
+  if (a.accepted) a.accepted[c] += 1;
+  const int64_t s1 = a.local_step1;
+  if (a.samples && a.thin > 0 && s1 % a.thin == 0) {
+    const int64_t count_c = a.sample_base + (gchain < a.sample_extra ? 1 : 0);
+    const int64_t offset_c = gchain * a.sample_base + (gchain < a.sample_extra ? gchain : a.sample_extra) - a.row0;
+    const int64_t rr = a.round_offset + s1 / a.thin - 1;
+    if (rr < count_c)
+      for (int w = 0; w < a.words; ++w) a.samples[(offset_c + rr) * a.words + w] = a.bits[c * a.words + w];
+  }
+}
+
 cudaError_t rescnn_launch(int L, int n_res, int fmt, const void* blob, uint32_t* bits, int64_t B, int words,
                           double* lp, int64_t* accepted, int64_t* status, int mh, uint64_t key, int64_t chain_offset,
                           int64_t init_draws, int64_t step_index, int proposal, uint32_t* samples, int64_t thin,
                           int64_t sample_base, int64_t sample_extra, int64_t round_offset, int64_t row0,
-                          int64_t local_step1, cudaStream_t st) {
+                          int64_t local_step1, cudaStream_t st, int32_t* list, int32_t* count) {
   Args a{};
   if (!make_shape(L, n_res, &a.S)) return cudaErrorInvalidValue;
   a.blob = (const uint8_t*)blob;
@@ -549,6 +585,11 @@ cudaError_t rescnn_launch(int L, int n_res, int fmt, const void* blob, uint32_t*
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t groups = (B + a.S.C - 1) / a.S.C;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(groups, n_sm));
+  if (mh && proposal == MPV_PROPOSAL_EXCHANGE && list && count) {
+    rescnn_propose_kernel<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(a, list, count);
+    a.list = list;
+    a.count = count + (step_index & 1);
+  }
   void* args[] = {&a};
   return cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, a.S.smem, st);
 }

@@ -160,9 +160,12 @@ class ChainEnsemble:
     def _bind_scratch(self):
         from .rescnn import ResCnnEvaluator
 
-        if isinstance(self._evaluator, (TableLogProb, ResCnnEvaluator)):
+        if isinstance(self._evaluator, TableLogProb):
             return
-        need = nat.load().mpv_sweep_scratch_bytes(ctypes.byref(self._snapshot().struct), self.n_chains)
+        if isinstance(self._evaluator, ResCnnEvaluator):  # compacted exchange steps
+            need = nat.load().mpv_rescnn_mh_scratch_bytes(self.n_chains)
+        else:
+            need = nat.load().mpv_sweep_scratch_bytes(ctypes.byref(self._snapshot().struct), self.n_chains)
         if self._scratch is None or self._scratch.numel() < need:
             import torch
 

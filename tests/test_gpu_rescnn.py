@@ -160,6 +160,28 @@ def test_mh_exchange_shards_and_launch_splits(cuda):
     np.testing.assert_array_equal(np.concatenate(parts), full)
 
 
+def test_mh_exchange_compacted_equals_full_step(cuda):
+    """Exchange steps evaluate only the chains whose swap moves (a list built by
+    the propose kernel, in nondeterministic order): chains, cached log p,
+    counters and recorded samples equal the uncompacted step (every chain
+    evaluated in place), which runs when the ensemble has no scratch."""
+    L, n = 6, 36
+    p = _params(L, 2, seed=8, scale=0.7)
+    ev = rescnn.log_prob_evaluator(p, F16)
+    prop = sampler.Proposal("exchange", n // 2)
+    key = derive_key(10, "chains")
+    a = sampler.ChainEnsemble(130, n, prop, ev, key)
+    b = sampler.ChainEnsemble(130, n, prop, ev, key)
+    b._chains.scratch = None  # no list / counters: the uncompacted step
+    b._chains.scratch_bytes = 0
+    sa, sb = a.collect(260, 11), b.collect(260, 11)
+    np.testing.assert_array_equal(sa, sb)
+    np.testing.assert_array_equal(a.bits, b.bits)
+    np.testing.assert_array_equal(a.log_probs, b.log_probs)
+    assert a.acceptance_rate == b.acceptance_rate
+    np.testing.assert_array_equal(a.log_probs, ev(a.bits))
+
+
 def test_log_derivatives_match_finite_differences(cuda):
     """O = d log psi / d theta (torch autograd over the torch restatement) against
     central differences of the device f64 forward, and the torch restatement's
