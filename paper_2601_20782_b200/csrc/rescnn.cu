@@ -410,15 +410,16 @@ __device__ __forceinline__ double gelu64(double z) {
 }
 
 constexpr int kF64Threads = 512;
+constexpr int kFS = kF + 1;  // doubles per site in the activation buffers (odd: conflict-free LDS.64 across sites)
 
 __global__ void __launch_bounds__(kF64Threads) rescnn_f64_kernel(const double* __restrict__ theta, int L, int n_res,
                                                                   const uint32_t* __restrict__ bits, int64_t B,
                                                                   int words, int G, double* __restrict__ out) {
   extern __shared__ double sm64[];
   const int N = L * L;
-  double* wsm = sm64;                 // [16 cout][16 cin][9]
-  double* bufA = wsm + kF * kF * kTaps;  // [G][N][16]
-  double* bufB = bufA + (size_t)G * N * kF;
+  double* wsm = sm64;                 // [9 taps][16 cin][16 cout]: a (tap, cin)'s 16 weights are 8 LDS.128
+  double* bufA = wsm + kF * kF * kTaps;  // [G][N][kFS]
+  double* bufB = bufA + (size_t)G * N * kFS;
   __shared__ double red[kF64Threads];
   const int tid = threadIdx.x;
   const int g = tid / N, p = tid % N;  // configuration slot, site
@@ -432,7 +433,10 @@ __global__ void __launch_bounds__(kF64Threads) rescnn_f64_kernel(const double* _
 
   auto stage = [&](const double* w) {  // one 16x16x9 convolution's weights
     __syncthreads();
-    for (int i = tid; i < kF * kF * kTaps; i += blockDim.x) wsm[i] = w[i];
+    for (int i = tid; i < kF * kF * kTaps; i += blockDim.x) {  // w: [cout][cin][tap] (oracle/rescnn.py)
+      const int c = i / (kF * kTaps), ci = (i / kTaps) % kF, d = i % kTaps;
+      wsm[(d * kF + ci) * kF + c] = w[i];
+    }
     __syncthreads();
   };
   // out[c] = bias[c] + sum_{tap, cin} w[c][cin][tap] src[nb(tap)][cin]
@@ -440,11 +444,17 @@ __global__ void __launch_bounds__(kF64Threads) rescnn_f64_kernel(const double* _
 #pragma unroll
     for (int c = 0; c < kF; ++c) o[c] = bias[c];
     for (int d = 0; d < kTaps; ++d) {
-      const double* sq = src + (size_t)nb[d] * kF;
+      const double* sq = src + (size_t)nb[d] * kFS;
+      const double2* wd = reinterpret_cast<const double2*>(wsm + d * kF * kF);
+#pragma unroll 2
       for (int ci = 0; ci < kF; ++ci) {
         const double a = sq[ci];
 #pragma unroll
-        for (int c = 0; c < kF; ++c) o[c] = fma(wsm[(c * kF + ci) * kTaps + d], a, o[c]);
+        for (int c2 = 0; c2 < kF / 2; ++c2) {
+          const double2 w2 = wd[ci * (kF / 2) + c2];
+          o[2 * c2] = fma(w2.x, a, o[2 * c2]);
+          o[2 * c2 + 1] = fma(w2.y, a, o[2 * c2 + 1]);
+        }
       }
     }
   };
@@ -463,10 +473,10 @@ __global__ void __launch_bounds__(kF64Threads) rescnn_f64_kernel(const double* _
   for (int64_t cfg0 = (int64_t)blockIdx.x * G; cfg0 < B; cfg0 += (int64_t)gridDim.x * G) {
     const int64_t cfg = cfg0 + g;
     const bool live = active && cfg < B;
-    double* A = bufA + (size_t)g * N * kF;
-    double* Bv = bufB + (size_t)g * N * kF;
+    double* A = bufA + (size_t)g * N * kFS;
+    double* Bv = bufB + (size_t)g * N * kFS;
     double h[kF], t[kF];
-    if (live) A[p * kF] = ((bits[cfg * words + (p >> 5)] >> (p & 31)) & 1u) ? -1.0 : 1.0;
+    if (live) A[p * kFS] = ((bits[cfg * words + (p >> 5)] >> (p & 31)) & 1u) ? -1.0 : 1.0;
     __syncthreads();
     // embedding (one input channel)
     if (live) {
@@ -475,7 +485,7 @@ __global__ void __launch_bounds__(kF64Threads) rescnn_f64_kernel(const double* _
 #pragma unroll
       for (int c = 0; c < kF; ++c) h[c] = b0[c];
       for (int d = 0; d < kTaps; ++d) {
-        const double sv = A[nb[d] * kF];
+        const double sv = A[nb[d] * kFS];
 #pragma unroll
         for (int c = 0; c < kF; ++c) h[c] = fma(w0[c * kTaps + d], sv, h[c]);
       }
@@ -492,13 +502,13 @@ __global__ void __launch_bounds__(kF64Threads) rescnn_f64_kernel(const double* _
       if (live) {
         ln(h, gm, be, t);
 #pragma unroll
-        for (int c = 0; c < kF; ++c) A[p * kF + c] = gelu64(t[c]);
+        for (int c = 0; c < kF; ++c) A[p * kFS + c] = gelu64(t[c]);
       }
       __syncthreads();
       if (live) {
         conv(A, ba, t);
 #pragma unroll
-        for (int c = 0; c < kF; ++c) Bv[p * kF + c] = gelu64(t[c]);
+        for (int c = 0; c < kF; ++c) Bv[p * kFS + c] = gelu64(t[c]);
       }
       stage(wb);
       if (live) {
@@ -599,7 +609,7 @@ cudaError_t rescnn_f64_launch(const double* theta, int L, int n_res, const uint3
   const int N = L * L;
   if (N > kF64Threads) return cudaErrorInvalidValue;
   const int G = kF64Threads / N;
-  const size_t smem = ((size_t)kF * kF * kTaps + 2ull * G * N * kF) * sizeof(double);
+  const size_t smem = ((size_t)kF * kF * kTaps + 2ull * G * N * kFS) * sizeof(double);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute((const void*)&rescnn_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
