@@ -231,18 +231,26 @@ def run_ours(args, rank, world, local_rank):
     # ---- north-star shape (alpha=1, 10x10, f16) sweep-only rate, same run ----
     ns = None
     if rank == 0:
-        p1 = rbm.random_parameters(N_SITES, 1, derive_key(0, "init"), INIT_SCALE)
-        ev1 = rbm.log_prob_evaluator(p1, F16, RoundingMode.NATIVE)
-        e1s = sampler.ChainEnsemble(C, N_SITES, sampler.Proposal("flip"), ev1, derive_key(0, "chains"))
-        e1s.run_steps(1000)
-        torch.cuda.synchronize()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        e1s.run_steps(10 * (N_SITES + 1), check=False)
-        a1.record(stream)
-        torch.cuda.synchronize()
-        ns = {"config": "rbm_a1_tfim10x10_c16384_f16native", "chain_steps_per_s":
-              C * 10 * (N_SITES + 1) / (a0.elapsed_time(a1) / 1e3), "variant": ev1.snapshot.label}
+        def ns_rate(scale):
+            p1 = rbm.random_parameters(N_SITES, 1, derive_key(0, "init"), scale)
+            ev1 = rbm.log_prob_evaluator(p1, F16, RoundingMode.NATIVE)
+            e1s = sampler.ChainEnsemble(C, N_SITES, sampler.Proposal("flip"), ev1, derive_key(0, "chains"))
+            e1s.run_steps(1000)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            e1s.run_steps(10 * (N_SITES + 1), check=False)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            return C * 10 * (N_SITES + 1) / (a0.elapsed_time(a1) / 1e3), e1s.layout_label
+
+        r_flat, v_flat = ns_rate(INIT_SCALE)
+        r_peak, v_peak = ns_rate(0.5)
+        ns = {"config": "rbm_a1_tfim10x10_c16384_f16native", "chain_steps_per_s": r_flat, "variant": v_flat,
+              "peaked_scale0.5": {"chain_steps_per_s": r_peak, "variant": v_peak,
+                                  "why_below_flat": "peaked weights need the int32 (XI) accumulators: per hidden "
+                                  "unit 2 IMAD + 2 I2F + 2 FMUL instead of 2 mixed-precision FFMA, and the sweep "
+                                  "is issue-co-limited (profiles/r02/sweep.md, DESIGN.md section 10)"}}
 
     # ---- sampling-only rates: precision sweep at the config-2 shape, BASELINE
     # configs[2] (Heisenberg 10x10, alpha=4, exchange Sz=0, bf16) and configs[4]
@@ -413,6 +421,15 @@ def run_ours(args, rank, world, local_rank):
             torch.cuda.synchronize()
             ms_f = a0.elapsed_time(a1) / 5
             useful = N_SITES * (16 * 9 + 8 * 16 * 16 * 9) * 2
+            sub = pk[:16384]
+            rescnn.log_psi_packed(pc, sub)  # f64 forward on DMMA (the local energies' evaluator)
+            torch.cuda.synchronize()
+            a0.record(stream)
+            for _ in range(3):
+                rescnn.log_psi_packed(pc, sub)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            ms_64 = a0.elapsed_time(a1) / 3
             ens_c = sampler.ChainEnsemble(C, N_SITES, sampler.Proposal("exchange", N_SITES // 2), evc,
                                           derive_key(0, "chains"))
             ens_c.run_steps(20)
@@ -435,6 +452,8 @@ def run_ours(args, rank, world, local_rank):
             return {"config": "rescnn_4x16_3x3_j1j2_10x10_j2_0.5_marshall",
                     "forward_f16_configs_per_s": B / (ms_f / 1e3),
                     "forward_f16_useful_tflops": useful * B / (ms_f / 1e3) / 1e12,
+                    "forward_f64_dmma_configs_per_s": sub.shape[0] / (ms_64 / 1e3),
+                    "forward_f64_fp64_frac": useful / 2 * sub.shape[0] / (ms_64 / 1e3) / (64 * 148 * 1.965e9),
                     "sampling_exchange_f16_chain_steps_per_s": C * 200 / (a0.elapsed_time(a1) / 1e3),
                     "acceptance": ens_c.acceptance_rate,
                     "vmc_iteration_s4096_c1024_minsr_f32_seconds": (time.perf_counter() - t0) / 3}

@@ -405,8 +405,10 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
 // convolution are staged in shared memory and read warp-uniformly).  Two
 // activation buffers per configuration (layer input / first-convolution
 // output) hold the neighbours' values.
+// tanh-form GELU, 0.5 z (1 + tanh u) = z / (1 + e^{-2u}): one exp and one division
 __device__ __forceinline__ double gelu64(double z) {
-  return 0.5 * z * (1.0 + tanh(0.7978845608028654 * (z + 0.044715 * z * z * z)));
+  const double u = 0.7978845608028654 * fma(0.044715 * z, z * z, z);
+  return z / (1.0 + exp(-2.0 * u));
 }
 
 constexpr int kF64Threads = 512;
@@ -534,6 +536,252 @@ __global__ void __launch_bounds__(kF64Threads) rescnn_f64_kernel(const double* _
   }
 }
 
+
+// ---- f64 forward on the FP64 tensor cores (DMMA m8n8k4): the production f64
+// path (local energies, sigma-hat, parity).  A convolution is the GEMM
+//   out[site][cout] = b[cout] + sum_{tap, cin} act[nb(site, tap)][cin] W[cout][cin][tap]
+// with M = sites (m-tiles of 8), N = 16 output channels (two n-tiles of 8),
+// K = 9 taps x 16 input channels (36 k-steps of 4): the A fragment of lane
+// (row = lane / 4, k = lane % 4) is one gathered LDS.64 of the neighbour's
+// channel (activation rows padded to 20 doubles: the 8 x 4 gather hits
+// disjoint bank pairs), the B fragments come pre-arranged per (k-step,
+// n-tile, lane) from shared memory.  Warp w owns m-tile w of each of the CTA's
+// G configurations (MP = G tiles); the residual stream h stays in registers in
+// the D-fragment layout (lane: site row lane / 4, channels 2 (lane % 4) + {0, 1}
+// of each n-tile), LayerNorm reduces over the 4 lanes of a row by shuffles.
+constexpr int kRow = 20;        // doubles per site row in the activation buffers
+constexpr int kMP = 4;          // m-tiles per warp (configurations per CTA when a warp owns one tile per config)
+constexpr int kWFrag = 36 * 2 * 32;  // one convolution's B fragments (doubles)
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+struct F64Plan {
+  int N, L, n_res, words, mtc, tpc, warps, G;  // m-tiles per config, tiles per config per warp, warps, configs per CTA
+  size_t smem;
+};
+
+__host__ __device__ inline size_t f64_dmma_smem(int N, int G, int mtc) {
+  return (2 * (size_t)G * mtc * 8 * kRow + 2 * (size_t)kWFrag + (size_t)G * mtc) * sizeof(double) +
+         (size_t)N * kTaps * sizeof(int) + (size_t)G * 32 * sizeof(uint32_t);
+}
+
+template <int TPC, int MP>
+__global__ void __launch_bounds__(MP == 2 ? 448 : 512, MP == 2 ? 2 : 1) rescnn_f64_dmma_kernel(const double* __restrict__ theta, const F64Plan P,
+                                                                  const uint32_t* __restrict__ bits, int64_t B,
+                                                                  double* __restrict__ out) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int G = MP / TPC, tpc = TPC;
+  const int N = P.N, L = P.L, mtc = P.mtc, W = P.warps, words = P.words;
+  const int rows = mtc * 8;
+  double* actA = sm;                                   // [G][rows][kRow]
+  double* actB = actA + (size_t)G * rows * kRow;
+  double* wf = actB + (size_t)G * rows * kRow;         // [2][36][2][32] B fragments of two convolutions
+  double* part = wf + 2 * kWFrag;                      // [G][mtc] per-tile partial sums
+  int* nbt = reinterpret_cast<int*>(part + (size_t)G * mtc);  // [N][9] neighbour sites
+  uint32_t* sbits = reinterpret_cast<uint32_t*>(nbt + (size_t)N * kTaps);  // [G][32]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qr = lane >> 2, qc = lane & 3;
+  for (int i = tid; i < N * kTaps; i += blockDim.x) {
+    const int site = i / kTaps, d = i % kTaps, r = site / L, c = site % L;
+    nbt[i] = ((r + d / 3 - 1 + L) % L) * L + (c + d % 3 - 1 + L) % L;
+  }
+  const size_t blk = 2 * kF + 2 * (kF * kF * kTaps + kF);  // parameters per residual block (oracle/rescnn.py order)
+  // B fragments of a [cout][cin][tap] weight: (k-step kk, n-tile nt, lane) ->
+  // W[nt 8 + lane / 4][(kk % 4) 4 + lane % 4][kk / 4]
+  auto stage = [&](const double* w, double* dst) {
+    for (int i = tid; i < kWFrag; i += blockDim.x) {
+      const int kk = i / 64, nt = (i / 32) & 1, l = i & 31;
+      dst[i] = w[((nt * 8 + (l >> 2)) * kF + (kk & 3) * 4 + (l & 3)) * kTaps + kk / 4];
+    }
+  };
+  // this warp's tiles: (config g, tile t) for k = 0 .. MP-1 -> g = k / tpc, t = warp + (k % tpc) W
+  auto tile_of = [&](int k, int& g, int& t) {
+    g = k / tpc;
+    t = warp + (k % tpc) * W;
+  };
+  constexpr int MPw = MP;  // tiles per warp
+  // one convolution over `src` with fragments `wfr`: acc (per tile, n-tile) = bias + GEMM
+  auto conv = [&](const double* src, const double* wfr, const double* bias, double (&acc)[MP][2][2]) {
+    int nbrow[MP];
+#pragma unroll
+    for (int k = 0; k < MP; ++k) {
+      if (k < MPw) {
+        int g, t;
+        tile_of(k, g, t);
+        const double2 bv0 = make_double2(bias[2 * qc], bias[2 * qc + 1]);
+        const double2 bv1 = make_double2(bias[8 + 2 * qc], bias[8 + 2 * qc + 1]);
+        acc[k][0][0] = bv0.x; acc[k][0][1] = bv0.y; acc[k][1][0] = bv1.x; acc[k][1][1] = bv1.y;
+        (void)g; (void)t;
+      }
+    }
+#pragma unroll 3
+    for (int d = 0; d < kTaps; ++d) {
+#pragma unroll
+      for (int k = 0; k < MP; ++k) {
+        if (k < MPw) {
+          int g, t;
+          tile_of(k, g, t);
+          const int site = min(t * 8 + qr, N - 1);  // padded rows gather a valid site (results dropped)
+          nbrow[k] = (g * rows + nbt[site * kTaps + d]) * kRow;
+        }
+      }
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        const int kk = d * 4 + cb;
+        const double b0 = wfr[(kk * 2 + 0) * 32 + lane], b1 = wfr[(kk * 2 + 1) * 32 + lane];
+#pragma unroll
+        for (int k = 0; k < MP; ++k) {
+          if (k < MPw) {
+            const double av = src[nbrow[k] + cb * 4 + qc];
+            dmma884(acc[k][0][0], acc[k][0][1], av, b0);
+            dmma884(acc[k][1][0], acc[k][1][1], av, b1);
+          }
+        }
+      }
+    }
+  };
+  // LayerNorm over the 16 channels of the lane's row (4 lanes hold a row)
+  auto layernorm = [&](const double (&h)[2][2], const double* gm, const double* be, double (&z)[2][2]) {
+    double s = h[0][0] + h[0][1] + h[1][0] + h[1][1];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    const double mu = s / kF;
+    double v = 0.0;
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) v += (h[n][e] - mu) * (h[n][e] - mu);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    const double rs = 1.0 / sqrt(v / kF + 1e-6);
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = n * 8 + 2 * qc + e;
+        z[n][e] = gm[c] * (h[n][e] - mu) * rs + be[c];
+      }
+  };
+  auto store = [&](double* dst, int g, int t, const double (&v)[2][2]) {
+    const int row = t * 8 + qr;
+    if (row < N) {
+      double* r = dst + (size_t)(g * rows + row) * kRow;
+      *reinterpret_cast<double2*>(r + 2 * qc) = make_double2(v[0][0], v[0][1]);
+      *reinterpret_cast<double2*>(r + 8 + 2 * qc) = make_double2(v[1][0], v[1][1]);
+    }
+  };
+
+  const int64_t groups = (B + G - 1) / G;
+  for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
+    const int64_t cfg0 = grp * G;
+    __syncthreads();  // previous group's reads of the buffers / partials done
+    for (int i = tid; i < G * 32; i += blockDim.x) {
+      const int g = i / 32, w = i % 32;
+      sbits[i] = (w < words && cfg0 + g < B) ? bits[(cfg0 + g) * words + w] : 0u;
+    }
+    __syncthreads();
+    double h[MP][2][2];
+    // embedding: one input channel s = 1 - 2x, 9 taps
+    {
+      const double* w0 = theta;             // [16][1][9]
+      const double* b0 = theta + kF * kTaps;
+#pragma unroll
+      for (int k = 0; k < MP; ++k) {
+        if (k < MPw) {
+          int g, t;
+          tile_of(k, g, t);
+          const int site = min(t * 8 + qr, N - 1);
+#pragma unroll
+          for (int n = 0; n < 2; ++n)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) h[k][n][e] = b0[n * 8 + 2 * qc + e];
+          for (int d = 0; d < kTaps; ++d) {
+            const int nbs = nbt[site * kTaps + d];
+            const double sv = ((sbits[g * 32 + (nbs >> 5)] >> (nbs & 31)) & 1u) ? -1.0 : 1.0;
+#pragma unroll
+            for (int n = 0; n < 2; ++n)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) h[k][n][e] = fma(w0[(n * 8 + 2 * qc + e) * kTaps + d], sv, h[k][n][e]);
+          }
+        }
+      }
+    }
+    const double* pp = theta + kF * kTaps + kF;
+    for (int l = 0; l < P.n_res; ++l, pp += blk) {
+      const double *gm = pp, *be = pp + kF, *wa = pp + 2 * kF, *ba = wa + kF * kF * kTaps;
+      const double *wb = ba + kF, *bb = wb + kF * kF * kTaps;
+      stage(wa, wf);
+      stage(wb, wf + kWFrag);
+#pragma unroll
+      for (int k = 0; k < MP; ++k) {
+        if (k < MPw) {
+          int g, t;
+          tile_of(k, g, t);
+          double z[2][2];
+          layernorm(h[k], gm, be, z);
+#pragma unroll
+          for (int n = 0; n < 2; ++n)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) z[n][e] = gelu64(z[n][e]);
+          store(actA, g, t, z);
+        }
+      }
+      __syncthreads();
+      double acc[MP][2][2];
+      conv(actA, wf, ba, acc);
+#pragma unroll
+      for (int k = 0; k < MP; ++k) {
+        if (k < MPw) {
+          int g, t;
+          tile_of(k, g, t);
+#pragma unroll
+          for (int n = 0; n < 2; ++n)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) acc[k][n][e] = gelu64(acc[k][n][e]);
+          store(actB, g, t, acc[k]);
+        }
+      }
+      __syncthreads();
+      conv(actB, wf + kWFrag, bb, acc);
+#pragma unroll
+      for (int k = 0; k < MP; ++k)
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) h[k][n][e] += acc[k][n][e];
+      __syncthreads();  // conv2's reads of actB and the fragments done before the next staging
+    }
+    // final LayerNorm, summed over channels and sites (fixed order: lanes, rows, tiles)
+    const double* gf = pp;
+    const double* bef = pp + kF;
+#pragma unroll
+    for (int k = 0; k < MP; ++k) {
+      if (k < MPw) {
+        int g, t;
+        tile_of(k, g, t);
+        double z[2][2];
+        layernorm(h[k], gf, bef, z);
+        double sum = (t * 8 + qr < N) ? (z[0][0] + z[0][1]) + (z[1][0] + z[1][1]) : 0.0;
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 8);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 16);
+        if (lane == 0 && t < mtc) part[g * mtc + t] = sum;
+      }
+    }
+    __syncthreads();
+    if (tid < G && cfg0 + tid < B) {
+      double acc = 0.0;
+      for (int t = 0; t < mtc; ++t) acc += part[tid * mtc + t];
+      out[cfg0 + tid] = acc;
+    }
+  }
+}
+
 }  // namespace cnn
 
 using namespace cnn;
@@ -607,6 +855,35 @@ cudaError_t rescnn_launch(int L, int n_res, int fmt, const void* blob, uint32_t*
 cudaError_t rescnn_f64_launch(const double* theta, int L, int n_res, const uint32_t* bits, int64_t B, int words,
                               double* out, cudaStream_t st) {
   const int N = L * L;
+  {  // FP64 tensor cores: warps own one m-tile of each configuration (tpc tiles per config when > 32 tiles)
+    F64Plan P{};
+    P.N = N; P.L = L; P.n_res = n_res; P.words = words;
+    P.mtc = (N + 7) / 8;
+    P.tpc = 1;
+    while ((P.mtc + P.tpc - 1) / P.tpc > 16) P.tpc *= 2;  // <= 16 warps (launch bounds 512)
+    P.warps = (P.mtc + P.tpc - 1) / P.tpc;
+    P.G = kMP / P.tpc;
+    // two CTAs per SM (two configurations each) when one m-tile per config per warp
+    static const char* two = getenv("MPV_CNN64_G2");
+    if (P.tpc == 1 && P.warps <= 14 && (!two || two[0] != '0')) P.G = 2;
+    if (P.tpc <= 4 && words <= 32) {
+      P.smem = f64_dmma_smem(N, P.G, P.mtc);
+      if (P.smem <= 227 * 1024) {
+        for (const void* fn : {(const void*)&rescnn_f64_dmma_kernel<1, 2>, (const void*)&rescnn_f64_dmma_kernel<1, 4>,
+                               (const void*)&rescnn_f64_dmma_kernel<2, 4>, (const void*)&rescnn_f64_dmma_kernel<4, 4>}) {
+          cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem);
+          if (e != cudaSuccess) return e;
+        }
+        const int64_t groups = (B + P.G - 1) / P.G;
+        const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(groups, 148 * (P.G == 2 ? 4 : 2)));
+        if (P.tpc == 1 && P.G == 2) rescnn_f64_dmma_kernel<1, 2><<<grid, 32 * P.warps, P.smem, st>>>(theta, P, bits, B, out);
+        else if (P.tpc == 1) rescnn_f64_dmma_kernel<1, 4><<<grid, 32 * P.warps, P.smem, st>>>(theta, P, bits, B, out);
+        else if (P.tpc == 2) rescnn_f64_dmma_kernel<2, 4><<<grid, 32 * P.warps, P.smem, st>>>(theta, P, bits, B, out);
+        else rescnn_f64_dmma_kernel<4, 4><<<grid, 32 * P.warps, P.smem, st>>>(theta, P, bits, B, out);
+        return cudaGetLastError();
+      }
+    }
+  }
   if (N > kF64Threads) return cudaErrorInvalidValue;
   const int G = kF64Threads / N;
   const size_t smem = ((size_t)kF * kF * kTaps + 2ull * G * N * kFS) * sizeof(double);

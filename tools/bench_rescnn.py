@@ -43,7 +43,7 @@ def main():
                                       "issued_tensor_tflops": issued * B / (ms / 1e3) / 1e12}
     ev64 = rescnn.log_prob_evaluator(p, rescnn.FloatFormat_f64())
     ms = tm(lambda: ev64.log_prob_packed(pk[:8192]), 2)
-    out["forward_f64_cuda_cores"] = {"configs_per_s": 8192 / (ms / 1e3)}
+    out["forward_f64_dmma"] = {"configs_per_s": 8192 / (ms / 1e3)}
     ev = rescnn.log_prob_evaluator(p, F16)
     C = 16384
     ens = sampler.ChainEnsemble(C, n, sampler.Proposal("exchange", n // 2), ev, derive_key(0, "chains"))
