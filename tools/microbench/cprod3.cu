@@ -80,13 +80,9 @@ void run(const char* name, int nsm, double* out, long long* cyc, int bps, int th
 int main() {
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   double* out; long long* cyc; cudaMalloc(&out, nsm * 4 * 1024 * 8); cudaMalloc(&cyc, nsm * 4 * 8);
+  // (the complex-recurrence modes are measured with their shared-memory loads in cprod2.cu)
   run<0, 4>("16 independent DFMA chains", nsm, out, cyc, 2, 416);
-  run<1, 4>("u + P(1+u) as in energy.cuh", nsm, out, cyc, 2, 416);
-  run<1, 4>("u + P(1+u) as in energy.cuh", nsm, out, cyc, 1, 416);
-  run<1, 8>("u + P(1+u) as in energy.cuh", nsm, out, cyc, 2, 416);
-  run<2, 4>("f = 1+u, P f (9 ops)", nsm, out, cyc, 2, 416);
-  run<3, 4>("P += P u, products first", nsm, out, cyc, 2, 416);
-  run<4, 4>("u chains only", nsm, out, cyc, 2, 416);
-  run<1, 4>("u + P(1+u), 4 CTAs x 128", nsm, out, cyc, 4, 128);
+  run<0, 4>("16 independent DFMA chains", nsm, out, cyc, 1, 1024);
+  run<0, 4>("16 independent DFMA chains", nsm, out, cyc, 4, 256);
   return 0;
 }
