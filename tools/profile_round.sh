@@ -5,7 +5,7 @@
 R=${1:-r02}
 O=gpurun_out/$R
 mkdir -p $O
-for b in pipes fp64lat dmma cprod2; do timeout 120 ./tools/microbench/$b > $O/micro_$b.txt 2>&1; done
+for b in pipes fp64lat dmma cprod2 cprod3; do timeout 120 ./tools/microbench/$b > $O/micro_$b.txt 2>&1; done
 SHORT="--no-cpu-baseline --no-extras --no-vmc"
 python bench.py --steps 2 --warmup 3 $SHORT > $O/bench_short.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
@@ -19,7 +19,9 @@ cap() {  # name, kernel regex, skip, count, command...
   rm -f $O/$name.ncu-rep
 }
 cap sweep sweep_kernel 3 1 python bench.py --steps 1 --warmup 3 $SHORT
-cap energy energy_kernel 0 1 python tools/bench_energy.py
+cap energy energy_kernel 0 1 python tools/bench_energy.py tfim
+cap energy_heis energy_kernel 0 1 python tools/bench_energy.py heis
+cap rescnn_f64 rescnn_f64_dmma 0 1 python tools/bench_rescnn_f64.py
 cap rescnn rescnn_kernel 0 1 python tools/bench_rescnn.py
 cap ld "ld_ov_kernel|ld_ohu_kernel" 1 2 python tools/bench_sr_cg.py
 cap sweep_f32 sweep_kernel 1 1 python tools/bench_sweep_one.py f32
