@@ -799,6 +799,8 @@ int mpv_local_energies_ex(int N, int M, const double* a, const double* b, const 
   const Cfg cfgs[] = {
       {4, 16, 4, 448, MPV_EK(4, 4, 448, 2)},  // 2 blocks/SM, 72 regs (T <= 112)
       {8, 16, 8, 256, MPV_EK(8, 8, 256, 2)},  // 2 blocks/SM, 128 regs (T <= 128)
+      {4, 16, 4, 800, MPV_EK(4, 4, 800, 1)},  // 1 block/SM of up to 25 warps, 80 regs (T <= 200)
+      {4, 8, 4, 800, MPV_EK(4, 4, 800, 1)},   // 8 samples per block (T <= 400: J1-J2)
       {8, 16, 4, 512, MPV_EK(8, 4, 512, 1)},
       {8, 16, 8, 512, MPV_EK(8, 8, 512, 1)},
       {8, 8, 4, 512, MPV_EK(8, 4, 512, 1)},

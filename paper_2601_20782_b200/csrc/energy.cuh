@@ -593,8 +593,8 @@ __global__ void __launch_bounds__(TMAX, MINB) energy_kernel(const EnergyArgs a, 
       return dg;
     };
     if (active && slow) {
-#pragma unroll 1
-      for (int j = 0; j < ST; ++j) {  // rolled: one call site, results straight to R
+#pragma unroll
+      for (int j = 0; j < ST; ++j) {  // unrolled (sidx stays in registers); slow_ratio is not inlined
         if (!((live >> j) & 1u)) continue;
         const int s = sidx[j];
         double2 v = make_double2(0.0, 0.0);

@@ -137,3 +137,28 @@ def test_many_terms_launch_configs(cuda, spec, alpha):
     want = port.local_energies(port.Params(p.a, p.b, p.w), ham, spec.lattice.bond_array(), spec.j,
                                getattr(spec, "h", 0.0), bits)
     assert np.max(np.abs(eps - want) / np.maximum(1, np.abs(want))) < 1e-10
+
+
+def test_bench_shapes_against_oracle(cuda):
+    """The energy launches of the bench's configs[2] (Heisenberg 10x10, alpha=4:
+    200 bonds, 400 hidden units; compacted 4-sample units, one block of up to 25
+    warps per SM) and configs[3]-shape J1-J2 (400 bonds, alpha=1: 8-sample
+    blocks) against the oracle.  J1-J2 is linear in the couplings: the oracle
+    value is the sum of two Heisenberg evaluations over the J1 and J2 bonds."""
+    from paper_2601_20782_b200.hamiltonians import J1J2Spec
+
+    lat = LatticeSpec.square(10)
+    rng = np.random.default_rng(11)
+    bits = np.zeros((37, 100), dtype=np.uint8)
+    np.put_along_axis(bits, np.argsort(rng.random((37, 100)), axis=1)[:, :50], 1, axis=1)
+    bits[-1] = rng.integers(0, 2, size=100)  # one row off the Sz = 0 sector
+    p4 = rbm.random_parameters(100, 4, derive_key(5, "heis-a4"), 0.05)
+    eps = vmc.local_energies(HeisenbergSpec(lat, 1.0), rbm.log_psi_evaluator(p4), bits)
+    want = port.local_energies(port.Params(p4.a, p4.b, p4.w), "heisenberg", lat.bond_array(), 1.0, 0.0, bits)
+    assert np.max(np.abs(eps - want) / np.maximum(1, np.abs(want))) < 1e-10
+    p1 = rbm.random_parameters(100, 1, derive_key(5, "j1j2-a1"), 0.05)
+    eps = vmc.local_energies(J1J2Spec(lat, 1.0, 0.5), rbm.log_psi_evaluator(p1), bits)
+    pp = port.Params(p1.a, p1.b, p1.w)
+    want = (port.local_energies(pp, "heisenberg", lat.bond_array(), 1.0, 0.0, bits)
+            + port.local_energies(pp, "heisenberg", lat.next_nearest_bonds(), 0.5, 0.0, bits))
+    assert np.max(np.abs(eps - want) / np.maximum(1, np.abs(want))) < 1e-10
