@@ -315,8 +315,85 @@ def torch_log_psi(theta, spins, L: int, n_res: int):
     return ln(h, p["gf"], p["bef"]).sum(dim=(1, 2, 3))
 
 
-def log_derivatives(params: ResCnnParameters, packed, chunk: int = 1024):
-    """O[s] = d log psi(x_s) / d theta (U, P) f64 on the device."""
+def log_derivatives(params: ResCnnParameters, packed):
+    """O[s] = d log psi(x_s) / d theta (U, P) f64 on the device.
+
+    Per-sample gradients from ONE batched backward: the samples are independent,
+    so d(sum_s log psi_s)/d(output of a layer)[s] is sample s's own output
+    gradient; each parametric layer's per-sample parameter gradient is then a
+    contraction over the lattice sites of that output gradient with the
+    layer's input (convolution: the unfolded 3x3 neighbourhoods, one batched
+    f64 GEMM; bias: a site sum; LayerNorm gain/shift: sums of dy * x_hat and
+    dy).  Equal to the per-sample autograd (`_log_derivatives_vmap`) to f64
+    rounding (tests/test_gpu_rescnn.py)."""
+    import torch
+    import torch.nn.functional as tf
+
+    dev = packed.device
+    L, n, n_res = params.L, params.n_visible, params.n_res
+    sites = torch.arange(n, device=dev)
+    bits = ((packed.view(torch.int32)[:, sites // 32] >> (sites % 32)) & 1).to(torch.float64)
+    B = bits.shape[0]
+    F = FILTERS
+    theta = torch.from_numpy(params.theta).to(dev)
+    p, k = {}, 0
+    for name, shape in param_layout(n_res):
+        size = int(np.prod(shape))
+        p[name] = theta[k:k + size].reshape(shape)
+        k += size
+    convs, lns = {}, {}  # name -> (padded input, output); name -> (x_hat, output)
+
+    def conv(h, wn, bn):
+        hp = tf.pad(h, (1, 1, 1, 1), mode="circular")
+        w = p[wn]
+        o = tf.conv2d(hp, w.reshape(w.shape[0], w.shape[1], 3, 3), p[bn])
+        convs[wn] = (hp, o)
+        return o
+
+    def ln(h, gn, bn):
+        mu = h.mean(dim=1, keepdim=True)
+        var = ((h - mu) ** 2).mean(dim=1, keepdim=True)
+        xh = (h - mu) / torch.sqrt(var + 1e-6)
+        y = p[gn][None, :, None, None] * xh + p[bn][None, :, None, None]
+        lns[gn] = (xh.detach(), y)
+        return y
+
+    with torch.enable_grad(), torch.backends.cudnn.flags(enabled=True, deterministic=True, benchmark=False):
+        spins = (1.0 - 2.0 * bits).reshape(B, 1, L, L).requires_grad_(True)  # graph root
+        h = conv(spins, "w0", "b0")
+        for i in range(n_res):
+            u = tf.gelu(ln(h, f"g{i}", f"be{i}"), approximate="tanh")
+            v = tf.gelu(conv(u, f"w{i}a", f"b{i}a"), approximate="tanh")
+            h = h + conv(v, f"w{i}b", f"b{i}b")
+        total = ln(h, "gf", "bef").sum()
+        outs = [convs[k_][1] for k_ in convs] + [lns[k_][1] for k_ in lns]
+        grads = torch.autograd.grad(total, outs)
+    go = dict(zip(list(convs) + list(lns), grads))
+    o = torch.empty((B, n_params(n_res)), dtype=torch.float64, device=dev)
+    k = 0
+    for name, shape in param_layout(n_res):
+        size = int(np.prod(shape))
+        dst = o[:, k:k + size]
+        if name.startswith("w"):
+            hp, _ = convs[name]
+            cin = hp.shape[1]                                  # 3x3 neighbourhoods as a strided view, one copy
+            unf = hp.detach().unfold(2, 3, 1).unfold(3, 3, 1).permute(0, 1, 4, 5, 2, 3).reshape(B, cin * 9, L * L)
+            g = go[name].reshape(B, F, L * L)                  # (B, Cout, L * L)
+            dst.copy_(torch.bmm(g, unf.transpose(1, 2)).reshape(B, size))
+        elif name.startswith("b") and not name.startswith("be"):
+            dst.copy_(go["w" + name[1:]].sum(dim=(2, 3)))      # conv bias: site sum
+        elif name.startswith("g"):
+            xh, _ = lns[name]
+            dst.copy_((go[name] * xh).sum(dim=(2, 3)))         # LN gain
+        else:                                                  # LN shift be{i} / bef
+            gname = "g" + name[2:] if name != "bef" else "gf"
+            dst.copy_(go[gname].sum(dim=(2, 3)))
+        k += size
+    return o
+
+
+def _log_derivatives_vmap(params: ResCnnParameters, packed, chunk: int = 1024):
+    """Per-sample autograd (torch.func vmap(grad)): the test reference of log_derivatives."""
     import torch
     from torch.func import grad, vmap
 

@@ -182,6 +182,20 @@ def test_mh_exchange_compacted_equals_full_step(cuda):
     np.testing.assert_array_equal(a.log_probs, ev(a.bits))
 
 
+def test_log_derivatives_equal_per_sample_autograd(cuda):
+    """The one-backward per-sample gradients equal torch.func vmap(grad) of the
+    torch restatement (the reference of the construction) to f64 rounding."""
+    L, n_res = 6, 2
+    p = _params(L, n_res, seed=41, scale=0.6)
+    bits = _bits(50, L * L, 9)
+    packed = torch.from_numpy(pack_bits(bits).view(np.int32)).to(cuda)
+    fast = rescnn.log_derivatives(p, packed)
+    ref = rescnn._log_derivatives_vmap(p, packed)
+    assert fast.shape == ref.shape == (50, rescnn.n_params(n_res))
+    err = (fast - ref).abs().max().item()
+    assert err <= 1e-11 * max(1.0, ref.abs().max().item()), err
+
+
 def test_log_derivatives_match_finite_differences(cuda):
     """O = d log psi / d theta (torch autograd over the torch restatement) against
     central differences of the device f64 forward, and the torch restatement's
