@@ -251,6 +251,7 @@ def local_energies_packed(spec, params: ResCnnParameters, packed, device=None):
         conn = (packed.to(torch.int64)[:, None, :] ^ mask[None]).reshape(B * N, words)
         owner = torch.arange(B, device=dev).repeat_interleave(N)
         coef = torch.full((B * N,), float(spec.h), dtype=torch.float64, device=dev)
+        slot = (owner, sites.repeat(B))
     elif isinstance(spec, (HeisenbergSpec, J1J2Spec)):
         b_np, jb_np, cf_np = spec.couplings()
         bonds = torch.from_numpy(b_np).to(dev)
@@ -266,13 +267,17 @@ def local_energies_packed(spec, params: ResCnnParameters, packed, device=None):
         conn = packed.to(torch.int64)[s_idx] ^ mask
         owner = s_idx
         coef = cf[b_idx].to(torch.float64)
+        slot = (s_idx, b_idx)  # each ratio's (sample, bond) cell: a fixed-order row sum below
     else:
         raise TypeError(f"unknown Hamiltonian spec {type(spec).__name__}")
     conn32 = conn.to(torch.int32).contiguous() if conn.numel() else torch.empty((0, words), dtype=torch.int32,
                                                                                      device=dev)
     lpc = log_psi_packed(params, conn32, dev)
     ratio = torch.exp(lpc - lp0[owner]) * coef
-    off = torch.zeros(B, dtype=torch.float64, device=dev).index_add_(0, owner, ratio)
+    # (sample, term) matrix summed along rows: a fixed summation order (no atomics)
+    cells = torch.zeros((B, N if isinstance(spec, TfimSpec) else bonds.shape[0]), dtype=torch.float64, device=dev)
+    cells[slot] = ratio
+    off = cells.sum(dim=1)
     eps = diag + off
     return torch.complex(eps, torch.zeros_like(eps))
 
@@ -280,9 +285,10 @@ def local_energies_packed(spec, params: ResCnnParameters, packed, device=None):
 # ---------------------------------------------------------------------------
 # Training (BASELINE configs[3]: "minSR in f32, chain sharding").  Sampling
 # uses the fused tensor-core MH step, local energies the f64 forward; the
-# per-sample log-derivatives O = d log psi / d theta come from torch autograd
-# over a torch restatement of the same network in f64 (vmap of grad; cuDNN
-# convolutions - the gradient statistics stay f32/f64, north_star (4)), and
+# per-sample log-derivatives O = d log psi / d theta come from one batched
+# torch autograd backward over a torch restatement of the same network in f64
+# plus per-layer site contractions (cuDNN / cuBLAS - the gradient statistics
+# stay f32/f64, north_star (4)), and
 # the SR step is solved in sample space (minSR) in f32 or f64, sharded.
 # ---------------------------------------------------------------------------
 
