@@ -231,6 +231,7 @@ template <int FMT> struct Acc<FMT, MPV_ACC_X1> {
     return d > 0 ? H::kOne : (d < 0 ? H::kMinusOne : (uint16_t)0);
   }
   __device__ __forceinline__ void init(Entry b) { re = H::lo(b); im = H::hi(b); }
+  __device__ __forceinline__ void value(float sc, float& xr, float& xi) const { xr = re; xi = im; }
   __device__ __forceinline__ void add(Entry e, Sign d) {
     re = H::fma_lo(e, d, re);
     im = H::fma_hi(e, d, im);
@@ -260,6 +261,7 @@ template <int FMT> struct Acc<FMT, MPV_ACC_X2> {
   __device__ __forceinline__ void init(Entry b) {
     hr = H::lo(b.x); hi_ = H::hi(b.x); lr = H::lo(b.y); li = H::hi(b.y);
   }
+  __device__ __forceinline__ void value(float sc, float& xr, float& xi) const { xr = hr + lr; xi = hi_ + li; }
   __device__ __forceinline__ void add(Entry e, Sign d) {
     hr = H::fma_lo(e.x, d, hr); hi_ = H::fma_hi(e.x, d, hi_);
     lr = H::fma_lo(e.y, d, lr); li = H::fma_hi(e.y, d, li);
@@ -285,6 +287,10 @@ template <int FMT> struct Acc<FMT, MPV_ACC_XI> {
   int re, im;
   __device__ __forceinline__ static Sign sign(int d) { return d; }
   __device__ __forceinline__ void init(Entry b) { re = b.x; im = b.y; }
+  __device__ __forceinline__ void value(float sc, float& xr, float& xi) const {
+    xr = __int2float_rn(re) * sc;
+    xi = __int2float_rn(im) * sc;
+  }
   __device__ __forceinline__ void add(Entry e, Sign d) { re += d * e.x; im += d * e.y; }
   __device__ __forceinline__ void prop1(Entry e, Sign d, float sc, float& xr, float& xi) const {
     xr = __int2float_rn(re + d * e.x) * sc;
@@ -305,6 +311,7 @@ template <> struct Acc<MPV_FMT_F32, MPV_ACC_X1> {
   float re, im;
   __device__ __forceinline__ static Sign sign(int d) { return (float)d; }
   __device__ __forceinline__ void init(Entry b) { re = b.x; im = b.y; }
+  __device__ __forceinline__ void value(float sc, float& xr, float& xi) const { xr = re; xi = im; }
   __device__ __forceinline__ void add(Entry e, Sign d) { re = fmaf(e.x, d, re); im = fmaf(e.y, d, im); }
   __device__ __forceinline__ void prop1(Entry e, Sign d, float sc, float& xr, float& xi) const {
     xr = fmaf(e.x, d, re);
@@ -325,6 +332,7 @@ template <> struct Acc<MPV_FMT_F32, MPV_ACC_X2> {
   float hr, hi_, lr, li;
   __device__ __forceinline__ static Sign sign(int d) { return (float)d; }
   __device__ __forceinline__ void init(Entry b) { hr = b.x; hi_ = b.y; lr = b.z; li = b.w; }
+  __device__ __forceinline__ void value(float sc, float& xr, float& xi) const { xr = hr + lr; xi = hi_ + li; }
   __device__ __forceinline__ void add(Entry e, Sign d) {
     hr = fmaf(e.x, d, hr); hi_ = fmaf(e.y, d, hi_); lr = fmaf(e.z, d, lr); li = fmaf(e.w, d, li);
   }
@@ -347,6 +355,7 @@ template <int FMT> struct Acc<FMT, MPV_ACC_F64> {
   double re, im;
   __device__ __forceinline__ static Sign sign(int d) { return (double)d; }
   __device__ __forceinline__ void init(Entry b) { re = b.x; im = b.y; }
+  __device__ __forceinline__ void value(float sc, double& xr, double& xi) const { xr = re; xi = im; }
   __device__ __forceinline__ void add(Entry e, Sign d) { re = fma(e.x, d, re); im = fma(e.y, d, im); }
   __device__ __forceinline__ void prop1(Entry e, Sign d, float sc, double& xr, double& xi) const {
     xr = fma(e.x, d, re);
@@ -702,6 +711,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
     }
     bool dead = isnan(lp);
 
+    A nxt[(PROP == MPV_PROPOSAL_EXCHANGE) ? U : 1];  // exchange: theta after the proposed move
     const uint64_t s0 = stream_state(a.key, (uint64_t)gchain);
     const int64_t count_c = a.sample_base + ((gchain < a.sample_extra) ? 1 : 0);
     const int64_t offset_c =
@@ -778,19 +788,31 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
 #pragma unroll
       for (int u = 0; u + 1 < U; u += 2) {
         Theta xr0, xi0, xr1, xi1;
-        if (PROP == MPV_PROPOSAL_FLIP) {
+        if constexpr (PROP == MPV_PROPOSAL_FLIP) {
           acc[u].prop1(c1[u * G], d, sc, xr0, xi0);
           acc[u + 1].prop1(c1[(u + 1) * G], d, sc, xr1, xi1);
-        } else {
-          acc[u].prop2(c1[u * G], c2[u * G], d, md, sc, xr0, xi0);
-          acc[u + 1].prop2(c1[(u + 1) * G], c2[(u + 1) * G], d, md, sc, xr1, xi1);
+        } else {  // exchange: the proposed theta is kept for the commit (nxt)
+          nxt[u] = acc[u];
+          nxt[u].add(c2[u * G], md);
+          nxt[u].add(c1[u * G], d);
+          nxt[u].value(sc, xr0, xi0);
+          nxt[u + 1] = acc[u + 1];
+          nxt[u + 1].add(c2[(u + 1) * G], md);
+          nxt[u + 1].add(c1[(u + 1) * G], d);
+          nxt[u + 1].value(sc, xr1, xi1);
         }
         E::pair(xr0, xi0, xr1, xi1, h, vmin);
       }
       if constexpr (U & 1) {
         Theta xr, xi;
-        if (PROP == MPV_PROPOSAL_FLIP) acc[U - 1].prop1(c1[(U - 1) * G], d, sc, xr, xi);
-        else acc[U - 1].prop2(c1[(U - 1) * G], c2[(U - 1) * G], d, md, sc, xr, xi);
+        if constexpr (PROP == MPV_PROPOSAL_FLIP) {
+          acc[U - 1].prop1(c1[(U - 1) * G], d, sc, xr, xi);
+        } else {
+          nxt[U - 1] = acc[U - 1];
+          nxt[U - 1].add(c2[(U - 1) * G], md);
+          nxt[U - 1].add(c1[(U - 1) * G], d);
+          nxt[U - 1].value(sc, xr, xi);
+        }
         E::single(xr, xi, h, vmin);
       }
       if constexpr (E::kFix) {
@@ -831,15 +853,15 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
       lp = moved ? lp_new : lp;
       myword ^= moved ? flip : 0u;
       n_acc += accept ? 1 : 0;
-      // commit: the column entries are re-read from shared memory (cheaper than
+      // commit (flip): the column entries are re-read from shared memory (cheaper than
       // keeping U entries live in registers across the evaluation)
-      const Sign dacc = moved ? d : A::sign(0);
+      if constexpr (PROP == MPV_PROPOSAL_FLIP) {
+        const Sign dacc = moved ? d : A::sign(0);
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc[u].add(c1[u * G], dacc);
-      if (PROP == MPV_PROPOSAL_EXCHANGE) {
-        const Sign mdacc = moved ? md : A::sign(0);
+        for (int u = 0; u < U; ++u) acc[u].add(c1[u * G], dacc);
+      } else {  // exchange: the evaluated theta becomes the state (no column re-read)
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc[u].add(c2[u * G], mdacc);
+        for (int u = 0; u < U; ++u) acc[u] = moved ? nxt[u] : acc[u];
       }
       if (s + 1 == next_record) {
         next_record += thin;
