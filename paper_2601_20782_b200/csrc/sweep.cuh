@@ -492,6 +492,9 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
   using Lp = typename E::Lp;
   using Theta = typename std::conditional<VAR == MPV_ACC_F64, double, float>::type;
   constexpr int CPW = 32 / G;
+  // keep each unit's proposed theta in registers and commit it by select
+  // (exchange: no second column read; table beyond shared memory: no L1/L2 re-read)
+  constexpr bool kKeep = (PROP == MPV_PROPOSAL_EXCHANGE) || !SMEM;
   constexpr int SW = (int)(sizeof(A) / sizeof(float));
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -711,7 +714,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
     }
     bool dead = isnan(lp);
 
-    A nxt[(PROP == MPV_PROPOSAL_EXCHANGE) ? U : 1];  // exchange: theta after the proposed move
+    A nxt[kKeep ? U : 1];  // exchange / global table: theta after the proposed move
     const uint64_t s0 = stream_state(a.key, (uint64_t)gchain);
     const int64_t count_c = a.sample_base + ((gchain < a.sample_extra) ? 1 : 0);
     const int64_t offset_c =
@@ -788,7 +791,14 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
 #pragma unroll
       for (int u = 0; u + 1 < U; u += 2) {
         Theta xr0, xi0, xr1, xi1;
-        if constexpr (PROP == MPV_PROPOSAL_FLIP) {
+        if constexpr (PROP == MPV_PROPOSAL_FLIP && kKeep) {  // table in L1/L2: keep theta' for the commit
+          nxt[u] = acc[u];
+          nxt[u].add(c1[u * G], d);
+          nxt[u].value(sc, xr0, xi0);
+          nxt[u + 1] = acc[u + 1];
+          nxt[u + 1].add(c1[(u + 1) * G], d);
+          nxt[u + 1].value(sc, xr1, xi1);
+        } else if constexpr (PROP == MPV_PROPOSAL_FLIP) {
           acc[u].prop1(c1[u * G], d, sc, xr0, xi0);
           acc[u + 1].prop1(c1[(u + 1) * G], d, sc, xr1, xi1);
         } else {  // exchange: the proposed theta is kept for the commit (nxt)
@@ -805,7 +815,11 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
       }
       if constexpr (U & 1) {
         Theta xr, xi;
-        if constexpr (PROP == MPV_PROPOSAL_FLIP) {
+        if constexpr (PROP == MPV_PROPOSAL_FLIP && kKeep) {
+          nxt[U - 1] = acc[U - 1];
+          nxt[U - 1].add(c1[(U - 1) * G], d);
+          nxt[U - 1].value(sc, xr, xi);
+        } else if constexpr (PROP == MPV_PROPOSAL_FLIP) {
           acc[U - 1].prop1(c1[(U - 1) * G], d, sc, xr, xi);
         } else {
           nxt[U - 1] = acc[U - 1];
@@ -855,7 +869,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
       n_acc += accept ? 1 : 0;
       // commit (flip): the column entries are re-read from shared memory (cheaper than
       // keeping U entries live in registers across the evaluation)
-      if constexpr (PROP == MPV_PROPOSAL_FLIP) {
+      if constexpr (PROP == MPV_PROPOSAL_FLIP && !kKeep) {
         const Sign dacc = moved ? d : A::sign(0);
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[u].add(c1[u * G], dacc);
