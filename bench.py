@@ -443,11 +443,11 @@ def run_ours(args, rank, world, local_rank):
                                          lambda_shift=1e-2, proposal=sampler.Proposal("exchange", N_SITES // 2),
                                          init_scale=0.3, burn_in_sweeps=0)
             cfgc.n_steps = 1
-            rescnn.train(cfgc)  # warm-up: autograd / cuDNN plans, allocator
+            rescnn.train(cfgc, local=True)  # warm-up: autograd / cuDNN plans, allocator (rank 0 only: no collectives)
             cfgc.n_steps = 3
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            rescnn.train(cfgc)
+            rescnn.train(cfgc, local=True)
             torch.cuda.synchronize()
             return {"config": "rescnn_4x16_3x3_j1j2_10x10_j2_0.5_marshall",
                     "forward_f16_configs_per_s": B / (ms_f / 1e3),
