@@ -52,6 +52,7 @@ constexpr int kIssuers = 4;      // threads issuing a convolution's MMAs
 
 struct Shape {
   int L, Lp, R, n_res, C, tiles, margin;  // R = Lp^2 rows per configuration
+  int Cg, GT;                             // configurations and MMA tiles per group (two groups)
   int n_conv;                             // 1 + 2 n_res
   size_t off_vec;                         // byte offset of the f32 vectors in the blob
   size_t blob_bytes;
@@ -66,9 +67,13 @@ inline bool make_shape(int L, int n_res, Shape* s) {
   s->Lp = L + 2;
   s->R = s->Lp * s->Lp;
   s->n_res = n_res;
-  s->C = kRowsMax / s->R;
-  if (s->C < 1 || s->C > kMaxC) return false;
-  s->tiles = (s->C * s->R + 127) / 128;
+  // two groups of Cg configurations, each starting on a tile boundary, so the
+  // tensor core runs one group's convolution under the other's epilogue
+  s->Cg = (kRowsMax / 2) / s->R;
+  s->C = 2 * s->Cg;
+  if (s->Cg < 1 || s->C > kMaxC) return false;
+  s->GT = (s->Cg * s->R + 127) / 128;
+  s->tiles = 2 * s->GT;
   s->margin = (s->Lp + 1 + 7) / 8 * 8;
   s->n_conv = 1 + 2 * n_res;
   s->off_vec = (size_t)s->n_conv * kTaps * kTapBytes;
@@ -182,7 +187,7 @@ template <int FMT>
 __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tmem_slot;
-  __shared__ __align__(8) uint64_t bar_mma;
+  __shared__ __align__(8) uint64_t bar_mma[2];  // MMA completion, one per group
   __shared__ int s_site[kMaxC];    // per configuration: flipped sites (MH), -1 none
   __shared__ int s_site2[kMaxC];
   __shared__ double s_logu[kMaxC];
@@ -197,14 +202,15 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
   float* rowsum = reinterpret_cast<float*>(sblob + S.blob_bytes);  // [tiles * 128]
   uint8_t* plane0 = planes + (size_t)S.margin * 16;      // row 0 of the grid rows
   const uint32_t aPlanes = smem_u32(plane0), aBlob = smem_u32(sblob);
-  const uint32_t sbar = smem_u32(&bar_mma);
+  const uint32_t sbar[2] = {smem_u32(&bar_mma[0]), smem_u32(&bar_mma[1])};
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sbar), "r"(kIssuers));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sbar[0]), "r"(kIssuers));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sbar[1]), "r"(kIssuers));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (size_t i = tid * 16; i < S.blob_bytes; i += kThreads * 16)
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
-  uint32_t phase = 0;
+  uint32_t phase[2] = {0u, 0u};
 
   const uint32_t fmtbits = FMT == MPV_FMT_BF16 ? 1u : 0u;
   const uint32_t idesc = (1u << 4) | (fmtbits << 7) | (fmtbits << 10) | ((uint32_t)(kF >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -224,16 +230,18 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
   const float* cb = vec;                          // [(n_res+1)][3][16]: cumulative bias, gain, shift
   const float* b1 = vec + (S.n_res + 1) * 3 * kF;  // [n_res][16]
 
-  // one convolution: 9 taps x tiles MMAs; accumulate into dst columns (acc0: first tap overwrites)
-  auto conv = [&](int ci, uint32_t dst_col, bool keep) {
+  const int GT = S.GT, Cg = S.Cg, gb = GT * 128;  // tiles and first row of group 1
+  // one convolution of group g: 9 taps x GT tile MMAs into dst columns (the
+  // first tap overwrites unless keep); every warp's epilogue writes must be done
+  auto issue = [&](int g, int ci, uint32_t dst_col, bool keep) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     // kIssuers threads (lane 0 of warps 0..kIssuers-1, one per SM sub-partition)
-    // issue the tiles round-robin; each commits its own MMAs to the barrier
+    // issue the group's tiles round-robin; each commits its own MMAs to the barrier
     if (lane == 0 && warp < kIssuers) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      for (int t = warp; t < S.tiles; t += kIssuers)
+      for (int t = g * GT + warp; t < (g + 1) * GT; t += kIssuers)
         for (int d = 0; d < kTaps; ++d) {
           const int off = (d / 3 - 1) * Lp + (d % 3 - 1);
           const uint32_t aaddr = aPlanes + (uint32_t)((t * 128 + off) * 16);
@@ -241,14 +249,22 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
           const uint64_t db = make_desc(aBlob + (uint32_t)((ci * kTaps + d) * kTapBytes), 128, 256);
           mma_f16(tmem + dst_col + t * kF, da, db, idesc, (keep || d > 0) ? 1u : 0u);
         }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sbar)
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sbar[g])
                    : "memory");
     }
-    mbar_wait(sbar, phase);
-    phase ^= 1;
+  };
+  auto wait = [&](int g) {
+    mbar_wait(sbar[g], phase[g]);
+    phase[g] ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   };
-
+  // convolution k of the network: 0 embedding -> h; odd: first conv of block
+  // (k-1)/2 -> acc; even >= 2: second conv of block (k-2)/2 accumulated into h
+  auto issue_conv = [&](int g, int k) {
+    if (k == 0) issue(g, 0, 0, false);
+    else if (k & 1) issue(g, k, 256, false);
+    else issue(g, k, 0, true);
+  };
   const int64_t B = a.list ? (int64_t)*a.count : a.B;  // compacted: only the chains that move
   auto chain_of = [&](int64_t idx) -> int64_t { return a.list ? (int64_t)a.list[idx] : idx; };
   for (int64_t grp = blockIdx.x; grp < (B + C - 1) / C; grp += gridDim.x) {
@@ -276,84 +292,111 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
       s_logu[tid] = log(ua);
     }
     __syncthreads();
-    // ---- input plane: s = 1 - 2x in channel 0 (all grid rows incl. halo) ----
-    for (int r = tid; r < S.tiles * 128; r += kThreads) {
-      const int j = r / R, pos = r % R;
-      float v[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = 0.0f;
-      if (j < nc) {
-        int pr = pos / Lp, pc = pos % Lp;
-        pr = pr == 0 ? L : (pr == L + 1 ? 1 : pr);
-        pc = pc == 0 ? L : (pc == L + 1 ? 1 : pc);
-        const int site = (pr - 1) * L + (pc - 1);
-        uint32_t x = (a.bits[chain_of(c0 + j) * words + (site >> 5)] >> (site & 31)) & 1u;
-        if (a.mh && (site == s_site[j] || site == s_site2[j])) x ^= 1u;
-        v[0] = x ? -1.0f : 1.0f;
-      }
-      uint4 lo, hi = make_uint4(0, 0, 0, 0);
-      lo.x = pack2<FMT>(v[0], 0.0f);
-      lo.y = lo.z = lo.w = 0;
-      *reinterpret_cast<uint4*>(plane0 + (size_t)r * 16) = lo;
-      *reinterpret_cast<uint4*>(plane0 + pstride + (size_t)r * 16) = hi;
-    }
-    // ---- embedding convolution -> h (TMEM columns [0, 256)) ----
-    conv(0, 0, false);
-    for (int l = 0; l <= S.n_res; ++l) {
-      // LN epilogue of h (+ the running bias): block input (GELU) or the final sum
-      const float* cbl = cb + l * 3 * kF;
-      for (int t = tg; t < S.tiles; t += 4) {
-        float h[16];
-        tmem_ld16(tmem + t_lane + t * kF, h);
-        const int r = t * 128 + q * 32 + lane;
-        const int j = r / R, pos = r % R, pr = pos / Lp, pc = pos % Lp;
-        const bool interior = j < nc && pr >= 1 && pr <= L && pc >= 1 && pc <= L;
-        float mu = 0.0f;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          h[k] += cbl[k];
-          mu += h[k];
+    // row r -> (configuration j, grid position pos); false for padding rows
+    auto rowmap = [&](int r, int& j, int& pos) -> bool {
+      const int g = r >= gb ? 1 : 0;
+      const int rr = r - g * gb, jj = rr / R;
+      pos = rr - jj * R;
+      j = g * Cg + jj;
+      return jj < Cg && j < nc;
+    };
+    // ---- input plane of group g: s = 1 - 2x in channel 0 (all grid rows incl. halo) ----
+    auto epi_in = [&](int g) {
+      for (int r = g * gb + tid; r < (g + 1) * gb; r += kThreads) {
+        int j, pos;
+        float v0 = 0.0f;
+        if (rowmap(r, j, pos)) {
+          int pr = pos / Lp, pc = pos % Lp;
+          pr = pr == 0 ? L : (pr == L + 1 ? 1 : pr);
+          pc = pc == 0 ? L : (pc == L + 1 ? 1 : pc);
+          const int site = (pr - 1) * L + (pc - 1);
+          uint32_t x = (a.bits[chain_of(c0 + j) * words + (site >> 5)] >> (site & 31)) & 1u;
+          if (a.mh && (site == s_site[j] || site == s_site2[j])) x ^= 1u;
+          v0 = x ? -1.0f : 1.0f;
         }
-        mu *= 1.0f / 16.0f;
-        float var = 0.0f;
+        uint4 lo, hi = make_uint4(0, 0, 0, 0);
+        lo.x = pack2<FMT>(v0, 0.0f);
+        lo.y = lo.z = lo.w = 0;
+        *reinterpret_cast<uint4*>(plane0 + (size_t)r * 16) = lo;
+        *reinterpret_cast<uint4*>(plane0 + pstride + (size_t)r * 16) = hi;
+      }
+    };
+    // ---- epilogue m (1 .. n_conv) of group g: odd m = LayerNorm of h (+ the running
+    // bias) for block (m-1)/2 -> GELU -> next input, or the final per-row sums;
+    // even m = GELU of the first convolution of block (m-2)/2 (+ its bias) ----
+    auto epi = [&](int g, int m) {
+      if (m & 1) {
+        const int l = (m - 1) / 2;
+        const float* cbl = cb + l * 3 * kF;
+        for (int t = g * GT + tg; t < (g + 1) * GT; t += 4) {
+          float h[16];
+          tmem_ld16(tmem + t_lane + t * kF, h);
+          const int r = t * 128 + q * 32 + lane;
+          int j, pos;
+          const bool valid = rowmap(r, j, pos);
+          const int pr = pos / Lp, pc = pos % Lp;
+          const bool interior = valid && pr >= 1 && pr <= L && pc >= 1 && pc <= L;
+          float mu = 0.0f;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) var = fmaf(h[k] - mu, h[k] - mu, var);
-        const float rs = rsqrtf(fmaf(var, 1.0f / 16.0f, 1e-6f));
-        if (l < S.n_res) {
+          for (int k = 0; k < 16; ++k) {
+            h[k] += cbl[k];
+            mu += h[k];
+          }
+          mu *= 1.0f / 16.0f;
+          float var = 0.0f;
 #pragma unroll
-          for (int k = 0; k < 16; ++k) h[k] = gelu(fmaf(cbl[kF + k] * rs, h[k] - mu, cbl[2 * kF + k]));
-          if (interior) store_row<FMT>(plane0, pstride, r, pr, pc, Lp, h);
-        } else {
-          float sum = 0.0f;
+          for (int k = 0; k < 16; ++k) var = fmaf(h[k] - mu, h[k] - mu, var);
+          const float rs = rsqrtf(fmaf(var, 1.0f / 16.0f, 1e-6f));
+          if (l < S.n_res) {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) sum += fmaf(cbl[kF + k] * rs, h[k] - mu, cbl[2 * kF + k]);
-          rowsum[r] = interior ? sum : 0.0f;
+            for (int k = 0; k < 16; ++k) h[k] = gelu(fmaf(cbl[kF + k] * rs, h[k] - mu, cbl[2 * kF + k]));
+            if (interior) store_row<FMT>(plane0, pstride, r, pr, pc, Lp, h);
+          } else {
+            float sum = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) sum += fmaf(cbl[kF + k] * rs, h[k] - mu, cbl[2 * kF + k]);
+            rowsum[r] = interior ? sum : 0.0f;
+          }
+        }
+      } else {
+        const float* b1l = b1 + ((m - 2) / 2) * kF;
+        for (int t = g * GT + tg; t < (g + 1) * GT; t += 4) {
+          float v[16];
+          tmem_ld16(tmem + t_lane + 256 + t * kF, v);
+          const int r = t * 128 + q * 32 + lane;
+          int j, pos;
+          const bool valid = rowmap(r, j, pos);
+          const int pr = pos / Lp, pc = pos % Lp;
+          if (valid && pr >= 1 && pr <= L && pc >= 1 && pc <= L) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = gelu(v[k] + b1l[k]);
+            store_row<FMT>(plane0, pstride, r, pr, pc, Lp, v);
+          }
         }
       }
-      if (l == S.n_res) break;
-      // first convolution of the block -> accumulators (TMEM columns [256, 512))
-      conv(1 + 2 * l, 256, false);
-      const float* b1l = b1 + l * kF;
-      for (int t = tg; t < S.tiles; t += 4) {
-        float v[16];
-        tmem_ld16(tmem + t_lane + 256 + t * kF, v);
-        const int r = t * 128 + q * 32 + lane;
-        const int j = r / R, pos = r % R, pr = pos / Lp, pc = pos % Lp;
-        if (j < nc && pr >= 1 && pr <= L && pc >= 1 && pc <= L) {
-#pragma unroll
-          for (int k = 0; k < 16; ++k) v[k] = gelu(v[k] + b1l[k]);
-          store_row<FMT>(plane0, pstride, r, pr, pc, Lp, v);
-        }
-      }
-      // second convolution accumulates into the residual stream h
-      conv(2 + 2 * l, 0, true);
+    };
+    // ---- two-group software pipeline: group 1's convolution k runs on the
+    // tensor core under group 0's epilogue k+1, group 0's convolution k+1 under
+    // group 1's epilogue k+1 ----
+    const int K = S.n_conv;
+    epi_in(0);
+    epi_in(1);
+    issue_conv(0, 0);
+    for (int k = 0; k < K; ++k) {
+      issue_conv(1, k);
+      wait(0);
+      epi(0, k + 1);
+      if (k + 1 < K) issue_conv(0, k + 1);
+      wait(1);
+      epi(1, k + 1);
     }
     __syncthreads();
     // ---- per-configuration sums (fixed order), accept / write ----
     if (tid < nc) {
       const int j = tid;
       float sum = 0.0f;
-      for (int pos = 0; pos < R; ++pos) sum += rowsum[j * R + pos];
+      const int base = (j / Cg) * gb + (j % Cg) * R;  // the configuration's first row
+      for (int pos = 0; pos < R; ++pos) sum += rowsum[base + pos];
       const double lp_new = 2.0 * (double)sum;
       const int64_t c = chain_of(c0 + j);
       if (!a.mh) {
