@@ -494,7 +494,8 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
   constexpr int CPW = 32 / G;
   // keep each unit's proposed theta in registers and commit it by select
   // (exchange: no second column read; table beyond shared memory: no L1/L2 re-read)
-  constexpr bool kKeep = (PROP == MPV_PROPOSAL_EXCHANGE) || !SMEM;
+  // (not for the f64 arithmetic's flip sweep: 26 doubles per lane spill there, -13%)
+  constexpr bool kKeep = (PROP == MPV_PROPOSAL_EXCHANGE) || (!SMEM && FMT != MPV_FMT_F64);
   constexpr int SW = (int)(sizeof(A) / sizeof(float));
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
