@@ -437,3 +437,28 @@ def test_cluster_split_sweep(cuda, monkeypatch, n, alpha, fmt, kind, scale):
     for s in (s0, s1):
         s.run_steps(700)
     np.testing.assert_array_equal(np.concatenate([s0.bits, s1.bits]), a.bits)
+
+
+@pytest.mark.parametrize("fmt", ["f16", "bf16", "f32", "f64"])
+def test_exchange_collect_rows_equal_stepped_bits(cuda, fmt):
+    """Fused exchange sweeps (one chain per warp; steps whose swap exchanges equal
+    bits are skipped by the warp but still counted and recorded): the collected
+    rows equal the chains' bits read after every `thin` steps of a stepped twin
+    (chain-major rows, sampler.py:142-167), and the acceptance counters agree."""
+    n, chains, per_chain, thin = 24, 40, 3, 5
+    p = rbm.random_parameters(n, 2, derive_key(6, "xrec"), 0.3)
+    mode = NATIVE if fmt != "f64" else PER_OP
+    ev = rbm.log_prob_evaluator(p, FORMATS[fmt], mode)
+    prop = sampler.Proposal("exchange", n // 2)
+    key = derive_key(8, "chains")
+    a = sampler.ChainEnsemble(chains, n, prop, ev, key)
+    rows = a.collect(chains * per_chain, thin)
+    b = sampler.ChainEnsemble(chains, n, prop, ev, key)
+    snaps = []
+    for _ in range(per_chain):
+        b.run_steps(thin)
+        snaps.append(b.bits.copy())
+    want = np.stack(snaps, axis=1).reshape(chains * per_chain, n)  # chain-major
+    assert np.array_equal(rows, want)
+    assert a.accepted == b.accepted and a.proposed == b.proposed
+    assert np.all(rows.sum(axis=1) == n // 2)
