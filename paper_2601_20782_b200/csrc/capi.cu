@@ -852,7 +852,11 @@ static int launch_ov(int mode, const double* t, const uint32_t* bits, int64_t U,
   const int64_t n = (int64_t)ld_rows(N) * ld_pitch(M);
   ld_transpose_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, st>>>(
       (const double2*)v, N, M, vwt, skip);
-  const int NT = (M + 3) / 4, kt = (NT + 7) / 8;
+  const int NT = (M + 3) / 4;
+  // O v (MODE 0): 16 warps per block, two blocks per SM; tanh (MODE 1): 8 warps
+  static const char* ovw = getenv("MPV_LD_OV_WARPS");  // experiments: 8 or 16
+  const int nw = (mode == 0 && !(ovw && atoi(ovw) == 8)) ? 16 : 8;
+  const int kt = (NT + nw - 1) / nw;
   const unsigned grid = (unsigned)((U + kLdSB - 1) / kLdSB);
   const int words = (N + 31) / 32;
   const double2* T = (const double2*)t;
@@ -861,7 +865,10 @@ static int launch_ov(int mode, const double* t, const uint32_t* bits, int64_t U,
   double2* TO = (double2*)t_out;
   const size_t tbytes = (size_t)kLdSB * M * 16;  // MODE 0: the block's T rows in shared memory
 #define MPV_OV(K)                                                                                             \
-  if (mode == 0) {                                                                                            \
+  if (mode == 0 && nw == 16) {                                                                                \
+    if (int rc = ensure_smem((const void*)&ld_ov_kernel<K, 0, 16>, tbytes)) return rc;                       \
+    ld_ov_kernel<K, 0, 16><<<grid, 512, tbytes, st>>>(T, bits, U, N, M, words, V, vwt, Q, w, TO, skip);     \
+  } else if (mode == 0) {                                                                                     \
     if (int rc = ensure_smem((const void*)&ld_ov_kernel<K, 0>, tbytes)) return rc;                           \
     ld_ov_kernel<K, 0><<<grid, 256, tbytes, st>>>(T, bits, U, N, M, words, V, vwt, Q, w, TO, skip);         \
   } else {                                                                                                    \

@@ -65,8 +65,9 @@ __device__ __forceinline__ double2 ctanh_f64(double x, double y) {
 
 // MODE 0 (ov):   q_s = w_s (O v)_s            (w NULL: 1)
 // MODE 1 (tanh): t_si = tanh(b_i + (X W^T)_si) with v = the parameter vector [a | b | W]
-template <int KT, int MODE = 0>
-__global__ void __launch_bounds__(256, KT >= 16 ? 1 : 2) ld_ov_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
+// NW warps per block (the block's 16 samples are shared by all warps' n-tiles)
+template <int KT, int MODE = 0, int NW = 8>
+__global__ void __launch_bounds__(32 * NW, (KT >= 16 || NW > 8) ? (NW > 8 ? 2 : 1) : 2) ld_ov_kernel(const double2* __restrict__ t, const uint32_t* __restrict__ bits,
                                                     int64_t U, int N, int M, int words, const double2* __restrict__ v,
                                                     const double* __restrict__ vwt, double2* __restrict__ q,
                                                     const double* __restrict__ w = nullptr,
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(256, KT >= 16 ? 1 : 2) ld_ov_kernel(const doub
                                                     const double* __restrict__ skip = nullptr) {
   if (skip && *skip != 0.0) return;
   __shared__ uint32_t smask[256 + 8];        // per-site masks of the block's 16 samples (N <= 256)
-  __shared__ double2 red[8][kLdSB];          // per-warp partial q
+  __shared__ double2 red[NW][kLdSB];         // per-warp partial q
   __shared__ __align__(8) uint64_t tbar;
   extern __shared__ __align__(16) double2 tsm[];  // MODE 0: the block's T rows [16][M], bulk-copied
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(256, KT >= 16 ? 1 : 2) ld_ov_kernel(const doub
   int col[KT];
 #pragma unroll
   for (int j = 0; j < KT; ++j) {
-    col[j] = min(warp + j * 8, NT - 1) * 8 + qc;
+    col[j] = min(warp + j * NW, NT - 1) * 8 + qc;
     acc[j][0][0] = acc[j][0][1] = acc[j][1][0] = acc[j][1][1] = 0.0;
   }
   // B fragments are prefetched one k-step ahead (L2 latency); n-tiles past NT
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(256, KT >= 16 ? 1 : 2) ld_ov_kernel(const doub
     const double a1 = __hiloint2double((int)(((mk >> (8 + qc)) & 1u) * 0x3ff00000u), 0);
 #pragma unroll
     for (int j = 0; j < KT; ++j) {
-      if (warp + j * 8 < NT) {
+      if (warp + j * NW < NT) {
         ld_dmma(acc[j][0][0], acc[j][0][1], a0, bf[j]);
         ld_dmma(acc[j][1][0], acc[j][1][1], a1, bf[j]);
       }
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(256, KT >= 16 ? 1 : 2) ld_ov_kernel(const doub
     // D fragment (sample m*8 + qc, unit nt*4 + qr) = theta - b: write tanh(theta)
 #pragma unroll
     for (int j = 0; j < KT; ++j) {
-      const int nt = warp + j * 8, i = nt * 4 + qr;
+      const int nt = warp + j * NW, i = nt * 4 + qr;
       if (nt < NT && i < M) {
         const double2 b = v[N + i];
 #pragma unroll
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(256, KT >= 16 ? 1 : 2) ld_ov_kernel(const doub
   double2 part[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
 #pragma unroll
   for (int j = 0; j < KT; ++j) {
-    const int nt = warp + j * 8, i = nt * 4 + qr;
+    const int nt = warp + j * NW, i = nt * 4 + qr;
     if (nt < NT && i < M) {
       const double2 vb = v[N + i];
 #pragma unroll
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(256, KT >= 16 ? 1 : 2) ld_ov_kernel(const doub
         acc2.x += v[k].x;
         acc2.y += v[k].y;
       }
-    for (int wp = 0; wp < 8; ++wp) {
+    for (int wp = 0; wp < NW; ++wp) {
       acc2.x += red[wp][tid].x;
       acc2.y += red[wp][tid].y;
     }
