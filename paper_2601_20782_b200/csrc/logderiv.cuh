@@ -240,8 +240,11 @@ __global__ void __launch_bounds__(256, 2) ld_ohu_kernel(const double2* __restric
                                                      const double* __restrict__ skip = nullptr) {
   if (skip && *skip != 0.0) return;
   __shared__ double as[2][64][kLdTile + 1];  // A' tiles [row][sample] (+1 pad: conflict-free column reads)
-  __shared__ uint32_t bs[2][kLdTile][9];
+  // B' = [X | 1] of the tile as per-column sample masks: cms[buf][n] bit s =
+  // X[tile sample s][site n] (built by warp ballots), column N = valid samples
+  __shared__ uint32_t cms[2][264];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 2 * 264; i += 256) (&cms[0][0])[i] = 0u;  // columns past the packed words stay 0
   const int rows_a = 2 * M + 2;
   const int u0 = blockIdx.x * 32;  // first unit of this block (64 A' rows)
   const int64_t k_begin = (int64_t)blockIdx.y * chunk;
@@ -251,6 +254,7 @@ __global__ void __launch_bounds__(256, 2) ld_ohu_kernel(const double2* __restric
   constexpr int kPer = kLdTile * 32 / 256;  // (sample, unit) pairs staged per thread
   double2 pt[kPer], pu[kPer];
   uint32_t pb = 0;
+  int pn = 0;
   auto load = [&](int64_t sb) {  // global -> registers for the tile at sb
 #pragma unroll
     for (int r = 0; r < kPer; ++r) {
@@ -269,10 +273,8 @@ __global__ void __launch_bounds__(256, 2) ld_ohu_kernel(const double2* __restric
         pt[r] = ui < M ? t[s * M + ui] : make_double2(2 * ui < rows_a ? 1.0 : 0.0, 0.0);  // rows 2M, 2M+1: u itself
       }
     }
-    if (tid < kLdTile * words) {
-      const int ls = tid / words, w = tid % words;
-      pb = (sb + ls < k_end) ? bits[(sb + ls) * words + w] : 0u;
-    }
+    if (warp < words) pb = (sb + lane < k_end) ? bits[(sb + lane) * words + warp] : 0u;  // warp w: word w, lane: sample
+    pn = (int)min((int64_t)kLdTile, k_end - sb);  // valid samples of the tile
   };
   auto store = [&](int buf) {  // registers -> shared: A' = (Re, Im) conj(t) u
 #pragma unroll
@@ -281,7 +283,14 @@ __global__ void __launch_bounds__(256, 2) ld_ohu_kernel(const double2* __restric
       as[buf][2 * lu][ls] = fma(pt[r].x, pu[r].x, pt[r].y * pu[r].y);
       as[buf][2 * lu + 1][ls] = fma(pt[r].x, pu[r].y, -pt[r].y * pu[r].x);
     }
-    if (tid < kLdTile * words) bs[buf][tid / words][tid % words] = pb;
+    if (warp < words) {  // transpose word `warp` of the 32 samples into 32 column masks
+#pragma unroll 8
+      for (int b = 0; b < 32; ++b) {
+        const uint32_t m = __ballot_sync(kFull, (pb >> b) & 1u);
+        if (lane == b && warp * 32 + b != N) cms[buf][warp * 32 + b] = m;
+      }
+    }
+    if (tid == 0) cms[buf][N] = pn >= 32 ? 0xFFFFFFFFu : ((1u << pn) - 1u);  // the ones column
   };
   double acc[NTC][2];
 #pragma unroll
@@ -293,15 +302,18 @@ __global__ void __launch_bounds__(256, 2) ld_ohu_kernel(const double2* __restric
   for (int64_t sb = k_begin; sb < k_end; sb += kLdTile) {
     const bool more = sb + kLdTile < k_end;
     if (more) load(sb + kLdTile);  // in flight during the DMMAs below
+    uint32_t mj[NTC];  // the lane's B' columns c0 + 8 j + qc of this tile
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) {
+      const int n = c0 + j * 8 + qc;
+      mj[j] = n < 264 ? cms[cur][n] : 0u;
+    }
 #pragma unroll 4
     for (int k0 = 0; k0 < kLdTile; k0 += 4) {
       const double av = as[cur][warp * 8 + qc][k0 + qr];
-      const uint32_t* bw = bs[cur][k0 + qr];
-      const bool valid = sb + k0 + qr < k_end;
 #pragma unroll
       for (int j = 0; j < NTC; ++j) {
-        const int n = c0 + j * 8 + qc;  // B' column of this lane
-        const uint32_t bit = n < N ? ((bw[n >> 5] >> (n & 31)) & 1u) : (n == N && valid ? 1u : 0u);
+        const uint32_t bit = (mj[j] >> (k0 + qr)) & 1u;
         ld_dmma(acc[j][0], acc[j][1], av, __hiloint2double((int)(bit * 0x3ff00000u), 0));
       }
     }
