@@ -45,6 +45,8 @@ __global__ void bench(float* out, long long* cyc, float seed) {
       if (OP == 22) { int r; asm volatile("cvt.rni.s32.f32 %0, %1;" : "=r"(r) : "f"(f[j])); f[j] = __int_as_float(r); }
       if (OP == 23) { unsigned short h = (unsigned short)u[j]; asm volatile("fma.rn.f32.bf16 %0, %1, %1, %0;" : "+f"(f[j]) : "h"(h)); }
       if (OP == 24) { int r; asm volatile("cvt.rzi.s32.f32 %0, %1;" : "=r"(r) : "f"(f[j] * 1.5f)); f[j] = __int_as_float(r); }
+      if (OP == 25) { double r; asm volatile("cvt.f64.f32 %0, %1;" : "=d"(r) : "f"(f[j])); f[j] = (float)__double2loint(r) + f[j]; }
+      if (OP == 26) { double r; asm volatile("cvt.f64.f32 %0, %1;" : "=d"(r) : "f"(f[j])); d[j] += r; }
       if (OP == 21) { unsigned long long z = ((unsigned long long)u[j] << 32) | u[(j+1)%CH]; z *= 0xBF58476D1CE4E5B9ull; u[j] = (unsigned)(z >> 29); }
     }
   }
@@ -88,6 +90,7 @@ int main() {
   run<22>("cvt.rni.s32.f32", out, cyc, nsm);
   run<24>("fmul + cvt.rzi.s32.f32", out, cyc, nsm);
   run<23>("fma.rn.f32.bf16 (mixed)", out, cyc, nsm);
+  run<26>("cvt.f64.f32 (+ dadd)", out, cyc, nsm);
   run<21>("u64 mul (splitmix step)", out, cyc, nsm);
   run<13>("lds.128", out, cyc, nsm);
   run<14>("lds.64", out, cyc, nsm);
