@@ -23,7 +23,8 @@ cap energy energy_kernel 0 1 python tools/bench_energy.py tfim
 cap energy_heis energy_kernel 0 1 python tools/bench_energy.py heis
 cap rescnn_f64 rescnn_f64_dmma 0 1 python tools/bench_rescnn_f64.py
 cap rescnn rescnn_kernel 0 1 python tools/bench_rescnn.py
-cap ld "ld_ov_kernel|ld_ohu_kernel" 1 2 python tools/bench_sr_cg.py
+cap ld ld_ov_kernel 1 1 python tools/bench_sr_cg.py
+cap ld_ohu ld_ohu_kernel 1 1 python tools/bench_sr_cg.py
 cap sweep_f32 sweep_kernel 1 1 python tools/bench_sweep_one.py f32
 cap sweep_c3 sweep_kernel 1 1 python tools/bench_sweep_one.py bf16 100 4 0.01 exchange
 cap sweep_c5 sweep_kernel 1 1 python tools/bench_sweep_one.py f16 256 1 0.01 flip
