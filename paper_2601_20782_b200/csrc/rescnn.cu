@@ -9,8 +9,10 @@
 //   log psi = sum LN(h_n);  3x3 periodic convolutions, F = 16 channels.
 //
 // Tensor-core mapping (no im2col): a CTA holds C configurations as padded
-// (L+2) x (L+2) grids, one row per grid position, rows of consecutive
-// configurations back to back (C (L+2)^2 <= 2048 rows = 16 MMA tiles of 128).
+// (L+2) x (L+2) grids, one row per grid position, in two groups of C/2
+// configurations (rows back to back within a group, each group starting on an
+// MMA tile boundary; <= 2 x 1024 rows = 16 tiles of 128), so one group's
+// convolution runs on the tensor core while the other group's epilogue runs.
 // Activations are two K planes (channels 0-7, 8-15) of 16 bytes per row, so a
 // K-major no-swizzle descriptor with SBO = 128 B (8-row groups contiguous) and
 // LBO = the plane stride addresses ANY row offset: the 3x3 neighbour of row r
