@@ -99,3 +99,33 @@ def test_config3_bf16_energy_vs_reference_f64_chains(cuda):
     print(f"\n[config3] E_bf16 {e16:.6f} +- {err16:.6f}  E_ref(f64) {e_ref:.6f} +- {err_ref:.6f}  "
           f"sigma_hat {sigma_hat:.3e}")
     assert abs(e16 - e_ref) <= 3 * math.hypot(err16, err_ref), (e16, e_ref, err16, err_ref)
+
+
+def test_config5_xi_global_flip_matches_model(cuda):
+    """BASELINE configs[4] shape: 16x16 TFIM RBM alpha=1 in f16.  The planner picks
+    XI accumulators and the 512 KB table is read through L1/L2 with the
+    select-commit of theta' (flip sweep): log p equals the arithmetic model,
+    and after many moves the chains' cached log p equals a fresh evaluation and
+    two shards reproduce the single ensemble."""
+    from paper_2601_20782_b200 import F16
+
+    n = 256
+    p = rbm.random_parameters(n, 1, derive_key(5, "c5"), 0.01)
+    ev = rbm.log_prob_evaluator(p, F16, RoundingMode.NATIVE)
+    snap = ev.snapshot
+    assert snap.variant == _native.ACC_XI and snap._table.numel() > SMEM_LIMIT, snap.label
+    bits = np.random.default_rng(2).integers(0, 2, size=(800, n), dtype=np.uint8)
+    r = rbm.round_parameters(p, F16)
+    want, tol = model.native_log_prob(r.a, r.b, r.w, bits, "f16")
+    got = ev(bits)
+    assert np.all(np.abs(got - want) <= tol), np.max(np.abs(got - want) - tol)
+    prop = sampler.Proposal("flip")
+    key = derive_key(6, "chains")
+    a = sampler.ChainEnsemble(600, n, prop, ev, key)
+    a.run_steps(1500)
+    np.testing.assert_array_equal(a.log_probs, ev(a.bits))
+    s0 = sampler.ChainEnsemble(250, n, prop, ev, key, chain_offset=0, n_chains_total=600)
+    s1 = sampler.ChainEnsemble(350, n, prop, ev, key, chain_offset=250, n_chains_total=600)
+    for s in (s0, s1):
+        s.run_steps(1500)
+    np.testing.assert_array_equal(np.concatenate([s0.bits, s1.bits]), a.bits)
