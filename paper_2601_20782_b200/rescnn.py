@@ -10,7 +10,8 @@ restatement oracle/rescnn.py and by exact H psi on enumerable lattices).
 site (learned gain / shift, eps 1e-6), GELU in its tanh form.  Evaluation runs
 in the CUDA library (csrc/rescnn.cu): a tcgen05 tensor-core forward with
 f16/bf16 operands and f32 accumulation (the sampler's evaluator, fused with the
-MH step), and an f64 CUDA-core forward (local energies, parity).
+MH step), and an f64 forward on the FP64 tensor cores (DMMA; local energies,
+parity).
 """
 from __future__ import annotations
 
@@ -158,8 +159,8 @@ def make_blob(params: ResCnnParameters, fmt: FloatFormat) -> np.ndarray:
 class ResCnnEvaluator:
     """Device log-probability evaluator of a ResCNN (the reference evaluator
     protocol, sampler.py:49-53: uint8[B, N] -> float64[B]).  fmt f16/bf16: the
-    tcgen05 forward (ChainEnsemble fuses it into the MH step); f64: the CUDA-core
-    f64 forward (2 log psi)."""
+    tcgen05 forward (ChainEnsemble fuses it into the MH step); f64: the DMMA f64
+    forward (2 log psi)."""
 
     def __init__(self, params: ResCnnParameters, fmt: FloatFormat, device=None):
         import torch
