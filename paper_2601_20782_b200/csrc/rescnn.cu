@@ -183,6 +183,7 @@ struct Args {
   // compacted MH step (exchange): the chains to evaluate, list[0 .. *count)
   const int32_t* list;
   const int32_t* count;
+  int cpc;  // configurations per CTA group (<= S.C; fewer spread small batches over more SMs)
 };
 
 template <int FMT>
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
   const float* b1 = vec + (S.n_res + 1) * 3 * kF;  // [n_res][16]
 
   const int GT = S.GT, Cg = S.Cg, gb = GT * 128;  // tiles and first row of group 1
+  int ntile[2] = {GT, GT};                        // tiles of each group in use (set per CTA group)
   // one convolution of group g: 9 taps x GT tile MMAs into dst columns (the
   // first tap overwrites unless keep); every warp's epilogue writes must be done
   auto issue = [&](int g, int ci, uint32_t dst_col, bool keep) {
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
     // issue the group's tiles round-robin; each commits its own MMAs to the barrier
     if (lane == 0 && warp < kIssuers) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      for (int t = g * GT + warp; t < (g + 1) * GT; t += kIssuers)
+      for (int t = g * GT + warp; t < g * GT + ntile[g]; t += kIssuers)
         for (int d = 0; d < kTaps; ++d) {
           const int off = (d / 3 - 1) * Lp + (d % 3 - 1);
           const uint32_t aaddr = aPlanes + (uint32_t)((t * 128 + off) * 16);
@@ -269,9 +271,12 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
   };
   const int64_t B = a.list ? (int64_t)*a.count : a.B;  // compacted: only the chains that move
   auto chain_of = [&](int64_t idx) -> int64_t { return a.list ? (int64_t)a.list[idx] : idx; };
-  for (int64_t grp = blockIdx.x; grp < (B + C - 1) / C; grp += gridDim.x) {
-    const int64_t c0 = grp * C;
-    const int nc = (int)min((int64_t)C, B - c0);
+  const int cpc = a.cpc > 0 ? min(a.cpc, C) : C;
+  for (int64_t grp = blockIdx.x; grp < (B + cpc - 1) / cpc; grp += gridDim.x) {
+    const int64_t c0 = grp * cpc;
+    const int nc = (int)min((int64_t)cpc, B - c0);
+    // MMA tiles holding this group's configurations (an empty second group is skipped)
+    const int used0 = (min(nc, Cg) * R + 127) / 128, used1 = (max(0, nc - Cg) * R + 127) / 128;
     // ---- proposals (MH) ----
     if (a.mh && tid < nc) {
       const int64_t c = chain_of(c0 + tid), gchain = a.chain_offset + c;
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
     };
     // ---- input plane of group g: s = 1 - 2x in channel 0 (all grid rows incl. halo) ----
     auto epi_in = [&](int g) {
-      for (int r = g * gb + tid; r < (g + 1) * gb; r += kThreads) {
+      for (int r = g * gb + tid; r < g * gb + ntile[g] * 128; r += kThreads) {
         int j, pos;
         float v0 = 0.0f;
         if (rowmap(r, j, pos)) {
@@ -330,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
       if (m & 1) {
         const int l = (m - 1) / 2;
         const float* cbl = cb + l * 3 * kF;
-        for (int t = g * GT + tg; t < (g + 1) * GT; t += 4) {
+        for (int t = g * GT + tg; t < g * GT + ntile[g]; t += 4) {
           float h[16];
           tmem_ld16(tmem + t_lane + t * kF, h);
           const int r = t * 128 + q * 32 + lane;
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
         }
       } else {
         const float* b1l = b1 + ((m - 2) / 2) * kF;
-        for (int t = g * GT + tg; t < (g + 1) * GT; t += 4) {
+        for (int t = g * GT + tg; t < g * GT + ntile[g]; t += 4) {
           float v[16];
           tmem_ld16(tmem + t_lane + 256 + t * kF, v);
           const int r = t * 128 + q * 32 + lane;
@@ -381,16 +386,21 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
     // tensor core under group 0's epilogue k+1, group 0's convolution k+1 under
     // group 1's epilogue k+1 ----
     const int K = S.n_conv;
+    ntile[0] = used0;
+    ntile[1] = used1;
+    const bool two = used1 > 0;  // block-uniform
     epi_in(0);
-    epi_in(1);
+    if (two) epi_in(1);
     issue_conv(0, 0);
     for (int k = 0; k < K; ++k) {
-      issue_conv(1, k);
+      if (two) issue_conv(1, k);
       wait(0);
       epi(0, k + 1);
       if (k + 1 < K) issue_conv(0, k + 1);
-      wait(1);
-      epi(1, k + 1);
+      if (two) {
+        wait(1);
+        epi(1, k + 1);
+      }
     }
     __syncthreads();
     // ---- per-configuration sums (fixed order), accept / write ----
@@ -886,7 +896,12 @@ cudaError_t rescnn_launch(int L, int n_res, int fmt, const void* blob, uint32_t*
   int dev = 0, n_sm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t groups = (B + a.S.C - 1) / a.S.C;
+  // small batches: fewer configurations per CTA so that every SM gets work (a
+  // compacted exchange step evaluates about half of the chains)
+  const bool compacted = mh && proposal == MPV_PROPOSAL_EXCHANGE && list && count;
+  const int64_t expect = compacted ? (B + 1) / 2 : B;
+  a.cpc = (int)std::max<int64_t>(1, std::min<int64_t>(a.S.C, (expect + n_sm - 1) / n_sm));
+  const int64_t groups = (B + a.cpc - 1) / a.cpc;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(groups, n_sm));
   if (mh && proposal == MPV_PROPOSAL_EXCHANGE && list && count) {
     rescnn_propose_kernel<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(a, list, count);
