@@ -460,10 +460,35 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
 // convolution are staged in shared memory and read warp-uniformly).  Two
 // activation buffers per configuration (layer input / first-convolution
 // output) hold the neighbours' values.
-// tanh-form GELU, 0.5 z (1 + tanh u) = z / (1 + e^{-2u}): one exp and one division
+// e^x for the GELU (a few ulp): x = n ln2 + r with |r| <= ln2/2 (Cody-Waite,
+// two-constant ln2), e^r by a degree-11 Taylor polynomial (truncation < 1e-16
+// relative), times 2^n by exponent arithmetic; saturates outside [-708, 708]
+// (the GELU only needs e^x -> 0 or -> inf there).
+__device__ __forceinline__ double exp_gelu(double x) {
+  x = fmin(fmax(x, -708.0), 708.0);
+  const double n = rint(x * 1.4426950408889634);
+  const double r = fma(n, -1.90821492927058770002e-10, fma(n, -6.93147180369123816490e-01, x));  // fdlibm ln2 hi/lo
+  double p = 2.5052108385441720e-08;  // 1/11!
+  p = fma(p, r, 2.7557319223985893e-07);
+  p = fma(p, r, 2.7557319223985888e-06);
+  p = fma(p, r, 2.4801587301587302e-05);
+  p = fma(p, r, 1.9841269841269841e-04);
+  p = fma(p, r, 1.3888888888888889e-03);
+  p = fma(p, r, 8.3333333333333332e-03);
+  p = fma(p, r, 4.1666666666666664e-02);
+  p = fma(p, r, 1.6666666666666666e-01);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  return __hiloint2double(__double2hiint(p) + ((int)n << 20), __double2loint(p));
+}
+// tanh-form GELU, 0.5 z (1 + tanh u) = z / (1 + e^{-2u}): one exp and one
+// reciprocal (MUFU seed + Newton steps, rounding of a few ulp)
 __device__ __forceinline__ double gelu64(double z) {
   const double u = 0.7978845608028654 * fma(0.044715 * z, z * z, z);
-  return z / (1.0 + exp(-2.0 * u));
+  const double d = 1.0 + exp_gelu(-2.0 * u);
+  double y = __drcp_rn(d);
+  return z * y;
 }
 
 constexpr int kF64Threads = 512;
