@@ -126,9 +126,11 @@ __device__ __forceinline__ float tanh_approx(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// tanh-form GELU: u = z (c + c 0.044715 z^2), 0.5 z (1 + tanh u) = z (0.5 + 0.5 tanh u)
+// (6 f32 ops + one MUFU per activation)
 __device__ __forceinline__ float gelu(float z) {
-  const float u = 0.7978845608028654f * fmaf(0.044715f * z, z * z, z);
-  return 0.5f * z * (1.0f + tanh_approx(u));
+  const float u = z * fmaf(0.035677408136300125f, z * z, 0.7978845608028654f);
+  return z * fmaf(0.5f, tanh_approx(u), 0.5f);
 }
 
 template <int FMT>
@@ -271,6 +273,18 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
   };
   const int64_t B = a.list ? (int64_t)*a.count : a.B;  // compacted: only the chains that move
   auto chain_of = [&](int64_t idx) -> int64_t { return a.list ? (int64_t)a.list[idx] : idx; };
+  // per-lane epilogue rows (tile slot m of group g: t = g GT + tg + 4 m): the
+  // configuration within the group and the grid position, computed once
+  // (integer divisions by runtime sizes stay out of the epilogues)
+  uint32_t rinfo[2][2];
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int rr = (tg + 4 * m) * 128 + q * 32 + lane;  // row within the group
+      const int jj = rr / R, pos = rr - jj * R;
+      rinfo[g][m] = jj < Cg ? ((uint32_t)jj << 16) | ((uint32_t)(pos / Lp) << 8) | (uint32_t)(pos % Lp) : 0xFFFF0000u;
+    }
   const int cpc = a.cpc > 0 ? min(a.cpc, C) : C;
   for (int64_t grp = blockIdx.x; grp < (B + cpc - 1) / cpc; grp += gridDim.x) {
     const int64_t c0 = grp * cpc;
@@ -335,13 +349,16 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
       if (m & 1) {
         const int l = (m - 1) / 2;
         const float* cbl = cb + l * 3 * kF;
-        for (int t = g * GT + tg; t < g * GT + ntile[g]; t += 4) {
+#pragma unroll
+        for (int m2 = 0; m2 < 2; ++m2) {
+          const int t = g * GT + tg + 4 * m2;
+          if (t >= g * GT + ntile[g]) break;
           float h[16];
           tmem_ld16(tmem + t_lane + t * kF, h);
           const int r = t * 128 + q * 32 + lane;
-          int j, pos;
-          const bool valid = rowmap(r, j, pos);
-          const int pr = pos / Lp, pc = pos % Lp;
+          const uint32_t ri = g ? rinfo[1][m2] : rinfo[0][m2];
+          const int jj = (int)(ri >> 16), pr = (int)((ri >> 8) & 0xFF), pc = (int)(ri & 0xFF);
+          const bool valid = jj < Cg && g * Cg + jj < nc;
           const bool interior = valid && pr >= 1 && pr <= L && pc >= 1 && pc <= L;
           float mu = 0.0f;
 #pragma unroll
@@ -367,13 +384,16 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
         }
       } else {
         const float* b1l = b1 + ((m - 2) / 2) * kF;
-        for (int t = g * GT + tg; t < g * GT + ntile[g]; t += 4) {
+#pragma unroll
+        for (int m2 = 0; m2 < 2; ++m2) {
+          const int t = g * GT + tg + 4 * m2;
+          if (t >= g * GT + ntile[g]) break;
           float v[16];
           tmem_ld16(tmem + t_lane + 256 + t * kF, v);
           const int r = t * 128 + q * 32 + lane;
-          int j, pos;
-          const bool valid = rowmap(r, j, pos);
-          const int pr = pos / Lp, pc = pos % Lp;
+          const uint32_t ri = g ? rinfo[1][m2] : rinfo[0][m2];
+          const int jj = (int)(ri >> 16), pr = (int)((ri >> 8) & 0xFF), pc = (int)(ri & 0xFF);
+          const bool valid = jj < Cg && g * Cg + jj < nc;
           if (valid && pr >= 1 && pr <= L && pc >= 1 && pc <= L) {
 #pragma unroll
             for (int k = 0; k < 16; ++k) v[k] = gelu(v[k] + b1l[k]);
