@@ -360,25 +360,36 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
           const int jj = (int)(ri >> 16), pr = (int)((ri >> 8) & 0xFF), pc = (int)(ri & 0xFF);
           const bool valid = jj < Cg && g * Cg + jj < nc;
           const bool interior = valid && pr >= 1 && pr <= L && pc >= 1 && pc <= L;
+          const float4* c4 = reinterpret_cast<const float4*>(cbl);  // [bias | gain | shift] x 16, LDS.128
           float mu = 0.0f;
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            h[k] += cbl[k];
-            mu += h[k];
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const float4 c = c4[k4];
+            h[4 * k4] += c.x; h[4 * k4 + 1] += c.y; h[4 * k4 + 2] += c.z; h[4 * k4 + 3] += c.w;
           }
+#pragma unroll
+          for (int k = 0; k < 16; ++k) mu += h[k];
           mu *= 1.0f / 16.0f;
           float var = 0.0f;
 #pragma unroll
           for (int k = 0; k < 16; ++k) var = fmaf(h[k] - mu, h[k] - mu, var);
           const float rs = rsqrtf(fmaf(var, 1.0f / 16.0f, 1e-6f));
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {  // LN: gain * (h - mu) * rs + shift
+            const float4 gk = c4[4 + k4], sk = c4[8 + k4];
+            h[4 * k4] = fmaf(gk.x * rs, h[4 * k4] - mu, sk.x);
+            h[4 * k4 + 1] = fmaf(gk.y * rs, h[4 * k4 + 1] - mu, sk.y);
+            h[4 * k4 + 2] = fmaf(gk.z * rs, h[4 * k4 + 2] - mu, sk.z);
+            h[4 * k4 + 3] = fmaf(gk.w * rs, h[4 * k4 + 3] - mu, sk.w);
+          }
           if (l < S.n_res) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) h[k] = gelu(fmaf(cbl[kF + k] * rs, h[k] - mu, cbl[2 * kF + k]));
+            for (int k = 0; k < 16; ++k) h[k] = gelu(h[k]);
             if (interior) store_row<FMT>(plane0, pstride, r, pr, pc, Lp, h);
           } else {
             float sum = 0.0f;
 #pragma unroll
-            for (int k = 0; k < 16; ++k) sum += fmaf(cbl[kF + k] * rs, h[k] - mu, cbl[2 * kF + k]);
+            for (int k = 0; k < 16; ++k) sum += h[k];
             rowsum[r] = interior ? sum : 0.0f;
           }
         }
@@ -395,8 +406,15 @@ __global__ void __launch_bounds__(kThreads, 1) rescnn_kernel(const Args a) {
           const int jj = (int)(ri >> 16), pr = (int)((ri >> 8) & 0xFF), pc = (int)(ri & 0xFF);
           const bool valid = jj < Cg && g * Cg + jj < nc;
           if (valid && pr >= 1 && pr <= L && pc >= 1 && pc <= L) {
+            const float4* b4 = reinterpret_cast<const float4*>(b1l);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) v[k] = gelu(v[k] + b1l[k]);
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const float4 bk = b4[k4];
+              v[4 * k4] = gelu(v[4 * k4] + bk.x);
+              v[4 * k4 + 1] = gelu(v[4 * k4 + 1] + bk.y);
+              v[4 * k4 + 2] = gelu(v[4 * k4 + 2] + bk.z);
+              v[4 * k4 + 3] = gelu(v[4 * k4 + 3] + bk.w);
+            }
             store_row<FMT>(plane0, pstride, r, pr, pc, Lp, v);
           }
         }
