@@ -205,8 +205,10 @@ __device__ __forceinline__ double lc_f64(double tr, double ti) {
   const double u = fabs(tr);
   const double v = tr >= 0.0 ? ti : -ti;
   const double t = exp(-2.0 * u);
-  const double wr = __dmul_rn(__dadd_rn(1.0, t), cos(v));
-  const double wi = __dmul_rn(__dadd_rn(1.0, -t), sin(v));
+  double sv, cv;
+  sincos(v, &sv, &cv);  // one shared argument reduction (same values as cos(v), sin(v))
+  const double wr = __dmul_rn(__dadd_rn(1.0, t), cv);
+  const double wi = __dmul_rn(__dadd_rn(1.0, -t), sv);
   const double q = __dadd_rn(__dmul_rn(wr, wr), __dmul_rn(wi, wi));
   return __dadd_rn(__dadd_rn(u, -0.69314718055994530942), __dmul_rn(0.5, log(q)));
 }
