@@ -88,8 +88,10 @@ __device__ double warp_forward_perop(const FwdArgs& a, const uint32_t* wbuf, dou
     const double u = fabs(dtr);
     const double v = dtr >= 0.0 ? dti : -dti;
     const double t = exp(-2.0 * u);
-    const double wr = __dmul_rn(__dadd_rn(1.0, t), cos(v));
-    const double wi = __dmul_rn(__dadd_rn(1.0, -t), sin(v));
+    double sv, cv;
+    sincos(v, &sv, &cv);  // one shared argument reduction (same values as cos(v), sin(v))
+    const double wr = __dmul_rn(__dadd_rn(1.0, t), cv);
+    const double wi = __dmul_rn(__dadd_rn(1.0, -t), sv);
     const double qq = __dadd_rn(__dmul_rn(wr, wr), __dmul_rn(wi, wi));
     const double hr = __dadd_rn(__dadd_rn(u, -0.69314718055994530942), __dmul_rn(0.5, log(qq)));
     hbuf[i] = P::f64(P::q(hr));
@@ -151,8 +153,10 @@ __device__ double warp_forward_f64(const FwdArgs& a, const uint32_t* wbuf, doubl
     const double u = fabs(th.x);
     const double v = th.x < 0.0 ? -th.y : th.y;
     const double t = exp(-2.0 * u);
-    const double wr = __dmul_rn(__dadd_rn(1.0, t), cos(v));
-    const double wi = __dmul_rn(__dadd_rn(1.0, -t), sin(v));
+    double sv, cv;
+    sincos(v, &sv, &cv);  // one shared argument reduction (same values as cos(v), sin(v))
+    const double wr = __dmul_rn(__dadd_rn(1.0, t), cv);
+    const double wi = __dmul_rn(__dadd_rn(1.0, -t), sv);
     const double qq = __dadd_rn(__dmul_rn(wr, wr), __dmul_rn(wi, wi));
     hr_part += __dadd_rn(__dadd_rn(u, -0.69314718055994530942), __dmul_rn(0.5, log(qq)));
     if (want_im) hi_part += atan2(wi, wr);
