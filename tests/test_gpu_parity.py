@@ -462,3 +462,37 @@ def test_exchange_collect_rows_equal_stepped_bits(cuda, fmt):
     assert np.array_equal(rows, want)
     assert a.accepted == b.accepted and a.proposed == b.proposed
     assert np.all(rows.sum(axis=1) == n // 2)
+
+
+def test_bench_workload_full_size_properties(cuda):
+    """The bench step at its full size (BASELINE configs[1]: 10x10 TFIM, alpha=2,
+    16,384 chains, f16 NATIVE, 2 re-burn sweeps, 65,536 samples at thinning
+    N+1), through size-independent properties: two chain shards reproduce the
+    single ensemble's samples bit for bit, every chain's cached log p equals a
+    fresh evaluation, and a random subsample's f64 local energies equal the
+    oracle's restatement of the reference."""
+    from oracle import port
+    from paper_2601_20782_b200 import vmc
+    from paper_2601_20782_b200.hamiltonians import TfimSpec
+    from paper_2601_20782_b200.lattice import LatticeSpec
+
+    n, chains = 100, 16384
+    p = rbm.random_parameters(n, 2, derive_key(0, "init"), 0.01)
+    ev = rbm.log_prob_evaluator(p, FORMATS["f16"], NATIVE)
+    prop = sampler.Proposal("flip")
+    key = derive_key(0, "chains")
+    full = sampler.ChainEnsemble(chains, n, prop, ev, key)
+    full.run_sweeps(2)
+    rows = full.collect(4 * chains, n + 1)
+    np.testing.assert_array_equal(full.log_probs, ev(full.bits))
+    parts = []
+    for off, cnt in ((0, 7000), (7000, chains - 7000)):
+        s = sampler.ChainEnsemble(cnt, n, prop, ev, key, chain_offset=off, n_chains_total=chains)
+        s.run_sweeps(2)
+        parts.append(s.collect(4 * chains, n + 1))
+    np.testing.assert_array_equal(np.concatenate(parts), rows)
+    spec = TfimSpec(LatticeSpec.square(10), 1.0, 3.04)
+    sub = rows[np.random.default_rng(0).choice(rows.shape[0], size=64, replace=False)]
+    eps = vmc.local_energies(spec, rbm.log_psi_evaluator(p), sub)
+    want = port.local_energies(port.Params(p.a, p.b, p.w), "tfim", spec.lattice.bond_array(), 1.0, 3.04, sub)
+    assert np.max(np.abs(eps - want) / np.maximum(1, np.abs(want))) < 1e-11
