@@ -197,7 +197,8 @@ def run_ours(args, rank, world, local_rank):
     # ---- end-to-end through the public API (host buffers, copies inside) ----
     e2e_ms = 0.0
     h2d = d2h = 0
-    n_e2e = max(1, min(args.steps, 3))
+    n_e2e = min(max(args.steps, 5), 10)  # host-side jitter: at least 5 timed public-API steps
+    e2e_each = []
     E2E_WARMUP = 3  # untimed: the pinned host blocks reach steady state in the caching allocator
     for it in range(n_e2e + E2E_WARMUP):
         torch.cuda.synchronize()
@@ -218,6 +219,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         if it >= E2E_WARMUP:
             e2e_ms += t0.elapsed_time(t1)
+            e2e_each.append(t0.elapsed_time(t1))
         snap = ev_e2e.snapshot
         # snapshot upload + the uint8 sample rows re-uploaded by local_energies (packed on the device)
         h2d = snap._table.numel() + snap._bias.numel() + snap._vis_im.numel() * 8 + samples.nbytes
@@ -615,6 +617,7 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk,
         "gpu_launches": launches["n"],
         "e2e": {"value": steps_per_step / (e2e_ms / 1e3), "unit": "chain-steps/s", "ms_per_step": e2e_ms,
+                "timed_steps": n_e2e, "ms_min_max_rank0": [min(e2e_each), max(e2e_each)],
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "api": "log_prob_evaluator + ChainEnsemble.set_evaluator/run_sweeps/collect + vmc.local_energies"},
         "north_star_shape": ns,
