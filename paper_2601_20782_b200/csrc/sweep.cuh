@@ -12,6 +12,9 @@
 // log p of a proposal is a fixed function of the proposed configuration, and
 // the accept test is the reference's f64 `log(u) < lp_new - lp_old`.
 #pragma once
+#ifndef MPV_SWEEP_UNDO
+#define MPV_SWEEP_UNDO 1  // experiments: 0 evaluates theta' aside and commits accepted moves
+#endif
 #include "common.cuh"
 
 namespace mpv {
@@ -498,6 +501,10 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
   // (exchange: no second column read; table beyond shared memory: no L1/L2 re-read)
   // (not for the f64 arithmetic's flip sweep: 26 doubles per lane spill there, -13%)
   constexpr bool kKeep = (PROP == MPV_PROPOSAL_EXCHANGE) || (!SMEM && FMT != MPV_FMT_F64);
+  // Flip sweeps with exact accumulators (X1 / X2 / XI): theta' is formed in
+  // place, so an accepted move needs no commit; a warp with a rejecting chain
+  // restores theta = theta' - d w exactly (every partial sum is exact).
+  constexpr bool kUndo = MPV_SWEEP_UNDO && PROP == MPV_PROPOSAL_FLIP && !kKeep && VAR != MPV_ACC_F64;
   constexpr int SW = (int)(sizeof(A) / sizeof(float));
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -801,6 +808,11 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
           nxt[u + 1] = acc[u + 1];
           nxt[u + 1].add(c1[(u + 1) * G], d);
           nxt[u + 1].value(sc, xr1, xi1);
+        } else if constexpr (kUndo) {
+          acc[u].add(c1[u * G], d);
+          acc[u].value(sc, xr0, xi0);
+          acc[u + 1].add(c1[(u + 1) * G], d);
+          acc[u + 1].value(sc, xr1, xi1);
         } else if constexpr (PROP == MPV_PROPOSAL_FLIP) {
           acc[u].prop1(c1[u * G], d, sc, xr0, xi0);
           acc[u + 1].prop1(c1[(u + 1) * G], d, sc, xr1, xi1);
@@ -822,6 +834,9 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
           nxt[U - 1] = acc[U - 1];
           nxt[U - 1].add(c1[(U - 1) * G], d);
           nxt[U - 1].value(sc, xr, xi);
+        } else if constexpr (kUndo) {
+          acc[U - 1].add(c1[(U - 1) * G], d);
+          acc[U - 1].value(sc, xr, xi);
         } else if constexpr (PROP == MPV_PROPOSAL_FLIP) {
           acc[U - 1].prop1(c1[(U - 1) * G], d, sc, xr, xi);
         } else {
@@ -845,7 +860,8 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
 #pragma unroll
             for (int j = 0; j < SW; ++j) reinterpret_cast<float*>(&au)[j] = sv[(u * SW + j) * 32];
             Theta xr, xi;
-            if (PROP == MPV_PROPOSAL_FLIP) au.prop1(c1[u * G], d, sc, xr, xi);
+            if (kUndo) au.value(sc, xr, xi);  // acc already holds theta'
+            else if (PROP == MPV_PROPOSAL_FLIP) au.prop1(c1[u * G], d, sc, xr, xi);
             else au.prop2(c1[u * G], c2[u * G], d, md, sc, xr, xi);
             E::fix(xr, xi, h);
           }
@@ -872,7 +888,13 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
       n_acc += accept ? 1 : 0;
       // commit (flip): the column entries are re-read from shared memory (cheaper than
       // keeping U entries live in registers across the evaluation)
-      if constexpr (PROP == MPV_PROPOSAL_FLIP && !kKeep) {
+      if constexpr (kUndo) {
+        if (__any_sync(kFull, !moved)) {  // warp-uniform: restore the rejecting chains' theta
+          const Sign dund = moved ? A::sign(0) : md;
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc[u].add(c1[u * G], dund);
+        }
+      } else if constexpr (PROP == MPV_PROPOSAL_FLIP && !kKeep) {
         const Sign dacc = moved ? d : A::sign(0);
 #pragma unroll
         for (int u = 0; u < U; ++u) acc[u].add(c1[u * G], dacc);
