@@ -82,7 +82,7 @@ typedef struct {
   const void* bias;
   const void* vis;
   const double* vis_im;
-  double quantum; /* XI: table integers are multiples of this power of two */
+  double quantum; /* XI: table integers are multiples of this power of two (>= 2^-100) */
   /* Frozen Gaussian log-density noise (ref: rbm.py:333-352 NoiseField,
    * rbm.py:408-416 noisy_log_prob_evaluator): log p(x) += noise_sigma *
    * ndtri(counter_uniform(noise_key, code(x))) with code(x) = sum_k bit_k 2^k

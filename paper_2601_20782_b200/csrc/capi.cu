@@ -410,7 +410,8 @@ int mpv_snapshot_fill(const mpv_snapshot* snap, const double* rounded, double sp
   if (!snap || !rounded || !snap->table || !snap->bias || !snap->vis || snap->n_visible < 1 ||
       snap->hidden_pad < snap->n_hidden || snap->n_hidden < 1)
     return fail(MPV_ERR_ARGS, "snapshot_fill: bad args");
-  if (snap->variant == MPV_ACC_XI && !(snap->quantum > 0.0)) return fail(MPV_ERR_ARGS, "snapshot_fill: XI quantum");
+  // XI: the quantum is applied in f32 (bf16: folded into the log cosh, exact for q >= 2^-100)
+  if (snap->variant == MPV_ACC_XI && !(snap->quantum >= 0x1p-100)) return fail(MPV_ERR_ARGS, "snapshot_fill: XI quantum");
   if (snap->variant == MPV_ACC_X2 && snap->mode == MPV_MODE_NATIVE && !(split > 0.0))
     return fail(MPV_ERR_ARGS, "snapshot_fill: X2 split");
   const int64_t n = (int64_t)(snap->n_visible + 1) * snap->hidden_pad + snap->n_visible;
@@ -571,7 +572,8 @@ int mpv_mh_sweep(const mpv_snapshot* snap, const mpv_chains* ch, uint64_t key, i
   a.xi_scale = (float)snap->quantum;
   a.noise_key = snap->noise_key;
   a.noise_sigma = snap->noise_sigma;
-  if (variant == MPV_ACC_XI && !(snap->quantum > 0.0)) return fail(MPV_ERR_ARGS, "mh_sweep: XI needs quantum > 0");
+  if (variant == MPV_ACC_XI && !(snap->quantum >= 0x1p-100))
+    return fail(MPV_ERR_ARGS, "mh_sweep: XI needs quantum >= 2^-100");
   if (int rc = ensure_smem(fn, smem)) return rc;
   int dev = 0, n_sm = 0;
   cudaGetDevice(&dev);

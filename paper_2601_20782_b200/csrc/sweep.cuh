@@ -12,6 +12,9 @@
 // log p of a proposal is a fixed function of the proposed configuration, and
 // the accept test is the reference's f64 `log(u) < lp_new - lp_old`.
 #pragma once
+#ifndef MPV_XI_FOLD
+#define MPV_XI_FOLD 1  // experiments: 0 scales bf16 XI theta by q before rounding
+#endif
 #ifndef MPV_SWEEP_UNDO
 #define MPV_SWEEP_UNDO 1  // experiments: 0 evaluates theta' aside and commits accepted moves
 #endif
@@ -144,9 +147,10 @@ __device__ __forceinline__ uint64_t segment_code(uint32_t word, int words, int G
 // 3 MUFU ops  ½ log(1 + t² + 2 t cos 2y) + |x| - ln2,  t = e^{-2|x|}
 // (the same closed form as ref _logcosh_pair, rbm.py:130-140), result rounded
 // to the format by the caller (pairs of units share one F2FP).
+constexpr float kLcK = -2.8853900817779268f;  // -2 log2(e) in f32
 __device__ __forceinline__ float lc_fast(float x, float y2, float& vmin) {
   const float ax = fabsf(x);
-  const float t = ex2_approx(ax * -2.8853900817779268f);  // e^{-2|x|}
+  const float t = ex2_approx(ax * kLcK);  // e^{-2|x|}
   const float c = cos_approx(y2);                          // cos 2y
   const float s = fmaf(2.0f, c, t);
   const float v = fmaf(t, s, 1.0f);                        // 4 e^{-2|x|} |cosh z|^2
@@ -154,6 +158,20 @@ __device__ __forceinline__ float lc_fast(float x, float y2, float& vmin) {
   return fmaf(lg2_approx(v), 0.34657359027997264f, ax - 0.69314718055994531f);
 }
 
+// lc_fast(m q, y2) for a power-of-two q folded into the constants (bf16 XI:
+// RN_bf16(m q) = RN_bf16(m) q over bf16's f32 exponent range): |m| (k q) and
+// |m| q - ln 2 are the same real numbers as |x| k and |x| - ln 2, so the
+// results are bit-identical to lc_fast(m q, y2) with one multiply fewer per
+// component.  ksc = k q with k the f32 constant of lc_fast.
+__device__ __forceinline__ float lc_fast_sc(float m, float y2, float q, float ksc, float& vmin) {
+  const float am = fabsf(m);
+  const float t = ex2_approx(am * ksc);
+  const float c = cos_approx(y2);
+  const float s = fmaf(2.0f, c, t);
+  const float v = fmaf(t, s, 1.0f);
+  vmin = fminf(vmin, v);
+  return fmaf(lg2_approx(v), 0.34657359027997264f, fmaf(am, q, -0.69314718055994531f));
+}
 // Near a zero of cosh (v = 1 + t^2 + 2t cos 2y -> 0) the MUFU form cancels.
 // There |x| < 0.02 and cos^2 y < 2.5e-4, and Re log cosh = ½ log(sinh^2 x +
 // cos^2 y) is evaluated with a short sinh series and cos y = ±sin r,
@@ -285,28 +303,36 @@ template <int FMT> struct Acc<FMT, MPV_ACC_X2> {
 // ---- XI, f16/bf16: theta as an exact int32 multiple of the snapshot quantum q
 // (host planner: B/q < 2^31); one IMAD per component, the f32 value is the
 // correctly rounded I2F of the integer times q (a power of two: exact).
+// bf16 (kFold): the values are returned unscaled and the evaluator applies q
+// (lc_fast_sc), exact over bf16's exponent range (host planner: q >= 2^-100).
 template <int FMT> struct Acc<FMT, MPV_ACC_XI> {
   using Entry = int2;
   using Vis = int;
   using Sign = int;
+  static constexpr bool kFold = MPV_XI_FOLD && FMT == MPV_FMT_BF16;
   int re, im;
   __device__ __forceinline__ static Sign sign(int d) { return d; }
+  __device__ __forceinline__ static float scaled(int v, float sc) {
+    return kFold ? __int2float_rn(v) : __int2float_rn(v) * sc;
+  }
   __device__ __forceinline__ void init(Entry b) { re = b.x; im = b.y; }
   __device__ __forceinline__ void value(float sc, float& xr, float& xi) const {
-    xr = __int2float_rn(re) * sc;
-    xi = __int2float_rn(im) * sc;
+    xr = scaled(re, sc);
+    xi = scaled(im, sc);
   }
   __device__ __forceinline__ void add(Entry e, Sign d) { re += d * e.x; im += d * e.y; }
   __device__ __forceinline__ void prop1(Entry e, Sign d, float sc, float& xr, float& xi) const {
-    xr = __int2float_rn(re + d * e.x) * sc;
-    xi = __int2float_rn(im + d * e.y) * sc;
+    xr = scaled(re + d * e.x, sc);
+    xi = scaled(im + d * e.y, sc);
   }
   __device__ __forceinline__ void prop2(Entry e1, Entry e2, Sign d, Sign md, float sc, float& xr,
                                         float& xi) const {
-    xr = __int2float_rn(re + d * e1.x + md * e2.x) * sc;
-    xi = __int2float_rn(im + d * e1.y + md * e2.y) * sc;
+    xr = scaled(re + d * e1.x + md * e2.x, sc);
+    xi = scaled(im + d * e1.y + md * e2.y, sc);
   }
 };
+template <int FMT, int VAR> struct FoldsScale { static constexpr bool value = false; };
+template <int FMT> struct FoldsScale<FMT, MPV_ACC_XI> { static constexpr bool value = Acc<FMT, MPV_ACC_XI>::kFold; };
 
 // ---- X1, f32 format: float pairs ----
 template <> struct Acc<MPV_FMT_F32, MPV_ACC_X1> {
@@ -386,8 +412,18 @@ template <int FMT, int VAR> struct Eval {
   // Contribution of two units (u0, u1) given proposed theta in f32 (or f64).
   // Reduced formats: theta rounded to fmt, lc in f32, lc rounded to fmt, then
   // accumulated in f32 (mask 0 for padded units).
+  static constexpr bool kFold = FoldsScale<FMT, VAR>::value;
+  // the unit's log cosh from the packed rounded pair (kFold: unscaled by q)
+  __device__ __forceinline__ static float lc_packed(uint32_t p, float sc, float& vmin) {
+    using H = Half<FMT>;
+    if constexpr (kFold)
+      return lc_fast_sc(H::lo(p), H::fma_hi(p, (uint16_t)(__float_as_uint(2.0f * sc) >> 16), -0.0f), sc, kLcK * sc,
+                        vmin);
+    else
+      return lc_fast(H::lo(p), H::hi2(p), vmin);
+  }
   template <typename T>
-  __device__ __forceinline__ static void pair(T xr0, T xi0, T xr1, T xi1, Sum& acc, float& vmin) {
+  __device__ __forceinline__ static void pair(T xr0, T xi0, T xr1, T xi1, Sum& acc, float& vmin, float sc) {
     if constexpr (kF64) {
       acc += lc_f64(xr0, xi0);
       acc += lc_f64(xr1, xi1);
@@ -399,8 +435,8 @@ template <int FMT, int VAR> struct Eval {
       } else {
         using H = Half<FMT>;
         const uint32_t p0 = H::pack(a0, b0), p1 = H::pack(a1, b1);
-        const float l0 = lc_fast(H::lo(p0), H::hi2(p0), vmin);
-        const float l1 = lc_fast(H::lo(p1), H::hi2(p1), vmin);
+        const float l0 = lc_packed(p0, sc, vmin);
+        const float l1 = lc_packed(p1, sc, vmin);
         const uint32_t lp = H::pack(l0, l1);
         acc = H::acc_lo(lp, acc);
         acc = H::acc_hi(lp, acc);
@@ -408,7 +444,7 @@ template <int FMT, int VAR> struct Eval {
     }
   }
   template <typename T>
-  __device__ __forceinline__ static void single(T xr, T xi, Sum& acc, float& vmin) {
+  __device__ __forceinline__ static void single(T xr, T xi, Sum& acc, float& vmin, float sc) {
     if constexpr (kF64) {
       acc += lc_f64(xr, xi);
     } else if constexpr (FMT == MPV_FMT_F32) {
@@ -416,21 +452,21 @@ template <int FMT, int VAR> struct Eval {
     } else {
       using H = Half<FMT>;
       const uint32_t p = H::pack((float)xr, (float)xi);
-      const uint32_t lp = H::pack(lc_fast(H::lo(p), H::hi2(p), vmin), 0.0f);
+      const uint32_t lp = H::pack(lc_packed(p, sc, vmin), 0.0f);
       acc = H::acc_lo(lp, acc);
     }
   }
   // Correction for units near a cosh zero: h += q(lc_near_zero) - q(lc_fast)
   // (both rounded to the format), in unit order.  Deterministic in theta.
   template <typename T>
-  __device__ __forceinline__ static void fix(T xr, T xi, Sum& acc) {
+  __device__ __forceinline__ static void fix(T xr, T xi, Sum& acc, float sc) {
     if constexpr (!kF64 && FMT != MPV_FMT_F32) {
       using H = Half<FMT>;
       const uint32_t p = H::pack((float)xr, (float)xi);
       float v = 1e30f;
-      const float lf = lc_fast(H::lo(p), H::hi2(p), v);
+      const float lf = lc_packed(p, sc, v);
       if (v < NearZero<FMT>::kV) {
-        const float la = lc_near_zero(H::lo(p), H::hi(p));
+        const float la = kFold ? lc_near_zero(H::lo(p) * sc, H::hi(p) * sc) : lc_near_zero(H::lo(p), H::hi(p));
         const uint32_t q = H::pack(lf, la);
         acc += H::hi(q) - H::lo(q);
       }
@@ -677,12 +713,12 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
         Theta xr0, xi0, xr1, xi1;
         acc[u].prop1(Entry{}, A::sign(0), sc, xr0, xi0);
         acc[u + 1].prop1(Entry{}, A::sign(0), sc, xr1, xi1);
-        E::pair(xr0, xi0, xr1, xi1, h0, vmin0);
+        E::pair(xr0, xi0, xr1, xi1, h0, vmin0, sc);
       }
       if constexpr (U & 1) {
         Theta xr, xi;
         acc[U - 1].prop1(Entry{}, A::sign(0), sc, xr, xi);
-        E::single(xr, xi, h0, vmin0);
+        E::single(xr, xi, h0, vmin0, sc);
       }
       if constexpr (E::kFix) {
         if (vmin0 < NearZero<FMT>::kV) {  // rare: a unit is near a cosh zero
@@ -700,7 +736,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
             for (int j = 0; j < SW; ++j) reinterpret_cast<float*>(&au)[j] = sv[(u * SW + j) * 32];
             Theta xr, xi;
             au.prop1(Entry{}, A::sign(0), sc, xr, xi);
-            E::fix(xr, xi, h0);
+            E::fix(xr, xi, h0, sc);
           }
         }
       }
@@ -826,7 +862,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
           nxt[u + 1].add(c1[(u + 1) * G], d);
           nxt[u + 1].value(sc, xr1, xi1);
         }
-        E::pair(xr0, xi0, xr1, xi1, h, vmin);
+        E::pair(xr0, xi0, xr1, xi1, h, vmin, sc);
       }
       if constexpr (U & 1) {
         Theta xr, xi;
@@ -845,7 +881,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
           nxt[U - 1].add(c1[(U - 1) * G], d);
           nxt[U - 1].value(sc, xr, xi);
         }
-        E::single(xr, xi, h, vmin);
+        E::single(xr, xi, h, vmin, sc);
       }
       if constexpr (E::kFix) {
         if (vmin < NearZero<FMT>::kV) {  // rare: a unit of this lane is near a cosh zero
@@ -863,7 +899,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
             if (kUndo) au.value(sc, xr, xi);  // acc already holds theta'
             else if (PROP == MPV_PROPOSAL_FLIP) au.prop1(c1[u * G], d, sc, xr, xi);
             else au.prop2(c1[u * G], c2[u * G], d, md, sc, xr, xi);
-            E::fix(xr, xi, h);
+            E::fix(xr, xi, h, sc);
           }
         }
       }

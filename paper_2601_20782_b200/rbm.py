@@ -138,7 +138,7 @@ class ExactPlan:
     All partial sums of the snapshot's values are multiples of ``quantum`` and
     bounded by ``bound``; f32 holds every multiple of q up to 2^24 q exactly.
     X1: one f32 per component (bound <= 2^24 q).  XI: one int32 per component
-    counting multiples of q (bound < 2^30 q).  X2: theta = hi + lo with hi on the
+    counting multiples of q (bound < 2^30 q, q >= 2^-100).  X2: theta = hi + lo with hi on the
     grid ``split`` (|hi| <= 2^24 split) and |lo| <= (N+1) split/2 <= 2^24 q.
     F64: otherwise (f64 accumulators, converted per unit)."""
 
@@ -159,7 +159,7 @@ def plan_from_bounds(q: float, bound_re: float, bound_im: float, bound_a: float,
         split = 0.0  # X2 not exact
     if bound <= 2.0**24 * q:
         return ExactPlan(nat.ACC_X1, q, bound, split)
-    if allow_xi and bound < 2.0**30 * q:
+    if allow_xi and bound < 2.0**30 * q and q >= 2.0**-100:  # q applied in f32 (bf16: exact above 2^-100)
         return ExactPlan(nat.ACC_XI, q, bound, split)
     if split > 0.0:
         return ExactPlan(nat.ACC_X2, q, bound, split)
@@ -231,7 +231,8 @@ class DeviceSnapshot:
                     raise ValueError("X2 accumulators are not exact for this snapshot")
                 elif variant == nat.ACC_XI and fmt.name not in ("f16", "bf16"):
                     raise ValueError("XI accumulators exist for f16/bf16 snapshots only")
-                elif variant == nat.ACC_XI and not self.plan.bound < 2.0**30 * self.plan.quantum:
+                elif variant == nat.ACC_XI and not (self.plan.bound < 2.0**30 * self.plan.quantum
+                                                    and self.plan.quantum >= 2.0**-100):
                     raise ValueError("XI accumulators are not exact for this snapshot")
                 split = self.plan.split
                 if variant == nat.ACC_XI:
