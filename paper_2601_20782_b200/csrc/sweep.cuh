@@ -321,6 +321,8 @@ template <int FMT> struct Acc<FMT, MPV_ACC_XI> {
     xi = scaled(im, sc);
   }
   __device__ __forceinline__ void add(Entry e, Sign d) { re += d * e.x; im += d * e.y; }
+  // theta + ea - eb (exchange with the columns ordered by the move's sign: one IADD3 per component)
+  __device__ __forceinline__ void add_diff(Entry ea, Entry eb) { re += ea.x - eb.x; im += ea.y - eb.y; }
   __device__ __forceinline__ void prop1(Entry e, Sign d, float sc, float& xr, float& xi) const {
     xr = scaled(re + d * e.x, sc);
     xi = scaled(im + d * e.y, sc);
@@ -832,6 +834,18 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
       const Sign md = A::sign(-dsign);
       const Entry* c1 = tab + (size_t)k1 * Mpad + gl;
       const Entry* c2 = tab + (size_t)k2 * Mpad + gl;
+      // exchange, XI: theta' = theta + ca - cb with the columns ordered by the sign
+      // of the move (cb = ca when the bits are equal: theta' = theta)
+      const Entry* ca = dsign >= 0 ? c1 : c2;
+      const Entry* cb = dsign > 0 ? c2 : (dsign < 0 ? c1 : ca);
+      auto xmove = [&](A& n, int u) {
+        if constexpr (VAR == MPV_ACC_XI) {
+          n.add_diff(ca[u * G], cb[u * G]);
+        } else {
+          n.add(c2[u * G], md);
+          n.add(c1[u * G], d);
+        }
+      };
       Sum h = Sum(0);
       float vmin = 1e30f;
 #pragma unroll
@@ -854,12 +868,10 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
           acc[u + 1].prop1(c1[(u + 1) * G], d, sc, xr1, xi1);
         } else {  // exchange: the proposed theta is kept for the commit (nxt)
           nxt[u] = acc[u];
-          nxt[u].add(c2[u * G], md);
-          nxt[u].add(c1[u * G], d);
+          xmove(nxt[u], u);
           nxt[u].value(sc, xr0, xi0);
           nxt[u + 1] = acc[u + 1];
-          nxt[u + 1].add(c2[(u + 1) * G], md);
-          nxt[u + 1].add(c1[(u + 1) * G], d);
+          xmove(nxt[u + 1], u + 1);
           nxt[u + 1].value(sc, xr1, xi1);
         }
         E::pair(xr0, xi0, xr1, xi1, h, vmin, sc);
@@ -877,8 +889,7 @@ __global__ void __launch_bounds__((PROP == MPV_PROPOSAL_FLIP) ? 512 : 256, (PROP
           acc[U - 1].prop1(c1[(U - 1) * G], d, sc, xr, xi);
         } else {
           nxt[U - 1] = acc[U - 1];
-          nxt[U - 1].add(c2[(U - 1) * G], md);
-          nxt[U - 1].add(c1[(U - 1) * G], d);
+          xmove(nxt[U - 1], U - 1);
           nxt[U - 1].value(sc, xr, xi);
         }
         E::single(xr, xi, h, vmin, sc);
