@@ -488,15 +488,18 @@ def run_ours(args, rank, world, local_rank):
             return time.perf_counter() - t0, res.records
 
         wall(3)  # warm-up
-        w2, _ = wall(2)
-        w12, recs = wall(12)
+        # host-side jitter (Python, allocator): median of three runs of each length
+        w2 = float(np.median([wall(2)[0] for _ in range(3)]))
+        runs12 = [wall(12) for _ in range(3)]
+        w12 = float(np.median([r[0] for r in runs12]))
+        recs = runs12[-1][1]
         recs = recs[2:]
         vmc_iter = {"config": "tfim_chain20_open_h1_a1_s4096_c1024_f16native",
                     "sampling_ms": 1e3 * float(np.median([r["sampling_seconds"] for r in recs])),
                     "update_ms": 1e3 * float(np.median([r["update_seconds"] for r in recs])),
                     "energy_last": recs[-1]["energy"], "kappa_last": recs[-1]["kappa"],
                     "iteration_ms": 1e3 * (w12 - w2) / 10,
-                    "timing": "iteration_ms = wall time of 10 training steps (12-step run minus a 2-step run), incl. "
+                    "timing": "iteration_ms = wall time of 10 training steps (12-step run minus a 2-step run, medians of 3), incl. "
                               "the per-step eigvalsh condition number of the reference's record (cuSOLVER, ~5 ms at P = 440)"}
         # BASELINE configs[1] (10x10 TFIM, alpha=2, 16,384 chains, 65,536 samples, f16
         # sampling + f64 energies): the dense S (P = 20,300) does not fit the
