@@ -155,6 +155,40 @@ def test_native_variants_identical(cuda, fmt):
         assert np.max(np.abs(o - firsts[0]) / np.maximum(1, np.abs(o))) < 2e-6
 
 
+@pytest.mark.parametrize("kind", ["flip", "exchange"])
+@pytest.mark.parametrize("fmt,scale", [("f16", 0.01), ("f16", 0.3), ("bf16", 0.01), ("bf16", 0.3), ("f32", 0.01)])
+def test_native_variant_sweeps_identical(cuda, fmt, scale, kind):
+    """MH sweeps with every exact accumulator variant (X1 / X2 / XI / F64, where
+    the planner admits it) follow bitwise identical trajectories in the same
+    lane layout: covers theta' formed in place and restored on rejection (flip,
+    table in shared memory), the select commit (exchange), the sign-ordered
+    column difference (XI exchange) and the bf16 XI scale folded into the log
+    cosh.  Acceptance is mixed at these scales, so both branches run."""
+    n = 40
+    p = rbm.random_parameters(n, 2, derive_key(6, "variant-sweeps"), scale)
+    prop = sampler.Proposal(kind)
+    key = derive_key(7, "chains")
+    runs = {}
+    for var in (_native.ACC_X1, _native.ACC_XI, _native.ACC_X2, _native.ACC_F64):
+        try:
+            ev = rbm.log_prob_evaluator(p, FORMATS[fmt], NATIVE, variant=var)
+        except ValueError:
+            continue
+        ens = sampler.ChainEnsemble(96, n, prop, ev, key)
+        ens.run_steps(600)
+        snap = ens._snapshot()
+        layout = (snap.cluster, snap.lanes_per_chain, snap.units_per_lane)
+        runs.setdefault(layout, []).append((var, ens.bits, ens.log_probs, ens.accepted, ens.collect(64, 5)))
+    assert max(len(v) for v in runs.values()) >= 2, {k: [g[0] for g in v] for k, v in runs.items()}
+    for group in runs.values():
+        var0, bits0, lp0, acc0, smp0 = group[0]
+        assert 0 < acc0 < 96 * 600  # both accepted and rejected moves
+        for var, bits, lp, acc, smp in group[1:]:
+            assert np.array_equal(bits, bits0), (var0, var)
+            assert np.array_equal(lp, lp0), (var0, var)
+            assert np.array_equal(acc, acc0) and np.array_equal(smp, smp0), (var0, var)
+
+
 @pytest.mark.parametrize("fmt", ["f16", "bf16", "f32", "f64"])
 @pytest.mark.parametrize("mode", [NATIVE, PER_OP])
 def test_zero_parameters_give_zero(cuda, fmt, mode):
