@@ -9,6 +9,7 @@
 
 #include "energy.cuh"
 #include "logderiv.cuh"
+#include "ov_tc.h"
 #include "perop.cuh"
 #include "snapshot.cuh"
 #include "sr.cuh"
@@ -839,7 +840,10 @@ int mpv_local_energies_ex(int N, int M, const double* a, const double* b, const 
   return fail(MPV_ERR_ARGS, "local_energies: n_hidden / terms too large for shared memory");
 }
 
-static size_t ld_ov_bytes(int N, int M) { return ((size_t)ld_rows(N) * ld_pitch(M) * sizeof(double) + 255) / 256 * 256; }
+static size_t ld_ov_bytes(int N, int M) {
+  // the DMMA kernel's padded vW^T, or the tcgen05 kernel's limb matrix (ov_tc.cu)
+  return std::max(((size_t)ld_rows(N) * ld_pitch(M) * sizeof(double) + 255) / 256 * 256, ov_tc_blob_bytes(N, M));
+}
 
 size_t mpv_logderiv_scratch_bytes(int64_t U, int N, int M) {
   const int64_t chunk = ld_chunk(std::max<int64_t>(U, 1), N, M), chunks = (U + chunk - 1) / chunk;
@@ -851,6 +855,15 @@ static int launch_ov(int mode, const double* t, const uint32_t* bits, int64_t U,
                      const double* w, double* q, double* t_out, void* scratch, cudaStream_t st,
                      const double* skip = nullptr) {
   double* vwt = (double*)scratch;
+  // O v on tcgen05 (exact f16 limbs, ov_tc.cu) unless MPV_OV_TC=0 (the DMMA kernel below)
+  if (mode == 0) {
+    const char* tc = getenv("MPV_OV_TC");
+    if (!(tc && atoi(tc) == 0)) {
+      const int rc = ov_tc_launch(t, bits, U, N, M, v, w, q, scratch, st, skip);
+      if (rc == 0) return check_launch("logderiv_ov_tc");
+      if (rc < 0) return check_launch("logderiv_ov_tc");
+    }
+  }
   const int64_t n = (int64_t)ld_rows(N) * ld_pitch(M);
   ld_transpose_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, st>>>(
       (const double2*)v, N, M, vwt, skip);

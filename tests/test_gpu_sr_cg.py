@@ -137,6 +137,33 @@ def test_train_minsr_matches_dense(cuda):
     np.testing.assert_allclose(ms.params.w, dense.params.w, rtol=1e-8, atol=1e-10)
 
 
+@pytest.mark.parametrize("n,alpha,U", [(100, 2, 3000), (20, 1, 1500), (37, 2, 2049), (8, 4, 5), (100, 2, 70000)])
+def test_ov_tensor_core_matches_dmma(cuda, n, alpha, U, monkeypatch):
+    """O v on tcgen05 with exact f16 limbs (ov_tc.cu, the default) against the
+    FP64-tensor-core kernel (MPV_OV_TC=0): both are f64-accurate, they differ
+    only in rounding (the limb sums are exact; DMMA rounds each of N products).
+    U = 70,000 covers several tiles per CTA and a ragged last tile."""
+    import torch
+
+    p, bits, w, _ = _setup(n=n, alpha=alpha, U=U)
+    fo = vmc.FactoredLogDerivatives(p, bits)
+    rng = np.random.default_rng(7)
+    P = n + p.n_hidden + n * p.n_hidden
+    v = torch.complex(torch.from_numpy(rng.normal(size=P)), torch.from_numpy(rng.normal(size=P))).cuda()
+    v[5] = 0  # zero and tiny entries in a column (sigma from the largest)
+    v[-3] = 1e-300
+    tc = fo.o_v(v, w)
+    tc_plain = fo.o_v(v)
+    monkeypatch.setenv("MPV_OV_TC", "0")
+    dm = fo.o_v(v, w)
+    dm_plain = fo.o_v(v)
+    monkeypatch.delenv("MPV_OV_TC")
+    scale = float(dm_plain.abs().max())
+    assert float((tc_plain - dm_plain).abs().max()) <= 1e-13 * scale
+    torch.testing.assert_close(tc, dm, rtol=1e-12, atol=1e-13 * scale * float(w.max()))
+    assert torch.equal(fo.o_v(v, w), tc)  # deterministic
+
+
 def test_factored_products_at_the_size_limits(cuda):
     """N = 256 sites (8 words), M = 512 hidden units: the largest shapes the
     O-product kernels accept, against the materialised O."""
