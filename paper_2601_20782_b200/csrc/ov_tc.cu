@@ -58,7 +58,8 @@ inline bool make_layout(int N, int M, Layout* L) {
   for (int hc = 48; hc >= 16; hc -= 16) {
     const size_t chunk = 2ull * kLimbs * hc * L->Kp * 2;
     const size_t tb = (size_t)kRows * (hc + 1) * 16;  // the tile's t rows of the chunk, padded rows
-    const size_t smem = L->a_bytes + chunk + tb + L->part_bytes + rup((size_t)N * 16, 16) + 2 * hc * 8 + 1024;
+    const size_t smem = L->a_bytes + chunk + tb + L->part_bytes + rup((size_t)N * 16, 16) + 2 * hc * 8 +
+                        (size_t)kMaxTiles * kRows * L->words * 4 + 1024;
     if (smem <= kSmemMax) {
       L->HC = hc;
       L->NB = kLimbs * hc;
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   double2* sPart = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(sT) + L.t_bytes);  // [tile][slice][row]
   double2* sVa = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(sPart) + L.part_bytes);  // [N]
   double* sSig = reinterpret_cast<double*>(sVa + N);                                   // [HC][2] of the chunk
+  uint32_t* sBits = reinterpret_cast<uint32_t*>(sSig + 2 * HC);  // [tile][row][words]: the CTA's samples
   const uint32_t aA = smem_u32(sA), aB = smem_u32(sB), aT = smem_u32(sT);
   const uint32_t bar_mma = smem_u32(&bars[0]), bar_b = smem_u32(&bars[1]), bar_t = smem_u32(&bars[2]);
   const double* sigma = reinterpret_cast<const double*>(blob + L.off_sigma);
@@ -225,6 +227,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   for (int k = tid; k < N; k += kThreads) sVa[k] = v[k];
   for (int i = tid; i < kMaxTiles * kSlices * kRows; i += kThreads) sPart[i] = make_double2(0.0, 0.0);
+  const int64_t u_cta = U - t0 * kRows;  // samples from the CTA's first row on
+  for (int i = tid; i < (int)(t1 - t0) * kRows * words; i += kThreads)
+    sBits[i] = i / words < u_cta ? bits[t0 * kRows * words + i] : 0u;  // the A tiles are rebuilt per chunk
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_t), "r"(rows * ncols * 16u)
                      : "memory");
       }
-      build_a(sA, bits, row0, U, N, Kp, words, tid);
+      build_a(sA, sBits, (tile - t0) * kRows, u_cta, N, Kp, words, tid);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
       if (tid == 0) {
