@@ -367,6 +367,7 @@ size_t ov_tc_blob_bytes(int N, int M) {
 int ov_tc_launch(const double* t, const uint32_t* bits, int64_t U, int N, int M, const double* v, const double* w,
                  double* q, void* blob, cudaStream_t st, const double* skip) {
   ovtc::Layout L;
+  if (U <= 0) return 0;
   if (!ovtc::make_layout(N, M, &L)) return 1;
   static int optin = -1;
   if (optin < 0) {
